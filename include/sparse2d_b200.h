@@ -1,0 +1,235 @@
+/*
+ * sparse2d_b200.h -- C ABI of the B200-native 2D-sparse-parallel embedding
+ * step (libsparse2d_b200.so).  Plain pointers and sizes only; no torch or
+ * CUDA types cross this boundary (streams are passed as void*).
+ *
+ * Every entry point returns an int status (S2D_OK = 0) and leaves a message
+ * for s2d_last_error() (thread-local) on failure.  The status codes map onto
+ * the exceptions the reference library throws:
+ *   S2D_EINVAL     std::invalid_argument   (bad config, N x N mismatch, zero batch)
+ *   S2D_ERANGE     std::out_of_range       (id outside every shard, embedding.cpp:61-63)
+ *   S2D_ENONFINITE std::invalid_argument   ("nonfinite row gradient", optimizer.cpp:69-72)
+ *   S2D_ERUNTIME   std::runtime_error      (checkpoint IO, embedding.cpp:133-219)
+ *   S2D_ECUDA / S2D_ENCCL                  device / collective failures (new)
+ *
+ * Each declaration names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ */
+#ifndef SPARSE2D_B200_H
+#define SPARSE2D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define S2D_OK 0
+#define S2D_EINVAL 1
+#define S2D_ERANGE 2
+#define S2D_ENONFINITE 3
+#define S2D_ERUNTIME 4
+#define S2D_ECUDA 5
+#define S2D_ENCCL 6
+
+/* ShardingStrategy (include/sparse2d/planner.hpp:29) */
+#define S2D_TABLE_WISE 0
+#define S2D_ROW_WISE 1
+/* OptimizerVariant (include/sparse2d/optimizer.hpp:10) */
+#define S2D_ROWWISE_ADAGRAD 0
+#define S2D_SGD 1
+/* weight storage */
+#define S2D_F32 0
+#define S2D_BF16 1
+/* where a buffer argument lives */
+#define S2D_HOST 0
+#define S2D_DEVICE 1
+
+/* TableLoadProfile (include/sparse2d/planner.hpp:12-20) */
+typedef struct {
+  uint32_t table_id;
+  uint64_t size_bytes;
+  double expected_lookups_per_batch;
+  uint64_t num_rows;
+} s2d_table_load_profile;
+
+/* PlanEntry (include/sparse2d/planner.hpp:22-27) */
+typedef struct {
+  uint32_t table_id;
+  uint32_t row_lo;
+  uint32_t row_hi; /* half-open */
+  uint32_t local_rank;
+} s2d_plan_entry;
+
+/* OptimizerConfig (include/sparse2d/optimizer.hpp:15-22) */
+typedef struct {
+  double eta;
+  double eps;
+  double c;        /* moment scaling factor; c = 1 is plain row-wise AdaGrad */
+  int32_t variant; /* S2D_ROWWISE_ADAGRAD | S2D_SGD */
+} s2d_optimizer_config;
+
+/* Topology (include/sparse2d/topology.hpp:13-26) */
+typedef struct {
+  uint32_t total_ranks;
+  uint32_t groups;
+  uint32_t ranks_per_group;
+} s2d_topology;
+
+/* One embedding table (FeatureSpec + EmbeddingTable shape, data.hpp:11-18,
+ * embedding.hpp:12-23); per-table rows and dims are an extension. */
+typedef struct {
+  uint32_t table_id; /* must equal its index in the registered list */
+  uint32_t rows;
+  uint32_t dim; /* multiple of 4, <= 512 (trainer.cpp:99 kMaxDim) */
+} s2d_table_desc;
+
+/* Per-step counters of the last step on this rank. */
+typedef struct {
+  uint64_t nnz_local;      /* ids in this rank's batch */
+  uint64_t nnz_owned;      /* ids this rank served as owner */
+  uint64_t entries_owned;  /* non-empty (bag, owner) pairs served (E) */
+  uint64_t unique_rows;    /* rows updated (U) */
+  uint64_t long_segments;  /* rows whose gradient was reduced in chunks */
+  uint64_t dirty_rows;     /* rows averaged by the last replica sync */
+  uint64_t a2a_bytes_sent; /* lookup+grad+id all-to-all bytes to other ranks */
+  uint64_t a2a_bytes_recv;
+  uint64_t sync_bytes;     /* replica-sync payload bytes sent */
+  uint32_t error_flags;    /* device-side fault bits of the last step */
+  uint32_t reserved;
+} s2d_step_stats;
+
+const char* s2d_last_error(void);
+const char* s2d_version(void);
+
+/* ---- host-side planning (no GPU needed) --------------------------------- */
+
+/* Topology(total, groups) ctor (src/topology.cpp:7-17). */
+int s2d_topology_init(uint32_t total_ranks, uint32_t groups, s2d_topology* out);
+
+/* plan_greedy (include/sparse2d/planner.hpp:47-48, src/planner.cpp:38-89).
+ * Writes at most `cap` entries; *n_out = entry count. */
+int s2d_plan_greedy(const s2d_table_load_profile* profiles, uint32_t n_profiles, uint32_t n,
+                    int32_t strategy, s2d_plan_entry* out, uint32_t cap, uint32_t* n_out);
+
+/* validate_plan (src/planner.cpp:91-123). */
+int s2d_validate_plan(const s2d_plan_entry* plan, uint32_t n_entries, uint32_t ranks_per_group,
+                      const s2d_table_load_profile* profiles, uint32_t n_profiles);
+
+/* ShardingPlan::owner_of (src/planner.cpp:20-28). */
+int s2d_plan_owner_of(const s2d_plan_entry* plan, uint32_t n_entries, uint32_t table_id,
+                      uint32_t row, uint32_t* owner);
+
+/* imbalance_ratio (src/planner.cpp:125-143). */
+int s2d_imbalance_ratio(const double* per_rank, uint32_t n, double* out);
+
+/* OptimizerConfig::validate (src/optimizer.cpp:19-23) + effective_lr (61-63). */
+int s2d_effective_lr(double v, const s2d_optimizer_config* cfg, double* out);
+
+/* ---- device context --------------------------------------------------- */
+
+typedef struct s2d_ctx s2d_ctx;
+
+int s2d_device_count(int* out);
+
+/* 128-byte NCCL bootstrap id; rank 0 creates it and the caller broadcasts it
+ * (e.g. over torch.distributed) before s2d_ctx_create on every rank. */
+int s2d_nccl_unique_id(uint8_t out[128]);
+
+/* Replaces the Trainer ctor's mesh set-up (src/trainer.cpp:180-214): one
+ * context per GPU, global rank `rank` of `total_ranks`, `groups` DP replicas.
+ * nccl_id may be NULL when total_ranks == 1. */
+int s2d_ctx_create(int device, uint32_t total_ranks, uint32_t groups, uint32_t rank,
+                   const uint8_t* nccl_id, s2d_ctx** out);
+int s2d_ctx_destroy(s2d_ctx* ctx);
+
+/* Runs all work of this context on `cuda_stream` (a cudaStream_t); NULL
+ * selects the context's own stream. */
+int s2d_ctx_set_stream(s2d_ctx* ctx, void* cuda_stream);
+
+/* strict = 1 (default): every call waits for its device work and reports
+ * device faults at the call, like the reference's exceptions.  strict = 0:
+ * calls return once work is queued; faults surface at s2d_synchronize. */
+int s2d_ctx_set_strict(s2d_ctx* ctx, int strict);
+
+/* Tables + plan (the identical-in-every-group plan).  The
+ * context allocates only the shards its local rank owns: fp32 or bf16
+ * weights, fp32 moments (embedding.hpp:16-17).  Replaces the replica
+ * allocation at src/trainer.cpp:216-224. */
+int s2d_register_tables(s2d_ctx* ctx, const s2d_table_desc* tables, uint32_t n_tables,
+                        const s2d_plan_entry* plan, uint32_t n_entries, int32_t weight_dtype);
+
+/* OptimizerConfig for the fused update; validates like
+ * OptimizerConfig::validate (src/optimizer.cpp:19-23). */
+int s2d_set_optimizer(s2d_ctx* ctx, const s2d_optimizer_config* cfg);
+
+/* Bit-exact device port of init_table (src/embedding.cpp:17-37) for the
+ * owned shards; moments start at zero. */
+int s2d_init_tables(s2d_ctx* ctx, uint64_t seed);
+
+/* Copy rows [row_lo,row_hi) of `table` (owned by this rank) in or out of the
+ * device shard; w: (hi-lo)*dim fp32, v: (hi-lo) fp32 (either may be NULL).
+ * Used for checkpoint / parity (apply_row_update-style writes,
+ * src/embedding.cpp:108-129). */
+int s2d_shard_write(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_hi,
+                    const float* w, const float* v);
+int s2d_shard_read(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_hi, float* w,
+                   float* v);
+/* Owned range of `table` on this rank ([0,0) when none). */
+int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* row_hi);
+
+/* Forward of one step for this rank's batch of `batch` samples: sample-major
+ * bags (s, f) given as lengths[batch*F] and the `nnz` global row ids of all
+ * bags concatenated.  Runs K1 input-dist bucketing + id all-to-all, K2 owner
+ * partial pooling, the pooled all-to-all and the requester combine, writing
+ * pooled[batch][sum_f dim_f] fp32.  Replaces build_demand + owner_lookup +
+ * route_all_to_all(LookupA2A) + the pooling half of pool_and_forward
+ * (src/trainer.cpp:283-390).  `mem` (S2D_HOST | S2D_DEVICE) says where the
+ * three buffers live; host buffers are copied inside the call. */
+int s2d_lookup_forward(s2d_ctx* ctx, uint32_t batch, const uint32_t* lengths, const uint32_t* ids,
+                       uint64_t nnz, float* pooled, int32_t mem);
+
+/* Backward + fused optimizer for the batch of the last s2d_lookup_forward:
+ * upstream[batch][sum_f dim_f] fp32 per-sample gradients (not batch-divided,
+ * src/trainer.cpp:424-427).  Runs the gradient all-to-all, K3 radix-sort
+ * dedup + segment reduce (x 1/(N*B)) and K4 moment-scaled row-wise AdaGrad
+ * (or SGD) reading and writing each row and its accumulator once.  Replaces
+ * build_grad_payloads + route_all_to_all(GradA2A) + owner_update
+ * (src/trainer.cpp:440-505, src/optimizer.cpp:25-90). */
+int s2d_backward_update(s2d_ctx* ctx, const float* upstream, int32_t mem);
+
+/* K5: weight + moment mean over the DP replicas of every row updated in any
+ * replica since the last sync (src/trainer.cpp:547-596).  No-op when M = 1.
+ * The caller decides the cadence ((step+1) % sync_interval == 0,
+ * src/trainer.cpp:661). */
+int s2d_replica_sync(s2d_ctx* ctx);
+
+/* Waits for the context's stream and reports deferred device faults
+ * (id out of range -> S2D_ERANGE, nonfinite gradient -> S2D_ENONFINITE). */
+int s2d_synchronize(s2d_ctx* ctx);
+
+int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out);
+
+/* K4 on caller rows (the binding behind Python adagrad_row_step,
+ * bindings/module.cpp:93-107): n_rows rows of `dim`, w fp32 [n][dim],
+ * v fp32 [n], g f64 [n][dim], host buffers; lr_out[n] receives the effective
+ * learning rate (may be NULL).  Runs the same device code as the step. */
+int s2d_adagrad_rows(const s2d_optimizer_config* cfg, uint32_t n_rows, uint32_t dim, float* w,
+                     float* v, const double* g, double* lr_out);
+
+/* Debug view of the last step's wire buffers for bit-exact layout tests.
+ * which: 0 demand lengths received [N requester][B*F] u32,
+ *        1 demand ids received (canonical order) u32,
+ *        2 pooled partials sent, concatenated over requesters, f32,
+ *        3 gradient payload sent by this rank, concatenated over owners, f32,
+ *        4 owner mask per local bag u32 [B*F],
+ *        5 unique rows updated (global row ids, ascending by (table,row)) u32.
+ * Copies min(cap, size) elements; *n = size. */
+int s2d_debug_read(s2d_ctx* ctx, int32_t which, void* out, uint64_t cap, uint64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPARSE2D_B200_H */

@@ -1,0 +1,40 @@
+"""B200-native 2D-sparse-parallel embedding training step (arXiv 2508.03854).
+
+Drop-in for the embedding path of the reference ``sparse2d`` library: table
+configs, the 2D mesh planner (``Topology``, ``plan_greedy``) and the
+moment-scaled row-wise AdaGrad optimizer keep the reference's names; the step
+(input-dist bucketing, pooled lookup, radix-sort dedup, fused AdaGrad, replica
+sync) runs as hand-written sm_100a CUDA kernels + NCCL in
+``libsparse2d_b200.so`` behind a C ABI (``include/sparse2d_b200.h``).
+"""
+from .api import (  # noqa: F401
+    OptimizerConfig,
+    Sparse2DEmbedding,
+    TableConfig,
+    Topology,
+    adagrad_row_step,
+    adagrad_rows,
+    effective_lr,
+    imbalance_ratio,
+    nccl_unique_id,
+    owner_of,
+    plan_greedy,
+    validate_plan,
+)
+
+__all__ = [
+    "OptimizerConfig",
+    "Sparse2DEmbedding",
+    "TableConfig",
+    "Topology",
+    "adagrad_row_step",
+    "adagrad_rows",
+    "effective_lr",
+    "imbalance_ratio",
+    "nccl_unique_id",
+    "owner_of",
+    "plan_greedy",
+    "validate_plan",
+]
+
+__version__ = "0.1.0"

@@ -1,0 +1,127 @@
+"""ctypes binding of libsparse2d_b200.so (include/sparse2d_b200.h).
+
+The library is built in-tree by ``paper_2508_03854_b200.build``.  There is no
+fallback: if the shared library is missing or cannot be loaded, importing the
+device API raises, so a GPU run can never silently use another code path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+S2D_OK, S2D_EINVAL, S2D_ERANGE, S2D_ENONFINITE, S2D_ERUNTIME, S2D_ECUDA, S2D_ENCCL = range(7)
+S2D_TABLE_WISE, S2D_ROW_WISE = 0, 1
+S2D_ROWWISE_ADAGRAD, S2D_SGD = 0, 1
+S2D_F32, S2D_BF16 = 0, 1
+S2D_HOST, S2D_DEVICE = 0, 1
+
+
+class TableLoadProfile(C.Structure):
+    _fields_ = [("table_id", C.c_uint32), ("size_bytes", C.c_uint64),
+                ("expected_lookups_per_batch", C.c_double), ("num_rows", C.c_uint64)]
+
+
+class PlanEntry(C.Structure):
+    _fields_ = [("table_id", C.c_uint32), ("row_lo", C.c_uint32), ("row_hi", C.c_uint32),
+                ("local_rank", C.c_uint32)]
+
+
+class OptimizerConfigC(C.Structure):
+    _fields_ = [("eta", C.c_double), ("eps", C.c_double), ("c", C.c_double), ("variant", C.c_int32)]
+
+
+class TopologyC(C.Structure):
+    _fields_ = [("total_ranks", C.c_uint32), ("groups", C.c_uint32), ("ranks_per_group", C.c_uint32)]
+
+
+class TableDesc(C.Structure):
+    _fields_ = [("table_id", C.c_uint32), ("rows", C.c_uint32), ("dim", C.c_uint32)]
+
+
+class StepStats(C.Structure):
+    _fields_ = [("nnz_local", C.c_uint64), ("nnz_owned", C.c_uint64), ("entries_owned", C.c_uint64),
+                ("unique_rows", C.c_uint64), ("long_segments", C.c_uint64), ("dirty_rows", C.c_uint64),
+                ("a2a_bytes_sent", C.c_uint64), ("a2a_bytes_recv", C.c_uint64), ("sync_bytes", C.c_uint64),
+                ("error_flags", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+# symbol -> (restype, argtypes); the full exported surface of the header
+_P = C.c_void_p
+SIGNATURES = {
+    "s2d_last_error": (C.c_char_p, []),
+    "s2d_version": (C.c_char_p, []),
+    "s2d_topology_init": (C.c_int, [C.c_uint32, C.c_uint32, C.POINTER(TopologyC)]),
+    "s2d_plan_greedy": (C.c_int, [C.POINTER(TableLoadProfile), C.c_uint32, C.c_uint32, C.c_int32,
+                                  C.POINTER(PlanEntry), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "s2d_validate_plan": (C.c_int, [C.POINTER(PlanEntry), C.c_uint32, C.c_uint32,
+                                    C.POINTER(TableLoadProfile), C.c_uint32]),
+    "s2d_plan_owner_of": (C.c_int, [C.POINTER(PlanEntry), C.c_uint32, C.c_uint32, C.c_uint32,
+                                    C.POINTER(C.c_uint32)]),
+    "s2d_imbalance_ratio": (C.c_int, [C.POINTER(C.c_double), C.c_uint32, C.POINTER(C.c_double)]),
+    "s2d_effective_lr": (C.c_int, [C.c_double, C.POINTER(OptimizerConfigC), C.POINTER(C.c_double)]),
+    "s2d_device_count": (C.c_int, [C.POINTER(C.c_int)]),
+    "s2d_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "s2d_ctx_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_char_p, C.POINTER(_P)]),
+    "s2d_ctx_destroy": (C.c_int, [_P]),
+    "s2d_ctx_set_stream": (C.c_int, [_P, _P]),
+    "s2d_ctx_set_strict": (C.c_int, [_P, C.c_int]),
+    "s2d_register_tables": (C.c_int, [_P, C.POINTER(TableDesc), C.c_uint32, C.POINTER(PlanEntry), C.c_uint32,
+                                      C.c_int32]),
+    "s2d_set_optimizer": (C.c_int, [_P, C.POINTER(OptimizerConfigC)]),
+    "s2d_init_tables": (C.c_int, [_P, C.c_uint64]),
+    "s2d_shard_write": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, _P, _P]),
+    "s2d_shard_read": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, _P, _P]),
+    "s2d_shard_range": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "s2d_lookup_forward": (C.c_int, [_P, C.c_uint32, _P, _P, C.c_uint64, _P, C.c_int32]),
+    "s2d_backward_update": (C.c_int, [_P, _P, C.c_int32]),
+    "s2d_replica_sync": (C.c_int, [_P]),
+    "s2d_synchronize": (C.c_int, [_P]),
+    "s2d_get_step_stats": (C.c_int, [_P, C.POINTER(StepStats)]),
+    "s2d_adagrad_rows": (C.c_int, [C.POINTER(OptimizerConfigC), C.c_uint32, C.c_uint32, _P, _P, _P, _P]),
+    "s2d_debug_read": (C.c_int, [_P, C.c_int32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
+}
+
+_lib = None
+
+
+def load(build_if_missing: bool = True) -> C.CDLL:
+    """Load (building first if needed and nvcc is available) the library.
+    Raises if it cannot be loaded -- there is no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH) or _build._stale(LIB_PATH, _build.sources() + _build._headers()):
+        if not build_if_missing:
+            raise ImportError(f"{LIB_PATH} missing; run python -m paper_2508_03854_b200.build")
+        _build.build()
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class Sparse2DError(RuntimeError):
+    pass
+
+
+_EXC = {
+    S2D_EINVAL: ValueError,       # std::invalid_argument (pybind -> ValueError)
+    S2D_ERANGE: IndexError,       # std::out_of_range -> IndexError
+    S2D_ENONFINITE: ValueError,   # invalid_argument("nonfinite row gradient")
+    S2D_ERUNTIME: RuntimeError,
+    S2D_ECUDA: Sparse2DError,
+    S2D_ENCCL: Sparse2DError,
+}
+
+
+def check(rc: int) -> None:
+    if rc != S2D_OK:
+        msg = _lib.s2d_last_error().decode() if _lib is not None else "error"
+        raise _EXC.get(rc, RuntimeError)(msg)

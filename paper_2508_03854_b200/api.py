@@ -1,0 +1,341 @@
+"""Python surface of the B200 2D-sparse-parallel embedding step.
+
+Reference-named functions keep the signatures of the reference's pybind11
+module (proj/bindings/module.cpp:35-164, proj/python/sparse2d/__init__.py):
+``Topology``, ``plan_greedy``, ``imbalance_ratio``, ``effective_lr``,
+``adagrad_row_step``.  The step itself is ``Sparse2DEmbedding``: one object
+per GPU rank, the drop-in for the embedding phases of
+``Trainer::Impl::run_step`` (proj/src/trainer.cpp:615-663).
+
+All compute runs in libsparse2d_b200.so (hand-written sm_100a kernels + NCCL);
+this module only marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Iterable, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+def _lib():
+    return L.load()
+
+
+# ---- Topology (include/sparse2d/topology.hpp:13-26) -------------------------
+
+class Topology:
+    """T ranks split into M groups of N = T/M; rank r -> (r // N, r % N)."""
+
+    def __init__(self, total_ranks: int, groups: int):
+        t = L.TopologyC()
+        L.check(_lib().s2d_topology_init(total_ranks, groups, C.byref(t)))
+        self.total_ranks = t.total_ranks
+        self.groups = t.groups
+        self.ranks_per_group = t.ranks_per_group
+
+    def group_of(self, rank: int) -> int:
+        return rank // self.ranks_per_group
+
+    def local_of(self, rank: int) -> int:
+        return rank % self.ranks_per_group
+
+    def rank_of(self, group: int, local: int) -> int:
+        return group * self.ranks_per_group + local
+
+    def __repr__(self):
+        return f"Topology(total_ranks={self.total_ranks}, groups={self.groups})"
+
+
+# ---- planner (src/planner.cpp) ----------------------------------------------
+
+def _profiles(profiles) -> tuple:
+    arr = (L.TableLoadProfile * len(profiles))()
+    for i, (tid, size, lookups, rows) in enumerate(profiles):
+        arr[i] = L.TableLoadProfile(int(tid), int(size), float(lookups), int(rows))
+    return arr
+
+
+def plan_greedy(profiles: Sequence[tuple], ranks: int, strategy: str = "table-wise") -> list[dict]:
+    """profiles: (table_id, size_bytes, expected_lookups, num_rows) tuples
+    (bindings/module.cpp:109-131).  Returns [{table_id,row_lo,row_hi,local_rank}]."""
+    if strategy not in ("table-wise", "row-wise"):
+        raise ValueError("unknown sharding strategy: " + str(strategy))
+    prof = _profiles(profiles)
+    cap = max(1, len(profiles) * max(1, ranks))
+    out = (L.PlanEntry * cap)()
+    n = C.c_uint32(0)
+    L.check(_lib().s2d_plan_greedy(prof, len(profiles), ranks,
+                                   L.S2D_ROW_WISE if strategy == "row-wise" else L.S2D_TABLE_WISE,
+                                   out, cap, C.byref(n)))
+    return [dict(table_id=out[i].table_id, row_lo=out[i].row_lo, row_hi=out[i].row_hi,
+                 local_rank=out[i].local_rank) for i in range(n.value)]
+
+
+def _plan_array(plan: Iterable[dict]):
+    plan = list(plan)
+    arr = (L.PlanEntry * max(1, len(plan)))()
+    for i, e in enumerate(plan):
+        arr[i] = L.PlanEntry(e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"])
+    return arr, len(plan)
+
+
+def validate_plan(plan: Iterable[dict], ranks_per_group: int, profiles: Sequence[tuple]) -> None:
+    arr, n = _plan_array(plan)
+    prof = _profiles(profiles)
+    L.check(_lib().s2d_validate_plan(arr, n, ranks_per_group, prof, len(profiles)))
+
+
+def owner_of(plan: Iterable[dict], table_id: int, row: int) -> int:
+    arr, n = _plan_array(plan)
+    o = C.c_uint32(0)
+    L.check(_lib().s2d_plan_owner_of(arr, n, table_id, row, C.byref(o)))
+    return o.value
+
+
+def imbalance_ratio(loads: Sequence[float]) -> float:
+    a = (C.c_double * max(1, len(loads)))(*loads)
+    out = C.c_double(0)
+    L.check(_lib().s2d_imbalance_ratio(a, len(loads), C.byref(out)))
+    return out.value
+
+
+# ---- optimizer (src/optimizer.cpp) ------------------------------------------
+
+@dataclass
+class OptimizerConfig:
+    """OptimizerConfig (include/sparse2d/optimizer.hpp:15-22)."""
+
+    eta: float = 0.05
+    eps: float = 1e-8
+    c: float = 1.0
+    variant: str = "rowwise-adagrad"  # | "sgd"
+
+    def to_c(self) -> L.OptimizerConfigC:
+        if self.variant not in ("rowwise-adagrad", "sgd"):
+            raise ValueError("unknown optimizer variant: " + str(self.variant))
+        return L.OptimizerConfigC(self.eta, self.eps, self.c,
+                                  L.S2D_SGD if self.variant == "sgd" else L.S2D_ROWWISE_ADAGRAD)
+
+
+def effective_lr(v: float, eta: float = 0.1, eps: float = 1e-8, c: float = 1.0) -> float:
+    """eta / (sqrt(v / c) + eps) (optimizer.cpp:61-63), validated like the binding."""
+    cfg = OptimizerConfig(eta, eps, c).to_c()
+    out = C.c_double(0)
+    L.check(_lib().s2d_effective_lr(v, C.byref(cfg), C.byref(out)))
+    return out.value
+
+
+def adagrad_row_step(w, v, g, eta: float = 0.1, eps: float = 1e-8, c: float = 1.0) -> dict:
+    """Fused moment-scaled row-wise AdaGrad step on one row, executed by the
+    same sm_100a row-update code as the training step
+    (bindings/module.cpp:93-107).  Returns {w, v, effective_lr}."""
+    return adagrad_rows([w], [v], [g], eta=eta, eps=eps, c=c)[0]
+
+
+def adagrad_rows(ws, vs, gs, eta=0.1, eps=1e-8, c=1.0, variant="rowwise-adagrad") -> list[dict]:
+    w = np.ascontiguousarray(np.array(ws, np.float32))
+    if w.ndim != 2:
+        raise ValueError("rows must share one dim")
+    g = np.ascontiguousarray(np.array(gs, np.float64))
+    if g.shape != w.shape:
+        raise ValueError("gradient dim mismatch")
+    v = np.ascontiguousarray(np.array(vs, np.float32).reshape(-1))
+    lr = np.zeros(len(v), np.float64)
+    cfg = OptimizerConfig(eta, eps, c, variant).to_c()
+    L.check(_lib().s2d_adagrad_rows(C.byref(cfg), w.shape[0], w.shape[1], w.ctypes.data, v.ctypes.data,
+                                    g.ctypes.data, lr.ctypes.data))
+    return [dict(w=w[i].tolist(), v=float(v[i]), effective_lr=float(lr[i])) for i in range(len(v))]
+
+
+# ---- the step engine -----------------------------------------------------------
+
+@dataclass
+class TableConfig:
+    """One embedding table: FeatureSpec / EmbeddingTable shape
+    (data.hpp:11-18, embedding.hpp:12-23) with per-table rows and dim."""
+
+    rows: int
+    dim: int
+    expected_lookups: float = 1.0  # expected lookups per batch (planner load)
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    L.check(_lib().s2d_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _numel(x) -> int:
+    return int(x.numel()) if hasattr(x, "numel") else int(x.size)
+
+
+def _ptr_kind(x, dtype, writable=False):
+    """(pointer, mem kind, keepalive) for a numpy array or torch tensor of a
+    4-byte `dtype` (np.uint32 or np.float32)."""
+    try:
+        import torch  # plumbing only: device memory / pinned host buffers
+        if isinstance(x, torch.Tensor):
+            ok = (torch.float32,) if dtype == np.float32 else (torch.int32, getattr(torch, "uint32", torch.int32))
+            if x.dtype not in ok:
+                raise TypeError(f"tensor dtype {x.dtype} does not match {np.dtype(dtype).name}")
+            if not x.is_contiguous():
+                raise ValueError("tensor must be contiguous")
+            return x.data_ptr(), (L.S2D_DEVICE if x.is_cuda else L.S2D_HOST), x
+    except ImportError:
+        pass
+    if writable:
+        if not (isinstance(x, np.ndarray) and x.dtype == dtype and x.flags.c_contiguous):
+            raise TypeError(f"output must be a C-contiguous {np.dtype(dtype).name} array")
+        return x.ctypes.data, L.S2D_HOST, x
+    a = np.ascontiguousarray(x, dtype)
+    return a.ctypes.data, L.S2D_HOST, a
+
+
+class Sparse2DEmbedding:
+    """Per-rank engine of the 2D-sparse-parallel embedding step.
+
+    One instance per GPU; rank r of T with M DP groups (N = T/M ranks per MP
+    group).  Every rank registers the same tables and plan (the plan is
+    identical in every group) and owns the shards its local rank
+    is assigned.  ``nccl_id`` (128 bytes from rank 0, e.g. broadcast over
+    torch.distributed) is required when T > 1.
+    """
+
+    def __init__(self, tables: Sequence[TableConfig], topology: Topology, rank: int = 0, device: int = 0,
+                 strategy: str = "table-wise", plan: Sequence[dict] | None = None,
+                 optimizer: OptimizerConfig | None = None, weight_dtype: str = "fp32",
+                 nccl_id: bytes | None = None, strict: bool = True):
+        self.lib = _lib()
+        self.topology = topology
+        self.rank = rank
+        self.tables = list(tables)
+        self.F = len(self.tables)
+        self.dims = np.array([t.dim for t in self.tables], np.uint32)
+        self.rows = np.array([t.rows for t in self.tables], np.uint64)
+        self.sum_dims = int(self.dims.sum())
+        N = topology.ranks_per_group
+        if plan is None:
+            prof = [(i, t.rows * t.dim * 4, t.expected_lookups, t.rows) for i, t in enumerate(self.tables)]
+            plan = plan_greedy(prof, N, strategy)
+        self.plan = [dict(e) for e in plan]
+        self._ctx = C.c_void_p()
+        L.check(self.lib.s2d_ctx_create(device, topology.total_ranks, topology.groups, rank,
+                                        nccl_id if nccl_id is not None else None, C.byref(self._ctx)))
+        self.set_strict(strict)
+        td = (L.TableDesc * self.F)(*[L.TableDesc(i, t.rows, t.dim) for i, t in enumerate(self.tables)])
+        parr, n = _plan_array(self.plan)
+        if weight_dtype not in ("fp32", "bf16"):
+            raise ValueError("weight_dtype must be fp32 or bf16")
+        self.weight_dtype = weight_dtype
+        L.check(self.lib.s2d_register_tables(self._ctx, td, self.F, parr, n,
+                                             L.S2D_BF16 if weight_dtype == "bf16" else L.S2D_F32))
+        self.optimizer = optimizer or OptimizerConfig()
+        self.set_optimizer(self.optimizer)
+        self._batch = None
+
+    # -- lifecycle --
+    def close(self):
+        if self._ctx:
+            self.lib.s2d_ctx_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_strict(self, strict: bool):
+        L.check(self.lib.s2d_ctx_set_strict(self._ctx, 1 if strict else 0))
+
+    def set_stream(self, stream_ptr: int | None):
+        L.check(self.lib.s2d_ctx_set_stream(self._ctx, stream_ptr))
+
+    def set_optimizer(self, cfg: OptimizerConfig):
+        c = cfg.to_c()
+        L.check(self.lib.s2d_set_optimizer(self._ctx, C.byref(c)))
+        self.optimizer = cfg
+
+    # -- state --
+    def init_tables(self, seed: int):
+        """init_table (embedding.cpp:17-37) for every owned shard, on device."""
+        L.check(self.lib.s2d_init_tables(self._ctx, seed))
+
+    def owned_range(self, table: int) -> tuple[int, int]:
+        lo, hi = C.c_uint32(0), C.c_uint32(0)
+        L.check(self.lib.s2d_shard_range(self._ctx, table, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def read_rows(self, table: int, lo: int, hi: int):
+        d = int(self.dims[table])
+        w = np.zeros((hi - lo, d), np.float32)
+        v = np.zeros(hi - lo, np.float32)
+        L.check(self.lib.s2d_shard_read(self._ctx, table, lo, hi, w.ctypes.data, v.ctypes.data))
+        return w, v
+
+    def write_rows(self, table: int, lo: int, w=None, v=None):
+        n = len(w) if w is not None else len(v)
+        wa = None if w is None else np.ascontiguousarray(w, np.float32)
+        va = None if v is None else np.ascontiguousarray(v, np.float32)
+        L.check(self.lib.s2d_shard_write(self._ctx, table, lo, lo + n,
+                                          wa.ctypes.data if wa is not None else None,
+                                          va.ctypes.data if va is not None else None))
+
+    # -- the step --
+    def forward(self, lengths, ids, pooled=None, batch: int | None = None):
+        """Pooled embeddings of this rank's batch.  lengths: [B*F] sample-major
+        bag lengths, ids: concatenated global row ids.  numpy / CPU tensors are
+        host buffers (copied inside); CUDA tensors stay on device."""
+        lp, lk, lka = _ptr_kind(lengths, np.uint32)
+        ip, ik, ika = _ptr_kind(ids, np.uint32)
+        nnz, nb = _numel(ika), _numel(lka)
+        if batch is None:
+            if nb % self.F:
+                raise ValueError("len(lengths) must be a multiple of the table count")
+            batch = nb // self.F
+        if lk != ik:
+            raise ValueError("lengths and ids must both be host or both be device buffers")
+        if pooled is None:
+            if lk == L.S2D_DEVICE:
+                import torch
+                pooled = torch.empty((batch, self.sum_dims), dtype=torch.float32, device=lka.device)
+            else:
+                pooled = np.zeros((batch, self.sum_dims), np.float32)
+        pp, pk, pka = _ptr_kind(pooled, np.float32, writable=True)
+        if pk != lk:
+            raise ValueError("pooled must live where the inputs live")
+        L.check(self.lib.s2d_lookup_forward(self._ctx, batch, lp, ip, nnz, pp, lk))
+        self._batch = batch
+        return pooled
+
+    def backward_update(self, upstream):
+        """Gradient all-to-all + dedup + fused moment-scaled row-wise AdaGrad for
+        the batch of the last forward.  upstream: [B][sum dims] fp32."""
+        up, uk, _ua = _ptr_kind(upstream, np.float32)
+        L.check(self.lib.s2d_backward_update(self._ctx, up, uk))
+
+    def sync_replicas(self):
+        """Weight + moment mean of dirty rows across the DP group
+        (trainer.cpp:547-596).  No-op for M = 1."""
+        L.check(self.lib.s2d_replica_sync(self._ctx))
+
+    def synchronize(self):
+        L.check(self.lib.s2d_synchronize(self._ctx))
+
+    def stats(self) -> dict:
+        s = L.StepStats()
+        L.check(self.lib.s2d_get_step_stats(self._ctx, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in L.StepStats._fields_}
+
+    def debug(self, which: int) -> np.ndarray:
+        """Wire buffers of the last step (see s2d_debug_read)."""
+        n = C.c_uint64(0)
+        L.check(self.lib.s2d_debug_read(self._ctx, which, None, 0, C.byref(n)))
+        dt = np.float32 if which in (2, 3) else np.uint32
+        out = np.zeros(n.value, dt)
+        L.check(self.lib.s2d_debug_read(self._ctx, which, out.ctypes.data, n.value, C.byref(n)))
+        return out

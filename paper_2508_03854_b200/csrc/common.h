@@ -1,0 +1,203 @@
+// Shared declarations of libsparse2d_b200: error type, device-side table
+// metadata, kernel launch wrappers.  Kernels live in k_*.cu, the per-rank
+// step driver in ctx.cu, the C ABI in capi.cpp.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/sparse2d_b200.h"
+
+namespace s2d {
+
+// Carries an S2D_* status; capi.cpp turns it into the return code +
+// s2d_last_error() message.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define S2D_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::s2d::Error(S2D_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define S2D_LAUNCH_CHECK() S2D_CUDA(cudaGetLastError())
+
+// Device fault bits (checked once per step, SURVEY.md 5 failure detection).
+enum : uint32_t { kErrIdRange = 1u, kErrNonfinite = 2u };
+
+// Per-feature metadata visible to every kernel.
+struct FeatDev {
+  uint32_t dim;     // D_f, multiple of 4
+  uint32_t rows;    // global rows of the table
+  uint32_t lo, hi;  // row range this rank owns (lo == hi: none)
+  uint64_t wbase;   // element offset of owned row `lo` in the weight store
+  uint32_t vbase;   // slot of owned row `lo` (slot = vbase + row - lo)
+  uint32_t coff;    // column offset inside a [sum_f D_f] pooled/upstream row
+  uint32_t rbeg;    // owner ranges of this table: ranges[rbeg, rend)
+  uint32_t rend;
+};
+
+// Owner range of a table inside the MP group (sorted by lo per table).
+struct RangeDev {
+  uint32_t lo, hi, owner, pad;
+};
+
+constexpr int kMaxDim = 512;       // trainer.cpp:99
+constexpr int kMaxRanksPerGroup = 32;  // owner bitmask width (trainer.cpp:193-195)
+constexpr uint32_t kChunk = 128;   // contributions per chunk of a long gradient segment
+
+// ---- launch wrappers (all asynchronous on `st`) --------------------------
+
+// scans (k_scan.cu)
+enum class ScanOp : int { Identity = 0, NonzeroDim = 1 };
+// out[i] = sum_{k<i} op(in[k]) for i in [0, n]; out has n+1 entries.
+// NonzeroDim: op(x at flat index k) = x ? feats[k % F].dim : 0.
+void scan_u32_to_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st, void* tmp,
+                     size_t tmp_bytes);
+void scan_nonzero_dim_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint32_t F,
+                          const FeatDev* feats, cudaStream_t st, void* tmp, size_t tmp_bytes);
+// out[i] = number of segment heads (first index of a run of equal keys
+// < n_slots) before i.
+void scan_heads_u32(const uint32_t* keys, uint32_t* out, uint64_t n, uint32_t n_slots, cudaStream_t st,
+                    void* tmp, size_t tmp_bytes);
+size_t scan_tmp_bytes(uint64_t n);
+
+// radix sort (k_sort.cu): stable LSD sort of (key, val) pairs by the low
+// `bits` bits of key.  keys/vals ping-pong between a and b; returns true if
+// the result ended in b.
+size_t radix_tmp_bytes(uint64_t n, int bits);
+bool radix_sort_pairs(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b,
+                      uint64_t n, int bits, void* tmp, size_t tmp_bytes, cudaStream_t st);
+
+// embedding kernels (k_embed.cu)
+void launch_init_rows(void* w, int bf16, const FeatDev* feats_host, uint32_t F, uint64_t seed,
+                      cudaStream_t st);
+
+struct LookupArgs {
+  const FeatDev* feats;
+  uint32_t F, B, n_req;        // bags = n_req * B * F (flattened [n][s][f])
+  uint32_t sum_dims;
+  const uint32_t* lengths;     // [n_req*B*F]
+  const uint32_t* id_off;      // [n_req*B*F + 1]
+  const uint32_t* ids;         // global row ids
+  const void* weights;
+  float* out;                  // direct: pooled [B][sumD]; else partial send buffer
+  const uint64_t* eoff;        // non-direct: float offset of each non-empty bag
+  uint32_t* keys;              // per id: slot (0xffffffff if invalid)
+  uint32_t* vals;              // per id: gradient row offset in float4 units
+  uint32_t* err;
+  int direct;                  // N == 1: write pooled rows (zero for empty bags)
+  int emit_keys;
+};
+void launch_owner_lookup(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
+
+struct CombineArgs {
+  const FeatDev* feats;
+  uint32_t F, B, N, sum_dims;
+  const uint32_t* cnt;         // [N][B*F] ids of local bag b owned by o
+  const uint64_t* eoff;        // [N*B*F + 1] float offsets into the per-owner blocks
+  const float* recv;           // partials received, concatenated by owner
+  float* pooled;               // [B][sumD]
+};
+void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st);
+
+struct GradGatherArgs {
+  const FeatDev* feats;
+  uint32_t F, B, N, sum_dims;
+  const uint32_t* cnt;
+  const uint64_t* eoff;
+  const float* upstream;       // [B][sumD]
+  float* send;                 // concatenated by owner
+};
+void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st);
+
+struct BucketArgs {
+  const FeatDev* feats;
+  const RangeDev* ranges;
+  uint32_t F, BF, N;
+  const uint32_t* lengths;     // [BF]
+  const uint32_t* id_off;      // [BF+1]
+  const uint32_t* ids;
+  uint32_t* cnt;               // [N][BF]
+  const uint32_t* send_off;    // [N*BF+1] (permute pass)
+  uint32_t* send_ids;          // (permute pass)
+  uint32_t* err;
+};
+void launch_bucket_count(const BucketArgs& a, cudaStream_t st);
+void launch_bucket_permute(const BucketArgs& a, cudaStream_t st);
+
+// update kernels (k_update.cu)
+struct SegmentArgs {
+  const uint32_t* keys;        // sorted slots
+  uint64_t n;
+  uint32_t n_slots;            // keys >= n_slots are invalid (sorted last)
+  uint32_t* uslot;             // [n+1] unique slots
+  uint32_t* useg;              // [n+2] segment starts; useg[U] = end of valid keys
+  uint32_t* counters;          // [0]=U [1]=total chunks [2]=long segments
+  uint32_t* chunk_base;        // [n+1]
+  uint32_t* chunk_seg;         // [n/kChunk+1]
+  void* tmp;
+  size_t tmp_bytes;
+};
+void run_segments(const SegmentArgs& a, cudaStream_t st);
+
+struct UpdateArgs {
+  const FeatDev* feats;
+  const uint32_t* vbase_sorted;  // [F+1] slot bases ascending (feature of a slot)
+  const uint32_t* feat_of_vbase; // [F] feature index for vbase_sorted[i]
+  uint32_t n_feat_owned;
+  const uint32_t* uslot;
+  const uint32_t* useg;
+  const uint32_t* vals;        // sorted gradient row offsets (float4 units)
+  const uint32_t* counters;
+  const uint32_t* chunk_base;
+  const uint32_t* chunk_seg;
+  double* chunk_part;          // [chunks][kMaxDim]
+  const float* grad;           // gradient rows (upstream or received payload)
+  void* weights;
+  float* moments;
+  uint8_t* dirty;              // may be null
+  double inv_batch;
+  double eta, eps, c;
+  int sgd;
+  uint32_t* err;
+};
+void launch_update(const UpdateArgs& a, int bf16, int max_dim, uint64_t max_rows, cudaStream_t st);
+
+// standalone fused row step on caller rows (s2d_adagrad_rows)
+void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32_t n, uint32_t dim,
+                         double eta, double eps, double c, int sgd, uint32_t* err, cudaStream_t st);
+
+// replica sync kernels (k_sync.cu)
+void launch_dirty_compact(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, uint32_t* count,
+                          void* tmp, size_t tmp_bytes, cudaStream_t st);
+void launch_pack_rows(const FeatDev* feats, const uint32_t* vbase_sorted,
+                      const uint32_t* feat_of_vbase, uint32_t n_feat_owned, const uint32_t* list,
+                      const uint32_t* count, const void* weights, int bf16, const float* moments,
+                      uint32_t row_floats, float* packed, uint32_t max_rows, cudaStream_t st);
+void launch_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted,
+                      const uint32_t* feat_of_vbase, uint32_t n_feat_owned, const uint32_t* list,
+                      const uint32_t* count, const float* gathered, uint32_t M, uint32_t row_floats,
+                      uint32_t rows_cap, void* weights, int bf16, float* moments, int sgd,
+                      uint8_t* dirty, cudaStream_t st);
+
+// host planning (host_plan.cpp)
+void check_optimizer(const s2d_optimizer_config& c);
+s2d_topology make_topology(uint32_t total, uint32_t groups);
+std::vector<s2d_plan_entry> plan_greedy(const std::vector<s2d_table_load_profile>& profiles, uint32_t n,
+                                        int strategy);
+void validate_plan(const std::vector<s2d_plan_entry>& plan, uint32_t ranks_per_group,
+                   const std::vector<s2d_table_load_profile>& profiles);
+uint32_t plan_owner_of(const s2d_plan_entry* plan, uint32_t n, uint32_t table, uint32_t row);
+double imbalance_ratio(const double* v, uint32_t n);
+double effective_lr(double v, const s2d_optimizer_config& c);
+
+}  // namespace s2d

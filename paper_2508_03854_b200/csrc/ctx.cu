@@ -1,0 +1,752 @@
+// Step driver of one rank.  Sequence per step (src/trainer.cpp:615-663,
+// embedding phases only):
+//
+//   N == 1:  lengths -> id offsets (scan) -> K2 lookup writes pooled rows and
+//            (slot, upstream-row) pairs -> [backward] radix sort -> segments
+//            -> K3+K4 fused update straight from the upstream gradient.
+//   N  > 1:  K1 count + scans + permute -> NCCL: counts, then lengths + ids
+//            inside the MP group -> owner K2 partials -> NCCL pooled a2a (C1)
+//            -> requester combine.  [backward] grad gather -> NCCL grad a2a
+//            (C2) -> radix sort -> segments -> fused update.
+//   M  > 1:  replica_sync(): byte-max all-reduce of dirty flags in the DP
+//            group -> ordered dirty list -> pack -> NCCL all-gather -> f64
+//            ascending-group mean (C3).
+//
+// Every buffer on the wire has the reference's layout: demand ids per owner
+// in (requester, sample, feature, occurrence) order, one partial / gradient
+// row per non-empty (bag, owner) entry in (sample, feature) order
+// (trainer.cpp:283-313, 331-335, 446-453).
+#include <algorithm>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace s2d {
+
+#define S2D_NCCL(call)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      throw ::s2d::Error(S2D_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+void DevBuf::ensure(size_t bytes) {
+  if (bytes <= cap && p) return;
+  release();
+  size_t want = std::max<size_t>(bytes + bytes / 8, 256);
+  S2D_CUDA(cudaMalloc(&p, want));
+  cap = want;
+}
+
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+}
+
+void HostBuf::ensure(size_t bytes) {
+  if (bytes <= cap && p) return;
+  if (p) cudaFreeHost(p);
+  S2D_CUDA(cudaMallocHost(&p, std::max<size_t>(bytes, 256)));
+  cap = std::max<size_t>(bytes, 256);
+}
+
+HostBuf::~HostBuf() {
+  if (p) cudaFreeHost(p);
+}
+
+namespace {
+
+__global__ void k_gather_bounds(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF,
+                                uint64_t* out) {
+  const uint32_t o = threadIdx.x;
+  if (o <= N) {
+    out[o] = send_off[(uint64_t)o * BF];
+    out[N + 1 + o] = eoff[(uint64_t)o * BF];
+  }
+}
+
+int bit_width(uint32_t x) {
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+}  // namespace
+
+Ctx::~Ctx() {
+  if (device >= 0) cudaSetDevice(device);
+  if (dp) ncclCommDestroy(dp);
+  if (mp) ncclCommDestroy(mp);
+  if (world) ncclCommDestroy(world);
+  if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uint8_t* nccl_id) {
+  if (total == 0 || groups == 0 || total % groups)
+    throw Error(S2D_EINVAL, "groups must divide total_ranks (both >= 1)");
+  if (r >= total) throw Error(S2D_EINVAL, "rank out of range");
+  T = total;
+  M = groups;
+  N = total / groups;
+  if (N > (uint32_t)kMaxRanksPerGroup)
+    throw Error(S2D_EINVAL, "owner bitmask limits ranks per group to 32");
+  rank = r;
+  group = r / N;
+  local = r % N;
+  device = dev;
+  S2D_CUDA(cudaSetDevice(dev));
+  S2D_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+  stream = own_stream;
+  err.ensure(4);
+  S2D_CUDA(cudaMemsetAsync(err.p, 0, 4, stream));
+  err_host.ensure(4);
+  *err_host.as<uint32_t>() = 0;
+  h_counts.ensure(4096);
+  if (T > 1) {
+    if (!nccl_id) throw Error(S2D_EINVAL, "nccl_id required when total_ranks > 1");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    S2D_NCCL(ncclCommInitRank(&world, (int)T, id, (int)rank));
+    // MP group: contiguous ranks {g*N .. g*N+N-1}; DP group: {l, l+N, ...}
+    S2D_NCCL(ncclCommSplit(world, (int)group, (int)local, &mp, nullptr));
+    S2D_NCCL(ncclCommSplit(world, (int)local, (int)group, &dp, nullptr));
+  }
+}
+
+void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_entry* p, uint32_t np,
+                          int dtype) {
+  if (n == 0) throw Error(S2D_EINVAL, "at least one table required");
+  if (dtype != S2D_F32 && dtype != S2D_BF16) throw Error(S2D_EINVAL, "weight dtype must be F32 or BF16");
+  S2D_CUDA(cudaSetDevice(device));
+  tables.assign(t, t + n);
+  plan.assign(p, p + np);
+  F = n;
+  bf16 = dtype == S2D_BF16;
+  feats.assign(F, FeatDev{});
+  ranges.clear();
+  sum_dims = 0;
+  max_dim = 0;
+  for (uint32_t f = 0; f < F; ++f) {
+    const auto& d = tables[f];
+    if (d.table_id != f) throw Error(S2D_EINVAL, "table_id must equal its index");
+    if (d.rows < 1 || d.dim < 1) throw Error(S2D_EINVAL, "table needs rows >= 1 and dim >= 1");
+    if (d.dim % 4 || d.dim > (uint32_t)kMaxDim)
+      throw Error(S2D_EINVAL, "dim must be a multiple of 4 and <= 512 (table " + std::to_string(f) + ")");
+    feats[f].dim = d.dim;
+    feats[f].rows = d.rows;
+    feats[f].coff = sum_dims;
+    sum_dims += d.dim;
+    max_dim = std::max(max_dim, d.dim);
+  }
+  // plan: coverage + ownership (validate_plan semantics)
+  std::vector<s2d_table_load_profile> prof(F);
+  for (uint32_t f = 0; f < F; ++f) prof[f] = {f, (uint64_t)tables[f].rows * tables[f].dim * 4, 0.0, tables[f].rows};
+  validate_plan(plan, N, prof);
+  n_slots = 0;
+  n_weight_elems = 0;
+  for (uint32_t f = 0; f < F; ++f) {
+    std::vector<s2d_plan_entry> mine;
+    for (const auto& e : plan)
+      if (e.table_id == f) mine.push_back(e);
+    std::sort(mine.begin(), mine.end(), [](const s2d_plan_entry& a, const s2d_plan_entry& b) { return a.row_lo < b.row_lo; });
+    feats[f].rbeg = (uint32_t)ranges.size();
+    bool owned = false;
+    for (const auto& e : mine) {
+      ranges.push_back({e.row_lo, e.row_hi, e.local_rank, 0});
+      if (e.local_rank == local) {
+        if (owned) throw Error(S2D_EINVAL, "a local rank may own at most one range per table");
+        owned = true;
+        feats[f].lo = e.row_lo;
+        feats[f].hi = e.row_hi;
+      }
+    }
+    feats[f].rend = (uint32_t)ranges.size();
+    feats[f].vbase = n_slots;
+    feats[f].wbase = n_weight_elems;
+    const uint64_t own = feats[f].hi - feats[f].lo;
+    if ((uint64_t)n_slots + own >= 0xffffffffull) throw Error(S2D_EINVAL, "too many rows on one rank (>= 2^32-1)");
+    n_slots += (uint32_t)own;
+    n_weight_elems += own * feats[f].dim;
+  }
+  vbase_sorted.clear();
+  feat_of_vbase.clear();
+  for (uint32_t f = 0; f < F; ++f)
+    if (feats[f].hi > feats[f].lo) {
+      vbase_sorted.push_back(feats[f].vbase);
+      feat_of_vbase.push_back(f);
+    }
+  if (vbase_sorted.empty()) {
+    vbase_sorted.push_back(0);
+    feat_of_vbase.push_back(0);
+  }
+  vbase_sorted.push_back(n_slots);
+  d_feats.ensure(sizeof(FeatDev) * F);
+  d_ranges.ensure(sizeof(RangeDev) * std::max<size_t>(1, ranges.size()));
+  d_vbase_sorted.ensure(4 * vbase_sorted.size());
+  d_feat_of_vbase.ensure(4 * feat_of_vbase.size());
+  S2D_CUDA(cudaMemcpy(d_feats.p, feats.data(), sizeof(FeatDev) * F, cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d_ranges.p, ranges.data(), sizeof(RangeDev) * ranges.size(), cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d_vbase_sorted.p, vbase_sorted.data(), 4 * vbase_sorted.size(), cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d_feat_of_vbase.p, feat_of_vbase.data(), 4 * feat_of_vbase.size(), cudaMemcpyHostToDevice));
+  const size_t wbytes = n_weight_elems * (bf16 ? 2 : 4);
+  weights.release();
+  moments.release();
+  dirty.release();
+  weights.ensure(std::max<size_t>(wbytes, 16));
+  moments.ensure(std::max<size_t>((size_t)n_slots * 4, 16));
+  S2D_CUDA(cudaMemsetAsync(weights.p, 0, wbytes, stream));
+  S2D_CUDA(cudaMemsetAsync(moments.p, 0, (size_t)n_slots * 4, stream));
+  if (M > 1) {
+    dirty.ensure(std::max<size_t>(n_slots, 16));
+    S2D_CUDA(cudaMemsetAsync(dirty.p, 0, n_slots, stream));
+  }
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  fwd_done = false;
+}
+
+void Ctx::set_optimizer(const s2d_optimizer_config& c) {
+  check_optimizer(c);
+  opt = c;
+  have_opt = true;
+}
+
+void Ctx::init_tables(uint64_t seed) {
+  if (!F) throw Error(S2D_EINVAL, "register tables first");
+  S2D_CUDA(cudaSetDevice(device));
+  launch_init_rows(weights.p, bf16, feats.data(), F, seed, stream);
+  S2D_CUDA(cudaMemsetAsync(moments.p, 0, (size_t)n_slots * 4, stream));
+  if (M > 1) S2D_CUDA(cudaMemsetAsync(dirty.p, 0, n_slots, stream));
+  finish_call();
+}
+
+void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v, bool write) {
+  if (table >= F) throw Error(S2D_EINVAL, "table out of range");
+  const FeatDev& fd = feats[table];
+  if (lo > hi || lo < fd.lo || hi > fd.hi)
+    throw Error(S2D_ERANGE, "rows [" + std::to_string(lo) + "," + std::to_string(hi) + ") outside owned range [" +
+                                std::to_string(fd.lo) + "," + std::to_string(fd.hi) + ") of table " +
+                                std::to_string(table));
+  if (hi == lo) return;
+  S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  const uint64_t n = (uint64_t)(hi - lo) * fd.dim;
+  const uint64_t off = fd.wbase + (uint64_t)(lo - fd.lo) * fd.dim;
+  if (w) {
+    if (!bf16) {
+      float* dst = weights.as<float>() + off;
+      if (write)
+        S2D_CUDA(cudaMemcpy(dst, w, n * 4, cudaMemcpyHostToDevice));
+      else
+        S2D_CUDA(cudaMemcpy(w, dst, n * 4, cudaMemcpyDeviceToHost));
+    } else {
+      std::vector<uint16_t> tmp(n);
+      uint16_t* dst = weights.as<uint16_t>() + off;
+      if (write) {
+        for (uint64_t i = 0; i < n; ++i) {  // round-to-nearest-even f32 -> bf16
+          uint32_t x;
+          std::memcpy(&x, &w[i], 4);
+          if ((x & 0x7f800000u) == 0x7f800000u && (x & 0x7fffffu))
+            tmp[i] = (uint16_t)((x >> 16) | 0x40);
+          else
+            tmp[i] = (uint16_t)((x + 0x7fffu + ((x >> 16) & 1u)) >> 16);
+        }
+        S2D_CUDA(cudaMemcpy(dst, tmp.data(), n * 2, cudaMemcpyHostToDevice));
+      } else {
+        S2D_CUDA(cudaMemcpy(tmp.data(), dst, n * 2, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < n; ++i) {
+          const uint32_t x = (uint32_t)tmp[i] << 16;
+          std::memcpy(&w[i], &x, 4);
+        }
+      }
+    }
+  }
+  if (v) {
+    float* dst = moments.as<float>() + fd.vbase + (lo - fd.lo);
+    if (write)
+      S2D_CUDA(cudaMemcpy(dst, v, (size_t)(hi - lo) * 4, cudaMemcpyHostToDevice));
+    else
+      S2D_CUDA(cudaMemcpy(v, dst, (size_t)(hi - lo) * 4, cudaMemcpyDeviceToHost));
+  }
+}
+
+void Ctx::check_faults() {
+  const uint32_t e = *err_host.as<uint32_t>();
+  if (!e) return;
+  *err_host.as<uint32_t>() = 0;
+  S2D_CUDA(cudaMemsetAsync(err.p, 0, 4, stream));
+  stats.error_flags = e;
+  if (e & kErrIdRange) throw Error(S2D_ERANGE, "lookup id outside the table's rows / shard ranges");
+  if (e & kErrNonfinite) throw Error(S2D_ENONFINITE, "nonfinite row gradient");
+}
+
+void Ctx::finish_call() {
+  S2D_CUDA(cudaMemcpyAsync(err_host.p, err.p, 4, cudaMemcpyDeviceToHost, stream));
+  if (strict) synchronize_and_check();
+}
+
+void Ctx::synchronize_and_check() {
+  S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaMemcpyAsync(err_host.p, err.p, 4, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  check_faults();
+}
+
+// ---- forward -------------------------------------------------------------
+
+void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t* ids, uint64_t nnz,
+                         float* pooled, int mem) {
+  if (!F) throw Error(S2D_EINVAL, "register tables first");
+  if (batch == 0) throw Error(S2D_EINVAL, "batch must be >= 1");
+  if (nnz >= 0xffffffffull) throw Error(S2D_EINVAL, "nnz must be < 2^32-1 per rank");
+  if (mem != S2D_HOST && mem != S2D_DEVICE) throw Error(S2D_EINVAL, "mem must be S2D_HOST or S2D_DEVICE");
+  S2D_CUDA(cudaSetDevice(device));
+  B = batch;
+  nnz_local = nnz;
+  const uint64_t BF = (uint64_t)B * F;
+  stats = s2d_step_stats{};
+  stats.nnz_local = nnz;
+  // stage inputs
+  const uint32_t* d_len = lengths;
+  const uint32_t* d_ids = ids;
+  float* d_pooled = pooled;
+  if (mem == S2D_HOST) {
+    in_lengths.ensure(BF * 4);
+    in_ids.ensure(std::max<uint64_t>(nnz, 1) * 4);
+    pooled_stage.ensure(BF ? (uint64_t)B * sum_dims * 4 : 16);
+    S2D_CUDA(cudaMemcpyAsync(in_lengths.p, lengths, BF * 4, cudaMemcpyHostToDevice, stream));
+    if (nnz) S2D_CUDA(cudaMemcpyAsync(in_ids.p, ids, nnz * 4, cudaMemcpyHostToDevice, stream));
+    d_len = in_lengths.as<uint32_t>();
+    d_ids = in_ids.as<uint32_t>();
+    d_pooled = pooled_stage.as<float>();
+  }
+  scan_tmp.ensure(scan_tmp_bytes(std::max<uint64_t>((uint64_t)N * BF, nnz) + 1));
+  in_off.ensure((BF + 1) * 4);
+  scan_u32_to_u32(d_len, in_off.as<uint32_t>(), BF, stream, scan_tmp.p, scan_tmp.cap);
+  const FeatDev* dfe = d_feats.as<FeatDev>();
+
+  if (N == 1) {
+    nnz_own = nnz;
+    keys_a.ensure(std::max<uint64_t>(nnz, 1) * 4);
+    vals_a.ensure(std::max<uint64_t>(nnz, 1) * 4);
+    LookupArgs a{};
+    a.feats = dfe;
+    a.F = F;
+    a.B = B;
+    a.n_req = 1;
+    a.sum_dims = sum_dims;
+    a.lengths = d_len;
+    a.id_off = in_off.as<uint32_t>();
+    a.ids = d_ids;
+    a.weights = weights.p;
+    a.out = d_pooled;
+    a.eoff = nullptr;
+    a.keys = keys_a.as<uint32_t>();
+    a.vals = vals_a.as<uint32_t>();
+    a.err = err.as<uint32_t>();
+    a.direct = 1;
+    a.emit_keys = 1;
+    launch_owner_lookup(a, bf16, (int)max_dim, stream);
+    stats.nnz_owned = nnz;
+  } else {
+    // K1: bucket by owner
+    cnt.ensure((uint64_t)N * BF * 4);
+    send_off.ensure(((uint64_t)N * BF + 1) * 4);
+    eoff_req.ensure(((uint64_t)N * BF + 1) * 8);
+    send_ids.ensure(std::max<uint64_t>(nnz, 1) * 4);
+    BucketArgs ba{};
+    ba.feats = dfe;
+    ba.ranges = d_ranges.as<RangeDev>();
+    ba.F = F;
+    ba.BF = (uint32_t)BF;
+    ba.N = N;
+    ba.lengths = d_len;
+    ba.id_off = in_off.as<uint32_t>();
+    ba.ids = d_ids;
+    ba.cnt = cnt.as<uint32_t>();
+    ba.send_off = send_off.as<uint32_t>();
+    ba.send_ids = send_ids.as<uint32_t>();
+    ba.err = err.as<uint32_t>();
+    launch_bucket_count(ba, stream);
+    scan_u32_to_u32(cnt.as<uint32_t>(), send_off.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p, scan_tmp.cap);
+    scan_nonzero_dim_u64(cnt.as<uint32_t>(), eoff_req.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream, scan_tmp.p,
+                         scan_tmp.cap);
+    launch_bucket_permute(ba, stream);
+    a2a_counts();
+    // ids + lengths all-to-all inside the MP group
+    recv_lengths.ensure((uint64_t)N * BF * 4);
+    recv_ids.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
+    S2D_NCCL(ncclGroupStart());
+    for (uint32_t p = 0; p < N; ++p) {
+      if (p == local) continue;
+      S2D_NCCL(ncclSend(cnt.as<uint32_t>() + (uint64_t)p * BF, BF, ncclUint32, (int)p, mp, stream));
+      S2D_NCCL(ncclRecv(recv_lengths.as<uint32_t>() + (uint64_t)p * BF, BF, ncclUint32, (int)p, mp, stream));
+      if (nnz_to[p]) S2D_NCCL(ncclSend(send_ids.as<uint32_t>() + ids_base_to[p], nnz_to[p], ncclUint32, (int)p, mp, stream));
+      if (nnz_from[p])
+        S2D_NCCL(ncclRecv(recv_ids.as<uint32_t>() + nnz_base_from[p], nnz_from[p], ncclUint32, (int)p, mp, stream));
+    }
+    S2D_NCCL(ncclGroupEnd());
+    S2D_CUDA(cudaMemcpyAsync(recv_lengths.as<uint32_t>() + (uint64_t)local * BF, cnt.as<uint32_t>() + (uint64_t)local * BF,
+                             BF * 4, cudaMemcpyDeviceToDevice, stream));
+    if (nnz_to[local])
+      S2D_CUDA(cudaMemcpyAsync(recv_ids.as<uint32_t>() + nnz_base_from[local], send_ids.as<uint32_t>() + ids_base_to[local],
+                               nnz_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
+    // owner side: offsets of the received demand, entry offsets of partials
+    own_idoff.ensure(((uint64_t)N * BF + 1) * 4);
+    own_eoff.ensure(((uint64_t)N * BF + 1) * 8);
+    scan_u32_to_u32(recv_lengths.as<uint32_t>(), own_idoff.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p,
+                    scan_tmp.cap);
+    scan_nonzero_dim_u64(recv_lengths.as<uint32_t>(), own_eoff.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream,
+                         scan_tmp.p, scan_tmp.cap);
+    uint64_t ef_own = 0, ef_req = 0;
+    for (uint32_t p = 0; p < N; ++p) {
+      ef_own += ef_from[p];
+      ef_req += ef_to[p];
+    }
+    part_send.ensure(std::max<uint64_t>(ef_own, 4) * 4);
+    part_recv.ensure(std::max<uint64_t>(ef_req, 4) * 4);
+    keys_a.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
+    vals_a.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
+    LookupArgs a{};
+    a.feats = dfe;
+    a.F = F;
+    a.B = B;
+    a.n_req = N;
+    a.sum_dims = sum_dims;
+    a.lengths = recv_lengths.as<uint32_t>();
+    a.id_off = own_idoff.as<uint32_t>();
+    a.ids = recv_ids.as<uint32_t>();
+    a.weights = weights.p;
+    a.out = part_send.as<float>();
+    a.eoff = own_eoff.as<uint64_t>();
+    a.keys = keys_a.as<uint32_t>();
+    a.vals = vals_a.as<uint32_t>();
+    a.err = err.as<uint32_t>();
+    a.direct = 0;
+    a.emit_keys = 1;
+    launch_owner_lookup(a, bf16, (int)max_dim, stream);
+    // C1: partials back to requesters
+    S2D_NCCL(ncclGroupStart());
+    for (uint32_t p = 0; p < N; ++p) {
+      if (p == local) continue;
+      if (ef_from[p]) S2D_NCCL(ncclSend(part_send.as<float>() + ef_base_from[p], ef_from[p], ncclFloat32, (int)p, mp, stream));
+      if (ef_to[p]) S2D_NCCL(ncclRecv(part_recv.as<float>() + ef_base_to[p], ef_to[p], ncclFloat32, (int)p, mp, stream));
+    }
+    S2D_NCCL(ncclGroupEnd());
+    if (ef_to[local])
+      S2D_CUDA(cudaMemcpyAsync(part_recv.as<float>() + ef_base_to[local], part_send.as<float>() + ef_base_from[local],
+                               ef_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
+    CombineArgs ca{};
+    ca.feats = dfe;
+    ca.F = F;
+    ca.B = B;
+    ca.N = N;
+    ca.sum_dims = sum_dims;
+    ca.cnt = cnt.as<uint32_t>();
+    ca.eoff = eoff_req.as<uint64_t>();
+    ca.recv = part_recv.as<float>();
+    ca.pooled = d_pooled;
+    launch_combine(ca, (int)max_dim, stream);
+    stats.nnz_owned = nnz_own;
+    uint64_t sent = 0, recv = 0;
+    for (uint32_t p = 0; p < N; ++p) {
+      if (p == local) continue;
+      sent += nnz_to[p] * 4 + BF * 4 + ef_from[p] * 4;
+      recv += nnz_from[p] * 4 + BF * 4 + ef_to[p] * 4;
+    }
+    stats.a2a_bytes_sent = sent;
+    stats.a2a_bytes_recv = recv;
+  }
+  if (mem == S2D_HOST) {
+    S2D_CUDA(cudaMemcpyAsync(pooled, d_pooled, (uint64_t)B * sum_dims * 4, cudaMemcpyDeviceToHost, stream));
+    S2D_CUDA(cudaStreamSynchronize(stream));
+  }
+  fwd_done = true;
+  finish_call();
+}
+
+// counts all-to-all: per peer p, (ids to p, partial floats for p's bags).
+void Ctx::a2a_counts() {
+  const uint64_t BF = (uint64_t)B * F;
+  bounds.ensure(8 * (2 * (N + 1) + 4 * N));
+  uint64_t* d_b = bounds.as<uint64_t>();
+  k_gather_bounds<<<1, 64, 0, stream>>>(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF, d_b);
+  S2D_LAUNCH_CHECK();
+  // d_b[0..N] id bounds, d_b[N+1..2N+1] float bounds; pack per-peer pairs
+  // into d_b[2N+2 ..] (send) and receive pairs after it.
+  h_counts.ensure(8 * (8 * (N + 1)));
+  S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_b, 8 * 2 * (N + 1), cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  const uint64_t* hb = h_counts.as<uint64_t>();
+  nnz_to.assign(N, 0);
+  ef_to.assign(N, 0);
+  ids_base_to.assign(N, 0);
+  ef_base_to.assign(N, 0);
+  for (uint32_t p = 0; p < N; ++p) {
+    ids_base_to[p] = hb[p];
+    nnz_to[p] = hb[p + 1] - hb[p];
+    ef_base_to[p] = hb[N + 1 + p];
+    ef_to[p] = hb[N + 2 + p] - hb[N + 1 + p];
+  }
+  // exchange (nnz, floats) pairs
+  std::vector<uint64_t> sendpairs(2 * N);
+  for (uint32_t p = 0; p < N; ++p) {
+    sendpairs[2 * p] = nnz_to[p];
+    sendpairs[2 * p + 1] = ef_to[p];
+  }
+  uint64_t* d_send = d_b + 2 * (N + 1);
+  uint64_t* d_recv = d_send + 2 * N;
+  S2D_CUDA(cudaMemcpyAsync(d_send, sendpairs.data(), 8 * 2 * N, cudaMemcpyHostToDevice, stream));
+  S2D_NCCL(ncclGroupStart());
+  for (uint32_t p = 0; p < N; ++p) {
+    if (p == local) continue;
+    S2D_NCCL(ncclSend(d_send + 2 * p, 2, ncclUint64, (int)p, mp, stream));
+    S2D_NCCL(ncclRecv(d_recv + 2 * p, 2, ncclUint64, (int)p, mp, stream));
+  }
+  S2D_NCCL(ncclGroupEnd());
+  std::vector<uint64_t> rp(2 * N, 0);
+  S2D_CUDA(cudaMemcpyAsync(rp.data(), d_recv, 8 * 2 * N, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  rp[2 * local] = nnz_to[local];
+  rp[2 * local + 1] = ef_to[local];
+  nnz_from.assign(N, 0);
+  ef_from.assign(N, 0);
+  nnz_base_from.assign(N, 0);
+  ef_base_from.assign(N, 0);
+  nnz_own = 0;
+  uint64_t efb = 0;
+  for (uint32_t p = 0; p < N; ++p) {
+    nnz_from[p] = rp[2 * p];
+    ef_from[p] = rp[2 * p + 1];
+    nnz_base_from[p] = nnz_own;
+    ef_base_from[p] = efb;
+    nnz_own += nnz_from[p];
+    efb += ef_from[p];
+  }
+  if (nnz_own >= 0xffffffffull) throw Error(S2D_EINVAL, "owner demand exceeds 2^32-1 ids");
+}
+
+// ---- backward + fused update ---------------------------------------------------
+
+void Ctx::backward_update(const float* upstream, int mem) {
+  if (!fwd_done) throw Error(S2D_EINVAL, "backward_update needs a preceding lookup_forward");
+  if (!have_opt) throw Error(S2D_EINVAL, "set_optimizer first");
+  if (mem != S2D_HOST && mem != S2D_DEVICE) throw Error(S2D_EINVAL, "mem must be S2D_HOST or S2D_DEVICE");
+  S2D_CUDA(cudaSetDevice(device));
+  const uint64_t BF = (uint64_t)B * F;
+  const float* d_up = upstream;
+  if (mem == S2D_HOST) {
+    upstream_stage.ensure((uint64_t)B * sum_dims * 4);
+    S2D_CUDA(cudaMemcpyAsync(upstream_stage.p, upstream, (uint64_t)B * sum_dims * 4, cudaMemcpyHostToDevice, stream));
+    d_up = upstream_stage.as<float>();
+  }
+  const float* grad = d_up;
+  if (N > 1) {
+    uint64_t ef_req = 0, ef_own = 0;
+    for (uint32_t p = 0; p < N; ++p) {
+      ef_req += ef_to[p];
+      ef_own += ef_from[p];
+    }
+    grad_send.ensure(std::max<uint64_t>(ef_req, 4) * 4);
+    grad_recv.ensure(std::max<uint64_t>(ef_own, 4) * 4);
+    GradGatherArgs ga{};
+    ga.feats = d_feats.as<FeatDev>();
+    ga.F = F;
+    ga.B = B;
+    ga.N = N;
+    ga.sum_dims = sum_dims;
+    ga.cnt = cnt.as<uint32_t>();
+    ga.eoff = eoff_req.as<uint64_t>();
+    ga.upstream = d_up;
+    ga.send = grad_send.as<float>();
+    launch_grad_gather(ga, (int)max_dim, stream);
+    // C2: gradients to owners; the owner's receive layout equals its
+    // partial send layout, so the lookup's (slot, val) pairs index it.
+    S2D_NCCL(ncclGroupStart());
+    for (uint32_t p = 0; p < N; ++p) {
+      if (p == local) continue;
+      if (ef_to[p]) S2D_NCCL(ncclSend(grad_send.as<float>() + ef_base_to[p], ef_to[p], ncclFloat32, (int)p, mp, stream));
+      if (ef_from[p])
+        S2D_NCCL(ncclRecv(grad_recv.as<float>() + ef_base_from[p], ef_from[p], ncclFloat32, (int)p, mp, stream));
+    }
+    S2D_NCCL(ncclGroupEnd());
+    if (ef_to[local])
+      S2D_CUDA(cudaMemcpyAsync(grad_recv.as<float>() + ef_base_from[local], grad_send.as<float>() + ef_base_to[local],
+                               ef_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
+    grad = grad_recv.as<float>();
+    uint64_t sent = 0, recv = 0;
+    for (uint32_t p = 0; p < N; ++p) {
+      if (p == local) continue;
+      sent += ef_to[p] * 4;
+      recv += ef_from[p] * 4;
+    }
+    stats.a2a_bytes_sent += sent;
+    stats.a2a_bytes_recv += recv;
+  }
+  (void)BF;
+  const uint64_t n = nnz_own;
+  uint64_t uniq = 0;
+  if (n > 0) {
+    keys_b.ensure(n * 4);
+    vals_b.ensure(n * 4);
+    const int bits = std::max(1, bit_width(n_slots));
+    sort_tmp.ensure(radix_tmp_bytes(n, bits));
+    sorted_in_b = radix_sort_pairs(keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_b.as<uint32_t>(),
+                                   vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, stream);
+    const uint32_t* sk = sorted_in_b ? keys_b.as<uint32_t>() : keys_a.as<uint32_t>();
+    const uint32_t* sv = sorted_in_b ? vals_b.as<uint32_t>() : vals_a.as<uint32_t>();
+    uslot.ensure((n + 1) * 4);
+    useg.ensure((n + 2) * 4);
+    counters.ensure(64);
+    chunk_base.ensure((n + 1) * 4);
+    chunk_seg.ensure((n / kChunk + 2) * 4);
+    chunk_part.ensure((n / kChunk + 2) * (uint64_t)max_dim * 8);
+    scan_tmp.ensure(scan_tmp_bytes(n + 1));
+    SegmentArgs sa{};
+    sa.keys = sk;
+    sa.n = n;
+    sa.n_slots = n_slots;
+    sa.uslot = uslot.as<uint32_t>();
+    sa.useg = useg.as<uint32_t>();
+    sa.counters = counters.as<uint32_t>();
+    sa.chunk_base = chunk_base.as<uint32_t>();
+    sa.chunk_seg = chunk_seg.as<uint32_t>();
+    sa.tmp = scan_tmp.p;
+    sa.tmp_bytes = scan_tmp.cap;
+    run_segments(sa, stream);
+    UpdateArgs ua{};
+    ua.feats = d_feats.as<FeatDev>();
+    ua.vbase_sorted = d_vbase_sorted.as<uint32_t>();
+    ua.feat_of_vbase = d_feat_of_vbase.as<uint32_t>();
+    ua.n_feat_owned = (uint32_t)feat_of_vbase.size();
+    ua.uslot = uslot.as<uint32_t>();
+    ua.useg = useg.as<uint32_t>();
+    ua.vals = sv;
+    ua.counters = counters.as<uint32_t>();
+    ua.chunk_base = chunk_base.as<uint32_t>();
+    ua.chunk_seg = chunk_seg.as<uint32_t>();
+    ua.chunk_part = chunk_part.as<double>();
+    ua.grad = grad;
+    ua.weights = weights.p;
+    ua.moments = moments.as<float>();
+    ua.dirty = M > 1 ? dirty.as<uint8_t>() : nullptr;
+    ua.inv_batch = 1.0 / (double)((uint64_t)N * B);  // group batch (trainer.cpp:462)
+    ua.eta = opt.eta;
+    ua.eps = opt.eps;
+    ua.c = opt.c;
+    ua.sgd = opt.variant == S2D_SGD;
+    ua.err = err.as<uint32_t>();
+    launch_update(ua, bf16, (int)max_dim, n, stream);
+    uniq = 1;
+  }
+  (void)uniq;
+  fwd_done = false;
+  finish_call();
+  if (strict && n > 0) {
+    uint32_t c[4];
+    S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
+    stats.unique_rows = c[0];
+    stats.long_segments = c[2];
+  }
+}
+
+// ---- K5 replica sync ---------------------------------------------------------
+
+void Ctx::replica_sync() {
+  if (M <= 1 || !F) return;
+  S2D_CUDA(cudaSetDevice(device));
+  // union of dirty rows across the DP group
+  S2D_NCCL(ncclAllReduce(dirty.p, dirty.p, n_slots, ncclUint8, ncclMax, dp, stream));
+  sync_list.ensure((uint64_t)std::max<uint32_t>(n_slots, 1) * 4);
+  sync_count.ensure(16);
+  sync_tmp.ensure(((uint64_t)n_slots / 4096 + 2) * 4);
+  launch_dirty_compact(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_count.as<uint32_t>(), sync_tmp.p,
+                       sync_tmp.cap, stream);
+  uint32_t count = 0;
+  S2D_CUDA(cudaMemcpyAsync(h_counts.p, sync_count.p, 4, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  count = *h_counts.as<uint32_t>();
+  stats.dirty_rows = count;
+  if (count) {
+    const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
+    sync_packed.ensure((uint64_t)count * row_floats * 4);
+    sync_gathered.ensure((uint64_t)count * row_floats * 4 * M);
+    launch_pack_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                     (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), sync_count.as<uint32_t>(), weights.p,
+                     bf16, moments.as<float>(), row_floats, sync_packed.as<float>(), count, stream);
+    S2D_NCCL(ncclAllGather(sync_packed.p, sync_gathered.p, (size_t)count * row_floats, ncclFloat32, dp, stream));
+    launch_mean_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                     (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), sync_count.as<uint32_t>(),
+                     sync_gathered.as<float>(), M, row_floats, count, weights.p, bf16, moments.as<float>(),
+                     opt.variant == S2D_SGD, dirty.as<uint8_t>(), stream);
+    stats.sync_bytes = (uint64_t)count * row_floats * 4 * (M - 1);
+  }
+  finish_call();
+}
+
+// ---- debug views ------------------------------------------------------------
+
+void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
+  S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  const uint64_t BF = (uint64_t)B * F;
+  auto copy = [&](const void* src, uint64_t elems, size_t esz) {
+    *n = elems;
+    const uint64_t k = std::min(cap, elems);
+    if (k && out) S2D_CUDA(cudaMemcpy(out, src, k * esz, cudaMemcpyDeviceToHost));
+  };
+  switch (which) {
+    case 0:
+      if (N == 1) copy(in_lengths.p, 0, 4);
+      else copy(recv_lengths.p, (uint64_t)N * BF, 4);
+      break;
+    case 1:
+      if (N == 1) copy(in_ids.p, 0, 4);
+      else copy(recv_ids.p, nnz_own, 4);
+      break;
+    case 2: {
+      uint64_t t = 0;
+      for (auto x : ef_from) t += x;
+      copy(part_send.p, N == 1 ? 0 : t, 4);
+      break;
+    }
+    case 3: {
+      uint64_t t = 0;
+      for (auto x : ef_to) t += x;
+      copy(grad_send.p, N == 1 ? 0 : t, 4);
+      break;
+    }
+    case 4: {
+      std::vector<uint32_t> c((uint64_t)N * BF, 0), mask(BF, 0);
+      if (N > 1) S2D_CUDA(cudaMemcpy(c.data(), cnt.p, c.size() * 4, cudaMemcpyDeviceToHost));
+      for (uint64_t b = 0; b < BF; ++b)
+        for (uint32_t o = 0; o < N; ++o)
+          if (N == 1 || c[(uint64_t)o * BF + b]) mask[b] |= 1u << o;
+      *n = BF;
+      if (out) std::memcpy(out, mask.data(), std::min(cap, BF) * 4);
+      break;
+    }
+    case 5: {
+      uint32_t c[4] = {0, 0, 0, 0};
+      if (nnz_own) S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> sl(c[0]);
+      if (c[0]) S2D_CUDA(cudaMemcpy(sl.data(), uslot.p, (uint64_t)c[0] * 4, cudaMemcpyDeviceToHost));
+      // slot -> global row of its table
+      for (auto& s : sl) {
+        const size_t i = std::upper_bound(vbase_sorted.begin(), vbase_sorted.end() - 1, s) - vbase_sorted.begin() - 1;
+        const FeatDev& fd = feats[feat_of_vbase[i]];
+        s = s - fd.vbase + fd.lo;
+      }
+      *n = c[0];
+      if (out) std::memcpy(out, sl.data(), std::min<uint64_t>(cap, c[0]) * 4);
+      break;
+    }
+    default:
+      throw Error(S2D_EINVAL, "unknown debug buffer");
+  }
+}
+
+}  // namespace s2d

@@ -1,0 +1,103 @@
+// Per-GPU context: owns the rank's shards, workspaces, stream and NCCL
+// communicators, and sequences one 2D-sparse-parallel step.  Mirrors
+// Trainer::Impl's per-rank state (src/trainer.cpp:164-257) minus the dense
+// MLP, with the simulated collectives replaced by NCCL over NVLink.
+#pragma once
+
+#include <nccl.h>
+
+#include <vector>
+
+#include "common.h"
+
+namespace s2d {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes);
+  void release();
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+  ~DevBuf() { release(); }
+};
+
+struct HostBuf {  // pinned
+  void* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t bytes);
+  ~HostBuf();
+  template <typename T>
+  T* as() const {
+    return reinterpret_cast<T*>(p);
+  }
+};
+
+struct Ctx {
+  // mesh (topology.hpp:13-26): rank -> (group = r / N, local = r % N)
+  int device = 0;
+  uint32_t T = 1, M = 1, N = 1, rank = 0, group = 0, local = 0;
+  cudaStream_t own_stream = nullptr, stream = nullptr;
+  ncclComm_t world = nullptr, mp = nullptr, dp = nullptr;
+  bool strict = true;
+
+  // tables + plan
+  uint32_t F = 0, sum_dims = 0, max_dim = 0;
+  int bf16 = 0;
+  std::vector<s2d_table_desc> tables;
+  std::vector<s2d_plan_entry> plan;
+  std::vector<FeatDev> feats;
+  std::vector<RangeDev> ranges;
+  std::vector<uint32_t> vbase_sorted, feat_of_vbase;  // owned features by slot base
+  uint32_t n_slots = 0;
+  uint64_t n_weight_elems = 0;
+  DevBuf d_feats, d_ranges, d_vbase_sorted, d_feat_of_vbase;
+  DevBuf weights, moments, dirty;
+
+  s2d_optimizer_config opt{0.05, 1e-8, 1.0, S2D_ROWWISE_ADAGRAD};
+  bool have_opt = false;
+
+  // device fault flag
+  DevBuf err;
+  HostBuf err_host;
+
+  // ---- per-step state ----
+  uint32_t B = 0;
+  uint64_t nnz_local = 0, nnz_own = 0;
+  bool fwd_done = false;
+  DevBuf in_lengths, in_ids, in_off, pooled_stage, upstream_stage;
+  DevBuf cnt, send_off, eoff_req, send_ids, bounds;  // requester side (N > 1)
+  DevBuf recv_lengths, recv_ids, own_idoff, own_eoff;  // owner side (N > 1)
+  DevBuf part_send, part_recv, grad_send, grad_recv;
+  DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
+  DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
+  DevBuf sync_list, sync_count, sync_packed, sync_gathered, sync_tmp;
+  HostBuf h_counts;
+  std::vector<uint64_t> nnz_to, nnz_from, ef_to, ef_from, ids_base_to, ef_base_to, ef_base_from,
+      nnz_base_from;
+  bool sorted_in_b = false;
+  s2d_step_stats stats{};
+
+  ~Ctx();
+  void create(int device, uint32_t T, uint32_t M, uint32_t rank, const uint8_t* nccl_id);
+  void register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_entry* p, uint32_t np,
+                       int dtype);
+  void set_optimizer(const s2d_optimizer_config& c);
+  void init_tables(uint64_t seed);
+  void shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v, bool write);
+  void lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t* ids, uint64_t nnz,
+                      float* pooled, int mem);
+  void backward_update(const float* upstream, int mem);
+  void replica_sync();
+  void synchronize_and_check();
+  void debug_read(int which, void* out, uint64_t cap, uint64_t* n);
+
+ private:
+  void finish_call();
+  void check_faults();
+  void a2a_counts();
+};
+
+}  // namespace s2d

@@ -1,0 +1,392 @@
+// Forward-side kernels of the step:
+//   init_rows      device port of init_table (src/embedding.cpp:17-37)
+//   bucket_count   K1: ids per (owner, bag) for the input-dist all-to-all
+//   bucket_permute K1: bit-exact permute of ids into per-owner send blocks,
+//                  canonical (sample, feature, occurrence) order
+//                  (build_demand, src/trainer.cpp:283-313)
+//   owner_lookup   K2: f64 occurrence-order partial pool of each bag's owned
+//                  rows -> f32 (owner_lookup, src/trainer.cpp:316-338;
+//                  pool_ids, src/embedding.cpp:39-92) + the (slot, gradient
+//                  row) pairs the backward dedup sorts
+//   combine        requester side: f32(sum_{owner asc} f64(partial))
+//                  (pool_and_forward, src/trainer.cpp:372-390)
+//   grad_gather    C2 send layout (build_grad_payloads, src/trainer.cpp:440-457)
+//
+// Lookup layout: LPB lanes serve one bag, each lane owns VPL 16-byte column
+// vectors of the row, so a row gather is LPB*16 contiguous bytes per
+// vector; UNROLL rows are in flight per lane before the in-order f64 adds.
+#include <algorithm>
+
+#include "device.cuh"
+
+namespace s2d {
+namespace {
+
+// ---- init_table ----------------------------------------------------------
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:12-19
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ULL;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBULL;
+  x ^= x >> 31;
+  return x;
+}
+
+__device__ __forceinline__ uint64_t row_key(uint64_t seed, uint64_t table, uint64_t row) {
+  uint64_t h = 0x8A5CD789635D2DFFULL;  // make_key, rng.hpp:22-28
+  h = mix64(h + 0x9E3779B97F4A7C15ULL + seed);
+  h = mix64(h + 0x9E3779B97F4A7C15ULL + table);
+  h = mix64(h + 0x9E3779B97F4A7C15ULL + row);
+  return h;
+}
+
+template <typename WT>
+__global__ void k_init_rows(WT* __restrict__ w, uint64_t wbase, uint32_t table_id, uint32_t lo,
+                            uint32_t nrows, uint32_t dim, uint64_t seed) {
+  const uint32_t d4 = dim / 4;
+  const uint64_t total = (uint64_t)nrows * d4;
+  const double bound = 1.0 / sqrt((double)dim);
+  const double lo_v = -bound, span = __dsub_rn(bound, lo_v);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t r = (uint32_t)(i / d4), c4 = (uint32_t)(i % d4);
+    const uint64_t key = row_key(seed, table_id, (uint64_t)lo + r);
+    double d[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t ctr = (uint64_t)c4 * 4 + q + 1;
+      const double u = (double)(mix64(key + ctr * 0x9E3779B97F4A7C15ULL) >> 11) * 0x1.0p-53;
+      d[q] = (double)(float)__dadd_rn(lo_v, __dmul_rn(span, u));
+    }
+    Vec4<WT>::store(w + wbase + (uint64_t)r * dim + (uint64_t)c4 * 4, d);
+  }
+}
+
+// ---- lookup --------------------------------------------------------------
+
+template <typename WT>
+struct Raw;
+template <>
+struct Raw<float> {
+  using T = float4;
+  static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  static __device__ __forceinline__ void add(double (&a)[4], const T& x) {
+    a[0] += (double)x.x;
+    a[1] += (double)x.y;
+    a[2] += (double)x.z;
+    a[3] += (double)x.w;
+  }
+};
+template <>
+struct Raw<__nv_bfloat16> {
+  using T = uint2;
+  static __device__ __forceinline__ T load(const __nv_bfloat16* p) {
+    return __ldg(reinterpret_cast<const uint2*>(p));
+  }
+  static __device__ __forceinline__ void add(double (&a)[4], const T& x) {
+    a[0] += (double)__uint_as_float(x.x << 16);
+    a[1] += (double)__uint_as_float(x.x & 0xffff0000u);
+    a[2] += (double)__uint_as_float(x.y << 16);
+    a[3] += (double)__uint_as_float(x.y & 0xffff0000u);
+  }
+};
+
+template <typename WT, int LPB, int VPL, int UNROLL>
+__global__ void __launch_bounds__(256) k_owner_lookup(const LookupArgs a) {
+  constexpr int GPW = 32 / LPB;  // bag groups per warp
+  const uint32_t lane = lane_id();
+  const uint32_t grp = lane / LPB, gl = lane % LPB;
+  const uint32_t gmask = (LPB == 32) ? 0xffffffffu : (((1u << LPB) - 1u) << (grp * LPB));
+  const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
+  const uint64_t slots = (uint64_t)gridDim.x * (blockDim.x / 32) * GPW;
+  const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * GPW + grp;
+  const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
+  for (uint64_t bag = first; bag < n_bags; bag += slots) {
+    const uint32_t f = (uint32_t)(bag % a.F);
+    const uint32_t len = __ldg(a.lengths + bag);
+    if (!a.direct && len == 0) continue;
+    const uint32_t off = __ldg(a.id_off + bag);
+    const uint32_t dim = __ldg(&a.feats[f].dim), flo = __ldg(&a.feats[f].lo), fhi = __ldg(&a.feats[f].hi);
+    const uint64_t wbase = __ldg(&a.feats[f].wbase);
+    const uint32_t vbase = __ldg(&a.feats[f].vbase);
+    const uint64_t out_off = a.direct ? (uint64_t)((bag / a.F) % a.B) * a.sum_dims + __ldg(&a.feats[f].coff)
+                                      : __ldg(a.eoff + bag);
+    const uint32_t d4 = dim >> 2;
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[v][q] = 0.0;
+    for (uint32_t c = 0; c < len; c += LPB) {
+      const bool have = c + gl < len;
+      const uint32_t id = have ? __ldg(a.ids + off + c + gl) : 0u;
+      const bool ok = have && id >= flo && id < fhi;
+      if (have && !ok) atomicOr(a.err, kErrIdRange);
+      if (a.emit_keys && have) {
+        a.keys[off + c + gl] = ok ? vbase + (id - flo) : 0xffffffffu;
+        a.vals[off + c + gl] = (uint32_t)(out_off >> 2);
+      }
+      const uint32_t cnt = min((uint32_t)LPB, len - c);
+      for (uint32_t t = 0; t < cnt; t += UNROLL) {
+        typename Raw<WT>::T raw[UNROLL][VPL];
+        bool use[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const uint32_t src = grp * LPB + min(t + u, (uint32_t)LPB - 1);
+          const uint32_t rid = __shfl_sync(gmask, id, src);
+          const bool rok = __shfl_sync(gmask, ok, src);
+          use[u] = (t + u < cnt) && rok;
+          if (use[u]) {
+            const WT* row = W + wbase + (uint64_t)(rid - flo) * dim;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              const uint32_t c4 = gl + v * LPB;
+              if (c4 < d4) raw[u][v] = Raw<WT>::load(row + c4 * 4);
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          if (use[u]) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+              if (gl + v * LPB < d4) Raw<WT>::add(acc[v], raw[u][v]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const uint32_t c4 = gl + v * LPB;
+      if (c4 < d4) store_f32x4_stream(a.out + out_off + c4 * 4, acc[v]);
+    }
+  }
+}
+
+// ---- combine (requester side) -----------------------------------------------
+
+template <int LPB, int VPL>
+__global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
+  constexpr int GPW = 32 / LPB;
+  const uint32_t lane = lane_id();
+  const uint32_t grp = lane / LPB, gl = lane % LPB;
+  const uint64_t BF = (uint64_t)a.B * a.F;
+  const uint64_t slots = (uint64_t)gridDim.x * (blockDim.x / 32) * GPW;
+  const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * GPW + grp;
+  for (uint64_t b = first; b < BF; b += slots) {
+    const uint32_t f = (uint32_t)(b % a.F);
+    const uint32_t d4 = __ldg(&a.feats[f].dim) >> 2;
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[v][q] = 0.0;
+    for (uint32_t o = 0; o < a.N; ++o) {  // ascending owner (trainer.cpp:378-386)
+      if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
+      const float* p = a.recv + __ldg(a.eoff + (uint64_t)o * BF + b);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const uint32_t c4 = gl + v * LPB;
+        if (c4 < d4) {
+          const float4 x = __ldg(reinterpret_cast<const float4*>(p + c4 * 4));
+          acc[v][0] += (double)x.x;
+          acc[v][1] += (double)x.y;
+          acc[v][2] += (double)x.z;
+          acc[v][3] += (double)x.w;
+        }
+      }
+    }
+    float* out = a.pooled + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const uint32_t c4 = gl + v * LPB;
+      if (c4 < d4) store_f32x4_stream(out + c4 * 4, acc[v]);
+    }
+  }
+}
+
+template <int LPB, int VPL>
+__global__ void __launch_bounds__(256) k_grad_gather(const GradGatherArgs a) {
+  constexpr int GPW = 32 / LPB;
+  const uint32_t lane = lane_id();
+  const uint32_t grp = lane / LPB, gl = lane % LPB;
+  const uint64_t BF = (uint64_t)a.B * a.F;
+  const uint64_t slots = (uint64_t)gridDim.x * (blockDim.x / 32) * GPW;
+  const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * GPW + grp;
+  for (uint64_t b = first; b < BF; b += slots) {
+    const uint32_t f = (uint32_t)(b % a.F);
+    const uint32_t d4 = __ldg(&a.feats[f].dim) >> 2;
+    const float* up = a.upstream + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
+    float4 x[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      const uint32_t c4 = gl + v * LPB;
+      if (c4 < d4) x[v] = __ldg(reinterpret_cast<const float4*>(up + c4 * 4));
+    }
+    for (uint32_t o = 0; o < a.N; ++o) {  // (s, f, o ascending) order, trainer.cpp:446-453
+      if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
+      float* dst = a.send + __ldg(a.eoff + (uint64_t)o * BF + b);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const uint32_t c4 = gl + v * LPB;
+        if (c4 < d4) *reinterpret_cast<float4*>(dst + c4 * 4) = x[v];
+      }
+    }
+  }
+}
+
+// ---- K1 input-dist bucketing -------------------------------------------------
+
+__device__ __forceinline__ uint32_t owner_of(const RangeDev* __restrict__ r, uint32_t beg, uint32_t end,
+                                             uint32_t id) {
+  // ranges of one table sorted by lo; largest lo <= id
+  uint32_t lo = beg, hi = end;
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(&r[mid].lo) <= id)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return __ldg(&r[lo].owner);
+}
+
+__global__ void __launch_bounds__(256) k_bucket_count(const BucketArgs a) {
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.BF;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = (uint32_t)(b % a.F);
+    const uint32_t rows = __ldg(&a.feats[f].rows), rb = __ldg(&a.feats[f].rbeg), re = __ldg(&a.feats[f].rend);
+    uint32_t cnt[kMaxRanksPerGroup];
+    for (uint32_t o = 0; o < a.N; ++o) cnt[o] = 0;
+    const uint32_t off = __ldg(a.id_off + b), len = __ldg(a.lengths + b);
+    for (uint32_t k = 0; k < len; ++k) {
+      const uint32_t id = __ldg(a.ids + off + k);
+      if (id >= rows) {
+        atomicOr(a.err, kErrIdRange);
+        continue;
+      }
+      cnt[owner_of(a.ranges, rb, re, id)]++;
+    }
+    for (uint32_t o = 0; o < a.N; ++o) a.cnt[(uint64_t)o * a.BF + b] = cnt[o];
+  }
+}
+
+__global__ void __launch_bounds__(256) k_bucket_permute(const BucketArgs a) {
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.BF;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = (uint32_t)(b % a.F);
+    const uint32_t rows = __ldg(&a.feats[f].rows), rb = __ldg(&a.feats[f].rbeg), re = __ldg(&a.feats[f].rend);
+    uint32_t pos[kMaxRanksPerGroup];
+    for (uint32_t o = 0; o < a.N; ++o) pos[o] = __ldg(a.send_off + (uint64_t)o * a.BF + b);
+    const uint32_t off = __ldg(a.id_off + b), len = __ldg(a.lengths + b);
+    for (uint32_t k = 0; k < len; ++k) {
+      const uint32_t id = __ldg(a.ids + off + k);
+      if (id >= rows) continue;
+      const uint32_t o = owner_of(a.ranges, rb, re, id);
+      a.send_ids[pos[o]++] = id;
+    }
+  }
+}
+
+unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
+  uint64_t g = (work + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+constexpr unsigned kGridCap = 148 * 16;
+
+template <typename WT>
+void lookup_dispatch(const LookupArgs& a, int max_dim, cudaStream_t st) {
+  const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
+  const int d4 = max_dim / 4;
+  if (d4 <= 8) {
+    k_owner_lookup<WT, 8, 1, 8><<<grid_for(n_bags, 32, kGridCap), 256, 0, st>>>(a);
+  } else if (d4 <= 16) {
+    k_owner_lookup<WT, 16, 1, 8><<<grid_for(n_bags, 16, kGridCap), 256, 0, st>>>(a);
+  } else if (d4 <= 32) {
+    k_owner_lookup<WT, 32, 1, 8><<<grid_for(n_bags, 8, kGridCap), 256, 0, st>>>(a);
+  } else if (d4 <= 64) {
+    k_owner_lookup<WT, 32, 2, 4><<<grid_for(n_bags, 8, kGridCap), 256, 0, st>>>(a);
+  } else {
+    k_owner_lookup<WT, 32, 4, 2><<<grid_for(n_bags, 8, kGridCap), 256, 0, st>>>(a);
+  }
+  S2D_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+void launch_init_rows(void* w, int bf16, const FeatDev* feats_host, uint32_t F, uint64_t seed,
+                      cudaStream_t st) {
+  for (uint32_t f = 0; f < F; ++f) {
+    const FeatDev& fd = feats_host[f];
+    if (fd.hi <= fd.lo) continue;
+    const uint64_t work = (uint64_t)(fd.hi - fd.lo) * (fd.dim / 4);
+    const unsigned grid = grid_for(work, 256, 148 * 32);
+    if (bf16)
+      k_init_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(w), fd.wbase, f,
+                                                       fd.lo, fd.hi - fd.lo, fd.dim, seed);
+    else
+      k_init_rows<float><<<grid, 256, 0, st>>>(reinterpret_cast<float*>(w), fd.wbase, f, fd.lo,
+                                               fd.hi - fd.lo, fd.dim, seed);
+    S2D_LAUNCH_CHECK();
+  }
+}
+
+void launch_owner_lookup(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st) {
+  if ((uint64_t)a.n_req * a.B * a.F == 0) return;
+  if (bf16)
+    lookup_dispatch<__nv_bfloat16>(a, max_dim, st);
+  else
+    lookup_dispatch<float>(a, max_dim, st);
+}
+
+void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st) {
+  const uint64_t BF = (uint64_t)a.B * a.F;
+  if (!BF) return;
+  const int d4 = max_dim / 4;
+  if (d4 <= 8)
+    k_combine<8, 1><<<grid_for(BF, 32, kGridCap), 256, 0, st>>>(a);
+  else if (d4 <= 16)
+    k_combine<16, 1><<<grid_for(BF, 16, kGridCap), 256, 0, st>>>(a);
+  else if (d4 <= 32)
+    k_combine<32, 1><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+  else if (d4 <= 64)
+    k_combine<32, 2><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+  else
+    k_combine<32, 4><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+  S2D_LAUNCH_CHECK();
+}
+
+void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st) {
+  const uint64_t BF = (uint64_t)a.B * a.F;
+  if (!BF) return;
+  const int d4 = max_dim / 4;
+  if (d4 <= 8)
+    k_grad_gather<8, 1><<<grid_for(BF, 32, kGridCap), 256, 0, st>>>(a);
+  else if (d4 <= 16)
+    k_grad_gather<16, 1><<<grid_for(BF, 16, kGridCap), 256, 0, st>>>(a);
+  else if (d4 <= 32)
+    k_grad_gather<32, 1><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+  else if (d4 <= 64)
+    k_grad_gather<32, 2><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+  else
+    k_grad_gather<32, 4><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+  S2D_LAUNCH_CHECK();
+}
+
+void launch_bucket_count(const BucketArgs& a, cudaStream_t st) {
+  if (!a.BF) return;
+  k_bucket_count<<<grid_for(a.BF, 256, kGridCap), 256, 0, st>>>(a);
+  S2D_LAUNCH_CHECK();
+}
+
+void launch_bucket_permute(const BucketArgs& a, cudaStream_t st) {
+  if (!a.BF) return;
+  k_bucket_permute<<<grid_for(a.BF, 256, kGridCap), 256, 0, st>>>(a);
+  S2D_LAUNCH_CHECK();
+}
+
+}  // namespace s2d

@@ -1,0 +1,136 @@
+// Device-wide exclusive scans used for bag offsets (lengths -> id offsets)
+// and entry offsets (non-empty bag -> float offset of its partial/gradient
+// row on the wire).  Three phases: per-tile reduce, scan of tile sums (one
+// CTA), per-tile scan.  HBM-bound: reads the input twice, writes once.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "device.cuh"
+
+namespace s2d {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 8;
+constexpr int kTile = kThreads * kItems;
+
+struct OpIdentity {
+  __device__ __forceinline__ uint64_t operator()(uint32_t x, uint64_t) const { return x; }
+};
+
+struct OpHead {  // 1 at the first index of every run of equal valid keys
+  const uint32_t* keys;
+  uint32_t n_slots;
+  __device__ __forceinline__ uint64_t operator()(uint32_t x, uint64_t k) const {
+    return (x < n_slots && (k == 0 || __ldg(keys + k - 1) != x)) ? 1ull : 0ull;
+  }
+};
+
+struct OpNonzeroDim {
+  const FeatDev* feats;
+  uint32_t F;
+  __device__ __forceinline__ uint64_t operator()(uint32_t x, uint64_t k) const {
+    return x ? (uint64_t)__ldg(&feats[k % F].dim) : 0ull;
+  }
+};
+
+template <typename T, typename Op>
+__global__ void __launch_bounds__(kThreads) k_tile_reduce(const uint32_t* __restrict__ in, uint64_t n,
+                                                          Op op, T* __restrict__ tile_sum) {
+  using BlockReduce = cub::BlockReduce<T, kThreads>;
+  __shared__ typename BlockReduce::TempStorage tmp;
+  const uint64_t base = (uint64_t)blockIdx.x * kTile;
+  T acc = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)i * kThreads + threadIdx.x;
+    if (k < n) acc += (T)op(__ldg(in + k), k);
+  }
+  const T s = BlockReduce(tmp).Sum(acc);
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_scan_tiles(T* __restrict__ tile_sum, uint64_t ntiles) {
+  using BlockScan = cub::BlockScan<T, kThreads>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  __shared__ T carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint64_t base = 0; base < ntiles; base += kThreads) {
+    const uint64_t k = base + threadIdx.x;
+    T x = k < ntiles ? tile_sum[k] : 0;
+    T excl, total;
+    BlockScan(tmp).ExclusiveSum(x, excl, total);
+    const T c = carry;
+    if (k < ntiles) tile_sum[k] = c + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c + total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_sum[ntiles] = carry;
+}
+
+template <typename T, typename Op>
+__global__ void __launch_bounds__(kThreads) k_tile_scan(const uint32_t* __restrict__ in, uint64_t n, Op op,
+                                                        const T* __restrict__ tile_sum, uint64_t ntiles,
+                                                        T* __restrict__ out) {
+  using BlockScan = cub::BlockScan<T, kThreads>;
+  __shared__ typename BlockScan::TempStorage tmp;
+  const uint64_t base = (uint64_t)blockIdx.x * kTile;
+  // blocked arrangement: thread t owns items [t*kItems, (t+1)*kItems)
+  T v[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)threadIdx.x * kItems + i;
+    v[i] = k < n ? (T)op(__ldg(in + k), k) : 0;
+  }
+  T excl[kItems];
+  BlockScan(tmp).ExclusiveSum(v, excl);
+  const T off = tile_sum[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)threadIdx.x * kItems + i;
+    if (k < n) out[k] = off + excl[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[n] = tile_sum[ntiles];
+}
+
+template <typename T, typename Op>
+void scan_impl(const uint32_t* in, T* out, uint64_t n, Op op, cudaStream_t st, void* tmp,
+               size_t tmp_bytes) {
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  if ((ntiles + 1) * sizeof(T) > tmp_bytes) throw Error(S2D_ECUDA, "scan workspace too small");
+  T* tile_sum = reinterpret_cast<T*>(tmp);
+  if (ntiles == 0) {
+    S2D_CUDA(cudaMemsetAsync(out, 0, sizeof(T), st));
+    return;
+  }
+  k_tile_reduce<T, Op><<<(unsigned)ntiles, kThreads, 0, st>>>(in, n, op, tile_sum);
+  S2D_LAUNCH_CHECK();
+  k_scan_tiles<T><<<1, kThreads, 0, st>>>(tile_sum, ntiles);
+  S2D_LAUNCH_CHECK();
+  k_tile_scan<T, Op><<<(unsigned)ntiles, kThreads, 0, st>>>(in, n, op, tile_sum, ntiles, out);
+  S2D_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+size_t scan_tmp_bytes(uint64_t n) { return ((n + kTile - 1) / kTile + 1) * sizeof(uint64_t); }
+
+void scan_u32_to_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st, void* tmp,
+                     size_t tmp_bytes) {
+  scan_impl<uint32_t>(in, out, n, OpIdentity{}, st, tmp, tmp_bytes);
+}
+
+void scan_heads_u32(const uint32_t* keys, uint32_t* out, uint64_t n, uint32_t n_slots, cudaStream_t st,
+                    void* tmp, size_t tmp_bytes) {
+  scan_impl<uint32_t>(keys, out, n, OpHead{keys, n_slots}, st, tmp, tmp_bytes);
+}
+
+void scan_nonzero_dim_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint32_t F,
+                          const FeatDev* feats, cudaStream_t st, void* tmp, size_t tmp_bytes) {
+  scan_impl<uint64_t>(in, out, n, OpNonzeroDim{feats, F}, st, tmp, tmp_bytes);
+}
+
+}  // namespace s2d

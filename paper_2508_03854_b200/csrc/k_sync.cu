@@ -1,0 +1,191 @@
+// K5 replica sync (sync_replicas, src/trainer.cpp:547-596):
+//   dirty_compact  ordered list of slots dirty in any replica (after the
+//                  byte-max all-reduce of the dirty flags); identical order
+//                  on every replica so the all-gathered rows line up
+//   pack_rows      (w row, v) of each listed slot -> fp32 wire rows
+//   mean_rows      x = f32((sum_{g ascending} f64(x_g)) * (1/M)) per element
+//                  (deterministic_mean_inplace, src/topology.cpp:150-163),
+//                  weights then moments (moments skipped for SGD); clears
+//                  the dirty flag.
+#include <cub/block/block_reduce.cuh>
+#include <cub/block/block_scan.cuh>
+
+#include "device.cuh"
+
+namespace s2d {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kThreads * kItems;
+
+__global__ void __launch_bounds__(kThreads) k_flag_count(const uint8_t* __restrict__ flags, uint32_t n,
+                                                         uint32_t* __restrict__ tile_sum) {
+  using BR = cub::BlockReduce<uint32_t, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint64_t base = (uint64_t)blockIdx.x * kTile;
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)i * kThreads + threadIdx.x;
+    if (k < n) c += flags[k] != 0;
+  }
+  const uint32_t s = BR(tmp).Sum(c);
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kThreads) k_flag_scan_tiles(uint32_t* __restrict__ tile_sum,
+                                                              uint32_t ntiles, uint32_t* __restrict__ count) {
+  using BS = cub::BlockScan<uint32_t, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < ntiles; base += kThreads) {
+    const uint32_t k = base + threadIdx.x;
+    const uint32_t x = k < ntiles ? tile_sum[k] : 0u;
+    uint32_t ex, tot;
+    BS(tmp).ExclusiveSum(x, ex, tot);
+    const uint32_t c0 = carry;
+    if (k < ntiles) tile_sum[k] = c0 + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = c0 + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *count = carry;
+}
+
+__global__ void __launch_bounds__(kThreads) k_flag_write(const uint8_t* __restrict__ flags, uint32_t n,
+                                                         const uint32_t* __restrict__ tile_sum,
+                                                         uint32_t* __restrict__ list) {
+  using BS = cub::BlockScan<uint32_t, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  const uint64_t base = (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kItems;
+  uint32_t f[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) f[i] = (base + i < n) ? (flags[base + i] != 0) : 0u;
+  uint32_t ex[kItems];
+  BS(tmp).ExclusiveSum(f, ex);
+  const uint32_t off = tile_sum[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i)
+    if (f[i]) list[off + ex[i]] = (uint32_t)(base + i);
+}
+
+template <typename WT>
+__global__ void k_pack_rows(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                            uint32_t n_feat, const uint32_t* __restrict__ list, const uint32_t* count,
+                            const WT* __restrict__ w, const float* __restrict__ moments, uint32_t row_floats,
+                            float* __restrict__ packed) {
+  const uint32_t n = *count;
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += warps) {
+    const uint32_t slot = list[i];
+    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+    const uint32_t dim = feats[f].dim;
+    const WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
+    float* out = packed + (uint64_t)i * row_floats;
+    for (uint32_t c4 = lane; c4 < dim / 4; c4 += 32) {
+      double d[4];
+      Vec4<WT>::load_rw(row + c4 * 4, d);
+      *reinterpret_cast<float4*>(out + c4 * 4) = make_float4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+    }
+    if (lane == 0) out[row_floats - 1] = moments[slot];
+  }
+}
+
+template <typename WT>
+__global__ void k_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                            uint32_t n_feat, const uint32_t* __restrict__ list, const uint32_t* count,
+                            const float* __restrict__ gathered, uint32_t M, uint32_t row_floats,
+                            uint32_t rows_cap, WT* __restrict__ w, float* __restrict__ moments, int sgd,
+                            uint8_t* __restrict__ dirty) {
+  const uint32_t n = *count;
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  const double inv_m = 1.0 / (double)M;
+  const uint64_t rstride = (uint64_t)rows_cap * row_floats;  // replica stride in `gathered`
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += warps) {
+    const uint32_t slot = list[i];
+    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+    const uint32_t dim = feats[f].dim;
+    WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
+    for (uint32_t c4 = lane; c4 < dim / 4; c4 += 32) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (uint32_t g = 0; g < M; ++g) {  // ascending group order
+        const float4 x = *reinterpret_cast<const float4*>(gathered + g * rstride + (uint64_t)i * row_floats + c4 * 4);
+        acc[0] += (double)x.x;
+        acc[1] += (double)x.y;
+        acc[2] += (double)x.z;
+        acc[3] += (double)x.w;
+      }
+      double d[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) d[j] = (double)(float)(acc[j] * inv_m);
+      Vec4<WT>::store(row + c4 * 4, d);
+    }
+    if (lane == 0) {
+      if (!sgd) {
+        double acc = 0.0;
+        for (uint32_t g = 0; g < M; ++g) acc += (double)gathered[g * rstride + (uint64_t)i * row_floats + row_floats - 1];
+        moments[slot] = (float)(acc * inv_m);
+      }
+      dirty[slot] = 0;
+    }
+  }
+}
+
+}  // namespace
+
+void launch_dirty_compact(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, uint32_t* count,
+                          void* tmp, size_t tmp_bytes, cudaStream_t st) {
+  const uint32_t ntiles = (n_slots + kTile - 1) / kTile;
+  if ((size_t)(ntiles + 1) * 4 > tmp_bytes) throw Error(S2D_ECUDA, "compaction workspace too small");
+  if (ntiles == 0) {
+    S2D_CUDA(cudaMemsetAsync(count, 0, 4, st));
+    return;
+  }
+  uint32_t* ts = reinterpret_cast<uint32_t*>(tmp);
+  k_flag_count<<<ntiles, kThreads, 0, st>>>(dirty, n_slots, ts);
+  S2D_LAUNCH_CHECK();
+  k_flag_scan_tiles<<<1, kThreads, 0, st>>>(ts, ntiles, count);
+  S2D_LAUNCH_CHECK();
+  k_flag_write<<<ntiles, kThreads, 0, st>>>(dirty, n_slots, ts, list);
+  S2D_LAUNCH_CHECK();
+}
+
+void launch_pack_rows(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                      uint32_t n_feat_owned, const uint32_t* list, const uint32_t* count, const void* weights,
+                      int bf16, const float* moments, uint32_t row_floats, float* packed, uint32_t max_rows,
+                      cudaStream_t st) {
+  if (!max_rows) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((max_rows + 7) / 8, 148ull * 8);
+  if (bf16)
+    k_pack_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(feats, vbase_sorted, feat_of_vbase, n_feat_owned, list, count,
+                                                     reinterpret_cast<const __nv_bfloat16*>(weights), moments,
+                                                     row_floats, packed);
+  else
+    k_pack_rows<float><<<grid, 256, 0, st>>>(feats, vbase_sorted, feat_of_vbase, n_feat_owned, list, count,
+                                             reinterpret_cast<const float*>(weights), moments, row_floats, packed);
+  S2D_LAUNCH_CHECK();
+}
+
+void launch_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                      uint32_t n_feat_owned, const uint32_t* list, const uint32_t* count, const float* gathered,
+                      uint32_t M, uint32_t row_floats, uint32_t rows_cap, void* weights, int bf16, float* moments,
+                      int sgd, uint8_t* dirty, cudaStream_t st) {
+  if (!rows_cap) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((rows_cap + 7) / 8, 148ull * 8);
+  if (bf16)
+    k_mean_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(feats, vbase_sorted, feat_of_vbase, n_feat_owned, list, count,
+                                                     gathered, M, row_floats, rows_cap,
+                                                     reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd, dirty);
+  else
+    k_mean_rows<float><<<grid, 256, 0, st>>>(feats, vbase_sorted, feat_of_vbase, n_feat_owned, list, count, gathered,
+                                             M, row_floats, rows_cap, reinterpret_cast<float*>(weights), moments, sgd,
+                                             dirty);
+  S2D_LAUNCH_CHECK();
+}
+
+}  // namespace s2d

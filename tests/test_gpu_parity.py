@@ -1,0 +1,254 @@
+"""GPU parity: the sm_100a step (through the C ABI) against the CPU oracle on
+identical seeded inputs.  Bar (BASELINE.json north_star): bucketing, dedup
+and wire layouts bit-exact; pooled outputs, accumulators and weights within
+1e-5 relative for fp32 (1e-2 for bf16).  The fp32 path is bit-exact by
+construction except for gradient segments longer than kChunk (hot rows),
+whose f64 sums are re-associated per chunk -- those cases are checked at
+the stated tolerance and additionally report their bit-equal fraction."""
+import numpy as np
+import pytest
+
+from cases import make_batch, upstream
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _engine(rows, dims, strategy="table-wise", eta=0.1, c=1.0, variant="rowwise-adagrad", dtype="fp32"):
+    import paper_2508_03854_b200 as s2d
+
+    tables = [s2d.TableConfig(int(r), int(d)) for r, d in zip(rows, dims)]
+    return s2d.Sparse2DEmbedding(tables, s2d.Topology(1, 1), rank=0, device=0, strategy=strategy,
+                                 optimizer=s2d.OptimizerConfig(eta=eta, eps=1e-8, c=c, variant=variant),
+                                 weight_dtype=dtype)
+
+
+def _spec(rows, dims, B, eta=0.1, c=1.0, sgd=False):
+    from oracle import MeshSpec, row_wise_plan
+
+    rows = np.array(rows, np.uint32)
+    return MeshSpec(rows=rows, dims=np.array(dims, np.uint32), plan=row_wise_plan(rows, 1), T=1, M=1, B=B,
+                    eta=eta, c=c, sgd=sgd)
+
+
+def _download(eng, spec):
+    ws, vs = [], []
+    for f in range(spec.F):
+        w, v = eng.read_rows(f, 0, int(spec.rows[f]))
+        ws.append(w.ravel())
+        vs.append(v)
+    return np.concatenate(ws), np.concatenate(vs)
+
+
+def _close(a, b, tol=TOL):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return np.all(np.abs(a - b) <= tol * np.maximum(np.abs(b), 1e-30) + 1e-30)
+
+
+def test_init_tables_bit_exact(port):
+    from oracle import MeshState
+
+    rows, dims = [1000, 37, 5], [64, 128, 8]
+    eng = _engine(rows, dims)
+    eng.init_tables(22)
+    spec = _spec(rows, dims, 1)
+    st = MeshState.init(port, spec, 22)
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+    assert np.all(v == 0)
+
+
+def test_adagrad_row_step_known_answers():
+    """test_optimizer.cpp:50-94 and tests/python/test_smoke.py:38-44 through the
+    device row-update kernel."""
+    import paper_2508_03854_b200 as s2d
+
+    out = s2d.adagrad_row_step([1.0, 1.0], 0.0, [2.0, 0.0], eta=0.1, eps=1e-8, c=4.0)
+    assert abs(out["v"] - 4.0) < 1e-6
+    assert abs(out["effective_lr"] - 0.1) < 1e-6
+    assert abs(out["w"][0] - 0.8) < 1e-6 and out["w"][1] == 1.0
+    out = s2d.adagrad_row_step([1.0, 1.0], 0.0, [2.0, 0.0], eta=0.1, eps=1e-8, c=1.0)
+    assert abs(out["effective_lr"] - 0.05) < 1e-6 and abs(out["w"][0] - 0.9) < 1e-6
+    out = s2d.adagrad_row_step([0.25, -0.5], 3.0, [0.0, 0.0], eta=0.1, c=1.0)
+    assert out["v"] == 3.0 and out["w"] == [0.25, -0.5]
+    with pytest.raises(ValueError):
+        s2d.adagrad_row_step([0.0], 0.0, [float("nan")])
+    with pytest.raises(ValueError):
+        s2d.adagrad_row_step([0.0], 0.0, [0.0], eta=0.0)
+
+
+def test_adagrad_rows_bit_exact_vs_reference_formula(port):
+    rng = np.random.default_rng(3)
+    import paper_2508_03854_b200 as s2d
+
+    for dim in (4, 64, 128, 256, 512, 6):
+        w = rng.standard_normal((50, dim)).astype(np.float32)
+        v = rng.random(50).astype(np.float32)
+        g = rng.standard_normal((50, dim)) * 1e-2
+        for c in (1.0, 4.0):
+            got = s2d.adagrad_rows(w, v, g, eta=0.1, eps=1e-8, c=c)
+            for i in range(50):
+                want = port.adagrad_row_step(w[i], v[i], g[i], eta=0.1, eps=1e-8, c=c)
+                assert np.array_equal(bits(got[i]["w"]), bits(want["w"])), (dim, c, i)
+                assert np.float32(got[i]["v"]) == np.float32(want["v"])
+
+
+@pytest.mark.parametrize("c,variant", [(1.0, "rowwise-adagrad"), (4.0, "rowwise-adagrad"), (1.0, "sgd")])
+def test_single_gpu_steps_vs_oracle(port, c, variant):
+    from oracle import MeshState
+
+    rng = np.random.default_rng(11)
+    rows, dims = [100, 1000, 7, 5000], [64, 64, 64, 64]
+    B = 64
+    spec = _spec(rows, dims, B, eta=0.1, c=c, sgd=variant == "sgd")
+    eng = _engine(rows, dims, eta=0.1, c=c, variant=variant)
+    eng.init_tables(5)
+    st = MeshState.init(port, spec, 5)
+    for step in range(4):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=12)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want)), f"pooled step {step}"
+        eng.backward_update(up)
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
+def test_cfg1_shape_bit_exact(port):
+    """BASELINE config 1 shape (8 x 100K x 64, B=512, L=20, Zipf 1.0, 1x1)."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(1)
+    rows, dims, B = [100_000] * 8, [64] * 8, 512
+    spec = _spec(rows, dims, B, eta=0.1, c=1.0)
+    eng = _engine(rows, dims)
+    eng.init_tables(2)
+    st = MeshState.init(port, spec, 2)
+    for step in range(2):
+        lengths, ids = make_batch(rng, spec.rows, B, fixed_len=20, zipf=1.0)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want))
+        eng.backward_update(up)
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
+def test_hot_rows_long_segments(port):
+    """Tiny tables => segments of thousands of contributions (chunked f64
+    reduction).  Within 1e-5 relative; report bit-equal share."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(7)
+    rows, dims, B = [3, 10, 2000], [128, 128, 128], 1024
+    spec = _spec(rows, dims, B, eta=0.1, c=2.0)
+    eng = _engine(rows, dims, eta=0.1, c=2.0)
+    eng.init_tables(9)
+    st = MeshState.init(port, spec, 9)
+    for step in range(3):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=40, zipf=1.2)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want))
+        eng.backward_update(up)
+        assert eng.stats()["long_segments"] > 0
+    w, v = _download(eng, spec)
+    assert _close(v, st.vs[0]) and _close(w, st.ws[0])
+    print("bit-equal w share", float(np.mean(bits(w) == bits(st.ws[0]))))
+
+
+def test_mixed_dims_variable_pooling_empty_bags(port):
+    from oracle import MeshState
+
+    rng = np.random.default_rng(5)
+    rows, dims, B = [3, 50, 1000, 7, 200, 64], [4, 8, 12, 16, 32, 256], 40
+    spec = _spec(rows, dims, B, eta=0.05, c=3.0)
+    eng = _engine(rows, dims, eta=0.05, c=3.0)
+    eng.init_tables(4)
+    st = MeshState.init(port, spec, 4)
+    for step in range(3):
+        lengths, _ = make_batch(rng, spec.rows, B, max_len=30)
+        lengths[::7] = 0  # empty bags pool to zero
+        lengths, ids = _regen(rng, spec.rows, lengths)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want))
+        eng.backward_update(up)
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
+def _regen(rng, rows, lengths):
+    from cases import zipf_ids
+
+    F = len(rows)
+    ids = [zipf_ids(rng, int(rows[b % F]), int(lengths[b])) for b in range(len(lengths))]
+    return lengths, np.concatenate(ids).astype(np.uint32)
+
+
+def test_empty_batch_and_all_empty_bags(port):
+    rows, dims = [10, 20], [8, 8]
+    eng = _engine(rows, dims)
+    eng.init_tables(1)
+    lengths = np.zeros(2 * 3, np.uint32)
+    ids = np.zeros(0, np.uint32)
+    got = eng.forward(lengths, ids)
+    assert got.shape == (3, 16) and np.all(got == 0)
+    eng.backward_update(np.ones((3, 16), np.float32))
+    w0, _ = eng.read_rows(0, 0, 10)
+    eng2 = _engine(rows, dims)
+    eng2.init_tables(1)
+    w1, _ = eng2.read_rows(0, 0, 10)
+    assert np.array_equal(bits(w0), bits(w1))
+
+
+def test_out_of_range_id_raises():
+    eng = _engine([10, 20], [8, 8])
+    eng.init_tables(1)
+    lengths = np.array([1, 1], np.uint32)
+    with pytest.raises(IndexError):
+        eng.forward(lengths, np.array([3, 20], np.uint32))
+
+
+def test_nonfinite_gradient_raises():
+    eng = _engine([10, 20], [8, 8])
+    eng.init_tables(1)
+    eng.forward(np.array([1, 1], np.uint32), np.array([3, 4], np.uint32))
+    up = np.zeros((1, 16), np.float32)
+    up[0, 3] = np.nan
+    with pytest.raises(ValueError):
+        eng.backward_update(up)
+
+
+def test_bf16_weights_within_tolerance(port):
+    """bf16 storage: no reference path (embedding.hpp:16); oracle = fp32
+    reference seeded each step from the GPU's bf16 weights."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(21)
+    rows, dims, B = [500, 40], [128, 64], 128
+    spec = _spec(rows, dims, B, eta=0.1, c=2.0)
+    eng = _engine(rows, dims, eta=0.1, c=2.0, dtype="bf16")
+    eng.init_tables(3)
+    for step in range(3):
+        w, v = _download(eng, spec)
+        st = MeshState(spec, [w.copy()], [v.copy()], [np.zeros(spec.replica_rows(), np.uint8)])
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=10)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want))  # pooling of bf16 rows is exact in f64
+        eng.backward_update(up)
+        w2, v2 = _download(eng, spec)
+        assert _close(v2, st.vs[0], 1e-5)
+        assert _close(w2, st.ws[0], 1e-2)
