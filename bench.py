@@ -1,0 +1,423 @@
+#!/usr/bin/env python3
+"""Benchmark of the 2D-sparse-parallel embedding step (fwd + bwd + fused
+moment-scaled row-wise AdaGrad [+ replica sync]) -- BASELINE.json metric
+"embedding fwd+bwd+update samples/s; HBM GB/s vs peak".
+
+    python bench.py                               # N=1, cfg2, defaults
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N --steps K --warmup W
+    python bench.py --impl reference ...          # reference CPU path (oracle/_ref)
+
+One JSON line on rank 0.  `value` = whole-job samples/s with inputs resident
+in HBM (CUDA events on the engine's stream, max over ranks); `e2e` = the same
+through the public API with pinned HOST buffers (H2D of lengths+ids+upstream
+and D2H of the pooled output inside the timed region).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default=None, help="cfg1..cfg5 (default: cfg2 at N=1, cfg3 at N>1)")
+    p.add_argument("--mesh", default=None, help="NxM (MP ranks per group x DP groups); default N x 1")
+    p.add_argument("--batch", type=int, default=None, help="per-GPU batch override")
+    p.add_argument("--strategy", default=None)
+    p.add_argument("--nbatches", type=int, default=3, help="distinct input batches cycled")
+    p.add_argument("--e2e-steps", type=int, default=None)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    p.add_argument("--seed", type=int, default=1234)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload(args, world):
+    from paper_2508_03854_b200 import workloads
+
+    name = args.config or ("cfg2" if world == 1 else "cfg3")
+    w = workloads.get(name)
+    if args.mesh:
+        n, m = (int(x) for x in args.mesh.lower().split("x"))
+    else:
+        n, m = (world, 1) if world > 1 else (1, 1)
+    if n * m != world:
+        raise SystemExit(f"mesh {n}x{m} needs {n * m} ranks, have {world}")
+    w.mesh = (n, m)
+    if m > 1:
+        w.c = float(m)  # paper default c = M
+    if args.batch:
+        w.batch = args.batch
+    if args.strategy:
+        w.strategy = args.strategy
+    return w
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(w, nnz_own, unique, entries, n_mp, world_bf):
+    """Algorithmic HBM bytes per launch of the dominant kernels."""
+    sw = 2 if w.dtype == "bf16" else 4
+    D = float(np.mean(w.dims))
+    BF = w.batch * w.F
+    lookup = nnz_own * (4 + sw * D + 8) + (world_bf + 1) * 8 + (entries * D * 4 if n_mp > 1 else w.batch * w.sum_dims * 4)
+    update = nnz_own * (4 + 4 * D) + unique * (2 * (sw * D + 4) + 8)
+    sort = nnz_own * 4 + nnz_own * 16 * 4  # histogram read + 4 passes x (8 B read + 8 B write)
+    return {"lookup": lookup, "update": update, "sort": sort}
+
+
+def traffic_from_profiles(kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
+# reference CPU arm: the unmodified reference library (oracle/_ref) on a
+# bounded sample of the same workload
+# ----------------------------------------------------------------------------
+
+def reference_step_sample(w, seed, n_samples, threads, step):
+    """One bounded-sample step of the reference CPU path.  Tables are
+    compacted to the rows the sample touches (each row's arithmetic is
+    independent).  Returns seconds of ref_group_step."""
+    from oracle import MeshSpec, Oracle
+
+    ref = Oracle("reference")
+    n_mp, m = w.mesh
+    lengths_all, ids_all = w.batch_for(seed, step, 0)
+    F = w.F
+    B = min(n_samples, w.batch)
+    lengths = lengths_all[: B * F]
+    ids = ids_all[: int(lengths.sum())]
+    feat = np.repeat(np.tile(np.arange(F), B), lengths)
+    rows = np.zeros(F, np.uint32)
+    cids = np.empty_like(ids)
+    for f in range(F):
+        sel = feat == f
+        u, inv = np.unique(ids[sel], return_inverse=True)
+        rows[f] = max(1, len(u))
+        cids[sel] = inv.astype(np.uint32)
+    dims = np.array(w.dims, np.uint32)
+    plan = np.array([[f, 0, int(rows[f]), 0] for f in range(F)], np.uint32)
+    spec = MeshSpec(rows=rows, dims=dims, plan=plan, T=1, M=1, B=B, eta=w.eta, c=w.c)
+    rng = np.random.default_rng(seed)
+    wt = (rng.standard_normal(spec.replica_floats()) * 0.05).astype(np.float32)
+    vt = np.zeros(spec.replica_rows(), np.float32)
+    up = w.upstream_for(seed, step, 0)[:B]
+    ref.group_step(spec, [lengths], [cids], [up], wt, vt, None, threads=threads)
+    return ref.last_compute_seconds, B
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    w = workload(args, world)
+    from oracle import reference_available
+
+    threads = os.cpu_count() or 1
+    kind = "reference" if reference_available() else "port"
+    if kind != "reference":
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libs2dref.so not built"}))
+        return
+    # calibrate the sample to ~target seconds per step
+    target = max(0.5, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
+    t, b = reference_step_sample(w, args.seed, 256, threads, 0)
+    n = int(max(64, min(w.batch, 256 * target / max(t, 1e-3))))
+    for k in range(args.warmup):
+        reference_step_sample(w, args.seed, n, threads, k)
+    tot_t, tot_s = 0.0, 0
+    for k in range(args.steps):
+        t, b = reference_step_sample(w, args.seed, n, threads, args.warmup + k)
+        tot_t += t
+        tot_s += b
+    sps = tot_s / tot_t
+    line = {
+        "impl": "reference", "metric": "embedding fwd+bwd+update samples/s", "value": sps,
+        "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32 storage / f64 accumulation", "data": "synthetic",
+        "config": {"workload": w.name + ": " + w.describe, "mesh": "1x1 (reference group step)",
+                   "global_batch": n, "sample": f"{n} samples/step, tables compacted to touched rows"},
+        "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": threads, "kind": kind,
+                         "sample": f"{n} of {w.batch} samples per step, touched-row tables"},
+        "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_03854_b200 as s2d
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args, world)
+    n_mp, m = w.mesh
+    topo = s2d.Topology(world, m)
+    nid = None
+    if world > 1:
+        obj = [s2d.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    tables = [s2d.TableConfig(int(r), int(d), float(w.batch * w.mean_len())) for r, d in zip(w.rows, w.dims)]
+    eng = s2d.Sparse2DEmbedding(tables, topo, rank=rank, device=local, strategy=w.strategy,
+                                optimizer=s2d.OptimizerConfig(eta=w.eta, eps=1e-8, c=w.c),
+                                weight_dtype=w.dtype, nccl_id=nid, strict=False)
+    stream = torch.cuda.current_stream()
+    eng.set_stream(stream.cuda_stream)
+    eng.init_tables(args.seed)
+    # inputs: NB distinct batches, resident in HBM for `value`
+    NB = max(1, args.nbatches)
+    host = []
+    for k in range(NB):
+        lengths, ids = w.batch_for(args.seed, k, rank)
+        up = w.upstream_for(args.seed, k, rank)
+        host.append((lengths, ids, up))
+    dev = [(torch.from_numpy(l.view(np.int32)).cuda(), torch.from_numpy(i.view(np.int32)).cuda(),
+            torch.from_numpy(u).cuda()) for l, i, u in host]
+    pooled = torch.empty((w.batch, w.sum_dims), dtype=torch.float32, device="cuda")
+    nnz_mean = float(np.mean([len(h[1]) for h in host]))
+
+    def step(k):
+        l, i, u = dev[k % NB]
+        eng.forward(l, i, pooled, batch=w.batch)
+        eng.backward_update(u)
+        if m > 1:
+            eng.sync_replicas()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for k in range(args.warmup):
+        step(k)
+    eng.synchronize()
+    torch.cuda.synchronize()
+    eng.phase_times()  # reset
+    eng.set_profiling(True)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = s2d.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for k in range(args.steps):
+            step(args.warmup + k)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = s2d.launch_count() - launches0
+    eng.synchronize()
+    eng.set_profiling(False)
+    phases = eng.phase_times()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ms_step = ms_max / args.steps
+    value = world * w.batch * args.steps / (ms_max / 1e3)
+    st = eng.stats()
+
+    # ---- e2e through the public API with pinned host buffers ----
+    K2 = args.e2e_steps or max(3, min(args.steps, 10))
+    pin = [(torch.from_numpy(l.view(np.int32)).pin_memory(), torch.from_numpy(i.view(np.int32)).pin_memory(),
+            torch.from_numpy(u).pin_memory()) for l, i, u in host]
+    pooled_h = torch.empty((w.batch, w.sum_dims), dtype=torch.float32).pin_memory()
+
+    def step_host(k):
+        l, i, u = pin[k % NB]
+        eng.forward(l, i, pooled_h, batch=w.batch)
+        eng.backward_update(u)
+        if m > 1:
+            eng.sync_replicas()
+
+    step_host(0)
+    eng.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(K2):
+        step_host(k)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    eng.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e = world * w.batch * K2 / (float(te.item()) / 1e3)
+    h2d = int(sum(x.numel() * 4 for x in pin[0]) / 1)
+    d2h = int(pooled_h.numel() * 4)
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = load_peaks()
+    ab = algorithmic_bytes(w, st["nnz_owned"] or nnz_mean, st["unique_rows"] or 0, st["entries_owned"], n_mp,
+                           w.batch * w.F * (n_mp if n_mp > 1 else 1))
+    per_phase = {}
+    for ph, (pms, cnt) in phases.items():
+        if cnt:
+            per_phase[ph] = {"ms_per_launch": pms / cnt, "share": pms / max(ms, 1e-9)}
+    dom = max(("lookup", "update", "sort"), key=lambda p: phases[p][0])
+    dom_ms = phases[dom][0] / max(1, phases[dom][1])
+    achieved = ab[dom] / (dom_ms / 1e3) / 1e9
+    for p in ("lookup", "update", "sort"):
+        if p in per_phase:
+            per_phase[p]["algo_gbs"] = ab[p] / (per_phase[p]["ms_per_launch"] / 1e3) / 1e9
+    kname = {"lookup": "k_owner_lookup", "update": "k_update", "sort": "k_radix_pass"}[dom]
+    line = {
+        "metric": "embedding fwd+bwd+update samples/s", "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": ("bf16 weights" if w.dtype == "bf16" else "f32") + " storage, f64 accumulation",
+        "data": "synthetic (seeded Zipf ids, power-law bag lengths, N(0,1e-3) upstream)",
+        "config": {"workload": w.name + ": " + w.describe, "global_batch": world * w.batch,
+                   "per_gpu_batch": w.batch, "tables": w.F, "dim": int(np.max(w.dims)),
+                   "mesh": f"{n_mp}x{m}", "strategy": w.strategy, "optimizer": f"rowwise-adagrad c={w.c}",
+                   "parallelism": f"mp{n_mp}xdp{m}", "nnz_per_gpu": nnz_mean,
+                   "l2": "inputs larger than L2 (tables 17.2 GB, upstream 218 MB/step), "
+                         f"{NB} distinct batches cycled"},
+        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "traffic": traffic_from_profiles(kname)},
+        "phases": per_phase,
+        "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "step_stats": {k: st[k] for k in ("nnz_owned", "unique_rows", "long_segments", "a2a_bytes_sent",
+                                          "sync_bytes")},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args)
+    if rank == 0:
+        print(json.dumps(line))
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_baseline(w, args):
+    from oracle import reference_available
+
+    threads = os.cpu_count() or 1
+    if not reference_available():
+        return None
+    t, b = reference_step_sample(w, args.seed, 256, threads, 0)
+    n = int(max(64, min(w.batch, 256 * 4.0 / max(t, 1e-3))))
+    tot_t, tot_s, k = 0.0, 0, 0
+    while tot_t < args.cpu_seconds and k < 20:
+        t, b = reference_step_sample(w, args.seed, n, threads, k)
+        tot_t += t
+        tot_s += b
+        k += 1
+    return {"value": tot_s / tot_t, "unit": "samples/s", "cores": threads, "kind": "reference",
+            "sample": f"{k} steps x {n} of {w.batch} samples, tables compacted to touched rows"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

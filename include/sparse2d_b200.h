@@ -211,6 +211,18 @@ int s2d_synchronize(s2d_ctx* ctx);
 
 int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out);
 
+/* Per-phase device time (CUDA events on the context's stream), summed since
+ * the last query.  Phases: 0 input staging, 1 K1 bucketing, 2 id all-to-all,
+ * 3 K2 lookup, 4 pooled all-to-all, 5 combine, 6 grad gather, 7 grad
+ * all-to-all, 8 radix sort, 9 segmentation, 10 fused update, 11 replica sync.
+ * n must be >= 12.  Profiling is off by default. */
+#define S2D_NUM_PHASES 12
+int s2d_ctx_set_profiling(s2d_ctx* ctx, int on);
+int s2d_get_phase_times(s2d_ctx* ctx, double* ms, uint32_t* counts, uint32_t n);
+
+/* Number of kernels this library has launched in the process. */
+uint64_t s2d_launch_count(void);
+
 /* K4 on caller rows (the binding behind Python adagrad_row_step,
  * bindings/module.cpp:93-107): n_rows rows of `dim`, w fp32 [n][dim],
  * v fp32 [n], g f64 [n][dim], host buffers; lr_out[n] receives the effective

@@ -159,7 +159,8 @@ class Oracle:
             L.ref_group_step.argtypes = [
                 C.c_uint32, C.c_uint32, C.c_uint32, _u32p, _u32p, C.c_uint32, _u32p,
                 C.c_double, C.c_double, C.c_double, C.c_int,
-                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _f32p, _f32p, C.c_void_p, C.c_uint32]
+                C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, _f32p, _f32p, C.c_void_p, C.c_uint32,
+                C.POINTER(C.c_double)]
             L.ref_group_step.restype = C.c_int
             L.ref_last_error.restype = C.c_char_p
             L.ref_gen_batch_ids.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -257,6 +258,7 @@ class Oracle:
     # ---- one MP group / the full mesh ---------------------------------------
     def group_step(self, spec: MeshSpec, lengths, ids, upstream, w, v, dirty=None,
                    want_dump=False, threads=1):
+        self.last_compute_seconds = None
         """lengths/ids/upstream: per local rank of the group.  Returns
         (pooled per rank, Dump|None).  w, v, dirty are updated in place."""
         N, B, F = spec.N, spec.B, spec.F
@@ -318,10 +320,12 @@ class Oracle:
                     mask=dd["mask"].reshape(N, B * F),
                     part=part, grad=grad)
         else:
+            secs = C.c_double(0.0)
             rc = self.lib.ref_group_step(
                 F, N, B, rows, dims, len(plan), plan, spec.eta, spec.eps, spec.c, int(spec.sgd),
                 _ptr_array(lengths), _ptr_array(ids), _ptr_array(upstream), _ptr_array(pooled),
-                w, v, C.c_void_p(_ptr(dirty) if dirty is not None else None), threads)
+                w, v, C.c_void_p(_ptr(dirty) if dirty is not None else None), threads, C.byref(secs))
+            self.last_compute_seconds = secs.value
         if rc == -2:
             raise IndexError("lookup id outside shard ranges")
         if rc == -3:

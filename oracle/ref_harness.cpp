@@ -12,6 +12,7 @@
 // DataGenerator.  The survey verified this composition reproduces
 // Trainer::replica_tables bitwise.
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <functional>
@@ -174,7 +175,7 @@ int ref_group_step(uint32_t F, uint32_t N, uint32_t B, const uint32_t* rows, con
                    uint32_t n_entries, const uint32_t* plan, double eta, double eps, double c,
                    int sgd, const uint32_t* const* lengths, const uint32_t* const* ids,
                    const float* const* upstream, float* const* pooled, float* w, float* v,
-                   uint8_t* dirty, uint32_t threads) {
+                   uint8_t* dirty, uint32_t threads, double* compute_seconds) {
   try {
     const uint32_t BF = B * F;
     OptimizerConfig opt{eta, eps, c, sgd ? OptimizerVariant::Sgd : OptimizerVariant::RowWiseAdagrad};
@@ -195,6 +196,8 @@ int ref_group_step(uint32_t F, uint32_t N, uint32_t B, const uint32_t* rows, con
       tables[f].weights.assign(w + woff[f], w + woff[f + 1]);
       tables[f].moments.assign(v + voff[f], v + voff[f + 1]);
     });
+    // timed region: everything between wrapping the replica and unwrapping it
+    const auto t_begin = std::chrono::steady_clock::now();
     // Shard ranges per (table, owner) from the plan.
     std::vector<std::vector<std::pair<uint32_t, uint32_t>>> range(F, std::vector<std::pair<uint32_t, uint32_t>>(N, {0, 0}));
     for (uint32_t e = 0; e < n_entries; ++e) range[plan[4 * e]][plan[4 * e + 3]] = {plan[4 * e + 1], plan[4 * e + 2]};
@@ -327,6 +330,8 @@ int ref_group_step(uint32_t F, uint32_t N, uint32_t B, const uint32_t* rows, con
         if (dirty) dirty[voff[f] + rg.row] = 1;
       }
     });
+    if (compute_seconds)
+      *compute_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_begin).count();
     par_for(F, threads, [&](uint32_t f) {
       std::memcpy(w + woff[f], tables[f].weights.data(), sizeof(float) * (woff[f + 1] - woff[f]));
       std::memcpy(v + voff[f], tables[f].moments.data(), sizeof(float) * (voff[f + 1] - voff[f]));

@@ -16,6 +16,7 @@ from .api import (  # noqa: F401
     adagrad_rows,
     effective_lr,
     imbalance_ratio,
+    launch_count,
     nccl_unique_id,
     owner_of,
     plan_greedy,
@@ -31,6 +32,7 @@ __all__ = [
     "adagrad_rows",
     "effective_lr",
     "imbalance_ratio",
+    "launch_count",
     "nccl_unique_id",
     "owner_of",
     "plan_greedy",

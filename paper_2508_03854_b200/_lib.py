@@ -82,6 +82,9 @@ SIGNATURES = {
     "s2d_synchronize": (C.c_int, [_P]),
     "s2d_get_step_stats": (C.c_int, [_P, C.POINTER(StepStats)]),
     "s2d_adagrad_rows": (C.c_int, [C.POINTER(OptimizerConfigC), C.c_uint32, C.c_uint32, _P, _P, _P, _P]),
+    "s2d_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "s2d_get_phase_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.c_uint32]),
+    "s2d_launch_count": (C.c_uint64, []),
     "s2d_debug_read": (C.c_int, [_P, C.c_int32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
 }
 
@@ -94,9 +97,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH) or _build._stale(LIB_PATH, _build.sources() + _build._headers()):
+    if not _build.up_to_date():
         if not build_if_missing:
-            raise ImportError(f"{LIB_PATH} missing; run python -m paper_2508_03854_b200.build")
+            raise ImportError(f"{LIB_PATH} missing or stale; run python -m paper_2508_03854_b200.build")
         _build.build()
     lib = C.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():

@@ -163,6 +163,11 @@ class TableConfig:
     expected_lookups: float = 1.0  # expected lookups per batch (planner load)
 
 
+def launch_count() -> int:
+    """Kernels launched by libsparse2d_b200 in this process."""
+    return int(_lib().s2d_launch_count())
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     L.check(_lib().s2d_nccl_unique_id(buf))
@@ -330,6 +335,20 @@ class Sparse2DEmbedding:
         s = L.StepStats()
         L.check(self.lib.s2d_get_step_stats(self._ctx, C.byref(s)))
         return {k: getattr(s, k) for k, _ in L.StepStats._fields_}
+
+    PHASES = ("input", "bucket", "a2a_ids", "lookup", "a2a_lookup", "combine", "grad_gather", "a2a_grad",
+              "sort", "segments", "update", "sync")
+
+    def set_profiling(self, on: bool):
+        L.check(self.lib.s2d_ctx_set_profiling(self._ctx, 1 if on else 0))
+
+    def phase_times(self) -> dict:
+        """{phase: (ms, launches)} summed since the last call (CUDA events on
+        the engine's stream)."""
+        ms = (C.c_double * 12)()
+        cnt = (C.c_uint32 * 12)()
+        L.check(self.lib.s2d_get_phase_times(self._ctx, ms, cnt, 12))
+        return {p: (ms[i], cnt[i]) for i, p in enumerate(self.PHASES)}
 
     def debug(self, which: int) -> np.ndarray:
         """Wire buffers of the last step (see s2d_debug_read)."""

@@ -11,7 +11,9 @@ torch-bundled nvidia-nccl wheel (the same libnccl.so.2 torch loads).
 from __future__ import annotations
 
 import concurrent.futures as cf
+import fcntl
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -59,9 +61,9 @@ def _headers() -> list[str]:
         os.path.join(INCLUDE, "sparse2d_b200.h")]
 
 
-def _compile(src: str, flags: list[str]) -> tuple[str, str]:
+def _compile(src: str, flags: list[str], incremental: bool) -> tuple[str, str]:
     obj = os.path.join(OBJ, os.path.basename(src) + ".o")
-    if not _stale(obj, [src] + _headers()):
+    if incremental and not _stale(obj, [src] + _headers()):
         return obj, ""
     cmd = [NVCC, "-c", src, "-o", obj, *flags]
     if src.endswith(".cpp"):
@@ -72,17 +74,48 @@ def _compile(src: str, flags: list[str]) -> tuple[str, str]:
     return obj, r.stderr
 
 
+STAMP = LIB + ".stamp"
+
+
+def source_hash() -> str:
+    h = hashlib.sha256()
+    for p in sorted(sources() + _headers()):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(ARCH).encode())
+    return h.hexdigest()
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+        return False
+    with open(STAMP) as f:
+        return f.read().strip() == source_hash()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Build unless the stamp (sha256 of sources + headers) matches.  A file
+    lock serialises concurrent builders (e.g. torchrun ranks)."""
     os.makedirs(OBJ, exist_ok=True)
+    with open(os.path.join(OBJ, ".lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        try:
+            if not force and up_to_date():
+                return LIB
+            return _build_locked(force, verbose)
+        finally:
+            fcntl.flock(lk, fcntl.LOCK_UN)
+
+
+def _build_locked(force: bool, verbose: bool) -> str:
     srcs = sources()
-    if not force and not _stale(LIB, srcs + _headers()):
-        return LIB
     flags = _flags()
-    if force:
-        for o in glob.glob(os.path.join(OBJ, "*.o")):
-            os.remove(o)
+    # object files are reused only when the previous library is present
+    # (a fresh checkout / GPU-box snapshot recompiles everything)
+    incremental = not force and os.path.exists(LIB)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
-        results = list(ex.map(lambda s: _compile(s, flags), srcs))
+        results = list(ex.map(lambda s: _compile(s, flags, incremental), srcs))
     log = "\n".join(r[1] for r in results if r[1])
     with open(os.path.join(OBJ, "ptxas.log"), "w") as f:
         f.write(log)
@@ -96,6 +129,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(LIB + ".tmp", LIB)
+    with open(STAMP, "w") as f:
+        f.write(source_hash())
     return LIB
 
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -12,6 +13,11 @@
 #include "ctx.h"
 
 using s2d::Error;
+
+namespace s2d {
+static std::atomic<uint64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace s2d
 
 namespace {
 
@@ -180,6 +186,23 @@ int s2d_replica_sync(s2d_ctx* ctx) {
   return guarded([&] { as_ctx(ctx)->replica_sync(); });
 }
 
+int s2d_ctx_set_profiling(s2d_ctx* ctx, int on) {
+  return guarded([&] {
+    auto* c = as_ctx(ctx);
+    c->phase_end();
+    c->profile = on != 0;
+  });
+}
+
+int s2d_get_phase_times(s2d_ctx* ctx, double* ms, uint32_t* counts, uint32_t n) {
+  return guarded([&] {
+    if (n < (uint32_t)s2d::kNumPhases) throw Error(S2D_EINVAL, "need room for every phase");
+    as_ctx(ctx)->phase_times(ms, counts);
+  });
+}
+
+uint64_t s2d_launch_count(void) { return s2d::g_launches.load(); }
+
 int s2d_synchronize(s2d_ctx* ctx) {
   return guarded([&] { as_ctx(ctx)->synchronize_and_check(); });
 }
@@ -187,7 +210,9 @@ int s2d_synchronize(s2d_ctx* ctx) {
 int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out) {
   return guarded([&] {
     if (!out) throw Error(S2D_EINVAL, "null output");
-    *out = as_ctx(ctx)->stats;
+    auto* c = as_ctx(ctx);
+    c->refresh_stats();
+    *out = c->stats;
   });
 }
 

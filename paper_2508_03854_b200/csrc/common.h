@@ -28,7 +28,14 @@ struct Error : std::runtime_error {
       throw ::s2d::Error(S2D_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-#define S2D_LAUNCH_CHECK() S2D_CUDA(cudaGetLastError())
+// Every kernel launch is followed by S2D_LAUNCH_CHECK, which also counts it
+// (s2d_launch_count: the bench's gpu_launches evidence).
+void count_launch();
+#define S2D_LAUNCH_CHECK()            \
+  do {                                \
+    ::s2d::count_launch();            \
+    S2D_CUDA(cudaGetLastError());     \
+  } while (0)
 
 // Device fault bits (checked once per step, SURVEY.md 5 failure detection).
 enum : uint32_t { kErrIdRange = 1u, kErrNonfinite = 2u };

@@ -55,6 +55,43 @@ HostBuf::~HostBuf() {
   if (p) cudaFreeHost(p);
 }
 
+void Ctx::phase_begin(int ph) {
+  if (!profile) return;
+  if (open_phase >= 0) phase_end();
+  while (ev_pool.size() < ev_used + 2) {
+    cudaEvent_t e;
+    S2D_CUDA(cudaEventCreate(&e));
+    ev_pool.push_back(e);
+  }
+  S2D_CUDA(cudaEventRecord(ev_pool[ev_used], stream));
+  ev_marks.push_back({ph, ev_used});
+  ev_used += 2;
+  open_phase = ph;
+}
+
+void Ctx::phase_end() {
+  if (!profile || open_phase < 0) return;
+  S2D_CUDA(cudaEventRecord(ev_pool[ev_marks.back().second + 1], stream));
+  open_phase = -1;
+}
+
+void Ctx::phase_times(double* ms, uint32_t* counts) {
+  for (int i = 0; i < kNumPhases; ++i) {
+    ms[i] = 0.0;
+    if (counts) counts[i] = 0;
+  }
+  phase_end();
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  for (const auto& m : ev_marks) {
+    float t = 0.f;
+    S2D_CUDA(cudaEventElapsedTime(&t, ev_pool[m.second], ev_pool[m.second + 1]));
+    ms[m.first] += t;
+    if (counts) counts[m.first] += 1;
+  }
+  ev_marks.clear();
+  ev_used = 0;
+}
+
 namespace {
 
 __global__ void k_gather_bounds(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF,
@@ -79,6 +116,7 @@ int bit_width(uint32_t x) {
 
 Ctx::~Ctx() {
   if (device >= 0) cudaSetDevice(device);
+  for (auto e : ev_pool) cudaEventDestroy(e);
   if (dp) ncclCommDestroy(dp);
   if (mp) ncclCommDestroy(mp);
   if (world) ncclCommDestroy(world);
@@ -308,8 +346,10 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   nnz_local = nnz;
   const uint64_t BF = (uint64_t)B * F;
   stats = s2d_step_stats{};
+  stats_counters_valid = false;
   stats.nnz_local = nnz;
   // stage inputs
+  phase_begin(kPhInput);
   const uint32_t* d_len = lengths;
   const uint32_t* d_ids = ids;
   float* d_pooled = pooled;
@@ -329,6 +369,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   const FeatDev* dfe = d_feats.as<FeatDev>();
 
   if (N == 1) {
+    phase_begin(kPhLookup);
     nnz_own = nnz;
     keys_a.ensure(std::max<uint64_t>(nnz, 1) * 4);
     vals_a.ensure(std::max<uint64_t>(nnz, 1) * 4);
@@ -351,8 +392,10 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.emit_keys = 1;
     launch_owner_lookup(a, bf16, (int)max_dim, stream);
     stats.nnz_owned = nnz;
+    stats.entries_owned = BF;
   } else {
     // K1: bucket by owner
+    phase_begin(kPhBucket);
     cnt.ensure((uint64_t)N * BF * 4);
     send_off.ensure(((uint64_t)N * BF + 1) * 4);
     eoff_req.ensure(((uint64_t)N * BF + 1) * 8);
@@ -375,6 +418,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     scan_nonzero_dim_u64(cnt.as<uint32_t>(), eoff_req.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream, scan_tmp.p,
                          scan_tmp.cap);
     launch_bucket_permute(ba, stream);
+    phase_begin(kPhA2AIds);
     a2a_counts();
     // ids + lengths all-to-all inside the MP group
     recv_lengths.ensure((uint64_t)N * BF * 4);
@@ -395,6 +439,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
       S2D_CUDA(cudaMemcpyAsync(recv_ids.as<uint32_t>() + nnz_base_from[local], send_ids.as<uint32_t>() + ids_base_to[local],
                                nnz_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
     // owner side: offsets of the received demand, entry offsets of partials
+    phase_begin(kPhLookup);
     own_idoff.ensure(((uint64_t)N * BF + 1) * 4);
     own_eoff.ensure(((uint64_t)N * BF + 1) * 8);
     scan_u32_to_u32(recv_lengths.as<uint32_t>(), own_idoff.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p,
@@ -429,6 +474,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.emit_keys = 1;
     launch_owner_lookup(a, bf16, (int)max_dim, stream);
     // C1: partials back to requesters
+    phase_begin(kPhA2ALookup);
     S2D_NCCL(ncclGroupStart());
     for (uint32_t p = 0; p < N; ++p) {
       if (p == local) continue;
@@ -439,6 +485,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     if (ef_to[local])
       S2D_CUDA(cudaMemcpyAsync(part_recv.as<float>() + ef_base_to[local], part_send.as<float>() + ef_base_from[local],
                                ef_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
+    phase_begin(kPhCombine);
     CombineArgs ca{};
     ca.feats = dfe;
     ca.F = F;
@@ -451,6 +498,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     ca.pooled = d_pooled;
     launch_combine(ca, (int)max_dim, stream);
     stats.nnz_owned = nnz_own;
+    stats.entries_owned = ef_own / std::max<uint32_t>(1, max_dim);
     uint64_t sent = 0, recv = 0;
     for (uint32_t p = 0; p < N; ++p) {
       if (p == local) continue;
@@ -461,9 +509,12 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     stats.a2a_bytes_recv = recv;
   }
   if (mem == S2D_HOST) {
+    phase_begin(kPhCombine);
     S2D_CUDA(cudaMemcpyAsync(pooled, d_pooled, (uint64_t)B * sum_dims * 4, cudaMemcpyDeviceToHost, stream));
+    phase_end();
     S2D_CUDA(cudaStreamSynchronize(stream));
   }
+  phase_end();
   fwd_done = true;
   finish_call();
 }
@@ -538,6 +589,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
   S2D_CUDA(cudaSetDevice(device));
   const uint64_t BF = (uint64_t)B * F;
   const float* d_up = upstream;
+  phase_begin(kPhInput);
   if (mem == S2D_HOST) {
     upstream_stage.ensure((uint64_t)B * sum_dims * 4);
     S2D_CUDA(cudaMemcpyAsync(upstream_stage.p, upstream, (uint64_t)B * sum_dims * 4, cudaMemcpyHostToDevice, stream));
@@ -552,6 +604,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     }
     grad_send.ensure(std::max<uint64_t>(ef_req, 4) * 4);
     grad_recv.ensure(std::max<uint64_t>(ef_own, 4) * 4);
+    phase_begin(kPhGradGather);
     GradGatherArgs ga{};
     ga.feats = d_feats.as<FeatDev>();
     ga.F = F;
@@ -563,6 +616,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ga.upstream = d_up;
     ga.send = grad_send.as<float>();
     launch_grad_gather(ga, (int)max_dim, stream);
+    phase_begin(kPhA2AGrad);
     // C2: gradients to owners; the owner's receive layout equals its
     // partial send layout, so the lookup's (slot, val) pairs index it.
     S2D_NCCL(ncclGroupStart());
@@ -590,6 +644,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
   const uint64_t n = nnz_own;
   uint64_t uniq = 0;
   if (n > 0) {
+    phase_begin(kPhSort);
     keys_b.ensure(n * 4);
     vals_b.ensure(n * 4);
     const int bits = std::max(1, bit_width(n_slots));
@@ -605,6 +660,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     chunk_seg.ensure((n / kChunk + 2) * 4);
     chunk_part.ensure((n / kChunk + 2) * (uint64_t)max_dim * 8);
     scan_tmp.ensure(scan_tmp_bytes(n + 1));
+    phase_begin(kPhSegments);
     SegmentArgs sa{};
     sa.keys = sk;
     sa.n = n;
@@ -617,6 +673,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     sa.tmp = scan_tmp.p;
     sa.tmp_bytes = scan_tmp.cap;
     run_segments(sa, stream);
+    phase_begin(kPhUpdate);
     UpdateArgs ua{};
     ua.feats = d_feats.as<FeatDev>();
     ua.vbase_sorted = d_vbase_sorted.as<uint32_t>();
@@ -643,14 +700,20 @@ void Ctx::backward_update(const float* upstream, int mem) {
     uniq = 1;
   }
   (void)uniq;
+  phase_end();
   fwd_done = false;
+  stats_counters_valid = n > 0;
   finish_call();
-  if (strict && n > 0) {
-    uint32_t c[4];
-    S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
-    stats.unique_rows = c[0];
-    stats.long_segments = c[2];
-  }
+}
+
+void Ctx::refresh_stats() {
+  if (!stats_counters_valid) return;
+  S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  uint32_t c[4];
+  S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
+  stats.unique_rows = c[0];
+  stats.long_segments = c[2];
 }
 
 // ---- K5 replica sync ---------------------------------------------------------
@@ -658,6 +721,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
 void Ctx::replica_sync() {
   if (M <= 1 || !F) return;
   S2D_CUDA(cudaSetDevice(device));
+  phase_begin(kPhSync);
   // union of dirty rows across the DP group
   S2D_NCCL(ncclAllReduce(dirty.p, dirty.p, n_slots, ncclUint8, ncclMax, dp, stream));
   sync_list.ensure((uint64_t)std::max<uint32_t>(n_slots, 1) * 4);
@@ -684,6 +748,7 @@ void Ctx::replica_sync() {
                      opt.variant == S2D_SGD, dirty.as<uint8_t>(), stream);
     stats.sync_bytes = (uint64_t)count * row_floats * 4 * (M - 1);
   }
+  phase_end();
   finish_call();
 }
 

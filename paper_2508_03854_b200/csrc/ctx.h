@@ -35,6 +35,23 @@ struct HostBuf {  // pinned
   }
 };
 
+// Phases timed with CUDA events when profiling is on (s2d_get_phase_times).
+enum Phase : int {
+  kPhInput = 0,   // H2D staging + bag offsets
+  kPhBucket,      // K1 count / scans / permute
+  kPhA2AIds,      // counts + lengths + ids all-to-all
+  kPhLookup,      // K2 owner lookup
+  kPhA2ALookup,   // C1 pooled partials all-to-all
+  kPhCombine,     // requester combine (+ D2H in host mode)
+  kPhGradGather,  // C2 send layout
+  kPhA2AGrad,     // C2 all-to-all
+  kPhSort,        // K3a radix sort
+  kPhSegments,    // run-length segmentation
+  kPhUpdate,      // K3b chunk sums + K4 fused update
+  kPhSync,        // K5 replica sync
+  kNumPhases
+};
+
 struct Ctx {
   // mesh (topology.hpp:13-26): rank -> (group = r / N, local = r % N)
   int device = 0;
@@ -79,6 +96,18 @@ struct Ctx {
       nnz_base_from;
   bool sorted_in_b = false;
   s2d_step_stats stats{};
+  bool stats_counters_valid = false;
+  void refresh_stats();
+
+  // profiling
+  bool profile = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<std::pair<int, size_t>> ev_marks;  // (phase, index of start event)
+  int open_phase = -1;
+  void phase_begin(int ph);
+  void phase_end();
+  void phase_times(double* ms, uint32_t* counts);
 
   ~Ctx();
   void create(int device, uint32_t T, uint32_t M, uint32_t rank, const uint8_t* nccl_id);
