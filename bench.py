@@ -260,7 +260,9 @@ def run_ours(args):
     eng = s2d.Sparse2DEmbedding(tables, topo, rank=rank, device=local, strategy=w.strategy,
                                 optimizer=s2d.OptimizerConfig(eta=w.eta, eps=1e-8, c=w.c),
                                 weight_dtype=w.dtype, nccl_id=nid, strict=False)
-    stream = torch.cuda.current_stream()
+    # a real (non-NULL) stream shared by the engine and the timing events
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     eng.set_stream(stream.cuda_stream)
     eng.init_tables(args.seed)
     # inputs: NB distinct batches, resident in HBM for `value`
