@@ -59,7 +59,6 @@ struct RangeDev {
 
 constexpr int kMaxDim = 512;       // trainer.cpp:99
 constexpr int kMaxRanksPerGroup = 32;  // owner bitmask width (trainer.cpp:193-195)
-constexpr uint32_t kChunk = 128;   // contributions per chunk of a long gradient segment
 
 // ---- launch wrappers (all asynchronous on `st`) --------------------------
 
@@ -103,8 +102,8 @@ struct LookupArgs {
   uint32_t* err;
   int direct;                  // N == 1: write pooled rows (zero for empty bags)
   int emit_keys;
+  uint32_t uni_d4;             // dim/4 shared by every table (0: mixed dims)
 };
-void launch_owner_lookup(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
 
 struct CombineArgs {
   const FeatDev* feats;
@@ -142,42 +141,33 @@ void launch_bucket_count(const BucketArgs& a, cudaStream_t st);
 void launch_bucket_permute(const BucketArgs& a, cudaStream_t st);
 
 // update kernels (k_update.cu)
-struct SegmentArgs {
-  const uint32_t* keys;        // sorted slots
+// streaming kernels (k_stream.cu): K2 lookup and K3b+K4 segment-reduce +
+// fused update over the sorted pairs
+struct StreamUpdateArgs {
+  const uint32_t* keys;          // sorted slots (invalid = 0xffffffff, sorted last)
+  const uint32_t* vals;          // gradient row offsets (float4 units), arrival order per slot
   uint64_t n;
-  uint32_t n_slots;            // keys >= n_slots are invalid (sorted last)
-  uint32_t* uslot;             // [n+1] unique slots
-  uint32_t* useg;              // [n+2] segment starts; useg[U] = end of valid keys
-  uint32_t* counters;          // [0]=U [1]=total chunks [2]=long segments
-  uint32_t* chunk_base;        // [n+1]
-  uint32_t* chunk_seg;         // [n/kChunk+1]
-  void* tmp;
-  size_t tmp_bytes;
-};
-void run_segments(const SegmentArgs& a, cudaStream_t st);
-
-struct UpdateArgs {
+  uint32_t n_slots;
   const FeatDev* feats;
-  const uint32_t* vbase_sorted;  // [F+1] slot bases ascending (feature of a slot)
-  const uint32_t* feat_of_vbase; // [F] feature index for vbase_sorted[i]
+  const uint32_t* vbase_sorted;
+  const uint32_t* feat_of_vbase;
   uint32_t n_feat_owned;
-  const uint32_t* uslot;
-  const uint32_t* useg;
-  const uint32_t* vals;        // sorted gradient row offsets (float4 units)
-  const uint32_t* counters;
-  const uint32_t* chunk_base;
-  const uint32_t* chunk_seg;
-  double* chunk_part;          // [chunks][kMaxDim]
-  const float* grad;           // gradient rows (upstream or received payload)
+  uint32_t uni_dim;              // every owned table has this dim (0: mixed dims)
+  uint32_t max_d4;
+  const float* grad;
   void* weights;
   float* moments;
-  uint8_t* dirty;              // may be null
-  double inv_batch;
-  double eta, eps, c;
+  uint8_t* dirty;                // may be null
+  double* part1;                 // level-1 range partials [n/C][max_dim]
+  double* part2;                 // level-2 partials [n/(C*P)][max_dim]
+  double inv_batch, eta, eps, c;
   int sgd;
   uint32_t* err;
+  uint32_t* counters;            // [0] unique rows updated, [1] rows spanning ranges
 };
-void launch_update(const UpdateArgs& a, int bf16, int max_dim, uint64_t max_rows, cudaStream_t st);
+size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
+void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
+void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 
 // standalone fused row step on caller rows (s2d_adagrad_rows)
 void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32_t n, uint32_t dim,

@@ -210,6 +210,15 @@ void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_en
     n_slots += (uint32_t)own;
     n_weight_elems += own * feats[f].dim;
   }
+  all_same_dim = true;
+  for (uint32_t f = 0; f < F; ++f) all_same_dim = all_same_dim && feats[f].dim == max_dim;
+  uni_dim = 0;
+  for (uint32_t f = 0; f < F; ++f)
+    if (feats[f].hi > feats[f].lo) {
+      if (uni_dim == 0) uni_dim = feats[f].dim;
+      else if (uni_dim != feats[f].dim) uni_dim = 0xffffffffu;
+    }
+  if (uni_dim == 0xffffffffu) uni_dim = 0;
   vbase_sorted.clear();
   feat_of_vbase.clear();
   for (uint32_t f = 0; f < F; ++f)
@@ -390,7 +399,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.err = err.as<uint32_t>();
     a.direct = 1;
     a.emit_keys = 1;
-    launch_owner_lookup(a, bf16, (int)max_dim, stream);
+    a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
+    launch_lookup_stream(a, bf16, (int)max_dim, stream);
     stats.nnz_owned = nnz;
     stats.entries_owned = BF;
   } else {
@@ -472,7 +482,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.err = err.as<uint32_t>();
     a.direct = 0;
     a.emit_keys = 1;
-    launch_owner_lookup(a, bf16, (int)max_dim, stream);
+    a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
+    launch_lookup_stream(a, bf16, (int)max_dim, stream);
     // C1: partials back to requesters
     phase_begin(kPhA2ALookup);
     S2D_NCCL(ncclGroupStart());
@@ -653,50 +664,35 @@ void Ctx::backward_update(const float* upstream, int mem) {
                                    vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, stream);
     const uint32_t* sk = sorted_in_b ? keys_b.as<uint32_t>() : keys_a.as<uint32_t>();
     const uint32_t* sv = sorted_in_b ? vals_b.as<uint32_t>() : vals_a.as<uint32_t>();
-    uslot.ensure((n + 1) * 4);
-    useg.ensure((n + 2) * 4);
-    counters.ensure(64);
-    chunk_base.ensure((n + 1) * 4);
-    chunk_seg.ensure((n / kChunk + 2) * 4);
-    chunk_part.ensure((n / kChunk + 2) * (uint64_t)max_dim * 8);
-    scan_tmp.ensure(scan_tmp_bytes(n + 1));
-    phase_begin(kPhSegments);
-    SegmentArgs sa{};
-    sa.keys = sk;
-    sa.n = n;
-    sa.n_slots = n_slots;
-    sa.uslot = uslot.as<uint32_t>();
-    sa.useg = useg.as<uint32_t>();
-    sa.counters = counters.as<uint32_t>();
-    sa.chunk_base = chunk_base.as<uint32_t>();
-    sa.chunk_seg = chunk_seg.as<uint32_t>();
-    sa.tmp = scan_tmp.p;
-    sa.tmp_bytes = scan_tmp.cap;
-    run_segments(sa, stream);
     phase_begin(kPhUpdate);
-    UpdateArgs ua{};
+    counters.ensure(64);
+    chunk_part.ensure(stream_partial_bytes(n, max_dim));
+    StreamUpdateArgs ua{};
+    ua.keys = sk;
+    ua.vals = sv;
+    ua.n = n;
+    ua.n_slots = n_slots;
     ua.feats = d_feats.as<FeatDev>();
     ua.vbase_sorted = d_vbase_sorted.as<uint32_t>();
     ua.feat_of_vbase = d_feat_of_vbase.as<uint32_t>();
     ua.n_feat_owned = (uint32_t)feat_of_vbase.size();
-    ua.uslot = uslot.as<uint32_t>();
-    ua.useg = useg.as<uint32_t>();
-    ua.vals = sv;
-    ua.counters = counters.as<uint32_t>();
-    ua.chunk_base = chunk_base.as<uint32_t>();
-    ua.chunk_seg = chunk_seg.as<uint32_t>();
-    ua.chunk_part = chunk_part.as<double>();
+    ua.uni_dim = uni_dim;
+    ua.max_d4 = max_dim / 4;
     ua.grad = grad;
     ua.weights = weights.p;
     ua.moments = moments.as<float>();
     ua.dirty = M > 1 ? dirty.as<uint8_t>() : nullptr;
+    const uint64_t nparts1 = n / 256 + 2;
+    ua.part1 = chunk_part.as<double>();
+    ua.part2 = chunk_part.as<double>() + nparts1 * max_dim;
     ua.inv_batch = 1.0 / (double)((uint64_t)N * B);  // group batch (trainer.cpp:462)
     ua.eta = opt.eta;
     ua.eps = opt.eps;
     ua.c = opt.c;
     ua.sgd = opt.variant == S2D_SGD;
     ua.err = err.as<uint32_t>();
-    launch_update(ua, bf16, (int)max_dim, n, stream);
+    ua.counters = counters.as<uint32_t>();
+    launch_update_stream(ua, bf16, stream);
     uniq = 1;
   }
   (void)uniq;
@@ -713,7 +709,7 @@ void Ctx::refresh_stats() {
   uint32_t c[4];
   S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
   stats.unique_rows = c[0];
-  stats.long_segments = c[2];
+  stats.long_segments = c[1];
 }
 
 // ---- K5 replica sync ---------------------------------------------------------
@@ -795,18 +791,19 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
       break;
     }
     case 5: {
-      uint32_t c[4] = {0, 0, 0, 0};
-      if (nnz_own) S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
-      std::vector<uint32_t> sl(c[0]);
-      if (c[0]) S2D_CUDA(cudaMemcpy(sl.data(), uslot.p, (uint64_t)c[0] * 4, cudaMemcpyDeviceToHost));
-      // slot -> global row of its table
-      for (auto& s : sl) {
-        const size_t i = std::upper_bound(vbase_sorted.begin(), vbase_sorted.end() - 1, s) - vbase_sorted.begin() - 1;
-        const FeatDev& fd = feats[feat_of_vbase[i]];
-        s = s - fd.vbase + fd.lo;
+      std::vector<uint32_t> k(nnz_own);
+      const void* src = sorted_in_b ? keys_b.p : keys_a.p;
+      if (nnz_own) S2D_CUDA(cudaMemcpy(k.data(), src, nnz_own * 4, cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> rows;
+      for (uint64_t i = 0; i < nnz_own; ++i) {
+        if (k[i] >= n_slots) break;
+        if (i && k[i] == k[i - 1]) continue;
+        const size_t j = std::upper_bound(vbase_sorted.begin(), vbase_sorted.end() - 1, k[i]) - vbase_sorted.begin() - 1;
+        const FeatDev& fd = feats[feat_of_vbase[j]];
+        rows.push_back(k[i] - fd.vbase + fd.lo);
       }
-      *n = c[0];
-      if (out) std::memcpy(out, sl.data(), std::min<uint64_t>(cap, c[0]) * 4);
+      *n = rows.size();
+      if (out) std::memcpy(out, rows.data(), std::min<uint64_t>(cap, rows.size()) * 4);
       break;
     }
     default:

@@ -69,6 +69,8 @@ struct Ctx {
   std::vector<RangeDev> ranges;
   std::vector<uint32_t> vbase_sorted, feat_of_vbase;  // owned features by slot base
   uint32_t n_slots = 0;
+  uint32_t uni_dim = 0;
+  bool all_same_dim = false;  // dim shared by every owned table (0: mixed)
   uint64_t n_weight_elems = 0;
   DevBuf d_feats, d_ranges, d_vbase_sorted, d_feat_of_vbase;
   DevBuf weights, moments, dirty;

@@ -4,17 +4,13 @@
 //   bucket_permute K1: bit-exact permute of ids into per-owner send blocks,
 //                  canonical (sample, feature, occurrence) order
 //                  (build_demand, src/trainer.cpp:283-313)
-//   owner_lookup   K2: f64 occurrence-order partial pool of each bag's owned
-//                  rows -> f32 (owner_lookup, src/trainer.cpp:316-338;
-//                  pool_ids, src/embedding.cpp:39-92) + the (slot, gradient
-//                  row) pairs the backward dedup sorts
+//   (K2 owner lookup lives in k_stream.cu)
 //   combine        requester side: f32(sum_{owner asc} f64(partial))
 //                  (pool_and_forward, src/trainer.cpp:372-390)
 //   grad_gather    C2 send layout (build_grad_payloads, src/trainer.cpp:440-457)
 //
-// Lookup layout: LPB lanes serve one bag, each lane owns VPL 16-byte column
-// vectors of the row, so a row gather is LPB*16 contiguous bytes per
-// vector; UNROLL rows are in flight per lane before the in-order f64 adds.
+// Layout: LPB lanes serve one bag, each lane owns VPL 16-byte column vectors
+// of the row (a row is LPB*16 contiguous bytes per vector).
 #include <algorithm>
 
 #include "device.cuh"
@@ -60,107 +56,6 @@ __global__ void k_init_rows(WT* __restrict__ w, uint64_t wbase, uint32_t table_i
       d[q] = (double)(float)__dadd_rn(lo_v, __dmul_rn(span, u));
     }
     Vec4<WT>::store(w + wbase + (uint64_t)r * dim + (uint64_t)c4 * 4, d);
-  }
-}
-
-// ---- lookup --------------------------------------------------------------
-
-template <typename WT>
-struct Raw;
-template <>
-struct Raw<float> {
-  using T = float4;
-  static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  static __device__ __forceinline__ void add(double (&a)[4], const T& x) {
-    a[0] += (double)x.x;
-    a[1] += (double)x.y;
-    a[2] += (double)x.z;
-    a[3] += (double)x.w;
-  }
-};
-template <>
-struct Raw<__nv_bfloat16> {
-  using T = uint2;
-  static __device__ __forceinline__ T load(const __nv_bfloat16* p) {
-    return __ldg(reinterpret_cast<const uint2*>(p));
-  }
-  static __device__ __forceinline__ void add(double (&a)[4], const T& x) {
-    a[0] += (double)__uint_as_float(x.x << 16);
-    a[1] += (double)__uint_as_float(x.x & 0xffff0000u);
-    a[2] += (double)__uint_as_float(x.y << 16);
-    a[3] += (double)__uint_as_float(x.y & 0xffff0000u);
-  }
-};
-
-template <typename WT, int LPB, int VPL, int UNROLL>
-__global__ void __launch_bounds__(256) k_owner_lookup(const LookupArgs a) {
-  constexpr int GPW = 32 / LPB;  // bag groups per warp
-  const uint32_t lane = lane_id();
-  const uint32_t grp = lane / LPB, gl = lane % LPB;
-  const uint32_t gmask = (LPB == 32) ? 0xffffffffu : (((1u << LPB) - 1u) << (grp * LPB));
-  const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
-  const uint64_t slots = (uint64_t)gridDim.x * (blockDim.x / 32) * GPW;
-  const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * GPW + grp;
-  const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
-  for (uint64_t bag = first; bag < n_bags; bag += slots) {
-    const uint32_t f = (uint32_t)(bag % a.F);
-    const uint32_t len = __ldg(a.lengths + bag);
-    if (!a.direct && len == 0) continue;
-    const uint32_t off = __ldg(a.id_off + bag);
-    const uint32_t dim = __ldg(&a.feats[f].dim), flo = __ldg(&a.feats[f].lo), fhi = __ldg(&a.feats[f].hi);
-    const uint64_t wbase = __ldg(&a.feats[f].wbase);
-    const uint32_t vbase = __ldg(&a.feats[f].vbase);
-    const uint64_t out_off = a.direct ? (uint64_t)((bag / a.F) % a.B) * a.sum_dims + __ldg(&a.feats[f].coff)
-                                      : __ldg(a.eoff + bag);
-    const uint32_t d4 = dim >> 2;
-    double acc[VPL][4];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[v][q] = 0.0;
-    for (uint32_t c = 0; c < len; c += LPB) {
-      const bool have = c + gl < len;
-      const uint32_t id = have ? __ldg(a.ids + off + c + gl) : 0u;
-      const bool ok = have && id >= flo && id < fhi;
-      if (have && !ok) atomicOr(a.err, kErrIdRange);
-      if (a.emit_keys && have) {
-        a.keys[off + c + gl] = ok ? vbase + (id - flo) : 0xffffffffu;
-        a.vals[off + c + gl] = (uint32_t)(out_off >> 2);
-      }
-      const uint32_t cnt = min((uint32_t)LPB, len - c);
-      for (uint32_t t = 0; t < cnt; t += UNROLL) {
-        typename Raw<WT>::T raw[UNROLL][VPL];
-        bool use[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          const uint32_t src = grp * LPB + min(t + u, (uint32_t)LPB - 1);
-          const uint32_t rid = __shfl_sync(gmask, id, src);
-          const bool rok = __shfl_sync(gmask, ok, src);
-          use[u] = (t + u < cnt) && rok;
-          if (use[u]) {
-            const WT* row = W + wbase + (uint64_t)(rid - flo) * dim;
-#pragma unroll
-            for (int v = 0; v < VPL; ++v) {
-              const uint32_t c4 = gl + v * LPB;
-              if (c4 < d4) raw[u][v] = Raw<WT>::load(row + c4 * 4);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-          if (use[u]) {
-#pragma unroll
-            for (int v = 0; v < VPL; ++v)
-              if (gl + v * LPB < d4) Raw<WT>::add(acc[v], raw[u][v]);
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const uint32_t c4 = gl + v * LPB;
-      if (c4 < d4) store_f32x4_stream(a.out + out_off + c4 * 4, acc[v]);
-    }
   }
 }
 
@@ -298,24 +193,6 @@ unsigned grid_for(uint64_t work, unsigned per_block, unsigned cap) {
 
 constexpr unsigned kGridCap = 148 * 16;
 
-template <typename WT>
-void lookup_dispatch(const LookupArgs& a, int max_dim, cudaStream_t st) {
-  const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
-  const int d4 = max_dim / 4;
-  if (d4 <= 8) {
-    k_owner_lookup<WT, 8, 1, 8><<<grid_for(n_bags, 32, kGridCap), 256, 0, st>>>(a);
-  } else if (d4 <= 16) {
-    k_owner_lookup<WT, 16, 1, 8><<<grid_for(n_bags, 16, kGridCap), 256, 0, st>>>(a);
-  } else if (d4 <= 32) {
-    k_owner_lookup<WT, 32, 1, 8><<<grid_for(n_bags, 8, kGridCap), 256, 0, st>>>(a);
-  } else if (d4 <= 64) {
-    k_owner_lookup<WT, 32, 2, 4><<<grid_for(n_bags, 8, kGridCap), 256, 0, st>>>(a);
-  } else {
-    k_owner_lookup<WT, 32, 4, 2><<<grid_for(n_bags, 8, kGridCap), 256, 0, st>>>(a);
-  }
-  S2D_LAUNCH_CHECK();
-}
-
 }  // namespace
 
 void launch_init_rows(void* w, int bf16, const FeatDev* feats_host, uint32_t F, uint64_t seed,
@@ -333,14 +210,6 @@ void launch_init_rows(void* w, int bf16, const FeatDev* feats_host, uint32_t F, 
                                                fd.hi - fd.lo, fd.dim, seed);
     S2D_LAUNCH_CHECK();
   }
-}
-
-void launch_owner_lookup(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st) {
-  if ((uint64_t)a.n_req * a.B * a.F == 0) return;
-  if (bf16)
-    lookup_dispatch<__nv_bfloat16>(a, max_dim, st);
-  else
-    lookup_dispatch<float>(a, max_dim, st);
 }
 
 void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st) {

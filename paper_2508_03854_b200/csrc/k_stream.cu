@@ -1,0 +1,796 @@
+// Streaming segmented gather-reduce kernels: the hot path of the step.
+//
+// One warp walks a contiguous run of items -- the ids of 32 consecutive
+// bags (K2 lookup), or the radix-sorted contributions of consecutive rows
+// (K3b segment reduce + K4 fused AdaGrad) -- as a single stream.  Rows are
+// gathered through a per-warp shared-memory ring with cp.async: lane l copies
+// (and later reads back) only its own 16-byte column vectors of every row,
+// so stage completion is a per-thread cp.async.wait_group and no block
+// barrier is needed.  kStages-1 stages of kRowsPerStage rows are in flight
+// per warp while the oldest stage is reduced, without spending registers on
+// in-flight data; f64 accumulators stay in registers (4 columns x VPL per
+// lane).  Every item is added into its accumulator strictly in stream order
+// -- the reference's canonical order inside each bag and each row segment --
+// so pooled rows and segment sums are bit-exact.  The accumulator is
+// flushed (pooled row store, or the fused AdaGrad row update) where the bag
+// / segment ends.
+//
+// History (profiles/r01/): warp-per-bag kernels were latency bound (11% of
+// DRAM peak, one round trip per bag); register double-buffered streams were
+// capped at 12-16 warps/SM by f64 accumulators + in-flight rows
+// (128 regs), stalling on shuffles and load latency.
+#include "device.cuh"
+
+namespace s2d {
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kRowsPerStage = 4;
+constexpr int kSlots = kStages * kRowsPerStage;
+constexpr int kBags = 32;  // bags per lookup unit (one per lane)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async(uint32_t dst, const void* src, int bytes) {
+  if (bytes == 16)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
+}
+// branch-free predicated cp.async (nothing is copied when pred == 0)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_p(uint32_t dst, const void* src, bool pred) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], %3;\n}\n" ::"r"(dst),
+      "l"(src), "r"((uint32_t)pred), "n"(BYTES));
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, uint32_t src) {
+  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
+  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
+  return ((uint64_t)hi << 32) | lo;
+}
+
+// Number of lanes j with end_j <= p (ends non-decreasing over lanes).
+__device__ __forceinline__ uint32_t count_le(uint32_t my_end, uint32_t p) {
+  uint32_t lo = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const uint32_t v = __shfl_sync(0xffffffffu, my_end, lo + step - 1);
+    if (v <= p) lo += step;
+  }
+  return lo;
+}
+
+// Element type of a stored row and the 4-column vector a lane copies.
+template <typename WT>
+struct Row;
+template <>
+struct Row<float> {
+  static constexpr int kVecBytes = 16;
+  static __device__ __forceinline__ void add_s(double (&a)[4], uint32_t saddr) {
+    const float4 x = lds128(saddr);
+    a[0] += (double)x.x;
+    a[1] += (double)x.y;
+    a[2] += (double)x.z;
+    a[3] += (double)x.w;
+  }
+  static __device__ __forceinline__ void add(double (&a)[4], const void* s) {
+    const float4 x = *reinterpret_cast<const float4*>(s);
+    a[0] += (double)x.x;
+    a[1] += (double)x.y;
+    a[2] += (double)x.z;
+    a[3] += (double)x.w;
+  }
+};
+template <>
+struct Row<__nv_bfloat16> {
+  static constexpr int kVecBytes = 8;
+  static __device__ __forceinline__ void add_s(double (&a)[4], uint32_t saddr) {
+    const uint2 x = lds64(saddr);
+    a[0] += (double)__uint_as_float(x.x << 16);
+    a[1] += (double)__uint_as_float(x.x & 0xffff0000u);
+    a[2] += (double)__uint_as_float(x.y << 16);
+    a[3] += (double)__uint_as_float(x.y & 0xffff0000u);
+  }
+  static __device__ __forceinline__ void add(double (&a)[4], const void* s) {
+    const uint2 x = *reinterpret_cast<const uint2*>(s);
+    a[0] += (double)__uint_as_float(x.x << 16);
+    a[1] += (double)__uint_as_float(x.x & 0xffff0000u);
+    a[2] += (double)__uint_as_float(x.y << 16);
+    a[3] += (double)__uint_as_float(x.y & 0xffff0000u);
+  }
+};
+
+// per-warp ring: slot s, vector v, lane l -> ((s*VPL + v)*32 + l) * VB
+template <int VPL, int VB>
+__device__ __forceinline__ uint32_t ring_off(uint32_t slot, int v, uint32_t lane) {
+  return ((slot * VPL + v) * 32 + lane) * VB;
+}
+
+// ============================================================================
+// K2: owner lookup.  A warp owns 32 consecutive bags (flattened [n][s][f]),
+// lane j holding bag j's metadata; the items are the bags' ids in (bag,
+// occurrence) order.
+// ============================================================================
+
+template <typename WT, int VPL>
+__global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
+  constexpr int VB = Row<WT>::kVecBytes;
+  constexpr int kWinStages = 32 / kRowsPerStage;
+  constexpr uint32_t kRowBytes = VPL * 32 * VB;  // ring slot stride
+  constexpr uint64_t kNone = ~0ull;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  // this lane's column chunk of slot 0 of the warp's ring
+  const uint32_t ring_s = smem_u32(smem) + warp * kSlots * kRowBytes + lane * VB;
+  const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
+  const uint64_t n_units = (n_bags + kBags - 1) / kBags;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
+  const uint32_t uni_d4 = a.uni_d4;
+
+  for (uint64_t unit = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; unit < n_units; unit += stride) {
+    const uint64_t b0 = unit * kBags;
+    const uint32_t nb = (n_bags - b0) < (uint64_t)kBags ? (uint32_t)(n_bags - b0) : (uint32_t)kBags;
+    const uint64_t my_bag = b0 + min(lane, nb - 1);
+    const uint32_t my_end = __ldg(a.id_off + my_bag + 1);
+    const uint32_t o0 = __ldg(a.id_off + b0);
+    uint32_t my_start = __shfl_up_sync(0xffffffffu, my_end, 1);
+    if (lane == 0) my_start = o0;
+    const uint32_t o1 = __shfl_sync(0xffffffffu, my_end, nb - 1);
+    const uint32_t f = (uint32_t)(my_bag % a.F);
+    const uint32_t dim = __ldg(&a.feats[f].dim);
+    const uint32_t flo = __ldg(&a.feats[f].lo), fhi = __ldg(&a.feats[f].hi);
+    const uint32_t vbase = __ldg(&a.feats[f].vbase);
+    const uint64_t wbase = __ldg(&a.feats[f].wbase);
+    const uint64_t out_off = a.direct ? (uint64_t)((my_bag / a.F) % a.B) * a.sum_dims + __ldg(&a.feats[f].coff)
+                                      : __ldg(a.eoff + my_bag);
+    if (a.direct) {  // empty bags pool to zero (embedding.cpp:43-44)
+      uint32_t empty = __ballot_sync(0xffffffffu, lane < nb && my_start == my_end);
+      while (empty) {
+        const uint32_t j = __ffs(empty) - 1;
+        empty &= empty - 1;
+        const uint64_t oo = shfl64(out_off, j);
+        const uint32_t d4j = __shfl_sync(0xffffffffu, dim, j) >> 2;
+        for (uint32_t c4 = lane; c4 < d4j; c4 += 32)
+          __stcs(reinterpret_cast<float4*>(a.out + oo + c4 * 4), make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+    }
+    const uint32_t n_items = o1 - o0;
+    if (n_items == 0) continue;
+    const uint32_t nwin = (n_items + 31) / 32;
+
+    // Window w (32 items): lane k holds item k's row address and bag word
+    // (bag | ok << 8 | d4 << 16); `simple` bit k = item k is a valid id of
+    // the same bag as item k-1 (no flush, no check needed).  Items past the
+    // end are invalid ids of the last item's bag.
+    uint32_t last_bag = 0xffffu;
+    auto gen = [&](uint32_t win, uint32_t id, uint32_t& bw, uint64_t& ad, uint32_t& simple) {
+      const uint32_t p = o0 + win * 32 + lane;
+      const bool have = p < o1;
+      const uint32_t j = min(count_le(my_end, have ? p : o1 - 1), nb - 1);
+      const uint32_t lo_j = __shfl_sync(0xffffffffu, flo, j), hi_j = __shfl_sync(0xffffffffu, fhi, j);
+      const uint32_t dim_j = __shfl_sync(0xffffffffu, dim, j), vb_j = __shfl_sync(0xffffffffu, vbase, j);
+      const uint64_t wb_j = shfl64(wbase, j);
+      const uint64_t oo_j = shfl64(out_off, j);
+      const bool ok = have && id >= lo_j && id < hi_j;
+      if (have && !ok) atomicOr(a.err, kErrIdRange);
+      if (a.emit_keys && have) {
+        a.keys[p] = ok ? vb_j + (id - lo_j) : 0xffffffffu;
+        a.vals[p] = (uint32_t)(oo_j >> 2);
+      }
+      ad = ok ? wb_j + (uint64_t)(id - lo_j) * dim_j : kNone;
+      bw = j | (ok ? 0x100u : 0u) | ((dim_j >> 2) << 16);
+      uint32_t before = __shfl_up_sync(0xffffffffu, j, 1);
+      if (lane == 0) before = last_bag;
+      last_bag = __shfl_sync(0xffffffffu, j, 31);
+      simple = __ballot_sync(0xffffffffu, ok && j == before);
+    };
+    auto load_id = [&](uint32_t win) -> uint32_t {
+      const uint32_t p = o0 + win * 32 + lane;
+      return (win < nwin && p < o1) ? __ldg(a.ids + p) : 0u;
+    };
+    uint32_t bw_c, bw_n, sm_c, sm_n;
+    uint64_t ad_c, ad_n;
+    gen(0, load_id(0), bw_c, ad_c, sm_c);
+    gen(1, load_id(1), bw_n, ad_n, sm_n);
+    uint32_t nid = load_id(2);
+    uint32_t wc = 0;  // window being consumed
+
+    auto produce = [&](uint32_t st) {
+      const bool nxt = (st / kWinStages) != wc;
+      const uint64_t A = nxt ? ad_n : ad_c;
+      const uint32_t Bw = nxt ? bw_n : bw_c;
+      const uint32_t q = (st % kWinStages) * kRowsPerStage;
+      const uint32_t base = ring_s + (st % kStages) * (kRowsPerStage * kRowBytes);
+#pragma unroll
+      for (int r = 0; r < kRowsPerStage; ++r) {
+        const uint64_t ad = shfl64(A, q + r);
+        const uint32_t d4 = uni_d4 ? uni_d4 : (__shfl_sync(0xffffffffu, Bw, q + r) >> 16);
+        const WT* src = W + ad + lane * 4;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          cp_async_p<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128, ad != kNone && lane + v * 32 < d4);
+      }
+      cp_commit();
+    };
+
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[v][k] = 0.0;
+    uint32_t cur = __shfl_sync(0xffffffffu, bw_c, 0);
+    uint32_t d4c = uni_d4 ? uni_d4 : (cur >> 16);
+    cur &= 0xffu;
+    auto flush = [&]() {
+      const uint64_t oo = shfl64(out_off, cur);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        if (lane + v * 32 < d4c) store_f32x4_stream(a.out + oo + (lane + v * 32) * 4, acc[v]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[v][k] = 0.0;
+      }
+    };
+    auto add_row = [&](uint32_t saddr) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        if (VPL == 1 || lane + v * 32 < d4c) Row<WT>::add_s(acc[v], saddr + v * 32 * VB);
+    };
+
+    const uint32_t nst = (n_items + kRowsPerStage - 1) / kRowsPerStage;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) produce(s);
+    for (uint32_t s = 0; s < nst; ++s) {
+      if (s > 0 && s % kWinStages == 0) {  // enter window wc + 1
+        ++wc;
+        bw_c = bw_n;
+        ad_c = ad_n;
+        sm_c = sm_n;
+        gen(wc + 1, nid, bw_n, ad_n, sm_n);
+        nid = load_id(wc + 2);
+      }
+      produce(s + kStages - 1);
+      cp_wait<kStages - 1>();
+      const uint32_t q = (s % kWinStages) * kRowsPerStage;
+      const uint32_t base = ring_s + (s % kStages) * (kRowsPerStage * kRowBytes);
+      if (((sm_c >> q) & ((1u << kRowsPerStage) - 1u)) == ((1u << kRowsPerStage) - 1u)) {
+        // no bag boundary and no invalid id in this stage
+#pragma unroll
+        for (int r = 0; r < kRowsPerStage; ++r) add_row(base + r * kRowBytes);
+      } else {
+#pragma unroll
+        for (int r = 0; r < kRowsPerStage; ++r) {
+          const uint32_t bw = __shfl_sync(0xffffffffu, bw_c, q + r);
+          if ((bw & 0xffu) != cur) {
+            flush();
+            cur = bw & 0xffu;
+            d4c = uni_d4 ? uni_d4 : (bw >> 16);
+          }
+          if (bw & 0x100u) add_row(base + r * kRowBytes);
+        }
+      }
+    }
+    cp_wait<0>();
+    flush();
+  }
+}
+
+// ============================================================================
+// K3b + K4: segment reduce + fused row update over the radix-sorted
+// (slot, gradient-row) pairs.  Warp u owns the segments whose head lies in
+// the nominal range [u*C, (u+1)*C).  A segment running past its head's range
+// continues with the in-order f64 partial sums of the fully covered ranges
+// (level-1: C items; level-2: kP ranges aligned to kP*C) and then its tail
+// items -- a fixed, launch-independent association.  It equals the
+// reference's strictly sequential f64 sum whenever the segment fits in its
+// head's range, and otherwise re-associates at fixed chunk boundaries
+// (|dg| ~ 1e-16 relative).  |g|^2 is a per-lane in-order sum followed by a
+// fixed xor-shuffle tree.  The weight row and moment of every segment are
+// fetched through the ring together with the segment's first gradient row.
+// ============================================================================
+
+constexpr uint32_t kC = 256;  // items per nominal range
+constexpr uint32_t kP = 32;   // ranges per level-2 partial
+
+__device__ __forceinline__ void row_ref(const StreamUpdateArgs& a, uint32_t key, uint64_t& wofs, uint32_t& d4) {
+  if (a.uni_dim) {
+    wofs = (uint64_t)key * a.uni_dim;
+    d4 = a.uni_dim >> 2;
+  } else {
+    const uint32_t f = feature_of_slot(a.vbase_sorted, a.feat_of_vbase, a.n_feat_owned, key);
+    const uint32_t dim = __ldg(&a.feats[f].dim);
+    wofs = __ldg(&a.feats[f].wbase) + (uint64_t)(key - __ldg(&a.feats[f].vbase)) * dim;
+    d4 = dim >> 2;
+  }
+}
+
+// In-order f64 sum of the gradient rows of items [s, t) of one segment,
+// through the warp's ring.  lane_s = ring base + lane * 16.
+template <int VPL>
+__device__ __forceinline__ void ring_sum(const StreamUpdateArgs& a, uint32_t lane_s, uint32_t lane, uint64_t s,
+                                         uint64_t t, uint32_t d4, double (&acc)[VPL][4]) {
+  constexpr uint32_t kRowBytes = VPL * 32 * 16;
+  constexpr int kWinStages = 32 / kRowsPerStage;
+  if (t <= s) return;
+  const uint32_t n = (uint32_t)(t - s);
+  const uint32_t nst = (n + kRowsPerStage - 1) / kRowsPerStage;
+  uint32_t my_val = 0;
+  auto produce = [&](uint32_t st) {
+    const uint32_t q = (st % kWinStages) * kRowsPerStage;
+    if (q == 0) {
+      const uint32_t i0 = st * kRowsPerStage;
+      my_val = (i0 + lane < n) ? __ldg(a.vals + s + i0 + lane) : 0u;
+    }
+    const uint32_t base = lane_s + (st % kStages) * (kRowsPerStage * kRowBytes);
+#pragma unroll
+    for (int r = 0; r < kRowsPerStage; ++r) {
+      const uint32_t i = st * kRowsPerStage + r;
+      const uint32_t val = __shfl_sync(0xffffffffu, my_val, q + r);
+      const float* row = a.grad + (uint64_t)val * 4 + lane * 4;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) cp_async_p<16>(base + r * kRowBytes + v * 512, row + v * 128, i < n && lane + v * 32 < d4);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < kStages - 1; ++st) produce(st);
+  for (uint32_t st = 0; st < nst; ++st) {
+    produce(st + kStages - 1);
+    cp_wait<kStages - 1>();
+    const uint32_t base = lane_s + (st % kStages) * (kRowsPerStage * kRowBytes);
+    const uint32_t cnt = min((uint32_t)kRowsPerStage, n - st * kRowsPerStage);
+#pragma unroll
+    for (int r = 0; r < kRowsPerStage; ++r)
+      if (r < cnt) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (VPL == 1 || lane + v * 32 < d4) Row<float>::add_s(acc[v], base + r * kRowBytes + v * 512);
+      }
+  }
+  cp_wait<0>();
+}
+
+template <int VPL>
+__device__ __forceinline__ void add_partial(const double* p, uint32_t lane, uint32_t d4, double (&acc)[VPL][4]) {
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const uint32_t c4 = lane + v * 32;
+    if (c4 < d4) {
+      const double2 x0 = __ldg(reinterpret_cast<const double2*>(p + c4 * 4));
+      const double2 x1 = __ldg(reinterpret_cast<const double2*>(p + c4 * 4) + 1);
+      acc[v][0] += x0.x;
+      acc[v][1] += x0.y;
+      acc[v][2] += x1.x;
+      acc[v][3] += x1.y;
+    }
+  }
+}
+
+template <int VPL>
+__device__ __forceinline__ void store_partial(double* p, uint32_t lane, uint32_t d4, const double (&acc)[VPL][4]) {
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const uint32_t c4 = lane + v * 32;
+    if (c4 < d4) {
+      reinterpret_cast<double2*>(p + c4 * 4)[0] = make_double2(acc[v][0], acc[v][1]);
+      reinterpret_cast<double2*>(p + c4 * 4)[1] = make_double2(acc[v][2], acc[v][3]);
+    }
+  }
+}
+
+// level-1 partials: range k = [kC, kC+C) lying inside one segment
+template <int VPL>
+__global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t lane_s = smem_u32(smem) + warp * kSlots * VPL * 32 * 16 + lane * 16;
+  const uint64_t n_ranges = a.n / kC;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t k = 1 + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < n_ranges; k += stride) {
+    const uint64_t s = k * kC, t = s + kC;
+    const uint32_t key = __ldg(a.keys + s - 1);
+    if (key >= a.n_slots || __ldg(a.keys + t - 1) != key) continue;
+    uint64_t wofs;
+    uint32_t d4;
+    row_ref(a, key, wofs, d4);
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    ring_sum<VPL>(a, lane_s, lane, s, t, d4, acc);
+    store_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+  }
+}
+
+// level-2 partials: kP consecutive level-1 ranges inside one segment
+template <int VPL>
+__global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t n_groups = a.n / ((uint64_t)kC * kP);
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t m = 1 + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; m < n_groups; m += stride) {
+    const uint64_t s = m * kC * kP, t = s + (uint64_t)kC * kP;
+    const uint32_t key = __ldg(a.keys + s - 1);
+    if (key >= a.n_slots || __ldg(a.keys + t - 1) != key) continue;
+    uint64_t wofs;
+    uint32_t d4;
+    row_ref(a, key, wofs, d4);
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    for (uint32_t r = 0; r < kP; ++r) add_partial<VPL>(a.part1 + (m * kP + r) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+    store_partial<VPL>(a.part2 + m * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+  }
+}
+
+template <typename WT, int VPL>
+__global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
+  constexpr int WB = Row<WT>::kVecBytes;
+  constexpr int kWinStages = 32 / kRowsPerStage;
+  constexpr uint32_t kGRow = VPL * 32 * 16, kWRow = VPL * 32 * WB;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t per_warp = kSlots * (kGRow + kWRow) + kSlots * 4;
+  const uint32_t gring_s = smem_u32(smem) + warp * per_warp;  // gradient rows
+  const uint32_t wring_s = gring_s + kSlots * kGRow;            // weight row at each head
+  const uint32_t mring_s = wring_s + kSlots * kWRow;            // moment at each head
+  const uint32_t g_lane = gring_s + lane * 16, w_lane = wring_s + lane * WB;
+  const uint64_t n = a.n;
+  const uint64_t n_units = (n + kC - 1) / kC;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  WT* __restrict__ W = reinterpret_cast<WT*>(a.weights);
+  uint32_t heads = 0, longs = 0;
+
+  for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; u < n_units; u += stride) {
+    const uint64_t ra = u * kC, re = (ra + kC < n) ? ra + kC : n;
+    // first segment head in [ra, re)
+    uint64_t h = ~0ull;
+    for (uint64_t c = ra; c < re; c += 32) {
+      const uint64_t p = c + lane;
+      bool head = false;
+      if (p < re) {
+        const uint32_t k = __ldg(a.keys + p);
+        head = k < a.n_slots && (p == 0 || __ldg(a.keys + p - 1) != k);
+      }
+      const uint32_t bal = __ballot_sync(0xffffffffu, head);
+      if (bal) {
+        h = c + (__ffs(bal) - 1);
+        break;
+      }
+    }
+    if (h == ~0ull) continue;
+    const uint32_t n_items = (uint32_t)(re - h);
+    const uint32_t nwin = (n_items + 31) / 32;
+
+    // Window w: lane k holds item k's key, gradient row, meta (d4 | valid <<
+    // 16 | head << 17) and weight offset; `simple` bit k = valid item of the
+    // same segment as item k-1.
+    uint32_t prev_key = 0xfffffffeu;  // key of the item before the window
+    auto gen = [&](uint32_t win, uint32_t& key, uint32_t& val, uint32_t& meta, uint64_t& wofs, uint32_t& simple) {
+      const uint64_t p = h + (uint64_t)win * 32 + lane;
+      const bool have = win < nwin && p < re;
+      key = have ? __ldg(a.keys + p) : 0xffffffffu;
+      val = have ? __ldg(a.vals + p) : 0u;
+      uint32_t before = __shfl_up_sync(0xffffffffu, key, 1);
+      if (lane == 0) before = prev_key;
+      prev_key = __shfl_sync(0xffffffffu, key, 31);
+      uint32_t d4 = 0;
+      wofs = 0;
+      const bool valid = key < a.n_slots;
+      if (valid) row_ref(a, key, wofs, d4);
+      const bool head = valid && key != before;
+      meta = d4 | (valid ? 0x10000u : 0u) | (head ? 0x20000u : 0u);
+      simple = __ballot_sync(0xffffffffu, valid && !head);
+    };
+    uint32_t k_c, v_c, m_c, s_c, k_n, v_n, m_n, s_n;
+    uint64_t w_c, w_n;
+    gen(0, k_c, v_c, m_c, w_c, s_c);
+    gen(1, k_n, v_n, m_n, w_n, s_n);
+    uint32_t wc = 0;
+
+    auto produce = [&](uint32_t st) {
+      const bool nxt = (st / kWinStages) != wc;
+      const uint32_t K = nxt ? k_n : k_c, V = nxt ? v_n : v_c, Mt = nxt ? m_n : m_c;
+      const uint64_t Wo = nxt ? w_n : w_c;
+      const uint32_t q = (st % kWinStages) * kRowsPerStage;
+      const uint32_t slot0 = (st % kStages) * kRowsPerStage;
+#pragma unroll
+      for (int r = 0; r < kRowsPerStage; ++r) {
+        const uint32_t meta = __shfl_sync(0xffffffffu, Mt, q + r);
+        const uint32_t val = __shfl_sync(0xffffffffu, V, q + r);
+        const uint32_t key = __shfl_sync(0xffffffffu, K, q + r);
+        const uint64_t wo = a.uni_dim ? (uint64_t)key * a.uni_dim : shfl64(Wo, q + r);
+        const uint32_t d4 = meta & 0xffffu, slot = slot0 + r;
+        const bool valid = meta & 0x10000u, head = meta & 0x20000u;
+        const float* grow = a.grad + (uint64_t)val * 4 + lane * 4;
+        const WT* wrow = W + wo + lane * 4;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const bool col = lane + v * 32 < d4;
+          cp_async_p<16>(g_lane + slot * kGRow + v * 512, grow + v * 128, valid && col);
+          cp_async_p<WB>(w_lane + slot * kWRow + v * 32 * WB, wrow + v * 128, head && col);
+        }
+        cp_async_p<4>(mring_s + slot * 4, a.moments + (head ? key : 0), head && lane == 0);
+      }
+      cp_commit();
+    };
+
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    uint32_t cur = 0xffffffffu, d4 = 0;
+    uint64_t wofs = 0;
+    double wold[VPL][4];  // weight row of `cur`
+    float vold = 0.f;
+    bool stop = false;
+
+    // fused K4 row step (optimizer.cpp:65-90); nonfinite rows are not written
+    auto flush = [&]() {
+      bool finite = true;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          acc[v][j] = acc[v][j] * a.inv_batch;  // g (optimizer.cpp:55)
+          if (lane + v * 32 < d4) finite &= isfinite(acc[v][j]);
+        }
+      if (!__all_sync(0xffffffffu, finite)) {
+        if (lane == 0) atomicOr(a.err, kErrNonfinite);
+      } else {
+        double lr = a.eta;
+        if (!a.sgd) {
+          double ns = 0.0;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            if (lane + v * 32 < d4)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) ns += acc[v][j] * acc[v][j];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+          const float v_new = (float)((double)vold + ns);
+          lr = a.eta / (sqrt((double)v_new / a.c) + a.eps);  // effective_lr (optimizer.cpp:61-63)
+          if (lane == 0) a.moments[cur] = v_new;
+        }
+        WT* w = W + wofs;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const uint32_t c4 = lane + v * 32;
+          if (c4 < d4) {
+            double x[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) x[j] = wold[v][j] - lr * acc[v][j];
+            Vec4<WT>::store(w + c4 * 4, x);
+          }
+        }
+        if (lane == 0 && a.dirty) a.dirty[cur] = 1;
+        ++heads;
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    };
+    auto add_grad = [&](uint32_t slot) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        if (VPL == 1 || lane + v * 32 < d4) Row<float>::add_s(acc[v], g_lane + slot * kGRow + v * 512);
+    };
+
+    const uint32_t nst = (n_items + kRowsPerStage - 1) / kRowsPerStage;
+#pragma unroll
+    for (int s = 0; s < kStages - 1; ++s) produce(s);
+    for (uint32_t s = 0; s < nst && !stop; ++s) {
+      if (s > 0 && s % kWinStages == 0) {
+        ++wc;
+        k_c = k_n;
+        v_c = v_n;
+        m_c = m_n;
+        w_c = w_n;
+        s_c = s_n;
+        gen(wc + 1, k_n, v_n, m_n, w_n, s_n);
+      }
+      produce(s + kStages - 1);
+      cp_wait<kStages - 1>();
+      const uint32_t q = (s % kWinStages) * kRowsPerStage;
+      const uint32_t slot0 = (s % kStages) * kRowsPerStage;
+      if (((s_c >> q) & ((1u << kRowsPerStage) - 1u)) == ((1u << kRowsPerStage) - 1u)) {
+#pragma unroll
+        for (int r = 0; r < kRowsPerStage; ++r) add_grad(slot0 + r);
+      } else {
+#pragma unroll
+        for (int r = 0; r < kRowsPerStage; ++r) {
+          const uint32_t key = __shfl_sync(0xffffffffu, k_c, q + r);
+          const uint32_t meta = __shfl_sync(0xffffffffu, m_c, q + r);
+          const uint64_t wo = a.uni_dim ? (uint64_t)key * a.uni_dim : shfl64(w_c, q + r);
+          const uint32_t slot = slot0 + r;
+          if (s * kRowsPerStage + r >= n_items) break;  // past this range: not a sentinel
+          if (!stop && key != cur) {
+            if (cur != 0xffffffffu) flush();
+            if (key >= a.n_slots) {
+              stop = true;
+            } else {  // segment head: take its weight row / moment out of the ring
+              cur = key;
+              wofs = wo;
+              d4 = meta & 0xffffu;
+#pragma unroll
+              for (int v = 0; v < VPL; ++v) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) wold[v][j] = 0.0;
+                if (lane + v * 32 < d4) Row<WT>::add_s(wold[v], w_lane + slot * kWRow + v * 32 * WB);
+              }
+              // the moment was copied by lane 0 alone: only lane 0's
+              // wait_group covers it, so lane 0 reads and broadcasts
+              vold = __uint_as_float(__shfl_sync(0xffffffffu, lane == 0 ? lds32(mring_s + slot * 4) : 0u, 0));
+            }
+          }
+          if (!stop) add_grad(slot);
+        }
+      }
+    }
+    cp_wait<0>();
+    if (stop) continue;
+    // continuation of the open segment past this range
+    if (re < n && __ldg(a.keys + re) == cur) {
+      ++longs;
+      uint64_t k = re / kC;  // == u + 1
+      uint64_t kend = ~0ull;
+      for (uint64_t base = k; kend == ~0ull; base += 32) {
+        const uint64_t kk = base + lane;
+        const uint64_t last = (kk + 1) * kC - 1;
+        const bool inside = last < n && __ldg(a.keys + last) == cur;
+        const uint32_t bal = __ballot_sync(0xffffffffu, !inside);
+        if (bal) kend = base + (__ffs(bal) - 1);
+      }
+      // ranges [k, kend) are fully inside; range kend holds the end
+      const uint64_t rs = kend * kC, rlim = (rs + kC < n) ? rs + kC : n;
+      uint64_t seg_end = rlim;
+      for (uint64_t c = rs; c < rlim; c += 32) {
+        const uint64_t p = c + lane;
+        const bool diff = p < rlim && __ldg(a.keys + p) != cur;
+        const uint32_t bal = __ballot_sync(0xffffffffu, diff);
+        if (bal) {
+          seg_end = c + (__ffs(bal) - 1);
+          break;
+        }
+      }
+      while (k < kend) {
+        if (k % kP == 0 && k + kP <= kend) {
+          add_partial<VPL>(a.part2 + (k / kP) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+          k += kP;
+        } else {
+          add_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+          k += 1;
+        }
+      }
+      ring_sum<VPL>(a, g_lane, lane, rs, seg_end, d4, acc);
+    }
+    flush();
+  }
+  if (lane == 0) {
+    if (heads) atomicAdd(&a.counters[0], heads);
+    if (longs) atomicAdd(&a.counters[1], longs);
+  }
+}
+
+unsigned grid_units(uint64_t units, uint32_t units_per_block, unsigned cap) {
+  uint64_t g = (units + units_per_block - 1) / units_per_block;
+  return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, cap));
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+  S2D_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+// warps per block so that one block's rings stay within ~72 KB (3 blocks/SM)
+constexpr size_t kBlockRingBudget = 72 * 1024;
+inline uint32_t warps_for(size_t per_warp, uint32_t max_warps) {
+  size_t w = kBlockRingBudget / per_warp;
+  if (w < 1) w = 1;
+  return (uint32_t)std::min<size_t>(w, max_warps);
+}
+
+template <typename WT, int VPL>
+void lookup_launch(const LookupArgs& a, cudaStream_t st) {
+  const uint64_t n_units = ((uint64_t)a.n_req * a.B * a.F + kBags - 1) / kBags;
+  const size_t per_warp = (size_t)kSlots * VPL * 32 * Row<WT>::kVecBytes;
+  const uint32_t nw = warps_for(per_warp, 8);
+  const size_t smem = nw * per_warp;
+  static bool init = false;
+  if (!init) {
+    set_smem(k_lookup_ring<WT, VPL>, smem);
+    init = true;
+  }
+  k_lookup_ring<WT, VPL><<<grid_units(n_units, nw, 148 * 64), nw * 32, smem, st>>>(a);
+  S2D_LAUNCH_CHECK();
+}
+
+template <typename WT, int VPL>
+void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
+  const size_t pw_p = (size_t)kSlots * VPL * 32 * 16;
+  const size_t pw_u = (size_t)kSlots * VPL * 32 * (16 + Row<WT>::kVecBytes) + kSlots * 4;
+  const uint32_t nw_p = warps_for(pw_p, 8), nw_u = warps_for(pw_u, 4);
+  static bool init = false;
+  if (!init) {
+    set_smem(k_range_partials<VPL>, nw_p * pw_p);
+    set_smem(k_update_ring<WT, VPL>, nw_u * pw_u);
+    init = true;
+  }
+  if (a.n >= 2 * kC) {
+    k_range_partials<VPL><<<grid_units(a.n / kC, nw_p, 148 * 16), nw_p * 32, nw_p * pw_p, st>>>(a);
+    S2D_LAUNCH_CHECK();
+  }
+  if (a.n >= 2ull * kC * kP) {
+    k_group_partials<VPL><<<grid_units(a.n / (kC * kP), 8, 148 * 8), 256, 0, st>>>(a);
+    S2D_LAUNCH_CHECK();
+  }
+  k_update_ring<WT, VPL><<<grid_units((a.n + kC - 1) / kC, nw_u, 148 * 64), nw_u * 32, nw_u * pw_u, st>>>(a);
+  S2D_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+size_t stream_partial_bytes(uint64_t n, uint32_t max_dim) {
+  return ((n / kC + 2) + (n / (kC * kP) + 2)) * (uint64_t)max_dim * sizeof(double);
+}
+
+void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st) {
+  if ((uint64_t)a.n_req * a.B * a.F == 0) return;
+  const int d4 = max_dim / 4;
+  if (bf16) {
+    if (d4 <= 32) lookup_launch<__nv_bfloat16, 1>(a, st);
+    else if (d4 <= 64) lookup_launch<__nv_bfloat16, 2>(a, st);
+    else lookup_launch<__nv_bfloat16, 4>(a, st);
+  } else {
+    if (d4 <= 32) lookup_launch<float, 1>(a, st);
+    else if (d4 <= 64) lookup_launch<float, 2>(a, st);
+    else lookup_launch<float, 4>(a, st);
+  }
+}
+
+void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st) {
+  S2D_CUDA(cudaMemsetAsync(a.counters, 0, 4 * sizeof(uint32_t), st));
+  if (a.n == 0) return;
+  const uint32_t d4 = a.max_d4;
+  if (bf16) {
+    if (d4 <= 32) update_launch<__nv_bfloat16, 1>(a, st);
+    else if (d4 <= 64) update_launch<__nv_bfloat16, 2>(a, st);
+    else update_launch<__nv_bfloat16, 4>(a, st);
+  } else {
+    if (d4 <= 32) update_launch<float, 1>(a, st);
+    else if (d4 <= 64) update_launch<float, 2>(a, st);
+    else update_launch<float, 4>(a, st);
+  }
+}
+
+}  // namespace s2d
