@@ -1,0 +1,146 @@
+"""Multi-GPU parity of the 2D step, run under torchrun (one process per GPU):
+
+    python -m torch.distributed.run --nproc-per-node T --master-addr 127.0.0.1 \
+        --master-port 29531 tests/mp_parity.py --groups M [--strategy row-wise]
+
+Every rank runs the sm_100a step through the C ABI with NCCL between ranks.
+Rank 0 replays the whole T-rank mesh with the CPU oracle on identical inputs
+and checks, bit for bit: every rank's pooled output of every step, the wire
+layouts of the last step on every rank (demand lengths and ids received,
+pooled partials sent, gradient payload sent, unique rows updated), and every
+rank's shard of its group's replica (weights + moments) at the end.
+torch.distributed (gloo) only carries the NCCL bootstrap id and the results.
+"""
+import argparse
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--groups", type=int, default=1)
+    ap.add_argument("--strategy", default="row-wise")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--sync-interval", type=int, default=1)
+    ap.add_argument("--sgd", action="store_true")
+    ap.add_argument("--batch", type=int, default=48)
+    args = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_03854_b200 as s2d
+    from cases import make_batch, upstream
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    M = args.groups
+    N = world // M
+    rows = np.array([300, 41, 7, 1000, 128], np.uint32)
+    dims = np.array([64, 64, 64, 64, 64], np.uint32)
+    F, B = len(rows), args.batch
+    eta, c = 0.1, float(M)
+    profiles = [(f, int(rows[f]) * int(dims[f]) * 4, float(10 - f), int(rows[f])) for f in range(F)]
+    plan = s2d.plan_greedy(profiles, N, args.strategy)
+    nid = [s2d.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(nid, src=0)
+    tables = [s2d.TableConfig(int(rows[f]), int(dims[f])) for f in range(F)]
+    opt = s2d.OptimizerConfig(eta=eta, eps=1e-8, c=c, variant="sgd" if args.sgd else "rowwise-adagrad")
+    eng = s2d.Sparse2DEmbedding(tables, s2d.Topology(world, M), rank=rank, device=local, plan=plan, optimizer=opt,
+                                nccl_id=nid[0])
+    eng.init_tables(31)
+
+    def inputs(step, r):
+        rng = np.random.default_rng([step, r, 77])
+        lengths, ids = make_batch(rng, rows, B, max_len=9, zipf=1.1)
+        return lengths, ids, upstream(rng, B, int(dims.sum()))
+
+    pooled_mine, layouts = [], None
+    for step in range(args.steps):
+        lengths, ids, up = inputs(step, rank)
+        pooled_mine.append(eng.forward(lengths, ids).copy())
+        eng.backward_update(up)
+        if M > 1 and (step + 1) % args.sync_interval == 0:
+            eng.sync_replicas()
+        if step == args.steps - 1:
+            layouts = {k: eng.debug(k) for k in (0, 1, 2, 3, 4, 5)}
+    shard = {}
+    for f in range(F):
+        lo, hi = eng.owned_range(f)
+        if hi > lo:
+            shard[f] = (lo, hi) + eng.read_rows(f, lo, hi)
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object((pooled_mine, layouts, shard), gathered, dst=0)
+    eng.close()
+    if rank != 0:
+        dist.barrier()
+        return
+
+    from oracle import MeshSpec, MeshState, Oracle
+
+    port = Oracle("port")
+    plan_arr = np.array([[e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]] for e in plan], np.uint32)
+    spec = MeshSpec(rows=rows, dims=dims, plan=plan_arr, T=world, M=M, B=B, eta=eta, c=c, sgd=args.sgd)
+    st = MeshState.init(port, spec, 31)
+    st_prev = ([w.copy() for w in st.ws], [v.copy() for v in st.vs])
+    fails = []
+    for step in range(args.steps):
+        ins = [inputs(step, r) for r in range(world)]
+        L = [x[0] for x in ins]
+        I = [x[1] for x in ins]
+        U = [x[2] for x in ins]
+        want = st.step(port, L, I, U, do_sync=(M > 1 and (step + 1) % args.sync_interval == 0))
+        for r in range(world):
+            got = gathered[r][0][step]
+            if not np.array_equal(got.view(np.uint32), want[r].view(np.uint32)):
+                fails.append(f"pooled step {step} rank {r}: max|d|={np.max(np.abs(got - want[r]))}")
+        if step == args.steps - 1:
+            # wire layouts of the last step, per MP group (oracle dump on a copy)
+            for g in range(M):
+                sl = slice(g * N, (g + 1) * N)
+                w0, v0 = st_prev[0][g].copy(), st_prev[1][g].copy()
+                _, dump = port.group_step(spec, L[sl], I[sl], U[sl], w0, v0, None, want_dump=True)
+                for l in range(N):
+                    r = g * N + l
+                    lay = gathered[r][1]
+                    if N > 1:
+                        if not np.array_equal(lay[0], dump.dem_len[l].ravel()):
+                            fails.append(f"demand lengths rank {r}")
+                        if not np.array_equal(lay[1], dump.dem_ids[l]):
+                            fails.append(f"demand ids rank {r}")
+                        if not np.array_equal(lay[2].view(np.uint32), np.concatenate(dump.part[l]).view(np.uint32)):
+                            fails.append(f"partial payload rank {r}")
+                        if not np.array_equal(lay[3].view(np.uint32), np.concatenate(dump.grad[l]).view(np.uint32)):
+                            fails.append(f"grad payload rank {r}")
+                        if not np.array_equal(lay[4], dump.mask[l]):
+                            fails.append(f"owner mask rank {r}")
+        st_prev = ([w.copy() for w in st.ws], [v.copy() for v in st.vs])
+    woff, voff = spec.woff(), spec.voff()
+    for r in range(world):
+        g = r // N
+        for f, (lo, hi, w, v) in gathered[r][2].items():
+            D = int(dims[f])
+            ww = st.ws[g][woff[f] + lo * D: woff[f] + hi * D].reshape(hi - lo, D)
+            vv = st.vs[g][voff[f] + lo: voff[f] + hi]
+            if not np.array_equal(w.view(np.uint32), ww.view(np.uint32)):
+                fails.append(f"weights rank {r} table {f}: max|d|={np.max(np.abs(w - ww))}")
+            if not np.array_equal(v.view(np.uint32), vv.view(np.uint32)):
+                fails.append(f"moments rank {r} table {f}")
+    if fails:
+        print("MP PARITY FAIL", world, M, args.strategy, *fails[:20], sep="\n  ")
+        dist.barrier()
+        sys.exit(1)
+    print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd}")
+    dist.barrier()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,123 @@
+"""CPU: the C-ABI library loads and exports every symbol include/*.h
+declares; host-side planning keeps the reference semantics and error
+behaviour (test_planner.cpp, test_topology.cpp, tests/python/test_smoke.py);
+device entry points fail loudly (no CPU fallback) when there is no GPU."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "sparse2d_b200.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*|uint64_t)\s+(s2d_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol():
+    from paper_2508_03854_b200 import _lib
+
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(syms) == set(_lib.SIGNATURES), "ctypes table and header drifted"
+    assert b"sm_100a" in lib.s2d_version()
+
+
+def test_topology_mapping():
+    import paper_2508_03854_b200 as s2d
+
+    t = s2d.Topology(8, 2)  # test_topology.cpp:22-31, test_smoke.py:12-18
+    assert t.ranks_per_group == 4 and t.group_of(5) == 1 and t.local_of(5) == 1 and t.rank_of(1, 1) == 5
+    with pytest.raises(ValueError):
+        s2d.Topology(8, 3)
+    with pytest.raises(ValueError):
+        s2d.Topology(0, 1)
+
+
+def test_plan_greedy_matches_oracle(port):
+    import paper_2508_03854_b200 as s2d
+
+    rng = np.random.default_rng(3)
+    for trial in range(30):
+        n_t = int(rng.integers(1, 12))
+        n = int(rng.integers(1, 9))
+        prof = [(i, int(rng.integers(1, 1e6)), float(rng.integers(0, 20)), int(rng.integers(1, 50)))
+                for i in range(n_t)]
+        for strat in ("table-wise", "row-wise"):
+            got = np.array([[e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]]
+                            for e in s2d.plan_greedy(prof, n, strat)], np.uint32).reshape(-1, 4)
+            want = port.plan_greedy(prof, n, strat)
+            assert np.array_equal(got, want), (trial, strat)
+            s2d.validate_plan(s2d.plan_greedy(prof, n, strat), n, prof)
+
+
+def test_plan_known_answers_and_errors():
+    import paper_2508_03854_b200 as s2d
+
+    plan = s2d.plan_greedy([(0, 640, 7.0, 10), (1, 640, 5.0, 10), (2, 640, 4.0, 10), (3, 640, 3.0, 10),
+                            (4, 640, 1.0, 10)], 2, "table-wise")  # test_smoke.py:47-53
+    owners = {e["table_id"]: e["local_rank"] for e in plan}
+    assert owners == {0: 0, 1: 1, 2: 1, 3: 0, 4: 1}
+    assert s2d.imbalance_ratio([10.0, 10.0, 10.0, 50.0]) == 2.5
+    with pytest.raises(ValueError):
+        s2d.imbalance_ratio([])
+    with pytest.raises(ValueError):
+        s2d.imbalance_ratio([0.0, 0.0])
+    with pytest.raises(ValueError):
+        s2d.plan_greedy([(0, 1, 1.0, 10)], 0)
+    with pytest.raises(ValueError):
+        s2d.plan_greedy([(0, 1, 1.0, 10)], 2, "column-wise")
+    bad = [{"table_id": 0, "row_lo": 0, "row_hi": 5, "local_rank": 0}]
+    with pytest.raises(ValueError):  # rows [5,10) uncovered (planner.cpp:91-123)
+        s2d.validate_plan(bad, 2, [(0, 40, 1.0, 10)])
+    assert s2d.owner_of(plan, 3, 7) == 0
+    with pytest.raises(IndexError):
+        s2d.owner_of(plan, 3, 10)
+
+
+def test_effective_lr_and_validation():
+    import paper_2508_03854_b200 as s2d
+
+    assert abs(s2d.effective_lr(4.0, eta=0.1, eps=1e-8, c=4.0) - 0.1) < 1e-6  # test_smoke.py:42-43
+    assert s2d.effective_lr(0.0, eta=0.1, eps=1e-8, c=1.0) == pytest.approx(0.1 / 1e-8)
+    prev = 0.0
+    for c in (0.5, 1.0, 2.0, 4.0, 8.0):  # strictly increasing in c (test_optimizer.cpp:106-112)
+        lr = s2d.effective_lr(2.0, eta=0.1, eps=1e-8, c=c)
+        assert lr > prev
+        prev = lr
+    for bad in (dict(eta=0.0), dict(eps=-1.0), dict(c=-1.0), dict(eta=float("nan"))):
+        with pytest.raises(ValueError):
+            s2d.effective_lr(1.0, **{**dict(eta=0.1, eps=1e-8, c=1.0), **bad})
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2508_03854_b200 as s2d
+
+    with pytest.raises(Exception):
+        s2d.Sparse2DEmbedding([s2d.TableConfig(10, 8)], s2d.Topology(1, 1))
+    with pytest.raises(Exception):
+        s2d.adagrad_row_step([1.0, 1.0], 0.0, [2.0, 0.0])
+
+
+def test_c_abi_error_codes_and_messages():
+    from paper_2508_03854_b200 import _lib
+
+    lib = _lib.load()
+    t = _lib.TopologyC()
+    assert lib.s2d_topology_init(8, 3, C.byref(t)) == _lib.S2D_EINVAL
+    assert b"must divide" in lib.s2d_last_error()
+    assert lib.s2d_topology_init(8, 2, C.byref(t)) == _lib.S2D_OK and t.ranks_per_group == 4
+    out = C.c_double(0)
+    cfg = _lib.OptimizerConfigC(0.1, 1e-8, 0.0, 0)
+    assert lib.s2d_effective_lr(1.0, C.byref(cfg), C.byref(out)) == _lib.S2D_EINVAL
+    assert b"optimizer.c" in lib.s2d_last_error()

@@ -1,0 +1,42 @@
+"""Multi-GPU parity (tests/mp_parity.py under torchrun); needs >= 2 GPUs."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpu():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+CASES = [
+    (2, 1, "row-wise", []),
+    (2, 1, "table-wise", []),
+    (2, 2, "row-wise", []),
+    (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4"]),
+    (4, 1, "table-wise", ["--sgd"]),
+    (4, 4, "table-wise", []),
+]
+
+
+@pytest.mark.parametrize("T,M,strategy,extra", CASES)
+def test_mesh_parity(T, M, strategy, extra):
+    if _ngpu() < T:
+        pytest.skip(f"needs {T} GPUs")
+    port = 29500 + 7 * T + M + (0 if strategy == "row-wise" else 50)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(T), "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_parity.py"), "--groups",
+           str(M), "--strategy", strategy, *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MP PARITY OK" in r.stdout

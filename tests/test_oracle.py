@@ -1,0 +1,190 @@
+"""CPU: pins the oracle (oracle/s2d_oracle.c) to the reference.
+
+(1) the reference's own known-answer tests, restated (test_embedding.cpp,
+test_optimizer.cpp, test_planner.cpp); (2) golden vectors produced by the
+compiled reference (tests/golden/make_golden.py); (3) when oracle/_ref is
+built, randomized port-vs-reference agreement."""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+# ---- (1) reference known answers ---------------------------------------------
+
+def test_pooling_known_answers(port):
+    w = np.array([1, 0, 0, 2], np.float32)  # r0=(1,0), r1=(0,2): test_embedding.cpp:26-86
+    assert list(port.pool_ids(w, 2, [(0, 2)], [1])) == [0.0, 2.0]
+    assert list(port.pool_ids(w, 2, [(0, 2)], [1, 1])) == [0.0, 4.0]
+    assert list(port.pool_ids(w, 2, [(0, 2)], [0, 1])) == [1.0, 2.0]
+    assert list(port.pool_ids(w, 2, [(0, 2)], [])) == [0.0, 0.0]
+    with pytest.raises(IndexError):
+        port.pool_ids(w, 2, [(0, 2)], [7])
+
+
+def test_pooling_linearity_and_sharding(port):
+    t = port.init_rows(0, 40, 0, 40, 8, 5).ravel()
+    ids = [1, 5, 5, 17, 39]
+    a = port.pool_ids(t, 8, [(0, 40)], ids)
+    b = port.pool_ids(2 * t, 8, [(0, 40)], ids)
+    assert np.array_equal(b, 2 * a)  # test_embedding.cpp:88-98 (x2 exact)
+    t = port.init_rows(0, 100, 0, 100, 4, 19).ravel()
+    ids = [0, 29, 30, 70, 71, 99, 29]
+    whole = port.pool_ids(t, 4, [(0, 100)], ids)
+    split = port.pool_ids(t, 4, [(0, 30), (30, 71), (71, 100)], ids)
+    assert np.allclose(whole, split, rtol=1e-6)  # 110-121
+
+
+def test_adagrad_known_answers(port):
+    o = port.adagrad_row_step([1, 1], 0.0, [2, 0], eta=0.1, eps=1e-8, c=4.0)  # test_optimizer.cpp:57-67
+    assert abs(o["v"] - 4.0) < 1e-6 and abs(o["effective_lr"] - 0.1) < 1e-6
+    assert abs(o["w"][0] - 0.8) < 1e-6 and o["w"][1] == 1.0
+    o = port.adagrad_row_step([1, 1], 0.0, [2, 0], eta=0.1, eps=1e-8, c=1.0)  # 69-77
+    assert abs(o["effective_lr"] - 0.05) < 1e-6 and abs(o["w"][0] - 0.9) < 1e-6
+    o = port.adagrad_row_step([0.25, -0.5], 3.0, [0, 0], c=1.0)  # 79-87
+    assert o["v"] == np.float32(3.0) and list(o["w"]) == [0.25, -0.5]
+    with pytest.raises(ValueError):  # 89-94
+        port.adagrad_row_step([0.0], 0.0, [float("nan")])
+    assert port.effective_lr(4.0, eta=0.1, eps=1e-8, c=4.0) == pytest.approx(0.1, rel=1e-6)
+
+
+def test_planner_known_answers(port):
+    plan = port.plan_greedy([(i, 6400, float(x), 100) for i, x in enumerate([7, 5, 4, 3, 1])], 2)
+    assert [int(e[3]) for e in plan] == [0, 1, 1, 0, 1]  # test_planner.cpp:60-79
+    plan = port.plan_greedy([(0, 640, 5.0, 10), (1, 640, 2.0, 10)], 3, "row-wise")
+    t0 = [tuple(int(x) for x in e) for e in plan if e[0] == 0]
+    assert t0 == [(0, 0, 3, 0), (0, 3, 6, 1), (0, 6, 10, 2)]  # 81-91
+
+
+# ---- (2) golden vectors from the compiled reference ---------------------------
+
+def test_known_golden(port):
+    g = load("known")
+    w = np.array([1, 0, 0, 2], np.float32)
+    for k, ids in {"single": [1], "dup": [1, 1], "two": [0, 1], "empty": []}.items():
+        assert np.array_equal(bits(port.pool_ids(w, 2, [(0, 2)], ids)), bits(g[f"pool_{k}"]))
+    t = port.init_rows(0, 100, 0, 100, 4, 19).ravel()
+    ids = [0, 29, 30, 70, 71, 99, 29]
+    assert np.array_equal(bits(port.pool_ids(t, 4, [(0, 100)], ids)), bits(g["shard_whole"]))
+    assert np.array_equal(bits(port.pool_ids(t, 4, [(0, 30), (30, 71), (71, 100)], ids)), bits(g["shard_split"]))
+    for c in (4, 1):
+        o = port.adagrad_row_step([1.0, 1.0], 0.0, [2.0, 0.0], eta=0.1, eps=1e-8, c=float(c))
+        assert np.array_equal(bits(o["w"]), bits(g[f"adagrad_c{c}_w"]))
+        assert np.float32(o["v"]) == g[f"adagrad_c{c}_v"]
+        assert o["effective_lr"] == g[f"adagrad_c{c}_lr"]
+    for i in range(64):
+        o = port.adagrad_row_step(g["rows_w"][i], g["rows_v"][i], g["rows_g"][i], eta=0.1, eps=1e-8, c=3.0)
+        assert np.array_equal(bits(o["w"]), bits(g["rows_w_out"][i]))
+        assert np.float32(o["v"]) == g["rows_v_out"][i]
+    assert np.array_equal(port.plan_greedy([(i, 6400, float(x), 100) for i, x in enumerate([7, 5, 4, 3, 1])], 2),
+                          g["lpt_plan"])
+    assert np.array_equal(port.plan_greedy([(0, 640, 5.0, 10), (1, 640, 2.0, 10)], 3, "row-wise"),
+                          g["rowwise_plan"])
+
+
+def test_init_golden(port):
+    g = load("init")
+    assert np.array_equal(bits(port.init_rows(3, 100, 0, 100, 16, 11)), bits(g["t3"]))
+    assert np.array_equal(bits(port.init_rows(0, 1000, 0, 1000, 64, 2)), bits(g["t0"]))
+    assert np.array_equal(bits(port.init_rows(7, 5, 0, 5, 128, 123456789)), bits(g["t7"]))
+
+
+@pytest.mark.parametrize("name", ["mesh_8x1_row", "mesh_4x2_row", "mesh_2x4_table", "mesh_2x2_sgd_sync3"])
+def test_mesh_golden(port, name):
+    from oracle import MeshSpec, MeshState
+
+    g = load(name)
+    T, M, B = int(g["T"]), int(g["M"]), int(g["B"])
+    spec = MeshSpec(rows=g["rows"], dims=g["dims"], plan=g["plan"], T=T, M=M, B=B, eta=float(g["eta"]),
+                    c=float(g["c"]), sgd=bool(g["sgd"]))
+    st = MeshState.init(port, spec, int(g["seed"]))
+    F = spec.F
+    for step in range(int(g["steps"])):
+        ids = [g[f"s{step}_r{r}_ids"] for r in range(T)]
+        lengths = [np.full(B * F, len(ids[r]) // (B * F), np.uint32) for r in range(T)]
+        up = [g[f"s{step}_r{r}_up"] for r in range(T)]
+        pooled = st.step(port, lengths, ids, up, do_sync=(M > 1 and (step + 1) % int(g["sync_interval"]) == 0))
+        for r in range(T):
+            assert np.array_equal(bits(pooled[r]), bits(g[f"s{step}_r{r}_pooled"])), (step, r)
+    for gg in range(M):
+        assert np.array_equal(bits(st.ws[gg]), bits(g[f"w{gg}"]))
+        assert np.array_equal(bits(st.vs[gg]), bits(g[f"v{gg}"]))
+    if M > 1 and int(g["sync_interval"]) == 1:  # replica consensus (test_trainer.cpp:141-151)
+        for gg in range(1, M):
+            assert np.array_equal(bits(st.ws[gg]), bits(st.ws[0]))
+
+
+def test_mixed_golden(port):
+    from oracle import MeshSpec, MeshState, row_wise_plan
+
+    g = load("mixed")
+    spec = MeshSpec(rows=g["rows"], dims=g["dims"], plan=row_wise_plan(g["rows"], 2), T=2, M=1, B=16, eta=0.1,
+                    c=2.0)
+    st = MeshState.init(port, spec, 4)
+    for step in range(3):
+        L = [g[f"s{step}_r{r}_len"] for r in range(2)]
+        I = [g[f"s{step}_r{r}_ids"] for r in range(2)]
+        U = [g[f"s{step}_r{r}_up"] for r in range(2)]
+        pooled = st.step(port, L, I, U, do_sync=False)
+        for r in range(2):
+            assert np.array_equal(bits(pooled[r]), bits(g[f"s{step}_r{r}_pooled"]))
+    assert np.array_equal(bits(st.ws[0]), bits(g["w"]))
+    assert np.array_equal(bits(st.vs[0]), bits(g["v"]))
+
+
+@pytest.mark.parametrize("c", [1, 4])
+def test_cfg1_golden(port, c):
+    """BASELINE config 1 shapes: 2 steps of 8 x 100K x 64, B=512, L=20."""
+    from oracle import MeshSpec, MeshState, row_wise_plan
+
+    g = load(f"cfg1_c{c}")
+    rows = np.full(8, 100_000, np.uint32)
+    spec = MeshSpec(rows=rows, dims=np.full(8, 64, np.uint32), plan=row_wise_plan(rows, 1), T=1, M=1, B=512,
+                    eta=0.1, c=float(c))
+    st = MeshState.init(port, spec, 2)
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for step in range(2):
+        up = (1e-3 * np.random.default_rng([step, 99]).standard_normal((512, 512))).astype(np.float32)
+        pooled = st.step(port, [np.full(512 * 8, 20, np.uint32)], [g[f"s{step}_ids"]], [up], do_sync=False)[0]
+        assert sha(pooled) == str(g[f"s{step}_pooled_sha"])
+    assert sha(st.ws[0]) == str(g["w_sha"])
+    assert sha(st.vs[0]) == str(g["v_sha"])
+
+
+# ---- (3) port vs compiled reference on random meshes --------------------------
+
+@pytest.mark.parametrize("T,M,strategy,sgd", [(8, 1, "row-wise", False), (8, 2, "table-wise", False),
+                                              (8, 4, "row-wise", True), (6, 3, "row-wise", False)])
+def test_port_matches_reference(port, ref, T, M, strategy, sgd):
+    from cases import make_batch
+    from oracle import MeshSpec, MeshState, row_wise_plan
+
+    rng = np.random.default_rng(T * 10 + M)
+    rows = np.array([64, 33, 7, 100, 1], np.uint32)
+    dims = np.array([8, 4, 12, 8, 4], np.uint32)
+    N = T // M
+    plan = row_wise_plan(rows, N) if strategy == "row-wise" else port.plan_greedy(
+        [(f, 0, float(9 - f), int(rows[f])) for f in range(5)], N)
+    spec = MeshSpec(rows=rows, dims=dims, plan=plan, T=T, M=M, B=5, eta=0.05, c=float(M), sgd=sgd)
+    a, b = MeshState.init(port, spec, 3), MeshState.init(ref, spec, 3)
+    for step in range(4):
+        batches = [make_batch(rng, rows, 5, max_len=6) for _ in range(T)]
+        L = [x[0] for x in batches]
+        I = [x[1] for x in batches]
+        U = [(1e-2 * rng.standard_normal((5, int(dims.sum())))).astype(np.float32) for _ in range(T)]
+        pa = a.step(port, L, I, U, True)
+        pb = b.step(ref, L, I, U, True, threads=3)
+        for x, y in zip(pa, pb):
+            assert np.array_equal(bits(x), bits(y))
+    for g in range(M):
+        assert np.array_equal(bits(a.ws[g]), bits(b.ws[g]))
+        assert np.array_equal(bits(a.vs[g]), bits(b.vs[g]))
