@@ -279,7 +279,7 @@ def run_ours(args):
 
     def step(k):
         l, i, u = dev[k % NB]
-        eng.forward(l, i, pooled, batch=w.batch)
+        eng.forward(l, i, "engine", batch=w.batch)  # zero-copy output (engine buffer)
         eng.backward_update(u)
         if m > 1:
             eng.sync_replicas()

@@ -190,6 +190,14 @@ int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* ro
 int s2d_lookup_forward(s2d_ctx* ctx, uint32_t batch, const uint32_t* lengths, const uint32_t* ids,
                        uint64_t nnz, float* pooled, int32_t mem);
 
+/* Zero-copy output: with mem == S2D_DEVICE and pooled == NULL,
+ * s2d_lookup_forward writes into this engine-owned buffer ([batch][sum dim]
+ * fp32, valid until the next forward), which the other ranks of the MP group
+ * map: owners of single-owner tables store their pooled rows straight into
+ * it over NVLink and the requester-side combine skips them.  *out = NULL
+ * before the first forward. */
+int s2d_pooled_buffer(s2d_ctx* ctx, float** out);
+
 /* Backward + fused optimizer for the batch of the last s2d_lookup_forward:
  * upstream[batch][sum_f dim_f] fp32 per-sample gradients (not batch-divided,
  * src/trainer.cpp:424-427).  Runs the gradient all-to-all, K3 radix-sort

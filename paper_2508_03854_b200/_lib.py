@@ -78,6 +78,7 @@ SIGNATURES = {
     "s2d_shard_range": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "s2d_lookup_forward": (C.c_int, [_P, C.c_uint32, _P, _P, C.c_uint64, _P, C.c_int32]),
     "s2d_backward_update": (C.c_int, [_P, _P, C.c_int32]),
+    "s2d_pooled_buffer": (C.c_int, [_P, C.POINTER(C.c_void_p)]),
     "s2d_replica_sync": (C.c_int, [_P]),
     "s2d_synchronize": (C.c_int, [_P]),
     "s2d_get_step_stats": (C.c_int, [_P, C.POINTER(StepStats)]),

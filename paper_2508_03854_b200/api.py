@@ -304,6 +304,14 @@ class Sparse2DEmbedding:
             batch = nb // self.F
         if lk != ik:
             raise ValueError("lengths and ids must both be host or both be device buffers")
+        if isinstance(pooled, str) and pooled == "engine":
+            # zero-copy: results land in the engine-owned, peer-mapped buffer
+            # (pooled_buffer_ptr()); owners store single-owner tables' rows there
+            if lk != L.S2D_DEVICE:
+                raise ValueError("engine output needs device inputs")
+            L.check(self.lib.s2d_lookup_forward(self._ctx, batch, lp, ip, nnz, None, lk))
+            self._batch = batch
+            return None
         if pooled is None:
             if lk == L.S2D_DEVICE:
                 import torch
@@ -322,6 +330,13 @@ class Sparse2DEmbedding:
         the batch of the last forward.  upstream: [B][sum dims] fp32."""
         up, uk, _ua = _ptr_kind(upstream, np.float32)
         L.check(self.lib.s2d_backward_update(self._ctx, up, uk))
+
+    def pooled_buffer_ptr(self) -> int:
+        """Device address of the engine-owned pooled output (see forward(...,
+        pooled="engine")); [batch][sum dims] fp32."""
+        p = C.c_void_p()
+        L.check(self.lib.s2d_pooled_buffer(self._ctx, C.byref(p)))
+        return p.value or 0
 
     def sync_replicas(self):
         """Weight + moment mean of dirty rows across the DP group
@@ -354,7 +369,7 @@ class Sparse2DEmbedding:
         """Wire buffers of the last step (see s2d_debug_read)."""
         n = C.c_uint64(0)
         L.check(self.lib.s2d_debug_read(self._ctx, which, None, 0, C.byref(n)))
-        dt = np.float32 if which in (2, 3) else np.uint32
+        dt = np.float32 if which in (2, 3, 6) else np.uint32
         out = np.zeros(n.value, dt)
         L.check(self.lib.s2d_debug_read(self._ctx, which, out.ctypes.data, n.value, C.byref(n)))
         return out

@@ -178,6 +178,13 @@ int s2d_lookup_forward(s2d_ctx* ctx, uint32_t batch, const uint32_t* lengths, co
   return guarded([&] { as_ctx(ctx)->lookup_forward(batch, lengths, ids, nnz, pooled, mem); });
 }
 
+int s2d_pooled_buffer(s2d_ctx* ctx, float** out) {
+  return guarded([&] {
+    if (!out) throw Error(S2D_EINVAL, "null output");
+    *out = as_ctx(ctx)->pooled_buffer();
+  });
+}
+
 int s2d_backward_update(s2d_ctx* ctx, const float* upstream, int32_t mem) {
   return guarded([&] { as_ctx(ctx)->backward_update(upstream, mem); });
 }

@@ -38,7 +38,14 @@ void count_launch();
   } while (0)
 
 // Device fault bits (checked once per step, SURVEY.md 5 failure detection).
-enum : uint32_t { kErrIdRange = 1u, kErrNonfinite = 2u };
+enum : uint32_t { kErrIdRange = 1u, kErrNonfinite = 2u, kErrPeerTimeout = 4u };
+
+constexpr int kMaxPeers = 32;
+// Per-peer device pointers of one IPC-shared buffer (index = local rank in
+// the MP group; the own entry is the local buffer).
+struct PeerPtrs {
+  void* p[kMaxPeers];
+};
 
 // Per-feature metadata visible to every kernel.
 struct FeatDev {
@@ -50,6 +57,7 @@ struct FeatDev {
   uint32_t coff;    // column offset inside a [sum_f D_f] pooled/upstream row
   uint32_t rbeg;    // owner ranges of this table: ranges[rbeg, rend)
   uint32_t rend;
+  uint32_t single;  // the plan gives the table one owner: partial == pooled row
 };
 
 // Owner range of a table inside the MP group (sorted by lo per table).
@@ -103,6 +111,15 @@ struct LookupArgs {
   int direct;                  // N == 1: write pooled rows (zero for empty bags)
   int emit_keys;
   uint32_t uni_d4;             // dim/4 shared by every table (0: mixed dims)
+  // non-direct: the partial of a bag of requester n goes to
+  // peer_out.p[n] + peer_adj[n] + eoff[bag] (requester n's receive buffer,
+  // over NVLink); the sort vals stay local (eoff[bag] / 4)
+  PeerPtrs peer_out;
+  int64_t peer_adj[kMaxPeers];
+  // zero-copy output: bags of single-owner tables are stored as final pooled
+  // rows straight into requester n's pooled buffer peer_pooled.p[n]
+  PeerPtrs peer_pooled;
+  int use_peer_pooled;
 };
 
 struct CombineArgs {
@@ -112,6 +129,7 @@ struct CombineArgs {
   const uint64_t* eoff;        // [N*B*F + 1] float offsets into the per-owner blocks
   const float* recv;           // partials received, concatenated by owner
   float* pooled;               // [B][sumD]
+  int skip_single;             // single-owner bags were written by their owners
 };
 void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st);
 
@@ -121,7 +139,9 @@ struct GradGatherArgs {
   const uint32_t* cnt;
   const uint64_t* eoff;
   const float* upstream;       // [B][sumD]
-  float* send;                 // concatenated by owner
+  // gradient row of bag b for owner o -> peer_dst.p[o] + peer_adj[o] + eoff[o*BF+b]
+  PeerPtrs peer_dst;
+  int64_t peer_adj[kMaxPeers];
 };
 void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st);
 
@@ -134,11 +154,23 @@ struct BucketArgs {
   const uint32_t* ids;
   uint32_t* cnt;               // [N][BF]
   const uint32_t* send_off;    // [N*BF+1] (permute pass)
-  uint32_t* send_ids;          // (permute pass)
   uint32_t* err;
+  uint32_t me;                 // local rank in the MP group
+  // count pass: cnt[o][b] is also stored into owner o's receive lengths
+  // peer_len.p[o] + me*BF + b; permute pass: id k of bag b owned by o goes
+  // to peer_ids.p[o] + ids_adj[o] + send_off[o*BF+b] + k
+  PeerPtrs peer_len;
+  PeerPtrs peer_ids;
+  int64_t ids_adj[kMaxPeers];
 };
 void launch_bucket_count(const BucketArgs& a, cudaStream_t st);
 void launch_bucket_permute(const BucketArgs& a, cudaStream_t st);
+
+// peer primitives (k_peer.cu)
+void launch_peer_barrier(const PeerPtrs& flags, uint64_t* my_flags, uint32_t me, uint32_t n, uint64_t epoch,
+                         uint32_t* err, cudaStream_t st);
+void launch_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF, uint32_t batch,
+                           const PeerPtrs& xcnt, uint32_t me, cudaStream_t st);
 
 // update kernels (k_update.cu)
 // streaming kernels (k_stream.cu): K2 lookup and K3b+K4 segment-reduce +

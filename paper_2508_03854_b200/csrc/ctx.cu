@@ -94,15 +94,6 @@ void Ctx::phase_times(double* ms, uint32_t* counts) {
 
 namespace {
 
-__global__ void k_gather_bounds(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF,
-                                uint64_t* out) {
-  const uint32_t o = threadIdx.x;
-  if (o <= N) {
-    out[o] = send_off[(uint64_t)o * BF];
-    out[N + 1 + o] = eoff[(uint64_t)o * BF];
-  }
-}
-
 int bit_width(uint32_t x) {
   int b = 0;
   while (x) {
@@ -116,6 +107,9 @@ int bit_width(uint32_t x) {
 
 Ctx::~Ctx() {
   if (device >= 0) cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (PeerBuf* pb : {&p_flags, &p_xcnt, &p_len, &p_ids, &p_part, &p_grad, &p_pooled})
+    for (void* q : pb->opened) cudaIpcCloseMemHandle(q);
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (dp) ncclCommDestroy(dp);
   if (mp) ncclCommDestroy(mp);
@@ -203,6 +197,7 @@ void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_en
       }
     }
     feats[f].rend = (uint32_t)ranges.size();
+    feats[f].single = mine.size() == 1 ? 1u : 0u;
     feats[f].vbase = n_slots;
     feats[f].wbase = n_weight_elems;
     const uint64_t own = feats[f].hi - feats[f].lo;
@@ -252,6 +247,10 @@ void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_en
     S2D_CUDA(cudaMemsetAsync(dirty.p, 0, n_slots, stream));
   }
   S2D_CUDA(cudaStreamSynchronize(stream));
+  if (N > 1) {  // collective: barrier flags and the count matrix
+    peer_alloc(p_flags, (size_t)N * 8);
+    peer_alloc(p_xcnt, (size_t)N * N * 3 * 8);
+  }
   fwd_done = false;
 }
 
@@ -328,6 +327,7 @@ void Ctx::check_faults() {
   stats.error_flags = e;
   if (e & kErrIdRange) throw Error(S2D_ERANGE, "lookup id outside the table's rows / shard ranges");
   if (e & kErrNonfinite) throw Error(S2D_ENONFINITE, "nonfinite row gradient");
+  if (e & kErrPeerTimeout) throw Error(S2D_ENCCL, "peer barrier timed out (a rank of the MP group stopped)");
 }
 
 void Ctx::finish_call() {
@@ -362,15 +362,24 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   const uint32_t* d_len = lengths;
   const uint32_t* d_ids = ids;
   float* d_pooled = pooled;
+  // zero-copy output: pooled == NULL (device mode) selects the engine-owned,
+  // peer-mapped pooled buffer (s2d_pooled_buffer); owners of single-owner
+  // tables then store pooled rows straight into it over NVLink
+  const bool engine_out = (mem == S2D_DEVICE && pooled == nullptr) || mem == S2D_HOST;
+  if (engine_out) {
+    if (N > 1)
+      peer_alloc(p_pooled, (uint64_t)B * sum_dims * 4);
+    else
+      p_pooled_local.ensure((uint64_t)B * sum_dims * 4);
+    d_pooled = N > 1 ? p_pooled.buf.as<float>() : p_pooled_local.as<float>();
+  }
   if (mem == S2D_HOST) {
     in_lengths.ensure(BF * 4);
     in_ids.ensure(std::max<uint64_t>(nnz, 1) * 4);
-    pooled_stage.ensure(BF ? (uint64_t)B * sum_dims * 4 : 16);
     S2D_CUDA(cudaMemcpyAsync(in_lengths.p, lengths, BF * 4, cudaMemcpyHostToDevice, stream));
     if (nnz) S2D_CUDA(cudaMemcpyAsync(in_ids.p, ids, nnz * 4, cudaMemcpyHostToDevice, stream));
     d_len = in_lengths.as<uint32_t>();
     d_ids = in_ids.as<uint32_t>();
-    d_pooled = pooled_stage.as<float>();
   }
   scan_tmp.ensure(scan_tmp_bytes(std::max<uint64_t>((uint64_t)N * BF, nnz) + 1));
   in_off.ensure((BF + 1) * 4);
@@ -404,12 +413,12 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     stats.nnz_owned = nnz;
     stats.entries_owned = BF;
   } else {
-    // K1: bucket by owner
+    // ---- K1 fused with the id all-to-all over NVLink peer memory ----
     phase_begin(kPhBucket);
+    peer_alloc(p_len, (uint64_t)N * BF * 4);  // collective; B is uniform across ranks
     cnt.ensure((uint64_t)N * BF * 4);
     send_off.ensure(((uint64_t)N * BF + 1) * 4);
     eoff_req.ensure(((uint64_t)N * BF + 1) * 8);
-    send_ids.ensure(std::max<uint64_t>(nnz, 1) * 4);
     BucketArgs ba{};
     ba.feats = dfe;
     ba.ranges = d_ranges.as<RangeDev>();
@@ -421,48 +430,29 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     ba.ids = d_ids;
     ba.cnt = cnt.as<uint32_t>();
     ba.send_off = send_off.as<uint32_t>();
-    ba.send_ids = send_ids.as<uint32_t>();
     ba.err = err.as<uint32_t>();
-    launch_bucket_count(ba, stream);
+    ba.me = local;
+    ba.peer_len = ptrs(p_len);
+    launch_bucket_count(ba, stream);  // also stores cnt[o][:] into owner o's receive lengths
     scan_u32_to_u32(cnt.as<uint32_t>(), send_off.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p, scan_tmp.cap);
     scan_nonzero_dim_u64(cnt.as<uint32_t>(), eoff_req.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream, scan_tmp.p,
                          scan_tmp.cap);
-    launch_bucket_permute(ba, stream);
+    launch_publish_counts(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF, B, ptrs(p_xcnt), local, stream);
+    peer_barrier();
+    read_counts();  // count matrix -> offsets; grows the peer buffers collectively
     phase_begin(kPhA2AIds);
-    a2a_counts();
-    // ids + lengths all-to-all inside the MP group
-    recv_lengths.ensure((uint64_t)N * BF * 4);
-    recv_ids.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
-    S2D_NCCL(ncclGroupStart());
-    for (uint32_t p = 0; p < N; ++p) {
-      if (p == local) continue;
-      S2D_NCCL(ncclSend(cnt.as<uint32_t>() + (uint64_t)p * BF, BF, ncclUint32, (int)p, mp, stream));
-      S2D_NCCL(ncclRecv(recv_lengths.as<uint32_t>() + (uint64_t)p * BF, BF, ncclUint32, (int)p, mp, stream));
-      if (nnz_to[p]) S2D_NCCL(ncclSend(send_ids.as<uint32_t>() + ids_base_to[p], nnz_to[p], ncclUint32, (int)p, mp, stream));
-      if (nnz_from[p])
-        S2D_NCCL(ncclRecv(recv_ids.as<uint32_t>() + nnz_base_from[p], nnz_from[p], ncclUint32, (int)p, mp, stream));
-    }
-    S2D_NCCL(ncclGroupEnd());
-    S2D_CUDA(cudaMemcpyAsync(recv_lengths.as<uint32_t>() + (uint64_t)local * BF, cnt.as<uint32_t>() + (uint64_t)local * BF,
-                             BF * 4, cudaMemcpyDeviceToDevice, stream));
-    if (nnz_to[local])
-      S2D_CUDA(cudaMemcpyAsync(recv_ids.as<uint32_t>() + nnz_base_from[local], send_ids.as<uint32_t>() + ids_base_to[local],
-                               nnz_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
-    // owner side: offsets of the received demand, entry offsets of partials
+    ba.peer_ids = ptrs(p_ids);
+    for (uint32_t o = 0; o < N; ++o) ba.ids_adj[o] = (int64_t)ids_base_at_owner[o] - (int64_t)send_bound[o];
+    launch_bucket_permute(ba, stream);  // ids straight into the owners' receive buffers
+    peer_barrier();
+    // ---- owner side: partial pools written into the requesters' buffers ----
     phase_begin(kPhLookup);
     own_idoff.ensure(((uint64_t)N * BF + 1) * 4);
     own_eoff.ensure(((uint64_t)N * BF + 1) * 8);
-    scan_u32_to_u32(recv_lengths.as<uint32_t>(), own_idoff.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p,
+    scan_u32_to_u32(p_len.buf.as<uint32_t>(), own_idoff.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p,
                     scan_tmp.cap);
-    scan_nonzero_dim_u64(recv_lengths.as<uint32_t>(), own_eoff.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream,
+    scan_nonzero_dim_u64(p_len.buf.as<uint32_t>(), own_eoff.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream,
                          scan_tmp.p, scan_tmp.cap);
-    uint64_t ef_own = 0, ef_req = 0;
-    for (uint32_t p = 0; p < N; ++p) {
-      ef_own += ef_from[p];
-      ef_req += ef_to[p];
-    }
-    part_send.ensure(std::max<uint64_t>(ef_own, 4) * 4);
-    part_recv.ensure(std::max<uint64_t>(ef_req, 4) * 4);
     keys_a.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
     vals_a.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
     LookupArgs a{};
@@ -471,11 +461,11 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.B = B;
     a.n_req = N;
     a.sum_dims = sum_dims;
-    a.lengths = recv_lengths.as<uint32_t>();
+    a.lengths = p_len.buf.as<uint32_t>();
     a.id_off = own_idoff.as<uint32_t>();
-    a.ids = recv_ids.as<uint32_t>();
+    a.ids = p_ids.buf.as<uint32_t>();
     a.weights = weights.p;
-    a.out = part_send.as<float>();
+    a.out = nullptr;
     a.eoff = own_eoff.as<uint64_t>();
     a.keys = keys_a.as<uint32_t>();
     a.vals = vals_a.as<uint32_t>();
@@ -483,19 +473,13 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.direct = 0;
     a.emit_keys = 1;
     a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
+    a.peer_out = ptrs(p_part);
+    a.use_peer_pooled = engine_out ? 1 : 0;
+    if (engine_out) a.peer_pooled = ptrs(p_pooled);
+    for (uint32_t n = 0; n < N; ++n) a.peer_adj[n] = (int64_t)part_base_at_req[n] - (int64_t)own_eoff_bound[n];
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
-    // C1: partials back to requesters
     phase_begin(kPhA2ALookup);
-    S2D_NCCL(ncclGroupStart());
-    for (uint32_t p = 0; p < N; ++p) {
-      if (p == local) continue;
-      if (ef_from[p]) S2D_NCCL(ncclSend(part_send.as<float>() + ef_base_from[p], ef_from[p], ncclFloat32, (int)p, mp, stream));
-      if (ef_to[p]) S2D_NCCL(ncclRecv(part_recv.as<float>() + ef_base_to[p], ef_to[p], ncclFloat32, (int)p, mp, stream));
-    }
-    S2D_NCCL(ncclGroupEnd());
-    if (ef_to[local])
-      S2D_CUDA(cudaMemcpyAsync(part_recv.as<float>() + ef_base_to[local], part_send.as<float>() + ef_base_from[local],
-                               ef_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
+    peer_barrier();  // every owner's partials have landed in p_part
     phase_begin(kPhCombine);
     CombineArgs ca{};
     ca.feats = dfe;
@@ -505,17 +489,19 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     ca.sum_dims = sum_dims;
     ca.cnt = cnt.as<uint32_t>();
     ca.eoff = eoff_req.as<uint64_t>();
-    ca.recv = part_recv.as<float>();
+    ca.recv = p_part.buf.as<float>();
     ca.pooled = d_pooled;
+    ca.skip_single = engine_out ? 1 : 0;
     launch_combine(ca, (int)max_dim, stream);
+    uint64_t ef_own = 0, sent = 0, recv = 0;
+    for (uint32_t q = 0; q < N; ++q) {
+      ef_own += ef_from[q];
+      if (q == local) continue;
+      sent += nnz_to[q] * 4 + BF * 4 + ef_from[q] * 4;
+      recv += nnz_from[q] * 4 + BF * 4 + ef_to[q] * 4;
+    }
     stats.nnz_owned = nnz_own;
     stats.entries_owned = ef_own / std::max<uint32_t>(1, max_dim);
-    uint64_t sent = 0, recv = 0;
-    for (uint32_t p = 0; p < N; ++p) {
-      if (p == local) continue;
-      sent += nnz_to[p] * 4 + BF * 4 + ef_from[p] * 4;
-      recv += nnz_from[p] * 4 + BF * 4 + ef_to[p] * 4;
-    }
     stats.a2a_bytes_sent = sent;
     stats.a2a_bytes_recv = recv;
   }
@@ -530,65 +516,120 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   finish_call();
 }
 
-// counts all-to-all: per peer p, (ids to p, partial floats for p's bags).
-void Ctx::a2a_counts() {
-  const uint64_t BF = (uint64_t)B * F;
-  bounds.ensure(8 * (2 * (N + 1) + 4 * N));
-  uint64_t* d_b = bounds.as<uint64_t>();
-  k_gather_bounds<<<1, 64, 0, stream>>>(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF, d_b);
-  S2D_LAUNCH_CHECK();
-  // d_b[0..N] id bounds, d_b[N+1..2N+1] float bounds; pack per-peer pairs
-  // into d_b[2N+2 ..] (send) and receive pairs after it.
-  h_counts.ensure(8 * (8 * (N + 1)));
-  S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_b, 8 * 2 * (N + 1), cudaMemcpyDeviceToHost, stream));
+// ---- MP-group peer memory -------------------------------------------------
+
+PeerPtrs Ctx::ptrs(const PeerBuf& pb) const {
+  PeerPtrs pp{};
+  for (uint32_t q = 0; q < N && q < pb.ptr.size(); ++q) pp.p[q] = pb.ptr[q];
+  return pp;
+}
+
+// Collective over the MP group: every rank calls it with the same `bytes`
+// (derived from data all ranks share), so growth decisions agree.
+void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) {
+  if (pb.buf.p && bytes <= pb.cap) return;
+  const size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
   S2D_CUDA(cudaStreamSynchronize(stream));
-  const uint64_t* hb = h_counts.as<uint64_t>();
+  for (void* q : pb.opened) cudaIpcCloseMemHandle(q);
+  pb.opened.clear();
+  hbuf.ensure((size_t)N * 64 + 64);
+  // everyone has unmapped the old buffers before anyone frees them
+  S2D_NCCL(ncclAllReduce(hbuf.p, hbuf.p, 1, ncclUint8, ncclMax, mp, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  pb.buf.release();
+  S2D_CUDA(cudaMalloc(&pb.buf.p, want));
+  pb.buf.cap = want;
+  pb.cap = want;
+  S2D_CUDA(cudaMemset(pb.buf.p, 0, want));
+  cudaIpcMemHandle_t h;
+  S2D_CUDA(cudaIpcGetMemHandle(&h, pb.buf.p));
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  uint8_t* dh = hbuf.as<uint8_t>();
+  S2D_CUDA(cudaMemcpy(dh + (size_t)N * 64, &h, 64, cudaMemcpyHostToDevice));
+  S2D_NCCL(ncclAllGather(dh + (size_t)N * 64, dh, 64, ncclUint8, mp, stream));
+  std::vector<cudaIpcMemHandle_t> all(N);
+  S2D_CUDA(cudaMemcpyAsync(all.data(), dh, (size_t)N * 64, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  pb.ptr.assign(N, nullptr);
+  for (uint32_t q = 0; q < N; ++q) {
+    if (q == local) {
+      pb.ptr[q] = pb.buf.p;
+      continue;
+    }
+    void* mapped = nullptr;
+    S2D_CUDA(cudaIpcOpenMemHandle(&mapped, all[q], cudaIpcMemLazyEnablePeerAccess));
+    pb.ptr[q] = mapped;
+    pb.opened.push_back(mapped);
+  }
+}
+
+float* Ctx::pooled_buffer() {
+  return N > 1 ? p_pooled.buf.as<float>() : p_pooled_local.as<float>();
+}
+
+void Ctx::peer_barrier() {
+  ++epoch;
+  launch_peer_barrier(ptrs(p_flags), p_flags.buf.as<uint64_t>(), local, N, epoch, err.as<uint32_t>(), stream);
+}
+
+// Count matrix xcnt[n][o] = (ids n sends to o, partial floats of those
+// entries, n's batch), published by every requester into every peer.
+void Ctx::read_counts() {
+  std::vector<uint64_t> x((size_t)N * N * 3);
+  S2D_CUDA(cudaMemcpyAsync(x.data(), p_xcnt.buf.p, x.size() * 8, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  check_faults();
+  auto at = [&](uint32_t n, uint32_t o, int k) { return x[((size_t)n * N + o) * 3 + k]; };
+  for (uint32_t n = 0; n < N; ++n)
+    if (at(n, 0, 2) != B)
+      throw Error(S2D_EINVAL, "per-rank batch must be identical in the MP group (" + std::to_string(at(n, 0, 2)) +
+                                  " vs " + std::to_string(B) + ")");
   nnz_to.assign(N, 0);
   ef_to.assign(N, 0);
-  ids_base_to.assign(N, 0);
-  ef_base_to.assign(N, 0);
-  for (uint32_t p = 0; p < N; ++p) {
-    ids_base_to[p] = hb[p];
-    nnz_to[p] = hb[p + 1] - hb[p];
-    ef_base_to[p] = hb[N + 1 + p];
-    ef_to[p] = hb[N + 2 + p] - hb[N + 1 + p];
-  }
-  // exchange (nnz, floats) pairs
-  std::vector<uint64_t> sendpairs(2 * N);
-  for (uint32_t p = 0; p < N; ++p) {
-    sendpairs[2 * p] = nnz_to[p];
-    sendpairs[2 * p + 1] = ef_to[p];
-  }
-  uint64_t* d_send = d_b + 2 * (N + 1);
-  uint64_t* d_recv = d_send + 2 * N;
-  S2D_CUDA(cudaMemcpyAsync(d_send, sendpairs.data(), 8 * 2 * N, cudaMemcpyHostToDevice, stream));
-  S2D_NCCL(ncclGroupStart());
-  for (uint32_t p = 0; p < N; ++p) {
-    if (p == local) continue;
-    S2D_NCCL(ncclSend(d_send + 2 * p, 2, ncclUint64, (int)p, mp, stream));
-    S2D_NCCL(ncclRecv(d_recv + 2 * p, 2, ncclUint64, (int)p, mp, stream));
-  }
-  S2D_NCCL(ncclGroupEnd());
-  std::vector<uint64_t> rp(2 * N, 0);
-  S2D_CUDA(cudaMemcpyAsync(rp.data(), d_recv, 8 * 2 * N, cudaMemcpyDeviceToHost, stream));
-  S2D_CUDA(cudaStreamSynchronize(stream));
-  rp[2 * local] = nnz_to[local];
-  rp[2 * local + 1] = ef_to[local];
   nnz_from.assign(N, 0);
   ef_from.assign(N, 0);
-  nnz_base_from.assign(N, 0);
-  ef_base_from.assign(N, 0);
+  send_bound.assign(N, 0);
+  eoff_req_bound.assign(N, 0);
+  own_eoff_bound.assign(N, 0);
+  ids_base_at_owner.assign(N, 0);
+  part_base_at_req.assign(N, 0);
+  grad_base_at_owner.assign(N, 0);
+  uint64_t need_ids = 0, need_part = 0, need_grad = 0;
+  for (uint32_t r = 0; r < N; ++r) {
+    uint64_t ids_in = 0, ef_in = 0, ef_out = 0;
+    for (uint32_t q = 0; q < N; ++q) {
+      ids_in += at(q, r, 0);
+      ef_in += at(q, r, 1);
+      ef_out += at(r, q, 1);
+    }
+    need_ids = std::max(need_ids, ids_in);
+    need_grad = std::max(need_grad, ef_in);
+    need_part = std::max(need_part, ef_out);
+  }
   nnz_own = 0;
-  uint64_t efb = 0;
-  for (uint32_t p = 0; p < N; ++p) {
-    nnz_from[p] = rp[2 * p];
-    ef_from[p] = rp[2 * p + 1];
-    nnz_base_from[p] = nnz_own;
-    ef_base_from[p] = efb;
-    nnz_own += nnz_from[p];
-    efb += ef_from[p];
+  uint64_t sb = 0, eb = 0, ob = 0;
+  for (uint32_t q = 0; q < N; ++q) {
+    nnz_to[q] = at(local, q, 0);
+    ef_to[q] = at(local, q, 1);
+    nnz_from[q] = at(q, local, 0);
+    ef_from[q] = at(q, local, 1);
+    send_bound[q] = sb;
+    eoff_req_bound[q] = eb;
+    own_eoff_bound[q] = ob;
+    sb += nnz_to[q];
+    eb += ef_to[q];
+    ob += ef_from[q];
+    nnz_own += nnz_from[q];
+    for (uint32_t n = 0; n < local; ++n) {
+      ids_base_at_owner[q] += at(n, q, 0);   // my block in owner q's id buffer
+      grad_base_at_owner[q] += at(n, q, 1);  // ... and in its gradient buffer
+    }
+    for (uint32_t o = 0; o < local; ++o) part_base_at_req[q] += at(q, o, 1);  // my block in requester q's partials
   }
   if (nnz_own >= 0xffffffffull) throw Error(S2D_EINVAL, "owner demand exceeds 2^32-1 ids");
+  peer_alloc(p_ids, std::max<uint64_t>(need_ids, 1) * 4);
+  peer_alloc(p_part, std::max<uint64_t>(need_part, 4) * 4);
+  peer_alloc(p_grad, std::max<uint64_t>(need_grad, 4) * 4);
 }
 
 // ---- backward + fused update ---------------------------------------------------
@@ -608,13 +649,9 @@ void Ctx::backward_update(const float* upstream, int mem) {
   }
   const float* grad = d_up;
   if (N > 1) {
-    uint64_t ef_req = 0, ef_own = 0;
-    for (uint32_t p = 0; p < N; ++p) {
-      ef_req += ef_to[p];
-      ef_own += ef_from[p];
-    }
-    grad_send.ensure(std::max<uint64_t>(ef_req, 4) * 4);
-    grad_recv.ensure(std::max<uint64_t>(ef_own, 4) * 4);
+    // C2 fused: gradient rows stored straight into the owners' buffers; the
+    // owner's receive layout equals its partial send layout, so the
+    // lookup's (slot, val) pairs index it.
     phase_begin(kPhGradGather);
     GradGatherArgs ga{};
     ga.feats = d_feats.as<FeatDev>();
@@ -625,28 +662,17 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ga.cnt = cnt.as<uint32_t>();
     ga.eoff = eoff_req.as<uint64_t>();
     ga.upstream = d_up;
-    ga.send = grad_send.as<float>();
+    ga.peer_dst = ptrs(p_grad);
+    for (uint32_t o = 0; o < N; ++o) ga.peer_adj[o] = (int64_t)grad_base_at_owner[o] - (int64_t)eoff_req_bound[o];
     launch_grad_gather(ga, (int)max_dim, stream);
     phase_begin(kPhA2AGrad);
-    // C2: gradients to owners; the owner's receive layout equals its
-    // partial send layout, so the lookup's (slot, val) pairs index it.
-    S2D_NCCL(ncclGroupStart());
-    for (uint32_t p = 0; p < N; ++p) {
-      if (p == local) continue;
-      if (ef_to[p]) S2D_NCCL(ncclSend(grad_send.as<float>() + ef_base_to[p], ef_to[p], ncclFloat32, (int)p, mp, stream));
-      if (ef_from[p])
-        S2D_NCCL(ncclRecv(grad_recv.as<float>() + ef_base_from[p], ef_from[p], ncclFloat32, (int)p, mp, stream));
-    }
-    S2D_NCCL(ncclGroupEnd());
-    if (ef_to[local])
-      S2D_CUDA(cudaMemcpyAsync(grad_recv.as<float>() + ef_base_from[local], grad_send.as<float>() + ef_base_to[local],
-                               ef_to[local] * 4, cudaMemcpyDeviceToDevice, stream));
-    grad = grad_recv.as<float>();
+    peer_barrier();
+    grad = p_grad.buf.as<float>();
     uint64_t sent = 0, recv = 0;
-    for (uint32_t p = 0; p < N; ++p) {
-      if (p == local) continue;
-      sent += ef_to[p] * 4;
-      recv += ef_from[p] * 4;
+    for (uint32_t q = 0; q < N; ++q) {
+      if (q == local) continue;
+      sent += ef_to[q] * 4;
+      recv += ef_from[q] * 4;
     }
     stats.a2a_bytes_sent += sent;
     stats.a2a_bytes_recv += recv;
@@ -761,23 +787,21 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
   };
   switch (which) {
     case 0:
-      if (N == 1) copy(in_lengths.p, 0, 4);
-      else copy(recv_lengths.p, (uint64_t)N * BF, 4);
+      copy(p_len.buf.p, N == 1 ? 0 : (uint64_t)N * BF, 4);
       break;
     case 1:
-      if (N == 1) copy(in_ids.p, 0, 4);
-      else copy(recv_ids.p, nnz_own, 4);
+      copy(p_ids.buf.p, N == 1 ? 0 : nnz_own, 4);
       break;
-    case 2: {
+    case 2: {  // partials received from the owners, concatenated by owner
       uint64_t t = 0;
-      for (auto x : ef_from) t += x;
-      copy(part_send.p, N == 1 ? 0 : t, 4);
+      for (auto q : ef_to) t += q;
+      copy(p_part.buf.p, N == 1 ? 0 : t, 4);
       break;
     }
-    case 3: {
+    case 3: {  // gradient rows received from the requesters, by requester
       uint64_t t = 0;
-      for (auto x : ef_to) t += x;
-      copy(grad_send.p, N == 1 ? 0 : t, 4);
+      for (auto q : ef_from) t += q;
+      copy(p_grad.buf.p, N == 1 ? 0 : t, 4);
       break;
     }
     case 4: {
@@ -806,6 +830,9 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
       if (out) std::memcpy(out, rows.data(), std::min<uint64_t>(cap, rows.size()) * 4);
       break;
     }
+    case 6:  // engine-owned pooled output of the last forward
+      copy(pooled_buffer(), pooled_buffer() ? (uint64_t)B * sum_dims : 0, 4);
+      break;
     default:
       throw Error(S2D_EINVAL, "unknown debug buffer");
   }

@@ -52,6 +52,14 @@ enum Phase : int {
   kNumPhases
 };
 
+// A buffer every rank of the MP group maps (CUDA IPC over NVLink).
+struct PeerBuf {
+  DevBuf buf;
+  size_t cap = 0;               // identical on every rank of the group
+  std::vector<void*> ptr;       // [N] (own entry = buf.p)
+  std::vector<void*> opened;    // IPC mappings to close
+};
+
 struct Ctx {
   // mesh (topology.hpp:13-26): rank -> (group = r / N, local = r % N)
   int device = 0;
@@ -86,16 +94,22 @@ struct Ctx {
   uint32_t B = 0;
   uint64_t nnz_local = 0, nnz_own = 0;
   bool fwd_done = false;
-  DevBuf in_lengths, in_ids, in_off, pooled_stage, upstream_stage;
-  DevBuf cnt, send_off, eoff_req, send_ids, bounds;  // requester side (N > 1)
-  DevBuf recv_lengths, recv_ids, own_idoff, own_eoff;  // owner side (N > 1)
-  DevBuf part_send, part_recv, grad_send, grad_recv;
+  DevBuf in_lengths, in_ids, in_off, upstream_stage;
+  DevBuf cnt, send_off, eoff_req;  // requester side (N > 1)
+  DevBuf own_idoff, own_eoff;      // owner side (N > 1)
+  // MP-group peer buffers: barrier flags, count matrix, received bag
+  // lengths [N][B*F], received ids, received partials (requester), received
+  // gradient rows (owner)
+  PeerBuf p_flags, p_xcnt, p_len, p_ids, p_part, p_grad, p_pooled;
+  DevBuf p_pooled_local;  // engine-owned pooled output when N == 1
+  DevBuf hbuf;
+  uint64_t epoch = 0;
   DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
   DevBuf sync_list, sync_count, sync_packed, sync_gathered, sync_tmp;
   HostBuf h_counts;
-  std::vector<uint64_t> nnz_to, nnz_from, ef_to, ef_from, ids_base_to, ef_base_to, ef_base_from,
-      nnz_base_from;
+  std::vector<uint64_t> nnz_to, nnz_from, ef_to, ef_from, send_bound, eoff_req_bound, own_eoff_bound,
+      ids_base_at_owner, part_base_at_req, grad_base_at_owner;
   bool sorted_in_b = false;
   s2d_step_stats stats{};
   bool stats_counters_valid = false;
@@ -128,7 +142,12 @@ struct Ctx {
  private:
   void finish_call();
   void check_faults();
-  void a2a_counts();
+  PeerPtrs ptrs(const PeerBuf& pb) const;
+  void peer_alloc(PeerBuf& pb, size_t bytes);
+  void peer_barrier();
+  void read_counts();
+ public:
+  float* pooled_buffer();
 };
 
 }  // namespace s2d

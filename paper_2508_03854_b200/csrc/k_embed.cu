@@ -72,6 +72,12 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
   for (uint64_t b = first; b < BF; b += slots) {
     const uint32_t f = (uint32_t)(b % a.F);
     const uint32_t d4 = __ldg(&a.feats[f].dim) >> 2;
+    if (a.skip_single && __ldg(&a.feats[f].single)) {
+      // the owner stored the pooled row itself; only empty bags remain (zero)
+      bool any = false;
+      for (uint32_t o = 0; o < a.N; ++o) any |= __ldg(a.cnt + (uint64_t)o * BF + b) != 0;
+      if (any) continue;
+    }
     double acc[VPL][4];
 #pragma unroll
     for (int v = 0; v < VPL; ++v)
@@ -121,7 +127,7 @@ __global__ void __launch_bounds__(256) k_grad_gather(const GradGatherArgs a) {
     }
     for (uint32_t o = 0; o < a.N; ++o) {  // (s, f, o ascending) order, trainer.cpp:446-453
       if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
-      float* dst = a.send + __ldg(a.eoff + (uint64_t)o * BF + b);
+      float* dst = reinterpret_cast<float*>(a.peer_dst.p[o]) + a.peer_adj[o] + __ldg(a.eoff + (uint64_t)o * BF + b);
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const uint32_t c4 = gl + v * LPB;
@@ -163,23 +169,55 @@ __global__ void __launch_bounds__(256) k_bucket_count(const BucketArgs a) {
       }
       cnt[owner_of(a.ranges, rb, re, id)]++;
     }
-    for (uint32_t o = 0; o < a.N; ++o) a.cnt[(uint64_t)o * a.BF + b] = cnt[o];
+    for (uint32_t o = 0; o < a.N; ++o) {
+      a.cnt[(uint64_t)o * a.BF + b] = cnt[o];
+      reinterpret_cast<uint32_t*>(a.peer_len.p[o])[(uint64_t)a.me * a.BF + b] = cnt[o];
+    }
   }
 }
 
+// Warp per 32 consecutive bags: ids are read 32 at a time in (bag,
+// occurrence) order, each lane finds its id's owner, and a per-owner ballot
+// prefix gives each id its rank inside the owner's run, so the ids bound for
+// one owner leave as contiguous runs (coalesced NVLink stores) in exactly the
+// canonical order of build_demand (trainer.cpp:286-307).
 __global__ void __launch_bounds__(256) k_bucket_permute(const BucketArgs a) {
-  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.BF;
-       b += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t f = (uint32_t)(b % a.F);
-    const uint32_t rows = __ldg(&a.feats[f].rows), rb = __ldg(&a.feats[f].rbeg), re = __ldg(&a.feats[f].rend);
-    uint32_t pos[kMaxRanksPerGroup];
-    for (uint32_t o = 0; o < a.N; ++o) pos[o] = __ldg(a.send_off + (uint64_t)o * a.BF + b);
-    const uint32_t off = __ldg(a.id_off + b), len = __ldg(a.lengths + b);
-    for (uint32_t k = 0; k < len; ++k) {
-      const uint32_t id = __ldg(a.ids + off + k);
-      if (id >= rows) continue;
-      const uint32_t o = owner_of(a.ranges, rb, re, id);
-      a.send_ids[pos[o]++] = id;
+  const uint32_t lane = lane_id();
+  const uint64_t n_units = (a.BF + 31) / 32;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); u < n_units; u += warps) {
+    const uint64_t b0 = u * 32;
+    const uint32_t nb = (a.BF - b0) < 32 ? (uint32_t)(a.BF - b0) : 32u;
+    const uint64_t my_bag = b0 + min(lane, nb - 1);
+    const uint32_t my_end = __ldg(a.id_off + my_bag + 1);
+    const uint32_t o0 = __ldg(a.id_off + b0);
+    const uint32_t o1 = __shfl_sync(0xffffffffu, my_end, nb - 1);
+    // running output position per owner (lane o holds owner o's)
+    uint32_t run = lane < a.N ? __ldg(a.send_off + (uint64_t)lane * a.BF + b0) : 0u;
+    for (uint32_t c = o0; c < o1; c += 32) {
+      const uint32_t p = c + lane;
+      const bool have = p < o1;
+      uint32_t j = 0;  // bag of item p within the unit: # lanes whose end <= p
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, my_end, j + step - 1);
+        if (v <= p) j += step;
+      }
+      const uint32_t f = (uint32_t)((b0 + min(j, nb - 1)) % a.F);
+      uint32_t o = 0xffffffffu, id = 0;
+      if (have) {
+        id = __ldg(a.ids + p);
+        if (id < __ldg(&a.feats[f].rows)) o = owner_of(a.ranges, __ldg(&a.feats[f].rbeg), __ldg(&a.feats[f].rend), id);
+      }
+      for (uint32_t q = 0; q < a.N; ++q) {
+        const uint32_t sel = __ballot_sync(0xffffffffu, o == q);
+        if (!sel) continue;
+        const uint32_t base = __shfl_sync(0xffffffffu, run, q);
+        if (o == q)
+          reinterpret_cast<uint32_t*>(a.peer_ids.p[q])[a.ids_adj[q] + (int64_t)(base + __popc(sel & ((1u << lane) - 1u)))] =
+              id;
+        if (lane == q) run += __popc(sel);
+      }
     }
   }
 }

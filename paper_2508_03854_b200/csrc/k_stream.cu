@@ -167,8 +167,19 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
     const uint32_t flo = __ldg(&a.feats[f].lo), fhi = __ldg(&a.feats[f].hi);
     const uint32_t vbase = __ldg(&a.feats[f].vbase);
     const uint64_t wbase = __ldg(&a.feats[f].wbase);
+    // out_off: local float offset of the bag's output (also the gradient-row
+    // offset the backward sorts); optr: where the flush stores it -- the
+    // pooled row (N = 1) or requester n's receive buffer over NVLink (N > 1)
     const uint64_t out_off = a.direct ? (uint64_t)((my_bag / a.F) % a.B) * a.sum_dims + __ldg(&a.feats[f].coff)
                                       : __ldg(a.eoff + my_bag);
+    float* const optr = a.direct ? a.out + out_off : [&] {
+      const uint64_t BF = (uint64_t)a.B * a.F;
+      const uint32_t n = (uint32_t)(my_bag / BF);
+      if (a.use_peer_pooled && __ldg(&a.feats[f].single))
+        return reinterpret_cast<float*>(a.peer_pooled.p[n]) + ((my_bag % BF) / a.F) * a.sum_dims +
+               __ldg(&a.feats[f].coff);
+      return reinterpret_cast<float*>(a.peer_out.p[n]) + a.peer_adj[n] + out_off;
+    }();
     if (a.direct) {  // empty bags pool to zero (embedding.cpp:43-44)
       uint32_t empty = __ballot_sync(0xffffffffu, lane < nb && my_start == my_end);
       while (empty) {
@@ -248,10 +259,10 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
     uint32_t d4c = uni_d4 ? uni_d4 : (cur >> 16);
     cur &= 0xffu;
     auto flush = [&]() {
-      const uint64_t oo = shfl64(out_off, cur);
+      float* const op = reinterpret_cast<float*>(shfl64(reinterpret_cast<uint64_t>(optr), cur));
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
-        if (lane + v * 32 < d4c) store_f32x4_stream(a.out + oo + (lane + v * 32) * 4, acc[v]);
+        if (lane + v * 32 < d4c) store_f32x4_stream(op + (lane + v * 32) * 4, acc[v]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[v][k] = 0.0;
       }

@@ -26,6 +26,8 @@ CASES = [
     (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4"]),
     (4, 1, "table-wise", ["--sgd"]),
     (4, 4, "table-wise", []),
+    (2, 1, "table-wise", ["--engine-out"]),
+    (4, 2, "table-wise", ["--engine-out"]),
 ]
 
 
@@ -33,7 +35,7 @@ CASES = [
 def test_mesh_parity(T, M, strategy, extra):
     if _ngpu() < T:
         pytest.skip(f"needs {T} GPUs")
-    port = 29500 + 7 * T + M + (0 if strategy == "row-wise" else 50)
+    port = 29500 + 7 * T + M + (0 if strategy == "row-wise" else 50) + (100 if extra else 0)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(T), "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_parity.py"), "--groups",
            str(M), "--strategy", strategy, *extra]
