@@ -62,6 +62,9 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -91,6 +94,14 @@ struct Row;
 template <>
 struct Row<float> {
   static constexpr int kVecBytes = 16;
+  using T = float4;
+  static __device__ __forceinline__ T ldg(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  static __device__ __forceinline__ void cvt(double (&d)[4], const T& x) {
+    d[0] = (double)x.x;
+    d[1] = (double)x.y;
+    d[2] = (double)x.z;
+    d[3] = (double)x.w;
+  }
   static __device__ __forceinline__ void add_s(double (&a)[4], uint32_t saddr) {
     const float4 x = lds128(saddr);
     a[0] += (double)x.x;
@@ -109,6 +120,14 @@ struct Row<float> {
 template <>
 struct Row<__nv_bfloat16> {
   static constexpr int kVecBytes = 8;
+  using T = uint2;
+  static __device__ __forceinline__ T ldg(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+  static __device__ __forceinline__ void cvt(double (&d)[4], const T& x) {
+    d[0] = (double)__uint_as_float(x.x << 16);
+    d[1] = (double)__uint_as_float(x.x & 0xffff0000u);
+    d[2] = (double)__uint_as_float(x.y << 16);
+    d[3] = (double)__uint_as_float(x.y & 0xffff0000u);
+  }
   static __device__ __forceinline__ void add_s(double (&a)[4], uint32_t saddr) {
     const uint2 x = lds64(saddr);
     a[0] += (double)__uint_as_float(x.x << 16);
@@ -464,16 +483,13 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
 
 template <typename WT, int VPL>
 __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
-  constexpr int WB = Row<WT>::kVecBytes;
   constexpr int kWinStages = 32 / kRowsPerStage;
-  constexpr uint32_t kGRow = VPL * 32 * 16, kWRow = VPL * 32 * WB;
+  constexpr uint32_t kGRow = VPL * 32 * 16;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t per_warp = kSlots * (kGRow + kWRow) + kSlots * 4;
+  const uint32_t per_warp = kSlots * kGRow;
   const uint32_t gring_s = smem_u32(smem) + warp * per_warp;  // gradient rows
-  const uint32_t wring_s = gring_s + kSlots * kGRow;            // weight row at each head
-  const uint32_t mring_s = wring_s + kSlots * kWRow;            // moment at each head
-  const uint32_t g_lane = gring_s + lane * 16, w_lane = wring_s + lane * WB;
+  const uint32_t g_lane = gring_s + lane * 16;
   const uint64_t n = a.n;
   const uint64_t n_units = (n + kC - 1) / kC;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -542,14 +558,15 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
         const uint32_t d4 = meta & 0xffffu, slot = slot0 + r;
         const bool valid = meta & 0x10000u, head = meta & 0x20000u;
         const float* grow = a.grad + (uint64_t)val * 4 + lane * 4;
-        const WT* wrow = W + wo + lane * 4;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) {
-          const bool col = lane + v * 32 < d4;
-          cp_async_p<16>(g_lane + slot * kGRow + v * 512, grow + v * 128, valid && col);
-          cp_async_p<WB>(w_lane + slot * kWRow + v * 32 * WB, wrow + v * 128, head && col);
+        for (int v = 0; v < VPL; ++v)
+          cp_async_p<16>(g_lane + slot * kGRow + v * 512, grow + v * 128, valid && lane + v * 32 < d4);
+        // segment head: warm L2 with its weight row and moment; they are
+        // loaded into registers when the consumer reaches the head
+        if (head) {
+          if (lane * VPL < d4) prefetch_l2(W + wo + lane * 4 * VPL);
+          if (lane == 0) prefetch_l2(a.moments + key);
         }
-        cp_async_p<4>(mring_s + slot * 4, a.moments + (head ? key : 0), head && lane == 0);
       }
       cp_commit();
     };
@@ -561,7 +578,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
     uint32_t cur = 0xffffffffu, d4 = 0;
     uint64_t wofs = 0;
-    double wold[VPL][4];  // weight row of `cur`
+    typename Row<WT>::T wraw[VPL];  // weight row of `cur` (raw storage type)
     float vold = 0.f;
     bool stop = false;
 
@@ -598,8 +615,9 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
           const uint32_t c4 = lane + v * 32;
           if (c4 < d4) {
             double x[4];
+            Row<WT>::cvt(x, wraw[v]);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) x[j] = wold[v][j] - lr * acc[v][j];
+            for (int j = 0; j < 4; ++j) x[j] = x[j] - lr * acc[v][j];
             Vec4<WT>::store(w + c4 * 4, x);
           }
         }
@@ -649,19 +667,14 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
             if (cur != 0xffffffffu) flush();
             if (key >= a.n_slots) {
               stop = true;
-            } else {  // segment head: take its weight row / moment out of the ring
+            } else {  // segment head: load its (L2-warm) weight row and moment
               cur = key;
               wofs = wo;
               d4 = meta & 0xffffu;
 #pragma unroll
-              for (int v = 0; v < VPL; ++v) {
-#pragma unroll
-                for (int j = 0; j < 4; ++j) wold[v][j] = 0.0;
-                if (lane + v * 32 < d4) Row<WT>::add_s(wold[v], w_lane + slot * kWRow + v * 32 * WB);
-              }
-              // the moment was copied by lane 0 alone: only lane 0's
-              // wait_group covers it, so lane 0 reads and broadcasts
-              vold = __uint_as_float(__shfl_sync(0xffffffffu, lane == 0 ? lds32(mring_s + slot * 4) : 0u, 0));
+              for (int v = 0; v < VPL; ++v)
+                if (lane + v * 32 < d4) wraw[v] = Row<WT>::ldg(W + wo + (lane + v * 32) * 4);
+              vold = a.moments[cur];
             }
           }
           if (!stop) add_grad(slot);
@@ -749,7 +762,7 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
 template <typename WT, int VPL>
 void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   const size_t pw_p = (size_t)kSlots * VPL * 32 * 16;
-  const size_t pw_u = (size_t)kSlots * VPL * 32 * (16 + Row<WT>::kVecBytes) + kSlots * 4;
+  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16;
   const uint32_t nw_p = warps_for(pw_p, 8), nw_u = warps_for(pw_u, 4);
   static bool init = false;
   if (!init) {
