@@ -193,6 +193,8 @@ struct StreamUpdateArgs {
   double* part1;                 // level-1 range partials [n/C][max_dim]
   double* part2;                 // level-2 partials [n/(C*P)][max_dim]
   double inv_batch, eta, eps, c;
+  double inv_c;                  // 1/c, exact when c_pow2
+  int c_pow2;                    // c is a power of two: v/c == v*inv_c bit for bit
   int sgd;
   uint32_t* err;
   uint32_t* counters;            // [0] unique rows updated, [1] rows spanning ranges

@@ -21,6 +21,8 @@
 
 #include "ctx.h"
 
+#include <cmath>
+
 namespace s2d {
 
 #define S2D_NCCL(call)                                                                    \
@@ -715,6 +717,12 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ua.eta = opt.eta;
     ua.eps = opt.eps;
     ua.c = opt.c;
+    {
+      int ex = 0;
+      const double mant = std::frexp(opt.c, &ex);
+      ua.c_pow2 = std::isfinite(opt.c) && mant == 0.5 && ex > -1000 && ex < 1000;
+      ua.inv_c = ua.c_pow2 ? std::ldexp(1.0, 1 - ex) : 0.0;
+    }
     ua.sgd = opt.variant == S2D_SGD;
     ua.err = err.as<uint32_t>();
     ua.counters = counters.as<uint32_t>();

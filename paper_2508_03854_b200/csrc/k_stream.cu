@@ -485,14 +485,14 @@ template <typename WT, int VPL>
 __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   constexpr int kWinStages = 32 / kRowsPerStage;
   constexpr uint32_t kGRow = VPL * 32 * 16;
+  constexpr uint32_t kNone = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t per_warp = kSlots * kGRow;
-  const uint32_t gring_s = smem_u32(smem) + warp * per_warp;  // gradient rows
-  const uint32_t g_lane = gring_s + lane * 16;
+  const uint32_t g_lane = smem_u32(smem) + warp * (kSlots * kGRow) + lane * 16;  // gradient ring
   const uint64_t n = a.n;
   const uint64_t n_units = (n + kC - 1) / kC;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  const uint32_t ud4 = a.uni_dim >> 2;
   WT* __restrict__ W = reinterpret_cast<WT*>(a.weights);
   uint32_t heads = 0, longs = 0;
 
@@ -502,12 +502,10 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     uint64_t h = ~0ull;
     for (uint64_t c = ra; c < re; c += 32) {
       const uint64_t p = c + lane;
-      bool head = false;
-      if (p < re) {
-        const uint32_t k = __ldg(a.keys + p);
-        head = k < a.n_slots && (p == 0 || __ldg(a.keys + p - 1) != k);
-      }
-      const uint32_t bal = __ballot_sync(0xffffffffu, head);
+      const uint32_t k = p < re ? __ldg(a.keys + p) : kNone;
+      uint32_t before = __shfl_up_sync(0xffffffffu, k, 1);
+      if (lane == 0) before = p > 0 ? __ldg(a.keys + p - 1) : kNone;
+      const uint32_t bal = __ballot_sync(0xffffffffu, k < a.n_slots && k != before);
       if (bal) {
         h = c + (__ffs(bal) - 1);
         break;
@@ -517,56 +515,65 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     const uint32_t n_items = (uint32_t)(re - h);
     const uint32_t nwin = (n_items + 31) / 32;
 
-    // Window w: lane k holds item k's key, gradient row, meta (d4 | valid <<
-    // 16 | head << 17) and weight offset; `simple` bit k = valid item of the
-    // same segment as item k-1.
+    // Window state, lane k = item k of the window: key, gradient row, row
+    // dim/4 and weight offset; vm / hm = ballots of valid items / segment
+    // heads.  Raw keys and rows are loaded one window before they are used.
+    struct Win {
+      uint32_t key, val, d4, vm, hm;
+      uint64_t wofs;
+    };
     uint32_t prev_key = 0xfffffffeu;  // key of the item before the window
-    auto gen = [&](uint32_t win, uint32_t& key, uint32_t& val, uint32_t& meta, uint64_t& wofs, uint32_t& simple) {
+    auto load_raw = [&](uint32_t win, uint32_t& key, uint32_t& val) {
       const uint64_t p = h + (uint64_t)win * 32 + lane;
       const bool have = win < nwin && p < re;
-      key = have ? __ldg(a.keys + p) : 0xffffffffu;
+      key = have ? __ldg(a.keys + p) : kNone;
       val = have ? __ldg(a.vals + p) : 0u;
+    };
+    auto gen = [&](uint32_t key, uint32_t val, Win& w) {
       uint32_t before = __shfl_up_sync(0xffffffffu, key, 1);
       if (lane == 0) before = prev_key;
       prev_key = __shfl_sync(0xffffffffu, key, 31);
-      uint32_t d4 = 0;
-      wofs = 0;
       const bool valid = key < a.n_slots;
-      if (valid) row_ref(a, key, wofs, d4);
       const bool head = valid && key != before;
-      meta = d4 | (valid ? 0x10000u : 0u) | (head ? 0x20000u : 0u);
-      simple = __ballot_sync(0xffffffffu, valid && !head);
+      w.key = key;
+      w.val = val;
+      w.d4 = 0;
+      w.wofs = 0;
+      if (valid) row_ref(a, key, w.wofs, w.d4);
+      w.vm = __ballot_sync(0xffffffffu, valid);
+      w.hm = __ballot_sync(0xffffffffu, head);
+      // warm L2 with the weight row and moment of every segment head; the
+      // consumer loads them into registers when it reaches the head
+      if (head) {
+        const char* row = reinterpret_cast<const char*>(W + w.wofs);
+        const uint32_t bytes = w.d4 * 4 * (uint32_t)sizeof(WT);
+        for (uint32_t o = 0; o < bytes; o += 128) prefetch_l2(row + o);
+        prefetch_l2(a.moments + key);
+      }
     };
-    uint32_t k_c, v_c, m_c, s_c, k_n, v_n, m_n, s_n;
-    uint64_t w_c, w_n;
-    gen(0, k_c, v_c, m_c, w_c, s_c);
-    gen(1, k_n, v_n, m_n, w_n, s_n);
+    Win wc_, wn_;
+    uint32_t rk, rv;
+    load_raw(0, rk, rv);
+    gen(rk, rv, wc_);
+    load_raw(1, rk, rv);
+    gen(rk, rv, wn_);
+    load_raw(2, rk, rv);
     uint32_t wc = 0;
 
     auto produce = [&](uint32_t st) {
       const bool nxt = (st / kWinStages) != wc;
-      const uint32_t K = nxt ? k_n : k_c, V = nxt ? v_n : v_c, Mt = nxt ? m_n : m_c;
-      const uint64_t Wo = nxt ? w_n : w_c;
+      const uint32_t V = nxt ? wn_.val : wc_.val, VM = nxt ? wn_.vm : wc_.vm, D = nxt ? wn_.d4 : wc_.d4;
       const uint32_t q = (st % kWinStages) * kRowsPerStage;
       const uint32_t slot0 = (st % kStages) * kRowsPerStage;
 #pragma unroll
       for (int r = 0; r < kRowsPerStage; ++r) {
-        const uint32_t meta = __shfl_sync(0xffffffffu, Mt, q + r);
         const uint32_t val = __shfl_sync(0xffffffffu, V, q + r);
-        const uint32_t key = __shfl_sync(0xffffffffu, K, q + r);
-        const uint64_t wo = a.uni_dim ? (uint64_t)key * a.uni_dim : shfl64(Wo, q + r);
-        const uint32_t d4 = meta & 0xffffu, slot = slot0 + r;
-        const bool valid = meta & 0x10000u, head = meta & 0x20000u;
+        const uint32_t d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, D, q + r);
+        const bool valid = (VM >> (q + r)) & 1u;
         const float* grow = a.grad + (uint64_t)val * 4 + lane * 4;
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
-          cp_async_p<16>(g_lane + slot * kGRow + v * 512, grow + v * 128, valid && lane + v * 32 < d4);
-        // segment head: warm L2 with its weight row and moment; they are
-        // loaded into registers when the consumer reaches the head
-        if (head) {
-          if (lane * VPL < d4) prefetch_l2(W + wo + lane * 4 * VPL);
-          if (lane == 0) prefetch_l2(a.moments + key);
-        }
+          cp_async_p<16>(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128, valid && lane + v * 32 < d4);
       }
       cp_commit();
     };
@@ -576,7 +583,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     for (int v = 0; v < VPL; ++v)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
-    uint32_t cur = 0xffffffffu, d4 = 0;
+    uint32_t cur = kNone, d4 = 0;
     uint64_t wofs = 0;
     typename Row<WT>::T wraw[VPL];  // weight row of `cur` (raw storage type)
     float vold = 0.f;
@@ -584,31 +591,41 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 
     // fused K4 row step (optimizer.cpp:65-90); nonfinite rows are not written
     auto flush = [&]() {
-      bool finite = true;
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc[v][j] = acc[v][j] * a.inv_batch;  // g (optimizer.cpp:55)
-          if (lane + v * 32 < d4) finite &= isfinite(acc[v][j]);
-        }
-      if (!__all_sync(0xffffffffu, finite)) {
-        if (lane == 0) atomicOr(a.err, kErrNonfinite);
-      } else {
-        double lr = a.eta;
-        if (!a.sgd) {
-          double ns = 0.0;
+        for (int j = 0; j < 4; ++j) acc[v][j] = acc[v][j] * a.inv_batch;  // g (optimizer.cpp:55)
+      bool finite;
+      double lr = a.eta;
+      if (!a.sgd) {
+        double ns = 0.0;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v)
-            if (lane + v * 32 < d4)
+        for (int v = 0; v < VPL; ++v)
+          if (lane + v * 32 < d4)
 #pragma unroll
-              for (int j = 0; j < 4; ++j) ns += acc[v][j] * acc[v][j];
+            for (int j = 0; j < 4; ++j) ns += acc[v][j] * acc[v][j];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        for (int o = 16; o > 0; o >>= 1) ns += __shfl_xor_sync(0xffffffffu, ns, o);
+        // |g|^2 is finite iff every g is: f64 sums of f32 rows cannot overflow
+        finite = isfinite(ns);
+        if (finite) {
           const float v_new = (float)((double)vold + ns);
-          lr = a.eta / (sqrt((double)v_new / a.c) + a.eps);  // effective_lr (optimizer.cpp:61-63)
+          const double vc = a.c_pow2 ? (double)v_new * a.inv_c : (double)v_new / a.c;  // exact either way
+          lr = a.eta / (sqrt(vc) + a.eps);  // effective_lr (optimizer.cpp:61-63)
           if (lane == 0) a.moments[cur] = v_new;
         }
+      } else {
+        bool f = true;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (lane + v * 32 < d4) f &= isfinite(acc[v][j]);
+        finite = __all_sync(0xffffffffu, f);
+      }
+      if (!finite) {
+        if (lane == 0) atomicOr(a.err, kErrNonfinite);
+      } else {
         WT* w = W + wofs;
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {
@@ -641,50 +658,45 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     for (uint32_t s = 0; s < nst && !stop; ++s) {
       if (s > 0 && s % kWinStages == 0) {
         ++wc;
-        k_c = k_n;
-        v_c = v_n;
-        m_c = m_n;
-        w_c = w_n;
-        s_c = s_n;
-        gen(wc + 1, k_n, v_n, m_n, w_n, s_n);
+        wc_ = wn_;
+        gen(rk, rv, wn_);
+        load_raw(wc + 2, rk, rv);
       }
       produce(s + kStages - 1);
       cp_wait<kStages - 1>();
       const uint32_t q = (s % kWinStages) * kRowsPerStage;
       const uint32_t slot0 = (s % kStages) * kRowsPerStage;
-      if (((s_c >> q) & ((1u << kRowsPerStage) - 1u)) == ((1u << kRowsPerStage) - 1u)) {
+      constexpr uint32_t kAll = (1u << kRowsPerStage) - 1u;
+      if ((((wc_.vm & ~wc_.hm) >> q) & kAll) == kAll) {  // 4 continuation rows
 #pragma unroll
         for (int r = 0; r < kRowsPerStage; ++r) add_grad(slot0 + r);
       } else {
 #pragma unroll
         for (int r = 0; r < kRowsPerStage; ++r) {
-          const uint32_t key = __shfl_sync(0xffffffffu, k_c, q + r);
-          const uint32_t meta = __shfl_sync(0xffffffffu, m_c, q + r);
-          const uint64_t wo = a.uni_dim ? (uint64_t)key * a.uni_dim : shfl64(w_c, q + r);
-          const uint32_t slot = slot0 + r;
+          const uint32_t i = q + r;
           if (s * kRowsPerStage + r >= n_items) break;  // past this range: not a sentinel
-          if (!stop && key != cur) {
-            if (cur != 0xffffffffu) flush();
-            if (key >= a.n_slots) {
-              stop = true;
-            } else {  // segment head: load its (L2-warm) weight row and moment
-              cur = key;
-              wofs = wo;
-              d4 = meta & 0xffffu;
-#pragma unroll
-              for (int v = 0; v < VPL; ++v)
-                if (lane + v * 32 < d4) wraw[v] = Row<WT>::ldg(W + wo + (lane + v * 32) * 4);
-              vold = a.moments[cur];
-            }
+          if (!((wc_.vm >> i) & 1u)) {                  // invalid-slot sentinels sort last
+            stop = true;
+            break;
           }
-          if (!stop) add_grad(slot);
+          if ((wc_.hm >> i) & 1u) {
+            if (cur != kNone) flush();
+            // segment head: load its (L2-warm) weight row and moment
+            cur = __shfl_sync(0xffffffffu, wc_.key, i);
+            wofs = a.uni_dim ? (uint64_t)cur * a.uni_dim : shfl64(wc_.wofs, i);
+            d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, wc_.d4, i);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+              if (lane + v * 32 < d4) wraw[v] = Row<WT>::ldg(W + wofs + (lane + v * 32) * 4);
+            vold = a.moments[cur];
+          }
+          add_grad(slot0 + r);
         }
       }
     }
     cp_wait<0>();
-    if (stop) continue;
     // continuation of the open segment past this range
-    if (re < n && __ldg(a.keys + re) == cur) {
+    if (!stop && re < n && __ldg(a.keys + re) == cur) {
       ++longs;
       uint64_t k = re / kC;  // == u + 1
       uint64_t kend = ~0ull;
@@ -718,7 +730,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       }
       ring_sum<VPL>(a, g_lane, lane, rs, seg_end, d4, acc);
     }
-    flush();
+    if (cur != kNone) flush();
   }
   if (lane == 0) {
     if (heads) atomicAdd(&a.counters[0], heads);
