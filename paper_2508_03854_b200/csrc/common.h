@@ -111,6 +111,7 @@ struct LookupArgs {
   int direct;                  // N == 1: write pooled rows (zero for empty bags)
   int emit_keys;
   uint32_t uni_d4;             // dim/4 shared by every table (0: mixed dims)
+  uint32_t* ticket;            // work counter of the persistent warps (zeroed per launch)
   // non-direct: the partial of a bag of requester n goes to
   // peer_out.p[n] + peer_adj[n] + eoff[bag] (requester n's receive buffer,
   // over NVLink); the sort vals stay local (eoff[bag] / 4)

@@ -411,6 +411,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.direct = 1;
     a.emit_keys = 1;
     a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
+    counters.ensure(64);
+    a.ticket = counters.as<uint32_t>() + 8;
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     stats.nnz_owned = nnz;
     stats.entries_owned = BF;
@@ -479,6 +481,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.use_peer_pooled = engine_out ? 1 : 0;
     if (engine_out) a.peer_pooled = ptrs(p_pooled);
     for (uint32_t n = 0; n < N; ++n) a.peer_adj[n] = (int64_t)part_base_at_req[n] - (int64_t)own_eoff_bound[n];
+    counters.ensure(64);
+    a.ticket = counters.as<uint32_t>() + 8;
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     phase_begin(kPhA2ALookup);
     peer_barrier();  // every owner's partials have landed in p_part

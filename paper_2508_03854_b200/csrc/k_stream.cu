@@ -168,11 +168,15 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   const uint32_t ring_s = smem_u32(smem) + warp * kSlots * kRowBytes + lane * VB;
   const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
   const uint64_t n_units = (n_bags + kBags - 1) / kBags;
-  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
   const uint32_t uni_d4 = a.uni_d4;
 
-  for (uint64_t unit = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; unit < n_units; unit += stride) {
+  // persistent warps take units in ascending order from a ticket counter
+  for (;;) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(a.ticket, 1u);
+    const uint64_t unit = __shfl_sync(0xffffffffu, t, 0);
+    if (unit >= n_units) break;
     const uint64_t b0 = unit * kBags;
     const uint32_t nb = (n_bags - b0) < (uint64_t)kBags ? (uint32_t)(n_bags - b0) : (uint32_t)kBags;
     const uint64_t my_bag = b0 + min(lane, nb - 1);
@@ -491,12 +495,16 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   const uint32_t g_lane = smem_u32(smem) + warp * (kSlots * kGRow) + lane * 16;  // gradient ring
   const uint64_t n = a.n;
   const uint64_t n_units = (n + kC - 1) / kC;
-  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   const uint32_t ud4 = a.uni_dim >> 2;
   WT* __restrict__ W = reinterpret_cast<WT*>(a.weights);
   uint32_t heads = 0, longs = 0;
 
-  for (uint64_t u = (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; u < n_units; u += stride) {
+  // persistent warps take ranges in ascending order from a ticket counter
+  for (;;) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(&a.counters[2], 1u);
+    const uint64_t u = __shfl_sync(0xffffffffu, t, 0);
+    if (u >= n_units) break;
     const uint64_t ra = u * kC, re = (ra + kC < n) ? ra + kC : n;
     // first segment head in [ra, re)
     uint64_t h = ~0ull;
@@ -767,7 +775,13 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
     set_smem(k_lookup_ring<WT, VPL>, smem);
     init = true;
   }
-  k_lookup_ring<WT, VPL><<<grid_units(n_units, nw, 148 * 64), nw * 32, smem, st>>>(a);
+  static int occ = 0;
+  if (!occ) {
+    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lookup_ring<WT, VPL>, nw * 32, smem));
+    if (occ < 1) occ = 1;
+  }
+  S2D_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(uint32_t), st));
+  k_lookup_ring<WT, VPL><<<grid_units(n_units, nw, 148 * occ), nw * 32, smem, st>>>(a);
   S2D_LAUNCH_CHECK();
 }
 
@@ -790,7 +804,12 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
     k_group_partials<VPL><<<grid_units(a.n / (kC * kP), 8, 148 * 8), 256, 0, st>>>(a);
     S2D_LAUNCH_CHECK();
   }
-  k_update_ring<WT, VPL><<<grid_units((a.n + kC - 1) / kC, nw_u, 148 * 64), nw_u * 32, nw_u * pw_u, st>>>(a);
+  static int occ = 0;
+  if (!occ) {
+    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_ring<WT, VPL>, nw_u * 32, nw_u * pw_u));
+    if (occ < 1) occ = 1;
+  }
+  k_update_ring<WT, VPL><<<grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ), nw_u * 32, nw_u * pw_u, st>>>(a);
   S2D_LAUNCH_CHECK();
 }
 
