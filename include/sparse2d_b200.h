@@ -153,6 +153,13 @@ int s2d_ctx_set_stream(s2d_ctx* ctx, void* cuda_stream);
  * calls return once work is queued; faults surface at s2d_synchronize. */
 int s2d_ctx_set_strict(s2d_ctx* ctx, int strict);
 
+/* async = 0 (default): an S2D_HOST pooled output is complete when
+ * s2d_lookup_forward returns.  async = 1: the read-back runs on the
+ * context's D2H copy stream and completes by the end of the following
+ * s2d_backward_update's work (or at s2d_synchronize), so it overlaps that
+ * call's upstream upload and sort.  Host buffers must stay valid until then. */
+int s2d_ctx_set_async_host(s2d_ctx* ctx, int async);
+
 /* Tables + plan (the identical-in-every-group plan).  The
  * context allocates only the shards its local rank owns: fp32 or bf16
  * weights, fp32 moments (embedding.hpp:16-17).  Replaces the replica

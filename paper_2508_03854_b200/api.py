@@ -257,6 +257,10 @@ class Sparse2DEmbedding:
     def set_strict(self, strict: bool):
         L.check(self.lib.s2d_ctx_set_strict(self._ctx, 1 if strict else 0))
 
+    def set_async_host(self, on: bool):
+        """Host-memory pooled output completes asynchronously (s2d_ctx_set_async_host)."""
+        L.check(self.lib.s2d_ctx_set_async_host(self._ctx, 1 if on else 0))
+
     def set_stream(self, stream_ptr: int | None):
         L.check(self.lib.s2d_ctx_set_stream(self._ctx, stream_ptr))
 

@@ -140,6 +140,10 @@ int s2d_ctx_set_strict(s2d_ctx* ctx, int strict) {
   return guarded([&] { as_ctx(ctx)->strict = strict != 0; });
 }
 
+int s2d_ctx_set_async_host(s2d_ctx* ctx, int async) {
+  return guarded([&] { as_ctx(ctx)->async_host = async != 0; });
+}
+
 int s2d_register_tables(s2d_ctx* ctx, const s2d_table_desc* tables, uint32_t n_tables, const s2d_plan_entry* plan,
                         uint32_t n_entries, int32_t weight_dtype) {
   return guarded([&] { as_ctx(ctx)->register_tables(tables, n_tables, plan, n_entries, weight_dtype); });

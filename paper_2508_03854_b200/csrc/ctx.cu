@@ -113,6 +113,13 @@ Ctx::~Ctx() {
   for (PeerBuf* pb : {&p_flags, &p_xcnt, &p_len, &p_ids, &p_part, &p_grad, &p_pooled})
     for (void* q : pb->opened) cudaIpcCloseMemHandle(q);
   for (auto e : ev_pool) cudaEventDestroy(e);
+  for (cudaStream_t q : {h2d_stream, d2h_stream})
+    if (q) {
+      cudaStreamSynchronize(q);
+      cudaStreamDestroy(q);
+    }
+  for (cudaEvent_t e : {ev_fwd, ev_d2h, ev_up, ev_upd})
+    if (e) cudaEventDestroy(e);
   if (dp) ncclCommDestroy(dp);
   if (mp) ncclCommDestroy(mp);
   if (world) ncclCommDestroy(world);
@@ -135,6 +142,10 @@ void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uin
   S2D_CUDA(cudaSetDevice(dev));
   S2D_CUDA(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
   stream = own_stream;
+  S2D_CUDA(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
+  S2D_CUDA(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_fwd, &ev_d2h, &ev_up, &ev_upd})
+    S2D_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   err.ensure(4);
   S2D_CUDA(cudaMemsetAsync(err.p, 0, 4, stream));
   err_host.ensure(4);
@@ -339,6 +350,8 @@ void Ctx::finish_call() {
 
 void Ctx::synchronize_and_check() {
   S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaStreamSynchronize(h2d_stream));
+  S2D_CUDA(cudaStreamSynchronize(d2h_stream));
   S2D_CUDA(cudaMemcpyAsync(err_host.p, err.p, 4, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   check_faults();
@@ -369,6 +382,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   // tables then store pooled rows straight into it over NVLink
   const bool engine_out = (mem == S2D_DEVICE && pooled == nullptr) || mem == S2D_HOST;
   if (engine_out) {
+    if (d2h_pending) S2D_CUDA(cudaStreamWaitEvent(stream, ev_d2h, 0));  // last read-back of the buffer
     if (N > 1)
       peer_alloc(p_pooled, (uint64_t)B * sum_dims * 4);
     else
@@ -512,10 +526,13 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     stats.a2a_bytes_recv = recv;
   }
   if (mem == S2D_HOST) {
-    phase_begin(kPhCombine);
-    S2D_CUDA(cudaMemcpyAsync(pooled, d_pooled, (uint64_t)B * sum_dims * 4, cudaMemcpyDeviceToHost, stream));
-    phase_end();
-    S2D_CUDA(cudaStreamSynchronize(stream));
+    // read-back on the D2H stream: overlaps the upstream upload and the sort
+    S2D_CUDA(cudaEventRecord(ev_fwd, stream));
+    S2D_CUDA(cudaStreamWaitEvent(d2h_stream, ev_fwd, 0));
+    S2D_CUDA(cudaMemcpyAsync(pooled, d_pooled, (uint64_t)B * sum_dims * 4, cudaMemcpyDeviceToHost, d2h_stream));
+    S2D_CUDA(cudaEventRecord(ev_d2h, d2h_stream));
+    d2h_pending = true;
+    if (!async_host) S2D_CUDA(cudaStreamSynchronize(d2h_stream));
   }
   phase_end();
   fwd_done = true;
@@ -648,13 +665,22 @@ void Ctx::backward_update(const float* upstream, int mem) {
   const uint64_t BF = (uint64_t)B * F;
   const float* d_up = upstream;
   phase_begin(kPhInput);
+  bool up_wait = false;  // the compute stream still has to wait for the upload
   if (mem == S2D_HOST) {
+    // upload on the H2D stream once the previous update stopped reading the
+    // staging buffer; the compute stream waits only where rows are read
     upstream_stage.ensure((uint64_t)B * sum_dims * 4);
-    S2D_CUDA(cudaMemcpyAsync(upstream_stage.p, upstream, (uint64_t)B * sum_dims * 4, cudaMemcpyHostToDevice, stream));
+    if (upd_recorded) S2D_CUDA(cudaStreamWaitEvent(h2d_stream, ev_upd, 0));
+    S2D_CUDA(cudaMemcpyAsync(upstream_stage.p, upstream, (uint64_t)B * sum_dims * 4, cudaMemcpyHostToDevice,
+                             h2d_stream));
+    S2D_CUDA(cudaEventRecord(ev_up, h2d_stream));
     d_up = upstream_stage.as<float>();
+    up_wait = true;
   }
   const float* grad = d_up;
   if (N > 1) {
+    if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));
+    up_wait = false;
     // C2 fused: gradient rows stored straight into the owners' buffers; the
     // owner's receive layout equals its partial send layout, so the
     // lookup's (slot, val) pairs index it.
@@ -697,6 +723,8 @@ void Ctx::backward_update(const float* upstream, int mem) {
     const uint32_t* sk = sorted_in_b ? keys_b.as<uint32_t>() : keys_a.as<uint32_t>();
     const uint32_t* sv = sorted_in_b ? vals_b.as<uint32_t>() : vals_a.as<uint32_t>();
     phase_begin(kPhUpdate);
+    if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));
+    up_wait = false;
     counters.ensure(64);
     chunk_part.ensure(stream_partial_bytes(n, max_dim));
     StreamUpdateArgs ua{};
@@ -734,6 +762,13 @@ void Ctx::backward_update(const float* upstream, int mem) {
     uniq = 1;
   }
   (void)uniq;
+  if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));  // n == 0: nothing read it
+  if (mem == S2D_HOST) {
+    S2D_CUDA(cudaEventRecord(ev_upd, stream));
+    upd_recorded = true;
+  }
+  // the step is complete when its update and its pooled read-back are
+  if (d2h_pending) S2D_CUDA(cudaStreamWaitEvent(stream, ev_d2h, 0));
   phase_end();
   fwd_done = false;
   stats_counters_valid = n > 0;

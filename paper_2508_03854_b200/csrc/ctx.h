@@ -65,6 +65,12 @@ struct Ctx {
   int device = 0;
   uint32_t T = 1, M = 1, N = 1, rank = 0, group = 0, local = 0;
   cudaStream_t own_stream = nullptr, stream = nullptr;
+  // host<->device copies of S2D_HOST calls run on their own streams so the
+  // pooled read-back (D2H) overlaps the upstream upload (H2D) and the sort
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_d2h = nullptr, ev_up = nullptr, ev_upd = nullptr;
+  bool async_host = false;  // S2D_HOST pooled output valid at return (false) or after s2d_synchronize (true)
+  bool d2h_pending = false, upd_recorded = false;
   ncclComm_t world = nullptr, mp = nullptr, dp = nullptr;
   bool strict = true;
 

@@ -141,6 +141,39 @@ def test_cfg1_shape_bit_exact(port):
     assert np.array_equal(bits(w), bits(st.ws[0]))
 
 
+def test_async_host_copies_bit_exact(port):
+    """async host mode: pooled read-back on the D2H stream, upstream upload
+    on the H2D stream, pinned buffers reused every step (s2d_ctx_set_async_host)."""
+    import torch
+
+    from oracle import MeshState
+
+    rng = np.random.default_rng(5)
+    rows, dims, B = [5000, 300, 70000], [64, 64, 64], 256
+    spec = _spec(rows, dims, B, eta=0.1, c=1.0)
+    eng = _engine(rows, dims)
+    eng.set_strict(False)
+    eng.set_async_host(True)
+    eng.init_tables(9)
+    st = MeshState.init(port, spec, 9)
+    pooled_h = torch.empty((B, spec.sum_dims), dtype=torch.float32).pin_memory()
+    up_h = torch.empty((B, spec.sum_dims), dtype=torch.float32).pin_memory()
+    for step in range(4):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=12, zipf=1.1)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        lh = torch.from_numpy(lengths.view(np.int32)).pin_memory()
+        ih = torch.from_numpy(ids.view(np.int32)).pin_memory()
+        up_h.copy_(torch.from_numpy(up))
+        eng.forward(lh, ih, pooled_h, batch=B)
+        eng.backward_update(up_h)
+        eng.synchronize()
+        assert np.array_equal(bits(pooled_h.numpy()), bits(want)), step
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
 def test_hot_rows_long_segments(port):
     """Tiny tables => segments of thousands of contributions (chunked f64
     reduction).  Within 1e-5 relative; report bit-equal share."""
