@@ -24,7 +24,7 @@
 namespace s2d {
 namespace {
 
-constexpr int kStages = 4;
+constexpr int kStages = 2;
 constexpr int kRowsPerStage = 4;
 constexpr int kSlots = kStages * kRowsPerStage;
 constexpr int kBags = 32;  // bags per lookup unit (one per lane)
