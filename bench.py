@@ -85,59 +85,94 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons DURING the timed region."""
+    """SM clocks + clock-event (throttle) reasons sampled through NVML every
+    ~5 ms DURING the timed region (in-process thread; the device calls of the
+    timed loop release the GIL).  Falls back to `nvidia-smi -lms 20`."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, dev):
         self.dev = dev
-        self.lines = []
+        self.sm, self.reasons, self.mx = [], set(), None
+        self._stop = threading.Event()
+        self.t = None
         self.proc = None
+        self.lines = []
+
+    def _handle(self, nv):
+        import torch
+        try:
+            pr = torch.cuda.get_device_properties(self.dev)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def _poll(self, nv, h):
+        masks = [(n, getattr(nv, a, 0)) for n, a in self.REASONS]
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                for n, m in masks:
+                    if m and (r & m):
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            try:
+                q = "clocks.sm,clocks.max.sm," + ",".join("clocks_event_reasons." + n for n, _ in self.REASONS[:4])
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                     "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            parts = [x.strip() for x in line.split(",")]
+            try:
+                self.sm.append(float(parts[0]))
+                self.mx = float(parts[1])
+            except (ValueError, IndexError):
+                continue
+            for (nm, _), val in zip(self.REASONS, parts[2:6]):
+                if val.lower() in ("active", "1"):
+                    self.reasons.add(nm)
 
     def __exit__(self, *a):
+        self._stop.set()
         if self.proc:
-            time.sleep(0.25)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for nm, val in zip(names, parts[3:7]):
-                if val.lower() in ("active", "1"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm)}
 
 
 def algorithmic_bytes(w, nnz_own, unique, entries, n_mp, world_bf):
@@ -152,11 +187,14 @@ def algorithmic_bytes(w, nnz_own, unique, entries, n_mp, world_bf):
 
 
 def traffic_from_profiles(kernel):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture (profiles/traffic.json, tools/ncu_summarize.py)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f).get(kernel)
+        return (t["dram_bytes_per_launch"], f"profiles/{t['round']}: {t['source']}") if t else (None, None)
     except Exception:
-        return None
+        return None, None
 
 
 # ----------------------------------------------------------------------------
@@ -293,7 +331,7 @@ def run_ours(args):
     eng.synchronize()
     torch.cuda.synchronize()
     eng.phase_times()  # reset
-    eng.set_profiling(True)
+    eng.set_profiling(True)  # phase events on the engine stream, inside the timed region
     barrier()
     torch.cuda.synchronize()
     launches0 = s2d.launch_count()
@@ -370,7 +408,8 @@ def run_ours(args):
     for p in ("lookup", "update", "sort"):
         if p in per_phase:
             per_phase[p]["algo_gbs"] = ab[p] / (per_phase[p]["ms_per_launch"] / 1e3) / 1e9
-    kname = {"lookup": "k_owner_lookup", "update": "k_update", "sort": "k_radix_pass"}[dom]
+    kname = {"lookup": "k_lookup_ring", "update": "k_update_ring", "sort": "k_radix_pass"}[dom]
+    traffic = traffic_from_profiles(kname)
     line = {
         "metric": "embedding fwd+bwd+update samples/s", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -385,7 +424,8 @@ def run_ours(args):
                          f"{NB} distinct batches cycled"},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src,
-                     "traffic": traffic_from_profiles(kname)},
+                     "traffic": traffic[0], "traffic_source": traffic[1],
+                     "algorithmic_bytes_per_launch": ab[dom]},
         "phases": per_phase,
         "e2e": {"value": e2e, "unit": "samples/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "forward(host ids) -> backward_update(host upstream) -> synchronize, pinned buffers",
