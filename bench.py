@@ -244,7 +244,7 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     kind = "reference" if reference_available() else "port"
     if kind != "reference":
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libs2dref.so not built"}))
+        _emit({"impl": "reference", "unavailable": "oracle/_ref/libs2dref.so not built"})
         return
     # calibrate the sample to ~target seconds per step
     target = max(0.5, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
@@ -269,7 +269,7 @@ def run_reference(args):
                          "sample": f"{n} of {w.batch} samples per step, touched-row tables"},
         "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    _emit(line)
 
 
 # ----------------------------------------------------------------------------
@@ -294,7 +294,8 @@ def run_ours(args):
         obj = [s2d.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
-    tables = [s2d.TableConfig(int(r), int(d), float(w.batch * w.mean_len())) for r, d in zip(w.rows, w.dims)]
+    # expected lookups = ids + weighted distinct rows per table (Workload.plan_cost)
+    tables = [s2d.TableConfig(int(r), int(d), w.plan_cost(f, n_mp)) for f, (r, d) in enumerate(zip(w.rows, w.dims))]
     eng = s2d.Sparse2DEmbedding(tables, topo, rank=rank, device=local, strategy=w.strategy,
                                 optimizer=s2d.OptimizerConfig(eta=w.eta, eps=1e-8, c=w.c),
                                 weight_dtype=w.dtype, nccl_id=nid, strict=False)
@@ -355,6 +356,12 @@ def run_ours(args):
     ms_step = ms_max / args.steps
     value = world * w.batch * args.steps / (ms_max / 1e3)
     st = eng.stats()
+    mine = {"nnz_owned": st["nnz_owned"], "unique_rows": st["unique_rows"], "ms": ms,
+            "phase_ms": {p: round(v[0] / max(1, args.steps), 4) for p, v in phases.items() if v[1]}}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
 
     # ---- e2e through the public API with pinned host buffers ----
     K2 = args.e2e_steps or max(3, min(args.steps, 10))
@@ -435,11 +442,12 @@ def run_ours(args):
         "clocks": clk.summary(),
         "step_stats": {k: st[k] for k in ("nnz_owned", "unique_rows", "long_segments", "a2a_bytes_sent",
                                           "sync_bytes")},
+        "per_rank": per_rank,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args)
     if rank == 0:
-        print(json.dumps(line))
+        _emit(line)
     eng.close()
     if world > 1:
         dist.destroy_process_group()
@@ -463,7 +471,21 @@ def cpu_baseline(w, args):
             "sample": f"{k} steps x {n} of {w.batch} samples, tables compacted to touched rows"}
 
 
+def _emit(line):
+    """The ONE JSON line, on the real stdout (C-level prints were moved off it)."""
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
+
+
+_JSON_FD = 1
+
+
 def main():
+    global _JSON_FD
+    # Libraries print to fd 1 from C (e.g. NCCL's version banner under
+    # NCCL_DEBUG=VERSION); keep stdout for the JSON line alone.
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

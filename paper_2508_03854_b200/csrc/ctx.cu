@@ -113,12 +113,12 @@ Ctx::~Ctx() {
   for (PeerBuf* pb : {&p_flags, &p_xcnt, &p_len, &p_ids, &p_part, &p_grad, &p_pooled})
     for (void* q : pb->opened) cudaIpcCloseMemHandle(q);
   for (auto e : ev_pool) cudaEventDestroy(e);
-  for (cudaStream_t q : {h2d_stream, d2h_stream})
+  for (cudaStream_t q : {h2d_stream, d2h_stream, sort_stream})
     if (q) {
       cudaStreamSynchronize(q);
       cudaStreamDestroy(q);
     }
-  for (cudaEvent_t e : {ev_fwd, ev_d2h, ev_up, ev_upd})
+  for (cudaEvent_t e : {ev_fwd, ev_d2h, ev_up, ev_upd, ev_keys, ev_sorted})
     if (e) cudaEventDestroy(e);
   if (dp) ncclCommDestroy(dp);
   if (mp) ncclCommDestroy(mp);
@@ -144,7 +144,8 @@ void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uin
   stream = own_stream;
   S2D_CUDA(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
   S2D_CUDA(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&ev_fwd, &ev_d2h, &ev_up, &ev_upd})
+  S2D_CUDA(cudaStreamCreateWithFlags(&sort_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_fwd, &ev_d2h, &ev_up, &ev_upd, &ev_keys, &ev_sorted})
     S2D_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   err.ensure(4);
   S2D_CUDA(cudaMemsetAsync(err.p, 0, 4, stream));
@@ -352,6 +353,7 @@ void Ctx::synchronize_and_check() {
   S2D_CUDA(cudaSetDevice(device));
   S2D_CUDA(cudaStreamSynchronize(h2d_stream));
   S2D_CUDA(cudaStreamSynchronize(d2h_stream));
+  S2D_CUDA(cudaStreamSynchronize(sort_stream));
   S2D_CUDA(cudaMemcpyAsync(err_host.p, err.p, 4, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   check_faults();
@@ -372,6 +374,10 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   stats = s2d_step_stats{};
   stats_counters_valid = false;
   stats.nnz_local = nnz;
+  if (sort_pending) {  // a forward without its backward: its sort still reads the keys
+    S2D_CUDA(cudaStreamWaitEvent(stream, ev_sorted, 0));
+    sort_pending = false;
+  }
   // stage inputs
   phase_begin(kPhInput);
   const uint32_t* d_len = lengths;
@@ -498,6 +504,12 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
+    // the gradient rows' (slot, offset) pairs are final: sort them now
+    S2D_CUDA(cudaEventRecord(ev_keys, stream));
+    S2D_CUDA(cudaStreamWaitEvent(sort_stream, ev_keys, 0));
+    launch_sort(sort_stream);
+    S2D_CUDA(cudaEventRecord(ev_sorted, sort_stream));
+    sort_pending = true;
     phase_begin(kPhA2ALookup);
     peer_barrier();  // every owner's partials have landed in p_part
     phase_begin(kPhCombine);
@@ -657,6 +669,18 @@ void Ctx::read_counts() {
 
 // ---- backward + fused update ---------------------------------------------------
 
+// K3a on `st`: stable radix sort of this rank's (slot, gradient offset) pairs
+void Ctx::launch_sort(cudaStream_t st) {
+  const uint64_t n = nnz_own;
+  if (n == 0) return;
+  keys_b.ensure(n * 4);
+  vals_b.ensure(n * 4);
+  const int bits = std::max(1, bit_width(n_slots));
+  sort_tmp.ensure(radix_tmp_bytes(n, bits));
+  sorted_in_b = radix_sort_pairs(keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_b.as<uint32_t>(),
+                                 vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, st);
+}
+
 void Ctx::backward_update(const float* upstream, int mem) {
   if (!fwd_done) throw Error(S2D_EINVAL, "backward_update needs a preceding lookup_forward");
   if (!have_opt) throw Error(S2D_EINVAL, "set_optimizer first");
@@ -714,12 +738,11 @@ void Ctx::backward_update(const float* upstream, int mem) {
   uint64_t uniq = 0;
   if (n > 0) {
     phase_begin(kPhSort);
-    keys_b.ensure(n * 4);
-    vals_b.ensure(n * 4);
-    const int bits = std::max(1, bit_width(n_slots));
-    sort_tmp.ensure(radix_tmp_bytes(n, bits));
-    sorted_in_b = radix_sort_pairs(keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_b.as<uint32_t>(),
-                                   vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, stream);
+    if (sort_pending)
+      S2D_CUDA(cudaStreamWaitEvent(stream, ev_sorted, 0));
+    else
+      launch_sort(stream);
+    sort_pending = false;
     const uint32_t* sk = sorted_in_b ? keys_b.as<uint32_t>() : keys_a.as<uint32_t>();
     const uint32_t* sv = sorted_in_b ? vals_b.as<uint32_t>() : vals_a.as<uint32_t>();
     phase_begin(kPhUpdate);

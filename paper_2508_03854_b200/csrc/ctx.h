@@ -71,6 +71,12 @@ struct Ctx {
   cudaEvent_t ev_fwd = nullptr, ev_d2h = nullptr, ev_up = nullptr, ev_upd = nullptr;
   bool async_host = false;  // S2D_HOST pooled output valid at return (false) or after s2d_synchronize (true)
   bool d2h_pending = false, upd_recorded = false;
+  // N > 1: the (slot, row) sort runs on its own stream from the end of the
+  // owner lookup, beside the combine and the gradient all-to-all
+  cudaStream_t sort_stream = nullptr;
+  cudaEvent_t ev_keys = nullptr, ev_sorted = nullptr;
+  bool sort_pending = false;
+  void launch_sort(cudaStream_t st);
   ncclComm_t world = nullptr, mp = nullptr, dp = nullptr;
   bool strict = true;
 

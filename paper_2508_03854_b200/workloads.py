@@ -53,6 +53,27 @@ class Workload:
         p = L ** (-self.len_alpha)
         return float((L * p).sum() / p.sum())
 
+    # ---- planning cost ----
+    # One distinct row costs about as much as UNIQUE_WEIGHT id contributions
+    # (segment flush: moment + row read-modify-write, an L2 miss for big
+    # tables), so the table-wise LPT of plan_greedy is fed expected ids plus
+    # weighted expected distinct rows as each table's "expected lookups".
+    UNIQUE_WEIGHT = 4.0
+
+    def expected_unique(self, f: int, n: float) -> float:
+        """E[#distinct rows] among n Zipf draws from table f."""
+        rows, s = int(self.rows[f]), self.zipf
+        if rows > 20_000_000:
+            return float(min(n, rows))
+        k = np.arange(1, rows + 1, dtype=np.float64)
+        p = k ** (-s)
+        p /= p.sum()
+        return float(np.sum(-np.expm1(n * np.log1p(-p))))
+
+    def plan_cost(self, f: int, n_req: int) -> float:
+        ids = self.batch * self.mean_len() * n_req
+        return ids + self.UNIQUE_WEIGHT * self.expected_unique(f, ids)
+
     # ---- sampling ----
     def _sample_ids(self, rng, rows: int, n: int) -> np.ndarray:
         if n == 0:
