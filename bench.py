@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     p.add_argument("--seed", type=int, default=1234)
+    p.add_argument("--plan-rotate", type=int, default=0, help="experiment: rotate the plan's local ranks by k")
     return p.parse_args()
 
 
@@ -86,7 +87,7 @@ def load_peaks():
 
 class ClockSampler:
     """SM clocks + clock-event (throttle) reasons sampled through NVML every
-    ~5 ms DURING the timed region (in-process thread; the device calls of the
+    ~10 ms DURING the timed region (in-process thread; the device calls of the
     timed loop release the GIL).  Falls back to `nvidia-smi -lms 20`."""
 
     REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
@@ -123,7 +124,7 @@ class ClockSampler:
                         self.reasons.add(n)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.010)
 
     def __enter__(self):
         try:
@@ -296,7 +297,13 @@ def run_ours(args):
         nid = obj[0]
     # expected lookups = ids + weighted distinct rows per table (Workload.plan_cost)
     tables = [s2d.TableConfig(int(r), int(d), w.plan_cost(f, n_mp)) for f, (r, d) in enumerate(zip(w.rows, w.dims))]
-    eng = s2d.Sparse2DEmbedding(tables, topo, rank=rank, device=local, strategy=w.strategy,
+    plan = None
+    if args.plan_rotate:
+        prof = [(i, t.rows * t.dim * 4, t.expected_lookups, t.rows) for i, t in enumerate(tables)]
+        plan = s2d.plan_greedy(prof, n_mp, w.strategy)
+        for e in plan:
+            e["local_rank"] = (e["local_rank"] + args.plan_rotate) % n_mp
+    eng = s2d.Sparse2DEmbedding(tables, topo, rank=rank, device=local, strategy=w.strategy, plan=plan,
                                 optimizer=s2d.OptimizerConfig(eta=w.eta, eps=1e-8, c=w.c),
                                 weight_dtype=w.dtype, nccl_id=nid, strict=False)
     # a real (non-NULL) stream shared by the engine and the timing events
@@ -316,10 +323,16 @@ def run_ours(args):
     pooled = torch.empty((w.batch, w.sum_dims), dtype=torch.float32, device="cuda")
     nnz_mean = float(np.mean([len(h[1]) for h in host]))
 
+    host_s = {"forward": 0.0, "backward": 0.0}
+
     def step(k):
         l, i, u = dev[k % NB]
+        t0 = time.perf_counter()
         eng.forward(l, i, "engine", batch=w.batch)  # zero-copy output (engine buffer)
+        t1 = time.perf_counter()
         eng.backward_update(u)
+        host_s["forward"] += t1 - t0
+        host_s["backward"] += time.perf_counter() - t1
         if m > 1:
             eng.sync_replicas()
 
@@ -337,6 +350,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     launches0 = s2d.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    host_s["forward"] = host_s["backward"] = 0.0
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for k in range(args.steps):
@@ -357,7 +371,8 @@ def run_ours(args):
     value = world * w.batch * args.steps / (ms_max / 1e3)
     st = eng.stats()
     mine = {"nnz_owned": st["nnz_owned"], "unique_rows": st["unique_rows"], "ms": ms,
-            "phase_ms": {p: round(v[0] / max(1, args.steps), 4) for p, v in phases.items() if v[1]}}
+            "phase_ms": {p: round(v[0] / max(1, args.steps), 4) for p, v in phases.items() if v[1]},
+            "host_ms_per_step": {k: round(1e3 * v / max(1, args.steps), 4) for k, v in host_s.items()}}
     per_rank = [mine]
     if world > 1:
         per_rank = [None] * world

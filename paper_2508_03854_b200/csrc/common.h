@@ -112,6 +112,8 @@ struct LookupArgs {
   int emit_keys;
   uint32_t uni_d4;             // dim/4 shared by every table (0: mixed dims)
   uint32_t* ticket;            // work counter of the persistent warps (zeroed per launch)
+  uint64_t unit_rot;           // ticket t processes 32-bag unit (t + unit_rot) % units: owners
+                               // start at different requesters so their NVLink stores spread out
   // non-direct: the partial of a bag of requester n goes to
   // peer_out.p[n] + peer_adj[n] + eoff[bag] (requester n's receive buffer,
   // over NVLink); the sort vals stay local (eoff[bag] / 4)

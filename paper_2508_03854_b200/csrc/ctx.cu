@@ -470,7 +470,6 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     launch_bucket_permute(ba, stream);  // ids straight into the owners' receive buffers
     peer_barrier();
     // ---- owner side: partial pools written into the requesters' buffers ----
-    phase_begin(kPhLookup);
     own_idoff.ensure(((uint64_t)N * BF + 1) * 4);
     own_eoff.ensure(((uint64_t)N * BF + 1) * 8);
     scan_u32_to_u32(p_len.buf.as<uint32_t>(), own_idoff.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p,
@@ -503,6 +502,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     for (uint32_t n = 0; n < N; ++n) a.peer_adj[n] = (int64_t)part_base_at_req[n] - (int64_t)own_eoff_bound[n];
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
+    a.unit_rot = ((uint64_t)((local + 1) % N) * BF) / 32;  // start at the next requester
+    phase_begin(kPhLookup);
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     // the gradient rows' (slot, offset) pairs are final: sort them now
     S2D_CUDA(cudaEventRecord(ev_keys, stream));

@@ -175,8 +175,9 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   for (;;) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(a.ticket, 1u);
-    const uint64_t unit = __shfl_sync(0xffffffffu, t, 0);
-    if (unit >= n_units) break;
+    const uint64_t tk = __shfl_sync(0xffffffffu, t, 0);
+    if (tk >= n_units) break;
+    const uint64_t unit = (tk + a.unit_rot) % n_units;
     const uint64_t b0 = unit * kBags;
     const uint32_t nb = (n_bags - b0) < (uint64_t)kBags ? (uint32_t)(n_bags - b0) : (uint32_t)kBags;
     const uint64_t my_bag = b0 + min(lane, nb - 1);
