@@ -211,8 +211,11 @@ void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32
                          double eta, double eps, double c, int sgd, uint32_t* err, cudaStream_t st);
 
 // replica sync kernels (k_sync.cu)
-void launch_dirty_compact(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, uint32_t* count,
-                          void* tmp, size_t tmp_bytes, cudaStream_t st);
+void launch_flag_count(const uint8_t* dirty, uint32_t n_slots, uint32_t* count, void* tmp, size_t tmp_bytes,
+                       cudaStream_t st);
+void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, const void* tmp, cudaStream_t st);
+size_t flag_tmp_bytes(uint32_t n_slots);
+void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, cudaStream_t st);
 void launch_pack_rows(const FeatDev* feats, const uint32_t* vbase_sorted,
                       const uint32_t* feat_of_vbase, uint32_t n_feat_owned, const uint32_t* list,
                       const uint32_t* count, const void* weights, int bf16, const float* moments,

@@ -815,32 +815,54 @@ void Ctx::replica_sync() {
   if (M <= 1 || !F) return;
   S2D_CUDA(cudaSetDevice(device));
   phase_begin(kPhSync);
-  // union of dirty rows across the DP group
-  S2D_NCCL(ncclAllReduce(dirty.p, dirty.p, n_slots, ncclUint8, ncclMax, dp, stream));
-  sync_list.ensure((uint64_t)std::max<uint32_t>(n_slots, 1) * 4);
-  sync_count.ensure(16);
-  sync_tmp.ensure(((uint64_t)n_slots / 4096 + 2) * 4);
-  launch_dirty_compact(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_count.as<uint32_t>(), sync_tmp.p,
-                       sync_tmp.cap, stream);
-  uint32_t count = 0;
-  S2D_CUDA(cudaMemcpyAsync(h_counts.p, sync_count.p, 4, cudaMemcpyDeviceToHost, stream));
+  // Union of the dirty rows across the DP group in O(dirty rows) wire bytes:
+  // each replica compacts its own flags into an ascending slot list, the
+  // lists are all-gathered, every replica flags the others' slots and
+  // compacts again -> the same ascending union list everywhere.
+  sync_tmp.ensure(flag_tmp_bytes(n_slots));
+  sync_count.ensure(64 + (size_t)M * 4);
+  uint32_t* d_count = sync_count.as<uint32_t>();
+  uint32_t* d_counts = d_count + 16;  // [M] list lengths of the group
+  launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
+  S2D_NCCL(ncclAllGather(d_count, d_counts, 1, ncclUint32, dp, stream));
+  S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_counts, (size_t)M * 4, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
-  count = *h_counts.as<uint32_t>();
-  stats.dirty_rows = count;
-  if (count) {
-    const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
-    sync_packed.ensure((uint64_t)count * row_floats * 4);
-    sync_gathered.ensure((uint64_t)count * row_floats * 4 * M);
-    launch_pack_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
-                     (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), sync_count.as<uint32_t>(), weights.p,
-                     bf16, moments.as<float>(), row_floats, sync_packed.as<float>(), count, stream);
-    S2D_NCCL(ncclAllGather(sync_packed.p, sync_gathered.p, (size_t)count * row_floats, ncclFloat32, dp, stream));
-    launch_mean_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
-                     (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), sync_count.as<uint32_t>(),
-                     sync_gathered.as<float>(), M, row_floats, count, weights.p, bf16, moments.as<float>(),
-                     opt.variant == S2D_SGD, dirty.as<uint8_t>(), stream);
-    stats.sync_bytes = (uint64_t)count * row_floats * 4 * (M - 1);
+  const uint32_t* hc = h_counts.as<uint32_t>();
+  const uint32_t mine = hc[group];
+  uint32_t cmax = 0;
+  for (uint32_t g = 0; g < M; ++g) cmax = std::max(cmax, hc[g]);
+  if (cmax == 0) {
+    stats.dirty_rows = 0;
+    phase_end();
+    finish_call();
+    return;
   }
+  sync_list.ensure((uint64_t)cmax * 4);
+  launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+  if (cmax > mine)  // pad to the longest list (0xffffffff is not a slot)
+    S2D_CUDA(cudaMemsetAsync(sync_list.as<uint32_t>() + mine, 0xff, (size_t)(cmax - mine) * 4, stream));
+  sync_lists.ensure((uint64_t)cmax * M * 4);
+  S2D_NCCL(ncclAllGather(sync_list.p, sync_lists.p, cmax, ncclUint32, dp, stream));
+  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
+  launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
+  S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_count, 4, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  const uint32_t count = *h_counts.as<uint32_t>();
+  stats.dirty_rows = count;
+  sync_list.ensure((uint64_t)count * 4);
+  launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+  const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
+  sync_packed.ensure((uint64_t)count * row_floats * 4);
+  sync_gathered.ensure((uint64_t)count * row_floats * 4 * M);
+  launch_pack_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                   (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), d_count, weights.p, bf16,
+                   moments.as<float>(), row_floats, sync_packed.as<float>(), count, stream);
+  S2D_NCCL(ncclAllGather(sync_packed.p, sync_gathered.p, (size_t)count * row_floats, ncclFloat32, dp, stream));
+  launch_mean_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                   (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), d_count, sync_gathered.as<float>(), M,
+                   row_floats, count, weights.p, bf16, moments.as<float>(), opt.variant == S2D_SGD,
+                   dirty.as<uint8_t>(), stream);
+  stats.sync_bytes = (uint64_t)count * row_floats * 4 * (M - 1) + (uint64_t)cmax * 4 * (M - 1);
   phase_end();
   finish_call();
 }

@@ -118,7 +118,7 @@ struct Ctx {
   uint64_t epoch = 0;
   DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
-  DevBuf sync_list, sync_count, sync_packed, sync_gathered, sync_tmp;
+  DevBuf sync_list, sync_lists, sync_count, sync_packed, sync_gathered, sync_tmp;
   HostBuf h_counts;
   std::vector<uint64_t> nnz_to, nnz_from, ef_to, ef_from, send_bound, eoff_req_bound, own_eoff_bound,
       ids_base_at_owner, part_base_at_req, grad_base_at_owner;

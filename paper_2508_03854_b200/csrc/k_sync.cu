@@ -1,7 +1,8 @@
 // K5 replica sync (sync_replicas, src/trainer.cpp:547-596):
-//   dirty_compact  ordered list of slots dirty in any replica (after the
-//                  byte-max all-reduce of the dirty flags); identical order
-//                  on every replica so the all-gathered rows line up
+//   flag_count /   ascending list of this replica's dirty slots; the
+//   flag_write     replicas all-gather their lists, mark each other's slots
+//   mark_slots     dirty and compact again, so every replica holds the same
+//                  ascending union list and the all-gathered rows line up
 //   pack_rows      (w row, v) of each listed slot -> fp32 wire rows
 //   mean_rows      x = f32((sum_{g ascending} f64(x_g)) * (1/M)) per element
 //                  (deterministic_mean_inplace, src/topology.cpp:150-163),
@@ -19,40 +20,31 @@ constexpr int kThreads = 256;
 constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;
 
+// 16 flags per thread, one 16-byte load when the tile is full
+__device__ __forceinline__ void load_flags(const uint8_t* __restrict__ flags, uint64_t base, uint32_t n,
+                                           uint32_t (&f)[kItems]) {
+  if (base + kItems <= n) {
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(flags + base));
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) f[i] = ((w[i / 4] >> (8 * (i % 4))) & 0xffu) != 0;
+  } else {
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) f[i] = (base + i < n) ? (flags[base + i] != 0) : 0u;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) k_flag_count(const uint8_t* __restrict__ flags, uint32_t n,
                                                          uint32_t* __restrict__ tile_sum) {
   using BR = cub::BlockReduce<uint32_t, kThreads>;
   __shared__ typename BR::TempStorage tmp;
-  const uint64_t base = (uint64_t)blockIdx.x * kTile;
+  uint32_t f[kItems];
+  load_flags(flags, (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kItems, n, f);
   uint32_t c = 0;
 #pragma unroll
-  for (int i = 0; i < kItems; ++i) {
-    const uint64_t k = base + (uint64_t)i * kThreads + threadIdx.x;
-    if (k < n) c += flags[k] != 0;
-  }
+  for (int i = 0; i < kItems; ++i) c += f[i];
   const uint32_t s = BR(tmp).Sum(c);
   if (threadIdx.x == 0) tile_sum[blockIdx.x] = s;
-}
-
-__global__ void __launch_bounds__(kThreads) k_flag_scan_tiles(uint32_t* __restrict__ tile_sum,
-                                                              uint32_t ntiles, uint32_t* __restrict__ count) {
-  using BS = cub::BlockScan<uint32_t, kThreads>;
-  __shared__ typename BS::TempStorage tmp;
-  __shared__ uint32_t carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (uint32_t base = 0; base < ntiles; base += kThreads) {
-    const uint32_t k = base + threadIdx.x;
-    const uint32_t x = k < ntiles ? tile_sum[k] : 0u;
-    uint32_t ex, tot;
-    BS(tmp).ExclusiveSum(x, ex, tot);
-    const uint32_t c0 = carry;
-    if (k < ntiles) tile_sum[k] = c0 + ex;
-    __syncthreads();
-    if (threadIdx.x == 0) carry = c0 + tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *count = carry;
 }
 
 __global__ void __launch_bounds__(kThreads) k_flag_write(const uint8_t* __restrict__ flags, uint32_t n,
@@ -62,14 +54,22 @@ __global__ void __launch_bounds__(kThreads) k_flag_write(const uint8_t* __restri
   __shared__ typename BS::TempStorage tmp;
   const uint64_t base = (uint64_t)blockIdx.x * kTile + (uint64_t)threadIdx.x * kItems;
   uint32_t f[kItems];
-#pragma unroll
-  for (int i = 0; i < kItems; ++i) f[i] = (base + i < n) ? (flags[base + i] != 0) : 0u;
+  load_flags(flags, base, n, f);
   uint32_t ex[kItems];
   BS(tmp).ExclusiveSum(f, ex);
   const uint32_t off = tile_sum[blockIdx.x];
 #pragma unroll
   for (int i = 0; i < kItems; ++i)
     if (f[i]) list[off + ex[i]] = (uint32_t)(base + i);
+}
+
+// union: flag every slot another replica listed (0xffffffff = padding)
+__global__ void k_mark_slots(const uint32_t* __restrict__ lists, uint64_t n, uint32_t n_slots,
+                             uint8_t* __restrict__ flags) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = __ldg(lists + i);
+    if (s < n_slots) flags[s] = 1;
+  }
 }
 
 template <typename WT>
@@ -138,20 +138,43 @@ __global__ void k_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, 
 
 }  // namespace
 
-void launch_dirty_compact(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, uint32_t* count,
-                          void* tmp, size_t tmp_bytes, cudaStream_t st) {
-  const uint32_t ntiles = (n_slots + kTile - 1) / kTile;
-  if ((size_t)(ntiles + 1) * 4 > tmp_bytes) throw Error(S2D_ECUDA, "compaction workspace too small");
+// tmp layout: tile counts [ntiles] | their exclusive scan [ntiles + 1] | scan workspace
+static uint32_t flag_tiles(uint32_t n_slots) { return (n_slots + kTile - 1) / kTile; }
+
+size_t flag_tmp_bytes(uint32_t n_slots) {
+  const uint32_t nt = flag_tiles(n_slots);
+  return ((size_t)2 * nt + 2) * 4 + scan_tmp_bytes((uint64_t)nt + 1) + 16;
+}
+
+void launch_flag_count(const uint8_t* dirty, uint32_t n_slots, uint32_t* count, void* tmp, size_t tmp_bytes,
+                       cudaStream_t st) {
+  const uint32_t ntiles = flag_tiles(n_slots);
+  if (flag_tmp_bytes(n_slots) > tmp_bytes) throw Error(S2D_ECUDA, "compaction workspace too small");
   if (ntiles == 0) {
     S2D_CUDA(cudaMemsetAsync(count, 0, 4, st));
     return;
   }
   uint32_t* ts = reinterpret_cast<uint32_t*>(tmp);
+  uint32_t* tx = ts + ntiles;
+  char* sw = reinterpret_cast<char*>(tx + ntiles + 2);
+  sw += (16 - reinterpret_cast<uintptr_t>(sw) % 16) % 16;
   k_flag_count<<<ntiles, kThreads, 0, st>>>(dirty, n_slots, ts);
   S2D_LAUNCH_CHECK();
-  k_flag_scan_tiles<<<1, kThreads, 0, st>>>(ts, ntiles, count);
+  scan_u32_to_u32(ts, tx, ntiles, st, sw, scan_tmp_bytes((uint64_t)ntiles + 1));
+  S2D_CUDA(cudaMemcpyAsync(count, tx + ntiles, 4, cudaMemcpyDeviceToDevice, st));
+}
+
+void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, const void* tmp, cudaStream_t st) {
+  const uint32_t ntiles = flag_tiles(n_slots);
+  if (ntiles == 0) return;
+  k_flag_write<<<ntiles, kThreads, 0, st>>>(dirty, n_slots, reinterpret_cast<const uint32_t*>(tmp) + ntiles, list);
   S2D_LAUNCH_CHECK();
-  k_flag_write<<<ntiles, kThreads, 0, st>>>(dirty, n_slots, ts, list);
+}
+
+void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, cudaStream_t st) {
+  if (!n) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  k_mark_slots<<<grid, 256, 0, st>>>(lists, n, n_slots, dirty);
   S2D_LAUNCH_CHECK();
 }
 
