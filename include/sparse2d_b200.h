@@ -186,6 +186,20 @@ int s2d_shard_read(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_h
 /* Owned range of `table` on this rank ([0,0) when none). */
 int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* row_hi);
 
+/* S2DCKPT1 checkpoint, byte-compatible with the reference's
+ * save_checkpoint / load_checkpoint (src/embedding.cpp:133-219): "S2DCKPT1",
+ * u32 count, per table u32 version = 1, u32 table_id, u64 rows, u64 dim,
+ * f32 weights[rows*dim], f32 moments[rows], little-endian, written to
+ * path.tmp and renamed.  Collective over all ranks of the context: DP group
+ * 0's ranks write their own row ranges in place (the replica
+ * Trainer::save_tables saves, src/trainer.cpp:875-878); every rank loads its
+ * owned rows into its replica (Trainer::load_tables copies the file into
+ * all replicas, trainer.cpp:880-896).  Table count / shape mismatch and IO
+ * failures -> S2D_ERUNTIME; bf16 shards are widened on save and rounded to
+ * nearest-even on load. */
+int s2d_save_tables(s2d_ctx* ctx, const char* path);
+int s2d_load_tables(s2d_ctx* ctx, const char* path);
+
 /* Forward of one step for this rank's batch of `batch` samples: sample-major
  * bags (s, f) given as lengths[batch*F] and the `nnz` global row ids of all
  * bags concatenated.  Runs K1 input-dist bucketing + id all-to-all, K2 owner

@@ -335,6 +335,33 @@ class Oracle:
         del keep
         return pooled, dump
 
+    def save_checkpoint(self, path: str, rows, dims, w: np.ndarray, v: np.ndarray) -> None:
+        """S2DCKPT1 of the flat replica (embedding.cpp:133-185); table_id = f."""
+        rows = np.ascontiguousarray(rows, np.uint32)
+        dims = np.ascontiguousarray(dims, np.uint32)
+        w = np.ascontiguousarray(w, np.float32)
+        v = np.ascontiguousarray(v, np.float32)
+        fn = getattr(self.lib, self._p + "save_checkpoint")
+        fn.argtypes = [C.c_char_p, C.c_uint32, _u32p, _u32p, _f32p, _f32p]
+        fn.restype = C.c_int
+        if fn(path.encode(), len(rows), rows, dims, w, v) != 0:
+            raise RuntimeError("checkpoint write failed")
+
+    def load_checkpoint(self, path: str, rows, dims):
+        """(w, v) flat replica from an S2DCKPT1 file (reference loader only)."""
+        if self.kind != "reference":
+            return read_checkpoint(path)[1:]
+        rows = np.ascontiguousarray(rows, np.uint32)
+        dims = np.ascontiguousarray(dims, np.uint32)
+        w = np.empty(int((rows.astype(np.uint64) * dims).sum()), np.float32)
+        v = np.empty(int(rows.astype(np.uint64).sum()), np.float32)
+        fn = self.lib.ref_load_checkpoint
+        fn.argtypes = [C.c_char_p, C.c_uint32, _u32p, _u32p, _f32p, _f32p]
+        fn.restype = C.c_int
+        if fn(path.encode(), len(rows), rows, dims, w, v) != 0:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return w, v
+
     def sync(self, spec: MeshSpec, ws, vs, dirties):
         M = len(ws)
         rows = np.ascontiguousarray(spec.rows, np.uint32)
@@ -388,3 +415,27 @@ def row_wise_plan(rows, n) -> np.ndarray:
             if hi > lo:
                 out.append((t, lo, hi, j))
     return np.array(out, np.uint32).reshape(-1, 4)
+
+
+def read_checkpoint(path: str):
+    """Parse an S2DCKPT1 file (embedding.cpp:187-219): (tables, w, v) with
+    tables = [(version, table_id, rows, dim)] and the flat replica arrays."""
+    b = open(path, "rb").read()
+    if b[:8] != b"S2DCKPT1":
+        raise RuntimeError("not a checkpoint file: " + path)
+    (count,) = np.frombuffer(b, np.uint32, 1, 8)
+    off, tables, ws, vs = 12, [], [], []
+    for _ in range(int(count)):
+        ver, tid = np.frombuffer(b, np.uint32, 2, off)
+        rows, dim = np.frombuffer(b, np.uint64, 2, off + 8)
+        off += 24
+        n = int(rows) * int(dim)
+        ws.append(np.frombuffer(b, np.float32, n, off))
+        off += 4 * n
+        vs.append(np.frombuffer(b, np.float32, int(rows), off))
+        off += 4 * int(rows)
+        tables.append((int(ver), int(tid), int(rows), int(dim)))
+    if off != len(b):
+        raise RuntimeError("trailing bytes in checkpoint: " + path)
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.float32)
+    return tables, cat(ws), cat(vs)

@@ -17,6 +17,7 @@
 #include <cstring>
 #include <functional>
 #include <stdexcept>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -373,6 +374,54 @@ int ref_sync(uint32_t M, uint32_t F, const uint32_t* rows, const uint32_t* dims,
     voff += rows[f];
   }
   return 0;
+}
+
+// save_checkpoint / load_checkpoint (embedding.cpp:133-219) on the flat
+// replica layout (table f = table_id f).  0 = ok, -1 = error (ref_last_error).
+int ref_save_checkpoint(const char* path, uint32_t F, const uint32_t* rows, const uint32_t* dims, const float* w,
+                        const float* v) {
+  try {
+    std::vector<EmbeddingTable> tables(F);
+    std::vector<const EmbeddingTable*> ptrs(F);
+    size_t woff = 0, voff = 0;
+    for (uint32_t f = 0; f < F; ++f) {
+      EmbeddingTable& t = tables[f];
+      t.table_id = f;
+      t.rows = rows[f];
+      t.dim = dims[f];
+      t.weights.assign(w + woff, w + woff + (size_t)rows[f] * dims[f]);
+      t.moments.assign(v + voff, v + voff + rows[f]);
+      woff += (size_t)rows[f] * dims[f];
+      voff += rows[f];
+      ptrs[f] = &t;
+    }
+    save_checkpoint(path, ptrs);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int ref_load_checkpoint(const char* path, uint32_t F, const uint32_t* rows, const uint32_t* dims, float* w,
+                        float* v) {
+  try {
+    const auto tables = load_checkpoint(path);
+    if (tables.size() != F) throw std::runtime_error("checkpoint table count mismatch");
+    size_t woff = 0, voff = 0;
+    for (uint32_t f = 0; f < F; ++f) {
+      const EmbeddingTable& t = tables[f];
+      if (t.rows != rows[f] || t.dim != dims[f]) throw std::runtime_error("checkpoint shape mismatch");
+      std::copy(t.weights.begin(), t.weights.end(), w + woff);
+      std::copy(t.moments.begin(), t.moments.end(), v + voff);
+      woff += (size_t)rows[f] * dims[f];
+      voff += rows[f];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"

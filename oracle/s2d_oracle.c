@@ -26,6 +26,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -630,4 +631,32 @@ void or_synthetic_upstream(uint64_t seed, uint64_t step, uint32_t rank, uint32_t
       col += dims[f];
     }
   }
+}
+
+/* ---- S2DCKPT1 checkpoint writer (embedding.cpp:133-185) --------------------
+ * "S2DCKPT1", u32 table count, then per table: u32 version (1), u32 table_id,
+ * u64 rows, u64 dim, f32 weights[rows*dim], f32 moments[rows]; little-endian
+ * host order; written to path.tmp and renamed.  Tables are the flat replica
+ * (table f's rows at woff/voff), table_id = f.  Returns 0, or -1 on IO error. */
+int or_save_checkpoint(const char* path, uint32_t F, const uint32_t* rows, const uint32_t* dims, const float* w,
+                       const float* v) {
+  char tmp[4096];
+  if (strlen(path) + 5 >= sizeof(tmp)) return -1;
+  strcpy(tmp, path);
+  strcat(tmp, ".tmp");
+  FILE* f = fopen(tmp, "wb");
+  if (!f) return -1;
+  int ok = fwrite("S2DCKPT1", 1, 8, f) == 8 && fwrite(&F, 4, 1, f) == 1;
+  size_t woff = 0, voff = 0;
+  for (uint32_t t = 0; ok && t < F; ++t) {
+    const uint32_t version = 1;
+    const uint64_t r = rows[t], d = dims[t];
+    ok = fwrite(&version, 4, 1, f) == 1 && fwrite(&t, 4, 1, f) == 1 && fwrite(&r, 8, 1, f) == 1 &&
+         fwrite(&d, 8, 1, f) == 1 && fwrite(w + woff, 4, r * d, f) == r * d && fwrite(v + voff, 4, r, f) == r;
+    woff += r * d;
+    voff += r;
+  }
+  if (fclose(f) != 0) ok = 0;
+  if (!ok) return -1;
+  return rename(tmp, path) == 0 ? 0 : -1;
 }

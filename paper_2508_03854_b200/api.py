@@ -13,6 +13,7 @@ this module only marshals arguments.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
@@ -256,6 +257,16 @@ class Sparse2DEmbedding:
 
     def set_strict(self, strict: bool):
         L.check(self.lib.s2d_ctx_set_strict(self._ctx, 1 if strict else 0))
+
+    def save_tables(self, path: str):
+        """S2DCKPT1 checkpoint of DP group 0's replica (Trainer::save_tables,
+        trainer.cpp:875-878); collective over every rank of the mesh."""
+        L.check(self.lib.s2d_save_tables(self._ctx, os.fsencode(path)))
+
+    def load_tables(self, path: str):
+        """Load an S2DCKPT1 checkpoint into every replica (Trainer::load_tables,
+        trainer.cpp:880-896)."""
+        L.check(self.lib.s2d_load_tables(self._ctx, os.fsencode(path)))
 
     def set_async_host(self, on: bool):
         """Host-memory pooled output completes asynchronously (s2d_ctx_set_async_host)."""

@@ -168,6 +168,14 @@ int s2d_shard_read(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_h
   return guarded([&] { as_ctx(ctx)->shard_io(table, row_lo, row_hi, w, v, false); });
 }
 
+int s2d_save_tables(s2d_ctx* ctx, const char* path) {
+  return guarded([&] { as_ctx(ctx)->save_tables(path); });
+}
+
+int s2d_load_tables(s2d_ctx* ctx, const char* path) {
+  return guarded([&] { as_ctx(ctx)->load_tables(path); });
+}
+
 int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* row_hi) {
   return guarded([&] {
     auto* c = as_ctx(ctx);

@@ -25,13 +25,6 @@
 
 namespace s2d {
 
-#define S2D_NCCL(call)                                                                    \
-  do {                                                                                    \
-    ncclResult_t r_ = (call);                                                             \
-    if (r_ != ncclSuccess)                                                                \
-      throw ::s2d::Error(S2D_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
-  } while (0)
-
 void DevBuf::ensure(size_t bytes) {
   if (bytes <= cap && p) return;
   release();
@@ -149,7 +142,7 @@ void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uin
     S2D_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   err.ensure(4);
   S2D_CUDA(cudaMemsetAsync(err.p, 0, 4, stream));
-  err_host.ensure(4);
+  err_host.ensure(16);
   *err_host.as<uint32_t>() = 0;
   h_counts.ensure(4096);
   if (T > 1) {

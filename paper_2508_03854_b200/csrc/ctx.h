@@ -10,6 +10,13 @@
 
 #include "common.h"
 
+#define S2D_NCCL(call)                                                                    \
+  do {                                                                                    \
+    ncclResult_t r_ = (call);                                                             \
+    if (r_ != ncclSuccess)                                                                \
+      throw ::s2d::Error(S2D_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
 namespace s2d {
 
 struct DevBuf {
@@ -149,6 +156,11 @@ struct Ctx {
   void backward_update(const float* upstream, int mem);
   void replica_sync();
   void synchronize_and_check();
+  // S2DCKPT1 checkpoint of DP group 0's replica (checkpoint.cpp)
+  DevBuf bar_buf;
+  int world_barrier(int failed);
+  void save_tables(const char* path);
+  void load_tables(const char* path);
   void debug_read(int which, void* out, uint64_t cap, uint64_t* n);
 
  private:

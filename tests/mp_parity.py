@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--sgd", action="store_true")
     ap.add_argument("--batch", type=int, default=48)
     ap.add_argument("--engine-out", action="store_true", help="zero-copy pooled output (owners write it)")
+    ap.add_argument("--ckpt", action="store_true", help="S2DCKPT1 save from the mesh + load into every replica")
     args = ap.parse_args()
 
     import torch
@@ -92,8 +93,22 @@ def main():
         lo, hi = eng.owned_range(f)
         if hi > lo:
             shard[f] = (lo, hi) + eng.read_rows(f, lo, hi)
+    ckpt_path, loaded = None, {}
+    if args.ckpt:
+        import tempfile
+
+        box = [tempfile.mkdtemp(prefix="s2d_ckpt_") + "/mesh.ckpt" if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        ckpt_path = box[0]
+        eng.save_tables(ckpt_path)
+        eng.init_tables(12345)  # clobber, then restore from the file
+        eng.load_tables(ckpt_path)
+        for f in range(F):
+            lo, hi = eng.owned_range(f)
+            if hi > lo:
+                loaded[f] = (lo, hi) + eng.read_rows(f, lo, hi)
     gathered = [None] * world if rank == 0 else None
-    dist.gather_object((pooled_mine, layouts, shard), gathered, dst=0)
+    dist.gather_object((pooled_mine, layouts, shard, loaded), gathered, dst=0)
     eng.close()
     if rank != 0:
         dist.barrier()
@@ -154,11 +169,26 @@ def main():
                 fails.append(f"weights rank {r} table {f}: max|d|={np.max(np.abs(w - ww))}")
             if not np.array_equal(v.view(np.uint32), vv.view(np.uint32)):
                 fails.append(f"moments rank {r} table {f}")
+    if args.ckpt:
+        # bytes of the mesh's checkpoint == the oracle's group-0 replica
+        # written by the S2DCKPT1 restatement; every replica reloads it
+        want_path = ckpt_path + ".oracle"
+        port.save_checkpoint(want_path, rows, dims, st.ws[0], st.vs[0])
+        if open(ckpt_path, "rb").read() != open(want_path, "rb").read():
+            fails.append("checkpoint bytes")
+        for r in range(world):
+            for f, (lo, hi, w, v) in gathered[r][3].items():
+                D = int(dims[f])
+                ww = st.ws[0][woff[f] + lo * D: woff[f] + hi * D].reshape(hi - lo, D)
+                vv = st.vs[0][voff[f] + lo: voff[f] + hi]
+                if not (np.array_equal(w.view(np.uint32), ww.view(np.uint32))
+                        and np.array_equal(v.view(np.uint32), vv.view(np.uint32))):
+                    fails.append(f"checkpoint reload rank {r} table {f}")
     if fails:
         print("MP PARITY FAIL", world, M, args.strategy, *fails[:20], sep="\n  ")
         dist.barrier()
         sys.exit(1)
-    print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd}")
+    print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd} ckpt={args.ckpt}")
     dist.barrier()
 
 

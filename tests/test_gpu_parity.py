@@ -285,3 +285,66 @@ def test_bf16_weights_within_tolerance(port):
         w2, v2 = _download(eng, spec)
         assert _close(v2, st.vs[0], 1e-5)
         assert _close(w2, st.ws[0], 1e-2)
+
+
+def test_checkpoint_save_load_bytes(port, tmp_path):
+    """s2d_save_tables writes the reference's S2DCKPT1 bytes for the trained
+    tables (oracle writer on the oracle's replica); s2d_load_tables restores
+    them into a fresh engine; count / shape / truncation errors raise."""
+    from oracle import MeshState, read_checkpoint
+
+    rng = np.random.default_rng(21)
+    rows, dims, B = [300, 5000, 17], [64, 128, 32], 96
+    spec = _spec(rows, dims, B, eta=0.1, c=1.0)
+    eng = _engine(rows, dims)
+    eng.init_tables(4)
+    st = MeshState.init(port, spec, 4)
+    for _ in range(2):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=10, zipf=1.1)
+        up = upstream(rng, B, spec.sum_dims)
+        st.step(port, [lengths], [ids], [up], do_sync=False)
+        eng.forward(lengths, ids)
+        eng.backward_update(up)
+    got, want = str(tmp_path / "gpu.ckpt"), str(tmp_path / "oracle.ckpt")
+    eng.save_tables(got)
+    port.save_checkpoint(want, spec.rows, spec.dims, st.ws[0], st.vs[0])
+    assert open(got, "rb").read() == open(want, "rb").read()
+    fresh = _engine(rows, dims)
+    fresh.init_tables(99)
+    fresh.load_tables(got)
+    w, v = _download(fresh, spec)
+    assert np.array_equal(bits(w), bits(st.ws[0])) and np.array_equal(bits(v), bits(st.vs[0]))
+    # error paths (std::runtime_error -> RuntimeError)
+    other = _engine(rows[:2], dims[:2])
+    with pytest.raises(RuntimeError, match="count"):
+        other.load_tables(got)
+    shape = _engine([300, 5000, 18], dims)
+    with pytest.raises(RuntimeError, match="shape"):
+        shape.load_tables(got)
+    raw = open(got, "rb").read()
+    cut = str(tmp_path / "cut.ckpt")
+    open(cut, "wb").write(raw[:-9])
+    with pytest.raises(RuntimeError, match="truncated"):
+        fresh.load_tables(cut)
+    tables, _, _ = read_checkpoint(got)
+    assert [t[2] for t in tables] == rows
+
+
+def test_checkpoint_bf16_widen_and_round(tmp_path):
+    """bf16 shards: save widens exactly to f32; load rounds f32 to nearest-even."""
+    from oracle import read_checkpoint
+
+    rows, dims = [40, 9], [64, 32]
+    eng = _engine(rows, dims, dtype="bf16")
+    eng.init_tables(5)
+    p = str(tmp_path / "bf16.ckpt")
+    eng.save_tables(p)
+    _, w, v = read_checkpoint(p)
+    w16 = np.concatenate([eng.read_rows(f, 0, rows[f])[0].ravel() for f in range(2)])
+    assert np.array_equal(bits(w), bits(w16))
+    assert np.all(bits(w) & 0xFFFF == 0)  # exactly representable bf16 values
+    fresh = _engine(rows, dims, dtype="bf16")
+    fresh.init_tables(6)
+    fresh.load_tables(p)
+    w2 = np.concatenate([fresh.read_rows(f, 0, rows[f])[0].ravel() for f in range(2)])
+    assert np.array_equal(bits(w2), bits(w16))

@@ -22,11 +22,11 @@ def _ngpu():
 CASES = [
     (2, 1, "row-wise", []),
     (2, 1, "table-wise", []),
-    (2, 2, "row-wise", []),
-    (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4"]),
+    (2, 2, "row-wise", ["--ckpt"]),
+    (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4", "--ckpt"]),
     (4, 1, "table-wise", ["--sgd"]),
     (4, 4, "table-wise", []),
-    (2, 1, "table-wise", ["--engine-out"]),
+    (2, 1, "table-wise", ["--engine-out", "--ckpt"]),
     (4, 2, "table-wise", ["--engine-out"]),
 ]
 

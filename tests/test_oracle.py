@@ -188,3 +188,28 @@ def test_port_matches_reference(port, ref, T, M, strategy, sgd):
     for g in range(M):
         assert np.array_equal(bits(a.ws[g]), bits(b.ws[g]))
         assert np.array_equal(bits(a.vs[g]), bits(b.vs[g]))
+
+
+def test_checkpoint_format_port_vs_reference(port, ref, tmp_path):
+    """S2DCKPT1 writer restated in the port is byte-identical to the
+    reference's save_checkpoint (embedding.cpp:133-185) and the reference's
+    load_checkpoint reads it back (187-219)."""
+    from oracle import read_checkpoint
+
+    rng = np.random.default_rng(3)
+    rows = np.array([7, 1, 300, 64], np.uint32)
+    dims = np.array([4, 8, 64, 128], np.uint32)
+    w = rng.standard_normal(int((rows.astype(np.uint64) * dims).sum())).astype(np.float32)
+    v = rng.random(int(rows.sum())).astype(np.float32)
+    a, b = str(tmp_path / "port.ckpt"), str(tmp_path / "ref.ckpt")
+    port.save_checkpoint(a, rows, dims, w, v)
+    ref.save_checkpoint(b, rows, dims, w, v)
+    assert open(a, "rb").read() == open(b, "rb").read()
+    assert not os.path.exists(a + ".tmp")
+    tables, w2, v2 = read_checkpoint(a)
+    assert tables == [(1, f, int(rows[f]), int(dims[f])) for f in range(len(rows))]
+    assert np.array_equal(bits(w2), bits(w)) and np.array_equal(bits(v2), bits(v))
+    w3, v3 = ref.load_checkpoint(a, rows, dims)
+    assert np.array_equal(bits(w3), bits(w)) and np.array_equal(bits(v3), bits(v))
+    with pytest.raises(RuntimeError):
+        ref.load_checkpoint(a, rows[:2], dims[:2])  # table count mismatch
