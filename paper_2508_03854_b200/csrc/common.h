@@ -111,6 +111,8 @@ struct LookupArgs {
   int direct;                  // N == 1: write pooled rows (zero for empty bags)
   int emit_keys;
   uint32_t uni_d4;             // dim/4 shared by every table (0: mixed dims)
+  int uni_rows;                // uni_d4 != 0 and weights offset = slot * dim (slot-indexed rows)
+  uint32_t zero_row;           // slot index of the all-zero row after the shard (uni_rows)
   uint32_t* ticket;            // work counter of the persistent warps (zeroed per launch)
   uint64_t unit_rot;           // ticket t processes 32-bag unit (t + unit_rot) % units: owners
                                // start at different requesters so their NVLink stores spread out

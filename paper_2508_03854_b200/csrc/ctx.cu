@@ -241,11 +241,16 @@ void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_en
   S2D_CUDA(cudaMemcpy(d_ranges.p, ranges.data(), sizeof(RangeDev) * ranges.size(), cudaMemcpyHostToDevice));
   S2D_CUDA(cudaMemcpy(d_vbase_sorted.p, vbase_sorted.data(), 4 * vbase_sorted.size(), cudaMemcpyHostToDevice));
   S2D_CUDA(cudaMemcpy(d_feat_of_vbase.p, feat_of_vbase.data(), 4 * feat_of_vbase.size(), cudaMemcpyHostToDevice));
-  const size_t wbytes = n_weight_elems * (bf16 ? 2 : 4);
+  // shard + padding: a zero row at slot n_slots (slot-indexed lookups of
+  // invalid ids) and room for whole-warp row chunks past a short row
+  const size_t pad_elems = 2 * (size_t)max_dim + 512;
+  const size_t wbytes = (n_weight_elems + pad_elems) * (bf16 ? 2 : 4);
+  slot_rows = all_same_dim;
+  for (uint32_t f = 0; f < F && slot_rows; ++f) slot_rows = feats[f].wbase == (uint64_t)feats[f].vbase * max_dim;
   weights.release();
   moments.release();
   dirty.release();
-  weights.ensure(std::max<size_t>(wbytes, 16));
+  weights.ensure(wbytes);
   moments.ensure(std::max<size_t>((size_t)n_slots * 4, 16));
   S2D_CUDA(cudaMemsetAsync(weights.p, 0, wbytes, stream));
   S2D_CUDA(cudaMemsetAsync(moments.p, 0, (size_t)n_slots * 4, stream));
@@ -424,6 +429,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.direct = 1;
     a.emit_keys = 1;
     a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
+    a.uni_rows = slot_rows ? 1 : 0;
+    a.zero_row = n_slots;
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
@@ -489,6 +496,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.direct = 0;
     a.emit_keys = 1;
     a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
+    a.uni_rows = slot_rows ? 1 : 0;
+    a.zero_row = n_slots;
     a.peer_out = ptrs(p_part);
     a.use_peer_pooled = engine_out ? 1 : 0;
     if (engine_out) a.peer_pooled = ptrs(p_pooled);

@@ -98,6 +98,7 @@ struct Ctx {
   uint32_t n_slots = 0;
   uint32_t uni_dim = 0;
   bool all_same_dim = false;  // dim shared by every owned table (0: mixed)
+  bool slot_rows = false;     // all_same_dim and weights offset = slot * dim
   uint64_t n_weight_elems = 0;
   DevBuf d_feats, d_ranges, d_vbase_sorted, d_feat_of_vbase;
   DevBuf weights, moments, dirty;

@@ -47,6 +47,10 @@ __device__ __forceinline__ void cp_async_p(uint32_t dst, const void* src, bool p
       "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p cp.async.ca.shared.global [%0], [%1], %3;\n}\n" ::"r"(dst),
       "l"(src), "r"((uint32_t)pred), "n"(BYTES));
 }
+template <int BYTES>
+__device__ __forceinline__ void cp_async_u(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(src), "n"(BYTES));
+}
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -156,7 +160,12 @@ __device__ __forceinline__ uint32_t ring_off(uint32_t slot, int v, uint32_t lane
 // occurrence) order.
 // ============================================================================
 
-template <typename WT, int VPL>
+// UNI: every table has dim uni_d4*4 and rows are slot-indexed (weights
+// offset = slot * dim), so a row is named by its 32-bit slot (invalid ids and
+// items past the end name the zero row `zero_row`), and every lane copies
+// its chunk unconditionally -- chunks past a short row land in the padding
+// rows after the shard and are never read back.
+template <typename WT, int VPL, bool UNI>
 __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   constexpr int VB = Row<WT>::kVecBytes;
   constexpr int kWinStages = 32 / kRowsPerStage;
@@ -169,6 +178,7 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
   const uint64_t n_units = (n_bags + kBags - 1) / kBags;
   const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
+  const WT* const Wl = W + lane * 4;  // this lane's column chunk of row 0
   const uint32_t uni_d4 = a.uni_d4;
 
   // persistent warps take units in ascending order from a ticket counter
@@ -238,7 +248,10 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
         a.keys[p] = ok ? vb_j + (id - lo_j) : 0xffffffffu;
         a.vals[p] = (uint32_t)(oo_j >> 2);
       }
-      ad = ok ? wb_j + (uint64_t)(id - lo_j) * dim_j : kNone;
+      if constexpr (UNI)
+        ad = ok ? vb_j + (id - lo_j) : a.zero_row;
+      else
+        ad = ok ? wb_j + (uint64_t)(id - lo_j) * dim_j : kNone;
       bw = j | (ok ? 0x100u : 0u) | ((dim_j >> 2) << 16);
       uint32_t before = __shfl_up_sync(0xffffffffu, j, 1);
       if (lane == 0) before = last_bag;
@@ -264,12 +277,19 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
       const uint32_t base = ring_s + (st % kStages) * (kRowsPerStage * kRowBytes);
 #pragma unroll
       for (int r = 0; r < kRowsPerStage; ++r) {
-        const uint64_t ad = shfl64(A, q + r);
-        const uint32_t d4 = uni_d4 ? uni_d4 : (__shfl_sync(0xffffffffu, Bw, q + r) >> 16);
-        const WT* src = W + ad + lane * 4;
+        if constexpr (UNI) {
+          const uint32_t ri = __shfl_sync(0xffffffffu, (uint32_t)A, q + r);
+          const WT* src = Wl + (uint64_t)ri * (uni_d4 * 4);
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          cp_async_p<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128, ad != kNone && lane + v * 32 < d4);
+          for (int v = 0; v < VPL; ++v) cp_async_u<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128);
+        } else {
+          const uint64_t ad = shfl64(A, q + r);
+          const uint32_t d4 = uni_d4 ? uni_d4 : (__shfl_sync(0xffffffffu, Bw, q + r) >> 16);
+          const WT* src = W + ad + lane * 4;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            cp_async_p<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128, ad != kNone && lane + v * 32 < d4);
+        }
       }
       cp_commit();
     };
@@ -765,25 +785,29 @@ inline uint32_t warps_for(size_t per_warp, uint32_t max_warps) {
   return (uint32_t)std::min<size_t>(w, max_warps);
 }
 
-template <typename WT, int VPL>
-void lookup_launch(const LookupArgs& a, cudaStream_t st) {
+template <typename WT, int VPL, bool UNI>
+void lookup_launch_t(const LookupArgs& a, cudaStream_t st) {
   const uint64_t n_units = ((uint64_t)a.n_req * a.B * a.F + kBags - 1) / kBags;
   const size_t per_warp = (size_t)kSlots * VPL * 32 * Row<WT>::kVecBytes;
   const uint32_t nw = warps_for(per_warp, 8);
   const size_t smem = nw * per_warp;
-  static bool init = false;
-  if (!init) {
-    set_smem(k_lookup_ring<WT, VPL>, smem);
-    init = true;
-  }
   static int occ = 0;
   if (!occ) {
-    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lookup_ring<WT, VPL>, nw * 32, smem));
+    set_smem(k_lookup_ring<WT, VPL, UNI>, smem);
+    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lookup_ring<WT, VPL, UNI>, nw * 32, smem));
     if (occ < 1) occ = 1;
   }
   S2D_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(uint32_t), st));
-  k_lookup_ring<WT, VPL><<<grid_units(n_units, nw, 148 * occ), nw * 32, smem, st>>>(a);
+  k_lookup_ring<WT, VPL, UNI><<<grid_units(n_units, nw, 148 * occ), nw * 32, smem, st>>>(a);
   S2D_LAUNCH_CHECK();
+}
+
+template <typename WT, int VPL>
+void lookup_launch(const LookupArgs& a, cudaStream_t st) {
+  if (a.uni_rows)
+    lookup_launch_t<WT, VPL, true>(a, st);
+  else
+    lookup_launch_t<WT, VPL, false>(a, st);
 }
 
 template <typename WT, int VPL>
