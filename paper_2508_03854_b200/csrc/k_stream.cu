@@ -506,7 +506,10 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
   }
 }
 
-template <typename WT, int VPL>
+// FULL: every owned row is exactly VPL*128 floats, so each lane's chunk of
+// any item's gradient row -- sentinel items keep a real row offset, items past
+// the range name row 0 -- is in bounds and the ring copies need no predicate.
+template <typename WT, int VPL, bool FULL>
 __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   constexpr int kWinStages = 32 / kRowsPerStage;
   constexpr uint32_t kGRow = VPL * 32 * 16;
@@ -518,6 +521,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   const uint64_t n_units = (n + kC - 1) / kC;
   const uint32_t ud4 = a.uni_dim >> 2;
   WT* __restrict__ W = reinterpret_cast<WT*>(a.weights);
+  const float* const Gl = a.grad + lane * 4;  // this lane's chunk of gradient row 0
   uint32_t heads = 0, longs = 0;
 
   // persistent warps take ranges in ascending order from a ticket counter
@@ -597,12 +601,18 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 #pragma unroll
       for (int r = 0; r < kRowsPerStage; ++r) {
         const uint32_t val = __shfl_sync(0xffffffffu, V, q + r);
-        const uint32_t d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, D, q + r);
-        const bool valid = (VM >> (q + r)) & 1u;
-        const float* grow = a.grad + (uint64_t)val * 4 + lane * 4;
+        if constexpr (FULL) {  // every item names a real gradient row; no predicate
+          const float* grow = Gl + (uint64_t)val * 4;
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          cp_async_p<16>(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128, valid && lane + v * 32 < d4);
+          for (int v = 0; v < VPL; ++v) cp_async_u<16>(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128);
+        } else {
+          const uint32_t d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, D, q + r);
+          const bool valid = (VM >> (q + r)) & 1u;
+          const float* grow = Gl + (uint64_t)val * 4;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v)
+            cp_async_p<16>(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128, valid && lane + v * 32 < d4);
+        }
       }
       cp_commit();
     };
@@ -818,9 +828,11 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   static bool init = false;
   if (!init) {
     set_smem(k_range_partials<VPL>, nw_p * pw_p);
-    set_smem(k_update_ring<WT, VPL>, nw_u * pw_u);
+    set_smem(k_update_ring<WT, VPL, false>, nw_u * pw_u);
+    set_smem(k_update_ring<WT, VPL, true>, nw_u * pw_u);
     init = true;
   }
+  const bool full = a.uni_dim == 128u * VPL;
   if (a.n >= 2 * kC) {
     k_range_partials<VPL><<<grid_units(a.n / kC, nw_p, 148 * 16), nw_p * 32, nw_p * pw_p, st>>>(a);
     S2D_LAUNCH_CHECK();
@@ -831,10 +843,15 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   }
   static int occ = 0;
   if (!occ) {
-    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_ring<WT, VPL>, nw_u * 32, nw_u * pw_u));
+    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_ring<WT, VPL, false>, nw_u * 32,
+                                                           nw_u * pw_u));
     if (occ < 1) occ = 1;
   }
-  k_update_ring<WT, VPL><<<grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ), nw_u * 32, nw_u * pw_u, st>>>(a);
+  const unsigned grid = grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ);
+  if (full)
+    k_update_ring<WT, VPL, true><<<grid, nw_u * 32, nw_u * pw_u, st>>>(a);
+  else
+    k_update_ring<WT, VPL, false><<<grid, nw_u * 32, nw_u * pw_u, st>>>(a);
   S2D_LAUNCH_CHECK();
 }
 
