@@ -458,12 +458,47 @@ __device__ __forceinline__ void store_partial(double* p, uint32_t lane, uint32_t
   }
 }
 
+// In-order f64 sum of the kC gradient rows of one full range [s, s+kC), all
+// of one segment, straight through registers: kG rows' loads in flight per
+// batch, the next window's row offsets loaded a window ahead.  No shared
+// memory (the ring's LDGSTS + LDS pair per row saturated the MIO queue).
+template <int VPL>
+__device__ __forceinline__ void reg_sum_range(const StreamUpdateArgs& a, uint32_t lane, uint64_t s, uint32_t d4,
+                                              double (&acc)[VPL][4]) {
+  constexpr int kG = 8 / VPL;
+  const float* const Gl = a.grad + lane * 4;
+  uint32_t val_n = __ldg(a.vals + s + lane);
+  for (uint32_t w = 0; w < kC; w += 32) {
+    const uint32_t val_c = val_n;
+    if (w + 32 < kC) val_n = __ldg(a.vals + s + w + 32 + lane);
+#pragma unroll
+    for (int g = 0; g < 32; g += kG) {
+      float4 x[kG][VPL];
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const float* row = Gl + (uint64_t)__shfl_sync(0xffffffffu, val_c, g + j) * 4;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (lane + v * 32 < d4) x[j][v] = __ldg(reinterpret_cast<const float4*>(row + v * 128));
+      }
+#pragma unroll
+      for (int j = 0; j < kG; ++j)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (lane + v * 32 < d4) {
+            acc[v][0] += (double)x[j][v].x;
+            acc[v][1] += (double)x[j][v].y;
+            acc[v][2] += (double)x[j][v].z;
+            acc[v][3] += (double)x[j][v].w;
+          }
+    }
+  }
+}
+
 // level-1 partials: range k = [kC, kC+C) lying inside one segment
 template <int VPL>
 __global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t lane_s = smem_u32(smem) + warp * kSlots * VPL * 32 * 16 + lane * 16;
   const uint64_t n_ranges = a.n / kC;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t k = 1 + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < n_ranges; k += stride) {
@@ -478,7 +513,7 @@ __global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a
     for (int v = 0; v < VPL; ++v)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
-    ring_sum<VPL>(a, lane_s, lane, s, t, d4, acc);
+    reg_sum_range<VPL>(a, lane, s, d4, acc);
     store_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
   }
 }
@@ -822,19 +857,17 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
 
 template <typename WT, int VPL>
 void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
-  const size_t pw_p = (size_t)kSlots * VPL * 32 * 16;
   const size_t pw_u = (size_t)kSlots * VPL * 32 * 16;
-  const uint32_t nw_p = warps_for(pw_p, 8), nw_u = warps_for(pw_u, 4);
+  const uint32_t nw_u = warps_for(pw_u, 4);
   static bool init = false;
   if (!init) {
-    set_smem(k_range_partials<VPL>, nw_p * pw_p);
     set_smem(k_update_ring<WT, VPL, false>, nw_u * pw_u);
     set_smem(k_update_ring<WT, VPL, true>, nw_u * pw_u);
     init = true;
   }
   const bool full = a.uni_dim == 128u * VPL;
   if (a.n >= 2 * kC) {
-    k_range_partials<VPL><<<grid_units(a.n / kC, nw_p, 148 * 16), nw_p * 32, nw_p * pw_p, st>>>(a);
+    k_range_partials<VPL><<<grid_units(a.n / kC, 8, 148 * 16), 256, 0, st>>>(a);
     S2D_LAUNCH_CHECK();
   }
   if (a.n >= 2ull * kC * kP) {
