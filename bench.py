@@ -459,6 +459,18 @@ def run_ours(args):
                                           "sync_bytes")},
         "per_rank": per_rank,
     }
+    if n_mp > 1:
+        # NVLink roofline of the MP exchanges (rank 0's phases): bytes this rank
+        # stores into peers / the phase time, against the measured peer-copy
+        # bandwidth (770 GB/s per direction, B200_PROFILING.md; 900 nominal)
+        nv = {}
+        for key, ph in (("grad_bytes_sent", "grad_gather"), ("lookup_bytes_sent", "lookup")):
+            pm = per_phase.get(ph, {}).get("ms_per_launch")
+            if pm:
+                gbs = st[key] / (pm / 1e3) / 1e9
+                nv[ph] = {"bytes": st[key], "ms": pm, "achieved_gbs": gbs, "frac": gbs / 770.0}
+        line["nvlink"] = {"peak_gbs": 770.0, "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                          "phases": nv}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args)
     if rank == 0:

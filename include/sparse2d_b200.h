@@ -98,6 +98,9 @@ typedef struct {
   uint64_t sync_bytes;     /* replica-sync payload bytes sent */
   uint32_t error_flags;    /* device-side fault bits of the last step */
   uint32_t reserved;
+  uint64_t ids_bytes_sent;    /* part of a2a_bytes_sent: lengths + ids (K1 permute) */
+  uint64_t lookup_bytes_sent; /* part of a2a_bytes_sent: partials / pooled rows (K2) */
+  uint64_t grad_bytes_sent;   /* part of a2a_bytes_sent: gradient rows (grad gather) */
 } s2d_step_stats;
 
 const char* s2d_last_error(void);

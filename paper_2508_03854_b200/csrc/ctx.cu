@@ -534,6 +534,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
       if (q == local) continue;
       sent += nnz_to[q] * 4 + BF * 4 + ef_from[q] * 4;
       recv += nnz_from[q] * 4 + BF * 4 + ef_to[q] * 4;
+      stats.ids_bytes_sent += nnz_to[q] * 4 + BF * 4;
+      stats.lookup_bytes_sent += ef_from[q] * 4;
     }
     stats.nnz_owned = nnz_own;
     stats.entries_owned = ef_own / std::max<uint32_t>(1, max_dim);
@@ -734,6 +736,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
       recv += ef_from[q] * 4;
     }
     stats.a2a_bytes_sent += sent;
+    stats.grad_bytes_sent = sent;
     stats.a2a_bytes_recv += recv;
   }
   (void)BF;
