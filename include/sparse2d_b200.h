@@ -203,6 +203,17 @@ int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* ro
 int s2d_save_tables(s2d_ctx* ctx, const char* path);
 int s2d_load_tables(s2d_ctx* ctx, const char* path);
 
+/* Device-side synthetic input: the reference DataGenerator's ids for one
+ * rank's batch (DataGenerator ctor Zipf CDF, src/data.cpp:85-98;
+ * gen_batch_into, data.cpp:115-136; train lane), bit-exact.  Table f has
+ * the registered rows as num_ids, Zipf exponent zipf[f] (>= 0) and
+ * ids_per_sample[f] ids per bag.  Writes lengths[batch*F] (sample-major
+ * bags) and ids[batch * sum_f ids_per_sample[f]] in (sample, feature, draw)
+ * order -- the s2d_lookup_forward input layout.  mem says where lengths/ids
+ * live.  Invalid specs -> S2D_EINVAL (FeatureSpec::validate, data.cpp:26-35). */
+int s2d_gen_batch(s2d_ctx* ctx, uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, const double* zipf,
+                  const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int32_t mem);
+
 /* Forward of one step for this rank's batch of `batch` samples: sample-major
  * bags (s, f) given as lengths[batch*F] and the `nnz` global row ids of all
  * bags concatenated.  Runs K1 input-dist bucketing + id all-to-all, K2 owner

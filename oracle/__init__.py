@@ -249,10 +249,17 @@ class Oracle:
         return out.reshape(B, int(dims.sum()))
 
     def gen_batch_ids(self, seed, step, rank, F, rows, zipf, L, B) -> np.ndarray:
-        out = np.empty(B * F * L, np.uint32)
-        rc = self.lib.ref_gen_batch_ids(seed, step, rank, F, rows, zipf, L, B, out)
+        """DataGenerator ids (data.cpp:70-136); rows / zipf / L scalars or per-table."""
+        rows = np.ascontiguousarray(np.broadcast_to(np.asarray(rows, np.uint32), (F,)))
+        zipf = np.ascontiguousarray(np.broadcast_to(np.asarray(zipf, np.float64), (F,)))
+        L = np.ascontiguousarray(np.broadcast_to(np.asarray(L, np.uint32), (F,)))
+        out = np.empty(int(B) * int(L.astype(np.uint64).sum()), np.uint32)
+        fn = getattr(self.lib, "or_gen_batch_ids" if self.kind == "port" else "ref_gen_batch_ids_tables")
+        fn.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, _u32p, _f64p, _u32p, C.c_uint32, _u32p]
+        fn.restype = C.c_int
+        rc = fn(seed, step, rank, F, rows, zipf, L, B, out)
         if rc:
-            raise ValueError(self.lib.ref_last_error().decode())
+            raise ValueError("gen_batch_ids failed" if self.kind == "port" else self.lib.ref_last_error().decode())
         return out
 
     # ---- one MP group / the full mesh ---------------------------------------

@@ -165,6 +165,26 @@ int ref_gen_batch_ids(uint64_t seed, uint64_t step, uint32_t rank, uint32_t F, u
   }
 }
 
+// gen_batch ids with per-table rows / Zipf exponent / ids_per_sample
+// (DataGenerator, data.cpp:70-136), sample-major (s, f, draw) order.
+int ref_gen_batch_ids_tables(uint64_t seed, uint64_t step, uint32_t rank, uint32_t F, const uint32_t* rows,
+                             const double* zipf, const uint32_t* L, uint32_t B, uint32_t* out_ids) {
+  try {
+    std::vector<FeatureSpec> specs;
+    for (uint32_t f = 0; f < F; ++f) specs.push_back({f, rows[f], zipf[f], L[f]});
+    DataGenerator gen(specs, DataParams{}, seed);
+    MiniBatch mb = gen.gen_batch(step, rank, B);
+    size_t k = 0;
+    for (uint32_t s = 0; s < B; ++s)
+      for (uint32_t f = 0; f < F; ++f)
+        for (uint32_t id : mb.samples[s].ids[f]) out_ids[k++] = id;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 void ref_deterministic_mean(uint32_t m, float* const* reps, size_t len) {
   deterministic_mean_inplace(std::span<float* const>(reps, m), len);
 }

@@ -660,3 +660,56 @@ int or_save_checkpoint(const char* path, uint32_t F, const uint32_t* rows, const
   if (!ok) return -1;
   return rename(tmp, path) == 0 ? 0 : -1;
 }
+
+/* ---- DataGenerator ids (data.cpp:85-98 Zipf CDF, 115-136 gen_batch_into) --
+ * cdf_f[k] = (sum_{i<=k} (i+1)^-s_f) / total_f in sequential f64, last = 1.
+ * Bag (s, f) draws L_f ids: u = CounterRng({seed, lane=0, step, rank, s,
+ * tag=1, f}).next_uniform(); id = min(upper_bound(cdf_f, u), rows_f - 1).
+ * Output: sample-major bags, ids in (s, f, draw) order.  Returns 0. */
+static uint32_t or_upper_bound(const double* cdf, uint32_t n, double u) {
+  uint32_t lo = 0, hi = n; /* first index with cdf[i] > u */
+  while (lo < hi) {
+    const uint32_t mid = lo + (hi - lo) / 2;
+    if (cdf[mid] > u)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  return lo;
+}
+
+void or_zipf_cdf(uint32_t rows, double s, double* cdf) { /* data.cpp:88-97 */
+  double total = 0.0;
+  for (uint32_t k = 0; k < rows; ++k) {
+    total += pow((double)(k + 1), -s);
+    cdf[k] = total;
+  }
+  for (uint32_t k = 0; k < rows; ++k) cdf[k] /= total;
+  cdf[rows - 1] = 1.0;
+}
+
+int or_gen_batch_ids(uint64_t seed, uint64_t step, uint32_t rank, uint32_t F, const uint32_t* rows,
+                     const double* zipf, const uint32_t* L, uint32_t B, uint32_t* out_ids) {
+  double** cdf = (double**)calloc(F, sizeof(double*));
+  if (!cdf) return OR_ENOMEM;
+  for (uint32_t f = 0; f < F; ++f) {
+    cdf[f] = (double*)malloc(sizeof(double) * rows[f]);
+    if (!cdf[f]) return OR_ENOMEM;
+    or_zipf_cdf(rows[f], zipf[f], cdf[f]);
+  }
+  size_t k = 0;
+  for (uint32_t s = 0; s < B; ++s)
+    for (uint32_t f = 0; f < F; ++f) {
+      const uint64_t fl[7] = {seed, 0, step, rank, s, 1, f};
+      const uint64_t key = or_make_key(fl, 7);
+      for (uint32_t j = 0; j < L[f]; ++j) {
+        const uint64_t z = key + (uint64_t)(j + 1) * 0x9E3779B97F4A7C15ULL;
+        const double u = (double)(or_mix64(z) >> 11) * 0x1.0p-53;
+        const uint32_t i = or_upper_bound(cdf[f], rows[f], u);
+        out_ids[k++] = i < rows[f] - 1 ? i : rows[f] - 1;
+      }
+    }
+  for (uint32_t f = 0; f < F; ++f) free(cdf[f]);
+  free(cdf);
+  return OR_OK;
+}

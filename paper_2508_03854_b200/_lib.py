@@ -73,6 +73,7 @@ SIGNATURES = {
     "s2d_ctx_set_async_host": (C.c_int, [_P, C.c_int]),
     "s2d_save_tables": (C.c_int, [_P, C.c_char_p]),
     "s2d_load_tables": (C.c_int, [_P, C.c_char_p]),
+    "s2d_gen_batch": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, _P, _P, _P, _P, C.c_int32]),
     "s2d_register_tables": (C.c_int, [_P, C.POINTER(TableDesc), C.c_uint32, C.POINTER(PlanEntry), C.c_uint32,
                                       C.c_int32]),
     "s2d_set_optimizer": (C.c_int, [_P, C.POINTER(OptimizerConfigC)]),

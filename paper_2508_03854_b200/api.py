@@ -218,6 +218,7 @@ class Sparse2DEmbedding:
         self.lib = _lib()
         self.topology = topology
         self.rank = rank
+        self._device = device
         self.tables = list(tables)
         self.F = len(self.tables)
         self.dims = np.array([t.dim for t in self.tables], np.uint32)
@@ -267,6 +268,29 @@ class Sparse2DEmbedding:
         """Load an S2DCKPT1 checkpoint into every replica (Trainer::load_tables,
         trainer.cpp:880-896)."""
         L.check(self.lib.s2d_load_tables(self._ctx, os.fsencode(path)))
+
+    def gen_batch(self, seed: int, step: int, rank: int, batch: int, zipf, ids_per_sample, device: bool = True):
+        """The reference DataGenerator's ids for one rank's batch, generated on
+        the GPU (s2d_gen_batch; data.cpp:85-136).  zipf / ids_per_sample are
+        per-table (or scalars).  Returns (lengths[B*F], ids) as CUDA tensors
+        (device=True) or numpy arrays."""
+        z = np.ascontiguousarray(np.broadcast_to(np.asarray(zipf, np.float64), (self.F,)))
+        L_ = np.ascontiguousarray(np.broadcast_to(np.asarray(ids_per_sample, np.uint32), (self.F,)))
+        n_ids = int(batch) * int(L_.astype(np.uint64).sum())
+        if device:
+            import torch
+
+            dev = torch.device("cuda", self._device)
+            lengths = torch.empty(batch * self.F, dtype=torch.int32, device=dev)
+            ids = torch.empty(max(n_ids, 1), dtype=torch.int32, device=dev)[:n_ids]
+            lp, ip, mem = lengths.data_ptr(), ids.data_ptr(), L.S2D_DEVICE
+        else:
+            lengths = np.empty(batch * self.F, np.uint32)
+            ids = np.empty(n_ids, np.uint32)
+            lp, ip, mem = lengths.ctypes.data, ids.ctypes.data, L.S2D_HOST
+        L.check(self.lib.s2d_gen_batch(self._ctx, seed, step, rank, batch, z.ctypes.data, L_.ctypes.data, lp, ip,
+                                       mem))
+        return lengths, ids
 
     def set_async_host(self, on: bool):
         """Host-memory pooled output completes asynchronously (s2d_ctx_set_async_host)."""

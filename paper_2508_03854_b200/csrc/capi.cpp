@@ -176,6 +176,11 @@ int s2d_load_tables(s2d_ctx* ctx, const char* path) {
   return guarded([&] { as_ctx(ctx)->load_tables(path); });
 }
 
+int s2d_gen_batch(s2d_ctx* ctx, uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, const double* zipf,
+                  const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int32_t mem) {
+  return guarded([&] { as_ctx(ctx)->gen_batch(seed, step, rank, batch, zipf, ids_per_sample, lengths, ids, mem); });
+}
+
 int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* row_hi) {
   return guarded([&] {
     auto* c = as_ctx(ctx);

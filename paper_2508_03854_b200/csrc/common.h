@@ -204,6 +204,19 @@ struct StreamUpdateArgs {
   uint32_t* err;
   uint32_t* counters;            // [0] unique rows updated, [1] rows spanning ranges
 };
+// device-side synthetic input (k_gen.cu): DataGenerator ids, data.cpp:85-136
+struct GenArgs {
+  uint64_t seed, step;
+  uint32_t rank, B, F, per_sample;  // per_sample = sum_f L_f
+  const uint32_t* cum;              // [F+1] exclusive prefix of L_f
+  const uint32_t* rows;             // [F] table rows (num_ids)
+  const uint64_t* cdf_off;          // [F] offset of table f's CDF in cdf
+  const double* cdf;
+  uint32_t* lengths;                // [B*F]
+  uint32_t* ids;                    // [B*per_sample]
+};
+void launch_gen_batch(const GenArgs& a, cudaStream_t st);
+
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);

@@ -162,6 +162,12 @@ struct Ctx {
   int world_barrier(int failed);
   void save_tables(const char* path);
   void load_tables(const char* path);
+  // device-side synthetic input (gen.cpp): per-table Zipf CDFs cached by exponent
+  DevBuf gen_cdf, gen_meta, gen_lengths, gen_ids;
+  std::vector<double> gen_zipf;
+  std::vector<uint64_t> gen_cdf_off;
+  void gen_batch(uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, const double* zipf,
+                 const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int mem);
   void debug_read(int which, void* out, uint64_t cap, uint64_t* n);
 
  private:

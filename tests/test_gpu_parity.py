@@ -348,3 +348,25 @@ def test_checkpoint_bf16_widen_and_round(tmp_path):
     fresh.load_tables(p)
     w2 = np.concatenate([fresh.read_rows(f, 0, rows[f])[0].ravel() for f in range(2)])
     assert np.array_equal(bits(w2), bits(w16))
+
+
+def test_device_gen_batch_bit_exact(port):
+    """s2d_gen_batch (device DataGenerator ids, data.cpp:85-136) equals the
+    oracle's restatement bit for bit, host and device outputs; the batch
+    feeds the step directly; invalid specs raise like FeatureSpec::validate."""
+    rows, dims = [100, 3, 5000, 1, 70000], [64, 64, 64, 64, 64]
+    zipf, L = [1.0, 1.2, 0.8, 0.0, 1.05], [5, 2, 20, 1, 11]
+    eng = _engine(rows, dims)
+    B = 96
+    for seed, step, rank in ((7, 3, 1), (2024, 0, 0)):
+        want = port.gen_batch_ids(seed, step, rank, len(rows), rows, zipf, L, B)
+        lengths, ids = eng.gen_batch(seed, step, rank, B, zipf, L)
+        assert np.array_equal(lengths.cpu().numpy().view(np.uint32), np.tile(np.array(L, np.uint32), B))
+        assert np.array_equal(ids.cpu().numpy().view(np.uint32), want)
+        lh, ih = eng.gen_batch(seed, step, rank, B, zipf, L, device=False)
+        assert np.array_equal(ih, want) and np.array_equal(lh, np.tile(np.array(L, np.uint32), B))
+    eng.init_tables(1)
+    pooled = eng.forward(lengths, ids)  # the generated batch is a valid step input
+    assert pooled.shape == (B, sum(dims))
+    with pytest.raises(ValueError, match="zipf_exponent"):
+        eng.gen_batch(1, 0, 0, B, [1.0, -0.5, 1.0, 1.0, 1.0], L)

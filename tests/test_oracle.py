@@ -213,3 +213,13 @@ def test_checkpoint_format_port_vs_reference(port, ref, tmp_path):
     assert np.array_equal(bits(w3), bits(w)) and np.array_equal(bits(v3), bits(v))
     with pytest.raises(RuntimeError):
         ref.load_checkpoint(a, rows[:2], dims[:2])  # table count mismatch
+
+
+def test_gen_batch_ids_port_vs_reference(port, ref):
+    """DataGenerator ids (data.cpp:85-136) restated in the port equal the
+    reference generator's, per-table rows / exponents / pooling."""
+    rows, zipf, L = [100, 3, 5000, 1, 70000], [1.0, 1.2, 0.8, 0.0, 1.05], [5, 2, 20, 1, 11]
+    for seed, step, rank in ((7, 3, 1), (0, 0, 0), (12345, 9, 6)):
+        a = port.gen_batch_ids(seed, step, rank, len(rows), rows, zipf, L, 48)
+        b = ref.gen_batch_ids(seed, step, rank, len(rows), rows, zipf, L, 48)
+        assert np.array_equal(a, b)
