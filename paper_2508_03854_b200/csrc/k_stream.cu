@@ -605,18 +605,27 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       const bool head = valid && key != before;
       w.key = key;
       w.val = val;
-      w.d4 = 0;
-      w.wofs = 0;
-      if (valid) row_ref(a, key, w.wofs, w.d4);
       w.vm = __ballot_sync(0xffffffffu, valid);
       w.hm = __ballot_sync(0xffffffffu, head);
       // warm L2 with the weight row and moment of every segment head; the
       // consumer loads them into registers when it reaches the head
-      if (head) {
-        const char* row = reinterpret_cast<const char*>(W + w.wofs);
-        const uint32_t bytes = w.d4 * 4 * (uint32_t)sizeof(WT);
-        for (uint32_t o = 0; o < bytes; o += 128) prefetch_l2(row + o);
-        prefetch_l2(a.moments + key);
+      if constexpr (FULL) {  // slot-indexed rows of VPL*128 elements: no per-item row metadata
+        if (head) {
+          const char* row = reinterpret_cast<const char*>(W + (uint64_t)key * (VPL * 128));
+#pragma unroll
+          for (uint32_t o = 0; o < VPL * 128 * sizeof(WT); o += 128) prefetch_l2(row + o);
+          prefetch_l2(a.moments + key);
+        }
+      } else {
+        w.d4 = 0;
+        w.wofs = 0;
+        if (valid) row_ref(a, key, w.wofs, w.d4);
+        if (head) {
+          const char* row = reinterpret_cast<const char*>(W + w.wofs);
+          const uint32_t bytes = w.d4 * 4 * (uint32_t)sizeof(WT);
+          for (uint32_t o = 0; o < bytes; o += 128) prefetch_l2(row + o);
+          prefetch_l2(a.moments + key);
+        }
       }
     };
     Win wc_, wn_;
@@ -630,7 +639,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 
     auto produce = [&](uint32_t st) {
       const bool nxt = (st / kWinStages) != wc;
-      const uint32_t V = nxt ? wn_.val : wc_.val, VM = nxt ? wn_.vm : wc_.vm, D = nxt ? wn_.d4 : wc_.d4;
+      const uint32_t V = nxt ? wn_.val : wc_.val, VM = nxt ? wn_.vm : wc_.vm;
       const uint32_t q = (st % kWinStages) * kRowsPerStage;
       const uint32_t slot0 = (st % kStages) * kRowsPerStage;
 #pragma unroll
@@ -641,7 +650,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 #pragma unroll
           for (int v = 0; v < VPL; ++v) cp_async_u<16>(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128);
         } else {
-          const uint32_t d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, D, q + r);
+          const uint32_t d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, nxt ? wn_.d4 : wc_.d4, q + r);
           const bool valid = (VM >> (q + r)) & 1u;
           const float* grow = Gl + (uint64_t)val * 4;
 #pragma unroll
@@ -757,8 +766,13 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
             if (cur != kNone) flush();
             // segment head: load its (L2-warm) weight row and moment
             cur = __shfl_sync(0xffffffffu, wc_.key, i);
-            wofs = a.uni_dim ? (uint64_t)cur * a.uni_dim : shfl64(wc_.wofs, i);
-            d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, wc_.d4, i);
+            if constexpr (FULL) {
+              wofs = (uint64_t)cur * (VPL * 128);
+              d4 = VPL * 32;
+            } else {
+              wofs = a.uni_dim ? (uint64_t)cur * a.uni_dim : shfl64(wc_.wofs, i);
+              d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, wc_.d4, i);
+            }
 #pragma unroll
             for (int v = 0; v < VPL; ++v)
               if (lane + v * 32 < d4) wraw[v] = Row<WT>::ldg(W + wofs + (lane + v * 32) * 4);
