@@ -204,35 +204,49 @@ def traffic_from_profiles(kernel):
 # ----------------------------------------------------------------------------
 
 def reference_step_sample(w, seed, n_samples, threads, step):
-    """One bounded-sample step of the reference CPU path.  Tables are
-    compacted to the rows the sample touches (each row's arithmetic is
-    independent).  Returns seconds of ref_group_step."""
+    """One bounded-sample step of the reference CPU path for one MP group of
+    the arm's mesh (N = w.mesh[0] virtual ranks, each with n_samples of its
+    own batch, the reference's group step incl. its all-to-all copies).
+    Tables are compacted to the rows the sample touches (each row's
+    arithmetic is independent); the plan is the reference
+    plan_greedy over the compacted tables with the arm's strategy.  Returns
+    (seconds of ref_group_step, samples processed)."""
     from oracle import MeshSpec, Oracle
 
     ref = Oracle("reference")
-    n_mp, m = w.mesh
-    lengths_all, ids_all = w.batch_for(seed, step, 0)
+    n_mp = w.mesh[0]
     F = w.F
     B = min(n_samples, w.batch)
-    lengths = lengths_all[: B * F]
-    ids = ids_all[: int(lengths.sum())]
-    feat = np.repeat(np.tile(np.arange(F), B), lengths)
+    L, I, U, feats = [], [], [], []
+    for r in range(n_mp):  # a B-sample batch per rank, same distributions as the arm's
+        lengths, ids = w.batch_for(seed, step, r, batch=B)
+        L.append(lengths)
+        I.append(ids)
+        feats.append(np.repeat(np.tile(np.arange(F), B), lengths))
+        U.append(w.upstream_for(seed, step, r, batch=B))
     rows = np.zeros(F, np.uint32)
-    cids = np.empty_like(ids)
+    cI = [np.empty_like(x) for x in I]
     for f in range(F):
-        sel = feat == f
-        u, inv = np.unique(ids[sel], return_inverse=True)
+        sel = [ft == f for ft in feats]
+        u, inv = np.unique(np.concatenate([x[m] for x, m in zip(I, sel)]), return_inverse=True)
         rows[f] = max(1, len(u))
-        cids[sel] = inv.astype(np.uint32)
+        o = 0
+        for r in range(n_mp):
+            k = int(sel[r].sum())
+            cI[r][sel[r]] = inv[o:o + k].astype(np.uint32)
+            o += k
     dims = np.array(w.dims, np.uint32)
-    plan = np.array([[f, 0, int(rows[f]), 0] for f in range(F)], np.uint32)
-    spec = MeshSpec(rows=rows, dims=dims, plan=plan, T=1, M=1, B=B, eta=w.eta, c=w.c)
+    if n_mp == 1:
+        plan = np.array([[f, 0, int(rows[f]), 0] for f in range(F)], np.uint32)
+    else:
+        prof = [(f, int(rows[f]) * int(dims[f]) * 4, w.plan_cost(f, n_mp), int(rows[f])) for f in range(F)]
+        plan = ref.plan_greedy(prof, n_mp, w.strategy)
+    spec = MeshSpec(rows=rows, dims=dims, plan=plan, T=n_mp, M=1, B=B, eta=w.eta, c=w.c)
     rng = np.random.default_rng(seed)
     wt = (rng.standard_normal(spec.replica_floats()) * 0.05).astype(np.float32)
     vt = np.zeros(spec.replica_rows(), np.float32)
-    up = w.upstream_for(seed, step, 0)[:B]
-    ref.group_step(spec, [lengths], [cids], [up], wt, vt, None, threads=threads)
-    return ref.last_compute_seconds, B
+    ref.group_step(spec, L, cI, U, wt, vt, None, threads=threads)
+    return ref.last_compute_seconds, B * n_mp
 
 
 def run_reference(args):
@@ -264,10 +278,12 @@ def run_reference(args):
         "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 storage / f64 accumulation", "data": "synthetic",
-        "config": {"workload": w.name + ": " + w.describe, "mesh": "1x1 (reference group step)",
-                   "global_batch": n, "sample": f"{n} samples/step, tables compacted to touched rows"},
+        "config": {"workload": w.name + ": " + w.describe, "mesh": f"{w.mesh[0]}x{w.mesh[1]}",
+                   "simulated": f"one MP group of {w.mesh[0]} virtual ranks (reference group step, all host threads)",
+                   "global_batch": n * w.mesh[0],
+                   "sample": f"{n} of {w.batch} samples per rank per step, tables compacted to touched rows"},
         "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": threads, "kind": kind,
-                         "sample": f"{n} of {w.batch} samples per step, touched-row tables"},
+                         "sample": f"{n} of {w.batch} samples per rank x {w.mesh[0]} ranks per step, touched-row tables"},
         "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     _emit(line)

@@ -101,8 +101,8 @@ class Workload:
             ids = _bijection(ids, rows)
         return ids.astype(np.uint32)
 
-    def lengths(self, rng) -> np.ndarray:
-        B, F = self.batch, self.F
+    def lengths(self, rng, batch: int | None = None) -> np.ndarray:
+        B, F = batch or self.batch, self.F
         if self.fixed_len is not None:
             return np.full(B * F, self.fixed_len, np.uint32)
         L = np.arange(self.len_lo, self.len_hi + 1)
@@ -110,22 +110,24 @@ class Workload:
         p /= p.sum()
         return rng.choice(L, size=B * F, p=p).astype(np.uint32)
 
-    def batch_for(self, seed: int, step: int, rank: int):
-        """(lengths[B*F], ids[nnz]) of one rank's batch: sample-major bags."""
+    def batch_for(self, seed: int, step: int, rank: int, batch: int | None = None):
+        """(lengths[B*F], ids[nnz]) of one rank's batch: sample-major bags
+        (batch overrides B, e.g. for a bounded CPU sample)."""
+        batch = batch or self.batch
         rng = np.random.default_rng([seed, step, rank, 1])
-        lengths = self.lengths(rng)
+        lengths = self.lengths(rng, batch)
         F = self.F
-        feat = np.repeat(np.tile(np.arange(F, dtype=np.int32), self.batch), lengths)
+        feat = np.repeat(np.tile(np.arange(F, dtype=np.int32), batch), lengths)
         ids = np.empty(len(feat), np.uint32)
         for f in range(F):
             pos = np.nonzero(feat == f)[0]
             ids[pos] = self._sample_ids(rng, int(self.rows[f]), len(pos))
         return lengths, ids
 
-    def upstream_for(self, seed: int, step: int, rank: int) -> np.ndarray:
+    def upstream_for(self, seed: int, step: int, rank: int, batch: int | None = None) -> np.ndarray:
         """Synthetic per-sample upstream gradient f32(1e-3 * N(0,1))."""
         rng = np.random.default_rng([seed, step, rank, 2])
-        out = rng.standard_normal((self.batch, self.sum_dims), dtype=np.float32)
+        out = rng.standard_normal((batch or self.batch, self.sum_dims), dtype=np.float32)
         out *= np.float32(1e-3)
         return out
 
