@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--batch", type=int, default=48)
     ap.add_argument("--engine-out", action="store_true", help="zero-copy pooled output (owners write it)")
     ap.add_argument("--ckpt", action="store_true", help="S2DCKPT1 save from the mesh + load into every replica")
+    ap.add_argument("--bf16", action="store_true",
+                    help="bf16 shards: the oracle is re-seeded every step from the mesh's (widened) weights")
     args = ap.parse_args()
 
     import torch
@@ -57,8 +59,10 @@ def main():
     tables = [s2d.TableConfig(int(rows[f]), int(dims[f])) for f in range(F)]
     opt = s2d.OptimizerConfig(eta=eta, eps=1e-8, c=c, variant="sgd" if args.sgd else "rowwise-adagrad")
     eng = s2d.Sparse2DEmbedding(tables, s2d.Topology(world, M), rank=rank, device=local, plan=plan, optimizer=opt,
-                                nccl_id=nid[0])
+                                weight_dtype="bf16" if args.bf16 else "fp32", nccl_id=nid[0])
     eng.init_tables(31)
+    if args.bf16:
+        sys.exit(run_bf16(args, eng, dist, rank, world, M, N, rows, dims, B, eta, c, plan))
 
     def inputs(step, r):
         rng = np.random.default_rng([step, r, 77])
@@ -190,6 +194,88 @@ def main():
         sys.exit(1)
     print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd} ckpt={args.ckpt}")
     dist.barrier()
+
+
+def _shards(eng, F):
+    out = {}
+    for f in range(F):
+        lo, hi = eng.owned_range(f)
+        if hi > lo:
+            out[f] = (lo, hi) + eng.read_rows(f, lo, hi)
+    return out
+
+
+def run_bf16(args, eng, dist, rank, world, M, N, rows, dims, B, eta, c, plan):
+    """bf16 storage has no reference path (embedding.hpp:16): every step the
+    oracle is seeded from the mesh's bf16 weights (widened exactly) and must
+    give bit-equal pooled outputs (f64 pooling of bf16 rows is exact), moments
+    within 1e-5 and weights within 1e-2 relative after the step (one bf16
+    rounding).  Sync every step (sync_interval = 1)."""
+    from cases import make_batch, upstream
+    from oracle import MeshSpec, MeshState, Oracle
+
+    F = len(rows)
+    port = Oracle("port") if rank == 0 else None
+    plan_arr = np.array([[e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]] for e in plan], np.uint32)
+    spec = MeshSpec(rows=rows, dims=dims, plan=plan_arr, T=world, M=M, B=B, eta=eta, c=c, sgd=False)
+    woff, voff = spec.woff(), spec.voff()
+    fails = []
+
+    def assemble(gathered):  # per-group replicas from every rank's shards
+        ws = [np.zeros(spec.replica_floats(), np.float32) for _ in range(M)]
+        vs = [np.zeros(spec.replica_rows(), np.float32) for _ in range(M)]
+        for r in range(world):
+            g = r // N
+            for f, (lo, hi, w, v) in gathered[r].items():
+                D = int(dims[f])
+                ws[g][woff[f] + lo * D: woff[f] + hi * D] = w.ravel()
+                vs[g][voff[f] + lo: voff[f] + hi] = v
+        return ws, vs
+
+    def close(a, b, tol, atol=1e-30):
+        a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+        return bool(np.all(np.abs(a - b) <= tol * np.maximum(np.abs(b), 1e-30) + atol))
+
+    for step in range(args.steps):
+        pre = [None] * world if rank == 0 else None
+        dist.gather_object(_shards(eng, F), pre, dst=0)
+        rng = np.random.default_rng([step, rank, 77])
+        lengths, ids = make_batch(rng, rows, B, max_len=9, zipf=1.1)
+        up = upstream(rng, B, int(dims.sum()))
+        got = eng.forward(lengths, ids)
+        eng.backward_update(up)
+        if M > 1:
+            eng.sync_replicas()
+        ins = [None] * world if rank == 0 else None
+        dist.gather_object((lengths, ids, up, got, _shards(eng, F)), ins, dst=0)
+        if rank != 0:
+            continue
+        ws, vs = assemble(pre)
+        st = MeshState(spec, ws, vs, [np.zeros(spec.replica_rows(), np.uint8) for _ in range(M)])
+        want = st.step(port, [x[0] for x in ins], [x[1] for x in ins], [x[2] for x in ins], do_sync=M > 1)
+        post_w, post_v = assemble([x[4] for x in ins])
+        for r in range(world):
+            if not np.array_equal(ins[r][3].view(np.uint32), want[r].view(np.uint32)):
+                fails.append(f"bf16 pooled step {step} rank {r}")
+        for g in range(M):
+            if not close(post_v[g], st.vs[g], 1e-5):
+                fails.append(f"bf16 moments step {step} group {g}")
+            # the replica mean of two bf16-rounded rows can cancel (opposite
+            # updates of a near-zero weight), so the relative bar gets an
+            # absolute floor of one bf16 ulp at the table's RMS magnitude
+            atol = 2.0 ** -8 * float(np.sqrt(np.mean(np.square(st.ws[g], dtype=np.float64))))
+            if not close(post_w[g], st.ws[g], 1e-2, atol):
+                d = np.abs(post_w[g].astype(np.float64) - st.ws[g])
+                fails.append(f"bf16 weights step {step} group {g}: max|d|={d.max():.3g} atol={atol:.3g}")
+    eng.close()
+    if rank == 0:
+        if fails:
+            print("MP PARITY FAIL", world, M, "bf16", *fails[:20], sep="\n  ")
+            dist.barrier()
+            return 1
+        print(f"MP PARITY OK T={world} M={M} N={N} bf16 steps={args.steps}")
+    dist.barrier()
+    return 0
 
 
 if __name__ == "__main__":

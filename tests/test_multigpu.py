@@ -28,10 +28,17 @@ CASES = [
     (4, 4, "table-wise", []),
     (2, 1, "table-wise", ["--engine-out", "--ckpt"]),
     (4, 2, "table-wise", ["--engine-out"]),
+    (4, 2, "row-wise", ["--bf16", "--steps", "3"]),
+    (2, 1, "row-wise", ["--bf16", "--steps", "3"]),
 ]
 
 
-@pytest.mark.parametrize("T,M,strategy,extra", CASES)
+def _case_id(c):
+    T, M, strategy, extra = c
+    return f"T{T}-M{M}-{strategy}" + "".join(x.replace("--", "-") for x in extra if x.startswith("--"))
+
+
+@pytest.mark.parametrize("T,M,strategy,extra", CASES, ids=[_case_id(c) for c in CASES])
 def test_mesh_parity(T, M, strategy, extra):
     if _ngpu() < T:
         pytest.skip(f"needs {T} GPUs")
