@@ -257,7 +257,7 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out);
 /* Per-phase device time (CUDA events on the context's stream), summed since
  * the last query.  Phases: 0 input staging, 1 K1 bucketing, 2 id all-to-all,
  * 3 K2 lookup, 4 pooled all-to-all, 5 combine, 6 grad gather, 7 grad
- * all-to-all, 8 radix sort, 9 segmentation, 10 fused update, 11 replica sync.
+ * all-to-all, 8 radix sort, 9 host count sync (N > 1), 10 fused update, 11 replica sync.
  * n must be >= 12.  Profiling is off by default. */
 #define S2D_NUM_PHASES 12
 int s2d_ctx_set_profiling(s2d_ctx* ctx, int on);

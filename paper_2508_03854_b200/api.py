@@ -391,7 +391,7 @@ class Sparse2DEmbedding:
         return {k: getattr(s, k) for k, _ in L.StepStats._fields_}
 
     PHASES = ("input", "bucket", "a2a_ids", "lookup", "a2a_lookup", "combine", "grad_gather", "a2a_grad",
-              "sort", "segments", "update", "sync")
+              "sort", "count_sync", "update", "sync")
 
     def set_profiling(self, on: bool):
         L.check(self.lib.s2d_ctx_set_profiling(self._ctx, 1 if on else 0))

@@ -140,6 +140,7 @@ void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st);
 
 struct GradGatherArgs {
   const FeatDev* feats;
+  const RangeDev* ranges;      // owner of a single-owner table = ranges[rbeg].owner
   uint32_t F, B, N, sum_dims;
   const uint32_t* cnt;
   const uint64_t* eoff;

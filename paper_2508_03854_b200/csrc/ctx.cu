@@ -463,6 +463,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
                          scan_tmp.cap);
     launch_publish_counts(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF, B, ptrs(p_xcnt), local, stream);
     peer_barrier();
+    phase_begin(kPhCountSync);
     read_counts();  // count matrix -> offsets; grows the peer buffers collectively
     phase_begin(kPhA2AIds);
     ba.peer_ids = ptrs(p_ids);
@@ -716,6 +717,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     phase_begin(kPhGradGather);
     GradGatherArgs ga{};
     ga.feats = d_feats.as<FeatDev>();
+    ga.ranges = d_ranges.as<RangeDev>();
     ga.F = F;
     ga.B = B;
     ga.N = N;

@@ -53,7 +53,7 @@ enum Phase : int {
   kPhGradGather,  // C2 send layout
   kPhA2AGrad,     // C2 all-to-all
   kPhSort,        // K3a radix sort
-  kPhSegments,    // run-length segmentation
+  kPhCountSync,   // N > 1: host read of the count matrix (GPU waits for the next launch)
   kPhUpdate,      // K3b chunk sums + K4 fused update
   kPhSync,        // K5 replica sync
   kNumPhases

@@ -109,29 +109,52 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
 
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256) k_grad_gather(const GradGatherArgs a) {
-  constexpr int GPW = 32 / LPB;
+  // kU bags per group iteration: all their row loads are issued before any
+  // store, so each group keeps kU rows in flight toward NVLink
+  constexpr int GPW = 32 / LPB, kU = 4;
   const uint32_t lane = lane_id();
   const uint32_t grp = lane / LPB, gl = lane % LPB;
   const uint64_t BF = (uint64_t)a.B * a.F;
   const uint64_t slots = (uint64_t)gridDim.x * (blockDim.x / 32) * GPW;
   const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * GPW + grp;
-  for (uint64_t b = first; b < BF; b += slots) {
-    const uint32_t f = (uint32_t)(b % a.F);
-    const uint32_t d4 = __ldg(&a.feats[f].dim) >> 2;
-    const float* up = a.upstream + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
-    float4 x[VPL];
+  for (uint64_t b0 = first * kU; b0 < BF; b0 += slots * kU) {
+    float4 x[kU][VPL];
+    uint32_t d4[kU];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const uint32_t c4 = gl + v * LPB;
-      if (c4 < d4) x[v] = __ldg(reinterpret_cast<const float4*>(up + c4 * 4));
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t b = b0 + u;
+      d4[u] = 0;
+      if (b < BF) {
+        const uint32_t f = (uint32_t)(b % a.F);
+        d4[u] = __ldg(&a.feats[f].dim) >> 2;
+        const float* up = a.upstream + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const uint32_t c4 = gl + v * LPB;
+          if (c4 < d4[u]) x[u][v] = __ldg(reinterpret_cast<const float4*>(up + c4 * 4));
+        }
+      }
     }
-    for (uint32_t o = 0; o < a.N; ++o) {  // (s, f, o ascending) order, trainer.cpp:446-453
-      if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
-      float* dst = reinterpret_cast<float*>(a.peer_dst.p[o]) + a.peer_adj[o] + __ldg(a.eoff + (uint64_t)o * BF + b);
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const uint32_t c4 = gl + v * LPB;
-        if (c4 < d4) *reinterpret_cast<float4*>(dst + c4 * 4) = x[v];
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t b = b0 + u;
+      if (b >= BF) break;
+      const uint32_t f = (uint32_t)(b % a.F);
+      // (s, f, o ascending) order, trainer.cpp:446-453; single-owner tables
+      // have exactly one candidate owner
+      uint32_t o = 0, o_end = a.N;
+      if (__ldg(&a.feats[f].single)) {
+        o = __ldg(&a.ranges[__ldg(&a.feats[f].rbeg)].owner);
+        o_end = o + 1;
+      }
+      for (; o < o_end; ++o) {
+        if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
+        float* dst = reinterpret_cast<float*>(a.peer_dst.p[o]) + a.peer_adj[o] + __ldg(a.eoff + (uint64_t)o * BF + b);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const uint32_t c4 = gl + v * LPB;
+          if (c4 < d4[u]) *reinterpret_cast<float4*>(dst + c4 * 4) = x[u][v];
+        }
       }
     }
   }
@@ -272,15 +295,15 @@ void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st) {
   if (!BF) return;
   const int d4 = max_dim / 4;
   if (d4 <= 8)
-    k_grad_gather<8, 1><<<grid_for(BF, 32, kGridCap), 256, 0, st>>>(a);
+    k_grad_gather<8, 1><<<grid_for(BF, 32 * 4, kGridCap), 256, 0, st>>>(a);
   else if (d4 <= 16)
-    k_grad_gather<16, 1><<<grid_for(BF, 16, kGridCap), 256, 0, st>>>(a);
+    k_grad_gather<16, 1><<<grid_for(BF, 16 * 4, kGridCap), 256, 0, st>>>(a);
   else if (d4 <= 32)
-    k_grad_gather<32, 1><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+    k_grad_gather<32, 1><<<grid_for(BF, 8 * 4, kGridCap), 256, 0, st>>>(a);
   else if (d4 <= 64)
-    k_grad_gather<32, 2><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+    k_grad_gather<32, 2><<<grid_for(BF, 8 * 4, kGridCap), 256, 0, st>>>(a);
   else
-    k_grad_gather<32, 4><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+    k_grad_gather<32, 4><<<grid_for(BF, 8 * 4, kGridCap), 256, 0, st>>>(a);
   S2D_LAUNCH_CHECK();
 }
 
