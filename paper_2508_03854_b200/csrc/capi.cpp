@@ -215,6 +215,7 @@ int s2d_ctx_set_profiling(s2d_ctx* ctx, int on) {
     auto* c = as_ctx(ctx);
     c->phase_end();
     c->profile = on != 0;
+    c->profile_hot_only = on == 2;
   });
 }
 

@@ -53,6 +53,9 @@ HostBuf::~HostBuf() {
 void Ctx::phase_begin(int ph) {
   if (!profile) return;
   if (open_phase >= 0) phase_end();
+  // every event pair drains the stream between two kernels, so the light
+  // mode brackets only the three hot kernels
+  if (profile_hot_only && ph != kPhLookup && ph != kPhSort && ph != kPhUpdate) return;
   while (ev_pool.size() < ev_used + 2) {
     cudaEvent_t e;
     S2D_CUDA(cudaEventCreate(&e));
