@@ -259,7 +259,7 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out);
  * 3 K2 lookup, 4 pooled all-to-all, 5 combine, 6 grad gather, 7 grad
  * all-to-all, 8 radix sort, 9 host count sync (N > 1), 10 fused update, 11 replica sync.
  * n must be >= 12.  Profiling is off by default; on = 1 times every phase,
- * on = 2 only the lookup, sort and update kernels (fewer stream drains). */
+ * on = 2 only the fused update (phase 10; fewer stream drains). */
 #define S2D_NUM_PHASES 12
 int s2d_ctx_set_profiling(s2d_ctx* ctx, int on);
 int s2d_get_phase_times(s2d_ctx* ctx, double* ms, uint32_t* counts, uint32_t n);

@@ -394,8 +394,8 @@ class Sparse2DEmbedding:
               "sort", "count_sync", "update", "sync")
 
     def set_profiling(self, on, hot_only: bool = False):
-        """Phase events on the engine stream; hot_only brackets only the
-        lookup / sort / update kernels (s2d_ctx_set_profiling levels 1 / 2)."""
+        """Phase events on the engine stream; hot_only brackets only the fused
+        update (s2d_ctx_set_profiling levels 1 / 2)."""
         L.check(self.lib.s2d_ctx_set_profiling(self._ctx, (2 if hot_only else 1) if on else 0))
 
     def phase_times(self) -> dict:

@@ -8,6 +8,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/sparse2d_b200.h"
@@ -36,6 +37,29 @@ void count_launch();
     ::s2d::count_launch();            \
     S2D_CUDA(cudaGetLastError());     \
   } while (0)
+
+// Kernel launch with programmatic stream serialization (PDL): the kernel may
+// be scheduled during its predecessor's tail and must call pdl_wait() first.
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  S2D_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+  S2D_LAUNCH_CHECK();
+}
+
+// zero `bytes` at p on st as a PDL kernel (keeps the launch chain unbroken,
+// unlike cudaMemsetAsync)
+void launch_zero(void* p, size_t bytes, cudaStream_t st);
 
 // Device fault bits (checked once per step, SURVEY.md 5 failure detection).
 enum : uint32_t { kErrIdRange = 1u, kErrNonfinite = 2u, kErrPeerTimeout = 4u };

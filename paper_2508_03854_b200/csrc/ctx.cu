@@ -53,9 +53,9 @@ HostBuf::~HostBuf() {
 void Ctx::phase_begin(int ph) {
   if (!profile) return;
   if (open_phase >= 0) phase_end();
-  // every event pair drains the stream between two kernels, so the light
-  // mode brackets only the three hot kernels
-  if (profile_hot_only && ph != kPhLookup && ph != kPhSort && ph != kPhUpdate) return;
+  // every event pair drains the stream between two kernels (and breaks their
+  // PDL overlap), so the light mode brackets only the dominant update kernels
+  if (profile_hot_only && ph != kPhUpdate) return;
   while (ev_pool.size() < ev_used + 2) {
     cudaEvent_t e;
     S2D_CUDA(cudaEventCreate(&e));
@@ -346,7 +346,8 @@ void Ctx::check_faults() {
 }
 
 void Ctx::finish_call() {
-  S2D_CUDA(cudaMemcpyAsync(err_host.p, err.p, 4, cudaMemcpyDeviceToHost, stream));
+  // strict: wait and raise now; otherwise faults surface at s2d_synchronize
+  // (no copy node here: it would break the kernels' PDL chain across calls)
   if (strict) synchronize_and_check();
 }
 

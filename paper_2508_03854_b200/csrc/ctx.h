@@ -137,7 +137,7 @@ struct Ctx {
 
   // profiling
   bool profile = false;
-  bool profile_hot_only = false;  // events only around the lookup, sort and update kernels
+  bool profile_hot_only = false;  // events only around the update kernels (the dominant phase)
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
   std::vector<std::pair<int, size_t>> ev_marks;  // (phase, index of start event)

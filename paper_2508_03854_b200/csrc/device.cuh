@@ -12,6 +12,15 @@ namespace s2d {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Programmatic dependent launch: a kernel launched with pdl_launch may be
+// scheduled while its predecessor on the stream drains; it waits here (first
+// statement, before touching any predecessor output) until that grid has
+// completed and flushed.  A no-op when launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Let the dependent grid be scheduled now (persistent single-wave kernels
+// only: a multi-wave grid would hand its free slots to waiting blocks).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // 16-byte weight vector -> 4 doubles.  fp32: one float4; bf16: 4 x bf16 (8 B).
 template <typename WT>
 struct Vec4;

@@ -37,6 +37,7 @@ struct OpNonzeroDim {
 template <typename T, typename Op>
 __global__ void __launch_bounds__(kThreads) k_tile_reduce(const uint32_t* __restrict__ in, uint64_t n,
                                                           Op op, T* __restrict__ tile_sum) {
+  pdl_wait();
   using BlockReduce = cub::BlockReduce<T, kThreads>;
   __shared__ typename BlockReduce::TempStorage tmp;
   const uint64_t base = (uint64_t)blockIdx.x * kTile;
@@ -52,6 +53,7 @@ __global__ void __launch_bounds__(kThreads) k_tile_reduce(const uint32_t* __rest
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_scan_tiles(T* __restrict__ tile_sum, uint64_t ntiles) {
+  pdl_wait();
   using BlockScan = cub::BlockScan<T, kThreads>;
   __shared__ typename BlockScan::TempStorage tmp;
   __shared__ T carry;
@@ -75,6 +77,7 @@ template <typename T, typename Op>
 __global__ void __launch_bounds__(kThreads) k_tile_scan(const uint32_t* __restrict__ in, uint64_t n, Op op,
                                                         const T* __restrict__ tile_sum, uint64_t ntiles,
                                                         T* __restrict__ out) {
+  pdl_wait();
   using BlockScan = cub::BlockScan<T, kThreads>;
   __shared__ typename BlockScan::TempStorage tmp;
   const uint64_t base = (uint64_t)blockIdx.x * kTile;
@@ -106,15 +109,29 @@ void scan_impl(const uint32_t* in, T* out, uint64_t n, Op op, cudaStream_t st, v
     S2D_CUDA(cudaMemsetAsync(out, 0, sizeof(T), st));
     return;
   }
-  k_tile_reduce<T, Op><<<(unsigned)ntiles, kThreads, 0, st>>>(in, n, op, tile_sum);
-  S2D_LAUNCH_CHECK();
-  k_scan_tiles<T><<<1, kThreads, 0, st>>>(tile_sum, ntiles);
-  S2D_LAUNCH_CHECK();
-  k_tile_scan<T, Op><<<(unsigned)ntiles, kThreads, 0, st>>>(in, n, op, tile_sum, ntiles, out);
-  S2D_LAUNCH_CHECK();
+  pdl_launch(k_tile_reduce<T, Op>, dim3((unsigned)ntiles), dim3(kThreads), 0, st, in, n, op, tile_sum);
+  pdl_launch(k_scan_tiles<T>, dim3(1), dim3(kThreads), 0, st, tile_sum, ntiles);
+  pdl_launch(k_tile_scan<T, Op>, dim3((unsigned)ntiles), dim3(kThreads), 0, st, in, n, op,
+             static_cast<const T*>(tile_sum), ntiles, out);
+}
+
+__global__ void k_zero(uint4* p, size_t n16, uint8_t* tail, uint32_t tail_n) {
+  pdl_wait();
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) p[i] = make_uint4(0, 0, 0, 0);
+  if (blockIdx.x == 0 && threadIdx.x < tail_n) tail[threadIdx.x] = 0;
 }
 
 }  // namespace
+
+void launch_zero(void* p, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  if (reinterpret_cast<uintptr_t>(p) % 16) throw Error(S2D_ECUDA, "launch_zero needs a 16-byte aligned buffer");
+  const size_t n16 = bytes / 16;
+  const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((n16 + 255) / 256, 148 * 8));
+  pdl_launch(k_zero, dim3(grid), dim3(256), 0, st, reinterpret_cast<uint4*>(p), n16,
+             reinterpret_cast<uint8_t*>(p) + n16 * 16, (uint32_t)(bytes % 16));
+}
 
 size_t scan_tmp_bytes(uint64_t n) { return ((n + kTile - 1) / kTile + 1) * sizeof(uint64_t); }
 

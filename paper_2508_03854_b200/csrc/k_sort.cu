@@ -58,6 +58,7 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t key, int shift, int pbits)
 template <int RADIX>
 __global__ void __launch_bounds__(kThreads) k_radix_hist(const uint32_t* __restrict__ keys, uint64_t n,
                                                          int bits, uint32_t* __restrict__ hist) {
+  pdl_wait();
   constexpr int DB = RADIX == 512 ? 9 : 8;
   __shared__ uint32_t h[kMaxPasses][RADIX];
   for (int i = threadIdx.x; i < kMaxPasses * RADIX; i += kThreads) (&h[0][0])[i] = 0;
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(const uint32_t* __restr
                                                          int shift, int pbits,
                                                          const uint32_t* __restrict__ hist,
                                                          uint64_t* lookback, uint32_t* tile_ctr) {
+  pdl_wait();
   constexpr int DPT = RADIX / kThreads;  // digits per thread in the per-digit phases
   __shared__ uint32_t s_keys[kTile];
   __shared__ uint32_t s_vals[kTile];
@@ -244,15 +246,15 @@ bool sort_impl(const Layout& L, uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
   uint64_t* lb = reinterpret_cast<uint64_t*>(base + L.lb_off);
   uint32_t* ctr = reinterpret_cast<uint32_t*>(base + L.ctr_off);
   const unsigned hblocks = (unsigned)std::min<uint64_t>(L.ntiles * 2, 148 * 8);
-  k_radix_hist<RADIX><<<hblocks ? hblocks : 1, kThreads, 0, st>>>(keys_a, n, bits, hist);
-  S2D_LAUNCH_CHECK();
+  pdl_launch(k_radix_hist<RADIX>, dim3(hblocks ? hblocks : 1), dim3(kThreads), 0, st,
+             static_cast<const uint32_t*>(keys_a), n, bits, hist);
   uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
   for (int p = 0; p < L.npass; ++p) {
     const int shift = p * L.dbits;
     const int pb = std::min(L.dbits, bits - shift);
-    k_radix_pass<RADIX><<<(unsigned)L.ntiles, kThreads, 0, st>>>(ki, vi, ko, vo, n, shift, pb, hist + p * RADIX,
-                                                                 lb + (size_t)p * L.ntiles * RADIX, ctr + p);
-    S2D_LAUNCH_CHECK();
+    pdl_launch(k_radix_pass<RADIX>, dim3((unsigned)L.ntiles), dim3(kThreads), 0, st, static_cast<const uint32_t*>(ki),
+               static_cast<const uint32_t*>(vi), ko, vo, n, shift, pb, static_cast<const uint32_t*>(hist + p * RADIX),
+               lb + (size_t)p * L.ntiles * RADIX, ctr + p);
     std::swap(ki, ko);
     std::swap(vi, vo);
   }
@@ -271,7 +273,7 @@ bool radix_sort_pairs(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint
   const Layout L = layout(n, bits);
   if (L.total > tmp_bytes) throw Error(S2D_ECUDA, "radix sort workspace too small");
   char* base = reinterpret_cast<char*>(tmp);
-  S2D_CUDA(cudaMemsetAsync(base, 0, L.total, st));
+  launch_zero(base, L.total, st);
   if (L.radix == 512) return sort_impl<512>(L, keys_a, vals_a, keys_b, vals_b, n, bits, base, st);
   return sort_impl<256>(L, keys_a, vals_a, keys_b, vals_b, n, bits, base, st);
 }

@@ -167,6 +167,8 @@ __device__ __forceinline__ uint32_t ring_off(uint32_t slot, int v, uint32_t lane
 // rows after the shard and are never read back.
 template <typename WT, int VPL, bool UNI>
 __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
+  pdl_wait();  // persistent single wave: let the next grid queue behind us
+  pdl_trigger();
   constexpr int VB = Row<WT>::kVecBytes;
   constexpr int kWinStages = 32 / kRowsPerStage;
   constexpr uint32_t kRowBytes = VPL * 32 * VB;  // ring slot stride
@@ -498,6 +500,7 @@ __device__ __forceinline__ void reg_sum_range(const StreamUpdateArgs& a, uint32_
 // level-1 partials: range k = [kC, kC+C) lying inside one segment
 template <int VPL>
 __global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a) {
+  pdl_wait();
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t n_ranges = a.n / kC;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -521,6 +524,7 @@ __global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a
 // level-2 partials: kP consecutive level-1 ranges inside one segment
 template <int VPL>
 __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a) {
+  pdl_wait();
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   const uint64_t n_groups = a.n / ((uint64_t)kC * kP);
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -546,6 +550,8 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
 // the range name row 0 -- is in bounds and the ring copies need no predicate.
 template <typename WT, int VPL, bool FULL>
 __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
+  pdl_wait();  // persistent single wave
+  pdl_trigger();
   constexpr int kWinStages = 32 / kRowsPerStage;
   constexpr uint32_t kGRow = VPL * 32 * 16;
   constexpr uint32_t kNone = 0xffffffffu;
@@ -856,9 +862,8 @@ void lookup_launch_t(const LookupArgs& a, cudaStream_t st) {
     S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lookup_ring<WT, VPL, UNI>, nw * 32, smem));
     if (occ < 1) occ = 1;
   }
-  S2D_CUDA(cudaMemsetAsync(a.ticket, 0, sizeof(uint32_t), st));
-  k_lookup_ring<WT, VPL, UNI><<<grid_units(n_units, nw, 148 * occ), nw * 32, smem, st>>>(a);
-  S2D_LAUNCH_CHECK();
+  launch_zero(a.ticket, 16, st);
+  pdl_launch(k_lookup_ring<WT, VPL, UNI>, dim3(grid_units(n_units, nw, 148 * occ)), dim3(nw * 32), smem, st, a);
 }
 
 template <typename WT, int VPL>
@@ -880,14 +885,9 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
     init = true;
   }
   const bool full = a.uni_dim == 128u * VPL;
-  if (a.n >= 2 * kC) {
-    k_range_partials<VPL><<<grid_units(a.n / kC, 8, 148 * 16), 256, 0, st>>>(a);
-    S2D_LAUNCH_CHECK();
-  }
-  if (a.n >= 2ull * kC * kP) {
-    k_group_partials<VPL><<<grid_units(a.n / (kC * kP), 8, 148 * 8), 256, 0, st>>>(a);
-    S2D_LAUNCH_CHECK();
-  }
+  if (a.n >= 2 * kC) pdl_launch(k_range_partials<VPL>, dim3(grid_units(a.n / kC, 8, 148 * 16)), dim3(256), 0, st, a);
+  if (a.n >= 2ull * kC * kP)
+    pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP), 8, 148 * 8)), dim3(256), 0, st, a);
   static int occ = 0;
   if (!occ) {
     S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_ring<WT, VPL, false>, nw_u * 32,
@@ -896,10 +896,9 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   }
   const unsigned grid = grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ);
   if (full)
-    k_update_ring<WT, VPL, true><<<grid, nw_u * 32, nw_u * pw_u, st>>>(a);
+    pdl_launch(k_update_ring<WT, VPL, true>, dim3(grid), dim3(nw_u * 32), nw_u * pw_u, st, a);
   else
-    k_update_ring<WT, VPL, false><<<grid, nw_u * 32, nw_u * pw_u, st>>>(a);
-  S2D_LAUNCH_CHECK();
+    pdl_launch(k_update_ring<WT, VPL, false>, dim3(grid), dim3(nw_u * 32), nw_u * pw_u, st, a);
 }
 
 }  // namespace
@@ -923,7 +922,7 @@ void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream
 }
 
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st) {
-  S2D_CUDA(cudaMemsetAsync(a.counters, 0, 4 * sizeof(uint32_t), st));
+  launch_zero(a.counters, 4 * sizeof(uint32_t), st);
   if (a.n == 0) return;
   const uint32_t d4 = a.max_d4;
   if (bf16) {
