@@ -383,6 +383,7 @@ def run_ours(args):
     eng.set_profiling(False)
     phases = eng.phase_times()
     ms = ev0.elapsed_time(ev1)
+    host_timed = dict(host_s)  # host time of the timed steps only
     # full phase split (every phase bracketed) from a separate pass of the same steps
     eng.set_profiling(True)
     n_split = min(args.steps, 20)
@@ -400,7 +401,7 @@ def run_ours(args):
     st = eng.stats()
     mine = {"nnz_owned": st["nnz_owned"], "unique_rows": st["unique_rows"], "ms": ms,
             "phase_ms": {p: round(v[0] / max(1, n_split), 4) for p, v in split.items()},
-            "host_ms_per_step": {k: round(1e3 * v / max(1, args.steps), 4) for k, v in host_s.items()}}
+            "host_ms_per_step": {k: round(1e3 * v / max(1, args.steps), 4) for k, v in host_timed.items()}}
     per_rank = [mine]
     if world > 1:
         per_rank = [None] * world

@@ -63,6 +63,7 @@ __global__ void k_init_rows(WT* __restrict__ w, uint64_t wbase, uint32_t table_i
 
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
+  pdl_wait();
   constexpr int GPW = 32 / LPB;
   const uint32_t lane = lane_id();
   const uint32_t grp = lane / LPB, gl = lane % LPB;
@@ -109,6 +110,7 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
 
 template <int LPB, int VPL>
 __global__ void __launch_bounds__(256) k_grad_gather(const GradGatherArgs a) {
+  pdl_wait();
   // kU bags per group iteration: all their row loads are issued before any
   // store, so each group keeps kU rows in flight toward NVLink
   constexpr int GPW = 32 / LPB, kU = 4;
@@ -177,6 +179,7 @@ __device__ __forceinline__ uint32_t owner_of(const RangeDev* __restrict__ r, uin
 }
 
 __global__ void __launch_bounds__(256) k_bucket_count(const BucketArgs a) {
+  pdl_wait();
   for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < a.BF;
        b += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t f = (uint32_t)(b % a.F);
@@ -205,6 +208,7 @@ __global__ void __launch_bounds__(256) k_bucket_count(const BucketArgs a) {
 // one owner leave as contiguous runs (coalesced NVLink stores) in exactly the
 // canonical order of build_demand (trainer.cpp:286-307).
 __global__ void __launch_bounds__(256) k_bucket_permute(const BucketArgs a) {
+  pdl_wait();
   const uint32_t lane = lane_id();
   const uint64_t n_units = (a.BF + 31) / 32;
   const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
@@ -278,16 +282,15 @@ void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st) {
   if (!BF) return;
   const int d4 = max_dim / 4;
   if (d4 <= 8)
-    k_combine<8, 1><<<grid_for(BF, 32, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_combine<8, 1>, dim3(grid_for(BF, 32, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 16)
-    k_combine<16, 1><<<grid_for(BF, 16, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_combine<16, 1>, dim3(grid_for(BF, 16, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 32)
-    k_combine<32, 1><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_combine<32, 1>, dim3(grid_for(BF, 8, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 64)
-    k_combine<32, 2><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_combine<32, 2>, dim3(grid_for(BF, 8, kGridCap)), dim3(256), 0, st, a);
   else
-    k_combine<32, 4><<<grid_for(BF, 8, kGridCap), 256, 0, st>>>(a);
-  S2D_LAUNCH_CHECK();
+    pdl_launch(k_combine<32, 4>, dim3(grid_for(BF, 8, kGridCap)), dim3(256), 0, st, a);
 }
 
 void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st) {
@@ -295,28 +298,25 @@ void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st) {
   if (!BF) return;
   const int d4 = max_dim / 4;
   if (d4 <= 8)
-    k_grad_gather<8, 1><<<grid_for(BF, 32 * 4, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_grad_gather<8, 1>, dim3(grid_for(BF, 32 * 4, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 16)
-    k_grad_gather<16, 1><<<grid_for(BF, 16 * 4, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_grad_gather<16, 1>, dim3(grid_for(BF, 16 * 4, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 32)
-    k_grad_gather<32, 1><<<grid_for(BF, 8 * 4, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_grad_gather<32, 1>, dim3(grid_for(BF, 8 * 4, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 64)
-    k_grad_gather<32, 2><<<grid_for(BF, 8 * 4, kGridCap), 256, 0, st>>>(a);
+    pdl_launch(k_grad_gather<32, 2>, dim3(grid_for(BF, 8 * 4, kGridCap)), dim3(256), 0, st, a);
   else
-    k_grad_gather<32, 4><<<grid_for(BF, 8 * 4, kGridCap), 256, 0, st>>>(a);
-  S2D_LAUNCH_CHECK();
+    pdl_launch(k_grad_gather<32, 4>, dim3(grid_for(BF, 8 * 4, kGridCap)), dim3(256), 0, st, a);
 }
 
 void launch_bucket_count(const BucketArgs& a, cudaStream_t st) {
   if (!a.BF) return;
-  k_bucket_count<<<grid_for(a.BF, 256, kGridCap), 256, 0, st>>>(a);
-  S2D_LAUNCH_CHECK();
+  pdl_launch(k_bucket_count, dim3(grid_for(a.BF, 256, kGridCap)), dim3(256), 0, st, a);
 }
 
 void launch_bucket_permute(const BucketArgs& a, cudaStream_t st) {
   if (!a.BF) return;
-  k_bucket_permute<<<grid_for(a.BF, 256, kGridCap), 256, 0, st>>>(a);
-  S2D_LAUNCH_CHECK();
+  pdl_launch(k_bucket_permute, dim3(grid_for(a.BF, 256, kGridCap)), dim3(256), 0, st, a);
 }
 
 }  // namespace s2d

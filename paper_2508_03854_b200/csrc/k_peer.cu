@@ -24,6 +24,7 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 
 __global__ void k_peer_barrier(PeerPtrs flags, uint64_t* my_flags, uint32_t me, uint32_t n, uint64_t epoch,
                                uint32_t* err) {
+  pdl_wait();  // every prior kernel (its peer stores included) completed and flushed
   const uint32_t p = threadIdx.x;
   __threadfence_system();
   if (p < n) st_release_sys(reinterpret_cast<uint64_t*>(flags.p[p]) + me, epoch);
@@ -45,6 +46,7 @@ __global__ void k_peer_barrier(PeerPtrs flags, uint64_t* my_flags, uint32_t me, 
 // partial floats for o) from the exclusive scans' block boundaries.
 __global__ void k_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF,
                                  uint32_t batch, PeerPtrs xcnt, uint32_t me) {
+  pdl_wait();
   const uint32_t o = threadIdx.x;
   if (o >= N) return;
   const uint64_t ids = (uint64_t)send_off[(uint64_t)(o + 1) * BF] - send_off[(uint64_t)o * BF];
@@ -61,14 +63,12 @@ __global__ void k_publish_counts(const uint32_t* send_off, const uint64_t* eoff,
 
 void launch_peer_barrier(const PeerPtrs& flags, uint64_t* my_flags, uint32_t me, uint32_t n, uint64_t epoch,
                          uint32_t* err, cudaStream_t st) {
-  k_peer_barrier<<<1, 32, 0, st>>>(flags, my_flags, me, n, epoch, err);
-  S2D_LAUNCH_CHECK();
+  pdl_launch(k_peer_barrier, dim3(1), dim3(32), 0, st, flags, my_flags, me, n, epoch, err);
 }
 
 void launch_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF, uint32_t batch,
                            const PeerPtrs& xcnt, uint32_t me, cudaStream_t st) {
-  k_publish_counts<<<1, 32, 0, st>>>(send_off, eoff, N, BF, batch, xcnt, me);
-  S2D_LAUNCH_CHECK();
+  pdl_launch(k_publish_counts, dim3(1), dim3(32), 0, st, send_off, eoff, N, BF, batch, xcnt, me);
 }
 
 }  // namespace s2d
