@@ -371,6 +371,7 @@ def run_ours(args):
     launches0 = s2d.launch_count()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     host_s["forward"] = host_s["backward"] = 0.0
+    wait0 = eng.stats()["host_wait_ns"]
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for k in range(args.steps):
@@ -384,6 +385,7 @@ def run_ours(args):
     phases = eng.phase_times()
     ms = ev0.elapsed_time(ev1)
     host_timed = dict(host_s)  # host time of the timed steps only
+    host_timed["blocked_on_counts"] = (eng.stats()["host_wait_ns"] - wait0) * 1e-9
     # full phase split (every phase bracketed) from a separate pass of the same steps
     eng.set_profiling(True)
     n_split = min(args.steps, 20)

@@ -101,6 +101,7 @@ typedef struct {
   uint64_t ids_bytes_sent;    /* part of a2a_bytes_sent: lengths + ids (K1 permute) */
   uint64_t lookup_bytes_sent; /* part of a2a_bytes_sent: partials / pooled rows (K2) */
   uint64_t grad_bytes_sent;   /* part of a2a_bytes_sent: gradient rows (grad gather) */
+  uint64_t host_wait_ns;      /* host time blocked on the device count read (N > 1), cumulative */
 } s2d_step_stats;
 
 const char* s2d_last_error(void);

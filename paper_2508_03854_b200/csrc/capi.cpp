@@ -238,6 +238,7 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out) {
     auto* c = as_ctx(ctx);
     c->refresh_stats();
     *out = c->stats;
+    out->host_wait_ns = c->host_wait_total_ns;
   });
 }
 

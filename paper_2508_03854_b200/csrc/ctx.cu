@@ -17,6 +17,7 @@
 // row per non-empty (bag, owner) entry in (sample, feature) order
 // (trainer.cpp:283-313, 331-335, 446-453).
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 
 #include "ctx.h"
@@ -533,6 +534,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     ca.pooled = d_pooled;
     ca.skip_single = engine_out ? 1 : 0;
     launch_combine(ca, (int)max_dim, stream);
+    phase_end();  // the gap until the backward call is no phase
     uint64_t ef_own = 0, sent = 0, recv = 0;
     for (uint32_t q = 0; q < N; ++q) {
       ef_own += ef_from[q];
@@ -620,10 +622,14 @@ void Ctx::peer_barrier() {
 // Count matrix xcnt[n][o] = (ids n sends to o, partial floats of those
 // entries, n's batch), published by every requester into every peer.
 void Ctx::read_counts() {
-  std::vector<uint64_t> x((size_t)N * N * 3);
-  S2D_CUDA(cudaMemcpyAsync(x.data(), p_xcnt.buf.p, x.size() * 8, cudaMemcpyDeviceToHost, stream));
+  const size_t nx = (size_t)N * N * 3;
+  h_xcnt.ensure(nx * 8);  // pinned: a pageable D2H would stage synchronously
+  S2D_CUDA(cudaMemcpyAsync(h_xcnt.p, p_xcnt.buf.p, nx * 8, cudaMemcpyDeviceToHost, stream));
+  const auto t0 = std::chrono::steady_clock::now();
   S2D_CUDA(cudaStreamSynchronize(stream));
-  check_faults();
+  host_wait_total_ns += (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+                            std::chrono::steady_clock::now() - t0).count();
+  const uint64_t* x = h_xcnt.as<uint64_t>();
   auto at = [&](uint32_t n, uint32_t o, int k) { return x[((size_t)n * N + o) * 3 + k]; };
   for (uint32_t n = 0; n < N; ++n)
     if (at(n, 0, 2) != B)

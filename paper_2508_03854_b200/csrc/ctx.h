@@ -127,7 +127,8 @@ struct Ctx {
   DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
   DevBuf sync_list, sync_lists, sync_count, sync_packed, sync_gathered, sync_tmp;
-  HostBuf h_counts;
+  HostBuf h_counts, h_xcnt;
+  uint64_t host_wait_total_ns = 0;  // host blocked on the count read, since creation
   std::vector<uint64_t> nnz_to, nnz_from, ef_to, ef_from, send_bound, eoff_req_bound, own_eoff_bound,
       ids_base_at_owner, part_base_at_req, grad_base_at_owner;
   bool sorted_in_b = false;

@@ -68,42 +68,60 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
   const uint32_t lane = lane_id();
   const uint32_t grp = lane / LPB, gl = lane % LPB;
   const uint64_t BF = (uint64_t)a.B * a.F;
-  const uint64_t slots = (uint64_t)gridDim.x * (blockDim.x / 32) * GPW;
-  const uint64_t first = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * GPW + grp;
-  for (uint64_t b = first; b < BF; b += slots) {
-    const uint32_t f = (uint32_t)(b % a.F);
-    const uint32_t d4 = __ldg(&a.feats[f].dim) >> 2;
-    if (a.skip_single && __ldg(&a.feats[f].single)) {
-      // the owner stored the pooled row itself; only empty bags remain (zero)
-      bool any = false;
-      for (uint32_t o = 0; o < a.N; ++o) any |= __ldg(a.cnt + (uint64_t)o * BF + b) != 0;
-      if (any) continue;
-    }
-    double acc[VPL][4];
-#pragma unroll
-    for (int v = 0; v < VPL; ++v)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) acc[v][q] = 0.0;
-    for (uint32_t o = 0; o < a.N; ++o) {  // ascending owner (trainer.cpp:378-386)
-      if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
-      const float* p = a.recv + __ldg(a.eoff + (uint64_t)o * BF + b);
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) {
-        const uint32_t c4 = gl + v * LPB;
-        if (c4 < d4) {
-          const float4 x = __ldg(reinterpret_cast<const float4*>(p + c4 * 4));
-          acc[v][0] += (double)x.x;
-          acc[v][1] += (double)x.y;
-          acc[v][2] += (double)x.z;
-          acc[v][3] += (double)x.w;
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  const uint64_t warp = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  for (uint64_t base = warp * 32; base < BF; base += warps * 32) {
+    // lane per bag: which of these 32 bags still need the combine?  (With
+    // the engine-owned output the owner of a single-owner table stored the
+    // pooled row itself; only its empty bags remain, to be zeroed.)
+    bool need = false;
+    {
+      const uint64_t b = base + lane;
+      if (b < BF) {
+        need = true;
+        const uint32_t f = (uint32_t)(b % a.F);
+        if (a.skip_single && __ldg(&a.feats[f].single)) {
+          bool any = false;
+          for (uint32_t o = 0; o < a.N; ++o) any |= __ldg(a.cnt + (uint64_t)o * BF + b) != 0;
+          need = !any;
         }
       }
     }
-    float* out = a.pooled + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
+    uint32_t m = __ballot_sync(0xffffffffu, need);
+    while (m) {  // group g takes the g-th remaining bag
+      uint32_t mm = m;
+      for (uint32_t q = 0; q < grp && mm; ++q) mm &= mm - 1;
+      for (int q = 0; q < GPW && m; ++q) m &= m - 1;
+      if (!mm) continue;
+      const uint64_t b = base + (__ffs(mm) - 1);
+      const uint32_t f = (uint32_t)(b % a.F);
+      const uint32_t d4 = __ldg(&a.feats[f].dim) >> 2;
+      double acc[VPL][4];
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) {
-      const uint32_t c4 = gl + v * LPB;
-      if (c4 < d4) store_f32x4_stream(out + c4 * 4, acc[v]);
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[v][q] = 0.0;
+      for (uint32_t o = 0; o < a.N; ++o) {  // ascending owner (trainer.cpp:378-386)
+        if (__ldg(a.cnt + (uint64_t)o * BF + b) == 0) continue;
+        const float* p = a.recv + __ldg(a.eoff + (uint64_t)o * BF + b);
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const uint32_t c4 = gl + v * LPB;
+          if (c4 < d4) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(p + c4 * 4));
+            acc[v][0] += (double)x.x;
+            acc[v][1] += (double)x.y;
+            acc[v][2] += (double)x.z;
+            acc[v][3] += (double)x.w;
+          }
+        }
+      }
+      float* out = a.pooled + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const uint32_t c4 = gl + v * LPB;
+        if (c4 < d4) store_f32x4_stream(out + c4 * 4, acc[v]);
+      }
     }
   }
 }
@@ -282,15 +300,15 @@ void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st) {
   if (!BF) return;
   const int d4 = max_dim / 4;
   if (d4 <= 8)
-    pdl_launch(k_combine<8, 1>, dim3(grid_for(BF, 32, kGridCap)), dim3(256), 0, st, a);
+    pdl_launch(k_combine<8, 1>, dim3(grid_for(BF, 256, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 16)
-    pdl_launch(k_combine<16, 1>, dim3(grid_for(BF, 16, kGridCap)), dim3(256), 0, st, a);
+    pdl_launch(k_combine<16, 1>, dim3(grid_for(BF, 256, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 32)
-    pdl_launch(k_combine<32, 1>, dim3(grid_for(BF, 8, kGridCap)), dim3(256), 0, st, a);
+    pdl_launch(k_combine<32, 1>, dim3(grid_for(BF, 256, kGridCap)), dim3(256), 0, st, a);
   else if (d4 <= 64)
-    pdl_launch(k_combine<32, 2>, dim3(grid_for(BF, 8, kGridCap)), dim3(256), 0, st, a);
+    pdl_launch(k_combine<32, 2>, dim3(grid_for(BF, 256, kGridCap)), dim3(256), 0, st, a);
   else
-    pdl_launch(k_combine<32, 4>, dim3(grid_for(BF, 8, kGridCap)), dim3(256), 0, st, a);
+    pdl_launch(k_combine<32, 4>, dim3(grid_for(BF, 256, kGridCap)), dim3(256), 0, st, a);
 }
 
 void launch_grad_gather(const GradGatherArgs& a, int max_dim, cudaStream_t st) {
