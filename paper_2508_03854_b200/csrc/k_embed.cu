@@ -202,9 +202,20 @@ __global__ void __launch_bounds__(256) k_bucket_count(const BucketArgs a) {
        b += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t f = (uint32_t)(b % a.F);
     const uint32_t rows = __ldg(&a.feats[f].rows), rb = __ldg(&a.feats[f].rbeg), re = __ldg(&a.feats[f].rend);
+    const uint32_t len = __ldg(a.lengths + b);
+    if (re - rb == 1) {  // single-owner table: every id goes to that owner, whose
+      // lookup range-checks it (kErrIdRange there); no per-id work here
+      const uint32_t ow = __ldg(&a.ranges[rb].owner);
+      for (uint32_t o = 0; o < a.N; ++o) {
+        const uint32_t c = o == ow ? len : 0u;
+        a.cnt[(uint64_t)o * a.BF + b] = c;
+        reinterpret_cast<uint32_t*>(a.peer_len.p[o])[(uint64_t)a.me * a.BF + b] = c;
+      }
+      continue;
+    }
     uint32_t cnt[kMaxRanksPerGroup];
     for (uint32_t o = 0; o < a.N; ++o) cnt[o] = 0;
-    const uint32_t off = __ldg(a.id_off + b), len = __ldg(a.lengths + b);
+    const uint32_t off = __ldg(a.id_off + b);
     for (uint32_t k = 0; k < len; ++k) {
       const uint32_t id = __ldg(a.ids + off + k);
       if (id >= rows) {
@@ -252,7 +263,11 @@ __global__ void __launch_bounds__(256) k_bucket_permute(const BucketArgs a) {
       uint32_t o = 0xffffffffu, id = 0;
       if (have) {
         id = __ldg(a.ids + p);
-        if (id < __ldg(&a.feats[f].rows)) o = owner_of(a.ranges, __ldg(&a.feats[f].rbeg), __ldg(&a.feats[f].rend), id);
+        const uint32_t rb = __ldg(&a.feats[f].rbeg), re = __ldg(&a.feats[f].rend);
+        if (re - rb == 1)  // single owner: every id goes there (its lookup flags bad ids)
+          o = __ldg(&a.ranges[rb].owner);
+        else if (id < __ldg(&a.feats[f].rows))
+          o = owner_of(a.ranges, rb, re, id);
       }
       for (uint32_t q = 0; q < a.N; ++q) {
         const uint32_t sel = __ballot_sync(0xffffffffu, o == q);

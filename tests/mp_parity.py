@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--batch", type=int, default=48)
     ap.add_argument("--engine-out", action="store_true", help="zero-copy pooled output (owners write it)")
     ap.add_argument("--ckpt", action="store_true", help="S2DCKPT1 save from the mesh + load into every replica")
+    ap.add_argument("--bad-id", action="store_true",
+                    help="rank 1 sends an id past its table's rows: some rank must raise IndexError")
     ap.add_argument("--bf16", action="store_true",
                     help="bf16 shards: the oracle is re-seeded every step from the mesh's (widened) weights")
     args = ap.parse_args()
@@ -63,6 +65,8 @@ def main():
     eng.init_tables(31)
     if args.bf16:
         sys.exit(run_bf16(args, eng, dist, rank, world, M, N, rows, dims, B, eta, c, plan))
+    if args.bad_id:
+        sys.exit(run_bad_id(eng, dist, rank, world, rows, dims, B))
 
     def inputs(step, r):
         rng = np.random.default_rng([step, r, 77])
@@ -194,6 +198,36 @@ def main():
         sys.exit(1)
     print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd} ckpt={args.ckpt}")
     dist.barrier()
+
+
+def run_bad_id(eng, dist, rank, world, rows, dims, B):
+    """An id >= rows (no bounds check in the reference's build_demand,
+    trainer.cpp:293-299; std::out_of_range in pool_ids, embedding.cpp:61-63)
+    must surface as IndexError (S2D_ERANGE) on the rank that detects it: the
+    requester's bucketing for multi-owner tables, the owner's lookup for
+    single-owner tables."""
+    from cases import make_batch, upstream
+
+    eng.set_strict(False)
+    rng = np.random.default_rng([5, rank])
+    lengths, ids = make_batch(rng, rows, B, max_len=9, zipf=1.1)
+    if rank == 1:
+        ids = ids.copy()
+        ids[0] = rows[0] + 7  # bag (0, 0) belongs to table 0
+    raised = 0
+    try:
+        eng.forward(lengths, ids)
+        eng.backward_update(upstream(rng, B, int(dims.sum())))
+        eng.synchronize()
+    except IndexError:
+        raised = 1
+    flags = [None] * world
+    dist.all_gather_object(flags, raised)
+    if rank == 0:
+        ok = sum(flags) >= 1
+        print(("MP PARITY OK" if ok else "MP PARITY FAIL") + f" bad-id raised on ranks {flags}")
+    dist.barrier()
+    return 0 if sum(flags) >= 1 else 1
 
 
 def _shards(eng, F):

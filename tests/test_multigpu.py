@@ -30,6 +30,8 @@ CASES = [
     (4, 2, "table-wise", ["--engine-out"]),
     (4, 2, "row-wise", ["--bf16", "--steps", "3"]),
     (2, 1, "row-wise", ["--bf16", "--steps", "3"]),
+    (2, 1, "table-wise", ["--bad-id"]),
+    (4, 1, "row-wise", ["--bad-id"]),
 ]
 
 
