@@ -107,6 +107,9 @@ void scan_nonzero_dim_u64(const uint32_t* in, uint64_t* out, uint64_t n, uint32_
 void scan_heads_u32(const uint32_t* keys, uint32_t* out, uint64_t n, uint32_t n_slots, cudaStream_t st,
                     void* tmp, size_t tmp_bytes);
 size_t scan_tmp_bytes(uint64_t n);
+// fused: out32 = scan_u32_to_u32(in), out64 = scan_nonzero_dim_u64(in) in one pass
+void scan_count_pair(const uint32_t* in, uint32_t* out32, uint64_t* out64, uint64_t n, uint32_t F,
+                     const FeatDev* feats, cudaStream_t st, void* tmp, size_t tmp_bytes);
 
 // radix sort (k_sort.cu): stable LSD sort of (key, val) pairs by the low
 // `bits` bits of key.  keys/vals ping-pong between a and b; returns true if

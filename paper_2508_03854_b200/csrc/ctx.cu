@@ -463,9 +463,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     ba.me = local;
     ba.peer_len = ptrs(p_len);
     launch_bucket_count(ba, stream);  // also stores cnt[o][:] into owner o's receive lengths
-    scan_u32_to_u32(cnt.as<uint32_t>(), send_off.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p, scan_tmp.cap);
-    scan_nonzero_dim_u64(cnt.as<uint32_t>(), eoff_req.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream, scan_tmp.p,
-                         scan_tmp.cap);
+    scan_count_pair(cnt.as<uint32_t>(), send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), (uint64_t)N * BF, F, dfe,
+                    stream, scan_tmp.p, scan_tmp.cap);
     launch_publish_counts(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF, B, ptrs(p_xcnt), local, stream);
     peer_barrier();
     phase_begin(kPhCountSync);
@@ -478,10 +477,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     // ---- owner side: partial pools written into the requesters' buffers ----
     own_idoff.ensure(((uint64_t)N * BF + 1) * 4);
     own_eoff.ensure(((uint64_t)N * BF + 1) * 8);
-    scan_u32_to_u32(p_len.buf.as<uint32_t>(), own_idoff.as<uint32_t>(), (uint64_t)N * BF, stream, scan_tmp.p,
-                    scan_tmp.cap);
-    scan_nonzero_dim_u64(p_len.buf.as<uint32_t>(), own_eoff.as<uint64_t>(), (uint64_t)N * BF, F, dfe, stream,
-                         scan_tmp.p, scan_tmp.cap);
+    scan_count_pair(p_len.buf.as<uint32_t>(), own_idoff.as<uint32_t>(), own_eoff.as<uint64_t>(), (uint64_t)N * BF, F,
+                    dfe, stream, scan_tmp.p, scan_tmp.cap);
     keys_a.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
     vals_a.ensure(std::max<uint64_t>(nnz_own, 1) * 4);
     LookupArgs a{};

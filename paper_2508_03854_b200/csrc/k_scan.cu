@@ -115,6 +115,93 @@ void scan_impl(const uint32_t* in, T* out, uint64_t n, Op op, cudaStream_t st, v
              static_cast<const T*>(tile_sum), ntiles, out);
 }
 
+// ---- fused pair: out32 = exclusive scan of x, out64 = exclusive scan of
+// (x ? dim(k % F) : 0) over the same input in one read (ids and entry
+// floats of the [peer][bag] count matrix) -----------------------------------
+struct Pair {
+  uint32_t a;
+  uint64_t b;
+};
+struct PairSum {
+  __device__ __forceinline__ Pair operator()(const Pair& x, const Pair& y) const { return {x.a + y.a, x.b + y.b}; }
+};
+
+__device__ __forceinline__ Pair pair_of(uint32_t x, uint64_t k, const FeatDev* feats, uint32_t F) {
+  return {x, x ? (uint64_t)__ldg(&feats[k % F].dim) : 0ull};
+}
+
+__global__ void __launch_bounds__(kThreads) k_pair_reduce(const uint32_t* __restrict__ in, uint64_t n,
+                                                          const FeatDev* feats, uint32_t F, Pair* __restrict__ tile_sum) {
+  pdl_wait();
+  using BR = cub::BlockReduce<Pair, kThreads>;
+  __shared__ typename BR::TempStorage tmp;
+  const uint64_t base = (uint64_t)blockIdx.x * kTile;
+  Pair acc{0u, 0ull};
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)i * kThreads + threadIdx.x;
+    if (k < n) {
+      const Pair p = pair_of(__ldg(in + k), k, feats, F);
+      acc.a += p.a;
+      acc.b += p.b;
+    }
+  }
+  const Pair s = BR(tmp).Reduce(acc, PairSum());
+  if (threadIdx.x == 0) tile_sum[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kThreads) k_pair_scan_tiles(Pair* __restrict__ tile_sum, uint64_t ntiles) {
+  pdl_wait();
+  using BS = cub::BlockScan<Pair, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ Pair carry;
+  if (threadIdx.x == 0) carry = {0u, 0ull};
+  __syncthreads();
+  for (uint64_t base = 0; base < ntiles; base += kThreads) {
+    const uint64_t k = base + threadIdx.x;
+    const Pair x = k < ntiles ? tile_sum[k] : Pair{0u, 0ull};
+    Pair excl, total;
+    BS(tmp).ExclusiveScan(x, excl, Pair{0u, 0ull}, PairSum(), total);
+    const Pair c = carry;
+    if (k < ntiles) tile_sum[k] = {c.a + excl.a, c.b + excl.b};
+    __syncthreads();
+    if (threadIdx.x == 0) carry = {c.a + total.a, c.b + total.b};
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) tile_sum[ntiles] = carry;
+}
+
+__global__ void __launch_bounds__(kThreads) k_pair_tile_scan(const uint32_t* __restrict__ in, uint64_t n,
+                                                             const FeatDev* feats, uint32_t F,
+                                                             const Pair* __restrict__ tile_sum, uint64_t ntiles,
+                                                             uint32_t* __restrict__ out32, uint64_t* __restrict__ out64) {
+  pdl_wait();
+  using BS = cub::BlockScan<Pair, kThreads>;
+  __shared__ typename BS::TempStorage tmp;
+  const uint64_t base = (uint64_t)blockIdx.x * kTile;
+  Pair v[kItems];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)threadIdx.x * kItems + i;
+    v[i] = k < n ? pair_of(__ldg(in + k), k, feats, F) : Pair{0u, 0ull};
+  }
+  Pair excl[kItems];
+  BS(tmp).ExclusiveScan(v, excl, Pair{0u, 0ull}, PairSum());
+  const Pair off = tile_sum[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const uint64_t k = base + (uint64_t)threadIdx.x * kItems + i;
+    if (k < n) {
+      out32[k] = off.a + excl[i].a;
+      out64[k] = off.b + excl[i].b;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out32[n] = tile_sum[ntiles].a;
+    out64[n] = tile_sum[ntiles].b;
+  }
+}
+
 __global__ void k_zero(uint4* p, size_t n16, uint8_t* tail, uint32_t tail_n) {
   pdl_wait();
   const size_t stride = (size_t)gridDim.x * blockDim.x;
@@ -133,7 +220,23 @@ void launch_zero(void* p, size_t bytes, cudaStream_t st) {
              reinterpret_cast<uint8_t*>(p) + n16 * 16, (uint32_t)(bytes % 16));
 }
 
-size_t scan_tmp_bytes(uint64_t n) { return ((n + kTile - 1) / kTile + 1) * sizeof(uint64_t); }
+size_t scan_tmp_bytes(uint64_t n) { return ((n + kTile - 1) / kTile + 1) * sizeof(Pair); }
+
+void scan_count_pair(const uint32_t* in, uint32_t* out32, uint64_t* out64, uint64_t n, uint32_t F,
+                     const FeatDev* feats, cudaStream_t st, void* tmp, size_t tmp_bytes) {
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  if ((ntiles + 1) * sizeof(Pair) > tmp_bytes) throw Error(S2D_ECUDA, "scan workspace too small");
+  if (ntiles == 0) {
+    S2D_CUDA(cudaMemsetAsync(out32, 0, sizeof(uint32_t), st));
+    S2D_CUDA(cudaMemsetAsync(out64, 0, sizeof(uint64_t), st));
+    return;
+  }
+  Pair* ts = reinterpret_cast<Pair*>(tmp);
+  pdl_launch(k_pair_reduce, dim3((unsigned)ntiles), dim3(kThreads), 0, st, in, n, feats, F, ts);
+  pdl_launch(k_pair_scan_tiles, dim3(1), dim3(kThreads), 0, st, ts, ntiles);
+  pdl_launch(k_pair_tile_scan, dim3((unsigned)ntiles), dim3(kThreads), 0, st, in, n, feats, F,
+             static_cast<const Pair*>(ts), ntiles, out32, out64);
+}
 
 void scan_u32_to_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t st, void* tmp,
                      size_t tmp_bytes) {
