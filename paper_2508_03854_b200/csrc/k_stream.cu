@@ -72,7 +72,9 @@ __device__ __forceinline__ void prefetch_l2(const void* p) {
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+  // "memory": the ring reads after the wait are plain shared loads the
+  // compiler may schedule freely among themselves, but not above the wait
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ uint64_t shfl64(uint64_t v, uint32_t src) {
@@ -106,8 +108,8 @@ struct Row<float> {
     d[2] = (double)x.z;
     d[3] = (double)x.w;
   }
-  static __device__ __forceinline__ void add_s(double (&a)[4], uint32_t saddr) {
-    const float4 x = lds128(saddr);
+  static __device__ __forceinline__ void add_s(double (&a)[4], const unsigned char* sp) {
+    const float4 x = *reinterpret_cast<const float4*>(sp);
     a[0] += (double)x.x;
     a[1] += (double)x.y;
     a[2] += (double)x.z;
@@ -132,8 +134,8 @@ struct Row<__nv_bfloat16> {
     d[2] = (double)__uint_as_float(x.y << 16);
     d[3] = (double)__uint_as_float(x.y & 0xffff0000u);
   }
-  static __device__ __forceinline__ void add_s(double (&a)[4], uint32_t saddr) {
-    const uint2 x = lds64(saddr);
+  static __device__ __forceinline__ void add_s(double (&a)[4], const unsigned char* sp) {
+    const uint2 x = *reinterpret_cast<const uint2*>(sp);
     a[0] += (double)__uint_as_float(x.x << 16);
     a[1] += (double)__uint_as_float(x.x & 0xffff0000u);
     a[2] += (double)__uint_as_float(x.y << 16);
@@ -174,6 +176,7 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   constexpr uint32_t kRowBytes = VPL * 32 * VB;  // ring slot stride
   constexpr uint64_t kNone = ~0ull;
   extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t sbase = smem_u32(smem);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   // this lane's column chunk of slot 0 of the warp's ring
   const uint32_t ring_s = smem_u32(smem) + warp * kSlots * kRowBytes + lane * VB;
@@ -316,7 +319,7 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
     auto add_row = [&](uint32_t saddr) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
-        if (VPL == 1 || lane + v * 32 < d4c) Row<WT>::add_s(acc[v], saddr + v * 32 * VB);
+        if (VPL == 1 || lane + v * 32 < d4c) Row<WT>::add_s(acc[v], smem + (saddr + v * 32 * VB - sbase));
     };
 
     const uint32_t nst = (n_items + kRowsPerStage - 1) / kRowsPerStage;
@@ -393,6 +396,8 @@ __device__ __forceinline__ void ring_sum(const StreamUpdateArgs& a, uint32_t lan
                                          uint64_t t, uint32_t d4, double (&acc)[VPL][4]) {
   constexpr uint32_t kRowBytes = VPL * 32 * 16;
   constexpr int kWinStages = 32 / kRowsPerStage;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t sbase = smem_u32(smem);
   if (t <= s) return;
   const uint32_t n = (uint32_t)(t - s);
   const uint32_t nst = (n + kRowsPerStage - 1) / kRowsPerStage;
@@ -426,7 +431,7 @@ __device__ __forceinline__ void ring_sum(const StreamUpdateArgs& a, uint32_t lan
       if (r < cnt) {
 #pragma unroll
         for (int v = 0; v < VPL; ++v)
-          if (VPL == 1 || lane + v * 32 < d4) Row<float>::add_s(acc[v], base + r * kRowBytes + v * 512);
+          if (VPL == 1 || lane + v * 32 < d4) Row<float>::add_s(acc[v], smem + (base + r * kRowBytes + v * 512 - sbase));
       }
   }
   cp_wait<0>();
@@ -556,8 +561,9 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   constexpr uint32_t kGRow = VPL * 32 * 16;
   constexpr uint32_t kNone = 0xffffffffu;
   extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t sbase = smem_u32(smem);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t g_lane = smem_u32(smem) + warp * (kSlots * kGRow) + lane * 16;  // gradient ring
+  const uint32_t g_lane = sbase + warp * (kSlots * kGRow) + lane * 16;  // gradient ring
   const uint64_t n = a.n;
   const uint64_t n_units = (n + kC - 1) / kC;
   const uint32_t ud4 = a.uni_dim >> 2;
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     auto add_grad = [&](uint32_t slot) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
-        if (VPL == 1 || lane + v * 32 < d4) Row<float>::add_s(acc[v], g_lane + slot * kGRow + v * 512);
+        if (VPL == 1 || lane + v * 32 < d4) Row<float>::add_s(acc[v], smem + (g_lane + slot * kGRow + v * 512 - sbase));
     };
 
     const uint32_t nst = (n_items + kRowsPerStage - 1) / kRowsPerStage;
