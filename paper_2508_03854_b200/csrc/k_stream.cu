@@ -32,14 +32,6 @@ constexpr int kBags = 32;  // bags per lookup unit (one per lane)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void cp_async(uint32_t dst, const void* src, int bytes) {
-  if (bytes == 16)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
-  else if (bytes == 8)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
-}
 // branch-free predicated cp.async (nothing is copied when pred == 0)
 template <int BYTES>
 __device__ __forceinline__ void cp_async_p(uint32_t dst, const void* src, bool pred) {
@@ -50,21 +42,6 @@ __device__ __forceinline__ void cp_async_p(uint32_t dst, const void* src, bool p
 template <int BYTES>
 __device__ __forceinline__ void cp_async_u(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(src), "n"(BYTES));
-}
-__device__ __forceinline__ float4 lds128(uint32_t a) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint2 lds64(uint32_t a) {
-  uint2 v;
-  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint32_t lds32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(a));
-  return v;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
@@ -370,8 +347,10 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
 // reference's strictly sequential f64 sum whenever the segment fits in its
 // head's range, and otherwise re-associates at fixed chunk boundaries
 // (|dg| ~ 1e-16 relative).  |g|^2 is a per-lane in-order sum followed by a
-// fixed xor-shuffle tree.  The weight row and moment of every segment are
-// fetched through the ring together with the segment's first gradient row.
+// fixed xor-shuffle tree.  Ranges are taken from a ticket counter by
+// persistent warps.  The weight row and moment of every segment head are
+// L2-prefetched when its window is set up (32-64 items ahead) and loaded
+// into registers at the head; the flush writes them back.
 // ============================================================================
 
 constexpr uint32_t kC = 256;  // items per nominal range
