@@ -18,6 +18,7 @@
 // (trainer.cpp:283-313, 331-335, 446-453).
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 
 #include "ctx.h"
@@ -107,8 +108,9 @@ int bit_width(uint32_t x) {
 Ctx::~Ctx() {
   if (device >= 0) cudaSetDevice(device);
   if (stream) cudaStreamSynchronize(stream);
-  for (PeerBuf* pb : {&p_flags, &p_xcnt, &p_len, &p_ids, &p_part, &p_grad, &p_pooled})
+  for (PeerBuf* pb : {&p_flags, &p_xcnt, &p_len, &p_ids, &p_part, &p_grad, &p_pooled, &dp_flags, &dp_stage})
     for (void* q : pb->opened) cudaIpcCloseMemHandle(q);
+  for (void* q : dp_opened) cudaIpcCloseMemHandle(q);
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (cudaStream_t q : {h2d_stream, d2h_stream, sort_stream})
     if (q) {
@@ -251,6 +253,9 @@ void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_en
   const size_t wbytes = (n_weight_elems + pad_elems) * (bf16 ? 2 : 4);
   slot_rows = all_same_dim;
   for (uint32_t f = 0; f < F && slot_rows; ++f) slot_rows = feats[f].wbase == (uint64_t)feats[f].vbase * max_dim;
+  for (void* q : dp_opened) cudaIpcCloseMemHandle(q);  // mappings of the old replicas
+  dp_opened.clear();
+  dp_p2p = -1;
   weights.release();
   moments.release();
   dirty.release();
@@ -564,21 +569,25 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
 
 PeerPtrs Ctx::ptrs(const PeerBuf& pb) const {
   PeerPtrs pp{};
-  for (uint32_t q = 0; q < N && q < pb.ptr.size(); ++q) pp.p[q] = pb.ptr[q];
+  for (uint32_t q = 0; q < pb.ptr.size() && q < (uint32_t)kMaxPeers; ++q) pp.p[q] = pb.ptr[q];
   return pp;
 }
 
 // Collective over the MP group: every rank calls it with the same `bytes`
 // (derived from data all ranks share), so growth decisions agree.
-void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) {
+void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) { peer_alloc_in(pb, bytes, mp, N, local); }
+
+// Collective over `comm` (n ranks, this one = me): (re)allocate pb and map
+// every member's copy through CUDA IPC.
+void Ctx::peer_alloc_in(PeerBuf& pb, size_t bytes, ncclComm_t comm, uint32_t n, uint32_t me) {
   if (pb.buf.p && bytes <= pb.cap) return;
   const size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
   S2D_CUDA(cudaStreamSynchronize(stream));
   for (void* q : pb.opened) cudaIpcCloseMemHandle(q);
   pb.opened.clear();
-  hbuf.ensure((size_t)N * 64 + 64);
+  hbuf.ensure((size_t)n * 64 + 64);
   // everyone has unmapped the old buffers before anyone frees them
-  S2D_NCCL(ncclAllReduce(hbuf.p, hbuf.p, 1, ncclUint8, ncclMax, mp, stream));
+  S2D_NCCL(ncclAllReduce(hbuf.p, hbuf.p, 1, ncclUint8, ncclMax, comm, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   pb.buf.release();
   S2D_CUDA(cudaMalloc(&pb.buf.p, want));
@@ -589,14 +598,14 @@ void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) {
   S2D_CUDA(cudaIpcGetMemHandle(&h, pb.buf.p));
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
   uint8_t* dh = hbuf.as<uint8_t>();
-  S2D_CUDA(cudaMemcpy(dh + (size_t)N * 64, &h, 64, cudaMemcpyHostToDevice));
-  S2D_NCCL(ncclAllGather(dh + (size_t)N * 64, dh, 64, ncclUint8, mp, stream));
-  std::vector<cudaIpcMemHandle_t> all(N);
-  S2D_CUDA(cudaMemcpyAsync(all.data(), dh, (size_t)N * 64, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaMemcpy(dh + (size_t)n * 64, &h, 64, cudaMemcpyHostToDevice));
+  S2D_NCCL(ncclAllGather(dh + (size_t)n * 64, dh, 64, ncclUint8, comm, stream));
+  std::vector<cudaIpcMemHandle_t> all(n);
+  S2D_CUDA(cudaMemcpyAsync(all.data(), dh, (size_t)n * 64, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
-  pb.ptr.assign(N, nullptr);
-  for (uint32_t q = 0; q < N; ++q) {
-    if (q == local) {
+  pb.ptr.assign(n, nullptr);
+  for (uint32_t q = 0; q < n; ++q) {
+    if (q == me) {
       pb.ptr[q] = pb.buf.p;
       continue;
     }
@@ -609,6 +618,67 @@ void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) {
 
 float* Ctx::pooled_buffer() {
   return N > 1 ? p_pooled.buf.as<float>() : p_pooled_local.as<float>();
+}
+
+// DP group over NVLink: map every replica's weights and moments (identical
+// shard layout in every group) once; every member must agree, else the sync
+// stays on the NCCL all-gather path (S2D_SYNC_NCCL=1 forces that path).
+void Ctx::dp_setup() {
+  if (dp_p2p >= 0) return;
+  dp_p2p = 0;
+  if (M <= 1) return;
+  const char* e = std::getenv("S2D_SYNC_NCCL");
+  if (e && e[0] == '1') return;
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  hbuf.ensure((size_t)M * 128 + 128);
+  uint8_t* dh = hbuf.as<uint8_t>();
+  cudaIpcMemHandle_t h[2];
+  S2D_CUDA(cudaIpcGetMemHandle(&h[0], weights.p));
+  S2D_CUDA(cudaIpcGetMemHandle(&h[1], moments.p));
+  S2D_CUDA(cudaMemcpy(dh + (size_t)M * 128, h, 128, cudaMemcpyHostToDevice));
+  S2D_NCCL(ncclAllGather(dh + (size_t)M * 128, dh, 128, ncclUint8, dp, stream));
+  std::vector<cudaIpcMemHandle_t> all((size_t)M * 2);
+  S2D_CUDA(cudaMemcpyAsync(all.data(), dh, (size_t)M * 128, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  dp_w.assign(M, nullptr);
+  dp_v.assign(M, nullptr);
+  int ok = 1;
+  for (uint32_t g = 0; g < M && ok; ++g) {
+    if (g == group) {
+      dp_w[g] = weights.p;
+      dp_v[g] = moments.p;
+      continue;
+    }
+    for (int k = 0; k < 2 && ok; ++k) {
+      void* m = nullptr;
+      if (cudaIpcOpenMemHandle(&m, all[(size_t)g * 2 + k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        (void)cudaGetLastError();
+        ok = 0;
+        break;
+      }
+      dp_opened.push_back(m);
+      (k == 0 ? dp_w : dp_v)[g] = m;
+    }
+  }
+  // agree across the group (min over members)
+  int* hi = err_host.as<int>() + 2;
+  *hi = ok;
+  S2D_CUDA(cudaMemcpyAsync(dh, hi, 4, cudaMemcpyHostToDevice, stream));
+  S2D_NCCL(ncclAllReduce(dh, dh, 1, ncclInt32, ncclMin, dp, stream));
+  S2D_CUDA(cudaMemcpyAsync(hi, dh, 4, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  if (!*hi) {
+    for (void* q : dp_opened) cudaIpcCloseMemHandle(q);
+    dp_opened.clear();
+    return;
+  }
+  peer_alloc_in(dp_flags, (size_t)M * 8, dp, M, group);
+  dp_p2p = 1;
+}
+
+void Ctx::dp_barrier() {
+  ++dp_epoch;
+  launch_peer_barrier(ptrs(dp_flags), dp_flags.buf.as<uint64_t>(), group, M, dp_epoch, err.as<uint32_t>(), stream);
 }
 
 void Ctx::peer_barrier() {
@@ -866,6 +936,34 @@ void Ctx::replica_sync() {
   sync_list.ensure((uint64_t)count * 4);
   launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
   const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
+  dp_setup();
+  if (dp_p2p == 1) {
+    // Every replica's update of this step is complete: the list all-gather
+    // above ran after each replica's update on its stream, and the host has
+    // read its result.  Slice s of the union list is averaged by replica s.
+    // Staging per replica: [M][slice_cap] copies of its slice | [count] means.
+    const uint64_t slice_cap = (uint64_t)count / M + 1;
+    const uint64_t copies = slice_cap * M * row_floats;
+    peer_alloc_in(dp_stage, (copies + (uint64_t)count * row_floats) * 4, dp, M, group);  // same size everywhere
+    const uint32_t lo = (uint32_t)((uint64_t)count * group / M), hi = (uint32_t)((uint64_t)count * (group + 1) / M);
+    PeerPtrs means{};
+    for (uint32_t g = 0; g < M; ++g) means.p[g] = reinterpret_cast<float*>(dp_stage.ptr[g]) + copies;
+    const int sgd = opt.variant == S2D_SGD;
+    launch_p2p_push(ptrs(dp_stage), group, M, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
+                    d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), count,
+                    weights.p, bf16, moments.as<float>(), row_floats, slice_cap, stream);
+    dp_barrier();  // every copy of every slice is staged at its owner
+    launch_p2p_mean(dp_stage.buf.as<float>(), means, M, lo, hi, row_floats, slice_cap, sgd, stream);
+    dp_barrier();  // every replica's staging holds every mean
+    launch_p2p_scatter(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                       (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), count, dp_stage.buf.as<float>() + copies,
+                       row_floats, weights.p, bf16, moments.as<float>(), sgd, stream);
+    launch_zero(dirty.p, n_slots, stream);
+    stats.sync_bytes = 2 * (uint64_t)(hi - lo) * (M - 1) * (uint64_t)row_floats * 4 + (uint64_t)cmax * 4 * (M - 1);
+    phase_end();
+    finish_call();
+    return;
+  }
   sync_packed.ensure((uint64_t)count * row_floats * 4);
   sync_gathered.ensure((uint64_t)count * row_floats * 4 * M);
   launch_pack_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),

@@ -177,7 +177,16 @@ struct Ctx {
   void check_faults();
   PeerPtrs ptrs(const PeerBuf& pb) const;
   void peer_alloc(PeerBuf& pb, size_t bytes);
+  void peer_alloc_in(PeerBuf& pb, size_t bytes, ncclComm_t comm, uint32_t n, uint32_t me);
   void peer_barrier();
+  // DP group over NVLink peer memory (replica sync): every replica's
+  // weights / moments mapped, a group barrier, a staging slice
+  int dp_p2p = -1;  // -1 undecided, 0 NCCL path, 1 P2P path
+  std::vector<void*> dp_w, dp_v, dp_opened;
+  PeerBuf dp_flags, dp_stage;
+  uint64_t dp_epoch = 0;
+  void dp_setup();
+  void dp_barrier();
   void read_counts();
  public:
   float* pooled_buffer();

@@ -136,6 +136,107 @@ __global__ void k_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, 
   }
 }
 
+// ---- P2P replica mean (DP group on one NVLink domain) --------------------
+// Replica s averages slice s = [count*s/M, count*(s+1)/M) of the union list.
+// Phase 1 (push): every replica stores its copy of each union row (f32 row +
+// moment) into the slice owner's staging area, slot [g][i - lo_s], over
+// NVLink.  Phase 2, after a group barrier: the owner reads the M copies of
+// its slice locally, forms f32((sum_{g asc} f64 x_g) * (1/M))
+// (deterministic_mean_inplace, topology.cpp:150-163; moments likewise unless
+// SGD) and stores the mean into every replica.  All NVLink traffic is posted
+// stores: 2(M-1)/M rows per union row per replica, vs M-1 for an all-gather.
+template <typename WT>
+__global__ void k_p2p_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDev* feats,
+                           const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                           const uint32_t* __restrict__ list, uint32_t count, const WT* __restrict__ w,
+                           const float* __restrict__ moments, uint32_t row_floats, uint64_t slice_cap) {
+  pdl_wait();
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < count; i += warps) {
+    // slice owner s of row i: largest s with count*s/M <= i
+    uint32_t s = (uint32_t)(((uint64_t)i * M) / count);
+    while (s + 1 < M && (uint64_t)count * (s + 1) / M <= i) ++s;
+    while (s > 0 && (uint64_t)count * s / M > i) --s;
+    const uint32_t lo = (uint32_t)((uint64_t)count * s / M);
+    const uint32_t slot = list[i];
+    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+    const uint32_t dim = feats[f].dim;
+    const WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
+    float* out = reinterpret_cast<float*>(stage.p[s]) + ((uint64_t)me * slice_cap + (i - lo)) * row_floats;
+    for (uint32_t c4 = lane; c4 < dim / 4; c4 += 32) {
+      double d[4];
+      Vec4<WT>::load_rw(row + c4 * 4, d);
+      *reinterpret_cast<float4*>(out + c4 * 4) = make_float4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+    }
+    if (lane == 0) out[row_floats - 1] = moments[slot];
+  }
+}
+
+// Phase 2: the owner averages its slice (M staged copies, local reads) and
+// stores each mean row into every replica's staging "means" area at its
+// union index -- contiguous NVLink stores (storing into the peers' weight
+// rows directly would scatter over their whole shard and thrash the
+// peer-mapping TLB: measured 3x slower).
+__global__ void k_p2p_mean(const float* __restrict__ local, PeerPtrs means, uint32_t M, uint32_t lo, uint32_t hi,
+                           uint32_t row_floats, uint64_t slice_cap, int sgd) {
+  pdl_wait();
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  const double inv_m = 1.0 / (double)M;
+  const uint64_t gstride = slice_cap * row_floats;
+  const uint32_t n4 = (row_floats - 4) / 4;  // row chunks (the last chunk holds the moment)
+  for (uint32_t i = lo + blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < hi; i += warps) {
+    const float* in = local + (uint64_t)(i - lo) * row_floats;
+    for (uint32_t c4 = lane; c4 < n4; c4 += 32) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      for (uint32_t g = 0; g < M; ++g) {  // ascending group order
+        const float4 x = *reinterpret_cast<const float4*>(in + g * gstride + c4 * 4);
+        acc[0] += (double)x.x;
+        acc[1] += (double)x.y;
+        acc[2] += (double)x.z;
+        acc[3] += (double)x.w;
+      }
+      const float4 m = make_float4((float)(acc[0] * inv_m), (float)(acc[1] * inv_m), (float)(acc[2] * inv_m),
+                                   (float)(acc[3] * inv_m));
+      for (uint32_t g = 0; g < M; ++g)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(means.p[g]) + (uint64_t)i * row_floats + c4 * 4) = m;
+    }
+    if (lane == 0 && !sgd) {
+      double acc = 0.0;
+      for (uint32_t g = 0; g < M; ++g) acc += (double)in[g * gstride + row_floats - 1];
+      const float m = (float)(acc * inv_m);
+      for (uint32_t g = 0; g < M; ++g)
+        reinterpret_cast<float*>(means.p[g])[(uint64_t)i * row_floats + row_floats - 1] = m;
+    }
+  }
+}
+
+// Phase 3 (local): every replica scatters the count mean rows into its
+// weights (one rounding to the storage type) and moments.
+template <typename WT>
+__global__ void k_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                              uint32_t n_feat, const uint32_t* __restrict__ list, uint32_t count,
+                              const float* __restrict__ means, uint32_t row_floats, WT* __restrict__ w,
+                              float* __restrict__ moments, int sgd) {
+  pdl_wait();
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < count; i += warps) {
+    const uint32_t slot = list[i];
+    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+    const uint32_t dim = feats[f].dim;
+    WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
+    const float* in = means + (uint64_t)i * row_floats;
+    for (uint32_t c4 = lane; c4 < dim / 4; c4 += 32) {
+      const float4 x = *reinterpret_cast<const float4*>(in + c4 * 4);
+      const double d[4] = {(double)x.x, (double)x.y, (double)x.z, (double)x.w};
+      Vec4<WT>::store(row + c4 * 4, d);
+    }
+    if (lane == 0 && !sgd) moments[slot] = in[row_floats - 1];
+  }
+}
+
 }  // namespace
 
 // tmp layout: tile counts [ntiles] | their exclusive scan [ntiles + 1] | scan workspace
@@ -209,6 +310,42 @@ void launch_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, const 
                                              M, row_floats, rows_cap, reinterpret_cast<float*>(weights), moments, sgd,
                                              dirty);
   S2D_LAUNCH_CHECK();
+}
+
+
+void launch_p2p_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
+                     const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                     const uint32_t* list, uint32_t count, const void* weights, int bf16, const float* moments,
+                     uint32_t row_floats, uint64_t slice_cap, cudaStream_t st) {
+  if (!count) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((count + 7) / 8, 148ull * 16);
+  if (bf16)
+    pdl_launch(k_p2p_push<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted,
+               feat_of_vbase, n_feat, list, count, reinterpret_cast<const __nv_bfloat16*>(weights), moments,
+               row_floats, slice_cap);
+  else
+    pdl_launch(k_p2p_push<float>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted, feat_of_vbase,
+               n_feat, list, count, reinterpret_cast<const float*>(weights), moments, row_floats, slice_cap);
+}
+
+void launch_p2p_mean(const float* local, const PeerPtrs& means, uint32_t M, uint32_t lo, uint32_t hi,
+                     uint32_t row_floats, uint64_t slice_cap, int sgd, cudaStream_t st) {
+  if (hi <= lo) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((hi - lo + 7) / 8, 148ull * 16);
+  pdl_launch(k_p2p_mean, dim3(grid), dim3(256), 0, st, local, means, M, lo, hi, row_floats, slice_cap, sgd);
+}
+
+void launch_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                        uint32_t n_feat, const uint32_t* list, uint32_t count, const float* means, uint32_t row_floats,
+                        void* weights, int bf16, float* moments, int sgd, cudaStream_t st) {
+  if (!count) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((count + 7) / 8, 148ull * 16);
+  if (bf16)
+    pdl_launch(k_p2p_scatter<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, feats, vbase_sorted, feat_of_vbase, n_feat,
+               list, count, means, row_floats, reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd);
+  else
+    pdl_launch(k_p2p_scatter<float>, dim3(grid), dim3(256), 0, st, feats, vbase_sorted, feat_of_vbase, n_feat, list,
+               count, means, row_floats, reinterpret_cast<float*>(weights), moments, sgd);
 }
 
 }  // namespace s2d
