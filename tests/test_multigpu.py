@@ -31,13 +31,15 @@ CASES = [
     (4, 2, "row-wise", ["--bf16", "--steps", "3"]),
     (2, 1, "row-wise", ["--bf16", "--steps", "3"]),
     (2, 1, "table-wise", ["--bad-id"]),
+    (4, 2, "table-wise", ["--sync-interval", "2", "--steps", "4", "ENV:S2D_SYNC_NCCL=1"]),
     (4, 1, "row-wise", ["--bad-id"]),
 ]
 
 
 def _case_id(c):
     T, M, strategy, extra = c
-    return f"T{T}-M{M}-{strategy}" + "".join(x.replace("--", "-") for x in extra if x.startswith("--"))
+    return (f"T{T}-M{M}-{strategy}" + "".join(x.replace("--", "-") for x in extra if x.startswith("--")) +
+            "".join("-nccl-sync" for x in extra if x.startswith("ENV:S2D_SYNC_NCCL")))
 
 
 @pytest.mark.parametrize("T,M,strategy,extra", CASES, ids=[_case_id(c) for c in CASES])
@@ -45,9 +47,16 @@ def test_mesh_parity(T, M, strategy, extra):
     if _ngpu() < T:
         pytest.skip(f"needs {T} GPUs")
     port = 29500 + 7 * T + M + (0 if strategy == "row-wise" else 50) + (100 if extra else 0)
+    env = dict(os.environ)
+    for x in extra:  # "ENV:K=V" entries set the environment of the ranks
+        if x.startswith("ENV:"):
+            k, v = x[4:].split("=", 1)
+            env[k] = v
+            port += 13
+    args = [x for x in extra if not x.startswith("ENV:")]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nproc-per-node", str(T), "--master-addr",
            "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mp_parity.py"), "--groups",
-           str(M), "--strategy", strategy, *extra]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           str(M), "--strategy", strategy, *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "MP PARITY OK" in r.stdout
