@@ -287,6 +287,54 @@ def test_bf16_weights_within_tolerance(port):
         assert _close(w2, st.ws[0], 1e-2)
 
 
+@pytest.mark.parametrize("dims", [[128, 128, 128], [256, 256]])
+def test_bf16_uniform_dims_fast_paths(port, dims):
+    """bf16 shards whose rows fill whole warp chunks (D = 128 * VPL): the
+    slot-indexed lookup and the unpredicated (FULL) update paths."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(33)
+    rows = [700, 3000, 9][: len(dims)]
+    B = 128
+    spec = _spec(rows, dims, B, eta=0.1, c=1.0)
+    eng = _engine(rows, dims, eta=0.1, c=1.0, dtype="bf16")
+    eng.init_tables(8)
+    for step in range(3):
+        w, v = _download(eng, spec)
+        st = MeshState(spec, [w.copy()], [v.copy()], [np.zeros(spec.replica_rows(), np.uint8)])
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=14, zipf=1.2)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want))
+        eng.backward_update(up)
+        w2, v2 = _download(eng, spec)
+        assert _close(v2, st.vs[0], 1e-5)
+        assert _close(w2, st.ws[0], 1e-2)
+
+
+def test_fp32_full_rows_vpl2_bit_exact(port):
+    """fp32 D = 256 (VPL = 2, FULL update path, slot-indexed lookup): bit-exact."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(34)
+    rows, dims, B = [400, 2000], [256, 256], 96
+    spec = _spec(rows, dims, B, eta=0.1, c=2.0)
+    eng = _engine(rows, dims, eta=0.1, c=2.0)
+    eng.init_tables(2)
+    st = MeshState.init(port, spec, 2)
+    for step in range(3):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=12, zipf=1.1)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want))
+        eng.backward_update(up)
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
 def test_checkpoint_save_load_bytes(port, tmp_path):
     """s2d_save_tables writes the reference's S2DCKPT1 bytes for the trained
     tables (oracle writer on the oracle's replica); s2d_load_tables restores
