@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
   const WT* const Wl = W + lane * 4;  // this lane's column chunk of row 0
   const uint32_t uni_d4 = a.uni_d4;
+  const uint32_t pitch_b = uni_d4 * 4 * (uint32_t)sizeof(WT);  // row bytes (UNI)
 
   // persistent warps take units in ascending order from a ticket counter
   for (;;) {
@@ -261,7 +262,8 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
       for (int r = 0; r < kRowsPerStage; ++r) {
         if constexpr (UNI) {
           const uint32_t ri = __shfl_sync(0xffffffffu, (uint32_t)A, q + r);
-          const WT* src = Wl + (uint64_t)ri * (uni_d4 * 4);
+          // one IMAD.WIDE.U32: row ri of the lane's chunk column
+          const WT* src = reinterpret_cast<const WT*>(reinterpret_cast<const char*>(Wl) + (uint64_t)ri * pitch_b);
 #pragma unroll
           for (int v = 0; v < VPL; ++v) cp_async_u<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128);
         } else {
