@@ -278,10 +278,11 @@ int s2d_adagrad_rows(const s2d_optimizer_config* cfg, uint32_t n_rows, uint32_t 
 /* Debug view of the last step's wire buffers for bit-exact layout tests.
  * which: 0 demand lengths received [N requester][B*F] u32,
  *        1 demand ids received (canonical order) u32,
- *        2 pooled partials sent, concatenated over requesters, f32,
- *        3 gradient payload sent by this rank, concatenated over owners, f32,
+ *        2 pooled partials received from the owners, concatenated by owner, f32,
+ *        3 gradient rows received from the requesters, concatenated by requester, f32,
  *        4 owner mask per local bag u32 [B*F],
- *        5 unique rows updated (global row ids, ascending by (table,row)) u32.
+ *        5 unique rows updated (global row ids, ascending by (table,row)) u32,
+ *        6 engine-owned pooled output [B][sum dims] f32.
  * Copies min(cap, size) elements; *n = size. */
 int s2d_debug_read(s2d_ctx* ctx, int32_t which, void* out, uint64_t cap, uint64_t* n);
 

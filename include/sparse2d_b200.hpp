@@ -1,0 +1,146 @@
+// C++ face of the C ABI in sparse2d_b200.h, shaped like the reference's C++
+// API (include/sparse2d/planner.hpp, optimizer.hpp, topology.hpp) so a
+// maintainer can swap the simulator's embedding phases for the B200 step
+// without touching call sites: same argument meaning, and the status codes
+// come back as the reference's exception types (std::invalid_argument,
+// std::out_of_range, std::runtime_error; SURVEY.md 8(b) "Error conventions").
+// Header-only; link libsparse2d_b200.so.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sparse2d_b200.h"
+
+namespace sparse2d_b200 {
+
+enum class ShardingStrategy : int32_t { kTableWise = S2D_TABLE_WISE, kRowWise = S2D_ROW_WISE };
+
+// status -> the reference's exception type
+inline void check(int rc) {
+  if (rc == S2D_OK) return;
+  const std::string m = s2d_last_error();
+  switch (rc) {
+    case S2D_ERANGE:
+      throw std::out_of_range(m);
+    case S2D_EINVAL:
+    case S2D_ENONFINITE:
+      throw std::invalid_argument(m);
+    default:
+      throw std::runtime_error(m);
+  }
+}
+
+// Topology(total, groups) (topology.hpp:13-26, topology.cpp:7-17)
+inline s2d_topology make_topology(uint32_t total_ranks, uint32_t groups) {
+  s2d_topology t{};
+  check(s2d_topology_init(total_ranks, groups, &t));
+  return t;
+}
+
+// plan_greedy (planner.hpp:47-48)
+inline std::vector<s2d_plan_entry> plan_greedy(const std::vector<s2d_table_load_profile>& profiles, uint32_t n,
+                                               ShardingStrategy strategy) {
+  std::vector<s2d_plan_entry> out((size_t)profiles.size() * (n ? n : 1));
+  uint32_t k = 0;
+  check(s2d_plan_greedy(profiles.data(), (uint32_t)profiles.size(), n, (int32_t)strategy, out.data(),
+                        (uint32_t)out.size(), &k));
+  out.resize(k);
+  return out;
+}
+
+// validate_plan (planner.cpp:91-123)
+inline void validate_plan(const std::vector<s2d_plan_entry>& plan, uint32_t ranks_per_group,
+                          const std::vector<s2d_table_load_profile>& profiles) {
+  check(s2d_validate_plan(plan.data(), (uint32_t)plan.size(), ranks_per_group, profiles.data(),
+                          (uint32_t)profiles.size()));
+}
+
+// ShardingPlan::owner_of (planner.cpp:20-28)
+inline uint32_t owner_of(const std::vector<s2d_plan_entry>& plan, uint32_t table_id, uint32_t row) {
+  uint32_t o = 0;
+  check(s2d_plan_owner_of(plan.data(), (uint32_t)plan.size(), table_id, row, &o));
+  return o;
+}
+
+// imbalance_ratio (planner.cpp:125-143)
+inline double imbalance_ratio(const std::vector<double>& per_rank) {
+  double r = 0;
+  check(s2d_imbalance_ratio(per_rank.data(), (uint32_t)per_rank.size(), &r));
+  return r;
+}
+
+// effective_lr (optimizer.cpp:61-63), with OptimizerConfig::validate
+inline double effective_lr(double v, const s2d_optimizer_config& cfg) {
+  double lr = 0;
+  check(s2d_effective_lr(v, &cfg, &lr));
+  return lr;
+}
+
+// adagrad_row_step (optimizer.hpp:52-53) on one row, through the device
+// kernel of the fused update; returns the effective learning rate
+inline double adagrad_row_step(std::vector<float>& w, float& v, const std::vector<double>& g,
+                               const s2d_optimizer_config& cfg) {
+  if (g.size() != w.size()) throw std::invalid_argument("g and w must have the same length");
+  double lr = 0;
+  check(s2d_adagrad_rows(&cfg, 1, (uint32_t)w.size(), w.data(), &v, g.data(), &lr));
+  return lr;
+}
+
+// One rank's step engine (replaces the embedding phases of
+// Trainer::Impl::run_step, trainer.cpp:615-663).  RAII over s2d_ctx.
+class Engine {
+ public:
+  Engine(int device, uint32_t total_ranks, uint32_t groups, uint32_t rank, const uint8_t* nccl_id = nullptr) {
+    check(s2d_ctx_create(device, total_ranks, groups, rank, nccl_id, &ctx_));
+  }
+  ~Engine() {
+    if (ctx_) s2d_ctx_destroy(ctx_);
+  }
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  void register_tables(const std::vector<s2d_table_desc>& tables, const std::vector<s2d_plan_entry>& plan,
+                       int32_t dtype = S2D_F32) {
+    check(s2d_register_tables(ctx_, tables.data(), (uint32_t)tables.size(), plan.data(), (uint32_t)plan.size(),
+                              dtype));
+  }
+  void set_optimizer(const s2d_optimizer_config& cfg) { check(s2d_set_optimizer(ctx_, &cfg)); }
+  void init_tables(uint64_t seed) { check(s2d_init_tables(ctx_, seed)); }
+  void set_stream(void* cuda_stream) { check(s2d_ctx_set_stream(ctx_, cuda_stream)); }
+  void set_strict(bool on) { check(s2d_ctx_set_strict(ctx_, on ? 1 : 0)); }
+  void set_async_host(bool on) { check(s2d_ctx_set_async_host(ctx_, on ? 1 : 0)); }
+
+  // forward: sample-major bags; mem = S2D_HOST | S2D_DEVICE for all buffers
+  void lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t* ids, uint64_t nnz, float* pooled,
+                      int32_t mem) {
+    check(s2d_lookup_forward(ctx_, batch, lengths, ids, nnz, pooled, mem));
+  }
+  void backward_update(const float* upstream, int32_t mem) { check(s2d_backward_update(ctx_, upstream, mem)); }
+  void replica_sync() { check(s2d_replica_sync(ctx_)); }
+  void synchronize() { check(s2d_synchronize(ctx_)); }
+
+  // Trainer::save_tables / load_tables (trainer.cpp:875-896)
+  void save_tables(const std::string& path) { check(s2d_save_tables(ctx_, path.c_str())); }
+  void load_tables(const std::string& path) { check(s2d_load_tables(ctx_, path.c_str())); }
+
+  void shard_read(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v) {
+    check(s2d_shard_read(ctx_, table, lo, hi, w, v));
+  }
+  void shard_write(uint32_t table, uint32_t lo, uint32_t hi, const float* w, const float* v) {
+    check(s2d_shard_write(ctx_, table, lo, hi, w, v));
+  }
+  s2d_step_stats stats() {
+    s2d_step_stats s{};
+    check(s2d_get_step_stats(ctx_, &s));
+    return s;
+  }
+  s2d_ctx* raw() const { return ctx_; }
+
+ private:
+  s2d_ctx* ctx_ = nullptr;
+};
+
+}  // namespace sparse2d_b200

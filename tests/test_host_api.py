@@ -121,3 +121,24 @@ def test_c_abi_error_codes_and_messages():
     cfg = _lib.OptimizerConfigC(0.1, 1e-8, 0.0, 0)
     assert lib.s2d_effective_lr(1.0, C.byref(cfg), C.byref(out)) == _lib.S2D_EINVAL
     assert b"optimizer.c" in lib.s2d_last_error()
+
+
+def test_cxx_wrapper_host_api(tmp_path):
+    """include/sparse2d_b200.hpp (the reference-shaped C++ API over the C ABI)
+    compiles and keeps planner / optimizer semantics and exception types."""
+    import shutil
+    import subprocess
+
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("no g++")
+    lib_dir = os.path.join(ROOT, "paper_2508_03854_b200")
+    exe = str(tmp_path / "wrapper_smoke")
+    r = subprocess.run([cxx, "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cxx", "wrapper_smoke.cpp"), "-L", lib_dir, "-lsparse2d_b200",
+                        f"-Wl,-rpath,{lib_dir}", "-o", exe], capture_output=True, text=True)
+    if r.returncode != 0 and "cannot find -lsparse2d_b200" in r.stderr:
+        pytest.skip("library not built")
+    assert r.returncode == 0, r.stderr[-2000:]
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "WRAPPER OK" in r.stdout, r.stdout + r.stderr
