@@ -875,13 +875,17 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   if (a.n >= 2 * kC) pdl_launch(k_range_partials<VPL>, dim3(grid_units(a.n / kC, 8, 148 * 16)), dim3(256), 0, st, a);
   if (a.n >= 2ull * kC * kP)
     pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP), 8, 148 * 8)), dim3(256), 0, st, a);
-  static int occ = 0;
-  if (!occ) {
-    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_update_ring<WT, VPL, false>, nw_u * 32,
-                                                           nw_u * pw_u));
-    if (occ < 1) occ = 1;
+  static int occ[2] = {0, 0};  // per variant: their register counts differ
+  if (!occ[full]) {
+    if (full)
+      S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_update_ring<WT, VPL, true>, nw_u * 32,
+                                                             nw_u * pw_u));
+    else
+      S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_update_ring<WT, VPL, false>, nw_u * 32,
+                                                             nw_u * pw_u));
+    if (occ[full] < 1) occ[full] = 1;
   }
-  const unsigned grid = grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ);
+  const unsigned grid = grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ[full]);
   if (full)
     pdl_launch(k_update_ring<WT, VPL, true>, dim3(grid), dim3(nw_u * 32), nw_u * pw_u, st, a);
   else
