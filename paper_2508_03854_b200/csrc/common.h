@@ -246,6 +246,7 @@ struct GenArgs {
 void launch_gen_batch(const GenArgs& a, cudaStream_t st);
 
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
+uint64_t stream_partial1_rows(uint64_t n);  // level-1 partial rows (part2 follows them)
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 

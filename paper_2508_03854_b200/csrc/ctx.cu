@@ -850,7 +850,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ua.weights = weights.p;
     ua.moments = moments.as<float>();
     ua.dirty = M > 1 ? dirty.as<uint8_t>() : nullptr;
-    const uint64_t nparts1 = n / 256 + 2;
+    const uint64_t nparts1 = stream_partial1_rows(n);
     ua.part1 = chunk_part.as<double>();
     ua.part2 = chunk_part.as<double>() + nparts1 * max_dim;
     ua.inv_batch = 1.0 / (double)((uint64_t)N * B);  // group batch (trainer.cpp:462)

@@ -894,6 +894,8 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+uint64_t stream_partial1_rows(uint64_t n) { return n / kC + 2; }
+
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim) {
   return ((n / kC + 2) + (n / (kC * kP) + 2)) * (uint64_t)max_dim * sizeof(double);
 }
