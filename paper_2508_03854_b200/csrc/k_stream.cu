@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
 // ============================================================================
 
 constexpr uint32_t kC = 128;  // items per nominal range
-constexpr uint32_t kP = 32;   // ranges per level-2 partial
+constexpr uint32_t kP = 16;   // ranges per level-2 partial
 
 __device__ __forceinline__ void row_ref(const StreamUpdateArgs& a, uint32_t key, uint64_t& wofs, uint32_t& d4) {
   if (a.uni_dim) {
