@@ -544,7 +544,10 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t sbase = smem_u32(smem);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint32_t g_lane = sbase + warp * (kSlots * kGRow) + lane * 16;  // gradient ring
+  // per warp: gradient ring | head moments of two windows (cp.async, 256 B)
+  constexpr uint32_t kWarpBytes = kSlots * kGRow + 256;
+  const uint32_t g_lane = sbase + warp * kWarpBytes + lane * 16;  // gradient ring
+  const uint32_t mom_s = sbase + warp * kWarpBytes + kSlots * kGRow;
   const uint64_t n = a.n;
   const uint64_t n_units = (n + kC - 1) / kC;
   const uint32_t ud4 = a.uni_dim >> 2;
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       key = have ? __ldg(a.keys + p) : kNone;
       val = have ? __ldg(a.vals + p) : 0u;
     };
-    auto gen = [&](uint32_t key, uint32_t val, Win& w) {
+    auto gen = [&](uint32_t key, uint32_t val, Win& w, uint32_t win) {
       uint32_t before = __shfl_up_sync(0xffffffffu, key, 1);
       if (lane == 0) before = prev_key;
       prev_key = __shfl_sync(0xffffffffu, key, 31);
@@ -602,12 +605,14 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       w.hm = __ballot_sync(0xffffffffu, head);
       // warm L2 with the weight row and moment of every segment head; the
       // consumer loads them into registers when it reaches the head
+      // each head's moment goes to shared memory by cp.async (it lands with
+      // the next stage's group, long before the consumer reaches the head)
+      cp_async_p<4>(mom_s + ((win & 1u) * 32u + lane) * 4u, a.moments + (head ? key : 0u), head);
       if constexpr (FULL) {  // slot-indexed rows of VPL*128 elements: no per-item row metadata
         if (head) {
           const char* row = reinterpret_cast<const char*>(W + (uint64_t)key * (VPL * 128));
 #pragma unroll
           for (uint32_t o = 0; o < VPL * 128 * sizeof(WT); o += 128) prefetch_l2(row + o);
-          prefetch_l2(a.moments + key);
         }
       } else {
         w.d4 = 0;
@@ -617,16 +622,15 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
           const char* row = reinterpret_cast<const char*>(W + w.wofs);
           const uint32_t bytes = w.d4 * 4 * (uint32_t)sizeof(WT);
           for (uint32_t o = 0; o < bytes; o += 128) prefetch_l2(row + o);
-          prefetch_l2(a.moments + key);
         }
       }
     };
     Win wc_, wn_;
     uint32_t rk, rv;
     load_raw(0, rk, rv);
-    gen(rk, rv, wc_);
+    gen(rk, rv, wc_, 0);
     load_raw(1, rk, rv);
-    gen(rk, rv, wn_);
+    gen(rk, rv, wn_, 1);
     load_raw(2, rk, rv);
     uint32_t wc = 0;
 
@@ -735,7 +739,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       if (s > 0 && s % kWinStages == 0) {
         ++wc;
         wc_ = wn_;
-        gen(rk, rv, wn_);
+        gen(rk, rv, wn_, wc + 1);
         load_raw(wc + 2, rk, rv);
       }
       produce(s + kStages - 1);
@@ -769,7 +773,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 #pragma unroll
             for (int v = 0; v < VPL; ++v)
               if (lane + v * 32 < d4) wraw[v] = Row<WT>::ldg(W + wofs + (lane + v * 32) * 4);
-            vold = a.moments[cur];
+            vold = *reinterpret_cast<const float*>(smem + (mom_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
           }
           add_grad(slot0 + r);
         }
@@ -863,7 +867,7 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
 
 template <typename WT, int VPL>
 void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
-  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16;
+  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16 + 256;  // ring + head moments
   const uint32_t nw_u = warps_for(pw_u, 4);
   static bool init = false;
   if (!init) {
