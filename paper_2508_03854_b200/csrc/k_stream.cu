@@ -544,10 +544,14 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t sbase = smem_u32(smem);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  // per warp: gradient ring | head moments of two windows (cp.async, 256 B)
-  constexpr uint32_t kWarpBytes = kSlots * kGRow + 256;
+  // per warp: gradient ring | head moments of two windows (cp.async, 256 B) |
+  // the range's sorted keys and row offsets (cp.async, 2 x kC x 4 B)
+  constexpr uint32_t kWarpBytes = kSlots * kGRow + 256 + 8 * kC;
   const uint32_t g_lane = sbase + warp * kWarpBytes + lane * 16;  // gradient ring
   const uint32_t mom_s = sbase + warp * kWarpBytes + kSlots * kGRow;
+  const uint32_t uk_s = mom_s + 256, uv_s = uk_s + 4 * kC;
+  const uint32_t* const ukeys = reinterpret_cast<const uint32_t*>(smem + (uk_s - sbase));
+  const uint32_t* const uvals = reinterpret_cast<const uint32_t*>(smem + (uv_s - sbase));
   const uint64_t n = a.n;
   const uint64_t n_units = (n + kC - 1) / kC;
   const uint32_t ud4 = a.uni_dim >> 2;
@@ -562,13 +566,31 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     const uint64_t u = __shfl_sync(0xffffffffu, t, 0);
     if (u >= n_units) break;
     const uint64_t ra = u * kC, re = (ra + kC < n) ? ra + kC : n;
+    {  // stage the range's keys and row offsets: one round trip per range
+      const uint32_t m = (uint32_t)(re - ra);
+      for (uint32_t c = lane * 4; c < kC; c += 128) {
+        if (c + 4 <= m) {
+          cp_async_u<16>(uk_s + c * 4, a.keys + ra + c);
+          cp_async_u<16>(uv_s + c * 4, a.vals + ra + c);
+        } else {
+          for (uint32_t q = c; q < m && q < c + 4; ++q) {
+            cp_async_u<4>(uk_s + q * 4, a.keys + ra + q);
+            cp_async_u<4>(uv_s + q * 4, a.vals + ra + q);
+          }
+        }
+      }
+      cp_commit();
+    }
+    const uint32_t key_before = (lane == 0 && ra > 0) ? __ldg(a.keys + ra - 1) : kNone;
+    cp_wait<0>();
+    __syncwarp();
     // first segment head in [ra, re)
     uint64_t h = ~0ull;
     for (uint64_t c = ra; c < re; c += 32) {
       const uint64_t p = c + lane;
-      const uint32_t k = p < re ? __ldg(a.keys + p) : kNone;
+      const uint32_t k = p < re ? ukeys[p - ra] : kNone;
       uint32_t before = __shfl_up_sync(0xffffffffu, k, 1);
-      if (lane == 0) before = p > 0 ? __ldg(a.keys + p - 1) : kNone;
+      if (lane == 0) before = c == ra ? key_before : ukeys[c - 1 - ra];
       const uint32_t bal = __ballot_sync(0xffffffffu, k < a.n_slots && k != before);
       if (bal) {
         h = c + (__ffs(bal) - 1);
@@ -590,8 +612,8 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     auto load_raw = [&](uint32_t win, uint32_t& key, uint32_t& val) {
       const uint64_t p = h + (uint64_t)win * 32 + lane;
       const bool have = win < nwin && p < re;
-      key = have ? __ldg(a.keys + p) : kNone;
-      val = have ? __ldg(a.vals + p) : 0u;
+      key = have ? ukeys[p - ra] : kNone;
+      val = have ? uvals[p - ra] : 0u;
     };
     auto gen = [&](uint32_t key, uint32_t val, Win& w, uint32_t win) {
       uint32_t before = __shfl_up_sync(0xffffffffu, key, 1);
@@ -867,7 +889,7 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
 
 template <typename WT, int VPL>
 void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
-  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16 + 256;  // ring + head moments
+  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16 + 256 + 8 * kC;  // ring + head moments + range keys/rows
   const uint32_t nw_u = warps_for(pw_u, 4);
   static bool init = false;
   if (!init) {
