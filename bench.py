@@ -314,7 +314,7 @@ def run_ours(args):
         nid = obj[0]
     # expected lookups = ids + weighted distinct rows per table (Workload.plan_cost)
     tables = [s2d.TableConfig(int(r), int(d), w.plan_cost(f, n_mp)) for f, (r, d) in enumerate(zip(w.rows, w.dims))]
-    plan = None
+    plan = w.table_plan(n_mp) if (w.strategy == "table-wise" and n_mp > 1) else None
     if args.plan_rotate:
         prof = [(i, t.rows * t.dim * 4, t.expected_lookups, t.rows) for i, t in enumerate(tables)]
         plan = s2d.plan_greedy(prof, n_mp, w.strategy)

@@ -225,6 +225,7 @@ struct StreamUpdateArgs {
   uint8_t* dirty;                // may be null
   double* part1;                 // level-1 range partials [n/C][max_dim]
   double* part2;                 // level-2 partials [n/(C*P)][max_dim]
+  double* part3;                 // level-3 partials [n/(C*P*P)][max_dim]
   double inv_batch, eta, eps, c;
   double inv_c;                  // 1/c, exact when c_pow2
   int c_pow2;                    // c is a power of two: v/c == v*inv_c bit for bit
@@ -247,6 +248,7 @@ void launch_gen_batch(const GenArgs& a, cudaStream_t st);
 
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
 uint64_t stream_partial1_rows(uint64_t n);  // level-1 partial rows (part2 follows them)
+uint64_t stream_partial2_rows(uint64_t n);  // level-2 partial rows (part3 follows them)
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 

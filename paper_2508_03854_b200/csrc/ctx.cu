@@ -853,6 +853,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     const uint64_t nparts1 = stream_partial1_rows(n);
     ua.part1 = chunk_part.as<double>();
     ua.part2 = chunk_part.as<double>() + nparts1 * max_dim;
+    ua.part3 = ua.part2 + stream_partial2_rows(n) * max_dim;
     ua.inv_batch = 1.0 / (double)((uint64_t)N * B);  // group batch (trainer.cpp:462)
     ua.eta = opt.eta;
     ua.eps = opt.eps;

@@ -507,15 +507,18 @@ __global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a
   }
 }
 
-// level-2 partials: kP consecutive level-1 ranges inside one segment
+// level-(L+1) partials: kP consecutive level-L partials, all inside one
+// segment (level 2 over level-1 ranges, level 3 over level-2 groups), so the
+// head warp of a segment of length S adds O(S / (kC kP^2) + 2 kP) partials
 template <int VPL>
-__global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a) {
+__global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a, const double* __restrict__ src,
+                                                        double* __restrict__ dst, uint64_t span) {
   pdl_wait();
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
-  const uint64_t n_groups = a.n / ((uint64_t)kC * kP);
+  const uint64_t n_groups = a.n / span;
   const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
   for (uint64_t m = 1 + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; m < n_groups; m += stride) {
-    const uint64_t s = m * kC * kP, t = s + (uint64_t)kC * kP;
+    const uint64_t s = m * span, t = s + span;
     const uint32_t key = __ldg(a.keys + s - 1);
     if (key >= a.n_slots || __ldg(a.keys + t - 1) != key) continue;
     uint64_t wofs;
@@ -526,8 +529,8 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
     for (int v = 0; v < VPL; ++v)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
-    for (uint32_t r = 0; r < kP; ++r) add_partial<VPL>(a.part1 + (m * kP + r) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
-    store_partial<VPL>(a.part2 + m * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+    for (uint32_t r = 0; r < kP; ++r) add_partial<VPL>(src + (m * kP + r) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+    store_partial<VPL>(dst + m * (uint64_t)a.max_d4 * 4, lane, d4, acc);
   }
 }
 
@@ -827,7 +830,10 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
         }
       }
       while (k < kend) {
-        if (k % kP == 0 && k + kP <= kend) {
+        if (k % (kP * kP) == 0 && k + kP * kP <= kend) {
+          add_partial<VPL>(a.part3 + (k / (kP * kP)) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+          k += kP * kP;
+        } else if (k % kP == 0 && k + kP <= kend) {
           add_partial<VPL>(a.part2 + (k / kP) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
           k += kP;
         } else {
@@ -900,7 +906,11 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   const bool full = a.uni_dim == 128u * VPL;
   if (a.n >= 2 * kC) pdl_launch(k_range_partials<VPL>, dim3(grid_units(a.n / kC, 8, 148 * 16)), dim3(256), 0, st, a);
   if (a.n >= 2ull * kC * kP)
-    pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP), 8, 148 * 8)), dim3(256), 0, st, a);
+    pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP), 8, 148 * 8)), dim3(256), 0, st, a,
+               static_cast<const double*>(a.part1), a.part2, (uint64_t)kC * kP);
+  if (a.n >= 2ull * kC * kP * kP)
+    pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP * kP), 8, 148 * 8)), dim3(256), 0, st, a,
+               static_cast<const double*>(a.part2), a.part3, (uint64_t)kC * kP * kP);
   static int occ[2] = {0, 0};  // per variant: their register counts differ
   if (!occ[full]) {
     if (full)
@@ -921,9 +931,11 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
 }  // namespace
 
 uint64_t stream_partial1_rows(uint64_t n) { return n / kC + 2; }
+uint64_t stream_partial2_rows(uint64_t n) { return n / ((uint64_t)kC * kP) + 2; }
 
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim) {
-  return ((n / kC + 2) + (n / (kC * kP) + 2)) * (uint64_t)max_dim * sizeof(double);
+  return (stream_partial1_rows(n) + stream_partial2_rows(n) + (n / ((uint64_t)kC * kP * kP) + 2)) *
+         (uint64_t)max_dim * sizeof(double);
 }
 
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st) {
