@@ -43,6 +43,10 @@ template <int BYTES>
 __device__ __forceinline__ void cp_async_u(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(src), "n"(BYTES));
 }
+// L2-only variant (16 B): no L1 allocation for streamed rows
+__device__ __forceinline__ void cp_async_cg16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
 }
@@ -265,7 +269,12 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
           // one IMAD.WIDE.U32: row ri of the lane's chunk column
           const WT* src = reinterpret_cast<const WT*>(reinterpret_cast<const char*>(Wl) + (uint64_t)ri * pitch_b);
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) cp_async_u<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128);
+          for (int v = 0; v < VPL; ++v) {
+            if constexpr (VB == 16)
+              cp_async_cg16(base + r * kRowBytes + v * 32 * VB, src + v * 128);
+            else
+              cp_async_u<VB>(base + r * kRowBytes + v * 32 * VB, src + v * 128);
+          }
         } else {
           const uint64_t ad = shfl64(A, q + r);
           const uint32_t d4 = uni_d4 ? uni_d4 : (__shfl_sync(0xffffffffu, Bw, q + r) >> 16);
