@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
         if constexpr (FULL) {  // every item names a real gradient row; no predicate
           const float* grow = Gl + (uint64_t)val * 4;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) cp_async_u<16>(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128);
+          for (int v = 0; v < VPL; ++v) cp_async_cg16(g_lane + (slot0 + r) * kGRow + v * 512, grow + v * 128);
         } else {
           const uint32_t d4 = a.uni_dim ? ud4 : __shfl_sync(0xffffffffu, nxt ? wn_.d4 : wc_.d4, q + r);
           const bool valid = (VM >> (q + r)) & 1u;
