@@ -278,7 +278,7 @@ def run_reference(args):
         "impl": "reference", "metric": "embedding fwd+bwd+update samples/s", "value": sps,
         "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 storage / f64 accumulation", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f64", "storage_dtype": "f32", "data": "synthetic",
         "config": {"workload": w.name + ": " + w.describe, "mesh": f"{w.mesh[0]}x{w.mesh[1]}",
                    "simulated": f"one MP group of {w.mesh[0]} virtual ranks (reference group step, all host threads)",
                    "global_batch": n * w.mesh[0],
@@ -469,7 +469,8 @@ def run_ours(args):
         "metric": "embedding fwd+bwd+update samples/s", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": ("bf16 weights" if w.dtype == "bf16" else "f32") + " storage, f64 accumulation",
+        "dtype": "f64",  # arithmetic type of the path (f64 accumulation, as the reference)
+        "storage_dtype": "bf16" if w.dtype == "bf16" else "f32",
         "data": "synthetic (seeded Zipf ids, power-law bag lengths, N(0,1e-3) upstream)",
         "config": {"workload": w.name + ": " + w.describe, "global_batch": world * w.batch,
                    "per_gpu_batch": w.batch, "tables": w.F, "dim": int(np.max(w.dims)),
