@@ -20,6 +20,7 @@ from .api import (  # noqa: F401
     nccl_unique_id,
     owner_of,
     plan_greedy,
+    traces_to_csv,
     validate_plan,
 )
 
@@ -36,6 +37,7 @@ __all__ = [
     "nccl_unique_id",
     "owner_of",
     "plan_greedy",
+    "traces_to_csv",
     "validate_plan",
 ]
 

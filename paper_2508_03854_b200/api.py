@@ -201,6 +201,24 @@ def _ptr_kind(x, dtype, writable=False):
     return a.ctypes.data, L.S2D_HOST, a
 
 
+def traces_to_csv(rows: Iterable[dict], config_hash: str = "") -> str:
+    """Trace CSV in the reference schema (experiment.cpp:47-62):
+    ``# config_hash=…`` comments, header ``step,kernel,rank,bytes,latency_s``,
+    latency printed ``%.9g`` (csv.cpp:11-15).  Rows are measured
+    (Sparse2DEmbedding.trace_rows, gathered over ranks by the caller), not
+    modelled by the alpha-beta bandwidth model."""
+    out = [f"# config_hash={config_hash}",
+           "# bytes = bytes sent by the rank to other ranks (self-delivery stays in HBM)",
+           "# latency_s = measured device time of the kernels carrying the exchange",
+           "step,kernel,rank,bytes,latency_s"]
+    for r in sorted(rows, key=lambda r: (r["step"], _TRACE_ORDER.get(r["kernel"], 9), r["rank"])):
+        out.append(f"{r['step']},{r['kernel']},{r['rank']},{r['bytes']},{r['latency_s']:.9g}")
+    return "\n".join(out) + "\n"
+
+
+_TRACE_ORDER = {"lookup_a2a": 0, "grad_a2a": 1, "table_allreduce": 2}
+
+
 class Sparse2DEmbedding:
     """Per-rank engine of the 2D-sparse-parallel embedding step.
 
@@ -405,6 +423,41 @@ class Sparse2DEmbedding:
         cnt = (C.c_uint32 * 12)()
         L.check(self.lib.s2d_get_phase_times(self._ctx, ms, cnt, 12))
         return {p: (ms[i], cnt[i]) for i, p in enumerate(self.PHASES)}
+
+    # Phases whose device time carries each reference collective.  The
+    # exchanges are fused into their producing kernels (owner lookup stores
+    # pooled rows into the requester's buffer over NVLink; the grad gather
+    # pulls upstream rows from peers), so a collective's latency is the time
+    # of the kernels that move its bytes.
+    TRACE_PHASES = {
+        "lookup_a2a": ("a2a_ids", "lookup", "a2a_lookup", "combine"),
+        "grad_a2a": ("grad_gather", "a2a_grad"),
+        "table_allreduce": ("sync",),
+    }
+
+    def trace_rows(self, step: int) -> list[dict]:
+        """Measured CollectiveTrace rows of this rank since the last
+        phase_times() call (topology.hpp:53-61, one row per participant as
+        traces_to_csv writes them, experiment.cpp:47-62).  Needs
+        set_profiling(True) around the step.  bytes = bytes this rank sent to
+        other ranks (ids + pooled rows for lookup_a2a); self-delivery stays in
+        HBM and is not counted, unlike the simulated trace.  table_allreduce
+        appears only when a replica sync ran."""
+        times = self.phase_times()
+        st = self.stats()
+        sent = {
+            "lookup_a2a": st["ids_bytes_sent"] + st["lookup_bytes_sent"],
+            "grad_a2a": st["grad_bytes_sent"],
+            "table_allreduce": st["sync_bytes"],
+        }
+        rows = []
+        for kernel, phases in self.TRACE_PHASES.items():
+            if kernel == "table_allreduce" and times["sync"][1] == 0:
+                continue
+            ms = sum(times[p][0] for p in phases)
+            rows.append({"step": int(step), "kernel": kernel, "rank": self.rank,
+                         "bytes": int(sent[kernel]), "latency_s": ms * 1e-3})
+        return rows
 
     def debug(self, which: int) -> np.ndarray:
         """Wire buffers of the last step (see s2d_debug_read)."""

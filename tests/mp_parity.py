@@ -74,7 +74,11 @@ def main():
         return lengths, ids, upstream(rng, B, int(dims.sum()))
 
     pooled_mine, layouts = [], None
+    trace = None
     for step in range(args.steps):
+        if step == args.steps - 1:  # measured trace covers the last step only
+            eng.set_profiling(True)
+            eng.phase_times()
         lengths, ids, up = inputs(step, rank)
         if args.engine_out:
             import torch
@@ -96,6 +100,9 @@ def main():
             eng.sync_replicas()
         if step == args.steps - 1:
             layouts = {k: eng.debug(k) for k in (0, 1, 2, 3, 4, 5)}
+            eng.synchronize()
+            trace = eng.trace_rows(step)
+            eng.set_profiling(False)
     shard = {}
     for f in range(F):
         lo, hi = eng.owned_range(f)
@@ -116,7 +123,7 @@ def main():
             if hi > lo:
                 loaded[f] = (lo, hi) + eng.read_rows(f, lo, hi)
     gathered = [None] * world if rank == 0 else None
-    dist.gather_object((pooled_mine, layouts, shard, loaded), gathered, dst=0)
+    dist.gather_object((pooled_mine, layouts, shard, loaded, trace), gathered, dst=0)
     eng.close()
     if rank != 0:
         dist.barrier()
@@ -192,6 +199,14 @@ def main():
                 if not (np.array_equal(w.view(np.uint32), ww.view(np.uint32))
                         and np.array_equal(v.view(np.uint32), vv.view(np.uint32))):
                     fails.append(f"checkpoint reload rank {r} table {f}")
+    # measured trace of the last step (reference trace.csv schema)
+    last_sync = M > 1 and args.steps % args.sync_interval == 0
+    for r in range(world):
+        kinds = [t["kernel"] for t in gathered[r][4]]
+        if kinds != ["lookup_a2a", "grad_a2a"] + (["table_allreduce"] if last_sync else []):
+            fails.append(f"trace kernels rank {r}: {kinds}")
+    if N > 1 and sum(t["bytes"] for r in range(world) for t in gathered[r][4] if t["kernel"] != "table_allreduce") == 0:
+        fails.append("trace: no MP exchange bytes")
     if fails:
         print("MP PARITY FAIL", world, M, args.strategy, *fails[:20], sep="\n  ")
         dist.barrier()

@@ -418,3 +418,28 @@ def test_device_gen_batch_bit_exact(port):
     assert pooled.shape == (B, sum(dims))
     with pytest.raises(ValueError, match="zipf_exponent"):
         eng.gen_batch(1, 0, 0, B, [1.0, -0.5, 1.0, 1.0, 1.0], L)
+
+
+def test_measured_trace_rows():
+    """trace_rows: measured per-collective rows in the reference trace schema
+    (topology.hpp:53-61).  At 1x1 nothing crosses ranks (0 bytes) and no
+    replica sync runs (no table_allreduce row); the lookup time is measured."""
+    import paper_2508_03854_b200 as s2d
+
+    rng = np.random.default_rng(5)
+    rows, dims, B = [5000, 300], [64, 32], 256
+    eng = _engine(rows, dims)
+    eng.init_tables(3)
+    eng.set_profiling(True)
+    eng.phase_times()
+    lengths, ids = make_batch(rng, np.array(rows, np.uint32), B)
+    eng.forward(lengths, ids)
+    eng.backward_update(upstream(rng, B, sum(dims)))
+    eng.synchronize()
+    tr = eng.trace_rows(7)
+    assert [r["kernel"] for r in tr] == ["lookup_a2a", "grad_a2a"]
+    assert all(r["step"] == 7 and r["rank"] == 0 and r["bytes"] == 0 for r in tr)
+    assert tr[0]["latency_s"] > 0
+    csv = s2d.traces_to_csv(tr, "x").splitlines()
+    assert csv[-2].startswith("7,lookup_a2a,0,0,")
+    eng.set_profiling(False)

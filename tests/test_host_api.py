@@ -142,3 +142,29 @@ def test_cxx_wrapper_host_api(tmp_path):
     assert r.returncode == 0, r.stderr[-2000:]
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0 and "WRAPPER OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_traces_to_csv_reference_schema():
+    """Measured trace rows written in the reference's trace.csv schema
+    (experiment.cpp:47-62): comment lines, header, (step, kernel order, rank)
+    row order, %.9g latency."""
+    import paper_2508_03854_b200 as s2d
+
+    rows = [
+        {"step": 1, "kernel": "grad_a2a", "rank": 1, "bytes": 64, "latency_s": 2.5e-5},
+        {"step": 0, "kernel": "table_allreduce", "rank": 0, "bytes": 8, "latency_s": 1.0 / 3.0},
+        {"step": 0, "kernel": "lookup_a2a", "rank": 1, "bytes": 128, "latency_s": 0.0},
+        {"step": 0, "kernel": "lookup_a2a", "rank": 0, "bytes": 256, "latency_s": 1e-4},
+    ]
+    text = s2d.traces_to_csv(rows, "abc123")
+    lines = text.splitlines()
+    assert lines[0] == "# config_hash=abc123"
+    body = [l for l in lines if not l.startswith("#")]
+    assert body[0] == "step,kernel,rank,bytes,latency_s"
+    assert body[1:] == [
+        "0,lookup_a2a,0,256,0.0001",
+        "0,lookup_a2a,1,128,0",
+        "0,table_allreduce,0,8,0.333333333",
+        "1,grad_a2a,1,64,2.5e-05",
+    ]
+    assert text.endswith("\n")
