@@ -44,6 +44,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
     p.add_argument("--seed", type=int, default=1234)
+    p.add_argument("--trace-csv", default=None, help="write one measured step's collective trace (reference schema)")
     p.add_argument("--plan-rotate", type=int, default=0, help="experiment: rotate the plan's local ranks by k")
     p.add_argument("--no-phases", action="store_true", help="experiment: no phase events in the timed region")
     return p.parse_args()
@@ -408,6 +409,22 @@ def run_ours(args):
     if world > 1:
         per_rank = [None] * world
         dist.all_gather_object(per_rank, mine)
+    if args.trace_csv:
+        # one more profiled step -> measured trace rows in the reference's
+        # trace.csv schema (experiment.cpp:47-62), written by rank 0
+        eng.set_profiling(True)
+        eng.phase_times()
+        step(0)
+        eng.synchronize()
+        eng.set_profiling(False)
+        rows = eng.trace_rows(0)
+        allrows = [rows]
+        if world > 1:
+            allrows = [None] * world
+            dist.all_gather_object(allrows, rows)
+        if rank == 0:
+            with open(args.trace_csv, "w") as f:
+                f.write(s2d.traces_to_csv([r for rr in allrows for r in rr], f"{w.name}-{n_mp}x{m}-seed{args.seed}"))
 
     # ---- e2e through the public API with pinned host buffers ----
     K2 = args.e2e_steps or max(3, min(args.steps, 10))
@@ -465,6 +482,10 @@ def run_ours(args):
     achieved = per_phase[dom]["algo_gbs"] if per_phase else 0.0
     kname = {"lookup": "k_lookup_ring", "update": "k_update_ring", "sort": "k_radix_pass"}[dom]
     traffic = traffic_from_profiles(kname)
+    if (w.name, n_mp, m, w.batch) != ("cfg2", 1, 1, 16384):  # captured on cfg2 1x1 only
+        traffic = (None, "no ncu capture for this workload/mesh (profiles/ hold cfg2 1x1)")
+    wbytes = 2 if w.dtype == "bf16" else 4
+    table_gb = sum(int(r) * (int(d) * wbytes + 4) for r, d in zip(w.rows, w.dims)) / 1e9
     line = {
         "metric": "embedding fwd+bwd+update samples/s", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -476,8 +497,8 @@ def run_ours(args):
                    "per_gpu_batch": w.batch, "tables": w.F, "dim": int(np.max(w.dims)),
                    "mesh": f"{n_mp}x{m}", "strategy": w.strategy, "optimizer": f"rowwise-adagrad c={w.c}",
                    "parallelism": f"mp{n_mp}xdp{m}", "nnz_per_gpu": nnz_mean,
-                   "l2": "inputs larger than L2 (tables 17.2 GB, upstream 218 MB/step), "
-                         f"{NB} distinct batches cycled"},
+                   "l2": f"inputs larger than L2 (tables {table_gb:.1f} GB, upstream "
+                         f"{w.batch * w.sum_dims * 4 / 1e6:.0f} MB/step), {NB} distinct batches cycled"},
         "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_src,
                      "traffic": traffic[0], "traffic_source": traffic[1],
