@@ -187,6 +187,14 @@ int s2d_shard_write(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_
                     const float* w, const float* v);
 int s2d_shard_read(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_hi, float* w,
                    float* v);
+/* apply_row_update (src/embedding.cpp:108-129) for n_rows rows of `table`
+ * (global row ids owned by this rank): w[row][j] = f32(f64(w) + delta[i][j])
+ * (bf16 tables: one RNE rounding of the f64 sum), v[row] = f32(new_moment[i]).
+ * delta is n_rows x dim f64, row-major, in call order; a row listed twice is
+ * updated twice in that order.  S2D_ERANGE for a row outside the owned range,
+ * S2D_EINVAL for a new_moment < 0 or nonfinite; nothing is written then. */
+int s2d_apply_row_updates(s2d_ctx* ctx, uint32_t table, uint32_t n_rows, const uint32_t* rows,
+                          const double* delta, const double* new_moment);
 /* Owned range of `table` on this rank ([0,0) when none). */
 int s2d_shard_range(s2d_ctx* ctx, uint32_t table, uint32_t* row_lo, uint32_t* row_hi);
 

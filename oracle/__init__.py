@@ -215,6 +215,27 @@ class Oracle:
             raise ValueError("pool_ids failed")
         return out
 
+    def apply_row_update(self, w: np.ndarray, v: np.ndarray, dim: int, shard, row: int, delta, new_moment):
+        """apply_row_update (embedding.cpp:108-129) in place on a whole table
+        (w rows x dim f32, v rows f32) through shard = (row_lo, row_hi)."""
+        assert w.dtype == np.float32 and v.dtype == np.float32 and w.flags.c_contiguous
+        d = np.ascontiguousarray(delta, np.float64)
+        if d.size != dim:
+            raise ValueError("delta length mismatch")
+        lo, hi = shard
+        if self.kind == "port":
+            rc = self.lib.or_apply_row_update(C.c_void_p(_ptr(w)), C.c_void_p(_ptr(v)), C.c_uint32(lo),
+                                              C.c_uint32(hi), C.c_uint32(dim), C.c_uint32(row),
+                                              C.c_void_p(_ptr(d)), C.c_double(new_moment))
+        else:
+            rc = self.lib.ref_apply_row_update(C.c_void_p(_ptr(w)), C.c_void_p(_ptr(v)), C.c_uint32(v.size),
+                                               C.c_uint32(lo), C.c_uint32(hi), C.c_uint32(dim), C.c_uint32(row),
+                                               C.c_void_p(_ptr(d)), C.c_double(new_moment))
+        if rc == -2:
+            raise IndexError(f"row {row} outside shard range [{lo},{hi})")
+        if rc:
+            raise ValueError("new_moment must be finite and >= 0")
+
     def adagrad_row_step(self, w, v, g, eta=0.1, eps=1e-8, c=1.0):
         w = np.array(w, np.float32)
         vv = np.array([v], np.float32)

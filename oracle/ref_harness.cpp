@@ -106,6 +106,27 @@ int ref_pool_ids(const float* w, uint32_t rows, uint32_t dim, uint32_t n_shards,
   }
 }
 
+int ref_apply_row_update(float* w, float* v, uint32_t rows, uint32_t lo, uint32_t hi, uint32_t dim,
+                         uint32_t row, const double* delta, double new_moment) {
+  EmbeddingTable t;
+  t.rows = rows;
+  t.dim = dim;
+  t.weights.assign(w, w + (size_t)rows * dim);
+  t.moments.assign(v, v + rows);
+  try {
+    apply_row_update(ShardRef{&t, lo, hi}, row, std::span<const double>(delta, dim), new_moment);
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return -2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+  std::copy(t.weights.begin(), t.weights.end(), w);
+  std::copy(t.moments.begin(), t.moments.end(), v);
+  return 0;
+}
+
 double ref_adagrad_row_step(float* w, float* v, const double* g, uint32_t dim, double eta,
                             double eps, double c, int* err) {
   OptimizerConfig cfg{eta, eps, c, OptimizerVariant::RowWiseAdagrad};

@@ -131,6 +131,20 @@ int or_pool_ids(const float* w, uint32_t dim, uint32_t n_shards, const uint32_t*
   return OR_OK;
 }
 
+/* ---- embedding.cpp:108-129 apply_row_update ---------------------------- */
+/* One call on a table of `dim`-float rows starting at `w`, shard [lo,hi).
+ * OR_ERANGE outside the shard, OR_EINVAL for a negative / nonfinite moment
+ * (checked in that order, nothing written on error). */
+int or_apply_row_update(float* w, float* v, uint32_t lo, uint32_t hi, uint32_t dim, uint32_t row,
+                        const double* delta, double new_moment) {
+  if (row < lo || row >= hi) return OR_ERANGE;
+  if (!(new_moment >= 0.0) || !isfinite(new_moment)) return OR_EINVAL;
+  float* r = w + (size_t)row * dim;
+  for (uint32_t j = 0; j < dim; ++j) r[j] = (float)((double)r[j] + delta[j]);
+  v[row] = (float)new_moment;
+  return OR_OK;
+}
+
 /* ---- planner.cpp:38-89 plan_greedy ------------------------------------- */
 /* Writes up to F*N entries (table_id,row_lo,row_hi,local_rank) to out; returns
  * the count.  strategy 0 = table-wise (LPT), 1 = row-wise. */

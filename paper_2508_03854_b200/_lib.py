@@ -79,6 +79,7 @@ SIGNATURES = {
     "s2d_set_optimizer": (C.c_int, [_P, C.POINTER(OptimizerConfigC)]),
     "s2d_init_tables": (C.c_int, [_P, C.c_uint64]),
     "s2d_shard_write": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, _P, _P]),
+    "s2d_apply_row_updates": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P]),
     "s2d_shard_read": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, _P, _P]),
     "s2d_shard_range": (C.c_int, [_P, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "s2d_lookup_forward": (C.c_int, [_P, C.c_uint32, _P, _P, C.c_uint64, _P, C.c_int32]),

@@ -348,6 +348,21 @@ class Sparse2DEmbedding:
                                           va.ctypes.data if va is not None else None))
 
     # -- the step --
+    def apply_row_updates(self, table: int, rows, delta, new_moment):
+        """apply_row_update (embedding.cpp:108-129) on owned rows of `table`:
+        w += delta (f64 add, rounded to storage), v = new_moment.  rows are
+        global row ids; delta is len(rows) x dim; a repeated row is updated in
+        call order.  IndexError outside the owned range, ValueError for a
+        negative or nonfinite moment (nothing written then)."""
+        r = np.ascontiguousarray(rows, np.uint32).ravel()
+        n = r.size
+        D = int(self.dims[table]) if 0 <= table < self.F else 0
+        d = np.ascontiguousarray(delta, np.float64).reshape(-1)
+        m = np.ascontiguousarray(new_moment, np.float64).ravel()
+        if d.size != n * D or m.size != n:
+            raise ValueError("delta length mismatch")
+        L.check(self.lib.s2d_apply_row_updates(self._ctx, table, n, r.ctypes.data, d.ctypes.data, m.ctypes.data))
+
     def forward(self, lengths, ids, pooled=None, batch: int | None = None):
         """Pooled embeddings of this rank's batch.  lengths: [B*F] sample-major
         bag lengths, ids: concatenated global row ids.  numpy / CPU tensors are

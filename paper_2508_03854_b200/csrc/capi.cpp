@@ -168,6 +168,11 @@ int s2d_shard_read(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_h
   return guarded([&] { as_ctx(ctx)->shard_io(table, row_lo, row_hi, w, v, false); });
 }
 
+int s2d_apply_row_updates(s2d_ctx* ctx, uint32_t table, uint32_t n_rows, const uint32_t* rows, const double* delta,
+                          const double* new_moment) {
+  return guarded([&] { as_ctx(ctx)->apply_row_updates(table, n_rows, rows, delta, new_moment); });
+}
+
 int s2d_save_tables(s2d_ctx* ctx, const char* path) {
   return guarded([&] { as_ctx(ctx)->save_tables(path); });
 }

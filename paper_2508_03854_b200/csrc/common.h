@@ -253,6 +253,9 @@ void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 
 // standalone fused row step on caller rows (s2d_adagrad_rows)
+void launch_apply_rows(void* w, bool bf16, float* v, const uint32_t* order, const uint32_t* seg,
+                       const uint32_t* seg_row, const double* delta, const double* moment, uint32_t nseg,
+                       uint32_t dim, cudaStream_t st);
 void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32_t n, uint32_t dim,
                          double eta, double eps, double c, int sgd, uint32_t* err, cudaStream_t st);
 

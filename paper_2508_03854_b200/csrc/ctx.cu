@@ -340,6 +340,57 @@ void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v,
   }
 }
 
+void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, const double* delta,
+                            const double* new_moment) {
+  if (table >= F) throw Error(S2D_EINVAL, "table out of range");
+  if (!n) return;
+  if (!rows || !delta || !new_moment) throw Error(S2D_EINVAL, "null rows / delta / new_moment");
+  const FeatDev& fd = feats[table];
+  // every row validated before any write (the reference throws per call,
+  // embedding.cpp:110-121; a batch is all-or-nothing)
+  for (uint32_t i = 0; i < n; ++i) {
+    if (rows[i] < fd.lo || rows[i] >= fd.hi)
+      throw Error(S2D_ERANGE, "row " + std::to_string(rows[i]) + " outside shard range [" + std::to_string(fd.lo) +
+                                  "," + std::to_string(fd.hi) + ")");
+    if (!(new_moment[i] >= 0.0) || !std::isfinite(new_moment[i]))
+      throw Error(S2D_EINVAL, "new_moment must be finite and >= 0 (got " + std::to_string(new_moment[i]) + ")");
+  }
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return rows[a] < rows[b]; });
+  std::vector<uint32_t> seg, seg_row;
+  for (uint32_t k = 0; k < n; ++k)
+    if (k == 0 || rows[order[k]] != rows[order[k - 1]]) {
+      seg.push_back(k);
+      seg_row.push_back(rows[order[k]] - fd.lo);
+    }
+  const uint32_t nseg = (uint32_t)seg.size();
+  seg.push_back(n);
+  S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  const size_t b_order = (size_t)n * 4, b_seg = seg.size() * 4, b_row = (size_t)nseg * 4;
+  const size_t b_delta = (size_t)n * fd.dim * 8, b_mom = (size_t)n * 8;
+  const size_t o_seg = b_order, o_row = o_seg + b_seg, o_delta = (o_row + b_row + 7) / 8 * 8,
+               o_mom = o_delta + b_delta;
+  char* d = nullptr;
+  S2D_CUDA(cudaMalloc(&d, o_mom + b_mom));
+  struct Free {
+    char* p;
+    ~Free() { cudaFree(p); }
+  } guard{d};
+  S2D_CUDA(cudaMemcpy(d, order.data(), b_order, cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d + o_seg, seg.data(), b_seg, cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d + o_row, seg_row.data(), b_row, cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d + o_delta, delta, b_delta, cudaMemcpyHostToDevice));
+  S2D_CUDA(cudaMemcpy(d + o_mom, new_moment, b_mom, cudaMemcpyHostToDevice));
+  void* wbase = bf16 ? (void*)(weights.as<uint16_t>() + fd.wbase) : (void*)(weights.as<float>() + fd.wbase);
+  launch_apply_rows(wbase, bf16, moments.as<float>() + fd.vbase, reinterpret_cast<uint32_t*>(d),
+                    reinterpret_cast<uint32_t*>(d + o_seg), reinterpret_cast<uint32_t*>(d + o_row),
+                    reinterpret_cast<double*>(d + o_delta), reinterpret_cast<double*>(d + o_mom), nseg, fd.dim,
+                    stream);
+  S2D_CUDA(cudaStreamSynchronize(stream));
+}
+
 void Ctx::check_faults() {
   const uint32_t e = *err_host.as<uint32_t>();
   if (!e) return;

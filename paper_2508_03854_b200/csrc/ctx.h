@@ -154,6 +154,8 @@ struct Ctx {
   void set_optimizer(const s2d_optimizer_config& c);
   void init_tables(uint64_t seed);
   void shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v, bool write);
+  void apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, const double* delta,
+                         const double* new_moment);
   void lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t* ids, uint64_t nnz,
                       float* pooled, int mem);
   void backward_update(const float* upstream, int mem);

@@ -86,4 +86,54 @@ void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32
   S2D_LAUNCH_CHECK();
 }
 
+namespace {
+
+// apply_row_update (src/embedding.cpp:108-129) over a batch of rows: one warp
+// per distinct row walks that row's updates in call order (order[] is the
+// stable row sort of the call), so a row listed twice gets both updates in
+// sequence, each rounded to storage, as two reference calls would.
+template <typename W>
+__global__ void __launch_bounds__(256) k_apply_rows(W* __restrict__ w, float* __restrict__ v,
+                                                    const uint32_t* __restrict__ order,
+                                                    const uint32_t* __restrict__ seg,
+                                                    const uint32_t* __restrict__ seg_row,
+                                                    const double* __restrict__ delta,
+                                                    const double* __restrict__ moment, uint32_t nseg,
+                                                    uint32_t dim) {
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); s < nseg; s += warps) {
+    const uint32_t b = seg[s], e = seg[s + 1];
+    W* row = w + (uint64_t)seg_row[s] * dim;
+    for (uint32_t c = lane; c < dim; c += 32) {
+      W x = row[c];
+      for (uint32_t k = b; k < e; ++k) {
+        const double y = (double)(float)x + delta[(uint64_t)order[k] * dim + c];
+        if constexpr (sizeof(W) == 4)
+          x = (W)(float)y;
+        else
+          x = __double2bfloat16(y);
+      }
+      row[c] = x;
+    }
+    if (lane == 0) v[seg_row[s]] = (float)moment[order[e - 1]];
+  }
+}
+
+}  // namespace
+
+void launch_apply_rows(void* w, bool bf16, float* v, const uint32_t* order, const uint32_t* seg,
+                       const uint32_t* seg_row, const double* delta, const double* moment, uint32_t nseg,
+                       uint32_t dim, cudaStream_t st) {
+  if (!nseg) return;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nseg + 7) / 8, 148ull * 8));
+  if (bf16)
+    k_apply_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(w), v, order, seg, seg_row,
+                                                      delta, moment, nseg, dim);
+  else
+    k_apply_rows<float><<<grid, 256, 0, st>>>(static_cast<float*>(w), v, order, seg, seg_row, delta, moment,
+                                              nseg, dim);
+  S2D_LAUNCH_CHECK();
+}
+
 }  // namespace s2d

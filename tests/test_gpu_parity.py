@@ -443,3 +443,41 @@ def test_measured_trace_rows():
     csv = s2d.traces_to_csv(tr, "x").splitlines()
     assert csv[-2].startswith("7,lookup_a2a,0,0,")
     eng.set_profiling(False)
+
+
+@pytest.mark.parametrize("strategy", ["table-wise", "row-wise"])
+def test_apply_row_updates_vs_oracle(port, strategy):
+    """s2d_apply_row_updates == apply_row_update (embedding.cpp:108-129)
+    called once per listed row in order (oracle), bit-exact, repeated rows
+    included; untouched rows bitwise unchanged; errors before any write."""
+    rows, dims = [3000, 77], [64, 128]
+    eng = _engine(rows, dims, strategy=strategy)
+    eng.init_tables(8)
+    rng = np.random.default_rng(21)
+    for f in range(2):
+        lo, hi = eng.owned_range(f)
+        w, v = eng.read_rows(f, lo, hi)
+        w = np.ascontiguousarray(w, np.float32).reshape(hi - lo, dims[f])
+        v = np.ascontiguousarray(v, np.float32)
+        n = 500
+        rr = rng.integers(lo, hi, size=n).astype(np.uint32)
+        rr[1] = rr[0]  # a repeated row: two updates in call order
+        delta = rng.standard_normal((n, dims[f])) * 1e-2
+        mom = np.abs(rng.standard_normal(n)) * 3
+        eng.apply_row_updates(f, rr, delta, mom)
+        want_w = np.zeros((hi, dims[f]), np.float32)
+        want_w[lo:hi] = w
+        want_v = np.zeros(hi, np.float32)
+        want_v[lo:] = v
+        for i in range(n):
+            port.apply_row_update(want_w, want_v, dims[f], (lo, hi), int(rr[i]), delta[i], float(mom[i]))
+        gw, gv = eng.read_rows(f, lo, hi)
+        assert np.array_equal(bits(np.asarray(gw).ravel()), bits(want_w[lo:hi].ravel()))
+        assert np.array_equal(bits(np.asarray(gv)), bits(want_v[lo:hi]))
+        with pytest.raises(IndexError):
+            eng.apply_row_updates(f, [lo, hi], np.zeros((2, dims[f])), [0.0, 0.0])
+        with pytest.raises(ValueError):
+            eng.apply_row_updates(f, [lo], np.ones((1, dims[f])), [-1.0])
+        gw2, gv2 = eng.read_rows(f, lo, hi)
+        assert np.array_equal(bits(np.asarray(gw2).ravel()), bits(np.asarray(gw).ravel()))
+        assert np.array_equal(bits(np.asarray(gv2)), bits(np.asarray(gv)))

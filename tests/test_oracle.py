@@ -223,3 +223,48 @@ def test_gen_batch_ids_port_vs_reference(port, ref):
         a = port.gen_batch_ids(seed, step, rank, len(rows), rows, zipf, L, 48)
         b = ref.gen_batch_ids(seed, step, rank, len(rows), rows, zipf, L, 48)
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ["port", "reference"])
+def test_apply_row_update_known_answers(kind):
+    """proj/tests/test_embedding.cpp:123-165 on init_table(0, 10, 4, 3)."""
+    from oracle import Oracle, reference_available
+
+    if kind == "reference" and not reference_available():
+        pytest.skip("oracle/_ref not built")
+    o = Oracle(kind)
+    w0 = o.init_rows(0, 10, 0, 10, 4, 3).reshape(10, 4).copy()
+    v0 = np.zeros(10, np.float32)
+    w, v = w0.copy(), v0.copy()
+    o.apply_row_update(w, v, 4, (0, 10), 3, [0.0] * 4, float(v[3]))
+    assert np.array_equal(w, w0) and np.array_equal(v, v0)
+    o.apply_row_update(w, v, 4, (0, 10), 3, [0.5, -0.5, 0.25, 0.0], 2.0)
+    keep = np.arange(10) != 3
+    assert np.array_equal(w[keep], w0[keep]) and np.array_equal(v[keep], v0[keep])
+    assert v[3] == 2.0 and w[3, 0] == np.float32(np.float64(w0[3, 0]) + 0.5)
+    o.apply_row_update(w, v, 4, (0, 10), 1, [0.0] * 4, 5.0)
+    o.apply_row_update(w, v, 4, (0, 10), 1, [0.0] * 4, 1.0)
+    assert v[1] == 1.0
+    with pytest.raises(ValueError):
+        o.apply_row_update(w, v, 4, (0, 10), 1, [0.0] * 4, -0.5)
+    with pytest.raises(IndexError):
+        o.apply_row_update(w, v, 4, (0, 10), 42, [0.0] * 4, 0.0)
+
+
+def test_apply_row_update_port_matches_reference():
+    from oracle import Oracle, reference_available
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    outs = []
+    for kind in ("port", "reference"):
+        o = Oracle(kind)
+        w = o.init_rows(2, 50, 0, 50, 8, 11).reshape(50, 8).copy()
+        v = np.abs(np.random.default_rng(9).standard_normal(50)).astype(np.float32)
+        r2 = np.random.default_rng(4)
+        for _ in range(40):
+            o.apply_row_update(w, v, 8, (10, 40), int(r2.integers(10, 40)), r2.standard_normal(8) * 1e-3,
+                               float(abs(r2.standard_normal())))
+        outs.append((w, v))
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
