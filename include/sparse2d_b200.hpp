@@ -132,6 +132,12 @@ class Engine {
   void shard_write(uint32_t table, uint32_t lo, uint32_t hi, const float* w, const float* v) {
     check(s2d_shard_write(ctx_, table, lo, hi, w, v));
   }
+  // apply_row_update (src/embedding.cpp:108-129) for n rows in call order;
+  // delta is n x dim doubles.  Throws std::out_of_range / std::invalid_argument.
+  void apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, const double* delta,
+                         const double* new_moment) {
+    check(s2d_apply_row_updates(ctx_, table, n, rows, delta, new_moment));
+  }
   s2d_step_stats stats() {
     s2d_step_stats s{};
     check(s2d_get_step_stats(ctx_, &s));
