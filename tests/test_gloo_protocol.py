@@ -152,3 +152,47 @@ def test_two_rank_wire_protocol(strategy):
     for p in procs:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def _trace_worker(rank, world, port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    import paper_2508_03854_b200 as s2d
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # per-rank measured rows as Sparse2DEmbedding.trace_rows returns them
+        mine = [{"step": 3, "kernel": k, "rank": rank, "bytes": 100 * (rank + 1) + i, "latency_s": 1e-4 * (rank + 1)}
+                for i, k in enumerate(("lookup_a2a", "grad_a2a", "table_allreduce"))]
+        allrows = [None] * world
+        dist.all_gather_object(allrows, mine)  # the gather bench.py --trace-csv does
+        if rank == 0:
+            out_q.put(s2d.traces_to_csv([r for rr in allrows for r in rr], "h"))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_trace_rows_gathered_over_ranks_gloo():
+    """world_size 2 (gloo): rank 0 writes every rank's measured trace rows in
+    the reference's per-collective, per-participant order
+    (experiment.cpp:53-60)."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_trace_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    text = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    body = [l for l in text.splitlines() if not l.startswith("#")]
+    assert body == ["step,kernel,rank,bytes,latency_s",
+                    "3,lookup_a2a,0,100,0.0001", "3,lookup_a2a,1,200,0.0002",
+                    "3,grad_a2a,0,101,0.0001", "3,grad_a2a,1,201,0.0002",
+                    "3,table_allreduce,0,102,0.0001", "3,table_allreduce,1,202,0.0002"]
