@@ -148,6 +148,22 @@ int s2d_ctx_create(int device, uint32_t total_ranks, uint32_t groups, uint32_t r
                    const uint8_t* nccl_id, s2d_ctx** out);
 int s2d_ctx_destroy(s2d_ctx* ctx);
 
+/* Single-process mesh ("virtual ranks", as the reference Trainer runs its
+ * T ranks inside one process: src/trainer.cpp:80-97, 164-257).  A hub is the
+ * in-process rendezvous of total_ranks contexts; each context is driven by
+ * its own host thread (calls of different ranks block on each other exactly
+ * like NCCL ranks do).  Ranks may share one GPU or sit on different GPUs of
+ * the process; peer buffers are plain device pointers, and every kernel of
+ * the step -- K1 bucketing, the fused exchanges, the device barriers, the
+ * K5 replica sync -- is the code the NCCL mesh runs.  The hub must outlive
+ * its contexts (s2d_hub_destroy drops the caller's reference; contexts keep
+ * their own). */
+typedef struct s2d_hub s2d_hub;
+int s2d_hub_create(uint32_t total_ranks, s2d_hub** out);
+int s2d_hub_destroy(s2d_hub* hub);
+int s2d_ctx_create_local(int device, uint32_t total_ranks, uint32_t groups, uint32_t rank, s2d_hub* hub,
+                         s2d_ctx** out);
+
 /* Runs all work of this context on `cuda_stream` (a cudaStream_t); NULL
  * selects the context's own stream. */
 int s2d_ctx_set_stream(s2d_ctx* ctx, void* cuda_stream);

@@ -8,6 +8,7 @@ sync) runs as hand-written sm_100a CUDA kernels + NCCL in
 ``libsparse2d_b200.so`` behind a C ABI (``include/sparse2d_b200.h``).
 """
 from .api import (  # noqa: F401
+    LocalHub,
     OptimizerConfig,
     Sparse2DEmbedding,
     TableConfig,
@@ -17,14 +18,17 @@ from .api import (  # noqa: F401
     effective_lr,
     imbalance_ratio,
     launch_count,
+    local_mesh,
     nccl_unique_id,
     owner_of,
     plan_greedy,
+    run_ranks,
     traces_to_csv,
     validate_plan,
 )
 
 __all__ = [
+    "LocalHub",
     "OptimizerConfig",
     "Sparse2DEmbedding",
     "TableConfig",
@@ -34,9 +38,11 @@ __all__ = [
     "effective_lr",
     "imbalance_ratio",
     "launch_count",
+    "local_mesh",
     "nccl_unique_id",
     "owner_of",
     "plan_greedy",
+    "run_ranks",
     "traces_to_csv",
     "validate_plan",
 ]

@@ -68,6 +68,9 @@ SIGNATURES = {
     "s2d_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "s2d_ctx_create": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, C.c_char_p, C.POINTER(_P)]),
     "s2d_ctx_destroy": (C.c_int, [_P]),
+    "s2d_hub_create": (C.c_int, [C.c_uint32, C.POINTER(_P)]),
+    "s2d_hub_destroy": (C.c_int, [_P]),
+    "s2d_ctx_create_local": (C.c_int, [C.c_int, C.c_uint32, C.c_uint32, C.c_uint32, _P, C.POINTER(_P)]),
     "s2d_ctx_set_stream": (C.c_int, [_P, _P]),
     "s2d_ctx_set_strict": (C.c_int, [_P, C.c_int]),
     "s2d_ctx_set_async_host": (C.c_int, [_P, C.c_int]),

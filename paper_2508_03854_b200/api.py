@@ -219,6 +219,70 @@ def traces_to_csv(rows: Iterable[dict], config_hash: str = "") -> str:
 _TRACE_ORDER = {"lookup_a2a": 0, "grad_a2a": 1, "table_allreduce": 2}
 
 
+class LocalHub:
+    """In-process rendezvous of a single-process mesh (s2d_hub_create): the
+    T virtual ranks of one process, each driven by its own thread, as the
+    reference Trainer runs its ranks (trainer.cpp:80-97).  Pass it as
+    ``hub=`` to every rank's Sparse2DEmbedding; ranks may share one GPU."""
+
+    def __init__(self, total_ranks: int):
+        self.lib = _lib()
+        self.total_ranks = int(total_ranks)
+        self._h = C.c_void_p()
+        L.check(self.lib.s2d_hub_create(self.total_ranks, C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            self.lib.s2d_hub_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_ranks(fn, n: int, timeout: float | None = 600.0) -> list:
+    """Run fn(rank) for rank in [0, n) on n threads (one host thread per
+    virtual rank; the C calls release the GIL) and return the results in rank
+    order.  The first exception raised by any rank is re-raised."""
+    import threading
+
+    out, errs = [None] * n, [None] * n
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001  (re-raised below)
+            errs[r] = e
+
+    th = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout)
+        if t.is_alive():
+            raise TimeoutError("a virtual rank did not finish")
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
+def local_mesh(tables, topology: Topology, devices=None, **kw) -> list:
+    """All T ranks of a mesh in this process (virtual ranks on one LocalHub).
+    devices: per-rank CUDA device (default: all on device 0).  Creation is
+    collective, so the engines are built on T threads.  Returns the engines in
+    rank order; each keeps the hub alive."""
+    T = topology.total_ranks
+    hub = LocalHub(T)
+    devs = list(devices) if devices is not None else [0] * T
+    engines = run_ranks(lambda r: Sparse2DEmbedding(tables, topology, rank=r, device=devs[r], hub=hub, **kw), T)
+    hub.close()  # the contexts hold their own references
+    return engines
+
+
 class Sparse2DEmbedding:
     """Per-rank engine of the 2D-sparse-parallel embedding step.
 
@@ -226,13 +290,15 @@ class Sparse2DEmbedding:
     group).  Every rank registers the same tables and plan (the plan is
     identical in every group) and owns the shards its local rank
     is assigned.  ``nccl_id`` (128 bytes from rank 0, e.g. broadcast over
-    torch.distributed) is required when T > 1.
+    torch.distributed) is required when T > 1 across processes; ``hub`` (a
+    LocalHub) instead makes this rank a virtual rank of a single-process mesh
+    (see local_mesh / run_ranks).
     """
 
     def __init__(self, tables: Sequence[TableConfig], topology: Topology, rank: int = 0, device: int = 0,
                  strategy: str = "table-wise", plan: Sequence[dict] | None = None,
                  optimizer: OptimizerConfig | None = None, weight_dtype: str = "fp32",
-                 nccl_id: bytes | None = None, strict: bool = True):
+                 nccl_id: bytes | None = None, strict: bool = True, hub: LocalHub | None = None):
         self.lib = _lib()
         self.topology = topology
         self.rank = rank
@@ -248,8 +314,12 @@ class Sparse2DEmbedding:
             plan = plan_greedy(prof, N, strategy)
         self.plan = [dict(e) for e in plan]
         self._ctx = C.c_void_p()
-        L.check(self.lib.s2d_ctx_create(device, topology.total_ranks, topology.groups, rank,
-                                        nccl_id if nccl_id is not None else None, C.byref(self._ctx)))
+        if hub is not None:
+            L.check(self.lib.s2d_ctx_create_local(device, topology.total_ranks, topology.groups, rank, hub._h,
+                                                  C.byref(self._ctx)))
+        else:
+            L.check(self.lib.s2d_ctx_create(device, topology.total_ranks, topology.groups, rank,
+                                            nccl_id if nccl_id is not None else None, C.byref(self._ctx)))
         self.set_strict(strict)
         td = (L.TableDesc * self.F)(*[L.TableDesc(i, t.rows, t.dim) for i, t in enumerate(self.tables)])
         parr, n = _plan_array(self.plan)

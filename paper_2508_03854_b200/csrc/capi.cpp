@@ -125,6 +125,32 @@ int s2d_ctx_create(int device, uint32_t total_ranks, uint32_t groups, uint32_t r
   });
 }
 
+struct s2d_hub {
+  std::shared_ptr<s2d::LocalHub> hub;
+};
+
+int s2d_hub_create(uint32_t total_ranks, s2d_hub** out) {
+  return guarded([&] {
+    if (!out) throw Error(S2D_EINVAL, "null output");
+    if (total_ranks == 0) throw Error(S2D_EINVAL, "total_ranks must be >= 1");
+    *out = new s2d_hub{std::make_shared<s2d::LocalHub>(total_ranks)};
+  });
+}
+
+int s2d_hub_destroy(s2d_hub* hub) {
+  return guarded([&] { delete hub; });
+}
+
+int s2d_ctx_create_local(int device, uint32_t total_ranks, uint32_t groups, uint32_t rank, s2d_hub* hub,
+                         s2d_ctx** out) {
+  return guarded([&] {
+    if (!out || !hub) throw Error(S2D_EINVAL, "null hub / output");
+    auto c = std::make_unique<s2d::Ctx>();
+    c->create(device, total_ranks, groups, rank, nullptr, hub->hub);
+    *out = reinterpret_cast<s2d_ctx*>(c.release());
+  });
+}
+
 int s2d_ctx_destroy(s2d_ctx* ctx) {
   return guarded([&] { delete reinterpret_cast<s2d::Ctx*>(ctx); });
 }
@@ -277,7 +303,7 @@ int s2d_adagrad_rows(const s2d_optimizer_config* cfg, uint32_t n_rows, uint32_t 
     struct Free {
       void* p[5];
       ~Free() {
-        for (void* q : p) cudaFree(q);
+        for (void* q : p) s2d::dev_free(q);
       }
     } fr{{dw, dv, dg, dlr, derr}};
     S2D_CUDA(cudaMemcpy(dw, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice));

@@ -87,7 +87,7 @@ int Ctx::world_barrier(int failed) {
   int* h = err_host.as<int>() + 1;  // pinned scratch next to the fault word
   *h = failed ? 1 : 0;
   S2D_CUDA(cudaMemcpyAsync(bar_buf.p, h, 4, cudaMemcpyHostToDevice, stream));
-  S2D_NCCL(ncclAllReduce(bar_buf.p, bar_buf.p, 1, ncclInt32, ncclSum, world, stream));
+  world.allreduce_i32(bar_buf.as<int32_t>(), ncclSum, stream);
   S2D_CUDA(cudaMemcpyAsync(h, bar_buf.p, 4, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   return *h;

@@ -27,31 +27,6 @@
 
 namespace s2d {
 
-void DevBuf::ensure(size_t bytes) {
-  if (bytes <= cap && p) return;
-  release();
-  size_t want = std::max<size_t>(bytes + bytes / 8, 256);
-  S2D_CUDA(cudaMalloc(&p, want));
-  cap = want;
-}
-
-void DevBuf::release() {
-  if (p) cudaFree(p);
-  p = nullptr;
-  cap = 0;
-}
-
-void HostBuf::ensure(size_t bytes) {
-  if (bytes <= cap && p) return;
-  if (p) cudaFreeHost(p);
-  S2D_CUDA(cudaMallocHost(&p, std::max<size_t>(bytes, 256)));
-  cap = std::max<size_t>(bytes, 256);
-}
-
-HostBuf::~HostBuf() {
-  if (p) cudaFreeHost(p);
-}
-
 void Ctx::phase_begin(int ph) {
   if (!profile) return;
   if (open_phase >= 0) phase_end();
@@ -119,13 +94,20 @@ Ctx::~Ctx() {
     }
   for (cudaEvent_t e : {ev_fwd, ev_d2h, ev_up, ev_upd, ev_keys, ev_sorted})
     if (e) cudaEventDestroy(e);
-  if (dp) ncclCommDestroy(dp);
-  if (mp) ncclCommDestroy(mp);
-  if (world) ncclCommDestroy(world);
+  dp.destroy();
+  mp.destroy();
+  world.destroy();
   if (own_stream) cudaStreamDestroy(own_stream);
+  if (hub) {
+    hub->release_rank(rank);
+    hub.reset();
+    // buffers released by the member destructors after this body go to the
+    // deferred-free list while other virtual ranks live (local_guard)
+  }
 }
 
-void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uint8_t* nccl_id) {
+void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uint8_t* nccl_id,
+                 std::shared_ptr<LocalHub> local_hub) {
   if (total == 0 || groups == 0 || total % groups)
     throw Error(S2D_EINVAL, "groups must divide total_ranks (both >= 1)");
   if (r >= total) throw Error(S2D_EINVAL, "rank out of range");
@@ -151,15 +133,33 @@ void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uin
   err_host.ensure(16);
   *err_host.as<uint32_t>() = 0;
   h_counts.ensure(4096);
-  if (T > 1) {
+  if (local_hub) {
+    // virtual ranks of one process: collectives rendezvous on the hub,
+    // peer buffers are plain device pointers
+    if (local_hub->T != T) throw Error(S2D_EINVAL, "hub size differs from total_ranks");
+    local_hub->claim_rank(rank);
+    hub = local_hub;
+    local_ctx_enter();
+    local_guard.armed = true;
+    world.hub = mp.hub = dp.hub = hub;
+    world.key = 1ull << 40;
+    mp.key = (2ull << 40) | group;
+    dp.key = (3ull << 40) | local;
+  } else if (T > 1) {
     if (!nccl_id) throw Error(S2D_EINVAL, "nccl_id required when total_ranks > 1");
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof(id));
-    S2D_NCCL(ncclCommInitRank(&world, (int)T, id, (int)rank));
+    S2D_NCCL(ncclCommInitRank(&world.nccl, (int)T, id, (int)rank));
     // MP group: contiguous ranks {g*N .. g*N+N-1}; DP group: {l, l+N, ...}
-    S2D_NCCL(ncclCommSplit(world, (int)group, (int)local, &mp, nullptr));
-    S2D_NCCL(ncclCommSplit(world, (int)local, (int)group, &dp, nullptr));
+    S2D_NCCL(ncclCommSplit(world.nccl, (int)group, (int)local, &mp.nccl, nullptr));
+    S2D_NCCL(ncclCommSplit(world.nccl, (int)local, (int)group, &dp.nccl, nullptr));
   }
+  world.n = T;
+  world.me = rank;
+  mp.n = N;
+  mp.me = local;
+  dp.n = M;
+  dp.me = group;
 }
 
 void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_entry* p, uint32_t np,
@@ -372,12 +372,8 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
   const size_t b_delta = (size_t)n * fd.dim * 8, b_mom = (size_t)n * 8;
   const size_t o_seg = b_order, o_row = o_seg + b_seg, o_delta = (o_row + b_row + 7) / 8 * 8,
                o_mom = o_delta + b_delta;
-  char* d = nullptr;
-  S2D_CUDA(cudaMalloc(&d, o_mom + b_mom));
-  struct Free {
-    char* p;
-    ~Free() { cudaFree(p); }
-  } guard{d};
+  row_upd_scratch.ensure(o_mom + b_mom);
+  char* d = row_upd_scratch.as<char>();
   S2D_CUDA(cudaMemcpy(d, order.data(), b_order, cudaMemcpyHostToDevice));
   S2D_CUDA(cudaMemcpy(d + o_seg, seg.data(), b_seg, cudaMemcpyHostToDevice));
   S2D_CUDA(cudaMemcpy(d + o_row, seg_row.data(), b_row, cudaMemcpyHostToDevice));
@@ -626,45 +622,25 @@ PeerPtrs Ctx::ptrs(const PeerBuf& pb) const {
 
 // Collective over the MP group: every rank calls it with the same `bytes`
 // (derived from data all ranks share), so growth decisions agree.
-void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) { peer_alloc_in(pb, bytes, mp, N, local); }
+void Ctx::peer_alloc(PeerBuf& pb, size_t bytes) { peer_alloc_in(pb, bytes, mp); }
 
-// Collective over `comm` (n ranks, this one = me): (re)allocate pb and map
-// every member's copy through CUDA IPC.
-void Ctx::peer_alloc_in(PeerBuf& pb, size_t bytes, ncclComm_t comm, uint32_t n, uint32_t me) {
+// Collective over `comm`: (re)allocate pb and map every member's copy
+// (CUDA IPC across processes, plain pointers between virtual ranks).
+void Ctx::peer_alloc_in(PeerBuf& pb, size_t bytes, Comm& comm) {
   if (pb.buf.p && bytes <= pb.cap) return;
   const size_t want = std::max<size_t>(bytes + bytes / 4, 4096);
   S2D_CUDA(cudaStreamSynchronize(stream));
   for (void* q : pb.opened) cudaIpcCloseMemHandle(q);
   pb.opened.clear();
-  hbuf.ensure((size_t)n * 64 + 64);
   // everyone has unmapped the old buffers before anyone frees them
-  S2D_NCCL(ncclAllReduce(hbuf.p, hbuf.p, 1, ncclUint8, ncclMax, comm, stream));
-  S2D_CUDA(cudaStreamSynchronize(stream));
+  comm.barrier(stream, hbuf);
   pb.buf.release();
   S2D_CUDA(cudaMalloc(&pb.buf.p, want));
   pb.buf.cap = want;
   pb.cap = want;
-  S2D_CUDA(cudaMemset(pb.buf.p, 0, want));
-  cudaIpcMemHandle_t h;
-  S2D_CUDA(cudaIpcGetMemHandle(&h, pb.buf.p));
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
-  uint8_t* dh = hbuf.as<uint8_t>();
-  S2D_CUDA(cudaMemcpy(dh + (size_t)n * 64, &h, 64, cudaMemcpyHostToDevice));
-  S2D_NCCL(ncclAllGather(dh + (size_t)n * 64, dh, 64, ncclUint8, comm, stream));
-  std::vector<cudaIpcMemHandle_t> all(n);
-  S2D_CUDA(cudaMemcpyAsync(all.data(), dh, (size_t)n * 64, cudaMemcpyDeviceToHost, stream));
+  S2D_CUDA(cudaMemsetAsync(pb.buf.p, 0, want, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
-  pb.ptr.assign(n, nullptr);
-  for (uint32_t q = 0; q < n; ++q) {
-    if (q == me) {
-      pb.ptr[q] = pb.buf.p;
-      continue;
-    }
-    void* mapped = nullptr;
-    S2D_CUDA(cudaIpcOpenMemHandle(&mapped, all[q], cudaIpcMemLazyEnablePeerAccess));
-    pb.ptr[q] = mapped;
-    pb.opened.push_back(mapped);
-  }
+  pb.ptr = map_peer_buffers(comm, pb.buf.p, device, stream, hbuf, pb.opened);
 }
 
 float* Ctx::pooled_buffer() {
@@ -681,58 +657,67 @@ void Ctx::dp_setup() {
   const char* e = std::getenv("S2D_SYNC_NCCL");
   if (e && e[0] == '1') return;
   S2D_CUDA(cudaStreamSynchronize(stream));
-  hbuf.ensure((size_t)M * 128 + 128);
-  uint8_t* dh = hbuf.as<uint8_t>();
-  cudaIpcMemHandle_t h[2];
-  S2D_CUDA(cudaIpcGetMemHandle(&h[0], weights.p));
-  S2D_CUDA(cudaIpcGetMemHandle(&h[1], moments.p));
-  S2D_CUDA(cudaMemcpy(dh + (size_t)M * 128, h, 128, cudaMemcpyHostToDevice));
-  S2D_NCCL(ncclAllGather(dh + (size_t)M * 128, dh, 128, ncclUint8, dp, stream));
-  std::vector<cudaIpcMemHandle_t> all((size_t)M * 2);
-  S2D_CUDA(cudaMemcpyAsync(all.data(), dh, (size_t)M * 128, cudaMemcpyDeviceToHost, stream));
-  S2D_CUDA(cudaStreamSynchronize(stream));
   dp_w.assign(M, nullptr);
   dp_v.assign(M, nullptr);
   int ok = 1;
-  for (uint32_t g = 0; g < M && ok; ++g) {
-    if (g == group) {
-      dp_w[g] = weights.p;
-      dp_v[g] = moments.p;
-      continue;
-    }
-    for (int k = 0; k < 2 && ok; ++k) {
-      void* m = nullptr;
-      if (cudaIpcOpenMemHandle(&m, all[(size_t)g * 2 + k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-        (void)cudaGetLastError();
-        ok = 0;
-        break;
+  if (dp.local()) {
+    dp_w = map_peer_buffers(dp, weights.p, device, stream, hbuf, dp_opened);
+    dp_v = map_peer_buffers(dp, moments.p, device, stream, hbuf, dp_opened);
+  } else {
+    cudaIpcMemHandle_t h[2];
+    S2D_CUDA(cudaIpcGetMemHandle(&h[0], weights.p));
+    S2D_CUDA(cudaIpcGetMemHandle(&h[1], moments.p));
+    std::vector<cudaIpcMemHandle_t> all((size_t)M * 2);
+    dp.host_allgather(h, sizeof(h), all.data(), stream, hbuf);
+    for (uint32_t g = 0; g < M && ok; ++g) {
+      if (g == group) {
+        dp_w[g] = weights.p;
+        dp_v[g] = moments.p;
+        continue;
       }
-      dp_opened.push_back(m);
-      (k == 0 ? dp_w : dp_v)[g] = m;
+      for (int k = 0; k < 2 && ok; ++k) {
+        void* m = nullptr;
+        if (cudaIpcOpenMemHandle(&m, all[(size_t)g * 2 + k], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          (void)cudaGetLastError();
+          ok = 0;
+          break;
+        }
+        dp_opened.push_back(m);
+        (k == 0 ? dp_w : dp_v)[g] = m;
+      }
     }
   }
   // agree across the group (min over members)
-  int* hi = err_host.as<int>() + 2;
-  *hi = ok;
-  S2D_CUDA(cudaMemcpyAsync(dh, hi, 4, cudaMemcpyHostToDevice, stream));
-  S2D_NCCL(ncclAllReduce(dh, dh, 1, ncclInt32, ncclMin, dp, stream));
-  S2D_CUDA(cudaMemcpyAsync(hi, dh, 4, cudaMemcpyDeviceToHost, stream));
-  S2D_CUDA(cudaStreamSynchronize(stream));
-  if (!*hi) {
+  std::vector<int32_t> oks(M);
+  dp.host_allgather(&ok, 4, oks.data(), stream, hbuf);
+  if (*std::min_element(oks.begin(), oks.end()) == 0) {
     for (void* q : dp_opened) cudaIpcCloseMemHandle(q);
     dp_opened.clear();
     return;
   }
-  peer_alloc_in(dp_flags, (size_t)M * 8, dp, M, group);
+  peer_alloc_in(dp_flags, (size_t)M * 8, dp);
   dp_p2p = 1;
 }
 
+// Virtual ranks of one process synchronise on the host (drain the stream,
+// rendezvous on the hub): a kernel spinning on a peer that shares the GPU
+// could wait behind that peer's host thread, which an implicitly
+// device-synchronising runtime call (first-touch cudaMalloc / cudaMallocHost)
+// can stall.  Across processes the barrier stays on the device.
 void Ctx::dp_barrier() {
+  if (dp.local()) {
+    dp.barrier(stream, hbuf);
+    return;
+  }
   ++dp_epoch;
   launch_peer_barrier(ptrs(dp_flags), dp_flags.buf.as<uint64_t>(), group, M, dp_epoch, err.as<uint32_t>(), stream);
 }
 
 void Ctx::peer_barrier() {
+  if (mp.local()) {
+    mp.barrier(stream, hbuf);
+    return;
+  }
   ++epoch;
   launch_peer_barrier(ptrs(p_flags), p_flags.buf.as<uint64_t>(), local, N, epoch, err.as<uint32_t>(), stream);
 }
@@ -960,7 +945,7 @@ void Ctx::replica_sync() {
   uint32_t* d_count = sync_count.as<uint32_t>();
   uint32_t* d_counts = d_count + 16;  // [M] list lengths of the group
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
-  S2D_NCCL(ncclAllGather(d_count, d_counts, 1, ncclUint32, dp, stream));
+  dp.allgather(d_count, d_counts, 4, stream);
   S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_counts, (size_t)M * 4, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   const uint32_t* hc = h_counts.as<uint32_t>();
@@ -978,7 +963,7 @@ void Ctx::replica_sync() {
   if (cmax > mine)  // pad to the longest list (0xffffffff is not a slot)
     S2D_CUDA(cudaMemsetAsync(sync_list.as<uint32_t>() + mine, 0xff, (size_t)(cmax - mine) * 4, stream));
   sync_lists.ensure((uint64_t)cmax * M * 4);
-  S2D_NCCL(ncclAllGather(sync_list.p, sync_lists.p, cmax, ncclUint32, dp, stream));
+  dp.allgather(sync_list.p, sync_lists.p, (size_t)cmax * 4, stream);
   launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
   S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_count, 4, cudaMemcpyDeviceToHost, stream));
@@ -996,7 +981,7 @@ void Ctx::replica_sync() {
     // Staging per replica: [M][slice_cap] copies of its slice | [count] means.
     const uint64_t slice_cap = (uint64_t)count / M + 1;
     const uint64_t copies = slice_cap * M * row_floats;
-    peer_alloc_in(dp_stage, (copies + (uint64_t)count * row_floats) * 4, dp, M, group);  // same size everywhere
+    peer_alloc_in(dp_stage, (copies + (uint64_t)count * row_floats) * 4, dp);  // same size everywhere
     const uint32_t lo = (uint32_t)((uint64_t)count * group / M), hi = (uint32_t)((uint64_t)count * (group + 1) / M);
     PeerPtrs means{};
     for (uint32_t g = 0; g < M; ++g) means.p[g] = reinterpret_cast<float*>(dp_stage.ptr[g]) + copies;
@@ -1021,7 +1006,7 @@ void Ctx::replica_sync() {
   launch_pack_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
                    (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), d_count, weights.p, bf16,
                    moments.as<float>(), row_floats, sync_packed.as<float>(), count, stream);
-  S2D_NCCL(ncclAllGather(sync_packed.p, sync_gathered.p, (size_t)count * row_floats, ncclFloat32, dp, stream));
+  dp.allgather(sync_packed.p, sync_gathered.p, (size_t)count * row_floats * 4, stream);
   launch_mean_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
                    (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), d_count, sync_gathered.as<float>(), M,
                    row_floats, count, weights.p, bf16, moments.as<float>(), opt.variant == S2D_SGD,

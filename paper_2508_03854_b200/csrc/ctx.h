@@ -8,6 +8,7 @@
 
 #include <vector>
 
+#include "comm.h"
 #include "common.h"
 
 #define S2D_NCCL(call)                                                                    \
@@ -18,29 +19,6 @@
   } while (0)
 
 namespace s2d {
-
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-  void ensure(size_t bytes);
-  void release();
-  template <typename T>
-  T* as() const {
-    return reinterpret_cast<T*>(p);
-  }
-  ~DevBuf() { release(); }
-};
-
-struct HostBuf {  // pinned
-  void* p = nullptr;
-  size_t cap = 0;
-  void ensure(size_t bytes);
-  ~HostBuf();
-  template <typename T>
-  T* as() const {
-    return reinterpret_cast<T*>(p);
-  }
-};
 
 // Phases timed with CUDA events when profiling is on (s2d_get_phase_times).
 enum Phase : int {
@@ -84,7 +62,16 @@ struct Ctx {
   cudaEvent_t ev_keys = nullptr, ev_sorted = nullptr;
   bool sort_pending = false;
   void launch_sort(cudaStream_t st);
-  ncclComm_t world = nullptr, mp = nullptr, dp = nullptr;
+  Comm world, mp, dp;
+  std::shared_ptr<LocalHub> hub;  // virtual ranks of one process (null: NCCL)
+  // runs after every member destructor: the last virtual rank frees the
+  // deferred buffers (comm.h)
+  struct LocalGuard {
+    bool armed = false;
+    ~LocalGuard() {
+      if (armed) local_ctx_leave();
+    }
+  } local_guard;
   bool strict = true;
 
   // tables + plan
@@ -122,7 +109,7 @@ struct Ctx {
   // gradient rows (owner)
   PeerBuf p_flags, p_xcnt, p_len, p_ids, p_part, p_grad, p_pooled;
   DevBuf p_pooled_local;  // engine-owned pooled output when N == 1
-  DevBuf hbuf;
+  DevBuf hbuf, row_upd_scratch;
   uint64_t epoch = 0;
   DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
@@ -148,7 +135,8 @@ struct Ctx {
   void phase_times(double* ms, uint32_t* counts);
 
   ~Ctx();
-  void create(int device, uint32_t T, uint32_t M, uint32_t rank, const uint8_t* nccl_id);
+  void create(int device, uint32_t T, uint32_t M, uint32_t rank, const uint8_t* nccl_id,
+              std::shared_ptr<LocalHub> hub = nullptr);
   void register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_entry* p, uint32_t np,
                        int dtype);
   void set_optimizer(const s2d_optimizer_config& c);
@@ -179,7 +167,7 @@ struct Ctx {
   void check_faults();
   PeerPtrs ptrs(const PeerBuf& pb) const;
   void peer_alloc(PeerBuf& pb, size_t bytes);
-  void peer_alloc_in(PeerBuf& pb, size_t bytes, ncclComm_t comm, uint32_t n, uint32_t me);
+  void peer_alloc_in(PeerBuf& pb, size_t bytes, Comm& comm);
   void peer_barrier();
   // DP group over NVLink peer memory (replica sync): every replica's
   // weights / moments mapped, a group barrier, a staging slice

@@ -22,6 +22,47 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
+class _ThreadDist:
+    """torch.distributed's object collectives for virtual ranks on threads
+    (--local): every call is a rendezvous of all `world` threads."""
+
+    def __init__(self, world):
+        import threading
+
+        self.world = world
+        self.bar = threading.Barrier(world, timeout=900)
+        self.box = [None] * world
+
+    def view(self, rank):
+        return _RankDist(self, rank)
+
+
+class _RankDist:
+    def __init__(self, hub, rank):
+        self.h, self.rank = hub, rank
+
+    def _exchange(self, obj):
+        self.h.box[self.rank] = obj
+        self.h.bar.wait()
+        out = list(self.h.box)
+        self.h.bar.wait()
+        return out
+
+    def broadcast_object_list(self, lst, src=0):
+        lst[0] = self._exchange(lst[0])[src]
+
+    def gather_object(self, obj, out, dst=0):
+        got = self._exchange(obj)
+        if self.rank == dst:
+            out[:] = got
+
+    def all_gather_object(self, out, obj):
+        out[:] = self._exchange(obj)
+
+    def barrier(self):
+        self._exchange(None)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--groups", type=int, default=1)
@@ -36,18 +77,32 @@ def main():
                     help="rank 1 sends an id past its table's rows: some rank must raise IndexError")
     ap.add_argument("--bf16", action="store_true",
                     help="bf16 shards: the oracle is re-seeded every step from the mesh's (widened) weights")
+    ap.add_argument("--local", type=int, default=0,
+                    help="run T virtual ranks as threads of this process on one GPU (LocalHub), no torchrun")
     args = ap.parse_args()
 
-    import torch
+    if args.local:
+        import paper_2508_03854_b200 as s2d
+
+        hub = s2d.LocalHub(args.local)
+        td = _ThreadDist(args.local)
+        rc = s2d.run_ranks(lambda r: rank_main(args, r, args.local, 0, td.view(r), hub), args.local, timeout=1200)
+        sys.exit(max(int(x or 0) for x in rc))
     import torch.distributed as dist
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    dist.init_process_group("gloo")
+    sys.exit(rank_main(args, rank, world, local, dist, None))
+
+
+def rank_main(args, rank, world, local, dist, hub):
+    import torch
 
     import paper_2508_03854_b200 as s2d
     from cases import make_batch, upstream
 
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
-    dist.init_process_group("gloo")
     M = args.groups
     N = world // M
     rows = np.array([300, 41, 7, 1000, 128], np.uint32)
@@ -56,17 +111,17 @@ def main():
     eta, c = 0.1, float(M)
     profiles = [(f, int(rows[f]) * int(dims[f]) * 4, float(10 - f), int(rows[f])) for f in range(F)]
     plan = s2d.plan_greedy(profiles, N, args.strategy)
-    nid = [s2d.nccl_unique_id() if rank == 0 else None]
+    nid = [s2d.nccl_unique_id() if rank == 0 and hub is None else None]
     dist.broadcast_object_list(nid, src=0)
     tables = [s2d.TableConfig(int(rows[f]), int(dims[f])) for f in range(F)]
     opt = s2d.OptimizerConfig(eta=eta, eps=1e-8, c=c, variant="sgd" if args.sgd else "rowwise-adagrad")
     eng = s2d.Sparse2DEmbedding(tables, s2d.Topology(world, M), rank=rank, device=local, plan=plan, optimizer=opt,
-                                weight_dtype="bf16" if args.bf16 else "fp32", nccl_id=nid[0])
+                                weight_dtype="bf16" if args.bf16 else "fp32", nccl_id=nid[0], hub=hub)
     eng.init_tables(31)
     if args.bf16:
-        sys.exit(run_bf16(args, eng, dist, rank, world, M, N, rows, dims, B, eta, c, plan))
+        return run_bf16(args, eng, dist, rank, world, M, N, rows, dims, B, eta, c, plan)
     if args.bad_id:
-        sys.exit(run_bad_id(eng, dist, rank, world, rows, dims, B))
+        return run_bad_id(eng, dist, rank, world, rows, dims, B)
 
     def inputs(step, r):
         rng = np.random.default_rng([step, r, 77])
@@ -127,7 +182,7 @@ def main():
     eng.close()
     if rank != 0:
         dist.barrier()
-        return
+        return 0
 
     from oracle import MeshSpec, MeshState, Oracle
 
@@ -210,9 +265,11 @@ def main():
     if fails:
         print("MP PARITY FAIL", world, M, args.strategy, *fails[:20], sep="\n  ")
         dist.barrier()
-        sys.exit(1)
-    print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd} ckpt={args.ckpt}")
+        return 1
+    print(f"MP PARITY OK T={world} M={M} N={N} {args.strategy} steps={args.steps} sgd={args.sgd} ckpt={args.ckpt}"
+          + (" local" if hub is not None else ""))
     dist.barrier()
+    return 0
 
 
 def run_bad_id(eng, dist, rank, world, rows, dims, B):

@@ -1,11 +1,19 @@
-"""Multi-GPU parity (tests/mp_parity.py under torchrun); needs >= 2 GPUs."""
+"""Mesh parity of the 2D step (tests/mp_parity.py).
+
+* test_mesh_parity_local: the T ranks run as virtual ranks (threads of one
+  process sharing one GPU over a LocalHub) -- every N > 1 kernel (K1
+  bucketing, the fused id / pooled / gradient exchanges, the combine, the
+  device barriers, the K5 replica sync) runs on a single B200.
+* test_mesh_parity: one process per GPU under torchrun with NCCL + CUDA IPC
+  over NVLink; needs >= T GPUs.
+"""
 import os
 import subprocess
 import sys
 
 import pytest
 
-pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+pytestmark = [pytest.mark.gpu]
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -42,6 +50,28 @@ def _case_id(c):
             "".join("-nccl-sync" for x in extra if x.startswith("ENV:S2D_SYNC_NCCL")))
 
 
+def _env_args(extra):
+    env = dict(os.environ)
+    for x in extra:  # "ENV:K=V" entries set the environment of the ranks
+        if x.startswith("ENV:"):
+            k, v = x[4:].split("=", 1)
+            env[k] = v
+    return env, [x for x in extra if not x.startswith("ENV:")]
+
+
+@pytest.mark.parametrize("T,M,strategy,extra", CASES, ids=[_case_id(c) for c in CASES])
+def test_mesh_parity_local(T, M, strategy, extra):
+    if _ngpu() < 1:
+        pytest.skip("needs a GPU")
+    env, args = _env_args(extra)
+    cmd = [sys.executable, os.path.join(ROOT, "tests", "mp_parity.py"), "--local", str(T), "--groups", str(M),
+           "--strategy", strategy, *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "MP PARITY OK" in r.stdout
+
+
+@pytest.mark.multigpu
 @pytest.mark.parametrize("T,M,strategy,extra", CASES, ids=[_case_id(c) for c in CASES])
 def test_mesh_parity(T, M, strategy, extra):
     if _ngpu() < T:
