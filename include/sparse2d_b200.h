@@ -77,12 +77,18 @@ typedef struct {
   uint32_t ranks_per_group;
 } s2d_topology;
 
+/* pooling mode of a table (s2d_table_desc.pooling) */
+#define S2D_POOL_SUM 0  /* the reference's pool_ids (embedding.cpp:39-92) */
+#define S2D_POOL_MEAN 1 /* extension: out = f32((sum_o f64(partial_o)) * (1/L)); the
+                           bag's gradient row is f32(f64(up) * (1/L)) */
+
 /* One embedding table (FeatureSpec + EmbeddingTable shape, data.hpp:11-18,
- * embedding.hpp:12-23); per-table rows and dims are an extension. */
+ * embedding.hpp:12-23); per-table rows, dims and pooling are extensions. */
 typedef struct {
   uint32_t table_id; /* must equal its index in the registered list */
   uint32_t rows;
-  uint32_t dim; /* multiple of 4, <= 512 (trainer.cpp:99 kMaxDim) */
+  uint32_t dim;     /* multiple of 4, <= 512 (trainer.cpp:99 kMaxDim) */
+  uint32_t pooling; /* S2D_POOL_SUM | S2D_POOL_MEAN */
 } s2d_table_desc;
 
 /* Per-step counters of the last step on this rank. */

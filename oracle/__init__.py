@@ -56,6 +56,7 @@ class _OrCfg(C.Structure):
         ("n_entries", C.c_uint32), ("plan", C.c_void_p),
         ("eta", C.c_double), ("eps", C.c_double), ("c", C.c_double),
         ("sgd", C.c_int),
+        ("mean", C.c_void_p),
     ]
 
 
@@ -91,6 +92,7 @@ class MeshSpec:
     eps: float = 1e-8
     c: float = 1.0
     sgd: bool = False
+    mean: np.ndarray | None = None  # [F] uint8 per-table mean pooling (None: all sum)
 
     @property
     def N(self) -> int:
@@ -297,11 +299,14 @@ class Oracle:
         rows = np.ascontiguousarray(spec.rows, np.uint32)
         dims = np.ascontiguousarray(spec.dims, np.uint32)
         plan = np.ascontiguousarray(spec.plan, np.uint32)
-        keep = [lengths, ids, upstream, pooled, rows, dims, plan]
+        mean = None if spec.mean is None else np.ascontiguousarray(spec.mean, np.uint8)
+        keep = [lengths, ids, upstream, pooled, rows, dims, plan, mean]
         dump = None
+        if mean is not None and mean.any() and self.kind != "port":
+            raise ValueError("mean pooling has no reference path (embedding.cpp:39-92 is sum-only); use the port")
         if self.kind == "port":
             cfg = _OrCfg(F, N, B, _ptr(rows), _ptr(dims), len(plan), _ptr(plan),
-                         spec.eta, spec.eps, spec.c, int(spec.sgd))
+                         spec.eta, spec.eps, spec.c, int(spec.sgd), _ptr(mean) if mean is not None else None)
             dmp = None
             if want_dump:
                 cap_ids = int(sum(int(x.sum()) for x in lengths)) + 1

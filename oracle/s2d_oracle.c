@@ -227,6 +227,18 @@ typedef struct {
   const uint32_t* plan; /* [n_entries][4] table_id,row_lo,row_hi,local_rank */
   double eta, eps, c;
   int sgd; /* OptimizerVariant::Sgd */
+  /* per-table pooling mode, NULL = all sum (the reference's only mode,
+   * embedding.cpp:39-92).  Mean pooling is this build's extension (north
+   * star K2 "sum/mean"); its definition, pinned here and mirrored by the
+   * CUDA path:
+   *   forward   out_j = f32( (sum_{o asc} f64(p_o,j)) * (1.0 / L) ), p_o the
+   *             owners' f32 partial sums (the sum-pooling wire format), L
+   *             the bag length; an empty bag pools to 0;
+   *   backward  the gradient row sent for the bag is
+   *             f32( f64(up_j) * (1.0 / L) ) (the f32 wire format of
+   *             trainer.cpp:424-427 applied to d out / d row = 1/L); the
+   *             owner then aggregates it exactly as for sum pooling. */
+  const uint8_t* mean;
 } or_cfg;
 
 typedef struct {
@@ -410,7 +422,13 @@ int or_group_step(const or_cfg* c, const uint32_t* const* lengths, const uint32_
             cursor[o] += D;
           }
           float* out = pooled[n] + (size_t)s * d.sum_dims + d.coff[f];
-          for (uint32_t j = 0; j < D; ++j) out[j] = (float)pool[j];
+          const uint32_t L = lengths[n][b];
+          if (c->mean && c->mean[f] && L) {
+            const double inv = 1.0 / (double)L;
+            for (uint32_t j = 0; j < D; ++j) out[j] = (float)(pool[j] * inv);
+          } else {
+            for (uint32_t j = 0; j < D; ++j) out[j] = (float)pool[j];
+          }
         }
       }
     }
@@ -447,9 +465,15 @@ int or_group_step(const or_cfg* c, const uint32_t* const* lengths, const uint32_
         const float* up = upstream[n] + (size_t)s * d.sum_dims;
         for (uint32_t f = 0; f < F; ++f) {
           const uint32_t m = mask[(size_t)n * BF + s * F + f], D = c->dims[f];
+          const uint32_t L = lengths[n][s * F + f];
+          const int scale = c->mean && c->mean[f] && L;
+          const double inv = scale ? 1.0 / (double)L : 1.0;
           for (uint32_t o = 0; o < N; ++o) {
             if (!(m & (1u << o))) continue;
-            memcpy(sg[n][o] + fill[o], up + d.coff[f], sizeof(float) * D);
+            if (scale)
+              for (uint32_t j = 0; j < D; ++j) sg[n][o][fill[o] + j] = (float)((double)up[d.coff[f] + j] * inv);
+            else
+              memcpy(sg[n][o] + fill[o], up + d.coff[f], sizeof(float) * D);
             fill[o] += D;
           }
         }

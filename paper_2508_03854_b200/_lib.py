@@ -18,6 +18,7 @@ S2D_TABLE_WISE, S2D_ROW_WISE = 0, 1
 S2D_ROWWISE_ADAGRAD, S2D_SGD = 0, 1
 S2D_F32, S2D_BF16 = 0, 1
 S2D_HOST, S2D_DEVICE = 0, 1
+S2D_POOL_SUM, S2D_POOL_MEAN = 0, 1
 
 
 class TableLoadProfile(C.Structure):
@@ -39,7 +40,7 @@ class TopologyC(C.Structure):
 
 
 class TableDesc(C.Structure):
-    _fields_ = [("table_id", C.c_uint32), ("rows", C.c_uint32), ("dim", C.c_uint32)]
+    _fields_ = [("table_id", C.c_uint32), ("rows", C.c_uint32), ("dim", C.c_uint32), ("pooling", C.c_uint32)]
 
 
 class StepStats(C.Structure):

@@ -162,6 +162,12 @@ class TableConfig:
     rows: int
     dim: int
     expected_lookups: float = 1.0  # expected lookups per batch (planner load)
+    pooling: str = "sum"  # "sum" (the reference's pool_ids) | "mean"
+
+    def pooling_code(self) -> int:
+        if self.pooling not in ("sum", "mean"):
+            raise ValueError("pooling must be 'sum' or 'mean'")
+        return L.S2D_POOL_MEAN if self.pooling == "mean" else L.S2D_POOL_SUM
 
 
 def launch_count() -> int:
@@ -211,7 +217,18 @@ def traces_to_csv(rows: Iterable[dict], config_hash: str = "") -> str:
            "# bytes = bytes sent by the rank to other ranks (self-delivery stays in HBM)",
            "# latency_s = measured device time of the kernels carrying the exchange",
            "step,kernel,rank,bytes,latency_s"]
-    for r in sorted(rows, key=lambda r: (r["step"], _TRACE_ORDER.get(r["kernel"], 9), r["rank"])):
+    def order(r):
+        # lookup / grad a2a: one trace per MP group, participants in local
+        # order -> global rank order; table_allreduce: one trace per local
+        # rank o over its replicas g = 0..M-1 (trainer.cpp:598-610,
+        # topology.cpp:128-131) -> (local, group)
+        if r["kernel"] == "table_allreduce":
+            sub = (r.get("local", r["rank"]), r.get("group", 0))
+        else:
+            sub = (r["rank"], 0)
+        return (r["step"], _TRACE_ORDER.get(r["kernel"], 9)) + sub
+
+    for r in sorted(rows, key=order):
         out.append(f"{r['step']},{r['kernel']},{r['rank']},{r['bytes']},{r['latency_s']:.9g}")
     return "\n".join(out) + "\n"
 
@@ -321,7 +338,7 @@ class Sparse2DEmbedding:
             L.check(self.lib.s2d_ctx_create(device, topology.total_ranks, topology.groups, rank,
                                             nccl_id if nccl_id is not None else None, C.byref(self._ctx)))
         self.set_strict(strict)
-        td = (L.TableDesc * self.F)(*[L.TableDesc(i, t.rows, t.dim) for i, t in enumerate(self.tables)])
+        td = (L.TableDesc * self.F)(*[L.TableDesc(i, t.rows, t.dim, t.pooling_code()) for i, t in enumerate(self.tables)])
         parr, n = _plan_array(self.plan)
         if weight_dtype not in ("fp32", "bf16"):
             raise ValueError("weight_dtype must be fp32 or bf16")
@@ -529,6 +546,10 @@ class Sparse2DEmbedding:
         HBM and is not counted, unlike the simulated trace.  table_allreduce
         appears only when a replica sync ran."""
         times = self.phase_times()
+        if times["lookup"][1] > 1:
+            # the byte counters describe the last step only
+            raise ValueError(f"trace_rows covers {times['lookup'][1]} forwards; call phase_times() right before "
+                             "the step to be traced")
         st = self.stats()
         sent = {
             "lookup_a2a": st["ids_bytes_sent"] + st["lookup_bytes_sent"],
@@ -537,12 +558,16 @@ class Sparse2DEmbedding:
         }
         rows = []
         for kernel, phases in self.TRACE_PHASES.items():
-            if kernel == "table_allreduce" and times["sync"][1] == 0:
-                continue
+            if kernel == "table_allreduce" and (times["sync"][1] == 0 or not self._owns_rows()):
+                continue  # the reference traces only local ranks with a non-empty shard
             ms = sum(times[p][0] for p in phases)
             rows.append({"step": int(step), "kernel": kernel, "rank": self.rank,
+                         "group": self.topology.group_of(self.rank), "local": self.topology.local_of(self.rank),
                          "bytes": int(sent[kernel]), "latency_s": ms * 1e-3})
         return rows
+
+    def _owns_rows(self) -> bool:
+        return any(hi > lo for lo, hi in (self.owned_range(f) for f in range(self.F)))
 
     def debug(self, which: int) -> np.ndarray:
         """Wire buffers of the last step (see s2d_debug_read)."""

@@ -63,6 +63,9 @@ void launch_zero(void* p, size_t bytes, cudaStream_t st);
 
 // Device fault bits (checked once per step, SURVEY.md 5 failure detection).
 enum : uint32_t { kErrIdRange = 1u, kErrNonfinite = 2u, kErrPeerTimeout = 4u };
+// batch word of the published count matrix: bit 32 = requester uses the
+// engine-owned pooled output
+constexpr uint64_t kEngineOutFlag = 1ull << 32;
 
 constexpr int kMaxPeers = 32;
 // Per-peer device pointers of one IPC-shared buffer (index = local rank in
@@ -82,6 +85,7 @@ struct FeatDev {
   uint32_t rbeg;    // owner ranges of this table: ranges[rbeg, rend)
   uint32_t rend;
   uint32_t single;  // the plan gives the table one owner: partial == pooled row
+  uint32_t mean;    // S2D_POOL_MEAN: pooled row scaled by 1/L, gradient row by 1/L
 };
 
 // Owner range of a table inside the MP group (sorted by lo per table).
@@ -151,7 +155,7 @@ struct LookupArgs {
   // zero-copy output: bags of single-owner tables are stored as final pooled
   // rows straight into requester n's pooled buffer peer_pooled.p[n]
   PeerPtrs peer_pooled;
-  int use_peer_pooled;
+  uint32_t use_peer_pooled;    // bit n: requester n takes single-owner pooled rows from the owners
 };
 
 struct CombineArgs {
@@ -162,6 +166,7 @@ struct CombineArgs {
   const float* recv;           // partials received, concatenated by owner
   float* pooled;               // [B][sumD]
   int skip_single;             // single-owner bags were written by their owners
+  const uint32_t* bag_off;     // [B*F+1] local bag offsets (mean pooling: L = bag_off[b+1] - bag_off[b])
 };
 void launch_combine(const CombineArgs& a, int max_dim, cudaStream_t st);
 
@@ -172,6 +177,7 @@ struct GradGatherArgs {
   const uint32_t* cnt;
   const uint64_t* eoff;
   const float* upstream;       // [B][sumD]
+  const uint32_t* bag_off;     // [B*F+1] local bag offsets (mean pooling scales by 1/L)
   // gradient row of bag b for owner o -> peer_dst.p[o] + peer_adj[o] + eoff[o*BF+b]
   PeerPtrs peer_dst;
   int64_t peer_adj[kMaxPeers];
@@ -202,7 +208,7 @@ void launch_bucket_permute(const BucketArgs& a, cudaStream_t st);
 // peer primitives (k_peer.cu)
 void launch_peer_barrier(const PeerPtrs& flags, uint64_t* my_flags, uint32_t me, uint32_t n, uint64_t epoch,
                          uint32_t* err, cudaStream_t st);
-void launch_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF, uint32_t batch,
+void launch_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF, uint64_t batch,
                            const PeerPtrs& xcnt, uint32_t me, cudaStream_t st);
 
 // update kernels (k_update.cu)
@@ -233,6 +239,10 @@ struct StreamUpdateArgs {
   uint32_t* err;
   uint32_t* counters;            // [0] unique rows updated, [1] rows spanning ranges
 };
+// mean pooling, N = 1 (k_embed.cu): out = upstream with the columns of
+// mean-pooled tables replaced by f32(f64(up) * (1/L_bag))
+void launch_mean_prescale(const FeatDev* feats, uint32_t F, uint32_t B, uint32_t sum_dims, const uint32_t* bag_off,
+                          const float* up, float* out, cudaStream_t st);
 // device-side synthetic input (k_gen.cu): DataGenerator ids, data.cpp:85-136
 struct GenArgs {
   uint64_t seed, step;
@@ -255,7 +265,7 @@ void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 // standalone fused row step on caller rows (s2d_adagrad_rows)
 void launch_apply_rows(void* w, bool bf16, float* v, const uint32_t* order, const uint32_t* seg,
                        const uint32_t* seg_row, const double* delta, const double* moment, uint32_t nseg,
-                       uint32_t dim, cudaStream_t st);
+                       uint32_t dim, uint8_t* dirty, cudaStream_t st);
 void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32_t n, uint32_t dim,
                          double eta, double eps, double c, int sgd, uint32_t* err, cudaStream_t st);
 

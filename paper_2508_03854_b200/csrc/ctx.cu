@@ -175,13 +175,18 @@ void Ctx::register_tables(const s2d_table_desc* t, uint32_t n, const s2d_plan_en
   ranges.clear();
   sum_dims = 0;
   max_dim = 0;
+  any_mean = false;
   for (uint32_t f = 0; f < F; ++f) {
     const auto& d = tables[f];
     if (d.table_id != f) throw Error(S2D_EINVAL, "table_id must equal its index");
     if (d.rows < 1 || d.dim < 1) throw Error(S2D_EINVAL, "table needs rows >= 1 and dim >= 1");
     if (d.dim % 4 || d.dim > (uint32_t)kMaxDim)
       throw Error(S2D_EINVAL, "dim must be a multiple of 4 and <= 512 (table " + std::to_string(f) + ")");
+    if (d.pooling != S2D_POOL_SUM && d.pooling != S2D_POOL_MEAN)
+      throw Error(S2D_EINVAL, "pooling must be S2D_POOL_SUM or S2D_POOL_MEAN (table " + std::to_string(f) + ")");
     feats[f].dim = d.dim;
+    feats[f].mean = d.pooling == S2D_POOL_MEAN ? 1u : 0u;
+    any_mean = any_mean || feats[f].mean;
     feats[f].rows = d.rows;
     feats[f].coff = sum_dims;
     sum_dims += d.dim;
@@ -331,6 +336,8 @@ void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v,
       }
     }
   }
+  if (write && M > 1)  // written rows join the next replica sync's dirty union
+    S2D_CUDA(cudaMemset(dirty.as<uint8_t>() + fd.vbase + (lo - fd.lo), 1, hi - lo));
   if (v) {
     float* dst = moments.as<float>() + fd.vbase + (lo - fd.lo);
     if (write)
@@ -380,10 +387,13 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
   S2D_CUDA(cudaMemcpy(d + o_delta, delta, b_delta, cudaMemcpyHostToDevice));
   S2D_CUDA(cudaMemcpy(d + o_mom, new_moment, b_mom, cudaMemcpyHostToDevice));
   void* wbase = bf16 ? (void*)(weights.as<uint16_t>() + fd.wbase) : (void*)(weights.as<float>() + fd.wbase);
+  // M > 1: the rows written here join the next replica sync's dirty union
+  // (the sync averages only dirty rows, so an unflagged write would leave
+  // the replicas different)
   launch_apply_rows(wbase, bf16, moments.as<float>() + fd.vbase, reinterpret_cast<uint32_t*>(d),
                     reinterpret_cast<uint32_t*>(d + o_seg), reinterpret_cast<uint32_t*>(d + o_row),
                     reinterpret_cast<double*>(d + o_delta), reinterpret_cast<double*>(d + o_mom), nseg, fd.dim,
-                    stream);
+                    M > 1 ? dirty.as<uint8_t>() + fd.vbase : nullptr, stream);
   S2D_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -442,12 +452,14 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   // peer-mapped pooled buffer (s2d_pooled_buffer); owners of single-owner
   // tables then store pooled rows straight into it over NVLink
   const bool engine_out = (mem == S2D_DEVICE && pooled == nullptr) || mem == S2D_HOST;
+  // N > 1: the peer-mapped pooled buffer is (re)allocated by every rank
+  // whatever its own output mode, so the collective growth decisions of the
+  // group never depend on a per-rank choice (B itself must agree across the
+  // MP group; read_counts checks it every step)
+  if (N > 1) peer_alloc(p_pooled, (uint64_t)B * sum_dims * 4);
   if (engine_out) {
     if (d2h_pending) S2D_CUDA(cudaStreamWaitEvent(stream, ev_d2h, 0));  // last read-back of the buffer
-    if (N > 1)
-      peer_alloc(p_pooled, (uint64_t)B * sum_dims * 4);
-    else
-      p_pooled_local.ensure((uint64_t)B * sum_dims * 4);
+    if (N == 1) p_pooled_local.ensure((uint64_t)B * sum_dims * 4);
     d_pooled = N > 1 ? p_pooled.buf.as<float>() : p_pooled_local.as<float>();
   }
   if (mem == S2D_HOST) {
@@ -517,7 +529,11 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     launch_bucket_count(ba, stream);  // also stores cnt[o][:] into owner o's receive lengths
     scan_count_pair(cnt.as<uint32_t>(), send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), (uint64_t)N * BF, F, dfe,
                     stream, scan_tmp.p, scan_tmp.cap);
-    launch_publish_counts(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF, B, ptrs(p_xcnt), local, stream);
+    // the batch word carries this requester's output mode: owners store
+    // single-owner pooled rows straight into a requester's pooled buffer
+    // only when that requester asked for the engine-owned output
+    launch_publish_counts(send_off.as<uint32_t>(), eoff_req.as<uint64_t>(), N, BF,
+                          (uint64_t)B | (engine_out ? kEngineOutFlag : 0ull), ptrs(p_xcnt), local, stream);
     peer_barrier();
     phase_begin(kPhCountSync);
     read_counts();  // count matrix -> offsets; grows the peer buffers collectively
@@ -554,8 +570,8 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.uni_rows = slot_rows ? 1 : 0;
     a.zero_row = n_slots;
     a.peer_out = ptrs(p_part);
-    a.use_peer_pooled = engine_out ? 1 : 0;
-    if (engine_out) a.peer_pooled = ptrs(p_pooled);
+    a.use_peer_pooled = (int)engine_mask;  // per requester (bit n), from the count matrix
+    a.peer_pooled = ptrs(p_pooled);
     for (uint32_t n = 0; n < N; ++n) a.peer_adj[n] = (int64_t)part_base_at_req[n] - (int64_t)own_eoff_bound[n];
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
@@ -582,6 +598,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     ca.recv = p_part.buf.as<float>();
     ca.pooled = d_pooled;
     ca.skip_single = engine_out ? 1 : 0;
+    ca.bag_off = in_off.as<uint32_t>();
     launch_combine(ca, (int)max_dim, stream);
     phase_end();  // the gap until the backward call is no phase
     uint64_t ef_own = 0, sent = 0, recv = 0;
@@ -640,6 +657,15 @@ void Ctx::peer_alloc_in(PeerBuf& pb, size_t bytes, Comm& comm) {
   pb.cap = want;
   S2D_CUDA(cudaMemsetAsync(pb.buf.p, 0, want, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
+  // every member must have asked for the same size (sizes derive from data
+  // the group shares, e.g. the per-rank batch); a mismatch is a caller error
+  std::vector<uint64_t> sizes(comm.n);
+  const uint64_t mine = bytes;
+  comm.host_allgather(&mine, 8, sizes.data(), stream, hbuf);
+  for (uint64_t s : sizes)
+    if (s != mine)
+      throw Error(S2D_EINVAL, "MP group members disagree on a shared buffer size (per-rank batch / table set must "
+                              "be identical in the group)");
   pb.ptr = map_peer_buffers(comm, pb.buf.p, device, stream, hbuf, pb.opened);
 }
 
@@ -734,10 +760,14 @@ void Ctx::read_counts() {
                             std::chrono::steady_clock::now() - t0).count();
   const uint64_t* x = h_xcnt.as<uint64_t>();
   auto at = [&](uint32_t n, uint32_t o, int k) { return x[((size_t)n * N + o) * 3 + k]; };
-  for (uint32_t n = 0; n < N; ++n)
-    if (at(n, 0, 2) != B)
-      throw Error(S2D_EINVAL, "per-rank batch must be identical in the MP group (" + std::to_string(at(n, 0, 2)) +
-                                  " vs " + std::to_string(B) + ")");
+  engine_mask = 0;
+  for (uint32_t n = 0; n < N; ++n) {
+    const uint64_t bw = at(n, 0, 2);
+    if ((bw & ~kEngineOutFlag) != B)
+      throw Error(S2D_EINVAL, "per-rank batch must be identical in the MP group (" +
+                                  std::to_string(bw & ~kEngineOutFlag) + " vs " + std::to_string(B) + ")");
+    if (bw & kEngineOutFlag) engine_mask |= 1u << n;
+  }
   nnz_to.assign(N, 0);
   ef_to.assign(N, 0);
   nnz_from.assign(N, 0);
@@ -821,6 +851,16 @@ void Ctx::backward_update(const float* upstream, int mem) {
     up_wait = true;
   }
   const float* grad = d_up;
+  if (N == 1 && any_mean && nnz_own > 0) {
+    // mean-pooled tables: the bag's gradient row is f32(f64(up) * (1/L))
+    // (the N > 1 gradient gather applies the same scale on its way out)
+    if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));
+    up_wait = false;
+    mean_stage.ensure((uint64_t)B * sum_dims * 4);
+    launch_mean_prescale(d_feats.as<FeatDev>(), F, B, sum_dims, in_off.as<uint32_t>(), d_up, mean_stage.as<float>(),
+                         stream);
+    grad = mean_stage.as<float>();
+  }
   if (N > 1) {
     if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));
     up_wait = false;
@@ -838,6 +878,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ga.cnt = cnt.as<uint32_t>();
     ga.eoff = eoff_req.as<uint64_t>();
     ga.upstream = d_up;
+    ga.bag_off = in_off.as<uint32_t>();
     ga.peer_dst = ptrs(p_grad);
     for (uint32_t o = 0; o < N; ++o) ga.peer_adj[o] = (int64_t)grad_base_at_owner[o] - (int64_t)eoff_req_bound[o];
     launch_grad_gather(ga, (int)max_dim, stream);

@@ -77,6 +77,7 @@ struct Ctx {
   // tables + plan
   uint32_t F = 0, sum_dims = 0, max_dim = 0;
   int bf16 = 0;
+  bool any_mean = false;  // some table uses S2D_POOL_MEAN
   std::vector<s2d_table_desc> tables;
   std::vector<s2d_plan_entry> plan;
   std::vector<FeatDev> feats;
@@ -101,7 +102,7 @@ struct Ctx {
   uint32_t B = 0;
   uint64_t nnz_local = 0, nnz_own = 0;
   bool fwd_done = false;
-  DevBuf in_lengths, in_ids, in_off, upstream_stage;
+  DevBuf in_lengths, in_ids, in_off, upstream_stage, mean_stage;
   DevBuf cnt, send_off, eoff_req;  // requester side (N > 1)
   DevBuf own_idoff, own_eoff;      // owner side (N > 1)
   // MP-group peer buffers: barrier flags, count matrix, received bag
@@ -111,6 +112,7 @@ struct Ctx {
   DevBuf p_pooled_local;  // engine-owned pooled output when N == 1
   DevBuf hbuf, row_upd_scratch;
   uint64_t epoch = 0;
+  uint32_t engine_mask = 0;  // requesters of the current step that asked for the engine-owned output
   DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
   DevBuf sync_list, sync_lists, sync_count, sync_packed, sync_gathered, sync_tmp;

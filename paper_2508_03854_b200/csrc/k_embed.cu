@@ -117,6 +117,14 @@ __global__ void __launch_bounds__(256) k_combine(const CombineArgs a) {
         }
       }
       float* out = a.pooled + (b / a.F) * a.sum_dims + __ldg(&a.feats[f].coff);
+      if (__ldg(&a.feats[f].mean)) {  // mean pooling: f32(C * (1/L))
+        const uint32_t L = __ldg(a.bag_off + b + 1) - __ldg(a.bag_off + b);
+        const double inv = L ? 1.0 / (double)L : 1.0;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[v][q] = acc[v][q] * inv;
+      }
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         const uint32_t c4 = gl + v * LPB;
@@ -153,6 +161,17 @@ __global__ void __launch_bounds__(256) k_grad_gather(const GradGatherArgs a) {
           const uint32_t c4 = gl + v * LPB;
           if (c4 < d4[u]) x[u][v] = __ldg(reinterpret_cast<const float4*>(up + c4 * 4));
         }
+        if (__ldg(&a.feats[f].mean)) {  // mean pooling: the wire row is f32(f64(up) * (1/L))
+          const uint32_t L = __ldg(a.bag_off + b + 1) - __ldg(a.bag_off + b);
+          const double inv = L ? 1.0 / (double)L : 1.0;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            x[u][v].x = (float)((double)x[u][v].x * inv);
+            x[u][v].y = (float)((double)x[u][v].y * inv);
+            x[u][v].z = (float)((double)x[u][v].z * inv);
+            x[u][v].w = (float)((double)x[u][v].w * inv);
+          }
+        }
       }
     }
 #pragma unroll
@@ -177,6 +196,38 @@ __global__ void __launch_bounds__(256) k_grad_gather(const GradGatherArgs a) {
         }
       }
     }
+  }
+}
+
+// ---- mean pooling, N = 1: scaled gradient rows ------------------------------
+
+// out[s][coff_f + j] = f32(f64(up) * (1/L_(s,f))) for mean-pooled tables,
+// up unchanged otherwise; one thread per float4
+__global__ void __launch_bounds__(256) k_mean_prescale(const FeatDev* __restrict__ feats, uint32_t F, uint32_t B,
+                                                       uint32_t sum_dims, const uint32_t* __restrict__ bag_off,
+                                                       const float* __restrict__ up, float* __restrict__ out) {
+  pdl_wait();
+  const uint32_t q4 = sum_dims / 4;
+  const uint64_t n = (uint64_t)B * q4;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = (uint32_t)(i / q4), c = (uint32_t)(i % q4) * 4;
+    uint32_t f = 0;  // feature of column c (feats sorted by coff)
+    for (uint32_t lo = 0, hi = F; hi - lo > 1;) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(&feats[mid].coff) <= c) lo = f = mid;
+      else hi = mid;
+    }
+    float4 x = __ldg(reinterpret_cast<const float4*>(up) + i);
+    if (__ldg(&feats[f].mean)) {
+      const uint64_t b = (uint64_t)s * F + f;
+      const uint32_t L = __ldg(bag_off + b + 1) - __ldg(bag_off + b);
+      const double inv = L ? 1.0 / (double)L : 1.0;
+      x.x = (float)((double)x.x * inv);
+      x.y = (float)((double)x.y * inv);
+      x.z = (float)((double)x.z * inv);
+      x.w = (float)((double)x.w * inv);
+    }
+    reinterpret_cast<float4*>(out)[i] = x;
   }
 }
 
@@ -350,6 +401,14 @@ void launch_bucket_count(const BucketArgs& a, cudaStream_t st) {
 void launch_bucket_permute(const BucketArgs& a, cudaStream_t st) {
   if (!a.BF) return;
   pdl_launch(k_bucket_permute, dim3(grid_for(a.BF, 256, kGridCap)), dim3(256), 0, st, a);
+}
+
+void launch_mean_prescale(const FeatDev* feats, uint32_t F, uint32_t B, uint32_t sum_dims, const uint32_t* bag_off,
+                          const float* up, float* out, cudaStream_t st) {
+  const uint64_t n = (uint64_t)B * (sum_dims / 4);
+  if (!n) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  pdl_launch(k_mean_prescale, dim3(grid), dim3(256), 0, st, feats, F, B, sum_dims, bag_off, up, out);
 }
 
 }  // namespace s2d

@@ -45,7 +45,7 @@ __global__ void k_peer_barrier(PeerPtrs flags, uint64_t* my_flags, uint32_t me, 
 // row `me` of every peer's count matrix: per destination owner o, (ids to o,
 // partial floats for o) from the exclusive scans' block boundaries.
 __global__ void k_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF,
-                                 uint32_t batch, PeerPtrs xcnt, uint32_t me) {
+                                 uint64_t batch, PeerPtrs xcnt, uint32_t me) {
   pdl_wait();
   const uint32_t o = threadIdx.x;
   if (o >= N) return;
@@ -66,7 +66,7 @@ void launch_peer_barrier(const PeerPtrs& flags, uint64_t* my_flags, uint32_t me,
   pdl_launch(k_peer_barrier, dim3(1), dim3(32), 0, st, flags, my_flags, me, n, epoch, err);
 }
 
-void launch_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF, uint32_t batch,
+void launch_publish_counts(const uint32_t* send_off, const uint64_t* eoff, uint32_t N, uint64_t BF, uint64_t batch,
                            const PeerPtrs& xcnt, uint32_t me, cudaStream_t st) {
   pdl_launch(k_publish_counts, dim3(1), dim3(32), 0, st, send_off, eoff, N, BF, batch, xcnt, me);
 }

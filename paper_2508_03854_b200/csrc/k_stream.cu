@@ -193,14 +193,21 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
     // pooled row (N = 1) or requester n's receive buffer over NVLink (N > 1)
     const uint64_t out_off = a.direct ? (uint64_t)((my_bag / a.F) % a.B) * a.sum_dims + __ldg(&a.feats[f].coff)
                                       : __ldg(a.eoff + my_bag);
+    bool pooled_row = a.direct;  // the flush stores a final pooled row (not a partial)
     float* const optr = a.direct ? a.out + out_off : [&] {
       const uint64_t BF = (uint64_t)a.B * a.F;
       const uint32_t n = (uint32_t)(my_bag / BF);
-      if (a.use_peer_pooled && __ldg(&a.feats[f].single))
+      if (((a.use_peer_pooled >> n) & 1u) && __ldg(&a.feats[f].single)) {
+        pooled_row = true;
         return reinterpret_cast<float*>(a.peer_pooled.p[n]) + ((my_bag % BF) / a.F) * a.sum_dims +
                __ldg(&a.feats[f].coff);
+      }
       return reinterpret_cast<float*>(a.peer_out.p[n]) + a.peer_adj[n] + out_off;
     }();
+    // mean pooling of a final pooled row: f32(f64(f32(sum)) * (1/L)); 0 = none
+    // (a single-owner table's owner sees the whole bag: L = its item count)
+    const double inv_len = (pooled_row && __ldg(&a.feats[f].mean) && my_end > my_start)
+                               ? 1.0 / (double)(my_end - my_start) : 0.0;
     if (a.direct) {  // empty bags pool to zero (embedding.cpp:43-44)
       uint32_t empty = __ballot_sync(0xffffffffu, lane < nb && my_start == my_end);
       while (empty) {
@@ -297,6 +304,13 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
     cur &= 0xffu;
     auto flush = [&]() {
       float* const op = reinterpret_cast<float*>(shfl64(reinterpret_cast<uint64_t>(optr), cur));
+      const double sc = __longlong_as_double((long long)shfl64((uint64_t)__double_as_longlong(inv_len), cur));
+      if (sc != 0.0) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[v][k] = (double)(float)acc[v][k] * sc;
+      }
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         if (lane + v * 32 < d4c) store_f32x4_stream(op + (lane + v * 32) * 4, acc[v]);

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) k_apply_rows(W* __restrict__ w, float* __
                                                     const uint32_t* __restrict__ seg_row,
                                                     const double* __restrict__ delta,
                                                     const double* __restrict__ moment, uint32_t nseg,
-                                                    uint32_t dim) {
+                                                    uint32_t dim, uint8_t* __restrict__ dirty) {
   const uint32_t lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   for (uint32_t s = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); s < nseg; s += warps) {
@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(256) k_apply_rows(W* __restrict__ w, float* __
       }
       row[c] = x;
     }
-    if (lane == 0) v[seg_row[s]] = (float)moment[order[e - 1]];
+    if (lane == 0) {
+      v[seg_row[s]] = (float)moment[order[e - 1]];
+      if (dirty) dirty[seg_row[s]] = 1;
+    }
   }
 }
 
@@ -124,15 +127,15 @@ __global__ void __launch_bounds__(256) k_apply_rows(W* __restrict__ w, float* __
 
 void launch_apply_rows(void* w, bool bf16, float* v, const uint32_t* order, const uint32_t* seg,
                        const uint32_t* seg_row, const double* delta, const double* moment, uint32_t nseg,
-                       uint32_t dim, cudaStream_t st) {
+                       uint32_t dim, uint8_t* dirty, cudaStream_t st) {
   if (!nseg) return;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nseg + 7) / 8, 148ull * 8));
   if (bf16)
     k_apply_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<__nv_bfloat16*>(w), v, order, seg, seg_row,
-                                                      delta, moment, nseg, dim);
+                                                      delta, moment, nseg, dim, dirty);
   else
     k_apply_rows<float><<<grid, 256, 0, st>>>(static_cast<float*>(w), v, order, seg, seg_row, delta, moment,
-                                              nseg, dim);
+                                              nseg, dim, dirty);
   S2D_LAUNCH_CHECK();
 }
 

@@ -72,6 +72,9 @@ def main():
     ap.add_argument("--sgd", action="store_true")
     ap.add_argument("--batch", type=int, default=48)
     ap.add_argument("--engine-out", action="store_true", help="zero-copy pooled output (owners write it)")
+    ap.add_argument("--mean", action="store_true", help="tables 0, 2, 4 use mean pooling")
+    ap.add_argument("--mixed-out", action="store_true",
+                    help="even ranks take the engine-owned output, odd ranks their own device buffer")
     ap.add_argument("--ckpt", action="store_true", help="S2DCKPT1 save from the mesh + load into every replica")
     ap.add_argument("--bad-id", action="store_true",
                     help="rank 1 sends an id past its table's rows: some rank must raise IndexError")
@@ -113,7 +116,8 @@ def rank_main(args, rank, world, local, dist, hub):
     plan = s2d.plan_greedy(profiles, N, args.strategy)
     nid = [s2d.nccl_unique_id() if rank == 0 and hub is None else None]
     dist.broadcast_object_list(nid, src=0)
-    tables = [s2d.TableConfig(int(rows[f]), int(dims[f])) for f in range(F)]
+    mean = np.array([1 if (args.mean and f % 2 == 0) else 0 for f in range(F)], np.uint8)
+    tables = [s2d.TableConfig(int(rows[f]), int(dims[f]), pooling="mean" if mean[f] else "sum") for f in range(F)]
     opt = s2d.OptimizerConfig(eta=eta, eps=1e-8, c=c, variant="sgd" if args.sgd else "rowwise-adagrad")
     eng = s2d.Sparse2DEmbedding(tables, s2d.Topology(world, M), rank=rank, device=local, plan=plan, optimizer=opt,
                                 weight_dtype="bf16" if args.bf16 else "fp32", nccl_id=nid[0], hub=hub)
@@ -135,7 +139,7 @@ def rank_main(args, rank, world, local, dist, hub):
             eng.set_profiling(True)
             eng.phase_times()
         lengths, ids, up = inputs(step, rank)
-        if args.engine_out:
+        if args.engine_out or (args.mixed_out and rank % 2 == 0):
             import torch
 
             dl = torch.from_numpy(lengths.view(np.int32)).cuda()
@@ -188,7 +192,7 @@ def rank_main(args, rank, world, local, dist, hub):
 
     port = Oracle("port")
     plan_arr = np.array([[e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]] for e in plan], np.uint32)
-    spec = MeshSpec(rows=rows, dims=dims, plan=plan_arr, T=world, M=M, B=B, eta=eta, c=c, sgd=args.sgd)
+    spec = MeshSpec(rows=rows, dims=dims, plan=plan_arr, T=world, M=M, B=B, eta=eta, c=c, sgd=args.sgd, mean=mean)
     st = MeshState.init(port, spec, 31)
     st_prev = ([w.copy() for w in st.ws], [v.copy() for v in st.vs])
     fails = []
@@ -221,7 +225,8 @@ def rank_main(args, rank, world, local, dist, hub):
                         want_p = np.concatenate([dump.part[o][l] for o in range(N)])
                         want_g = np.concatenate([dump.grad[n][l] for n in range(N)])
                         # (engine output: single-owner tables' rows bypass the partial buffer)
-                        if not args.engine_out and not np.array_equal(lay[2].view(np.uint32), want_p.view(np.uint32)):
+                        engine_r = args.engine_out or (args.mixed_out and r % 2 == 0)
+                        if not engine_r and not np.array_equal(lay[2].view(np.uint32), want_p.view(np.uint32)):
                             fails.append(f"partial payload rank {r}")
                         if not np.array_equal(lay[3].view(np.uint32), want_g.view(np.uint32)):
                             fails.append(f"grad payload rank {r}")

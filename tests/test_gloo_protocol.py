@@ -154,7 +154,7 @@ def test_two_rank_wire_protocol(strategy):
     assert res == {0: "ok", 1: "ok"}, res
 
 
-def _trace_worker(rank, world, port, out_q):
+def _trace_worker(rank, world, port, out_q, N=None):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
@@ -164,7 +164,9 @@ def _trace_worker(rank, world, port, out_q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         # per-rank measured rows as Sparse2DEmbedding.trace_rows returns them
-        mine = [{"step": 3, "kernel": k, "rank": rank, "bytes": 100 * (rank + 1) + i, "latency_s": 1e-4 * (rank + 1)}
+        N = N or world
+        mine = [{"step": 3, "kernel": k, "rank": rank, "group": rank // N, "local": rank % N,
+                 "bytes": 100 * (rank + 1) + i, "latency_s": 1e-4 * (rank + 1)}
                 for i, k in enumerate(("lookup_a2a", "grad_a2a", "table_allreduce"))]
         allrows = [None] * world
         dist.all_gather_object(allrows, mine)  # the gather bench.py --trace-csv does
@@ -196,3 +198,27 @@ def test_trace_rows_gathered_over_ranks_gloo():
                     "3,lookup_a2a,0,100,0.0001", "3,lookup_a2a,1,200,0.0002",
                     "3,grad_a2a,0,101,0.0001", "3,grad_a2a,1,201,0.0002",
                     "3,table_allreduce,0,102,0.0001", "3,table_allreduce,1,202,0.0002"]
+
+
+def test_trace_rows_2x2_mesh_table_allreduce_order_gloo():
+    """world_size 4 as a 2x2 mesh (N = 2 ranks per MP group, M = 2 groups):
+    the reference writes one table_allreduce trace per local rank o over its
+    replicas rank_of(g, o) (trainer.cpp:598-610, topology.cpp:128-131), so
+    the rows come in rank order 0, 2, 1, 3; the all-to-alls stay in rank order."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_trace_worker, args=(r, 4, port, q, 2)) for r in range(4)]
+    for p in ps:
+        p.start()
+    text = q.get(timeout=180)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    body = [l for l in text.splitlines() if not l.startswith("#")]
+    ranks = lambda k: [int(l.split(",")[2]) for l in body[1:] if l.split(",")[1] == k]
+    assert ranks("lookup_a2a") == [0, 1, 2, 3]
+    assert ranks("grad_a2a") == [0, 1, 2, 3]
+    assert ranks("table_allreduce") == [0, 2, 1, 3]

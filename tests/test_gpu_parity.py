@@ -16,21 +16,23 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-5
 
 
-def _engine(rows, dims, strategy="table-wise", eta=0.1, c=1.0, variant="rowwise-adagrad", dtype="fp32"):
+def _engine(rows, dims, strategy="table-wise", eta=0.1, c=1.0, variant="rowwise-adagrad", dtype="fp32",
+            mean=None):
     import paper_2508_03854_b200 as s2d
 
-    tables = [s2d.TableConfig(int(r), int(d)) for r, d in zip(rows, dims)]
+    mean = mean if mean is not None else [0] * len(rows)
+    tables = [s2d.TableConfig(int(r), int(d), pooling="mean" if m else "sum") for r, d, m in zip(rows, dims, mean)]
     return s2d.Sparse2DEmbedding(tables, s2d.Topology(1, 1), rank=0, device=0, strategy=strategy,
                                  optimizer=s2d.OptimizerConfig(eta=eta, eps=1e-8, c=c, variant=variant),
                                  weight_dtype=dtype)
 
 
-def _spec(rows, dims, B, eta=0.1, c=1.0, sgd=False):
+def _spec(rows, dims, B, eta=0.1, c=1.0, sgd=False, mean=None):
     from oracle import MeshSpec, row_wise_plan
 
     rows = np.array(rows, np.uint32)
     return MeshSpec(rows=rows, dims=np.array(dims, np.uint32), plan=row_wise_plan(rows, 1), T=1, M=1, B=B,
-                    eta=eta, c=c, sgd=sgd)
+                    eta=eta, c=c, sgd=sgd, mean=None if mean is None else np.array(mean, np.uint8))
 
 
 def _download(eng, spec):
@@ -215,6 +217,35 @@ def test_mixed_dims_variable_pooling_empty_bags(port):
         want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
         got = eng.forward(lengths, ids)
         assert np.array_equal(bits(got), bits(want))
+        eng.backward_update(up)
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
+@pytest.mark.parametrize("variant", ["rowwise-adagrad", "sgd"])
+def test_mean_pooling_bit_exact(port, variant):
+    """Mean pooling (north star K2 "sum/mean"; the reference is sum-only, so
+    the semantics are this build's, pinned by the oracle restatement):
+    out = f32(f64(f32 sum) * (1/L)), gradient row f32(f64(up) * (1/L)).
+    Mixed sum / mean tables, mixed dims, variable lengths, empty bags."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(17)
+    rows, dims, B = [50, 1000, 7, 200], [8, 12, 128, 32], 48
+    mean = [1, 0, 1, 1]
+    spec = _spec(rows, dims, B, eta=0.05, c=2.0, sgd=variant == "sgd", mean=mean)
+    eng = _engine(rows, dims, eta=0.05, c=2.0, variant=variant, mean=mean)
+    eng.init_tables(9)
+    st = MeshState.init(port, spec, 9)
+    for step in range(3):
+        lengths, _ = make_batch(rng, spec.rows, B, max_len=25)
+        lengths[::5] = 0
+        lengths, ids = _regen(rng, spec.rows, lengths)
+        up = upstream(rng, B, spec.sum_dims)
+        want = st.step(port, [lengths], [ids], [up], do_sync=False)[0]
+        got = eng.forward(lengths, ids)
+        assert np.array_equal(bits(got), bits(want)), step
         eng.backward_update(up)
     w, v = _download(eng, spec)
     assert np.array_equal(bits(v), bits(st.vs[0]))

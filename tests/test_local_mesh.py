@@ -1,0 +1,100 @@
+"""Single-process meshes (LocalHub virtual ranks on one GPU) driven directly
+from pytest threads: host-side writes join the replica sync."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _mesh(T, M, rows=(64, 40), dim=16):
+    import paper_2508_03854_b200 as s2d
+
+    tables = [s2d.TableConfig(r, dim) for r in rows]
+    engs = s2d.local_mesh(tables, s2d.Topology(T, M), strategy="row-wise",
+                          optimizer=s2d.OptimizerConfig(eta=0.1, eps=1e-8, c=float(M)))
+    s2d.run_ranks(lambda r: engs[r].init_tables(5), T)
+    return s2d, engs
+
+
+def test_apply_row_updates_join_replica_sync():
+    """apply_row_updates on one replica marks its rows dirty, so the next
+    sync averages them (f32((w_0 + w_1) * 0.5), trainer.cpp:574-594) and the
+    replicas agree again."""
+    s2d, engs = _mesh(2, 2)
+    try:
+        w0, v0 = engs[0].read_rows(0, 0, 64)
+        rows = np.array([3, 9, 3], np.uint32)
+        delta = np.full((3, 16), 0.25, np.float64)
+        engs[0].apply_row_updates(0, rows, delta, np.array([1.0, 2.0, 3.0]))
+        s2d.run_ranks(lambda r: engs[r].sync_replicas(), 2)
+        (wa, va), (wb, vb) = engs[0].read_rows(0, 0, 64), engs[1].read_rows(0, 0, 64)
+        assert np.array_equal(wa.view(np.uint32), wb.view(np.uint32))
+        assert np.array_equal(va.view(np.uint32), vb.view(np.uint32))
+        w3 = np.float32(np.float32(w0[3] + 0.25) + 0.25)  # two updates of row 3 in call order (f64 adds)
+        want = ((w3.astype(np.float64) + w0[3].astype(np.float64)) * 0.5).astype(np.float32)
+        assert np.array_equal(wa[3].view(np.uint32), want.view(np.uint32))
+        assert va[3] == np.float32((3.0 + 0.0) * 0.5) and va[9] == np.float32(1.0)
+        untouched = [r for r in range(64) if r not in (3, 9)]
+        assert np.array_equal(wa[untouched].view(np.uint32), w0[untouched].view(np.uint32))
+    finally:
+        for e in engs:
+            e.close()
+
+
+def test_shard_write_joins_replica_sync():
+    s2d, engs = _mesh(2, 2)
+    try:
+        w0, v0 = engs[1].read_rows(1, 0, 40)
+        engs[1].write_rows(1, 10, np.ones((2, 16), np.float32), np.full(2, 4.0, np.float32))
+        s2d.run_ranks(lambda r: engs[r].sync_replicas(), 2)
+        wa, va = engs[0].read_rows(1, 0, 40)
+        wb, vb = engs[1].read_rows(1, 0, 40)
+        assert np.array_equal(wa.view(np.uint32), wb.view(np.uint32))
+        want = ((1.0 + w0[10:12].astype(np.float64)) * 0.5).astype(np.float32)
+        assert np.array_equal(wa[10:12].view(np.uint32), want.view(np.uint32))
+        assert np.all(va[10:12] == np.float32(2.0))
+    finally:
+        for e in engs:
+            e.close()
+
+
+def test_local_mesh_matches_oracle_2x1():
+    """A 2x1 row-wise mesh driven in-process: pooled outputs and shards after
+    two steps are bit-exact against the oracle."""
+    from cases import make_batch, upstream
+    from oracle import MeshSpec, MeshState, Oracle
+
+    rows = np.array([64, 40], np.uint32)
+    dims = np.array([16, 16], np.uint32)
+    s2d, engs = _mesh(2, 1)
+    try:
+        port = Oracle("port")
+        plan = np.array([[e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]] for e in engs[0].plan], np.uint32)
+        spec = MeshSpec(rows=rows, dims=dims, plan=plan, T=2, M=1, B=8, eta=0.1, c=1.0)
+        st = MeshState.init(port, spec, 5)
+        for step in range(2):
+            ins = []
+            for r in range(2):
+                rng = np.random.default_rng([step, r])
+                ln, ids = make_batch(rng, rows, 8, max_len=5)
+                ins.append((ln, ids, upstream(rng, 8, 32)))
+            want = st.step(port, [x[0] for x in ins], [x[1] for x in ins], [x[2] for x in ins], do_sync=False)
+
+            def go(r):
+                out = engs[r].forward(ins[r][0], ins[r][1])
+                engs[r].backward_update(ins[r][2])
+                return out
+
+            got = s2d.run_ranks(go, 2)
+            for r in range(2):
+                assert np.array_equal(got[r].view(np.uint32), want[r].view(np.uint32)), (step, r)
+        off = spec.woff()
+        for r in range(2):
+            for f in range(2):
+                lo, hi = engs[r].owned_range(f)
+                w, _ = engs[r].read_rows(f, lo, hi)
+                ref = st.ws[0][off[f]:off[f + 1]].reshape(int(rows[f]), 16)[lo:hi]
+                assert np.array_equal(w.view(np.uint32), ref.view(np.uint32)), (r, f)
+    finally:
+        for e in engs:
+            e.close()

@@ -36,6 +36,9 @@ CASES = [
     (4, 4, "table-wise", []),
     (2, 1, "table-wise", ["--engine-out", "--ckpt"]),
     (4, 2, "table-wise", ["--engine-out"]),
+    (4, 1, "table-wise", ["--mixed-out"]),
+    (2, 1, "row-wise", ["--mean"]),
+    (4, 2, "table-wise", ["--mean", "--engine-out"]),
     (4, 2, "row-wise", ["--bf16", "--steps", "3"]),
     (2, 1, "row-wise", ["--bf16", "--steps", "3"]),
     (2, 1, "table-wise", ["--bad-id"]),

@@ -268,3 +268,30 @@ def test_apply_row_update_port_matches_reference():
         outs.append((w, v))
     assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
     assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
+
+
+def test_mean_pooling_oracle_definition(port):
+    """The mean-pooling definition the oracle pins (s2d_oracle.c or_cfg.mean):
+    rows r0 = (1, 0), r1 = (0, 2) (test_embedding.cpp:26-86 shapes): bag
+    [0, 1] -> f32((1 + 0, 0 + 2) * (1/2)) = (0.5, 1); [1] -> (0, 2); [] -> 0.
+    SGD with eta = 1, B = 1: the bag's gradient row is f32(up * (1/L)), so
+    row 0 moves by -up/2 and row 1 (in both bags) by -(up/2 + up')."""
+    from oracle import MeshSpec
+
+    spec = MeshSpec(rows=np.array([2], np.uint32), dims=np.array([4], np.uint32),
+                    plan=np.array([[0, 0, 2, 0]], np.uint32), T=1, M=1, B=3, eta=1.0, sgd=True,
+                    mean=np.array([1], np.uint8))
+    w = np.array([1, 0, 0, 0, 0, 2, 0, 0], np.float32)
+    v = np.zeros(2, np.float32)
+    lengths = np.array([2, 1, 0], np.uint32)
+    ids = np.array([0, 1, 1], np.uint32)
+    up = np.array([[3, 3, 3, 3], [1, 1, 1, 1], [9, 9, 9, 9]], np.float32)
+    pooled, _ = port.group_step(spec, [lengths], [ids], [up], w, v)
+    assert np.array_equal(pooled[0], np.array([[0.5, 1, 0, 0], [0, 2, 0, 0], [0, 0, 0, 0]], np.float32))
+    inv_b = 1.0 / 3.0  # 1 / (N * B)
+    g0 = np.float64(np.float32(3 * 0.5)) * inv_b
+    g1 = (np.float64(np.float32(3 * 0.5)) + np.float64(np.float32(1.0))) * inv_b
+    assert np.array_equal(w[:4], np.array([np.float32(1 - g0), np.float32(-g0), np.float32(-g0), np.float32(-g0)],
+                                          np.float32))
+    assert np.array_equal(w[4:], np.array([np.float32(-g1), np.float32(2 - g1), np.float32(-g1), np.float32(-g1)],
+                                          np.float32))
