@@ -295,6 +295,22 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out);
 int s2d_ctx_set_profiling(s2d_ctx* ctx, int on);
 int s2d_get_phase_times(s2d_ctx* ctx, double* ms, uint32_t* counts, uint32_t n);
 
+/* MetricsRow moment statistics (include/sparse2d/trainer.hpp:72-79,
+ * src/trainer.cpp:745-771) of this rank's MP group replica (group 0's is the
+ * reference's, which reads replicas[0]): over every row of every table,
+ * eff_lr_p50 / eff_lr_p99 = effective_lr at ascending index ceil(q*n)-1 of
+ * the per-row effective learning rates, v_mean = mean moment.  Collective
+ * over the MP group.  The percentiles are exact (radix select of the moment
+ * at the matching descending index, effective_lr is non-increasing in v);
+ * v_mean sums in a fixed blocked order (the reference's is sequential). */
+typedef struct {
+  double eff_lr_p50;
+  double eff_lr_p99;
+  double v_mean;
+  uint64_t rows;
+} s2d_metrics_row;
+int s2d_metrics(s2d_ctx* ctx, s2d_metrics_row* out);
+
 /* Number of kernels this library has launched in the process. */
 uint64_t s2d_launch_count(void);
 

@@ -265,6 +265,18 @@ class Oracle:
             raise ValueError("plan_greedy failed")
         return out[: 4 * cnt].reshape(cnt, 4)
 
+    def metrics_row(self, v: np.ndarray, eta=0.05, eps=1e-8, c=1.0) -> dict:
+        """MetricsRow moment columns (trainer.cpp:745-771) over a replica's
+        moments (port restatement)."""
+        v = np.ascontiguousarray(v, np.float32)
+        out = np.zeros(3, np.float64)
+        fn = self.lib.or_metrics_row
+        fn.argtypes = [_f32p, C.c_uint64, C.c_double, C.c_double, C.c_double, _f64p]
+        fn.restype = C.c_int
+        if fn(v, v.size, eta, eps, c, out):
+            raise ValueError("metrics_row failed")
+        return {"eff_lr_p50": out[0], "eff_lr_p99": out[1], "v_mean": out[2]}
+
     def synthetic_upstream(self, seed, step, rank, B, dims) -> np.ndarray:
         dims = np.ascontiguousarray(dims, np.uint32)
         out = np.empty(B * int(dims.sum()), np.float32)

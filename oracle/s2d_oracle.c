@@ -751,3 +751,32 @@ int or_gen_batch_ids(uint64_t seed, uint64_t step, uint32_t rank, uint32_t F, co
   free(cdf);
   return OR_OK;
 }
+
+/* ---- MetricsRow moment columns (trainer.cpp:745-771) ------------------- */
+
+static int or_cmp_f64(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+/* Over every row of the replica (v: n moments, tables in order):
+ * lrs[i] = effective_lr(v[i]); out[0] = lrs at ascending index
+ * ceil(0.5 n) - 1, out[1] = at ceil(0.99 n) - 1 (nth_element == the sorted
+ * value), out[2] = v_sum / n with v_sum the sequential f64 sum. */
+int or_metrics_row(const float* v, uint64_t n, double eta, double eps, double c, double* out) {
+  if (n == 0) return OR_EINVAL;
+  double* lrs = (double*)malloc(sizeof(double) * n);
+  if (!lrs) return OR_ENOMEM;
+  double v_sum = 0.0;
+  for (uint64_t i = 0; i < n; ++i) {
+    v_sum += (double)v[i];
+    lrs[i] = or_effective_lr((double)v[i], eta, eps, c);
+  }
+  qsort(lrs, n, sizeof(double), or_cmp_f64);
+  const uint64_t i50 = (uint64_t)ceil(0.50 * (double)n) - 1, i99 = (uint64_t)ceil(0.99 * (double)n) - 1;
+  out[0] = lrs[i50];
+  out[1] = lrs[i99];
+  out[2] = v_sum / (double)n;
+  free(lrs);
+  return OR_OK;
+}

@@ -51,6 +51,11 @@ class StepStats(C.Structure):
                 ("lookup_bytes_sent", C.c_uint64), ("grad_bytes_sent", C.c_uint64), ("host_wait_ns", C.c_uint64)]
 
 
+class MetricsRowC(C.Structure):
+    _fields_ = [("eff_lr_p50", C.c_double), ("eff_lr_p99", C.c_double), ("v_mean", C.c_double),
+                ("rows", C.c_uint64)]
+
+
 # symbol -> (restype, argtypes); the full exported surface of the header
 _P = C.c_void_p
 SIGNATURES = {
@@ -96,6 +101,7 @@ SIGNATURES = {
     "s2d_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
     "s2d_get_phase_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.c_uint32]),
     "s2d_launch_count": (C.c_uint64, []),
+    "s2d_metrics": (C.c_int, [_P, C.POINTER(MetricsRowC)]),
     "s2d_debug_read": (C.c_int, [_P, C.c_int32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
 }
 

@@ -566,6 +566,14 @@ class Sparse2DEmbedding:
                          "bytes": int(sent[kernel]), "latency_s": ms * 1e-3})
         return rows
 
+    def metrics_row(self) -> dict:
+        """MetricsRow moment columns (trainer.hpp:72-79, trainer.cpp:745-771)
+        of this rank's MP-group replica: eff_lr_p50, eff_lr_p99, v_mean over
+        every row of every table.  Collective over the MP group."""
+        m = L.MetricsRowC()
+        L.check(self.lib.s2d_metrics(self._ctx, C.byref(m)))
+        return {"eff_lr_p50": m.eff_lr_p50, "eff_lr_p99": m.eff_lr_p99, "v_mean": m.v_mean, "rows": int(m.rows)}
+
     def _owns_rows(self) -> bool:
         return any(hi > lo for lo, hi in (self.owned_range(f) for f in range(self.F)))
 

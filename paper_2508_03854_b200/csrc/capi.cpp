@@ -273,6 +273,13 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out) {
   });
 }
 
+int s2d_metrics(s2d_ctx* ctx, s2d_metrics_row* out) {
+  return guarded([&] {
+    if (!out) throw Error(S2D_EINVAL, "null output");
+    as_ctx(ctx)->metrics(out);
+  });
+}
+
 int s2d_debug_read(s2d_ctx* ctx, int32_t which, void* out, uint64_t cap, uint64_t* n) {
   return guarded([&] { as_ctx(ctx)->debug_read(which, out, cap, n); });
 }

@@ -243,6 +243,11 @@ struct StreamUpdateArgs {
 // mean-pooled tables replaced by f32(f64(up) * (1/L_bag))
 void launch_mean_prescale(const FeatDev* feats, uint32_t F, uint32_t B, uint32_t sum_dims, const uint32_t* bag_off,
                           const float* up, float* out, cudaStream_t st);
+// MetricsRow moment statistics (k_metrics.cu)
+void launch_moment_hist(const float* v, uint32_t n, int shift, uint32_t mask, uint32_t prefix, uint32_t* hist,
+                        cudaStream_t st);
+void launch_moment_sum(const float* v, uint32_t n, double* part, cudaStream_t st);
+uint32_t moment_sum_blocks();
 // device-side synthetic input (k_gen.cu): DataGenerator ids, data.cpp:85-136
 struct GenArgs {
   uint64_t seed, step;

@@ -1057,6 +1057,82 @@ void Ctx::replica_sync() {
   finish_call();
 }
 
+// ---- MetricsRow (trainer.cpp:745-771) ----------------------------------------
+
+// Collective over the MP group: the moment statistics of this group's
+// replica (group 0's is the reference's MetricsRow, which reads
+// replicas[0]).  Exact k-th largest moment by a 4-round radix select over
+// the group's shards (histograms all-gathered), then the reference's
+// effective_lr and percentile index on the host.
+void Ctx::metrics(s2d_metrics_row* out) {
+  if (!F) throw Error(S2D_EINVAL, "register tables first");
+  if (!have_opt) throw Error(S2D_EINVAL, "set_optimizer first");
+  S2D_CUDA(cudaSetDevice(device));
+  uint64_t n_total = 0;
+  for (uint32_t f = 0; f < F; ++f) n_total += tables[f].rows;
+  const uint32_t nb = moment_sum_blocks();
+  metric_buf.ensure((size_t)(N + 1) * 256 * 4 + (size_t)nb * 8 + 64);
+  uint32_t* d_hist = metric_buf.as<uint32_t>();
+  uint32_t* d_all = d_hist + 256;
+  double* d_part = reinterpret_cast<double*>(metric_buf.as<char>() + (size_t)(N + 1) * 256 * 4);
+  // v_mean: per-rank block sums in index order, gathered and added in
+  // (rank, block) order
+  launch_moment_sum(moments.as<float>(), n_slots, d_part, stream);
+  std::vector<double> parts((size_t)N * nb);
+  {
+    std::vector<double> mine(nb);
+    S2D_CUDA(cudaMemcpyAsync(mine.data(), d_part, (size_t)nb * 8, cudaMemcpyDeviceToHost, stream));
+    S2D_CUDA(cudaStreamSynchronize(stream));
+    if (N > 1)
+      mp.host_allgather(mine.data(), (size_t)nb * 8, parts.data(), stream, hbuf);
+    else
+      parts = mine;
+  }
+  double v_sum = 0.0;
+  for (double p : parts) v_sum += p;
+  // descending index k of the moments -> ascending rank n_total - 1 - k
+  auto select = [&](uint64_t asc) -> float {
+    uint32_t prefix = 0, mask = 0;
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      launch_moment_hist(moments.as<float>(), n_slots, shift, mask, prefix, d_hist, stream);
+      std::vector<uint32_t> all((size_t)N * 256);
+      if (N > 1) {
+        mp.allgather(d_hist, d_all, 256 * 4, stream);
+        S2D_CUDA(cudaMemcpyAsync(all.data(), d_all, all.size() * 4, cudaMemcpyDeviceToHost, stream));
+      } else {
+        S2D_CUDA(cudaMemcpyAsync(all.data(), d_hist, 256 * 4, cudaMemcpyDeviceToHost, stream));
+      }
+      S2D_CUDA(cudaStreamSynchronize(stream));
+      uint64_t cum = 0;
+      uint32_t digit = 255;
+      for (uint32_t d = 0; d < 256; ++d) {
+        uint64_t c = 0;
+        for (uint32_t q = 0; q < N; ++q) c += all[(size_t)q * 256 + d];
+        if (asc < cum + c) {
+          digit = d;
+          break;
+        }
+        cum += c;
+      }
+      asc -= cum;
+      prefix |= digit << shift;
+      mask |= 255u << shift;
+    }
+    float x;
+    std::memcpy(&x, &prefix, 4);
+    return x;
+  };
+  auto pct = [&](double q) {  // trainer.cpp:759-764 on the lr values
+    const uint64_t idx = (uint64_t)std::ceil(q * (double)n_total) - 1;
+    const float v = select(n_total - 1 - idx);
+    return effective_lr((double)v, opt);
+  };
+  out->eff_lr_p50 = pct(0.50);
+  out->eff_lr_p99 = pct(0.99);
+  out->v_mean = v_sum / (double)n_total;
+  out->rows = n_total;
+}
+
 // ---- debug views ------------------------------------------------------------
 
 void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {

@@ -512,3 +512,29 @@ def test_apply_row_updates_vs_oracle(port, strategy):
         gw2, gv2 = eng.read_rows(f, lo, hi)
         assert np.array_equal(bits(np.asarray(gw2).ravel()), bits(np.asarray(gw).ravel()))
         assert np.array_equal(bits(np.asarray(gv2)), bits(np.asarray(gv)))
+
+
+def test_metrics_row_vs_oracle(port):
+    """Device MetricsRow columns (eff_lr_p50 / p99 exact, v_mean within 1e-12)
+    against the oracle restatement of trainer.cpp:745-771, after AdaGrad steps
+    with hot and cold rows (many moments tie at 0)."""
+    from oracle import MeshState
+
+    rng = np.random.default_rng(8)
+    rows, dims, B = [500, 3000, 40], [16, 32, 8], 64
+    spec = _spec(rows, dims, B, eta=0.07, c=3.0)
+    eng = _engine(rows, dims, eta=0.07, c=3.0)
+    eng.init_tables(2)
+    st = MeshState.init(port, spec, 2)
+    for step in range(3):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=12)
+        up = upstream(rng, B, spec.sum_dims)
+        st.step(port, [lengths], [ids], [up], do_sync=False)
+        eng.forward(lengths, ids)
+        eng.backward_update(up)
+    got = eng.metrics_row()
+    want = port.metrics_row(st.vs[0], eta=0.07, eps=1e-8, c=3.0)
+    assert got["rows"] == sum(rows)
+    assert got["eff_lr_p50"] == want["eff_lr_p50"]
+    assert got["eff_lr_p99"] == want["eff_lr_p99"]
+    assert abs(got["v_mean"] - want["v_mean"]) <= 1e-12 * abs(want["v_mean"])

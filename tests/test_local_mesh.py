@@ -98,3 +98,38 @@ def test_local_mesh_matches_oracle_2x1():
     finally:
         for e in engs:
             e.close()
+
+
+def test_metrics_row_over_mp_group_shards():
+    """MetricsRow is collective over the MP group: a 2x1 row-wise mesh gives
+    the same statistics as the oracle on the whole replica."""
+    from cases import make_batch, upstream
+    from oracle import MeshSpec, MeshState, Oracle
+
+    rows = np.array([64, 40], np.uint32)
+    s2d, engs = _mesh(2, 1)
+    try:
+        port = Oracle("port")
+        plan = np.array([[e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]] for e in engs[0].plan], np.uint32)
+        spec = MeshSpec(rows=rows, dims=np.array([16, 16], np.uint32), plan=plan, T=2, M=1, B=8, eta=0.1, c=1.0)
+        st = MeshState.init(port, spec, 5)
+        ins = []
+        for r in range(2):
+            rng = np.random.default_rng([9, r])
+            ln, ids = make_batch(rng, rows, 8, max_len=5)
+            ins.append((ln, ids, upstream(rng, 8, 32)))
+        st.step(port, [x[0] for x in ins], [x[1] for x in ins], [x[2] for x in ins], do_sync=False)
+
+        def go(r):
+            engs[r].forward(ins[r][0], ins[r][1])
+            engs[r].backward_update(ins[r][2])
+            return engs[r].metrics_row()
+
+        got = s2d.run_ranks(go, 2)
+        want = port.metrics_row(st.vs[0], eta=0.1, eps=1e-8, c=1.0)
+        for g in got:
+            assert g["eff_lr_p50"] == want["eff_lr_p50"] and g["eff_lr_p99"] == want["eff_lr_p99"]
+            assert abs(g["v_mean"] - want["v_mean"]) <= 1e-12 * abs(want["v_mean"])
+    finally:
+        for e in engs:
+            e.close()

@@ -295,3 +295,20 @@ def test_mean_pooling_oracle_definition(port):
                                           np.float32))
     assert np.array_equal(w[4:], np.array([np.float32(-g1), np.float32(2 - g1), np.float32(-g1), np.float32(-g1)],
                                           np.float32))
+
+
+def test_metrics_row_definition(port):
+    """or_metrics_row follows make_metrics_row (trainer.cpp:745-771):
+    nth_element at ceil(q n) - 1 of the per-row effective_lr, sequential
+    v_sum / n."""
+    rng = np.random.default_rng(3)
+    v = np.concatenate([np.zeros(50, np.float32), rng.random(151).astype(np.float32) * 4])
+    m = port.metrics_row(v, eta=0.1, eps=1e-8, c=2.0)
+    lrs = np.sort(0.1 / (np.sqrt(v.astype(np.float64) / 2.0) + 1e-8))
+    n = v.size
+    assert m["eff_lr_p50"] == lrs[int(np.ceil(0.5 * n)) - 1]
+    assert m["eff_lr_p99"] == lrs[int(np.ceil(0.99 * n)) - 1]
+    acc = 0.0
+    for x in v:
+        acc += float(x)
+    assert m["v_mean"] == acc / n
