@@ -89,6 +89,18 @@ void HostBuf::ensure(size_t bytes) {
 
 HostBuf::~HostBuf() { host_free(p); }
 
+void set_max_dynamic_smem_raw(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
+  int dev = 0;
+  S2D_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first.first == kernel && e.first.second == dev && e.second >= bytes) return;
+  S2D_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done.push_back({{kernel, dev}, bytes});
+}
+
 // ---- LocalHub ---------------------------------------------------------------
 
 LocalHub::Slot& LocalHub::slot(uint64_t key) {

@@ -62,6 +62,7 @@ struct Ctx {
   cudaEvent_t ev_keys = nullptr, ev_sorted = nullptr;
   bool sort_pending = false;
   void launch_sort(cudaStream_t st);
+  uint32_t* prepare_sort(uint64_t n);
   Comm world, mp, dp;
   std::shared_ptr<LocalHub> hub;  // virtual ranks of one process (null: NCCL)
   // runs after every member destructor: the last virtual rank frees the
@@ -113,14 +114,13 @@ struct Ctx {
   DevBuf hbuf, row_upd_scratch;
   uint64_t epoch = 0;
   uint32_t engine_mask = 0;  // requesters of the current step that asked for the engine-owned output
-  DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
+  DevBuf keys_a, vals_a, keys_b, vals_b, keys_c, vals_c, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
   DevBuf sync_list, sync_lists, sync_count, sync_packed, sync_gathered, sync_tmp;
   HostBuf h_counts, h_xcnt;
   uint64_t host_wait_total_ns = 0;  // host blocked on the count read, since creation
   std::vector<uint64_t> nnz_to, nnz_from, ef_to, ef_from, send_bound, eoff_req_bound, own_eoff_bound,
       ids_base_at_owner, part_base_at_req, grad_base_at_owner;
-  bool sorted_in_b = false;
   s2d_step_stats stats{};
   bool stats_counters_valid = false;
   void refresh_stats();
