@@ -124,22 +124,12 @@ size_t scan_tmp_bytes(uint64_t n);
 void scan_count_pair(const uint32_t* in, uint32_t* out32, uint64_t* out64, uint64_t n, uint32_t F,
                      const FeatDev* feats, cudaStream_t st, void* tmp, size_t tmp_bytes);
 
-// dedup sort (k_sort.cu): stable sort of (slot, val) pairs by slot (slots
-// >= n_slots are invalid and sort last) through dense ranks of the touched
-// slots.  Input (keys, vals) is read only by the first pass; (keys_tmp,
-// vals_tmp) and (keys_tmp2, vals_tmp2) are ping-pong buffers (tmp2 may alias
-// the input); the result always lands in (keys_out, vals_out).
-size_t dedup_sort_tmp_bytes(uint64_t n, uint32_t n_slots);
-int dedup_sort_max_passes(uint64_t n, uint32_t n_slots);
-// the touched-slot bitmap inside the workspace (one bit per slot; a
-// producer of the keys -- the lookup -- may mark it and pass premarked, the
-// bitmap having been zeroed first); independent of n
-uint32_t* dedup_sort_bitmap(void* tmp);
-size_t dedup_sort_bitmap_bytes(uint32_t n_slots);
-// keys is overwritten (dense ranks); the sorted pairs land in keys_out/vals_out
-void dedup_sort(uint32_t* keys, const uint32_t* vals, uint32_t* keys_tmp, uint32_t* vals_tmp,
-                uint32_t* keys_tmp2, uint32_t* vals_tmp2, uint32_t* keys_out, uint32_t* vals_out, uint64_t n,
-                uint32_t n_slots, void* tmp, size_t tmp_bytes, bool premarked, cudaStream_t st);
+// radix sort (k_sort.cu): stable LSD sort of (key, val) pairs by the low
+// `bits` bits of key.  keys/vals ping-pong between a and b; returns true if
+// the result ended in b.
+size_t radix_tmp_bytes(uint64_t n, int bits);
+bool radix_sort_pairs(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b,
+                      uint64_t n, int bits, void* tmp, size_t tmp_bytes, cudaStream_t st);
 
 // embedding kernels (k_embed.cu)
 void launch_init_rows(void* w, int bf16, const FeatDev* feats_host, uint32_t F, uint64_t seed,
@@ -164,7 +154,6 @@ struct LookupArgs {
   int uni_rows;                // uni_d4 != 0 and weights offset = slot * dim (slot-indexed rows)
   uint32_t zero_row;           // slot index of the all-zero row after the shard (uni_rows)
   uint32_t* ticket;            // work counter of the persistent warps (zeroed per launch)
-  uint32_t* mark;              // touched-slot bitmap of the dedup sort (null: not marked here)
   uint64_t unit_rot;           // ticket t processes 32-bag unit (t + unit_rot) % units: owners
                                // start at different requesters so their NVLink stores spread out
   // non-direct: the partial of a bag of requester n goes to

@@ -502,7 +502,6 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.zero_row = n_slots;
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
-    a.mark = prepare_sort(nnz);
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     stats.nnz_owned = nnz;
     stats.entries_owned = BF;
@@ -576,7 +575,6 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     for (uint32_t n = 0; n < N; ++n) a.peer_adj[n] = (int64_t)part_base_at_req[n] - (int64_t)own_eoff_bound[n];
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
-    a.mark = prepare_sort(nnz_own);
     a.unit_rot = ((uint64_t)((local + 1) % N) * BF) / 32;  // start at the next requester
     phase_begin(kPhLookup);
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
@@ -820,29 +818,21 @@ void Ctx::read_counts() {
 
 // ---- backward + fused update ---------------------------------------------------
 
-// K3a on `st`: stable dedup sort of this rank's (slot, gradient offset)
-// pairs; the sorted pairs land in (keys_c, vals_c)
+// K3a on `st`: stable radix sort of this rank's (slot, gradient offset)
+// pairs; the sorted pairs land in (keys_c, vals_c).  (A dense-rank variant
+// -- touched-slot bitmap, 2 passes of 10 bits -- measured no faster; see
+// DESIGN.md section 5.)
 void Ctx::launch_sort(cudaStream_t st) {
   const uint64_t n = nnz_own;
   if (n == 0) return;
   keys_b.ensure(n * 4);
   vals_b.ensure(n * 4);
-  keys_c.ensure(n * 4);
-  vals_c.ensure(n * 4);
-  sort_tmp.ensure(dedup_sort_tmp_bytes(n, n_slots));
-  dedup_sort(keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_b.as<uint32_t>(), vals_b.as<uint32_t>(),
-             keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_c.as<uint32_t>(), vals_c.as<uint32_t>(), n, n_slots,
-             sort_tmp.p, sort_tmp.cap, /*premarked=*/true, st);
-}
-
-// Before the lookup that emits the sort keys: size the sort workspace for n
-// pairs and zero its touched-slot bitmap, which the lookup marks (a
-// separate marking pass measured 131 us against +15 us inside the lookup).
-uint32_t* Ctx::prepare_sort(uint64_t n) {
-  sort_tmp.ensure(dedup_sort_tmp_bytes(std::max<uint64_t>(n, 1), n_slots));
-  uint32_t* bm = dedup_sort_bitmap(sort_tmp.p);
-  launch_zero(bm, dedup_sort_bitmap_bytes(n_slots), stream);
-  return bm;
+  const int bits = std::max(1, bit_width(n_slots));
+  sort_tmp.ensure(radix_tmp_bytes(n, bits));
+  const bool in_b = radix_sort_pairs(keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_b.as<uint32_t>(),
+                                     vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, st);
+  sorted_k = in_b ? keys_b.as<uint32_t>() : keys_a.as<uint32_t>();
+  sorted_v = in_b ? vals_b.as<uint32_t>() : vals_a.as<uint32_t>();
 }
 
 void Ctx::backward_update(const float* upstream, int mem) {
@@ -920,8 +910,8 @@ void Ctx::backward_update(const float* upstream, int mem) {
     else
       launch_sort(stream);
     sort_pending = false;
-    const uint32_t* sk = keys_c.as<uint32_t>();
-    const uint32_t* sv = vals_c.as<uint32_t>();
+    const uint32_t* sk = sorted_k;
+    const uint32_t* sv = sorted_v;
     phase_begin(kPhUpdate);
     if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));
     up_wait = false;
@@ -1190,7 +1180,7 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
     }
     case 5: {
       std::vector<uint32_t> k(nnz_own);
-      const void* src = keys_c.p;
+      const void* src = sorted_k;
       if (nnz_own) S2D_CUDA(cudaMemcpy(k.data(), src, nnz_own * 4, cudaMemcpyDeviceToHost));
       std::vector<uint32_t> rows;
       for (uint64_t i = 0; i < nnz_own; ++i) {

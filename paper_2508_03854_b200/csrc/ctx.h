@@ -62,7 +62,8 @@ struct Ctx {
   cudaEvent_t ev_keys = nullptr, ev_sorted = nullptr;
   bool sort_pending = false;
   void launch_sort(cudaStream_t st);
-  uint32_t* prepare_sort(uint64_t n);
+  const uint32_t* sorted_k = nullptr;  // sorted pairs of the last launch_sort
+  const uint32_t* sorted_v = nullptr;
   Comm world, mp, dp;
   std::shared_ptr<LocalHub> hub;  // virtual ranks of one process (null: NCCL)
   // runs after every member destructor: the last virtual rank frees the
@@ -114,7 +115,7 @@ struct Ctx {
   DevBuf hbuf, row_upd_scratch;
   uint64_t epoch = 0;
   uint32_t engine_mask = 0;  // requesters of the current step that asked for the engine-owned output
-  DevBuf keys_a, vals_a, keys_b, vals_b, keys_c, vals_c, sort_tmp, scan_tmp;
+  DevBuf keys_a, vals_a, keys_b, vals_b, sort_tmp, scan_tmp;
   DevBuf uslot, useg, counters, chunk_base, chunk_seg, chunk_part;
   DevBuf sync_list, sync_lists, sync_count, sync_packed, sync_gathered, sync_tmp;
   HostBuf h_counts, h_xcnt;

@@ -28,7 +28,6 @@ constexpr int kStages = 2;
 constexpr int kRowsPerStage = 4;
 constexpr int kSlots = kStages * kRowsPerStage;
 constexpr int kBags = 32;  // bags per lookup unit (one per lane)
-constexpr uint32_t kMarkCacheL = 2048;  // per-CTA cache of slots marked in the dedup bitmap
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -162,12 +161,6 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   // this lane's column chunk of slot 0 of the warp's ring
   const uint32_t ring_s = smem_u32(smem) + warp * kSlots * kRowBytes + lane * VB;
-  // after the rings: the CTA's cache of slots marked in the sort bitmap
-  uint32_t* const mark_cache = reinterpret_cast<uint32_t*>(smem + (blockDim.x >> 5) * kSlots * kRowBytes);
-  if (a.mark) {
-    for (uint32_t i = threadIdx.x; i < kMarkCacheL; i += blockDim.x) mark_cache[i] = 0xffffffffu;
-    __syncthreads();
-  }
   const uint64_t n_bags = (uint64_t)a.n_req * a.B * a.F;
   const uint64_t n_units = (n_bags + kBags - 1) / kBags;
   const WT* __restrict__ W = reinterpret_cast<const WT*>(a.weights);
@@ -246,19 +239,8 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
       const bool ok = have && id >= lo_j && id < hi_j;
       if (have && !ok) atomicOr(a.err, kErrIdRange);
       if (a.emit_keys && have) {
-        const uint32_t sk = ok ? vb_j + (id - lo_j) : 0xffffffffu;
-        a.keys[p] = sk;
+        a.keys[p] = ok ? vb_j + (id - lo_j) : 0xffffffffu;
         a.vals[p] = (uint32_t)(oo_j >> 2);
-        // touched-slot bitmap of the dedup sort: a direct-mapped per-CTA
-        // cache keeps Zipf-hot rows' repeats on chip, the rest is a
-        // fire-and-forget atomicOr (RED) per distinct slot per CTA
-        if (a.mark && ok) {
-          uint32_t* c = mark_cache + (sk & (kMarkCacheL - 1));
-          if (*(volatile uint32_t*)c != sk) {
-            *(volatile uint32_t*)c = sk;
-            atomicOr(a.mark + (sk >> 5), 1u << (sk & 31u));
-          }
-        }
       }
       if constexpr (UNI)
         ad = ok ? vb_j + (id - lo_j) : a.zero_row;
@@ -915,7 +897,7 @@ void lookup_launch_t(const LookupArgs& a, cudaStream_t st) {
   const uint64_t n_units = ((uint64_t)a.n_req * a.B * a.F + kBags - 1) / kBags;
   const size_t per_warp = (size_t)kSlots * VPL * 32 * Row<WT>::kVecBytes;
   const uint32_t nw = warps_for(per_warp, 8);
-  const size_t smem = nw * per_warp + kMarkCacheL * 4;
+  const size_t smem = nw * per_warp;
   static int occ = 0;
   if (!occ) {
     set_smem(k_lookup_ring<WT, VPL, UNI>, smem);
