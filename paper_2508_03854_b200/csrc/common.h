@@ -247,7 +247,6 @@ struct StreamUpdateArgs {
   int sgd;
   uint32_t* err;
   uint32_t* counters;            // [0] unique rows updated, [1] rows spanning ranges
-  uint32_t* sync;                // stream_sync_words(n) flags / counters of the in-kernel partials
 };
 // mean pooling, N = 1 (k_embed.cu): out = upstream with the columns of
 // mean-pooled tables replaced by f32(f64(up) * (1/L_bag))
@@ -274,7 +273,6 @@ void launch_gen_batch(const GenArgs& a, cudaStream_t st);
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
 uint64_t stream_partial1_rows(uint64_t n);  // level-1 partial rows (part2 follows them)
 uint64_t stream_partial2_rows(uint64_t n);  // level-2 partial rows (part3 follows them)
-uint64_t stream_sync_words(uint64_t n);     // u32 sync words of the fused update
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 

@@ -916,7 +916,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
     if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));
     up_wait = false;
     counters.ensure(64);
-    chunk_part.ensure(stream_partial_bytes(n, max_dim) + stream_sync_words(n) * 4 + 64);
+    chunk_part.ensure(stream_partial_bytes(n, max_dim));
     StreamUpdateArgs ua{};
     ua.keys = sk;
     ua.vals = sv;
@@ -936,7 +936,6 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ua.part1 = chunk_part.as<double>();
     ua.part2 = chunk_part.as<double>() + nparts1 * max_dim;
     ua.part3 = ua.part2 + stream_partial2_rows(n) * max_dim;
-    ua.sync = reinterpret_cast<uint32_t*>(chunk_part.as<char>() + stream_partial_bytes(n, max_dim));
     ua.inv_batch = 1.0 / (double)((uint64_t)N * B);  // group batch (trainer.cpp:462)
     ua.eta = opt.eta;
     ua.eps = opt.eps;

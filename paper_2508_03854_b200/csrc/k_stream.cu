@@ -441,16 +441,14 @@ __device__ __forceinline__ void ring_sum(const StreamUpdateArgs& a, uint32_t lan
   cp_wait<0>();
 }
 
-// partials are written by other warps of the same launch: L2 (coherent)
-// loads, after the producer's release / the consumer's acquire
 template <int VPL>
 __device__ __forceinline__ void add_partial(const double* p, uint32_t lane, uint32_t d4, double (&acc)[VPL][4]) {
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     const uint32_t c4 = lane + v * 32;
     if (c4 < d4) {
-      const double2 x0 = __ldcg(reinterpret_cast<const double2*>(p + c4 * 4));
-      const double2 x1 = __ldcg(reinterpret_cast<const double2*>(p + c4 * 4) + 1);
+      const double2 x0 = __ldg(reinterpret_cast<const double2*>(p + c4 * 4));
+      const double2 x1 = __ldg(reinterpret_cast<const double2*>(p + c4 * 4) + 1);
       acc[v][0] += x0.x;
       acc[v][1] += x0.y;
       acc[v][2] += x1.x;
@@ -508,107 +506,62 @@ __device__ __forceinline__ void reg_sum_range(const StreamUpdateArgs& a, uint32_
   }
 }
 
-// ---- in-kernel partial sums of the ranges inside long segments -----------
-//
-// Sync words (zeroed before every launch): flag1[range], then per level-2
-// group flag2[g2] | cnt2[g2], per level-3 group flag3[g3] | cnt3[g3].
-struct SyncView {
-  uint32_t *flag1, *flag2, *cnt2, *flag3, *cnt3;
-};
-
-__device__ __forceinline__ SyncView sync_view(uint32_t* s, uint64_t n) {
-  const uint64_t u = n / kC + 2, g2 = n / ((uint64_t)kC * kP) + 2, g3 = n / ((uint64_t)kC * kP * kP) + 2;
-  SyncView v;
-  v.flag1 = s;
-  v.flag2 = s + u;
-  v.cnt2 = v.flag2 + g2;
-  v.flag3 = v.cnt2 + g2;
-  v.cnt3 = v.flag3 + g3;
-  return v;
-}
-
-__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-// one lane polls, the warp proceeds together (acquire by lane 0, then the
-// warp-synchronous barrier orders the other lanes' loads after it)
-__device__ __forceinline__ void wait_flag(const uint32_t* f, uint32_t lane) {
-  if (lane == 0)
-    while (!ld_acquire_gpu(f)) __nanosleep(100);
-  __syncwarp();
-}
-
-// the kP consecutive lower-level partials of group m, summed in order
+// level-1 partials: range k = [kC, kC+C) lying inside one segment
 template <int VPL>
-__device__ __forceinline__ void sum_group(const double* src, double* dst, uint64_t m, uint32_t max_d4, uint32_t lane,
-                                          uint32_t d4) {
-  double acc[VPL][4];
+__global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a) {
+  pdl_wait();
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t n_ranges = a.n / kC;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t k = 1 + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; k < n_ranges; k += stride) {
+    const uint64_t s = k * kC, t = s + kC;
+    const uint32_t key = __ldg(a.keys + s - 1);
+    if (key >= a.n_slots || __ldg(a.keys + t - 1) != key) continue;
+    uint64_t wofs;
+    uint32_t d4;
+    row_ref(a, key, wofs, d4);
+    double acc[VPL][4];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v)
+    for (int v = 0; v < VPL; ++v)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
-  for (uint32_t r = 0; r < kP; ++r) add_partial<VPL>(src + (m * kP + r) * (uint64_t)max_d4 * 4, lane, d4, acc);
-  store_partial<VPL>(dst + m * (uint64_t)max_d4 * 4, lane, d4, acc);
+      for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    reg_sum_range<VPL>(a, lane, s, d4, acc);
+    store_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+  }
 }
 
-// Interior range u (all kC items inside one segment that began earlier):
-// level-1 partial, published with flag1[u].  The warp that completes the
-// last level-1 partial of a level-2 group lying inside the segment sums the
-// group (level 2), and likewise for level 3 -- so no warp ever waits for
-// another to produce a partial; only segment heads wait (for partials of
-// later ranges, which the ticket order hands out to non-waiting warps).
+// level-(L+1) partials: kP consecutive level-L partials, all inside one
+// segment (level 2 over level-1 ranges, level 3 over level-2 groups), so the
+// head warp of a segment of length S adds O(S / (kC kP^2) + 2 kP) partials
 template <int VPL>
-__device__ __forceinline__ void interior_range(const StreamUpdateArgs& a, const SyncView& sv, uint64_t u, uint32_t key,
-                                               uint32_t lane) {
-  uint64_t wofs;
-  uint32_t d4;
-  row_ref(a, key, wofs, d4);
-  double acc[VPL][4];
+__global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a, const double* __restrict__ src,
+                                                        double* __restrict__ dst, uint64_t span) {
+  pdl_wait();
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint64_t n_groups = a.n / span;
+  const uint64_t stride = (uint64_t)gridDim.x * (blockDim.x >> 5);
+  for (uint64_t m = 1 + (uint64_t)blockIdx.x * (blockDim.x >> 5) + warp; m < n_groups; m += stride) {
+    const uint64_t s = m * span, t = s + span;
+    const uint32_t key = __ldg(a.keys + s - 1);
+    if (key >= a.n_slots || __ldg(a.keys + t - 1) != key) continue;
+    uint64_t wofs;
+    uint32_t d4;
+    row_ref(a, key, wofs, d4);
+    double acc[VPL][4];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v)
+    for (int v = 0; v < VPL; ++v)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
-  reg_sum_range<VPL>(a, lane, u * kC, d4, acc);
-  const uint64_t pr = (uint64_t)a.max_d4 * 4;
-  store_partial<VPL>(a.part1 + u * pr, lane, d4, acc);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release_gpu(sv.flag1 + u, 1u);
-  // level 2: group m = u / kP, if the whole group lies inside this segment
-  const uint64_t span2 = (uint64_t)kC * kP, m = u / kP;
-  if (m == 0 || (m + 1) * span2 > a.n) return;
-  if (__ldg(a.keys + m * span2 - 1) != key || __ldg(a.keys + (m + 1) * span2 - 1) != key) return;
-  uint32_t last = 0;
-  if (lane == 0) last = atomicAdd(sv.cnt2 + m, 1u) == kP - 1;
-  if (!__shfl_sync(0xffffffffu, last, 0)) return;
-  __threadfence();
-  sum_group<VPL>(a.part1, a.part2, m, a.max_d4, lane, d4);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release_gpu(sv.flag2 + m, 1u);
-  // level 3
-  const uint64_t span3 = span2 * kP, g = m / kP;
-  if (g == 0 || (g + 1) * span3 > a.n) return;
-  if (__ldg(a.keys + g * span3 - 1) != key || __ldg(a.keys + (g + 1) * span3 - 1) != key) return;
-  if (lane == 0) last = atomicAdd(sv.cnt3 + g, 1u) == kP - 1;
-  if (!__shfl_sync(0xffffffffu, last, 0)) return;
-  __threadfence();
-  sum_group<VPL>(a.part2, a.part3, g, a.max_d4, lane, d4);
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) st_release_gpu(sv.flag3 + g, 1u);
+      for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    for (uint32_t r = 0; r < kP; ++r) add_partial<VPL>(src + (m * kP + r) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+    store_partial<VPL>(dst + m * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+  }
 }
 
 // FULL: every owned row is exactly VPL*128 floats, so each lane's chunk of
 // any item's gradient row -- sentinel items keep a real row offset, items past
 // the range name row 0 -- is in bounds and the ring copies need no predicate.
 template <typename WT, int VPL, bool FULL>
-__global__ void __launch_bounds__(128, 5) k_update_ring(const StreamUpdateArgs a) {
+__global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   pdl_wait();  // persistent single wave
   pdl_trigger();
   constexpr int kWinStages = 32 / kRowsPerStage;
@@ -630,18 +583,14 @@ __global__ void __launch_bounds__(128, 5) k_update_ring(const StreamUpdateArgs a
   const uint32_t ud4 = a.uni_dim >> 2;
   WT* __restrict__ W = reinterpret_cast<WT*>(a.weights);
   const float* const Gl = a.grad + lane * 4;  // this lane's chunk of gradient row 0
-  const SyncView sv = sync_view(a.sync, a.n);
   uint32_t heads = 0, longs = 0;
 
   // persistent warps take ranges in ascending order from a ticket counter
   for (;;) {
     uint32_t t = 0;
     if (lane == 0) t = atomicAdd(&a.counters[2], 1u);
-    const uint64_t tk = __shfl_sync(0xffffffffu, t, 0);
-    if (tk >= n_units) break;
-    // descending: the interior ranges of a long segment are taken before its
-    // head range, so a head rarely waits for its partials
-    const uint64_t u = n_units - 1 - tk;
+    const uint64_t u = __shfl_sync(0xffffffffu, t, 0);
+    if (u >= n_units) break;
     const uint64_t ra = u * kC, re = (ra + kC < n) ? ra + kC : n;
     {  // stage the range's keys and row offsets: one round trip per range
       const uint32_t m = (uint32_t)(re - ra);
@@ -658,13 +607,9 @@ __global__ void __launch_bounds__(128, 5) k_update_ring(const StreamUpdateArgs a
       }
       cp_commit();
     }
-    const uint32_t key_before = __shfl_sync(0xffffffffu, (lane == 0 && ra > 0) ? __ldg(a.keys + ra - 1) : kNone, 0);
+    const uint32_t key_before = (lane == 0 && ra > 0) ? __ldg(a.keys + ra - 1) : kNone;
     cp_wait<0>();
     __syncwarp();
-    if (re - ra == kC && key_before < a.n_slots && ukeys[kC - 1] == key_before) {
-      interior_range<VPL>(a, sv, u, key_before, lane);  // no head here: a partial for the head's warp
-      continue;
-    }
     // first segment head in [ra, re)
     uint64_t h = ~0ull;
     for (uint64_t c = ra; c < re; c += 32) {
@@ -907,17 +852,14 @@ __global__ void __launch_bounds__(128, 5) k_update_ring(const StreamUpdateArgs a
           break;
         }
       }
-      while (k < kend) {  // the partials are produced concurrently by other warps: wait for each
+      while (k < kend) {
         if (k % (kP * kP) == 0 && k + kP * kP <= kend) {
-          wait_flag(sv.flag3 + k / (kP * kP), lane);
           add_partial<VPL>(a.part3 + (k / (kP * kP)) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
           k += kP * kP;
         } else if (k % kP == 0 && k + kP <= kend) {
-          wait_flag(sv.flag2 + k / kP, lane);
           add_partial<VPL>(a.part2 + (k / kP) * (uint64_t)a.max_d4 * 4, lane, d4, acc);
           k += kP;
         } else {
-          wait_flag(sv.flag1 + k, lane);
           add_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
           k += 1;
         }
@@ -985,7 +927,13 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
     init = true;
   }
   const bool full = a.uni_dim == 128u * VPL;
-  launch_zero(a.sync, stream_sync_words(a.n) * 4, st);  // flags / counters of the in-kernel partials
+  if (a.n >= 2 * kC) pdl_launch(k_range_partials<VPL>, dim3(grid_units(a.n / kC, 8, 148 * 16)), dim3(256), 0, st, a);
+  if (a.n >= 2ull * kC * kP)
+    pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP), 8, 148 * 8)), dim3(256), 0, st, a,
+               static_cast<const double*>(a.part1), a.part2, (uint64_t)kC * kP);
+  if (a.n >= 2ull * kC * kP * kP)
+    pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP * kP), 8, 148 * 8)), dim3(256), 0, st, a,
+               static_cast<const double*>(a.part2), a.part3, (uint64_t)kC * kP * kP);
   static int occ[2] = {0, 0};  // per variant: their register counts differ
   if (!occ[full]) {
     if (full)
@@ -1004,10 +952,6 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
-
-uint64_t stream_sync_words(uint64_t n) {
-  return (n / kC + 2) + 2 * (n / ((uint64_t)kC * kP) + 2) + 2 * (n / ((uint64_t)kC * kP * kP) + 2);
-}
 
 uint64_t stream_partial1_rows(uint64_t n) { return n / kC + 2; }
 uint64_t stream_partial2_rows(uint64_t n) { return n / ((uint64_t)kC * kP) + 2; }
