@@ -209,6 +209,11 @@ int s2d_shard_write(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_
                     const float* w, const float* v);
 int s2d_shard_read(s2d_ctx* ctx, uint32_t table, uint32_t row_lo, uint32_t row_hi, float* w,
                    float* v);
+/* Rows of `table` by global id (each owned by this rank, any order, repeats
+ * allowed): w n x dim fp32 (bf16 shards widened exactly), v n fp32; either
+ * may be NULL.  The row-access half of EmbeddingTable::row()
+ * (include/sparse2d/embedding.hpp:19-22) for scattered rows. */
+int s2d_shard_gather(s2d_ctx* ctx, uint32_t table, uint32_t n_rows, const uint32_t* rows, float* w, float* v);
 /* apply_row_update (src/embedding.cpp:108-129) for n_rows rows of `table`
  * (global row ids owned by this rank): w[row][j] = f32(f64(w) + delta[i][j])
  * (bf16 tables: one RNE rounding of the f64 sum), v[row] = f32(new_moment[i]).
@@ -328,9 +333,16 @@ int s2d_adagrad_rows(const s2d_optimizer_config* cfg, uint32_t n_rows, uint32_t 
  *        3 gradient rows received from the requesters, concatenated by requester, f32,
  *        4 owner mask per local bag u32 [B*F],
  *        5 unique rows updated (global row ids, ascending by (table,row)) u32,
- *        6 engine-owned pooled output [B][sum dims] f32.
+ *        6 engine-owned pooled output [B][sum dims] f32,
+ *        8 table id of each row of view 5 u32,
+ *        7 f64 gradient of every row of the last update, rows as in view 5,
+ *          max dim columns (needs s2d_ctx_set_debug_grad(ctx, 1) before the
+ *          backward; aggregate_group_gradient's output, optimizer.cpp:25-59).
  * Copies min(cap, size) elements; *n = size. */
 int s2d_debug_read(s2d_ctx* ctx, int32_t which, void* out, uint64_t cap, uint64_t* n);
+/* on = 1: every backward also records the f64 row gradients (debug view 7;
+ * one extra scan and a host read of the row count per step). */
+int s2d_ctx_set_debug_grad(s2d_ctx* ctx, int on);
 
 #ifdef __cplusplus
 }

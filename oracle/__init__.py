@@ -188,6 +188,36 @@ class Oracle:
                 raise ValueError(self.lib.ref_last_error().decode())
         return out.reshape(hi - lo, dim)
 
+    def init_rows_list(self, table_id, rows, dim, seed) -> np.ndarray:
+        """init_table rows for a list of row ids (port), n x dim."""
+        rows = np.ascontiguousarray(rows, np.uint32)
+        out = np.empty((rows.size, dim), np.float32)
+        fn = self.lib.or_init_rows_list
+        fn.argtypes = [C.c_uint32, _u32p, C.c_uint64, C.c_uint32, C.c_uint64, _f32p]
+        fn(table_id, rows, rows.size, dim, seed, out)
+        return out
+
+    def row_gradients(self, rows, dims, B, lengths, ids, upstream):
+        """(keys, g): every touched (table, row) of one N = 1 step in
+        ascending (table, row) order (key = table << 32 | row) and its f64
+        gradient (item-order sum x 1/B, optimizer.cpp:25-59), zero-padded to
+        max(dims) columns (port)."""
+        rows = np.ascontiguousarray(rows, np.uint32)
+        dims = np.ascontiguousarray(dims, np.uint32)
+        lengths = np.ascontiguousarray(lengths, np.uint32)
+        ids = np.ascontiguousarray(ids, np.uint32)
+        upstream = np.ascontiguousarray(upstream, np.float32)
+        cap = int(min(ids.size, int(rows.astype(np.uint64).sum()))) + 1
+        keys = np.zeros(cap, np.uint64)
+        g = np.zeros((cap, int(dims.max())), np.float64)
+        fn = self.lib.or_row_gradients
+        fn.argtypes = [C.c_uint32, _u32p, _u32p, C.c_uint32, _u32p, _u32p, _f32p, C.c_uint64, _u64p, _f64p]
+        fn.restype = C.c_int64
+        u = fn(len(rows), rows, dims, B, lengths, ids, upstream, cap, keys, g)
+        if u < 0:
+            raise RuntimeError("row_gradients capacity")
+        return keys[:u], g[:u]
+
     def init_replica(self, spec: MeshSpec, seed: int):
         w = np.empty(spec.replica_floats(), np.float32)
         woff = spec.woff()

@@ -71,6 +71,12 @@ void or_init_rows(uint32_t table_id, uint32_t row_lo, uint32_t row_hi, uint32_t 
   }
 }
 
+/* init_table rows for an arbitrary list of row ids (out: n x dim), for
+ * tests that compact a big table to the rows a step touches. */
+void or_init_rows_list(uint32_t table_id, const uint32_t* rows, uint64_t n, uint32_t dim, uint64_t seed, float* out) {
+  for (uint64_t i = 0; i < n; ++i) or_init_rows(table_id, rows[i], rows[i] + 1, dim, seed, out + i * dim);
+}
+
 /* ---- optimizer.cpp:61-90 ------------------------------------------------ */
 
 double or_effective_lr(double v, double eta, double eps, double c) {
@@ -779,4 +785,76 @@ int or_metrics_row(const float* v, uint64_t n, double eta, double eps, double c,
   out[2] = v_sum / (double)n;
   free(lrs);
   return OR_OK;
+}
+
+/* The f64 row gradients of one rank's step at N = 1 (aggregate_group_gradient,
+ * optimizer.cpp:25-59; owner_update, trainer.cpp:459-505): for every touched
+ * (table, row) in ascending (table, row) order, g_j = (sum over the row's ids
+ * in item order of f64(up[s][coff_f + j])) * (1.0 / B).  rows_out[u] =
+ * (table << 32 | row); g_out: u x max_dim (row-major, zero-padded). Returns
+ * the number of touched rows (or < 0 if a capacity is exceeded). */
+int64_t or_row_gradients(uint32_t F, const uint32_t* rows, const uint32_t* dims, uint32_t B, const uint32_t* lengths,
+                         const uint32_t* ids, const float* upstream, uint64_t cap, uint64_t* rows_out,
+                         double* g_out) {
+  uint32_t sum_dims = 0, max_dim = 0;
+  for (uint32_t f = 0; f < F; ++f) {
+    sum_dims += dims[f];
+    if (dims[f] > max_dim) max_dim = dims[f];
+  }
+  uint32_t* coff = (uint32_t*)malloc(sizeof(uint32_t) * (F + 1));
+  coff[0] = 0;
+  for (uint32_t f = 0; f < F; ++f) coff[f + 1] = coff[f] + dims[f];
+  const uint64_t BF = (uint64_t)B * F;
+  uint64_t nnz = 0;
+  for (uint64_t b = 0; b < BF; ++b) nnz += lengths[b];
+  /* per table: counting sort of items by row (stable) */
+  uint64_t* item_bag = (uint64_t*)malloc(sizeof(uint64_t) * (nnz + 1));
+  uint64_t* item_table_off = (uint64_t*)calloc(F + 1, sizeof(uint64_t));
+  {
+    uint64_t k = 0;
+    for (uint64_t b = 0; b < BF; ++b)
+      for (uint32_t q = 0; q < lengths[b]; ++q) item_bag[k++] = b;
+  }
+  int64_t u = 0;
+  const double inv_b = 1.0 / (double)B;
+  for (uint32_t f = 0; f < F && u >= 0; ++f) {
+    const uint32_t R = rows[f], D = dims[f];
+    uint64_t* cnt = (uint64_t*)calloc((size_t)R + 1, sizeof(uint64_t));
+    uint64_t nf = 0;
+    for (uint64_t i = 0; i < nnz; ++i)
+      if (item_bag[i] % F == f) {
+        cnt[ids[i] + 1]++;
+        ++nf;
+      }
+    for (uint32_t r = 0; r < R; ++r) cnt[r + 1] += cnt[r];
+    uint64_t* order = (uint64_t*)malloc(sizeof(uint64_t) * (nf + 1));
+    uint64_t* fill = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)R + 1));
+    memcpy(fill, cnt, sizeof(uint64_t) * ((size_t)R + 1));
+    for (uint64_t i = 0; i < nnz; ++i)
+      if (item_bag[i] % F == f) order[fill[ids[i]]++] = i;
+    for (uint32_t r = 0; r < R; ++r) {
+      if (cnt[r] == cnt[r + 1]) continue;
+      if ((uint64_t)u >= cap) {
+        u = -1;
+        break;
+      }
+      double* g = g_out + (uint64_t)u * max_dim;
+      for (uint32_t j = 0; j < max_dim; ++j) g[j] = 0.0;
+      for (uint64_t q = cnt[r]; q < cnt[r + 1]; ++q) {
+        const uint64_t b = item_bag[order[q]];
+        const float* up = upstream + (b / F) * sum_dims + coff[f];
+        for (uint32_t j = 0; j < D; ++j) g[j] += (double)up[j];
+      }
+      for (uint32_t j = 0; j < D; ++j) g[j] *= inv_b;
+      rows_out[u] = ((uint64_t)f << 32) | r;
+      ++u;
+    }
+    free(order);
+    free(fill);
+    free(cnt);
+  }
+  free(item_bag);
+  free(item_table_off);
+  free(coff);
+  return u;
 }

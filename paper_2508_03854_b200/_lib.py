@@ -102,6 +102,8 @@ SIGNATURES = {
     "s2d_get_phase_times": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_uint32), C.c_uint32]),
     "s2d_launch_count": (C.c_uint64, []),
     "s2d_metrics": (C.c_int, [_P, C.POINTER(MetricsRowC)]),
+    "s2d_shard_gather": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P]),
+    "s2d_ctx_set_debug_grad": (C.c_int, [_P, C.c_int]),
     "s2d_debug_read": (C.c_int, [_P, C.c_int32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
 }
 

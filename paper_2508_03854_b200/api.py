@@ -426,6 +426,19 @@ class Sparse2DEmbedding:
         L.check(self.lib.s2d_shard_read(self._ctx, table, lo, hi, w.ctypes.data, v.ctypes.data))
         return w, v
 
+    def gather_rows(self, table: int, rows):
+        """Weights (n x dim fp32) and moments of owned rows by global id."""
+        r = np.ascontiguousarray(rows, np.uint32).ravel()
+        d = int(self.dims[table]) if 0 <= table < self.F else 0
+        w = np.zeros((r.size, d), np.float32)
+        v = np.zeros(r.size, np.float32)
+        L.check(self.lib.s2d_shard_gather(self._ctx, table, r.size, r.ctypes.data, w.ctypes.data, v.ctypes.data))
+        return w, v
+
+    def set_debug_grad(self, on: bool):
+        """Record each backward's f64 row gradients (debug(7))."""
+        L.check(self.lib.s2d_ctx_set_debug_grad(self._ctx, 1 if on else 0))
+
     def write_rows(self, table: int, lo: int, w=None, v=None):
         n = len(w) if w is not None else len(v)
         wa = None if w is None else np.ascontiguousarray(w, np.float32)
@@ -581,7 +594,7 @@ class Sparse2DEmbedding:
         """Wire buffers of the last step (see s2d_debug_read)."""
         n = C.c_uint64(0)
         L.check(self.lib.s2d_debug_read(self._ctx, which, None, 0, C.byref(n)))
-        dt = np.float32 if which in (2, 3, 6) else np.uint32
+        dt = np.float32 if which in (2, 3, 6) else (np.float64 if which == 7 else np.uint32)
         out = np.zeros(n.value, dt)
         L.check(self.lib.s2d_debug_read(self._ctx, which, out.ctypes.data, n.value, C.byref(n)))
         return out

@@ -273,6 +273,14 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out) {
   });
 }
 
+int s2d_shard_gather(s2d_ctx* ctx, uint32_t table, uint32_t n_rows, const uint32_t* rows, float* w, float* v) {
+  return guarded([&] { as_ctx(ctx)->gather_rows(table, n_rows, rows, w, v); });
+}
+
+int s2d_ctx_set_debug_grad(s2d_ctx* ctx, int on) {
+  return guarded([&] { as_ctx(ctx)->debug_grad = on != 0; });
+}
+
 int s2d_metrics(s2d_ctx* ctx, s2d_metrics_row* out) {
   return guarded([&] {
     if (!out) throw Error(S2D_EINVAL, "null output");

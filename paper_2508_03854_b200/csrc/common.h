@@ -247,6 +247,8 @@ struct StreamUpdateArgs {
   int sgd;
   uint32_t* err;
   uint32_t* counters;            // [0] unique rows updated, [1] rows spanning ranges
+  double* grad_dbg;              // debug: row gradients [U][max_dim] at head ordinals (null: off)
+  const uint32_t* head_ord;      // debug: heads before each sorted position (scan_heads_u32)
 };
 // mean pooling, N = 1 (k_embed.cu): out = upstream with the columns of
 // mean-pooled tables replaced by f32(f64(up) * (1/L_bag))
@@ -280,6 +282,10 @@ void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 void launch_apply_rows(void* w, bool bf16, float* v, const uint32_t* order, const uint32_t* seg,
                        const uint32_t* seg_row, const double* delta, const double* moment, uint32_t nseg,
                        uint32_t dim, uint8_t* dirty, cudaStream_t st);
+// gather rows of one table into f32 rows (fp32 or bf16 storage): out[i] =
+// row rows_local[i] of the shard (local row index), v_out[i] its moment
+void launch_gather_rows(const void* w, int bf16, const float* v, const uint32_t* rows_local, uint32_t n, uint32_t dim,
+                        float* w_out, float* v_out, cudaStream_t st);
 void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32_t n, uint32_t dim,
                          double eta, double eps, double c, int sgd, uint32_t* err, cudaStream_t st);
 

@@ -397,6 +397,36 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
   S2D_CUDA(cudaStreamSynchronize(stream));
 }
 
+// Rows `rows` (global ids of `table`, owned here) -> f32 weights + moments
+// (bf16 widened exactly); S2D_ERANGE for a row outside the owned range.
+void Ctx::gather_rows(uint32_t table, uint32_t n, const uint32_t* rows, float* w, float* v) {
+  if (table >= F) throw Error(S2D_EINVAL, "table out of range");
+  if (!n) return;
+  if (!rows) throw Error(S2D_EINVAL, "null rows");
+  const FeatDev& fd = feats[table];
+  std::vector<uint32_t> loc(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (rows[i] < fd.lo || rows[i] >= fd.hi)
+      throw Error(S2D_ERANGE, "row " + std::to_string(rows[i]) + " outside owned range [" + std::to_string(fd.lo) +
+                                  "," + std::to_string(fd.hi) + ")");
+    loc[i] = rows[i] - fd.lo;
+  }
+  S2D_CUDA(cudaSetDevice(device));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  const size_t bw = (size_t)n * fd.dim * 4, bv = (size_t)n * 4;
+  gather_scratch.ensure(bw + bv + (size_t)n * 4 + 64);
+  char* d = gather_scratch.as<char>();
+  float* dw = reinterpret_cast<float*>(d);
+  float* dv = reinterpret_cast<float*>(d + bw);
+  uint32_t* dr = reinterpret_cast<uint32_t*>(d + bw + bv);
+  S2D_CUDA(cudaMemcpy(dr, loc.data(), (size_t)n * 4, cudaMemcpyHostToDevice));
+  const void* wb = bf16 ? (const void*)(weights.as<uint16_t>() + fd.wbase) : (const void*)(weights.as<float>() + fd.wbase);
+  launch_gather_rows(wb, bf16, moments.as<float>() + fd.vbase, dr, n, fd.dim, dw, dv, stream);
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  if (w) S2D_CUDA(cudaMemcpy(w, dw, bw, cudaMemcpyDeviceToHost));
+  if (v) S2D_CUDA(cudaMemcpy(v, dv, bv, cudaMemcpyDeviceToHost));
+}
+
 void Ctx::check_faults() {
   const uint32_t e = *err_host.as<uint32_t>();
   if (!e) return;
@@ -949,6 +979,19 @@ void Ctx::backward_update(const float* upstream, int mem) {
     ua.sgd = opt.variant == S2D_SGD;
     ua.err = err.as<uint32_t>();
     ua.counters = counters.as<uint32_t>();
+    if (debug_grad) {  // debug view of the row gradients (s2d_debug_read 7): head ordinals, one host read of U
+      dbg_head.ensure((n + 1) * 4);
+      scan_tmp.ensure(scan_tmp_bytes(n + 1));
+      scan_heads_u32(sk, dbg_head.as<uint32_t>(), n, n_slots, stream, scan_tmp.p, scan_tmp.cap);
+      uint32_t U = 0;
+      S2D_CUDA(cudaMemcpyAsync(&U, dbg_head.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, stream));
+      S2D_CUDA(cudaStreamSynchronize(stream));
+      dbg_rows = U;
+      dbg_grad.ensure(std::max<uint64_t>(U, 1) * max_dim * 8);
+      S2D_CUDA(cudaMemsetAsync(dbg_grad.p, 0, std::max<uint64_t>(U, 1) * max_dim * 8, stream));
+      ua.grad_dbg = dbg_grad.as<double>();
+      ua.head_ord = dbg_head.as<uint32_t>();
+    }
     launch_update_stream(ua, bf16, stream);
     uniq = 1;
   }
@@ -1178,7 +1221,8 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
       if (out) std::memcpy(out, mask.data(), std::min(cap, BF) * 4);
       break;
     }
-    case 5: {
+    case 5:
+    case 8: {  // unique rows updated (5: global row ids, 8: their table ids)
       std::vector<uint32_t> k(nnz_own);
       const void* src = sorted_k;
       if (nnz_own) S2D_CUDA(cudaMemcpy(k.data(), src, nnz_own * 4, cudaMemcpyDeviceToHost));
@@ -1188,7 +1232,7 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
         if (i && k[i] == k[i - 1]) continue;
         const size_t j = std::upper_bound(vbase_sorted.begin(), vbase_sorted.end() - 1, k[i]) - vbase_sorted.begin() - 1;
         const FeatDev& fd = feats[feat_of_vbase[j]];
-        rows.push_back(k[i] - fd.vbase + fd.lo);
+        rows.push_back(which == 5 ? k[i] - fd.vbase + fd.lo : feat_of_vbase[j]);
       }
       *n = rows.size();
       if (out) std::memcpy(out, rows.data(), std::min<uint64_t>(cap, rows.size()) * 4);
@@ -1196,6 +1240,9 @@ void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
     }
     case 6:  // engine-owned pooled output of the last forward
       copy(pooled_buffer(), pooled_buffer() ? (uint64_t)B * sum_dims : 0, 4);
+      break;
+    case 7:  // f64 row gradients of the last update (debug_grad on), rows as in view 5, max_dim columns
+      copy(dbg_grad.p, debug_grad ? dbg_rows * max_dim : 0, 8);
       break;
     default:
       throw Error(S2D_EINVAL, "unknown debug buffer");

@@ -164,6 +164,10 @@ struct Ctx {
   void gen_batch(uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, const double* zipf,
                  const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int mem);
   void debug_read(int which, void* out, uint64_t cap, uint64_t* n);
+  void gather_rows(uint32_t table, uint32_t n, const uint32_t* rows, float* w, float* v);
+  DevBuf gather_scratch, dbg_head, dbg_grad;
+  bool debug_grad = false;
+  uint64_t dbg_rows = 0;
   void metrics(s2d_metrics_row* out);
   DevBuf metric_buf;
 

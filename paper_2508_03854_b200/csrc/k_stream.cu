@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
     uint32_t cur = kNone, d4 = 0;
-    uint64_t wofs = 0;
+    uint64_t wofs = 0, cur_pos = 0;
     typename Row<WT>::T wraw[VPL];  // weight row of `cur` (raw storage type)
     float vold = 0.f;
     bool stop = false;
@@ -723,6 +723,15 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       for (int v = 0; v < VPL; ++v)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[v][j] = acc[v][j] * a.inv_batch;  // g (optimizer.cpp:55)
+      if (a.grad_dbg) {  // debug view: the row's f64 gradient at its head ordinal
+        double* gd = a.grad_dbg + (uint64_t)__ldg(a.head_ord + cur_pos) * a.max_d4 * 4;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (lane + v * 32 < d4) {
+            reinterpret_cast<double2*>(gd + (lane + v * 32) * 4)[0] = make_double2(acc[v][0], acc[v][1]);
+            reinterpret_cast<double2*>(gd + (lane + v * 32) * 4)[1] = make_double2(acc[v][2], acc[v][3]);
+          }
+      }
       bool finite;
       double lr = a.eta;
       if (!a.sgd) {
@@ -811,6 +820,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
             if (cur != kNone) flush();
             // segment head: load its (L2-warm) weight row and moment
             cur = __shfl_sync(0xffffffffu, wc_.key, i);
+            cur_pos = h + (uint64_t)s * kRowsPerStage + r;
             if constexpr (FULL) {
               wofs = (uint64_t)cur * (VPL * 128);
               d4 = VPL * 32;

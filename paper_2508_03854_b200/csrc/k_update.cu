@@ -139,4 +139,31 @@ void launch_apply_rows(void* w, bool bf16, float* v, const uint32_t* order, cons
   S2D_LAUNCH_CHECK();
 }
 
+namespace {
+template <typename W>
+__global__ void __launch_bounds__(256) k_gather_rows(const W* __restrict__ w, const float* __restrict__ v,
+                                                     const uint32_t* __restrict__ rows, uint32_t n, uint32_t dim,
+                                                     float* __restrict__ w_out, float* __restrict__ v_out) {
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += warps) {
+    const uint64_t r = rows[i];
+    for (uint32_t c = lane; c < dim; c += 32) w_out[(uint64_t)i * dim + c] = (float)w[r * dim + c];
+    if (lane == 0) v_out[i] = v[r];
+  }
+}
+}  // namespace
+
+void launch_gather_rows(const void* w, int bf16, const float* v, const uint32_t* rows_local, uint32_t n, uint32_t dim,
+                        float* w_out, float* v_out, cudaStream_t st) {
+  if (!n) return;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 7) / 8, 148ull * 8));
+  if (bf16)
+    k_gather_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(w), v, rows_local, n, dim,
+                                                       w_out, v_out);
+  else
+    k_gather_rows<float><<<grid, 256, 0, st>>>(static_cast<const float*>(w), v, rows_local, n, dim, w_out, v_out);
+  S2D_LAUNCH_CHECK();
+}
+
 }  // namespace s2d
