@@ -445,6 +445,63 @@ class Oracle:
                                             _ptr_array(vs), _ptr_array(dirties))
 
 
+class RefTrainerOpts(C.Structure):
+    """TrainerOptions subset (trainer.hpp:47-70) of ref_harness.cpp."""
+
+    _fields_ = [("T", C.c_uint32), ("M", C.c_uint32), ("F", C.c_uint32), ("rows", C.c_uint32), ("dim", C.c_uint32),
+                ("dense_hidden", C.c_uint32), ("over_hidden", C.c_uint32), ("dense_dim", C.c_uint32),
+                ("ids_per_sample", C.c_uint32), ("B", C.c_uint32), ("strategy", C.c_int32), ("zipf", C.c_double),
+                ("eta", C.c_double), ("eps", C.c_double), ("c", C.c_double), ("sgd", C.c_int32),
+                ("sync_interval", C.c_uint32), ("data_seed", C.c_uint64), ("init_seed", C.c_uint64),
+                ("eval_seed", C.c_uint64), ("steps", C.c_uint32)]
+
+
+def trainer_options(T, M, F=3, rows=64, dim=8, B=4, L=3, steps=4, strategy="row-wise", zipf=1.0, eta=0.1, c=None,
+                    sgd=False, sync_interval=1, dense_hidden=6, over_hidden=10, dense_dim=4, seeds=(1, 2, 3)):
+    return RefTrainerOpts(T, M, F, rows, dim, dense_hidden, over_hidden, dense_dim, L, B,
+                          1 if strategy == "row-wise" else 0, zipf, eta, 1e-8, float(M if c is None else c),
+                          1 if sgd else 0, sync_interval, seeds[0], seeds[1], seeds[2], steps)
+
+
+def reference_trainer(o: RefTrainerOpts):
+    """The REAL reference Trainer (trainer.cpp, compiled into oracle/_ref):
+    Trainer(opts).step_n(steps).  Returns (ws[g], vs[g], plan [E,4])."""
+    lib = C.CDLL(REF_SO)
+    fn = lib.ref_trainer_run
+    fn.argtypes = [C.POINTER(RefTrainerOpts), C.c_void_p, C.c_void_p, _u32p, C.POINTER(C.c_uint32)]
+    fn.restype = C.c_int
+    ws = [np.zeros(o.F * o.rows * o.dim, np.float32) for _ in range(o.M)]
+    vs = [np.zeros(o.F * o.rows, np.float32) for _ in range(o.M)]
+    plan = np.zeros(4 * o.F * (o.T // o.M), np.uint32)
+    n = C.c_uint32(0)
+    if fn(C.byref(o), _ptr_array(ws), _ptr_array(vs), plan, C.byref(n)):
+        lib.ref_last_error.restype = C.c_char_p
+        raise RuntimeError(lib.ref_last_error().decode())
+    return ws, vs, plan[: 4 * n.value].reshape(-1, 4)
+
+
+def restated_trainer(o: RefTrainerOpts):
+    """The same loop composed from the reference's public API
+    (ref_harness.cpp ref_restated_run), recording every step's per-rank
+    embedding-path inputs: (ws, vs, lengths[step][rank], ids[step][rank],
+    upstream[step][rank], pooled[step][rank])."""
+    lib = C.CDLL(REF_SO)
+    fn = lib.ref_restated_run
+    fn.argtypes = [C.POINTER(RefTrainerOpts), _u32p, _u32p, _f32p, _f32p, C.c_void_p, C.c_void_p]
+    fn.restype = C.c_int
+    S, T, BF = o.steps, o.T, o.B * o.F
+    ln = np.zeros((S, T, BF), np.uint32)
+    ids = np.zeros((S, T, BF * o.ids_per_sample), np.uint32)
+    up = np.zeros((S, T, o.B, o.F * o.dim), np.float32)
+    pooled = np.zeros((S, T, o.B, o.F * o.dim), np.float32)
+    ws = [np.zeros(o.F * o.rows * o.dim, np.float32) for _ in range(o.M)]
+    vs = [np.zeros(o.F * o.rows, np.float32) for _ in range(o.M)]
+    if fn(C.byref(o), ln, ids, up, pooled, _ptr_array(ws), _ptr_array(vs)):
+        lib.ref_last_error.restype = C.c_char_p
+        raise RuntimeError(lib.ref_last_error().decode())
+    return ws, vs, ln, ids, up, pooled
+
+
 @dataclass
 class MeshState:
     """Full-replica state of every DP group, as the reference keeps it

@@ -23,9 +23,11 @@
 
 #include "sparse2d/data.hpp"
 #include "sparse2d/embedding.hpp"
+#include "sparse2d/model.hpp"
 #include "sparse2d/optimizer.hpp"
 #include "sparse2d/planner.hpp"
 #include "sparse2d/topology.hpp"
+#include "sparse2d/trainer.hpp"
 
 using namespace sparse2d;
 
@@ -326,6 +328,7 @@ int ref_group_step(uint32_t F, uint32_t N, uint32_t B, const uint32_t* rows, con
           for (uint32_t j = 0; j < D; ++j) out[j] = (float)pool[j];
         }
     });
+    if (!upstream) return 0;  // forward only (the pooled rows, replica untouched)
     // grad payloads (trainer.cpp:440-457) and owner_update (459-505) with
     // aggregate_group_gradient + adagrad_row_step / sgd_row_step.
     // Per (owner, table) work items, static chunking.
@@ -457,6 +460,237 @@ int ref_load_checkpoint(const char* path, uint32_t F, const uint32_t* rows, cons
       std::copy(t.moments.begin(), t.moments.end(), v + voff);
       woff += (size_t)rows[f] * dims[f];
       voff += rows[f];
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// ---- the real Trainer, and the step restated on the public API --------------
+
+// TrainerOptions subset (include/sparse2d/trainer.hpp:47-70) the pin needs.
+struct RefTrainerOpts {
+  uint32_t T, M, F, rows, dim, dense_hidden, over_hidden, dense_dim, ids_per_sample, B;
+  int32_t strategy;  // 0 table-wise, 1 row-wise
+  double zipf, eta, eps, c;
+  int32_t sgd;
+  uint32_t sync_interval;
+  uint64_t data_seed, init_seed, eval_seed;
+  uint32_t steps;
+};
+
+static TrainerOptions make_options(const RefTrainerOpts& o) {
+  TrainerOptions t;
+  t.topo = Topology(o.T, o.M);
+  t.model.num_tables = o.F;
+  t.model.rows_per_table = o.rows;
+  t.model.dim = o.dim;
+  t.model.dense_hidden = o.dense_hidden;
+  t.model.over_hidden = o.over_hidden;
+  t.data.dense_dim = o.dense_dim;
+  t.opt = OptimizerConfig{o.eta, o.eps, o.c, o.sgd ? OptimizerVariant::Sgd : OptimizerVariant::RowWiseAdagrad};
+  t.strategy = o.strategy ? ShardingStrategy::RowWise : ShardingStrategy::TableWise;
+  t.zipf_exponent = o.zipf;
+  t.ids_per_sample = o.ids_per_sample;
+  t.per_rank_batch = o.B;
+  t.steps = o.steps;
+  t.sync_interval = o.sync_interval;
+  t.data_seed = o.data_seed;
+  t.init_seed = o.init_seed;
+  t.eval_seed = o.eval_seed;
+  t.eval_samples = 512;
+  t.threads = 1;
+  return t;
+}
+
+// Trainer(opts).step_n(steps) (trainer.hpp:106-132); replica_tables(g) into
+// w_out[g] (F*rows*dim) / v_out[g] (F*rows); the plan into plan_out (4 u32
+// per entry, *n_plan entries, cap >= F*N).
+int ref_trainer_run(const RefTrainerOpts* o, float* const* w_out, float* const* v_out, uint32_t* plan_out,
+                    uint32_t* n_plan) {
+  try {
+    Trainer tr(make_options(*o));
+    tr.step_n(o->steps);
+    for (uint32_t g = 0; g < o->M; ++g) {
+      const auto tabs = tr.replica_tables(g);
+      for (uint32_t f = 0; f < o->F; ++f) {
+        std::memcpy(w_out[g] + (size_t)f * o->rows * o->dim, tabs[f]->weights.data(),
+                    sizeof(float) * (size_t)o->rows * o->dim);
+        std::memcpy(v_out[g] + (size_t)f * o->rows, tabs[f]->moments.data(), sizeof(float) * o->rows);
+      }
+    }
+    const auto& pl = tr.plan();
+    *n_plan = (uint32_t)pl.entries.size();
+    for (size_t i = 0; i < pl.entries.size(); ++i) {
+      plan_out[4 * i] = pl.entries[i].table_id;
+      plan_out[4 * i + 1] = pl.entries[i].row_lo;
+      plan_out[4 * i + 2] = pl.entries[i].row_hi;
+      plan_out[4 * i + 3] = pl.entries[i].local_rank;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// The same training loop composed from the public API (run_step,
+// trainer.cpp:615-663): DataGenerator batches, the embedding phases through
+// ref_group_step (forward, then backward with the MLP's f32 wire gradient),
+// the per-rank MLPs (init_rank_model, Mlp forward / backward_dx /
+// accumulate_grads / apply_sgd: pool_and_forward 366-402, backward_rank
+// 404-438, dense_sync_and_apply 507-545) and the replica sync (ref_sync,
+// 547-596).  Records every step's per-rank inputs of the embedding path:
+// rec_len[step][rank][B*F], rec_ids[step][rank][B*F*L],
+// rec_up[step][rank][B][F*D], rec_pooled likewise (any may be NULL).
+int ref_restated_run(const RefTrainerOpts* o, uint32_t* rec_len, uint32_t* rec_ids, float* rec_up,
+                     float* rec_pooled, float* const* w_out, float* const* v_out) {
+  try {
+    const TrainerOptions t = make_options(*o);
+    const uint32_t T = o->T, M = o->M, N = T / M, F = o->F, D = o->dim, B = o->B, L = o->ids_per_sample;
+    DataGenerator gen(t.feature_specs(), t.data, t.data_seed, t.eval_seed);
+    std::vector<TableLoadProfile> prof;
+    for (const auto& s : gen.specs()) prof.push_back(profile_from_spec(s, D, N * B));
+    const ShardingPlan plan = plan_greedy(prof, N, t.strategy);
+    std::vector<uint32_t> pl;
+    for (const auto& e : plan.entries) pl.insert(pl.end(), {e.table_id, e.row_lo, e.row_hi, e.local_rank});
+    const uint32_t ne = (uint32_t)plan.entries.size();
+    std::vector<uint32_t> rows(F, o->rows), dims(F, D);
+    const size_t rf = (size_t)F * o->rows * D, rv = (size_t)F * o->rows;
+    std::vector<std::vector<float>> ws(M, std::vector<float>(rf)), vs(M, std::vector<float>(rv, 0.0f));
+    std::vector<std::vector<uint8_t>> dirty(M, std::vector<uint8_t>(rv, 0));
+    for (uint32_t f = 0; f < F; ++f) {
+      const EmbeddingTable tb = init_table(f, o->rows, D, t.init_seed);
+      for (uint32_t g = 0; g < M; ++g) std::memcpy(ws[g].data() + (size_t)f * o->rows * D, tb.weights.data(), sizeof(float) * (size_t)o->rows * D);
+    }
+    std::vector<RankModel> models;
+    for (uint32_t r = 0; r < T; ++r) models.push_back(init_rank_model(t.model, t.data.dense_dim, t.init_seed));
+    const uint32_t oin = t.model.over_in(), dh = t.model.dense_hidden, oh = t.model.over_hidden;
+    const size_t up_n = (size_t)B * F * D;
+    MlpGrads dense_mean, over_mean;
+    dense_mean.resize(models[0].dense_arch.dims());
+    over_mean.resize(models[0].over_arch.dims());
+    for (uint32_t step = 0; step < o->steps; ++step) {
+      std::vector<MiniBatch> mb(T);
+      std::vector<std::vector<uint32_t>> len(T, std::vector<uint32_t>((size_t)B * F)), ids(T);
+      for (uint32_t r = 0; r < T; ++r) {
+        gen.gen_batch_into(mb[r], step, r, B);
+        for (uint32_t s = 0; s < B; ++s)
+          for (uint32_t f = 0; f < F; ++f) {
+            len[r][(size_t)s * F + f] = (uint32_t)mb[r].samples[s].ids[f].size();
+            ids[r].insert(ids[r].end(), mb[r].samples[s].ids[f].begin(), mb[r].samples[s].ids[f].end());
+          }
+      }
+      // forward of every group (pooled rows, pre-update replica)
+      std::vector<std::vector<float>> pooled(T, std::vector<float>(up_n)), upstream(T, std::vector<float>(up_n));
+      for (uint32_t g = 0; g < M; ++g) {
+        std::vector<const uint32_t*> lp(N), ip(N);
+        std::vector<float*> pp(N);
+        for (uint32_t n = 0; n < N; ++n) {
+          lp[n] = len[g * N + n].data();
+          ip[n] = ids[g * N + n].data();
+          pp[n] = pooled[g * N + n].data();
+        }
+        if (ref_group_step(F, N, B, rows.data(), dims.data(), ne, pl.data(), t.opt.eta, t.opt.eps, t.opt.c,
+                           o->sgd, lp.data(), ip.data(), nullptr, pp.data(), ws[g].data(), vs[g].data(), nullptr, 1,
+                           nullptr))
+          return -1;
+      }
+      // per rank: MLP forward + backward -> f32 wire gradient
+      struct Act {
+        std::vector<float> over_in, dense_hidden, over_hidden;
+        std::vector<double> probs, dh_over, dh_dense, ddense_out;
+      };
+      std::vector<Act> act(T);
+      for (uint32_t r = 0; r < T; ++r) {
+        Act& a = act[r];
+        const RankModel& m = models[r];
+        a.over_in.assign((size_t)B * oin, 0.f);
+        a.dense_hidden.assign((size_t)B * dh, 0.f);
+        a.over_hidden.assign((size_t)B * oh, 0.f);
+        a.probs.assign(B, 0.0);
+        a.dh_over.assign((size_t)B * oh, 0.0);
+        a.dh_dense.assign((size_t)B * dh, 0.0);
+        a.ddense_out.assign((size_t)B * D, 0.0);
+        std::vector<double> dx(oin);
+        for (uint32_t s = 0; s < B; ++s) {
+          float* oi = &a.over_in[(size_t)s * oin];
+          std::memcpy(oi, &pooled[r][(size_t)s * F * D], sizeof(float) * F * D);
+          m.dense_arch.forward(mb[r].samples[s].dense.data(), &a.dense_hidden[(size_t)s * dh], oi + (size_t)F * D);
+          float logit = 0.f;
+          m.over_arch.forward(oi, &a.over_hidden[(size_t)s * oh], &logit);
+          a.probs[s] = sigmoid((double)logit);
+          const double y = (double)mb[r].samples[s].label;
+          const double dlogit = a.probs[s] - y;
+          m.over_arch.backward_dx(&a.over_hidden[(size_t)s * oh], &dlogit, &a.dh_over[(size_t)s * oh], dx.data());
+          for (uint32_t k = 0; k < F * D; ++k) upstream[r][(size_t)s * F * D + k] = (float)dx[k];
+          for (uint32_t j = 0; j < D; ++j) a.ddense_out[(size_t)s * D + j] = dx[(size_t)F * D + j];
+          m.dense_arch.backward_dx(&a.dense_hidden[(size_t)s * dh], &a.ddense_out[(size_t)s * D],
+                                   &a.dh_dense[(size_t)s * dh], nullptr);
+        }
+      }
+      // backward of every group: embedding gradient + fused update
+      for (uint32_t g = 0; g < M; ++g) {
+        std::vector<const uint32_t*> lp(N), ip(N);
+        std::vector<const float*> up(N);
+        std::vector<float*> pp(N);
+        std::vector<std::vector<float>> scratch(N, std::vector<float>(up_n));
+        for (uint32_t n = 0; n < N; ++n) {
+          lp[n] = len[g * N + n].data();
+          ip[n] = ids[g * N + n].data();
+          up[n] = upstream[g * N + n].data();
+          pp[n] = scratch[n].data();
+        }
+        if (ref_group_step(F, N, B, rows.data(), dims.data(), ne, pl.data(), t.opt.eta, t.opt.eps, t.opt.c,
+                           o->sgd, lp.data(), ip.data(), up.data(), pp.data(), ws[g].data(), vs[g].data(),
+                           dirty[g].data(), 1, nullptr))
+          return -1;
+      }
+      // dense_sync_and_apply: one left fold in (rank, sample) order
+      dense_mean.reset();
+      over_mean.reset();
+      for (uint32_t r = 0; r < T; ++r) {
+        const Act& a = act[r];
+        const RankModel& m = models[r];
+        for (uint32_t s = 0; s < B; ++s) {
+          const double dlogit = a.probs[s] - (double)mb[r].samples[s].label;
+          m.over_arch.accumulate_grads(&a.over_in[(size_t)s * oin], &a.over_hidden[(size_t)s * oh], &dlogit,
+                                       &a.dh_over[(size_t)s * oh], over_mean);
+          m.dense_arch.accumulate_grads(mb[r].samples[s].dense.data(), &a.dense_hidden[(size_t)s * dh],
+                                        &a.ddense_out[(size_t)s * D], &a.dh_dense[(size_t)s * dh], dense_mean);
+        }
+      }
+      const double inv_global = 1.0 / ((double)T * B);
+      models[0].dense_arch.apply_sgd(dense_mean, t.opt.eta, inv_global);
+      models[0].over_arch.apply_sgd(over_mean, t.opt.eta, inv_global);
+      for (uint32_t r = 1; r < T; ++r) {
+        models[r].dense_arch.copy_params_from(models[0].dense_arch);
+        models[r].over_arch.copy_params_from(models[0].over_arch);
+      }
+      if (M > 1 && (step + 1) % t.sync_interval == 0) {
+        std::vector<float*> wp(M), vp(M);
+        std::vector<uint8_t*> dp(M);
+        for (uint32_t g = 0; g < M; ++g) {
+          wp[g] = ws[g].data();
+          vp[g] = vs[g].data();
+          dp[g] = dirty[g].data();
+        }
+        ref_sync(M, F, rows.data(), dims.data(), o->sgd, wp.data(), vp.data(), dp.data());
+      }
+      const size_t bf = (size_t)B * F, ni = bf * L;
+      for (uint32_t r = 0; r < T; ++r) {
+        const size_t at = (size_t)step * T + r;
+        if (rec_len) std::memcpy(rec_len + at * bf, len[r].data(), bf * 4);
+        if (rec_ids) std::memcpy(rec_ids + at * ni, ids[r].data(), ni * 4);
+        if (rec_up) std::memcpy(rec_up + at * up_n, upstream[r].data(), up_n * 4);
+        if (rec_pooled) std::memcpy(rec_pooled + at * up_n, pooled[r].data(), up_n * 4);
+      }
+    }
+    for (uint32_t g = 0; g < M; ++g) {
+      std::memcpy(w_out[g], ws[g].data(), rf * 4);
+      std::memcpy(v_out[g], vs[g].data(), rv * 4);
     }
     return 0;
   } catch (const std::exception& e) {

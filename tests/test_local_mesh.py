@@ -133,3 +133,66 @@ def test_metrics_row_over_mp_group_shards():
     finally:
         for e in engs:
             e.close()
+
+
+TRAINER_MESHES = [
+    dict(T=1, M=1, steps=5),
+    dict(T=4, M=1),
+    dict(T=4, M=2),
+    dict(T=8, M=2, strategy="table-wise", sync_interval=3, steps=6),
+    dict(T=4, M=2, sgd=True, sync_interval=2),
+    dict(T=6, M=3, rows=50, dim=12, L=5),
+]
+
+
+@pytest.mark.parametrize("mesh", TRAINER_MESHES, ids=[str(m) for m in TRAINER_MESHES])
+def test_gpu_mesh_matches_real_reference_trainer(mesh):
+    """End to end against the REAL reference Trainer (trainer.cpp in
+    oracle/_ref): its training loop, restated on the public API and pinned
+    bitwise to Trainer::replica_tables (tests/test_oracle.py), records every
+    step's per-rank batch and the f32 gradient its MLP sends back; the same
+    T-rank mesh on the GPU (virtual ranks, one B200) consumes those inputs.
+    Every pooled output of every step and every replica after the last step
+    are bitwise equal to the reference's (acceptance criterion 1 shape,
+    tests/acceptance/main.cpp:95-125, for M = 1 and the 2D meshes)."""
+    import paper_2508_03854_b200 as s2d
+    from oracle import reference_available, reference_trainer, restated_trainer, trainer_options
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    o = trainer_options(**mesh)
+    ws_real, vs_real, plan = reference_trainer(o)
+    _, _, ln, ids, up, pooled = restated_trainer(o)
+    N = o.T // o.M
+    tables = [s2d.TableConfig(o.rows, o.dim) for _ in range(o.F)]
+    plan_d = [dict(table_id=int(e[0]), row_lo=int(e[1]), row_hi=int(e[2]), local_rank=int(e[3])) for e in plan]
+    opt = s2d.OptimizerConfig(eta=o.eta, eps=o.eps, c=o.c, variant="sgd" if o.sgd else "rowwise-adagrad")
+    engs = s2d.local_mesh(tables, s2d.Topology(o.T, o.M), plan=plan_d, optimizer=opt)
+    try:
+        s2d.run_ranks(lambda r: engs[r].init_tables(o.init_seed), o.T)
+
+        def step(r, k):
+            got = engs[r].forward(ln[k, r], ids[k, r])
+            engs[r].backward_update(up[k, r])
+            if o.M > 1 and (k + 1) % o.sync_interval == 0:
+                engs[r].sync_replicas()
+            return got
+
+        for k in range(o.steps):
+            got = s2d.run_ranks(lambda r: step(r, k), o.T)
+            for r in range(o.T):
+                assert np.array_equal(got[r].view(np.uint32), pooled[k, r].view(np.uint32)), (k, r)
+        for r in range(o.T):
+            g = r // N
+            for f in range(o.F):
+                lo, hi = engs[r].owned_range(f)
+                if hi <= lo:
+                    continue
+                w, v = engs[r].read_rows(f, lo, hi)
+                wr = ws_real[g][f * o.rows * o.dim:(f + 1) * o.rows * o.dim].reshape(o.rows, o.dim)[lo:hi]
+                vr = vs_real[g][f * o.rows:(f + 1) * o.rows][lo:hi]
+                assert np.array_equal(w.view(np.uint32), wr.view(np.uint32)), (r, f)
+                assert np.array_equal(v.view(np.uint32), vr.view(np.uint32)), (r, f)
+    finally:
+        for e in engs:
+            e.close()

@@ -312,3 +312,38 @@ def test_metrics_row_definition(port):
     for x in v:
         acc += float(x)
     assert m["v_mean"] == acc / n
+
+
+PIN_MESHES = [
+    dict(T=1, M=1),
+    dict(T=4, M=1),
+    dict(T=4, M=2),
+    dict(T=4, M=4, strategy="table-wise"),
+    dict(T=8, M=2, strategy="table-wise", sync_interval=3, steps=6),
+    dict(T=4, M=2, sgd=True, sync_interval=2),
+    dict(T=6, M=3, rows=50, dim=12, L=5),
+]
+
+
+@pytest.mark.parametrize("mesh", PIN_MESHES, ids=[str(m) for m in PIN_MESHES])
+def test_restated_loop_equals_real_trainer(mesh):
+    """Oracle pin against the REAL reference Trainer (trainer.cpp compiled
+    into oracle/_ref): the step composed from the public API in
+    ref_harness.cpp -- DataGenerator batches, the restated build_demand /
+    owner split / combine / grad payloads / owner update (ref_group_step),
+    the per-rank MLPs and the replica sync -- leaves every group's replica
+    bitwise equal to Trainer::replica_tables(g) (acceptance criterion 1 shape,
+    tests/acceptance/main.cpp:95-125; replica consensus, test_trainer.cpp:141-151)."""
+    from oracle import reference_available, reference_trainer, restated_trainer, trainer_options
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    o = trainer_options(**mesh)
+    ws_real, vs_real, _ = reference_trainer(o)
+    ws, vs = restated_trainer(o)[:2]
+    for g in range(o.M):
+        assert np.array_equal(ws[g].view(np.uint32), ws_real[g].view(np.uint32)), g
+        assert np.array_equal(vs[g].view(np.uint32), vs_real[g].view(np.uint32)), g
+    if o.M > 1 and o.steps % o.sync_interval == 0:  # consensus after a sync step
+        for g in range(1, o.M):
+            assert np.array_equal(ws_real[g].view(np.uint32), ws_real[0].view(np.uint32))
