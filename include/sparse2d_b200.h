@@ -137,6 +137,21 @@ int s2d_imbalance_ratio(const double* per_rank, uint32_t n, double* out);
 /* OptimizerConfig::validate (src/optimizer.cpp:19-23) + effective_lr (61-63). */
 int s2d_effective_lr(double v, const s2d_optimizer_config* cfg, double* out);
 
+/* Analytic helpers of the reference's Python module (bindings/module.cpp:43-89,
+ * 133-145); host-only, outside the step. */
+/* memory_overhead / sync_latency / qps_scaling_factor (src/cost_model.cpp:24-55) */
+int s2d_memory_overhead(double table_size_gb, uint32_t groups, uint32_t total_gpus, double* out);
+int s2d_sync_latency(double table_size_gb, uint32_t groups, uint32_t total_gpus, double sync_bw_gbps, double* out);
+int s2d_qps_scaling_factor(double qps_base, double gpus_base, double qps_new, double gpus_new, double* out);
+/* evaluate_ne (src/trainer.cpp:14-43): mean log-loss / entropy of the mean-CTR predictor */
+int s2d_evaluate_ne(const double* probs, const float* labels, uint64_t n, double* ne, double* baseline_ctr);
+/* Proposition 1 moment analysis (src/moment_analysis.cpp:69-148) behind the
+ * choice of the AdaGrad scaling factor c */
+int s2d_closed_form_ratio(double mu_norm, double sigma, uint32_t dim, uint32_t batch, uint32_t groups, double* out);
+int s2d_recommend_c(double mu_norm, double sigma, uint32_t dim, uint32_t batch, uint32_t groups, double* out);
+int s2d_estimate_increment_ratio(double mu_norm, double sigma, uint32_t dim, uint32_t batch, uint32_t groups,
+                                 uint64_t trials, uint64_t seed, double* ratio, double* std_error);
+
 /* ---- device context --------------------------------------------------- */
 
 typedef struct s2d_ctx s2d_ctx;
@@ -315,6 +330,68 @@ typedef struct {
   uint64_t rows;
 } s2d_metrics_row;
 int s2d_metrics(s2d_ctx* ctx, s2d_metrics_row* out);
+
+/* Synthetic upstream gradient for one rank's batch:
+ * out[s][coff_f + j] = f32(1e-3 * z), z the Box-Muller normals of
+ * CounterRng({seed, step, rank, s, f}) (rng.hpp) in draw order.  mem says
+ * where out ([batch][sum dims] fp32) lives. */
+int s2d_gen_upstream(s2d_ctx* ctx, uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, float* out,
+                     int32_t mem);
+
+/* ---- Trainer facade (include/sparse2d/trainer.hpp:106-132) ---------------
+ * The reference's one-object training loop over the 2D mesh: every rank a
+ * virtual rank of this process on the GPUs given (rank r -> devices[r %
+ * n_devices], all GPUs round-robin when devices is NULL).  Per step and
+ * rank: the reference DataGenerator's ids (fixed pooling, trainer.hpp
+ * ids_per_sample), the lookup, the upstream gradient, the backward + fused
+ * update, and the replica sync every sync_interval steps
+ * ((step+1) % sync_interval == 0, trainer.cpp:661).  The dense MLP is not
+ * part of this build: the upstream gradient comes from the caller's callback
+ * (the dense model's backward) or, without one, from s2d_gen_upstream. */
+typedef struct {
+  uint32_t total_ranks, groups;                 /* Topology */
+  uint32_t num_tables, rows_per_table, dim;     /* DlrmConfig (embedding part) */
+  int32_t strategy;                             /* S2D_ROW_WISE (reference default) | S2D_TABLE_WISE */
+  double zipf_exponent;
+  uint32_t ids_per_sample;
+  uint32_t per_rank_batch;
+  uint64_t steps;
+  uint32_t sync_interval;
+  uint64_t data_seed, init_seed;
+  s2d_optimizer_config opt;
+  int32_t weight_dtype;                         /* S2D_F32 | S2D_BF16 */
+  uint32_t n_devices;
+  const int32_t* devices;
+} s2d_trainer_options;
+
+/* Called on rank `rank`'s thread after the step's forward: fill upstream
+ * ([batch][num_tables*dim] fp32, device, per-sample, not batch-divided:
+ * trainer.cpp:424-427) from the pooled rows (device) of the batch whose bag
+ * lengths are `lengths` (device); cuda_stream is the rank's stream.
+ * Non-zero return aborts the step. */
+typedef int (*s2d_upstream_fn)(void* user, uint32_t rank, uint64_t step, uint32_t batch, const uint32_t* lengths,
+                               const float* pooled, float* upstream, void* cuda_stream);
+
+typedef struct s2d_trainer s2d_trainer;
+int s2d_trainer_create(const s2d_trainer_options* opts, s2d_trainer** out);
+int s2d_trainer_destroy(s2d_trainer* t);
+int s2d_trainer_set_upstream(s2d_trainer* t, s2d_upstream_fn fn, void* user);
+/* Trainer::step_n (trainer.hpp:117) and run (opts.steps - steps done). */
+int s2d_trainer_step_n(s2d_trainer* t, uint64_t count);
+int s2d_trainer_run(s2d_trainer* t);
+int s2d_trainer_steps_done(s2d_trainer* t, uint64_t* out);
+/* Trainer::plan (trainer.hpp:124). */
+int s2d_trainer_plan(s2d_trainer* t, s2d_plan_entry* out, uint32_t cap, uint32_t* n);
+/* Trainer::replica_tables(group)[table] (trainer.hpp:123): w rows*dim, v rows
+ * (tables() = group 0). */
+int s2d_trainer_replica_table(s2d_trainer* t, uint32_t group, uint32_t table, float* w, float* v);
+/* Trainer::save_tables / load_tables (trainer.hpp:126-127), S2DCKPT1. */
+int s2d_trainer_save_tables(s2d_trainer* t, const char* path);
+int s2d_trainer_load_tables(s2d_trainer* t, const char* path);
+/* MetricsRow moment columns of group 0's replica. */
+int s2d_trainer_metrics(s2d_trainer* t, s2d_metrics_row* out);
+/* The context of one virtual rank (owned by the trainer). */
+int s2d_trainer_rank_ctx(s2d_trainer* t, uint32_t rank, s2d_ctx** out);
 
 /* Number of kernels this library has launched in the process. */
 uint64_t s2d_launch_count(void);

@@ -149,4 +149,92 @@ class Engine {
   s2d_ctx* ctx_ = nullptr;
 };
 
+// Host-side table view (EmbeddingTable, include/sparse2d/embedding.hpp:12-23).
+struct TableCopy {
+  uint32_t rows = 0, dim = 0;
+  std::vector<float> weights, moments;
+  const float* row(uint32_t r) const { return weights.data() + (size_t)r * dim; }
+};
+
+// Trainer (include/sparse2d/trainer.hpp:106-132) over s2d_trainer_*: the
+// whole 2D mesh as virtual ranks of this process.  The dense model's
+// gradient comes from set_upstream (else the synthetic one).
+class Trainer {
+ public:
+  explicit Trainer(const s2d_trainer_options& opts) : opts_(opts) { check(s2d_trainer_create(&opts, &t_)); }
+  ~Trainer() {
+    if (t_) s2d_trainer_destroy(t_);
+  }
+  Trainer(const Trainer&) = delete;
+  Trainer& operator=(const Trainer&) = delete;
+
+  void set_upstream(s2d_upstream_fn fn, void* user) { check(s2d_trainer_set_upstream(t_, fn, user)); }
+  void run() { check(s2d_trainer_run(t_)); }
+  void step_n(uint64_t count) { check(s2d_trainer_step_n(t_, count)); }
+  uint64_t steps_done() const {
+    uint64_t n = 0;
+    check(s2d_trainer_steps_done(t_, &n));
+    return n;
+  }
+  std::vector<s2d_plan_entry> plan() const {
+    uint32_t n = 0;
+    check(s2d_trainer_plan(t_, nullptr, 0, &n));
+    std::vector<s2d_plan_entry> out(n);
+    check(s2d_trainer_plan(t_, out.data(), n, &n));
+    return out;
+  }
+  std::vector<TableCopy> replica_tables(uint32_t group) const {
+    std::vector<TableCopy> out(opts_.num_tables);
+    for (uint32_t f = 0; f < opts_.num_tables; ++f) {
+      TableCopy& t = out[f];
+      t.rows = opts_.rows_per_table;
+      t.dim = opts_.dim;
+      t.weights.resize((size_t)t.rows * t.dim);
+      t.moments.resize(t.rows);
+      check(s2d_trainer_replica_table(t_, group, f, t.weights.data(), t.moments.data()));
+    }
+    return out;
+  }
+  std::vector<TableCopy> tables() const { return replica_tables(0); }
+  void save_tables(const std::string& path) const { check(s2d_trainer_save_tables(t_, path.c_str())); }
+  void load_tables(const std::string& path) { check(s2d_trainer_load_tables(t_, path.c_str())); }
+  s2d_metrics_row metrics() const {
+    s2d_metrics_row m{};
+    check(s2d_trainer_metrics(t_, &m));
+    return m;
+  }
+
+ private:
+  s2d_trainer_options opts_;
+  s2d_trainer* t_ = nullptr;
+};
+
+// Analytic helpers of the reference module (cost_model.hpp, trainer.hpp
+// evaluate_ne, moment_analysis.hpp), same names.
+inline double memory_overhead(double table_size_gb, uint32_t groups, uint32_t total_gpus) {
+  double r = 0;
+  check(s2d_memory_overhead(table_size_gb, groups, total_gpus, &r));
+  return r;
+}
+inline double sync_latency(double table_size_gb, uint32_t groups, uint32_t total_gpus, double bw) {
+  double r = 0;
+  check(s2d_sync_latency(table_size_gb, groups, total_gpus, bw, &r));
+  return r;
+}
+inline double qps_scaling_factor(double qps_base, double gpus_base, double qps_new, double gpus_new) {
+  double r = 0;
+  check(s2d_qps_scaling_factor(qps_base, gpus_base, qps_new, gpus_new, &r));
+  return r;
+}
+inline double closed_form_ratio(double mu_norm, double sigma, uint32_t dim, uint32_t batch, uint32_t groups) {
+  double r = 0;
+  check(s2d_closed_form_ratio(mu_norm, sigma, dim, batch, groups, &r));
+  return r;
+}
+inline double recommend_c(double mu_norm, double sigma, uint32_t dim, uint32_t batch, uint32_t groups) {
+  double r = 0;
+  check(s2d_recommend_c(mu_norm, sigma, dim, batch, groups, &r));
+  return r;
+}
+
 }  // namespace sparse2d_b200

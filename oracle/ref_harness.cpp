@@ -21,7 +21,9 @@
 #include <thread>
 #include <vector>
 
+#include "sparse2d/cost_model.hpp"
 #include "sparse2d/data.hpp"
+#include "sparse2d/moment_analysis.hpp"
 #include "sparse2d/embedding.hpp"
 #include "sparse2d/model.hpp"
 #include "sparse2d/optimizer.hpp"
@@ -697,6 +699,26 @@ int ref_restated_run(const RefTrainerOpts* o, uint32_t* rec_len, uint32_t* rec_i
     g_err = e.what();
     return -1;
   }
+}
+
+// ---- analytic helpers (cost_model.cpp, moment_analysis.cpp, trainer.cpp) ----
+double ref_memory_overhead(double s, uint32_t g, uint32_t t) { return memory_overhead(s, g, t); }
+double ref_sync_latency(double s, uint32_t g, uint32_t t, double bw) { return sync_latency(s, g, t, bw); }
+double ref_qps_scaling_factor(double a, double b, double c, double d) { return qps_scaling_factor(a, b, c, d); }
+double ref_closed_form_ratio(double mu, double sigma, uint32_t dim, uint32_t b, uint32_t g) {
+  return closed_form_ratio(make_noise_model(mu, sigma, dim, b), g);
+}
+double ref_recommend_c(double mu, double sigma, uint32_t dim, uint32_t b, uint32_t g) {
+  return recommend_c(make_noise_model(mu, sigma, dim, b), g);
+}
+void ref_estimate_increment_ratio(double mu, double sigma, uint32_t dim, uint32_t b, uint32_t g, uint64_t trials,
+                                  uint64_t seed, double* out2) {
+  const auto r = estimate_increment_ratio(make_noise_model(mu, sigma, dim, b), g, trials, seed);
+  out2[0] = r.ratio_estimate;
+  out2[1] = r.std_error;
+}
+double ref_evaluate_ne(const double* p, const float* y, uint64_t n) {
+  return evaluate_ne(std::span<const double>(p, n), std::span<const float>(y, n)).ne;
 }
 
 }  // extern "C"

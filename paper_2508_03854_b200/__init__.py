@@ -8,6 +8,15 @@ sync) runs as hand-written sm_100a CUDA kernels + NCCL in
 ``libsparse2d_b200.so`` behind a C ABI (``include/sparse2d_b200.h``).
 """
 from .api import (  # noqa: F401
+    Trainer,
+    TrainerOptions,
+    closed_form_ratio,
+    estimate_increment_ratio,
+    evaluate_ne,
+    memory_overhead,
+    qps_scaling_factor,
+    recommend_c,
+    sync_latency,
     LocalHub,
     OptimizerConfig,
     Sparse2DEmbedding,
@@ -28,6 +37,15 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
+    "Trainer",
+    "TrainerOptions",
+    "closed_form_ratio",
+    "estimate_increment_ratio",
+    "evaluate_ne",
+    "memory_overhead",
+    "qps_scaling_factor",
+    "recommend_c",
+    "sync_latency",
     "LocalHub",
     "OptimizerConfig",
     "Sparse2DEmbedding",

@@ -51,6 +51,19 @@ class StepStats(C.Structure):
                 ("lookup_bytes_sent", C.c_uint64), ("grad_bytes_sent", C.c_uint64), ("host_wait_ns", C.c_uint64)]
 
 
+class TrainerOptionsC(C.Structure):
+    _fields_ = [("total_ranks", C.c_uint32), ("groups", C.c_uint32), ("num_tables", C.c_uint32),
+                ("rows_per_table", C.c_uint32), ("dim", C.c_uint32), ("strategy", C.c_int32),
+                ("zipf_exponent", C.c_double), ("ids_per_sample", C.c_uint32), ("per_rank_batch", C.c_uint32),
+                ("steps", C.c_uint64), ("sync_interval", C.c_uint32), ("data_seed", C.c_uint64),
+                ("init_seed", C.c_uint64), ("opt", OptimizerConfigC), ("weight_dtype", C.c_int32),
+                ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int32))]
+
+
+UPSTREAM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
+                          C.c_void_p, C.c_void_p)
+
+
 class MetricsRowC(C.Structure):
     _fields_ = [("eff_lr_p50", C.c_double), ("eff_lr_p99", C.c_double), ("v_mean", C.c_double),
                 ("rows", C.c_uint64)]
@@ -104,6 +117,29 @@ SIGNATURES = {
     "s2d_metrics": (C.c_int, [_P, C.POINTER(MetricsRowC)]),
     "s2d_shard_gather": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P, _P]),
     "s2d_ctx_set_debug_grad": (C.c_int, [_P, C.c_int]),
+    "s2d_gen_upstream": (C.c_int, [_P, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, _P, C.c_int32]),
+    "s2d_trainer_create": (C.c_int, [C.POINTER(TrainerOptionsC), C.POINTER(_P)]),
+    "s2d_trainer_destroy": (C.c_int, [_P]),
+    "s2d_trainer_set_upstream": (C.c_int, [_P, UPSTREAM_FN, _P]),
+    "s2d_trainer_step_n": (C.c_int, [_P, C.c_uint64]),
+    "s2d_trainer_run": (C.c_int, [_P]),
+    "s2d_trainer_steps_done": (C.c_int, [_P, C.POINTER(C.c_uint64)]),
+    "s2d_trainer_plan": (C.c_int, [_P, C.POINTER(PlanEntry), C.c_uint32, C.POINTER(C.c_uint32)]),
+    "s2d_trainer_replica_table": (C.c_int, [_P, C.c_uint32, C.c_uint32, _P, _P]),
+    "s2d_trainer_save_tables": (C.c_int, [_P, C.c_char_p]),
+    "s2d_trainer_load_tables": (C.c_int, [_P, C.c_char_p]),
+    "s2d_trainer_metrics": (C.c_int, [_P, C.POINTER(MetricsRowC)]),
+    "s2d_trainer_rank_ctx": (C.c_int, [_P, C.c_uint32, C.POINTER(_P)]),
+    "s2d_memory_overhead": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
+    "s2d_sync_latency": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.c_double, C.POINTER(C.c_double)]),
+    "s2d_qps_scaling_factor": (C.c_int, [C.c_double] * 4 + [C.POINTER(C.c_double)]),
+    "s2d_evaluate_ne": (C.c_int, [_P, _P, C.c_uint64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "s2d_closed_form_ratio": (C.c_int, [C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
+                                        C.POINTER(C.c_double)]),
+    "s2d_recommend_c": (C.c_int, [C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
+    "s2d_estimate_increment_ratio": (C.c_int, [C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
+                                               C.c_uint64, C.c_uint64, C.POINTER(C.c_double),
+                                               C.POINTER(C.c_double)]),
     "s2d_debug_read": (C.c_int, [_P, C.c_int32, _P, C.c_uint64, C.POINTER(C.c_uint64)]),
 }
 

@@ -152,6 +152,60 @@ def adagrad_rows(ws, vs, gs, eta=0.1, eps=1e-8, c=1.0, variant="rowwise-adagrad"
     return [dict(w=w[i].tolist(), v=float(v[i]), effective_lr=float(lr[i])) for i in range(len(v))]
 
 
+# ---- analytic helpers of the reference module (bindings/module.cpp:43-89, 133-145)
+
+def _dbl(fn, *args) -> float:
+    out = C.c_double(0)
+    L.check(fn(*args, C.byref(out)))
+    return out.value
+
+
+def memory_overhead(table_size_gb: float, groups: int, total_gpus: int) -> float:
+    """S (M-1) / T (src/cost_model.cpp:24-28)."""
+    return _dbl(_lib().s2d_memory_overhead, table_size_gb, groups, total_gpus)
+
+
+def sync_latency(table_size_gb: float, groups: int, total_gpus: int, sync_bw_gbps: float) -> float:
+    """2 memory_overhead / bandwidth (src/cost_model.cpp:30-34)."""
+    return _dbl(_lib().s2d_sync_latency, table_size_gb, groups, total_gpus, sync_bw_gbps)
+
+
+def qps_scaling_factor(qps_base: float, gpus_base: float, qps_new: float, gpus_new: float) -> float:
+    """(qps_new / qps_base) / (gpus_new / gpus_base) (src/cost_model.cpp:46-55)."""
+    return _dbl(_lib().s2d_qps_scaling_factor, qps_base, gpus_base, qps_new, gpus_new)
+
+
+def evaluate_ne(probs, labels) -> dict:
+    """Normalized entropy (src/trainer.cpp:14-43): {ne, baseline_ctr, eval_samples}."""
+    p = np.ascontiguousarray(probs, np.float64)
+    y = np.ascontiguousarray(labels, np.float32)
+    if p.size != y.size:
+        raise ValueError("evaluate_ne: empty or mismatched inputs")
+    ne, ctr = C.c_double(0), C.c_double(0)
+    L.check(_lib().s2d_evaluate_ne(p.ctypes.data, y.ctypes.data, p.size, C.byref(ne), C.byref(ctr)))
+    return {"ne": ne.value, "baseline_ctr": ctr.value, "eval_samples": int(p.size)}
+
+
+def closed_form_ratio(mu_norm: float, sigma: float, dim: int, batch: int, groups: int) -> float:
+    """Proposition 1 closed form (src/moment_analysis.cpp:128-141)."""
+    return _dbl(_lib().s2d_closed_form_ratio, mu_norm, sigma, dim, batch, groups)
+
+
+def recommend_c(mu_norm: float, sigma: float, dim: int, batch: int, groups: int) -> float:
+    """The AdaGrad moment scaling factor c recommended for M groups
+    (src/moment_analysis.cpp:143-146)."""
+    return _dbl(_lib().s2d_recommend_c, mu_norm, sigma, dim, batch, groups)
+
+
+def estimate_increment_ratio(mu_norm: float, sigma: float, dim: int, batch: int, groups: int, trials: int,
+                             seed: int = 1) -> dict:
+    """Monte Carlo E|g_group|^2 / E|g_full|^2 (src/moment_analysis.cpp:69-124)."""
+    r, se = C.c_double(0), C.c_double(0)
+    L.check(_lib().s2d_estimate_increment_ratio(mu_norm, sigma, dim, batch, groups, trials, seed, C.byref(r),
+                                                C.byref(se)))
+    return {"ratio_estimate": r.value, "std_error": se.value, "trials": int(trials), "groups": int(groups)}
+
+
 # ---- the step engine -----------------------------------------------------------
 
 @dataclass
@@ -590,6 +644,12 @@ class Sparse2DEmbedding:
     def _owns_rows(self) -> bool:
         return any(hi > lo for lo, hi in (self.owned_range(f) for f in range(self.F)))
 
+    def gen_upstream(self, seed: int, step: int, rank: int, batch: int) -> np.ndarray:
+        """The synthetic upstream gradient (s2d_gen_upstream) as a host array."""
+        out = np.zeros((batch, self.sum_dims), np.float32)
+        L.check(self.lib.s2d_gen_upstream(self._ctx, seed, step, rank, batch, out.ctypes.data, L.S2D_HOST))
+        return out
+
     def debug(self, which: int) -> np.ndarray:
         """Wire buffers of the last step (see s2d_debug_read)."""
         n = C.c_uint64(0)
@@ -598,3 +658,156 @@ class Sparse2DEmbedding:
         out = np.zeros(n.value, dt)
         L.check(self.lib.s2d_debug_read(self._ctx, which, out.ctypes.data, n.value, C.byref(n)))
         return out
+
+
+# ---- Trainer facade (include/sparse2d/trainer.hpp:106-132) -----------------------
+
+@dataclass
+class TrainerOptions:
+    """TrainerOptions (trainer.hpp:47-70), embedding part: topology, tables
+    (num_tables x rows_per_table x dim), the DataGenerator's Zipf exponent and
+    pooling fan-in, per-rank batch, steps, sync cadence, seeds, optimizer."""
+
+    total_ranks: int = 1
+    groups: int = 1
+    num_tables: int = 8
+    rows_per_table: int = 10000
+    dim: int = 16
+    strategy: str = "row-wise"
+    zipf_exponent: float = 1.0
+    ids_per_sample: int = 2
+    per_rank_batch: int = 4
+    steps: int = 1000
+    sync_interval: int = 1
+    data_seed: int = 1
+    init_seed: int = 2
+    optimizer: OptimizerConfig | None = None
+    weight_dtype: str = "fp32"
+    devices: Sequence[int] | None = None
+
+
+class _DevArray:
+    """A raw CUDA pointer as __cuda_array_interface__ (for torch.as_tensor)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (int(ptr), False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3}
+
+
+class Trainer:
+    """The reference's one-object training loop over the 2D mesh
+    (Trainer, trainer.hpp:106-132): every rank a virtual rank of this
+    process (s2d_trainer_*).  The upstream gradient of each step comes from
+    ``set_upstream(fn)`` -- fn(rank, step, lengths, pooled, upstream) with
+    torch CUDA tensor views, fn filling ``upstream`` (the dense model's
+    backward) -- or, by default, the synthetic f32(1e-3 N(0,1)) gradient."""
+
+    def __init__(self, opts: TrainerOptions):
+        self.lib = _lib()
+        self.opts = opts
+        opt = (opts.optimizer or OptimizerConfig()).to_c()
+        devs = list(opts.devices) if opts.devices else []
+        self._devs = (C.c_int32 * max(1, len(devs)))(*devs) if devs else None
+        if opts.strategy not in ("table-wise", "row-wise"):
+            raise ValueError("unknown sharding strategy: " + str(opts.strategy))
+        c = L.TrainerOptionsC(opts.total_ranks, opts.groups, opts.num_tables, opts.rows_per_table, opts.dim,
+                              L.S2D_ROW_WISE if opts.strategy == "row-wise" else L.S2D_TABLE_WISE,
+                              opts.zipf_exponent, opts.ids_per_sample, opts.per_rank_batch, opts.steps,
+                              opts.sync_interval, opts.data_seed, opts.init_seed, opt,
+                              L.S2D_BF16 if opts.weight_dtype == "bf16" else L.S2D_F32, len(devs),
+                              C.cast(self._devs, C.POINTER(C.c_int32)) if devs else None)
+        self._t = C.c_void_p()
+        L.check(self.lib.s2d_trainer_create(C.byref(c), C.byref(self._t)))
+        self._cb = None
+
+    def close(self):
+        if self._t:
+            self.lib.s2d_trainer_destroy(self._t)
+            self._t = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_upstream(self, fn):
+        """fn(rank, step, lengths, pooled, upstream) -> None, called on the
+        rank's thread after each forward; tensors are CUDA views (lengths
+        [B*F] int32, pooled and upstream [B, F*D] fp32)."""
+        if fn is None:
+            L.check(self.lib.s2d_trainer_set_upstream(self._t, L.UPSTREAM_FN(), None))
+            self._cb = None
+            return
+        import torch
+
+        o = self.opts
+        F, D = o.num_tables, o.dim
+
+        def cb(_user, rank, step, batch, lengths, pooled, upstream, _stream):
+            try:
+                dev = torch.device("cuda", (list(o.devices) if o.devices else [0])[rank % max(1, len(o.devices or [0]))])
+                with torch.cuda.device(dev):
+                    ln = torch.as_tensor(_DevArray(lengths, (batch * F,), "<i4"), device=dev)
+                    pl = torch.as_tensor(_DevArray(pooled, (batch, F * D), "<f4"), device=dev)
+                    up = torch.as_tensor(_DevArray(upstream, (batch, F * D), "<f4"), device=dev)
+                    fn(int(rank), int(step), ln, pl, up)
+                    torch.cuda.synchronize(dev)
+                return 0
+            except Exception:  # noqa: BLE001  (reported as a failed step)
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self._cb = L.UPSTREAM_FN(cb)
+        L.check(self.lib.s2d_trainer_set_upstream(self._t, self._cb, None))
+
+    def step_n(self, count: int):
+        """Trainer::step_n (trainer.hpp:117)."""
+        L.check(self.lib.s2d_trainer_step_n(self._t, count))
+
+    def run(self):
+        """Trainer::run: the remaining of opts.steps."""
+        L.check(self.lib.s2d_trainer_run(self._t))
+
+    @property
+    def steps_done(self) -> int:
+        n = C.c_uint64(0)
+        L.check(self.lib.s2d_trainer_steps_done(self._t, C.byref(n)))
+        return n.value
+
+    def plan(self) -> list[dict]:
+        n = C.c_uint32(0)
+        L.check(self.lib.s2d_trainer_plan(self._t, None, 0, C.byref(n)))
+        out = (L.PlanEntry * max(1, n.value))()
+        L.check(self.lib.s2d_trainer_plan(self._t, out, n.value, C.byref(n)))
+        return [dict(table_id=out[i].table_id, row_lo=out[i].row_lo, row_hi=out[i].row_hi,
+                     local_rank=out[i].local_rank) for i in range(n.value)]
+
+    def replica_tables(self, group: int) -> list[tuple]:
+        """[(weights [rows, dim] fp32, moments [rows] fp32)] per table of DP
+        group `group` (Trainer::replica_tables, trainer.hpp:123)."""
+        o = self.opts
+        out = []
+        for f in range(o.num_tables):
+            w = np.zeros((o.rows_per_table, o.dim), np.float32)
+            v = np.zeros(o.rows_per_table, np.float32)
+            L.check(self.lib.s2d_trainer_replica_table(self._t, group, f, w.ctypes.data, v.ctypes.data))
+            out.append((w, v))
+        return out
+
+    def tables(self) -> list[tuple]:
+        """Consensus view: group 0's replica (Trainer::tables, trainer.hpp:122)."""
+        return self.replica_tables(0)
+
+    def save_tables(self, path: str):
+        L.check(self.lib.s2d_trainer_save_tables(self._t, os.fsencode(path)))
+
+    def load_tables(self, path: str):
+        L.check(self.lib.s2d_trainer_load_tables(self._t, os.fsencode(path)))
+
+    def metrics_row(self) -> dict:
+        m = L.MetricsRowC()
+        L.check(self.lib.s2d_trainer_metrics(self._t, C.byref(m)))
+        return {"eff_lr_p50": m.eff_lr_p50, "eff_lr_p99": m.eff_lr_p99, "v_mean": m.v_mean, "rows": int(m.rows)}

@@ -48,6 +48,10 @@ s2d::Ctx* as_ctx(s2d_ctx* c) {
 
 }  // namespace
 
+namespace s2d {
+void set_last_error(const char* m) { g_last_error = m ? m : ""; }
+}  // namespace s2d
+
 extern "C" {
 
 const char* s2d_last_error(void) { return g_last_error.c_str(); }
@@ -271,6 +275,11 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out) {
     *out = c->stats;
     out->host_wait_ns = c->host_wait_total_ns;
   });
+}
+
+int s2d_gen_upstream(s2d_ctx* ctx, uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, float* out,
+                     int32_t mem) {
+  return guarded([&] { as_ctx(ctx)->gen_upstream(seed, step, rank, batch, out, mem); });
 }
 
 int s2d_shard_gather(s2d_ctx* ctx, uint32_t table, uint32_t n_rows, const uint32_t* rows, float* w, float* v) {

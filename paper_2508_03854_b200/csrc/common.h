@@ -32,6 +32,8 @@ struct Error : std::runtime_error {
 // Every kernel launch is followed by S2D_LAUNCH_CHECK, which also counts it
 // (s2d_launch_count: the bench's gpu_launches evidence).
 void count_launch();
+// the thread's s2d_last_error() message (capi.cpp)
+void set_last_error(const char* m);
 #define S2D_LAUNCH_CHECK()            \
   do {                                \
     ::s2d::count_launch();            \
@@ -271,6 +273,8 @@ struct GenArgs {
   uint32_t* ids;                    // [B*per_sample]
 };
 void launch_gen_batch(const GenArgs& a, cudaStream_t st);
+void launch_gen_upstream(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, const FeatDev* feats,
+                         uint32_t sum_dims, uint32_t max_dim, float* out, cudaStream_t st);
 
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
 uint64_t stream_partial1_rows(uint64_t n);  // level-1 partial rows (part2 follows them)

@@ -89,4 +89,24 @@ void Ctx::gen_batch(uint64_t seed, uint64_t step, uint32_t rnk, uint32_t batch, 
   S2D_CUDA(cudaStreamSynchronize(stream));
 }
 
+// Synthetic upstream gradient for this rank's batch:
+// out[s][coff_f + j] = f32(1e-3 * N(0,1)) from CounterRng({seed, step, rank,
+// s, f}); mem says where out lives.
+void Ctx::gen_upstream(uint64_t seed, uint64_t step, uint32_t rnk, uint32_t batch, float* out, int mem) {
+  if (!F) throw Error(S2D_EINVAL, "register tables first");
+  if (mem != S2D_HOST && mem != S2D_DEVICE) throw Error(S2D_EINVAL, "mem must be S2D_HOST or S2D_DEVICE");
+  S2D_CUDA(cudaSetDevice(device));
+  const uint64_t n = (uint64_t)batch * sum_dims;
+  float* d = out;
+  if (mem == S2D_HOST) {
+    upstream_stage.ensure(std::max<uint64_t>(n, 1) * 4);
+    d = upstream_stage.as<float>();
+  }
+  launch_gen_upstream(seed, step, rnk, batch, F, d_feats.as<FeatDev>(), sum_dims, max_dim, d, stream);
+  if (mem == S2D_HOST) {
+    if (n) S2D_CUDA(cudaMemcpyAsync(out, d, n * 4, cudaMemcpyDeviceToHost, stream));
+    S2D_CUDA(cudaStreamSynchronize(stream));
+  }
+}
+
 }  // namespace s2d

@@ -62,7 +62,48 @@ __global__ void k_gen_lengths(const GenArgs a) {
   }
 }
 
+// Synthetic per-sample upstream gradient of the embedding path (SURVEY.md
+// 8(d); oracle or_synthetic_upstream): out[s][coff_f + j] =
+// f32(1e-3 * z_j), z the Box-Muller normals of CounterRng({seed, step, rank,
+// s, f}) in draw order (rng.hpp next_normal: cos first, then the cached sin).
+// One thread per (s, f, pair of columns).
+__global__ void k_gen_upstream(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F,
+                               const FeatDev* __restrict__ feats, uint32_t sum_dims, uint32_t max_pairs,
+                               float* __restrict__ out) {
+  const uint64_t total = (uint64_t)B * F * max_pairs;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t p = (uint32_t)(i % max_pairs);
+    const uint64_t sf = i / max_pairs;
+    const uint32_t f = (uint32_t)(sf % F), s = (uint32_t)(sf / F);
+    const uint32_t D = __ldg(&feats[f].dim);
+    if (2 * p >= D) continue;
+    const uint64_t fields[5] = {seed, step, rank, s, f};
+    uint64_t key = 0x8A5CD789635D2DFFULL;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) key = mix64(key + 0x9E3779B97F4A7C15ULL + fields[q]);
+    const uint64_t c1 = 2ull * p + 1, c2 = 2ull * p + 2;
+    const double u1 = (double)((mix64(key + c1 * 0x9E3779B97F4A7C15ULL) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = (double)(mix64(key + c2 * 0x9E3779B97F4A7C15ULL) >> 11) * 0x1.0p-53;
+    const double r = sqrt(-2.0 * log(u1));
+    const double t = 2.0 * 3.141592653589793 * u2;
+    float* o = out + (uint64_t)s * sum_dims + __ldg(&feats[f].coff) + 2 * p;
+    o[0] = (float)(1e-3 * (r * cos(t)));
+    if (2 * p + 1 < D) o[1] = (float)(1e-3 * (r * sin(t)));
+  }
+}
+
 }  // namespace
+
+void launch_gen_upstream(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, const FeatDev* feats,
+                         uint32_t sum_dims, uint32_t max_dim, float* out, cudaStream_t st) {
+  const uint32_t pairs = (max_dim + 1) / 2;
+  const uint64_t n = (uint64_t)B * F * pairs;
+  if (!n) return;
+  k_gen_upstream<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 32), 256, 0, st>>>(seed, step, rank, B, F, feats,
+                                                                                          sum_dims, pairs, out);
+  S2D_LAUNCH_CHECK();
+}
 
 void launch_gen_batch(const GenArgs& a, cudaStream_t st) {
   const uint64_t n_ids = (uint64_t)a.B * a.per_sample, n_bags = (uint64_t)a.B * a.F;

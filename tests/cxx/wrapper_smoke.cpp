@@ -58,5 +58,10 @@ int main() {
   const s2d_optimizer_config badc{0.1, 1e-8, 0.0, S2D_ROWWISE_ADAGRAD};
   EXPECT(throws<std::invalid_argument>([&] { b::effective_lr(1.0, badc); }));
   std::printf("WRAPPER OK\n");
+  EXPECT(b::memory_overhead(1700.0, 1, 1024) == 0.0);
+  EXPECT(std::fabs(b::memory_overhead(1700.0, 4, 1024) - 4.98046875) < 1e-12);
+  EXPECT(b::closed_form_ratio(0.0, 1.0, 16, 32, 4) == 4.0);
+  EXPECT(std::fabs(b::recommend_c(1.0, 0.5, 4, 1, 4) - 1.6) < 1e-12);
+  EXPECT(throws<std::invalid_argument>([] { b::qps_scaling_factor(1.0, 4, 2.0, 4); }));
   return 0;
 }

@@ -168,3 +168,59 @@ def test_traces_to_csv_reference_schema():
         "1,grad_a2a,1,64,2.5e-05",
     ]
     assert text.endswith("\n")
+
+
+def test_reference_helper_functions_match_the_reference():
+    """The analytic helpers of the reference module (cost formulas, NE,
+    Proposition-1 moment analysis) equal the compiled reference functions
+    bit for bit, and the reference Python smoke test's known answers hold
+    (tests/python/test_smoke.py:20-53, 62-66)."""
+    import ctypes as C
+    import math
+
+    import paper_2508_03854_b200 as s2d
+    from oracle import REF_SO, reference_available
+
+    assert s2d.memory_overhead(1700.0, 1, 1024) == 0.0
+    assert abs(s2d.memory_overhead(1700.0, 4, 1024) - 4.98046875) < 1e-12
+    assert s2d.sync_latency(1700.0, 4, 1024, 100.0) == 2.0 * s2d.memory_overhead(1700.0, 4, 1024) / 100.0
+    assert abs(100.0 * s2d.qps_scaling_factor(1.76e5, 256, 5.61e5, 1024) - 79.7) < 0.05
+    assert s2d.closed_form_ratio(0.0, 1.0, 16, 32, 4) == 4.0
+    assert s2d.closed_form_ratio(1.0, 0.0, 16, 32, 4) == 1.0
+    assert abs(s2d.recommend_c(1.0, 0.5, 4, 1, 4) - 1.6) < 1e-12
+    rep = s2d.estimate_increment_ratio(0.0, 1.0, 8, 8, 4, 20000, 7)
+    assert abs(rep["ratio_estimate"] - 4.0) <= 0.2 and rep["std_error"] > 0.0
+    ne = s2d.evaluate_ne([0.8, 0.4], [1.0, 0.0])["ne"]
+    assert abs(ne - (-(math.log(0.8) + math.log(0.6)) / 2.0 / math.log(2.0))) < 1e-12
+    with pytest.raises(ValueError):
+        s2d.qps_scaling_factor(1.0, 4, 2.0, 4)
+    with pytest.raises(ValueError):
+        s2d.evaluate_ne([0.5, 0.5], [1.0, 1.0])
+    if not reference_available():
+        return
+    ref = C.CDLL(REF_SO)
+    for name in ("ref_memory_overhead", "ref_sync_latency", "ref_qps_scaling_factor", "ref_closed_form_ratio",
+                 "ref_recommend_c", "ref_evaluate_ne"):
+        getattr(ref, name).restype = C.c_double
+    ref.ref_memory_overhead.argtypes = [C.c_double, C.c_uint32, C.c_uint32]
+    ref.ref_sync_latency.argtypes = [C.c_double, C.c_uint32, C.c_uint32, C.c_double]
+    ref.ref_qps_scaling_factor.argtypes = [C.c_double] * 4
+    ref.ref_closed_form_ratio.argtypes = [C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32]
+    ref.ref_recommend_c.argtypes = [C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32]
+    ref.ref_estimate_increment_ratio.argtypes = [C.c_double, C.c_double, C.c_uint32, C.c_uint32, C.c_uint32,
+                                                 C.c_uint64, C.c_uint64, C.POINTER(C.c_double)]
+    ref.ref_evaluate_ne.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
+    assert s2d.memory_overhead(123.5, 3, 24) == ref.ref_memory_overhead(123.5, 3, 24)
+    assert s2d.sync_latency(123.5, 3, 24, 7.5) == ref.ref_sync_latency(123.5, 3, 24, 7.5)
+    assert s2d.qps_scaling_factor(3e5, 8, 1.1e6, 64) == ref.ref_qps_scaling_factor(3e5, 8, 1.1e6, 64)
+    for args in [(0.3, 1.7, 32, 16, 4), (2.0, 0.1, 8, 64, 8), (0.0, 0.5, 4, 2, 3)]:
+        assert s2d.closed_form_ratio(*args) == ref.ref_closed_form_ratio(*args)
+        assert s2d.recommend_c(*args) == ref.ref_recommend_c(*args)
+        out = (C.c_double * 2)()
+        ref.ref_estimate_increment_ratio(*args, 500, 11, out)
+        rep = s2d.estimate_increment_ratio(*args, 500, 11)
+        assert rep["ratio_estimate"] == out[0] and rep["std_error"] == out[1]
+    rng = np.random.default_rng(1)
+    p = rng.uniform(0.05, 0.95, 1000)
+    y = (rng.random(1000) < 0.3).astype(np.float32)
+    assert s2d.evaluate_ne(p, y)["ne"] == ref.ref_evaluate_ne(p.ctypes.data, y.ctypes.data, 1000)

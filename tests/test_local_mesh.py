@@ -196,3 +196,93 @@ def test_gpu_mesh_matches_real_reference_trainer(mesh):
     finally:
         for e in engs:
             e.close()
+
+
+FACADE_MESHES = [dict(T=1, M=1, steps=5), dict(T=4, M=2), dict(T=8, M=2, strategy="table-wise", sync_interval=3,
+                                                                  steps=6), dict(T=4, M=2, sgd=True, sync_interval=2)]
+
+
+@pytest.mark.parametrize("mesh", FACADE_MESHES, ids=[str(m) for m in FACADE_MESHES])
+def test_trainer_facade_matches_real_reference_trainer(mesh):
+    """The Trainer facade (s2d_trainer_*: device DataGenerator ids, plan_greedy
+    over profile_from_spec, internal (step+1) % sync_interval cadence) with the
+    dense model's gradient supplied through the upstream callback -- here the
+    f32 gradient the reference's MLP produced, recorded by the pinned restated
+    loop -- reproduces the REAL reference Trainer: same plan, the same batch
+    and pooled rows at every step and rank, and every replica bitwise after
+    run()."""
+    import torch
+
+    import paper_2508_03854_b200 as s2d
+    from oracle import reference_available, reference_trainer, restated_trainer, trainer_options
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    o = trainer_options(**mesh)
+    ws_real, vs_real, plan_real = reference_trainer(o)
+    _, _, ln, _, up, pooled = restated_trainer(o)
+    tr = s2d.Trainer(s2d.TrainerOptions(
+        total_ranks=o.T, groups=o.M, num_tables=o.F, rows_per_table=o.rows, dim=o.dim,
+        strategy="row-wise" if o.strategy else "table-wise", zipf_exponent=o.zipf, ids_per_sample=o.ids_per_sample,
+        per_rank_batch=o.B, steps=o.steps, sync_interval=o.sync_interval, data_seed=o.data_seed,
+        init_seed=o.init_seed, optimizer=s2d.OptimizerConfig(o.eta, o.eps, o.c, "sgd" if o.sgd else "rowwise-adagrad"),
+        devices=[0]))
+    try:
+        seen = {}
+
+        def fn(rank, step, lengths, pooled_t, up_t):
+            seen[(rank, step)] = (np.array_equal(lengths.cpu().numpy().view(np.uint32), ln[step, rank])
+                                  and np.array_equal(pooled_t.cpu().numpy().view(np.uint32),
+                                                     pooled[step, rank].view(np.uint32)))
+            up_t.copy_(torch.from_numpy(up[step, rank]).to(up_t.device))
+
+        tr.set_upstream(fn)
+        tr.run()
+        assert tr.steps_done == o.steps
+        assert len(seen) == o.T * o.steps and all(seen.values()), [k for k, v in seen.items() if not v][:5]
+        got_plan = sorted((e["table_id"], e["row_lo"], e["row_hi"], e["local_rank"]) for e in tr.plan())
+        assert got_plan == sorted(tuple(int(x) for x in e) for e in plan_real)
+        for g in range(o.M):
+            for f, (w, v) in enumerate(tr.replica_tables(g)):
+                wr = ws_real[g][f * o.rows * o.dim:(f + 1) * o.rows * o.dim].reshape(o.rows, o.dim)
+                assert np.array_equal(w.view(np.uint32), wr.view(np.uint32)), (g, f)
+                assert np.array_equal(v.view(np.uint32), vs_real[g][f * o.rows:(f + 1) * o.rows].view(np.uint32))
+    finally:
+        tr.close()
+
+
+def test_trainer_facade_default_upstream_checkpoint_metrics(tmp_path, port):
+    """Without a callback the facade trains on the synthetic upstream
+    (s2d_gen_upstream, equal to the oracle's or_synthetic_upstream); the
+    replicas agree after a sync step, the S2DCKPT1 save / load round trip
+    restores them, and MetricsRow comes from group 0."""
+    import paper_2508_03854_b200 as s2d
+
+    opts = s2d.TrainerOptions(total_ranks=4, groups=2, num_tables=3, rows_per_table=200, dim=16, ids_per_sample=4,
+                              per_rank_batch=32, steps=3, optimizer=s2d.OptimizerConfig(eta=0.1, c=2.0),
+                              devices=[0])
+    tr = s2d.Trainer(opts)
+    try:
+        tr.run()
+        t0, t1 = tr.replica_tables(0), tr.replica_tables(1)
+        for (w0, v0), (w1, v1) in zip(t0, t1):
+            assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+            assert np.array_equal(v0.view(np.uint32), v1.view(np.uint32))
+        assert any(np.any(v > 0) for _, v in t0)
+        m = tr.metrics_row()
+        assert m["rows"] == 600 and m["eff_lr_p50"] <= m["eff_lr_p99"]  # ascending lr percentiles
+        path = str(tmp_path / "t.ckpt")
+        tr.save_tables(path)
+        tr.step_n(2)
+        tr.load_tables(path)
+        for (w0, v0), (w1, v1) in zip(t0, tr.tables()):
+            assert np.array_equal(w0.view(np.uint32), w1.view(np.uint32))
+    finally:
+        tr.close()
+    eng = s2d.Sparse2DEmbedding([s2d.TableConfig(10, 12), s2d.TableConfig(7, 4)], s2d.Topology(1, 1))
+    try:
+        got = eng.gen_upstream(9, 4, 3, 17)
+        want = port.synthetic_upstream(9, 4, 3, 17, np.array([12, 4], np.uint32))
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    finally:
+        eng.close()
