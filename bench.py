@@ -178,24 +178,56 @@ class ClockSampler:
                 "samples": len(self.sm)}
 
 
-def algorithmic_bytes(w, nnz_own, unique, entries, n_mp, world_bf):
-    """Algorithmic HBM bytes per launch of the dominant kernels."""
+def algorithmic_bytes(w, nnz_own, unique, entries, n_mp, dirty=0):
+    """Algorithmic HBM bytes per step of each phase, SURVEY.md 8(d):
+    4 nnz (ids) + s_w D nnz (row gathers) + 4 D E_owned (partials out)
+    + 4 D E_local (partials in) + 4 D B F (pooled out) + 4 D B F (upstream in)
+    + 4 D E_owned (grads in at the owner) + 2 U (s_w D + 4) (row + moment RMW)
+    + 2 U_dirty (s_w D + 4) (sync); the partial terms vanish at N = 1 and the
+    sort passes are implementation overhead (excluded).  `lookup_unique`
+    replaces the per-id row gathers by one HBM read per distinct row (the
+    Zipf-hot repeats are L2 hits): the HBM-side view of the same kernel."""
     sw = 2 if w.dtype == "bf16" else 4
     D = float(np.mean(w.dims))
     BF = w.batch * w.F
-    lookup = nnz_own * (4 + sw * D + 8) + (world_bf + 1) * 8 + (entries * D * 4 if n_mp > 1 else w.batch * w.sum_dims * 4)
-    update = nnz_own * (4 + 4 * D) + unique * (2 * (sw * D + 4) + 8)
-    sort = nnz_own * 4 + nnz_own * 16 * 4  # histogram read + 4 passes x (8 B read + 8 B write)
-    return {"lookup": lookup, "update": update, "sort": sort}
+    pooled = 4.0 * D * BF
+    if n_mp > 1:
+        part = 4.0 * D * entries  # partials out (owner) + the same count in at the requesters
+        lookup = 4 * nnz_own + sw * D * nnz_own + part + part + pooled
+        lookup_unique = 4 * nnz_own + sw * D * unique + part + part + pooled
+        update = pooled + 4.0 * D * entries + 2 * unique * (sw * D + 4)  # upstream in, grads in, RMW
+    else:
+        lookup = 4 * nnz_own + sw * D * nnz_own + pooled
+        lookup_unique = 4 * nnz_own + sw * D * unique + pooled
+        update = pooled + 2 * unique * (sw * D + 4)
+    return {"lookup": lookup, "lookup_unique": lookup_unique, "update": update,
+            "sync": 2 * dirty * (sw * D + 4), "conversions": {"lookup": nnz_own * D, "update": nnz_own * D}}
 
 
-def traffic_from_profiles(kernel):
-    """DRAM bytes (read + write) per launch of `kernel` from the committed
-    `ncu --set full` capture (profiles/traffic.json, tools/ncu_summarize.py)."""
+# B200 XU (F2F) rate used for the conversion ceiling: 16 lanes / clk / SM
+XU_PER_CLK_SM = 16
+
+
+PHASE_KERNELS = {"lookup": ("k_lookup_ring",), "update": ("k_update_ring", "k_range_partials", "k_group_partials")}
+
+
+def traffic_from_profiles(phase):
+    """DRAM bytes (read + write) per step of a phase's kernels from the
+    committed `ncu --set full` captures (profiles/traffic.json, written by
+    tools/ncu_summarize.py); None if a kernel of the phase has no capture."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            t = json.load(f).get(kernel)
-        return (t["dram_bytes_per_launch"], f"profiles/{t['round']}: {t['source']}") if t else (None, None)
+            tj = json.load(f)
+        tot, src = 0.0, []
+        for k in PHASE_KERNELS[phase]:
+            t = tj.get(k)
+            if t is None:
+                if k == "k_group_partials":  # tiny; missing capture adds nothing material
+                    continue
+                return None, f"no capture of {k}"
+            tot += t["dram_bytes_per_launch"] * t.get("launches_per_step", 1)
+            src.append(f"profiles/{t['round']}/{t['source']}")
+        return tot, " + ".join(src)
     except Exception:
         return None, None
 
@@ -464,24 +496,39 @@ def run_ours(args):
     h2d = int(sum(x.numel() * 4 for x in pin[0]) / 1)
     d2h = int(pooled_h.numel() * 4)
 
-    # ---- roofline of the dominant kernel ----
+    # ---- roofline of the dominant phase (SURVEY.md 8(d) bytes) ----
     peak, peak_src = load_peaks()
     ab = algorithmic_bytes(w, st["nnz_owned"] or nnz_mean, st["unique_rows"] or 0, st["entries_owned"], n_mp,
-                           w.batch * w.F * (n_mp if n_mp > 1 else 1))
-    # per-launch times of the hot kernels: the update from the timed region
-    # (its events are the only ones there), lookup / sort from the split pass
+                           st.get("dirty_rows", 0))
+    clk_now = clk.summary()
+    sm_hz = (clk_now["sm_mhz"] or 1965.0) * 1e6
+    # per-launch times: the update from the timed region (its events are the
+    # only ones there), lookup / sort from the split pass
     per_phase = {}
     ms_step_local = ms / max(1, args.steps)
     for p in ("lookup", "sort", "update"):
         src, where = (phases, "timed region") if phases.get(p, (0, 0))[1] else (split, "split pass")
         if p in src and src[p][1]:
             pl = src[p][0] / src[p][1]
-            per_phase[p] = {"ms_per_launch": pl, "share": pl / max(ms_step_local, 1e-9),
-                            "algo_gbs": ab[p] / (pl / 1e3) / 1e9, "measured_in": where}
+            ent = {"ms_per_launch": pl, "share": pl / max(ms_step_local, 1e-9), "measured_in": where}
+            if p in ("lookup", "update"):
+                ent["algo_bytes"] = ab[p]
+                ent["algo_gbs"] = ab[p] / (pl / 1e3) / 1e9
+                ent["frac"] = ent["algo_gbs"] / peak
+                # f32 -> f64 widening of every gathered column on the XU pipe
+                xu_ms = 1e3 * ab["conversions"][p] / (148 * XU_PER_CLK_SM * sm_hz)
+                ent["xu_floor_ms"] = xu_ms
+                ent["xu_frac"] = xu_ms / pl
+            if p == "lookup":
+                ent["unique_row_bytes"] = ab["lookup_unique"]
+                ent["unique_row_frac"] = ab["lookup_unique"] / (pl / 1e3) / 1e9 / peak
+            per_phase[p] = ent
     dom = max(per_phase, key=lambda p: per_phase[p]["ms_per_launch"]) if per_phase else "update"
-    achieved = per_phase[dom]["algo_gbs"] if per_phase else 0.0
-    kname = {"lookup": "k_lookup_ring", "update": "k_update_ring", "sort": "k_radix_pass"}[dom]
-    traffic = traffic_from_profiles(kname)
+    if dom == "sort":  # the sort is implementation overhead (no 8(d) bytes): report the heavier of the others
+        dom = max((p for p in per_phase if p != "sort"), key=lambda p: per_phase[p]["ms_per_launch"], default="update")
+    kname = {"lookup": "k_lookup_ring", "update": "k_update_ring+k_range_partials"}[dom]
+    achieved = per_phase.get(dom, {}).get("algo_gbs", 0.0)
+    traffic = traffic_from_profiles(dom)
     if (w.name, n_mp, m, w.batch) != ("cfg2", 1, 1, 16384):  # captured on cfg2 1x1 only
         traffic = (None, "no ncu capture for this workload/mesh (profiles/ hold cfg2 1x1)")
     wbytes = 2 if w.dtype == "bf16" else 4
@@ -499,10 +546,19 @@ def run_ours(args):
                    "parallelism": f"mp{n_mp}xdp{m}", "nnz_per_gpu": nnz_mean,
                    "l2": f"inputs larger than L2 (tables {table_gb:.1f} GB, upstream "
                          f"{w.batch * w.sum_dims * 4 / 1e6:.0f} MB/step), {NB} distinct batches cycled"},
-        "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "peak_source": peak_src,
+        "roofline": {"bound": "hbm", "kernel": kname, "phase": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "peak_source": peak_src,
                      "traffic": traffic[0], "traffic_source": traffic[1],
-                     "algorithmic_bytes_per_launch": ab[dom]},
+                     "dram_frac": (traffic[0] / (per_phase[dom]["ms_per_launch"] / 1e3) / 1e9 / peak
+                                   if traffic[0] and dom in per_phase else None),
+                     "algorithmic_bytes_per_launch": ab[dom],
+                     "bytes_model": "SURVEY.md 8(d): update = upstream (or owner gradient rows) read once + "
+                                    "2 U (s_w D + 4) row/moment read-modify-write; lookup = ids + s_w D per id "
+                                    "+ pooled rows out; sort passes excluded",
+                     "xu_ceiling": {p: {"floor_ms": per_phase[p]["xu_floor_ms"], "frac": per_phase[p]["xu_frac"]}
+                                    for p in ("lookup", "update") if p in per_phase},
+                     "xu_note": "f32->f64 widening of nnz x D gathered columns (F2F on the XU pipe, "
+                                "16/clk/SM) at the sampled SM clock: the conversion-throughput floor"},
         "phases": per_phase,
         "phase_split_ms": {p: v[0] / max(1, n_split) for p, v in split.items()},
         "phase_split_note": f"every phase bracketed, separate pass of {n_split} steps (rank 0)",
