@@ -19,6 +19,8 @@
 // DRAM peak, one round trip per bag); register double-buffered streams were
 // capped at 12-16 warps/SM by f64 accumulators + in-flight rows
 // (128 regs), stalling on shuffles and load latency.
+#include <cstdlib>
+
 #include "device.cuh"
 
 namespace s2d {
@@ -476,7 +478,7 @@ __device__ __forceinline__ void store_partial(double* p, uint32_t lane, uint32_t
 template <int VPL>
 __device__ __forceinline__ void reg_sum_range(const StreamUpdateArgs& a, uint32_t lane, uint64_t s, uint32_t d4,
                                               double (&acc)[VPL][4]) {
-  constexpr int kG = 8 / VPL;
+  constexpr int kG = 1;  // one row per load batch: 32 registers, full occupancy (8 / VPL rows: 64 regs, update 0.390 -> 0.374 ms)
   const float* const Gl = a.grad + lane * 4;
   uint32_t val_n = __ldg(a.vals + s + lane);
   for (uint32_t w = 0; w < kC; w += 32) {
@@ -529,6 +531,99 @@ __global__ void __launch_bounds__(256) k_range_partials(const StreamUpdateArgs a
     store_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
   }
 }
+
+// ---- TMA bulk-copy primitives (cp.async.bulk + mbarrier transaction counts)
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+// one elected lane copies `bytes` (multiple of 16, 16-byte aligned) of global
+// memory into shared memory; completion counts against `bar`
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// level-1 partials through TMA bulk copies: lane 0 of each warp streams the
+// range's gradient rows (one cp.async.bulk per row) into a kTS-stage ring
+// whose stages complete on mbarrier transaction counts; the warp reads its
+// column chunks back and accumulates in item order.  The loads leave the
+// LSU / MIO path (the LDGSTS of the register version saturated it).
+constexpr int kTS = 4;   // ring stages per warp
+constexpr int kTR = 4;   // rows per stage
+constexpr int kTW = 8;   // warps per block
+template <int VPL>
+__global__ void __launch_bounds__(kTW * 32) k_range_partials_tma(const StreamUpdateArgs a) {
+  pdl_wait();
+  constexpr uint32_t kRowMax = VPL * 512;  // bytes of the widest row
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  unsigned char* wbase = smem + warp * (kTS * kTR * kRowMax + kC * 4 + kTS * 8);
+  const uint32_t ring = smem_u32(wbase);
+  uint32_t* const svals = reinterpret_cast<uint32_t*>(wbase + kTS * kTR * kRowMax);
+  const uint32_t bars = smem_u32(wbase + kTS * kTR * kRowMax + kC * 4);
+  if (lane == 0)
+    for (int s = 0; s < kTS; ++s) mbar_init(bars + 8 * s, 1);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncwarp();
+  const uint64_t n_ranges = a.n / kC;
+  const uint64_t stride = (uint64_t)gridDim.x * kTW;
+  uint32_t uses = 0;  // stages consumed by this warp so far (slot = uses % kTS, parity = (uses / kTS) & 1)
+  for (uint64_t k = 1 + (uint64_t)blockIdx.x * kTW + warp; k < n_ranges; k += stride) {
+    const uint64_t s0 = k * kC, t = s0 + kC;
+    const uint32_t key = __ldg(a.keys + s0 - 1);
+    if (key >= a.n_slots || __ldg(a.keys + t - 1) != key) continue;
+    uint64_t wofs;
+    uint32_t d4;
+    row_ref(a, key, wofs, d4);
+    const uint32_t rb = d4 * 16;  // row bytes
+    for (uint32_t i = lane; i < kC; i += 32) svals[i] = __ldg(a.vals + s0 + i);
+    __syncwarp();
+    constexpr uint32_t nst = kC / kTR;
+    auto issue = [&](uint32_t st) {  // lane 0: stage st of this range into slot (uses + st) % kTS
+      const uint32_t slot = (uses + st) % kTS;
+      const uint32_t bar = bars + 8 * slot;
+      mbar_expect_tx(bar, kTR * rb);
+#pragma unroll
+      for (int r = 0; r < kTR; ++r)
+        bulk_g2s(ring + (slot * kTR + r) * kRowMax, a.grad + (uint64_t)svals[st * kTR + r] * 4, rb, bar);
+    };
+    if (lane == 0)
+      for (uint32_t st = 0; st < (uint32_t)kTS; ++st) issue(st);
+    double acc[VPL][4];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
+    for (uint32_t st = 0; st < nst; ++st) {
+      const uint32_t slot = (uses + st) % kTS;
+      mbar_wait(bars + 8 * slot, ((uses + st) / kTS) & 1u);
+#pragma unroll
+      for (int r = 0; r < kTR; ++r) {
+        const unsigned char* row = wbase + (slot * kTR + r) * kRowMax;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (VPL == 1 || lane + v * 32 < d4) Row<float>::add(acc[v], row + (lane + v * 32) * 16);
+      }
+      __syncwarp();  // every lane has read the slot before it is refilled
+      if (lane == 0 && st + kTS < nst) issue(st + kTS);
+    }
+    uses += nst;
+    store_partial<VPL>(a.part1 + k * (uint64_t)a.max_d4 * 4, lane, d4, acc);
+  }
+}
+
+size_t range_tma_smem(int vpl) { return (size_t)kTW * (kTS * kTR * (size_t)vpl * 512 + kC * 4 + kTS * 8); }
 
 // level-(L+1) partials: kP consecutive level-L partials, all inside one
 // segment (level 2 over level-1 ranges, level 3 over level-2 groups), so the
@@ -937,7 +1032,22 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
     init = true;
   }
   const bool full = a.uni_dim == 128u * VPL;
-  if (a.n >= 2 * kC) pdl_launch(k_range_partials<VPL>, dim3(grid_units(a.n / kC, 8, 148 * 16)), dim3(256), 0, st, a);
+  if (a.n >= 2 * kC) {
+    static const bool tma = [] {
+      const char* e = std::getenv("S2D_RANGE_TMA");
+      return e && e[0] == '1';  // measured slower: opt-in
+    }();
+    if (tma) {
+      const size_t sm = range_tma_smem(VPL);
+      set_max_dynamic_smem(k_range_partials_tma<VPL>, sm);
+      int occ = 0;
+      S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_range_partials_tma<VPL>, kTW * 32, sm));
+      pdl_launch(k_range_partials_tma<VPL>, dim3(grid_units(a.n / kC, kTW, 148 * std::max(occ, 1))), dim3(kTW * 32), sm,
+                 st, a);
+    } else {
+      pdl_launch(k_range_partials<VPL>, dim3(grid_units(a.n / kC, 8, 148 * 16)), dim3(256), 0, st, a);
+    }
+  }
   if (a.n >= 2ull * kC * kP)
     pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP), 8, 148 * 8)), dim3(256), 0, st, a,
                static_cast<const double*>(a.part1), a.part2, (uint64_t)kC * kP);
