@@ -39,6 +39,7 @@ def parse():
     p.add_argument("--mesh", default=None, help="NxM (MP ranks per group x DP groups); default N x 1")
     p.add_argument("--batch", type=int, default=None, help="per-GPU batch override")
     p.add_argument("--strategy", default=None)
+    p.add_argument("--scramble", action="store_true", help="hashed id -> row bijection (balances row-wise owners)")
     p.add_argument("--nbatches", type=int, default=3, help="distinct input batches cycled")
     p.add_argument("--e2e-steps", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -75,6 +76,8 @@ def workload(args, world):
         w.batch = args.batch
     if args.strategy:
         w.strategy = args.strategy
+    if args.scramble:
+        w.scramble = True
     return w
 
 
@@ -540,7 +543,8 @@ def run_ours(args):
         "dtype": "f64",  # arithmetic type of the path (f64 accumulation, as the reference)
         "storage_dtype": "bf16" if w.dtype == "bf16" else "f32",
         "data": "synthetic (seeded Zipf ids, power-law bag lengths, N(0,1e-3) upstream)",
-        "config": {"workload": w.name + ": " + w.describe, "global_batch": world * w.batch,
+        "config": {"workload": w.name + ": " + w.describe + (" (ids scrambled)" if w.scramble else ""),
+                   "global_batch": world * w.batch,
                    "per_gpu_batch": w.batch, "tables": w.F, "dim": int(np.max(w.dims)),
                    "mesh": f"{n_mp}x{m}", "strategy": w.strategy, "optimizer": f"rowwise-adagrad c={w.c}",
                    "parallelism": f"mp{n_mp}xdp{m}", "nnz_per_gpu": nnz_mean,

@@ -308,10 +308,12 @@ int s2d_get_step_stats(s2d_ctx* ctx, s2d_step_stats* out);
 /* Per-phase device time (CUDA events on the context's stream), summed since
  * the last query.  Phases: 0 input staging, 1 K1 bucketing, 2 id all-to-all,
  * 3 K2 lookup, 4 pooled all-to-all, 5 combine, 6 grad gather, 7 grad
- * all-to-all, 8 radix sort, 9 host count sync (N > 1), 10 fused update, 11 replica sync.
- * n must be >= 12.  Profiling is off by default; on = 1 times every phase,
- * on = 2 only the fused update (phase 10; fewer stream drains). */
-#define S2D_NUM_PHASES 12
+ * all-to-all, 8 radix sort, 9 host count sync (N > 1), 10 fused update,
+ * 11 replica sync (dirty-row union), 12 sync push, 13 sync mean, 14 sync
+ * scatter.  n must be >= 12 (the first n phases are written).  Profiling is
+ * off by default; on = 1 times every phase, on = 2 only the fused update
+ * (phase 10; fewer stream drains). */
+#define S2D_NUM_PHASES 15
 int s2d_ctx_set_profiling(s2d_ctx* ctx, int on);
 int s2d_get_phase_times(s2d_ctx* ctx, double* ms, uint32_t* counts, uint32_t n);
 

@@ -578,7 +578,7 @@ class Sparse2DEmbedding:
         return {k: getattr(s, k) for k, _ in L.StepStats._fields_}
 
     PHASES = ("input", "bucket", "a2a_ids", "lookup", "a2a_lookup", "combine", "grad_gather", "a2a_grad",
-              "sort", "count_sync", "update", "sync")
+              "sort", "count_sync", "update", "sync", "sync_push", "sync_mean", "sync_scatter")
 
     def set_profiling(self, on, hot_only: bool = False):
         """Phase events on the engine stream; hot_only brackets only the fused
@@ -588,9 +588,10 @@ class Sparse2DEmbedding:
     def phase_times(self) -> dict:
         """{phase: (ms, launches)} summed since the last call (CUDA events on
         the engine's stream)."""
-        ms = (C.c_double * 12)()
-        cnt = (C.c_uint32 * 12)()
-        L.check(self.lib.s2d_get_phase_times(self._ctx, ms, cnt, 12))
+        n = len(self.PHASES)
+        ms = (C.c_double * n)()
+        cnt = (C.c_uint32 * n)()
+        L.check(self.lib.s2d_get_phase_times(self._ctx, ms, cnt, n))
         return {p: (ms[i], cnt[i]) for i, p in enumerate(self.PHASES)}
 
     # Phases whose device time carries each reference collective.  The
@@ -601,7 +602,7 @@ class Sparse2DEmbedding:
     TRACE_PHASES = {
         "lookup_a2a": ("a2a_ids", "lookup", "a2a_lookup", "combine"),
         "grad_a2a": ("grad_gather", "a2a_grad"),
-        "table_allreduce": ("sync",),
+        "table_allreduce": ("sync", "sync_push", "sync_mean", "sync_scatter"),
     }
 
     def trace_rows(self, step: int) -> list[dict]:

@@ -256,8 +256,14 @@ int s2d_ctx_set_profiling(s2d_ctx* ctx, int on) {
 
 int s2d_get_phase_times(s2d_ctx* ctx, double* ms, uint32_t* counts, uint32_t n) {
   return guarded([&] {
-    if (n < (uint32_t)s2d::kNumPhases) throw Error(S2D_EINVAL, "need room for every phase");
-    as_ctx(ctx)->phase_times(ms, counts);
+    if (n < 12) throw Error(S2D_EINVAL, "need room for at least the 12 step phases");
+    double all_ms[s2d::kNumPhases];
+    uint32_t all_cnt[s2d::kNumPhases];
+    as_ctx(ctx)->phase_times(all_ms, all_cnt);
+    for (uint32_t i = 0; i < n && i < (uint32_t)s2d::kNumPhases; ++i) {
+      ms[i] = all_ms[i];
+      if (counts) counts[i] = all_cnt[i];
+    }
   });
 }
 

@@ -2,15 +2,27 @@
 // embedding phases only):
 //
 //   N == 1:  lengths -> id offsets (scan) -> K2 lookup writes pooled rows and
-//            (slot, upstream-row) pairs -> [backward] radix sort -> segments
-//            -> K3+K4 fused update straight from the upstream gradient.
-//   N  > 1:  K1 count + scans + permute -> NCCL: counts, then lengths + ids
-//            inside the MP group -> owner K2 partials -> NCCL pooled a2a (C1)
-//            -> requester combine.  [backward] grad gather -> NCCL grad a2a
-//            (C2) -> radix sort -> segments -> fused update.
-//   M  > 1:  replica_sync(): byte-max all-reduce of dirty flags in the DP
-//            group -> ordered dirty list -> pack -> NCCL all-gather -> f64
-//            ascending-group mean (C3).
+//            (slot, upstream-row) pairs -> [backward] radix sort -> K3b/K4
+//            range partials + fused segment reduce / AdaGrad straight from the
+//            upstream gradient.
+//   N  > 1:  K1 count (lengths stored into the owners' receive buffers over
+//            peer memory) + scans -> count matrix published to every peer ->
+//            barrier -> one host read of the matrix (buffer sizes) -> K1
+//            permute (ids stored into the owners' buffers) -> barrier -> owner
+//            K2 lookup storing partials / final pooled rows into the
+//            requesters' buffers (C1 fused) -> barrier -> requester combine;
+//            the sort of the owner's pairs starts on a side stream right after
+//            the lookup.  [backward] gradient gather storing each (bag, owner)
+//            upstream row into the owner's buffer (C2 fused) -> barrier ->
+//            fused update.
+//   M  > 1:  replica_sync(): dirty-flag lists all-gathered into one ascending
+//            union; over peer memory each replica owns a slice of the union,
+//            receives every replica's copy of its rows, forms the f64
+//            ascending-group mean and stores it into every replica (C3);
+//            NCCL all-gather + mean is the fallback when the DP group cannot
+//            map each other's memory.
+// Barriers are device flags (st.release / ld.acquire, system scope) across
+// processes, host rendezvous between virtual ranks of one process (comm.h).
 //
 // Every buffer on the wire has the reference's layout: demand ids per owner
 // in (requester, sample, feature, occurrence) order, one partial / gradient
@@ -1075,12 +1087,15 @@ void Ctx::replica_sync() {
     PeerPtrs means{};
     for (uint32_t g = 0; g < M; ++g) means.p[g] = reinterpret_cast<float*>(dp_stage.ptr[g]) + copies;
     const int sgd = opt.variant == S2D_SGD;
+    phase_begin(kPhSyncPush);
     launch_p2p_push(ptrs(dp_stage), group, M, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
                     d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), count,
                     weights.p, bf16, moments.as<float>(), row_floats, slice_cap, stream);
     dp_barrier();  // every copy of every slice is staged at its owner
+    phase_begin(kPhSyncMean);
     launch_p2p_mean(dp_stage.buf.as<float>(), means, M, lo, hi, row_floats, slice_cap, sgd, stream);
     dp_barrier();  // every replica's staging holds every mean
+    phase_begin(kPhSyncScatter);
     launch_p2p_scatter(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
                        (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), count, dp_stage.buf.as<float>() + copies,
                        row_floats, weights.p, bf16, moments.as<float>(), sgd, stream);

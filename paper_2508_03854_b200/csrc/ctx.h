@@ -33,7 +33,10 @@ enum Phase : int {
   kPhSort,        // K3a radix sort
   kPhCountSync,   // N > 1: host read of the count matrix (GPU waits for the next launch)
   kPhUpdate,      // K3b chunk sums + K4 fused update
-  kPhSync,        // K5 replica sync
+  kPhSync,        // K5 replica sync: dirty-row union (flag compaction, list exchange, host reads)
+  kPhSyncPush,    // K5: rows pushed to the slice owners + barrier
+  kPhSyncMean,    // K5: slice means stored into every replica + barrier
+  kPhSyncScatter, // K5: means scattered into the shard, dirty flags cleared
   kNumPhases
 };
 
