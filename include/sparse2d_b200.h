@@ -195,10 +195,14 @@ int s2d_ctx_set_stream(s2d_ctx* ctx, void* cuda_stream);
 int s2d_ctx_set_strict(s2d_ctx* ctx, int strict);
 
 /* async = 0 (default): an S2D_HOST pooled output is complete when
- * s2d_lookup_forward returns.  async = 1: the read-back runs on the
- * context's D2H copy stream and completes by the end of the following
- * s2d_backward_update's work (or at s2d_synchronize), so it overlaps that
- * call's upstream upload and sort.  Host buffers must stay valid until then. */
+ * s2d_lookup_forward returns.  async = 1: host inputs go up on the context's
+ * H2D copy stream and the pooled read-back runs on its D2H copy stream,
+ * overlapping the upstream upload, the sort and the update; at N = 1 two
+ * staging buffers alternate, so the next step's lookup also overlaps it and
+ * the read-back is complete at s2d_synchronize (or when the forward after
+ * next reuses its staging); at N > 1 it completes by the end of the
+ * following s2d_backward_update's work.  Host buffers must stay valid (and
+ * unchanged) until then. */
 int s2d_ctx_set_async_host(s2d_ctx* ctx, int async);
 
 /* Tables + plan (the identical-in-every-group plan).  The

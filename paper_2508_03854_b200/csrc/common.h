@@ -308,13 +308,14 @@ void launch_pack_rows(const FeatDev* feats, const uint32_t* vbase_sorted,
 // staging means; each replica scatters the means into its shard
 void launch_p2p_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
                      const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                     const uint32_t* list, uint32_t count, const void* weights, int bf16, const float* moments,
-                     uint32_t row_floats, uint64_t slice_cap, cudaStream_t st);
-void launch_p2p_mean(const float* local, const PeerPtrs& means, uint32_t M, uint32_t lo, uint32_t hi,
-                     uint32_t row_floats, uint64_t slice_cap, int sgd, cudaStream_t st);
+                     const uint32_t* list, const uint32_t* count, uint32_t count_ub, const void* weights, int bf16,
+                     const float* moments, uint32_t row_floats, uint64_t slice_cap, cudaStream_t st);
+void launch_p2p_mean(const float* local, const PeerPtrs& means, uint32_t M, uint32_t me, const uint32_t* count,
+                     uint32_t count_ub, uint32_t row_floats, uint64_t slice_cap, int sgd, cudaStream_t st);
 void launch_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
-                        uint32_t n_feat, const uint32_t* list, uint32_t count, const float* means, uint32_t row_floats,
-                        void* weights, int bf16, float* moments, int sgd, cudaStream_t st);
+                        uint32_t n_feat, const uint32_t* list, const uint32_t* count, uint32_t count_ub,
+                        const float* means, uint32_t row_floats, void* weights, int bf16, float* moments, int sgd,
+                        cudaStream_t st);
 void launch_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted,
                       const uint32_t* feat_of_vbase, uint32_t n_feat_owned, const uint32_t* list,
                       const uint32_t* count, const float* gathered, uint32_t M, uint32_t row_floats,

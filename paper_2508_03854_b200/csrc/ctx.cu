@@ -99,12 +99,13 @@ Ctx::~Ctx() {
     for (void* q : pb->opened) cudaIpcCloseMemHandle(q);
   for (void* q : dp_opened) cudaIpcCloseMemHandle(q);
   for (auto e : ev_pool) cudaEventDestroy(e);
-  for (cudaStream_t q : {h2d_stream, d2h_stream, sort_stream})
+  for (cudaStream_t q : {h2d_stream, d2h_stream, sort_stream, sync_stream})
     if (q) {
       cudaStreamSynchronize(q);
       cudaStreamDestroy(q);
     }
-  for (cudaEvent_t e : {ev_fwd, ev_d2h, ev_up, ev_upd, ev_keys, ev_sorted})
+  for (cudaEvent_t e : {ev_fwd, ev_d2h, ev_up, ev_keys, ev_sorted, ev_union, ev_sync_done, ev_in_ready, ev_in_used[0],
+                        ev_in_used[1], ev_up_used[0], ev_up_used[1], ev_d2h_done[0], ev_d2h_done[1]})
     if (e) cudaEventDestroy(e);
   dp.destroy();
   mp.destroy();
@@ -138,7 +139,10 @@ void Ctx::create(int dev, uint32_t total, uint32_t groups, uint32_t r, const uin
   S2D_CUDA(cudaStreamCreateWithFlags(&h2d_stream, cudaStreamNonBlocking));
   S2D_CUDA(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking));
   S2D_CUDA(cudaStreamCreateWithFlags(&sort_stream, cudaStreamNonBlocking));
-  for (cudaEvent_t* e : {&ev_fwd, &ev_d2h, &ev_up, &ev_upd, &ev_keys, &ev_sorted})
+  S2D_CUDA(cudaStreamCreateWithFlags(&sync_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_fwd, &ev_d2h, &ev_up, &ev_keys, &ev_sorted, &ev_union, &ev_sync_done, &ev_in_ready,
+                         &ev_in_used[0], &ev_in_used[1], &ev_up_used[0], &ev_up_used[1], &ev_d2h_done[0],
+                         &ev_d2h_done[1]})
     S2D_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
   err.ensure(4);
   S2D_CUDA(cudaMemsetAsync(err.p, 0, 4, stream));
@@ -301,6 +305,7 @@ void Ctx::set_optimizer(const s2d_optimizer_config& c) {
 void Ctx::init_tables(uint64_t seed) {
   if (!F) throw Error(S2D_EINVAL, "register tables first");
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   launch_init_rows(weights.p, bf16, feats.data(), F, seed, stream);
   S2D_CUDA(cudaMemsetAsync(moments.p, 0, (size_t)n_slots * 4, stream));
   if (M > 1) S2D_CUDA(cudaMemsetAsync(dirty.p, 0, n_slots, stream));
@@ -316,6 +321,7 @@ void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v,
                                 std::to_string(table));
   if (hi == lo) return;
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   S2D_CUDA(cudaStreamSynchronize(stream));
   const uint64_t n = (uint64_t)(hi - lo) * fd.dim;
   const uint64_t off = fd.wbase + (uint64_t)(lo - fd.lo) * fd.dim;
@@ -386,6 +392,7 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
   const uint32_t nseg = (uint32_t)seg.size();
   seg.push_back(n);
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   S2D_CUDA(cudaStreamSynchronize(stream));
   const size_t b_order = (size_t)n * 4, b_seg = seg.size() * 4, b_row = (size_t)nseg * 4;
   const size_t b_delta = (size_t)n * fd.dim * 8, b_mom = (size_t)n * 8;
@@ -424,6 +431,7 @@ void Ctx::gather_rows(uint32_t table, uint32_t n, const uint32_t* rows, float* w
     loc[i] = rows[i] - fd.lo;
   }
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   S2D_CUDA(cudaStreamSynchronize(stream));
   const size_t bw = (size_t)n * fd.dim * 4, bv = (size_t)n * 4;
   gather_scratch.ensure(bw + bv + (size_t)n * 4 + 64);
@@ -458,6 +466,7 @@ void Ctx::finish_call() {
 
 void Ctx::synchronize_and_check() {
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   S2D_CUDA(cudaStreamSynchronize(h2d_stream));
   S2D_CUDA(cudaStreamSynchronize(d2h_stream));
   S2D_CUDA(cudaStreamSynchronize(sort_stream));
@@ -480,11 +489,13 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   const uint64_t BF = (uint64_t)B * F;
   stats = s2d_step_stats{};
   stats_counters_valid = false;
+  sync_stats_pending = false;  // the counters describe this step from here on
   stats.nnz_local = nnz;
   if (sort_pending) {  // a forward without its backward: its sort still reads the keys
     S2D_CUDA(cudaStreamWaitEvent(stream, ev_sorted, 0));
     sort_pending = false;
   }
+  if (N == 1) join_sync();  // the lookup below reads the weights (N > 1: after the id exchange)
   // stage inputs
   phase_begin(kPhInput);
   const uint32_t* d_len = lengths;
@@ -499,18 +510,36 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
   // group never depend on a per-rank choice (B itself must agree across the
   // MP group; read_counts checks it every step)
   if (N > 1) peer_alloc(p_pooled, (uint64_t)B * sum_dims * 4);
-  if (engine_out) {
+  // N == 1 host mode: the read-back alternates between two staging buffers,
+  // so this step's lookup runs while the previous step's rows still travel
+  // to the host (the buffer written now was last read back two steps ago)
+  const bool host_pair = mem == S2D_HOST && N == 1;
+  if (host_pair) {
+    out_sel ^= 1;
+    if (d2h_done_rec[out_sel]) S2D_CUDA(cudaStreamWaitEvent(stream, ev_d2h_done[out_sel], 0));
+    p_pooled_host[out_sel].ensure((uint64_t)B * sum_dims * 4);
+    d_pooled = p_pooled_host[out_sel].as<float>();
+  } else if (engine_out) {
     if (d2h_pending) S2D_CUDA(cudaStreamWaitEvent(stream, ev_d2h, 0));  // last read-back of the buffer
     if (N == 1) p_pooled_local.ensure((uint64_t)B * sum_dims * 4);
     d_pooled = N > 1 ? p_pooled.buf.as<float>() : p_pooled_local.as<float>();
   }
   if (mem == S2D_HOST) {
-    in_lengths.ensure(BF * 4);
-    in_ids.ensure(std::max<uint64_t>(nnz, 1) * 4);
-    S2D_CUDA(cudaMemcpyAsync(in_lengths.p, lengths, BF * 4, cudaMemcpyHostToDevice, stream));
-    if (nnz) S2D_CUDA(cudaMemcpyAsync(in_ids.p, ids, nnz * 4, cudaMemcpyHostToDevice, stream));
-    d_len = in_lengths.as<uint32_t>();
-    d_ids = in_ids.as<uint32_t>();
+    // ids + lengths go up on the H2D copy stream into one of two staging
+    // pairs (the one this forward's predecessor-but-one read), so the upload
+    // overlaps the previous step's update; the compute stream waits here
+    in_sel ^= 1;
+    DevBuf& bl = in_len2[in_sel];
+    DevBuf& bi = in_ids2[in_sel];
+    bl.ensure(BF * 4);
+    bi.ensure(std::max<uint64_t>(nnz, 1) * 4);
+    if (in_used_rec[in_sel]) S2D_CUDA(cudaStreamWaitEvent(h2d_stream, ev_in_used[in_sel], 0));
+    S2D_CUDA(cudaMemcpyAsync(bl.p, lengths, BF * 4, cudaMemcpyHostToDevice, h2d_stream));
+    if (nnz) S2D_CUDA(cudaMemcpyAsync(bi.p, ids, nnz * 4, cudaMemcpyHostToDevice, h2d_stream));
+    S2D_CUDA(cudaEventRecord(ev_in_ready, h2d_stream));
+    S2D_CUDA(cudaStreamWaitEvent(stream, ev_in_ready, 0));
+    d_len = bl.as<uint32_t>();
+    d_ids = bi.as<uint32_t>();
   }
   scan_tmp.ensure(scan_tmp_bytes(std::max<uint64_t>((uint64_t)N * BF, nnz) + 1));
   in_off.ensure((BF + 1) * 4);
@@ -618,6 +647,7 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
     a.unit_rot = ((uint64_t)((local + 1) % N) * BF) / 32;  // start at the next requester
+    join_sync();  // the bucketing and id exchange above overlapped the last replica sync's tail
     phase_begin(kPhLookup);
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     // the gradient rows' (slot, offset) pairs are final: sort them now
@@ -658,12 +688,22 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     stats.a2a_bytes_recv = recv;
   }
   if (mem == S2D_HOST) {
-    // read-back on the D2H stream: overlaps the upstream upload and the sort
+    // every reader of this forward's input staging is queued: the next
+    // upload into it waits for this point
+    S2D_CUDA(cudaEventRecord(ev_in_used[in_sel], stream));
+    in_used_rec[in_sel] = true;
+    // read-back on the D2H stream: overlaps the upstream upload, the sort and
+    // the update (and, N == 1, the next step's lookup)
     S2D_CUDA(cudaEventRecord(ev_fwd, stream));
     S2D_CUDA(cudaStreamWaitEvent(d2h_stream, ev_fwd, 0));
     S2D_CUDA(cudaMemcpyAsync(pooled, d_pooled, (uint64_t)B * sum_dims * 4, cudaMemcpyDeviceToHost, d2h_stream));
-    S2D_CUDA(cudaEventRecord(ev_d2h, d2h_stream));
-    d2h_pending = true;
+    if (host_pair) {
+      S2D_CUDA(cudaEventRecord(ev_d2h_done[out_sel], d2h_stream));
+      d2h_done_rec[out_sel] = true;
+    } else {
+      S2D_CUDA(cudaEventRecord(ev_d2h, d2h_stream));
+      d2h_pending = true;
+    }
     if (!async_host) S2D_CUDA(cudaStreamSynchronize(d2h_stream));
   }
   phase_end();
@@ -772,13 +812,13 @@ void Ctx::dp_setup() {
 // could wait behind that peer's host thread, which an implicitly
 // device-synchronising runtime call (first-touch cudaMalloc / cudaMallocHost)
 // can stall.  Across processes the barrier stays on the device.
-void Ctx::dp_barrier() {
+void Ctx::dp_barrier(cudaStream_t st) {
   if (dp.local()) {
-    dp.barrier(stream, hbuf);
+    dp.barrier(st, hbuf);
     return;
   }
   ++dp_epoch;
-  launch_peer_barrier(ptrs(dp_flags), dp_flags.buf.as<uint64_t>(), group, M, dp_epoch, err.as<uint32_t>(), stream);
+  launch_peer_barrier(ptrs(dp_flags), dp_flags.buf.as<uint64_t>(), group, M, dp_epoch, err.as<uint32_t>(), st);
 }
 
 void Ctx::peer_barrier() {
@@ -889,12 +929,13 @@ void Ctx::backward_update(const float* upstream, int mem) {
   if (mem == S2D_HOST) {
     // upload on the H2D stream once the previous update stopped reading the
     // staging buffer; the compute stream waits only where rows are read
-    upstream_stage.ensure((uint64_t)B * sum_dims * 4);
-    if (upd_recorded) S2D_CUDA(cudaStreamWaitEvent(h2d_stream, ev_upd, 0));
-    S2D_CUDA(cudaMemcpyAsync(upstream_stage.p, upstream, (uint64_t)B * sum_dims * 4, cudaMemcpyHostToDevice,
+    up_sel ^= 1;  // two staging buffers: the upload overlaps the update that reads the other one
+    up_stage2[up_sel].ensure((uint64_t)B * sum_dims * 4);
+    if (up_used_rec[up_sel]) S2D_CUDA(cudaStreamWaitEvent(h2d_stream, ev_up_used[up_sel], 0));
+    S2D_CUDA(cudaMemcpyAsync(up_stage2[up_sel].p, upstream, (uint64_t)B * sum_dims * 4, cudaMemcpyHostToDevice,
                              h2d_stream));
     S2D_CUDA(cudaEventRecord(ev_up, h2d_stream));
-    d_up = upstream_stage.as<float>();
+    d_up = up_stage2[up_sel].as<float>();
     up_wait = true;
   }
   const float* grad = d_up;
@@ -1010,10 +1051,11 @@ void Ctx::backward_update(const float* upstream, int mem) {
   (void)uniq;
   if (up_wait) S2D_CUDA(cudaStreamWaitEvent(stream, ev_up, 0));  // n == 0: nothing read it
   if (mem == S2D_HOST) {
-    S2D_CUDA(cudaEventRecord(ev_upd, stream));
-    upd_recorded = true;
+    S2D_CUDA(cudaEventRecord(ev_up_used[up_sel], stream));
+    up_used_rec[up_sel] = true;
   }
-  // the step is complete when its update and its pooled read-back are
+  // N > 1: the step is complete when its update and its pooled read-back are
+  // (the peer-mapped pooled buffer is written by the owners of the next step)
   if (d2h_pending) S2D_CUDA(cudaStreamWaitEvent(stream, ev_d2h, 0));
   phase_end();
   fwd_done = false;
@@ -1022,8 +1064,19 @@ void Ctx::backward_update(const float* upstream, int mem) {
 }
 
 void Ctx::refresh_stats() {
-  if (!stats_counters_valid) return;
   S2D_CUDA(cudaSetDevice(device));
+  if (sync_stats_pending) {  // the last replica sync's union length (device-side count)
+    join_sync();
+    S2D_CUDA(cudaStreamSynchronize(stream));
+    uint32_t count = 0;
+    S2D_CUDA(cudaMemcpy(&count, sync_count.p, 4, cudaMemcpyDeviceToHost));
+    const uint64_t rf = max_dim + 4;
+    const uint64_t lo = (uint64_t)count * group / M, hi = (uint64_t)count * (group + 1) / M;
+    stats.dirty_rows = count;
+    stats.sync_bytes = 2 * (hi - lo) * (M - 1) * rf * 4 + (uint64_t)sync_cmax * 4 * (M - 1);
+    sync_stats_pending = false;
+  }
+  if (!stats_counters_valid) return;
   S2D_CUDA(cudaStreamSynchronize(stream));
   uint32_t c[4];
   S2D_CUDA(cudaMemcpy(c, counters.p, 16, cudaMemcpyDeviceToHost));
@@ -1033,9 +1086,19 @@ void Ctx::refresh_stats() {
 
 // ---- K5 replica sync ---------------------------------------------------------
 
+// The weights / moments / dirty flags are final only once the previous
+// replica sync's tail (on sync_stream) has run: every reader and writer of
+// them on the main stream joins it first.
+void Ctx::join_sync() {
+  if (!sync_pending) return;
+  S2D_CUDA(cudaStreamWaitEvent(stream, ev_sync_done, 0));
+  sync_pending = false;
+}
+
 void Ctx::replica_sync() {
   if (M <= 1 || !F) return;
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   phase_begin(kPhSync);
   // Union of the dirty rows across the DP group in O(dirty rows) wire bytes:
   // each replica compacts its own flags into an ascending slot list, the
@@ -1067,44 +1130,66 @@ void Ctx::replica_sync() {
   dp.allgather(sync_list.p, sync_lists.p, (size_t)cmax * 4, stream);
   launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
+  const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
+  dp_setup();
+  if (dp_p2p == 1) {
+    // The union's length stays on the device: every size below uses the
+    // bound count_ub = min(M * cmax, n_slots), identical on every replica,
+    // and the kernels read the count itself.  Every replica's update of this
+    // step is complete (the list all-gather above ran after each replica's
+    // update on its stream, and the host read its counts).  Slice s of the
+    // union list is averaged by replica s.  Staging per replica:
+    // [M][slice_cap] copies of its slice | [count_ub] means.
+    const uint32_t count_ub = (uint32_t)std::min<uint64_t>((uint64_t)M * cmax, n_slots);
+    sync_list.ensure((uint64_t)count_ub * 4);
+    launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+    const uint64_t slice_cap = (uint64_t)count_ub / M + 1;
+    const uint64_t copies = slice_cap * M * row_floats;
+    peer_alloc_in(dp_stage, (copies + (uint64_t)count_ub * row_floats) * 4, dp);  // same size everywhere
+    PeerPtrs means{};
+    for (uint32_t g = 0; g < M; ++g) means.p[g] = reinterpret_cast<float*>(dp_stage.ptr[g]) + copies;
+    const int sgd = opt.variant == S2D_SGD;
+    // Across processes the push / mean / scatter tail runs on its own stream:
+    // the next forward's bucketing and id exchange (which touch no weights)
+    // overlap it, and its lookup waits for it (join_sync).  Virtual ranks
+    // synchronise on the host, so their tail stays on the main stream, as
+    // does a profiled one (its phases are timed on the main stream).
+    const bool overlap = !dp.local() && !profile;
+    cudaStream_t ts = stream;
+    if (overlap) {
+      S2D_CUDA(cudaEventRecord(ev_union, stream));
+      S2D_CUDA(cudaStreamWaitEvent(sync_stream, ev_union, 0));
+      ts = sync_stream;
+    }
+    phase_begin(kPhSyncPush);
+    launch_p2p_push(ptrs(dp_stage), group, M, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
+                    d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), d_count,
+                    count_ub, weights.p, bf16, moments.as<float>(), row_floats, slice_cap, ts);
+    dp_barrier(ts);  // every copy of every slice is staged at its owner
+    phase_begin(kPhSyncMean);
+    launch_p2p_mean(dp_stage.buf.as<float>(), means, M, group, d_count, count_ub, row_floats, slice_cap, sgd, ts);
+    dp_barrier(ts);  // every replica's staging holds every mean
+    phase_begin(kPhSyncScatter);
+    launch_p2p_scatter(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                       (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), d_count, count_ub,
+                       dp_stage.buf.as<float>() + copies, row_floats, weights.p, bf16, moments.as<float>(), sgd, ts);
+    launch_zero(dirty.p, n_slots, ts);
+    if (overlap) {
+      S2D_CUDA(cudaEventRecord(ev_sync_done, ts));
+      sync_pending = true;
+    }
+    sync_stats_pending = true;  // dirty_rows / sync_bytes from the device count (refresh_stats)
+    sync_cmax = cmax;
+    phase_end();
+    finish_call();
+    return;
+  }
   S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_count, 4, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   const uint32_t count = *h_counts.as<uint32_t>();
   stats.dirty_rows = count;
   sync_list.ensure((uint64_t)count * 4);
   launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
-  const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
-  dp_setup();
-  if (dp_p2p == 1) {
-    // Every replica's update of this step is complete: the list all-gather
-    // above ran after each replica's update on its stream, and the host has
-    // read its result.  Slice s of the union list is averaged by replica s.
-    // Staging per replica: [M][slice_cap] copies of its slice | [count] means.
-    const uint64_t slice_cap = (uint64_t)count / M + 1;
-    const uint64_t copies = slice_cap * M * row_floats;
-    peer_alloc_in(dp_stage, (copies + (uint64_t)count * row_floats) * 4, dp);  // same size everywhere
-    const uint32_t lo = (uint32_t)((uint64_t)count * group / M), hi = (uint32_t)((uint64_t)count * (group + 1) / M);
-    PeerPtrs means{};
-    for (uint32_t g = 0; g < M; ++g) means.p[g] = reinterpret_cast<float*>(dp_stage.ptr[g]) + copies;
-    const int sgd = opt.variant == S2D_SGD;
-    phase_begin(kPhSyncPush);
-    launch_p2p_push(ptrs(dp_stage), group, M, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
-                    d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), count,
-                    weights.p, bf16, moments.as<float>(), row_floats, slice_cap, stream);
-    dp_barrier();  // every copy of every slice is staged at its owner
-    phase_begin(kPhSyncMean);
-    launch_p2p_mean(dp_stage.buf.as<float>(), means, M, lo, hi, row_floats, slice_cap, sgd, stream);
-    dp_barrier();  // every replica's staging holds every mean
-    phase_begin(kPhSyncScatter);
-    launch_p2p_scatter(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
-                       (uint32_t)feat_of_vbase.size(), sync_list.as<uint32_t>(), count, dp_stage.buf.as<float>() + copies,
-                       row_floats, weights.p, bf16, moments.as<float>(), sgd, stream);
-    launch_zero(dirty.p, n_slots, stream);
-    stats.sync_bytes = 2 * (uint64_t)(hi - lo) * (M - 1) * (uint64_t)row_floats * 4 + (uint64_t)cmax * 4 * (M - 1);
-    phase_end();
-    finish_call();
-    return;
-  }
   sync_packed.ensure((uint64_t)count * row_floats * 4);
   sync_gathered.ensure((uint64_t)count * row_floats * 4 * M);
   launch_pack_rows(d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
@@ -1131,6 +1216,7 @@ void Ctx::metrics(s2d_metrics_row* out) {
   if (!F) throw Error(S2D_EINVAL, "register tables first");
   if (!have_opt) throw Error(S2D_EINVAL, "set_optimizer first");
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   uint64_t n_total = 0;
   for (uint32_t f = 0; f < F; ++f) n_total += tables[f].rows;
   const uint32_t nb = moment_sum_blocks();
@@ -1200,6 +1286,7 @@ void Ctx::metrics(s2d_metrics_row* out) {
 
 void Ctx::debug_read(int which, void* out, uint64_t cap, uint64_t* n) {
   S2D_CUDA(cudaSetDevice(device));
+  join_sync();
   S2D_CUDA(cudaStreamSynchronize(stream));
   const uint64_t BF = (uint64_t)B * F;
   auto copy = [&](const void* src, uint64_t elems, size_t esz) {

@@ -56,14 +56,28 @@ struct Ctx {
   // host<->device copies of S2D_HOST calls run on their own streams so the
   // pooled read-back (D2H) overlaps the upstream upload (H2D) and the sort
   cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
-  cudaEvent_t ev_fwd = nullptr, ev_d2h = nullptr, ev_up = nullptr, ev_upd = nullptr;
+  cudaEvent_t ev_fwd = nullptr, ev_d2h = nullptr, ev_up = nullptr;
+  // host-mode staging pairs (ids + lengths, upstream, N == 1 pooled
+  // read-back): buffer k is refilled only after the event of its last use
+  cudaEvent_t ev_in_ready = nullptr, ev_in_used[2] = {nullptr, nullptr}, ev_up_used[2] = {nullptr, nullptr},
+              ev_d2h_done[2] = {nullptr, nullptr};
+  bool in_used_rec[2] = {false, false}, up_used_rec[2] = {false, false}, d2h_done_rec[2] = {false, false};
+  int in_sel = 0, up_sel = 0, out_sel = 0;
   bool async_host = false;  // S2D_HOST pooled output valid at return (false) or after s2d_synchronize (true)
-  bool d2h_pending = false, upd_recorded = false;
+  bool d2h_pending = false;
   // N > 1: the (slot, row) sort runs on its own stream from the end of the
   // owner lookup, beside the combine and the gradient all-to-all
   cudaStream_t sort_stream = nullptr;
   cudaEvent_t ev_keys = nullptr, ev_sorted = nullptr;
   bool sort_pending = false;
+  // M > 1: the replica sync's device tail runs on sync_stream (overlapping
+  // the next forward's bucketing / id exchange); join_sync orders the main
+  // stream after it wherever weights, moments or dirty flags are touched
+  cudaStream_t sync_stream = nullptr;
+  cudaEvent_t ev_union = nullptr, ev_sync_done = nullptr;
+  bool sync_pending = false, sync_stats_pending = false;
+  uint32_t sync_cmax = 0;
+  void join_sync();
   void launch_sort(cudaStream_t st);
   const uint32_t* sorted_k = nullptr;  // sorted pairs of the last launch_sort
   const uint32_t* sorted_v = nullptr;
@@ -107,7 +121,7 @@ struct Ctx {
   uint32_t B = 0;
   uint64_t nnz_local = 0, nnz_own = 0;
   bool fwd_done = false;
-  DevBuf in_lengths, in_ids, in_off, upstream_stage, mean_stage;
+  DevBuf in_len2[2], in_ids2[2], in_off, upstream_stage, up_stage2[2], p_pooled_host[2], mean_stage;
   DevBuf cnt, send_off, eoff_req;  // requester side (N > 1)
   DevBuf own_idoff, own_eoff;      // owner side (N > 1)
   // MP-group peer buffers: barrier flags, count matrix, received bag
@@ -189,7 +203,7 @@ struct Ctx {
   PeerBuf dp_flags, dp_stage;
   uint64_t dp_epoch = 0;
   void dp_setup();
-  void dp_barrier();
+  void dp_barrier(cudaStream_t st);
   void read_counts();
  public:
   float* pooled_buffer();

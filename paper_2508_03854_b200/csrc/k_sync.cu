@@ -19,6 +19,7 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;
+constexpr int kSyncRows = 4;  // rows per warp and iteration in the P2P sync kernels
 
 // 16 flags per thread, one 16-byte load when the tile is full
 __device__ __forceinline__ void load_flags(const uint8_t* __restrict__ flags, uint64_t base, uint32_t n,
@@ -145,31 +146,61 @@ __global__ void k_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, 
 // (deterministic_mean_inplace, topology.cpp:150-163; moments likewise unless
 // SGD) and stores the mean into every replica.  All NVLink traffic is posted
 // stores: 2(M-1)/M rows per union row per replica, vs M-1 for an all-gather.
-template <typename WT>
+// 4 stored elements widened to f32 (exact for fp32 and bf16)
+__device__ __forceinline__ float4 load4_f32(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 load4_f32(const __nv_bfloat16* p) {
+  const uint2 x = *reinterpret_cast<const uint2*>(p);
+  return make_float4(__uint_as_float(x.x << 16), __uint_as_float(x.x & 0xffff0000u), __uint_as_float(x.y << 16),
+                     __uint_as_float(x.y & 0xffff0000u));
+}
+
+template <typename WT, int kSyncV>  // kSyncV: 16-byte chunks per lane (rows up to kSyncV * 128 floats)
 __global__ void k_p2p_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDev* feats,
                            const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                           const uint32_t* __restrict__ list, uint32_t count, const WT* __restrict__ w,
-                           const float* __restrict__ moments, uint32_t row_floats, uint64_t slice_cap) {
+                           const uint32_t* __restrict__ list, const uint32_t* __restrict__ count_ptr,
+                           const WT* __restrict__ w, const float* __restrict__ moments, uint32_t row_floats,
+                           uint64_t slice_cap) {
   pdl_wait();
+  const uint32_t count = *count_ptr;  // the union's length (device-side)
   const uint32_t lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < count; i += warps) {
-    // slice owner s of row i: largest s with count*s/M <= i
-    uint32_t s = (uint32_t)(((uint64_t)i * M) / count);
-    while (s + 1 < M && (uint64_t)count * (s + 1) / M <= i) ++s;
-    while (s > 0 && (uint64_t)count * s / M > i) --s;
-    const uint32_t lo = (uint32_t)((uint64_t)count * s / M);
-    const uint32_t slot = list[i];
-    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
-    const uint32_t dim = feats[f].dim;
-    const WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
-    float* out = reinterpret_cast<float*>(stage.p[s]) + ((uint64_t)me * slice_cap + (i - lo)) * row_floats;
-    for (uint32_t c4 = lane; c4 < dim / 4; c4 += 32) {
-      double d[4];
-      Vec4<WT>::load_rw(row + c4 * 4, d);
-      *reinterpret_cast<float4*>(out + c4 * 4) = make_float4((float)d[0], (float)d[1], (float)d[2], (float)d[3]);
+  // kSyncRows rows per warp and iteration: their loads are all in flight
+  // before the first peer store (the loop is latency-bound otherwise)
+  for (uint32_t i0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kSyncRows; i0 < count;
+       i0 += warps * kSyncRows) {
+    float4 d[kSyncRows][kSyncV];
+    float mom[kSyncRows];
+    float* out[kSyncRows];
+    uint32_t dim[kSyncRows];
+#pragma unroll
+    for (int r = 0; r < kSyncRows; ++r) {
+      const uint32_t i = i0 + r;
+      dim[r] = 0;
+      out[r] = nullptr;
+      if (i >= count) continue;
+      // slice owner s of row i: largest s with count*s/M <= i
+      uint32_t s = (uint32_t)(((uint64_t)i * M) / count);
+      while (s + 1 < M && (uint64_t)count * (s + 1) / M <= i) ++s;
+      while (s > 0 && (uint64_t)count * s / M > i) --s;
+      const uint32_t lo = (uint32_t)((uint64_t)count * s / M);
+      const uint32_t slot = list[i];
+      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+      dim[r] = feats[f].dim;
+      const WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim[r];
+      out[r] = reinterpret_cast<float*>(stage.p[s]) + ((uint64_t)me * slice_cap + (i - lo)) * row_floats;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) d[r][v] = load4_f32(row + (lane + v * 32) * 4);
+      mom[r] = lane == 0 ? moments[slot] : 0.f;
     }
-    if (lane == 0) out[row_floats - 1] = moments[slot];
+#pragma unroll
+    for (int r = 0; r < kSyncRows; ++r) {
+      if (!out[r]) continue;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) *reinterpret_cast<float4*>(out[r] + (lane + v * 32) * 4) = d[r][v];
+      if (lane == 0) out[r][row_floats - 1] = mom[r];
+    }
   }
 }
 
@@ -178,9 +209,11 @@ __global__ void k_p2p_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDe
 // union index -- contiguous NVLink stores (storing into the peers' weight
 // rows directly would scatter over their whole shard and thrash the
 // peer-mapping TLB: measured 3x slower).
-__global__ void k_p2p_mean(const float* __restrict__ local, PeerPtrs means, uint32_t M, uint32_t lo, uint32_t hi,
-                           uint32_t row_floats, uint64_t slice_cap, int sgd) {
+__global__ void k_p2p_mean(const float* __restrict__ local, PeerPtrs means, uint32_t M, uint32_t me,
+                           const uint32_t* __restrict__ count_ptr, uint32_t row_floats, uint64_t slice_cap, int sgd) {
   pdl_wait();
+  const uint32_t count = *count_ptr;  // this replica's slice [lo, hi) of the union
+  const uint32_t lo = (uint32_t)((uint64_t)count * me / M), hi = (uint32_t)((uint64_t)count * (me + 1) / M);
   const uint32_t lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
   const double inv_m = 1.0 / (double)M;
@@ -214,26 +247,48 @@ __global__ void k_p2p_mean(const float* __restrict__ local, PeerPtrs means, uint
 
 // Phase 3 (local): every replica scatters the count mean rows into its
 // weights (one rounding to the storage type) and moments.
-template <typename WT>
+template <typename WT, int kSyncV>
 __global__ void k_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
-                              uint32_t n_feat, const uint32_t* __restrict__ list, uint32_t count,
-                              const float* __restrict__ means, uint32_t row_floats, WT* __restrict__ w,
-                              float* __restrict__ moments, int sgd) {
+                              uint32_t n_feat, const uint32_t* __restrict__ list,
+                              const uint32_t* __restrict__ count_ptr, const float* __restrict__ means,
+                              uint32_t row_floats, WT* __restrict__ w, float* __restrict__ moments, int sgd) {
   pdl_wait();
+  const uint32_t count = *count_ptr;
   const uint32_t lane = lane_id();
   const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < count; i += warps) {
-    const uint32_t slot = list[i];
-    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
-    const uint32_t dim = feats[f].dim;
-    WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
-    const float* in = means + (uint64_t)i * row_floats;
-    for (uint32_t c4 = lane; c4 < dim / 4; c4 += 32) {
-      const float4 x = *reinterpret_cast<const float4*>(in + c4 * 4);
-      const double d[4] = {(double)x.x, (double)x.y, (double)x.z, (double)x.w};
-      Vec4<WT>::store(row + c4 * 4, d);
+  for (uint32_t i0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kSyncRows; i0 < count;
+       i0 += warps * kSyncRows) {
+    float4 x[kSyncRows][kSyncV];
+    float mom[kSyncRows];
+    WT* row[kSyncRows];
+    uint32_t dim[kSyncRows], slot[kSyncRows];
+#pragma unroll
+    for (int r = 0; r < kSyncRows; ++r) {
+      const uint32_t i = i0 + r;
+      row[r] = nullptr;
+      dim[r] = 0;
+      if (i >= count) continue;
+      slot[r] = list[i];
+      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot[r]);
+      dim[r] = feats[f].dim;
+      row[r] = w + feats[f].wbase + (uint64_t)(slot[r] - feats[f].vbase) * dim[r];
+      const float* in = means + (uint64_t)i * row_floats;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) x[r][v] = *reinterpret_cast<const float4*>(in + (lane + v * 32) * 4);
+      mom[r] = in[row_floats - 1];
     }
-    if (lane == 0 && !sgd) moments[slot] = in[row_floats - 1];
+#pragma unroll
+    for (int r = 0; r < kSyncRows; ++r) {
+      if (!row[r]) continue;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) {
+          const double d[4] = {(double)x[r][v].x, (double)x[r][v].y, (double)x[r][v].z, (double)x[r][v].w};
+          Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
+        }
+      if (lane == 0 && !sgd) moments[slot[r]] = mom[r];
+    }
   }
 }
 
@@ -313,39 +368,73 @@ void launch_mean_rows(const FeatDev* feats, const uint32_t* vbase_sorted, const 
 }
 
 
-void launch_p2p_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
-                     const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                     const uint32_t* list, uint32_t count, const void* weights, int bf16, const float* moments,
-                     uint32_t row_floats, uint64_t slice_cap, cudaStream_t st) {
-  if (!count) return;
-  const unsigned grid = (unsigned)std::min<uint64_t>((count + 7) / 8, 148ull * 16);
+template <int V>
+void p2p_push_v(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats, const uint32_t* vbase_sorted,
+                const uint32_t* feat_of_vbase, uint32_t n_feat, const uint32_t* list, const uint32_t* count,
+                unsigned grid, const void* weights, int bf16, const float* moments, uint32_t row_floats,
+                uint64_t slice_cap, cudaStream_t st) {
   if (bf16)
-    pdl_launch(k_p2p_push<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted,
+    pdl_launch(k_p2p_push<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted,
                feat_of_vbase, n_feat, list, count, reinterpret_cast<const __nv_bfloat16*>(weights), moments,
                row_floats, slice_cap);
   else
-    pdl_launch(k_p2p_push<float>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted, feat_of_vbase,
+    pdl_launch(k_p2p_push<float, V>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted, feat_of_vbase,
                n_feat, list, count, reinterpret_cast<const float*>(weights), moments, row_floats, slice_cap);
 }
 
-void launch_p2p_mean(const float* local, const PeerPtrs& means, uint32_t M, uint32_t lo, uint32_t hi,
-                     uint32_t row_floats, uint64_t slice_cap, int sgd, cudaStream_t st) {
-  if (hi <= lo) return;
-  const unsigned grid = (unsigned)std::min<uint64_t>((hi - lo + 7) / 8, 148ull * 16);
-  pdl_launch(k_p2p_mean, dim3(grid), dim3(256), 0, st, local, means, M, lo, hi, row_floats, slice_cap, sgd);
+void launch_p2p_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
+                     const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                     const uint32_t* list, const uint32_t* count, uint32_t count_ub, const void* weights, int bf16,
+                     const float* moments, uint32_t row_floats, uint64_t slice_cap, cudaStream_t st) {
+  if (!count_ub) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((count_ub + 8 * kSyncRows - 1) / (8 * kSyncRows), 148ull * 16);
+  const uint32_t d4 = (row_floats - 4) / 4;
+  if (d4 <= 32)
+    p2p_push_v<1>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
+                  row_floats, slice_cap, st);
+  else if (d4 <= 64)
+    p2p_push_v<2>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
+                  row_floats, slice_cap, st);
+  else
+    p2p_push_v<4>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
+                  row_floats, slice_cap, st);
+}
+
+void launch_p2p_mean(const float* local, const PeerPtrs& means, uint32_t M, uint32_t me, const uint32_t* count,
+                     uint32_t count_ub, uint32_t row_floats, uint64_t slice_cap, int sgd, cudaStream_t st) {
+  if (!count_ub) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((count_ub / M + 8) / 8, 148ull * 16);
+  pdl_launch(k_p2p_mean, dim3(grid), dim3(256), 0, st, local, means, M, me, count, row_floats, slice_cap, sgd);
+}
+
+template <int V>
+void p2p_scatter_v(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                   const uint32_t* list, const uint32_t* count, unsigned grid, const float* means, uint32_t row_floats,
+                   void* weights, int bf16, float* moments, int sgd, cudaStream_t st) {
+  if (bf16)
+    pdl_launch(k_p2p_scatter<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, feats, vbase_sorted, feat_of_vbase,
+               n_feat, list, count, means, row_floats, reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd);
+  else
+    pdl_launch(k_p2p_scatter<float, V>, dim3(grid), dim3(256), 0, st, feats, vbase_sorted, feat_of_vbase, n_feat,
+               list, count, means, row_floats, reinterpret_cast<float*>(weights), moments, sgd);
 }
 
 void launch_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
-                        uint32_t n_feat, const uint32_t* list, uint32_t count, const float* means, uint32_t row_floats,
-                        void* weights, int bf16, float* moments, int sgd, cudaStream_t st) {
-  if (!count) return;
-  const unsigned grid = (unsigned)std::min<uint64_t>((count + 7) / 8, 148ull * 16);
-  if (bf16)
-    pdl_launch(k_p2p_scatter<__nv_bfloat16>, dim3(grid), dim3(256), 0, st, feats, vbase_sorted, feat_of_vbase, n_feat,
-               list, count, means, row_floats, reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd);
+                        uint32_t n_feat, const uint32_t* list, const uint32_t* count, uint32_t count_ub,
+                        const float* means, uint32_t row_floats, void* weights, int bf16, float* moments, int sgd,
+                        cudaStream_t st) {
+  if (!count_ub) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((count_ub + 8 * kSyncRows - 1) / (8 * kSyncRows), 148ull * 16);
+  const uint32_t d4 = (row_floats - 4) / 4;
+  if (d4 <= 32)
+    p2p_scatter_v<1>(feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, means, row_floats, weights, bf16,
+                     moments, sgd, st);
+  else if (d4 <= 64)
+    p2p_scatter_v<2>(feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, means, row_floats, weights, bf16,
+                     moments, sgd, st);
   else
-    pdl_launch(k_p2p_scatter<float>, dim3(grid), dim3(256), 0, st, feats, vbase_sorted, feat_of_vbase, n_feat, list,
-               count, means, row_floats, reinterpret_cast<float*>(weights), moments, sgd);
+    p2p_scatter_v<4>(feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, means, row_floats, weights, bf16,
+                     moments, sgd, st);
 }
 
 }  // namespace s2d

@@ -171,11 +171,20 @@ class Workload:
         rng = np.random.default_rng([seed, step, rank, 1])
         lengths = self.lengths(rng, batch)
         F = self.F
-        feat = np.repeat(np.tile(np.arange(F, dtype=np.int32), batch), lengths)
-        ids = np.empty(len(feat), np.uint32)
-        for f in range(F):
-            pos = np.nonzero(feat == f)[0]
-            ids[pos] = self._sample_ids(rng, int(self.rows[f]), len(pos))
+        off = np.zeros(len(lengths) + 1, np.int64)
+        np.cumsum(lengths, out=off[1:])
+        ids = np.empty(int(off[-1]), np.uint32)
+        for f in range(F):  # table f's item positions in ascending order, O(its ids)
+            bags = np.arange(f, batch * F, F)
+            lf = lengths[bags].astype(np.int64)
+            n = int(lf.sum())
+            if n == 0:
+                self._sample_ids(rng, int(self.rows[f]), 0)
+                continue
+            first = np.zeros(len(lf), np.int64)
+            np.cumsum(lf[:-1], out=first[1:])
+            pos = np.repeat(off[bags] - first, lf) + np.arange(n, dtype=np.int64)
+            ids[pos] = self._sample_ids(rng, int(self.rows[f]), n)
         return lengths, ids
 
     def upstream_for(self, seed: int, step: int, rank: int, batch: int | None = None) -> np.ndarray:

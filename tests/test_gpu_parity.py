@@ -176,6 +176,44 @@ def test_async_host_copies_bit_exact(port):
     assert np.array_equal(bits(w), bits(st.ws[0]))
 
 
+def test_async_host_pipelined_steps(port):
+    """async host mode without a host wait between steps (the e2e loop of
+    bench.py): inputs on the H2D stream into alternating staging buffers, the
+    pooled read-back of step k overlapping step k+1 (N = 1); every step's
+    pooled rows and the final tables bit-exact after one synchronize."""
+    import torch
+
+    from oracle import MeshState
+
+    rng = np.random.default_rng(6)
+    rows, dims, B = [5000, 300, 70000], [64, 64, 64], 256
+    spec = _spec(rows, dims, B, eta=0.1, c=1.0)
+    eng = _engine(rows, dims)
+    eng.set_strict(False)
+    eng.set_async_host(True)
+    eng.init_tables(9)
+    st = MeshState.init(port, spec, 9)
+    outs, wants, keep = [], [], []
+    for step in range(5):
+        lengths, ids = make_batch(rng, spec.rows, B, max_len=12, zipf=1.1)
+        up = upstream(rng, B, spec.sum_dims)
+        wants.append(st.step(port, [lengths], [ids], [up], do_sync=False)[0])
+        lh = torch.from_numpy(lengths.view(np.int32)).pin_memory()
+        ih = torch.from_numpy(ids.view(np.int32)).pin_memory()
+        uh = torch.from_numpy(up).pin_memory()
+        ph = torch.empty((B, spec.sum_dims), dtype=torch.float32).pin_memory()
+        keep.append((lh, ih, uh))
+        outs.append(ph)
+        eng.forward(lh, ih, ph, batch=B)
+        eng.backward_update(uh)
+    eng.synchronize()
+    for step in range(5):
+        assert np.array_equal(bits(outs[step].numpy()), bits(wants[step])), step
+    w, v = _download(eng, spec)
+    assert np.array_equal(bits(v), bits(st.vs[0]))
+    assert np.array_equal(bits(w), bits(st.ws[0]))
+
+
 def test_hot_rows_long_segments(port):
     """Tiny tables => segments of thousands of contributions (chunked f64
     reduction).  Within 1e-5 relative; report bit-equal share."""

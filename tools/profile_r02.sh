@@ -29,5 +29,24 @@ for k in k_bucket_count k_bucket_permute k_combine k_grad_gather k_p2p_push k_p2
       > gpurun_out/ncu_$k.log 2>&1
   echo "$k rc=$?"
 done
-cuobjdump -sass paper_2508_03854_b200/libsparse2d_b200.so > gpurun_out/sass_all.txt 2>&1
+# summarise on the box (the .ncu-rep files exceed what gpurun brings back)
+OUT=gpurun_out/profile_out; mkdir -p $OUT
+python tools/ncu_summarize.py --round r02 --tag ${TAG} --full gpurun_out/full_k_lookup_ring.ncu-rep \
+    gpurun_out/full_k_update_ring.ncu-rep gpurun_out/full_k_range_partials.ncu-rep gpurun_out/full_k_radix_pass.ncu-rep \
+    gpurun_out/full_k_radix_hist.ncu-rep gpurun_out/full_k_group_partials.ncu-rep --launches gpurun_out/launches_${TAG}.csv
+cp profiles/r02/ncu_full_${TAG}_summary.csv $OUT/; cp profiles/r02/launches_${TAG}_summary.csv $OUT/
+python tools/ncu_summarize.py --round r02 --tag ${TAG}_mesh2x2 --full gpurun_out/full_k_bucket_count.ncu-rep \
+    gpurun_out/full_k_bucket_permute.ncu-rep gpurun_out/full_k_combine.ncu-rep gpurun_out/full_k_grad_gather.ncu-rep \
+    gpurun_out/full_k_p2p_push.ncu-rep gpurun_out/full_k_p2p_mean.ncu-rep gpurun_out/full_k_p2p_scatter.ncu-rep \
+    gpurun_out/full_k_flag_count.ncu-rep gpurun_out/full_k_flag_write.ncu-rep gpurun_out/full_k_mark_slots.ncu-rep \
+    gpurun_out/full_k_publish_counts.ncu-rep --launches gpurun_out/launches_${TAG}_mesh2x2.csv
+cp profiles/r02/ncu_full_${TAG}_mesh2x2_summary.csv $OUT/; cp profiles/r02/launches_${TAG}_mesh2x2_summary.csv $OUT/
+cp profiles/traffic.json $OUT/
+for k in k_lookup_ring k_update_ring k_range_partials k_radix_pass; do
+  python tools/ncu_hot_src.py gpurun_out/full_$k.ncu-rep 30 > $OUT/hot_src_${TAG}_$k.txt 2>&1
+done
+cuobjdump -sass paper_2508_03854_b200/libsparse2d_b200.so 2>/dev/null | grep -E "Function :|UBLKCP|LDGSTS|F2F.F64.F32|SYNCS" \
+    | awk '/Function :/{f=$0} !/Function :/{c[f" "$2]++} END{for (k in c) print c[k], k}' | sort -k2 > $OUT/sass_opcounts.txt
+cp gpurun_out/bench_${TAG}_n1.json gpurun_out/bench_${TAG}_reference_n1.json gpurun_out/gather_probe_${TAG}.txt $OUT/
+rm -f gpurun_out/*.ncu-rep gpurun_out/launches_*.csv
 echo done
