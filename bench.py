@@ -322,7 +322,7 @@ def run_reference(args):
                    "simulated": f"one MP group of {w.mesh[0]} virtual ranks (reference group step, all host threads)",
                    "global_batch": n * w.mesh[0],
                    "sample": f"{n} of {w.batch} samples per rank per step, tables compacted to touched rows"},
-        "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": threads, "kind": kind,
+        "cpu_baseline": {"value": sps, "unit": "samples/s", "cores": threads, "kind": kind, "cpu_model": cpu_model(),
                          "sample": f"{n} of {w.batch} samples per rank x {w.mesh[0]} ranks per step, touched-row tables"},
         "e2e": {"value": sps, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -585,18 +585,28 @@ def run_ours(args):
                                           "sync_bytes")},
         "per_rank": per_rank,
     }
-    if n_mp > 1:
-        # NVLink roofline of the MP exchanges (rank 0's phases): bytes this rank
-        # stores into peers / the phase time, against the measured peer-copy
-        # bandwidth (770 GB/s per direction, B200_PROFILING.md; 900 nominal)
+    if world > 1:
+        # NVLink roofline of the exchanges (rank 0): bytes this rank stores into
+        # peers / the time of the kernels that carry them (the profiled split
+        # pass), against the measured peer-store ceiling (tools/nvlink_probe.cu,
+        # profiles/r01/nvlink_probe.json: 690 GB/s one way, 652 per direction both
+        # ways; 900 nominal)
+        def ph_ms(*names):
+            return sum(split[p][0] / max(1, n_split) for p in names if p in split)
+
         nv = {}
-        for key, ph in (("grad_bytes_sent", "grad_gather"), ("lookup_bytes_sent", "lookup")):
-            pm = per_phase.get(ph, {}).get("ms_per_launch")
-            if pm:
-                gbs = st[key] / (pm / 1e3) / 1e9
-                nv[ph] = {"bytes": st[key], "ms": pm, "achieved_gbs": gbs, "frac": gbs / 770.0}
-        line["nvlink"] = {"peak_gbs": 770.0, "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
-                          "phases": nv}
+        for name, nbytes, phs in (("C1_ids", st["ids_bytes_sent"], ("bucket", "a2a_ids")),
+                                  ("C1_pooled", st["lookup_bytes_sent"], ("lookup",)),
+                                  ("C2_grad", st["grad_bytes_sent"], ("grad_gather",)),
+                                  ("C3_sync", st["sync_bytes"], ("sync_push", "sync_mean"))):
+            pm = ph_ms(*phs)
+            if pm and nbytes:
+                gbs = nbytes / (pm / 1e3) / 1e9
+                nv[name] = {"bytes": nbytes, "ms": pm, "achieved_gbs": gbs, "frac": gbs / 652.4,
+                            "phases": list(phs)}
+        line["nvlink"] = {"peak_gbs": 652.4, "peak_source": "measured peer stores per direction, both directions "
+                                                            "active (profiles/r01/nvlink_probe.json)",
+                          "exchanges": nv}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(w, args)
     if rank == 0:
@@ -604,6 +614,18 @@ def run_ours(args):
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def cpu_baseline(w, args):
@@ -621,6 +643,7 @@ def cpu_baseline(w, args):
         tot_s += b
         k += 1
     return {"value": tot_s / tot_t, "unit": "samples/s", "cores": threads, "kind": "reference",
+            "cpu_model": cpu_model(),
             "sample": f"{k} steps x {n} of {w.batch} samples, tables compacted to touched rows"}
 
 

@@ -156,6 +156,7 @@ struct LookupArgs {
   int uni_rows;                // uni_d4 != 0 and weights offset = slot * dim (slot-indexed rows)
   uint32_t zero_row;           // slot index of the all-zero row after the shard (uni_rows)
   uint32_t* ticket;            // work counter of the persistent warps (zeroed per launch)
+  uint32_t blocks_per_sm;      // 0: as many as fit; else a cap (leaves room for a concurrent kernel)
   uint64_t unit_rot;           // ticket t processes 32-bag unit (t + unit_rot) % units: owners
                                // start at different requesters so their NVLink stores spread out
   // non-direct: the partial of a bag of requester n goes to
@@ -280,6 +281,9 @@ size_t stream_partial_bytes(uint64_t n, uint32_t max_dim);
 uint64_t stream_partial1_rows(uint64_t n);  // level-1 partial rows (part2 follows them)
 uint64_t stream_partial2_rows(uint64_t n);  // level-2 partial rows (part3 follows them)
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st);
+// N = 1: the lookup's (slot, upstream-row) sort pairs from the ids alone
+void launch_emit_pairs(const FeatDev* feats, uint32_t F, uint32_t B, uint32_t sum_dims, const uint32_t* id_off,
+                       const uint32_t* ids, uint32_t* keys, uint32_t* vals, cudaStream_t st);
 void launch_update_stream(const StreamUpdateArgs& a, int bf16, cudaStream_t st);
 
 // standalone fused row step on caller rows (s2d_adagrad_rows)

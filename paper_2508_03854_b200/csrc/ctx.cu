@@ -567,12 +567,32 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.vals = vals_a.as<uint32_t>();
     a.err = err.as<uint32_t>();
     a.direct = 1;
-    a.emit_keys = 1;
+    // S2D_SORT_BESIDE=1: the sort pairs come from a pass over the ids and
+    // the sort runs on the side stream beside the lookup (experiment)
+    static const bool beside = [] {
+      const char* e = std::getenv("S2D_SORT_BESIDE");
+      return e && e[0] == '1';
+    }();
+    static const uint32_t lookup_bps = [] {
+      const char* e = std::getenv("S2D_LOOKUP_BPS");
+      return e ? (uint32_t)std::atoi(e) : 0u;
+    }();
+    a.emit_keys = beside ? 0 : 1;
+    a.blocks_per_sm = lookup_bps;
     a.uni_d4 = all_same_dim ? max_dim / 4 : 0;
     a.uni_rows = slot_rows ? 1 : 0;
     a.zero_row = n_slots;
     counters.ensure(64);
     a.ticket = counters.as<uint32_t>() + 8;
+    if (beside && nnz) {
+      launch_emit_pairs(dfe, F, B, sum_dims, in_off.as<uint32_t>(), d_ids, keys_a.as<uint32_t>(),
+                        vals_a.as<uint32_t>(), stream);
+      S2D_CUDA(cudaEventRecord(ev_keys, stream));
+      S2D_CUDA(cudaStreamWaitEvent(sort_stream, ev_keys, 0));
+      launch_sort(sort_stream);
+      S2D_CUDA(cudaEventRecord(ev_sorted, sort_stream));
+      sort_pending = true;
+    }
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     stats.nnz_owned = nnz;
     stats.entries_owned = BF;

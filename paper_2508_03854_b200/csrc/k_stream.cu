@@ -979,6 +979,29 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   }
 }
 
+// The lookup's sort pairs without the lookup (N = 1): per id its slot
+// (0xffffffff if outside the shard) and its bag's upstream row (float4
+// units).  They depend on the ids only, so the sort can run beside the
+// lookup instead of after it.  Thread per bag.
+__global__ void __launch_bounds__(256) k_emit_pairs(const FeatDev* __restrict__ feats, uint32_t F, uint32_t B,
+                                                    uint32_t sum_dims, const uint32_t* __restrict__ id_off,
+                                                    const uint32_t* __restrict__ ids, uint32_t* __restrict__ keys,
+                                                    uint32_t* __restrict__ vals) {
+  pdl_wait();
+  const uint64_t BF = (uint64_t)B * F;
+  for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; b < BF; b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t f = (uint32_t)(b % F);
+    const uint32_t lo = __ldg(&feats[f].lo), hi = __ldg(&feats[f].hi), vb = __ldg(&feats[f].vbase);
+    const uint32_t val = (uint32_t)(((b / F) * sum_dims + __ldg(&feats[f].coff)) >> 2);
+    const uint32_t e = __ldg(id_off + b + 1);
+    for (uint32_t p = __ldg(id_off + b); p < e; ++p) {
+      const uint32_t id = __ldg(ids + p);
+      keys[p] = (id >= lo && id < hi) ? vb + (id - lo) : 0xffffffffu;
+      vals[p] = val;
+    }
+  }
+}
+
 unsigned grid_units(uint64_t units, uint32_t units_per_block, unsigned cap) {
   uint64_t g = (units + units_per_block - 1) / units_per_block;
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(g, cap));
@@ -986,7 +1009,7 @@ unsigned grid_units(uint64_t units, uint32_t units_per_block, unsigned cap) {
 
 template <typename K>
 void set_smem(K kernel, size_t bytes) {
-  S2D_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  set_max_dynamic_smem(kernel, bytes);  // per device (a process may drive several GPUs)
 }
 
 // warps per block so that one block's rings stay within ~72 KB (3 blocks/SM)
@@ -1010,7 +1033,8 @@ void lookup_launch_t(const LookupArgs& a, cudaStream_t st) {
     if (occ < 1) occ = 1;
   }
   launch_zero(a.ticket, 16, st);
-  pdl_launch(k_lookup_ring<WT, VPL, UNI>, dim3(grid_units(n_units, nw, 148 * occ)), dim3(nw * 32), smem, st, a);
+  const int per_sm = a.blocks_per_sm ? std::min<int>(occ, (int)a.blocks_per_sm) : occ;
+  pdl_launch(k_lookup_ring<WT, VPL, UNI>, dim3(grid_units(n_units, nw, 148 * per_sm)), dim3(nw * 32), smem, st, a);
 }
 
 template <typename WT, int VPL>
@@ -1079,6 +1103,14 @@ uint64_t stream_partial2_rows(uint64_t n) { return n / ((uint64_t)kC * kP) + 2; 
 size_t stream_partial_bytes(uint64_t n, uint32_t max_dim) {
   return (stream_partial1_rows(n) + stream_partial2_rows(n) + (n / ((uint64_t)kC * kP * kP) + 2)) *
          (uint64_t)max_dim * sizeof(double);
+}
+
+void launch_emit_pairs(const FeatDev* feats, uint32_t F, uint32_t B, uint32_t sum_dims, const uint32_t* id_off,
+                       const uint32_t* ids, uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+  const uint64_t BF = (uint64_t)B * F;
+  if (!BF) return;
+  pdl_launch(k_emit_pairs, dim3(grid_units(BF, 256, 148 * 8)), dim3(256), 0, st, feats, F, B, sum_dims, id_off, ids,
+             keys, vals);
 }
 
 void launch_lookup_stream(const LookupArgs& a, int bf16, int max_dim, cudaStream_t st) {
