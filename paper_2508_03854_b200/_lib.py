@@ -47,7 +47,7 @@ class StepStats(C.Structure):
     _fields_ = [("nnz_local", C.c_uint64), ("nnz_owned", C.c_uint64), ("entries_owned", C.c_uint64),
                 ("unique_rows", C.c_uint64), ("long_segments", C.c_uint64), ("dirty_rows", C.c_uint64),
                 ("a2a_bytes_sent", C.c_uint64), ("a2a_bytes_recv", C.c_uint64), ("sync_bytes", C.c_uint64),
-                ("error_flags", C.c_uint32), ("reserved", C.c_uint32), ("ids_bytes_sent", C.c_uint64),
+                ("error_flags", C.c_uint32), ("sync_mode", C.c_uint32), ("ids_bytes_sent", C.c_uint64),
                 ("lookup_bytes_sent", C.c_uint64), ("grad_bytes_sent", C.c_uint64), ("host_wait_ns", C.c_uint64)]
 
 

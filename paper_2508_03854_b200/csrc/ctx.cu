@@ -354,8 +354,10 @@ void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v,
       }
     }
   }
-  if (write && M > 1)  // written rows join the next replica sync's dirty union
+  if (write && M > 1) {  // written rows join the next replica sync's dirty union
     S2D_CUDA(cudaMemset(dirty.as<uint8_t>() + fd.vbase + (lo - fd.lo), 1, hi - lo));
+    snap_broken = true;  // not in the snapshot log: the next sync exchanges every union row
+  }
   if (v) {
     float* dst = moments.as<float>() + fd.vbase + (lo - fd.lo);
     if (write)
@@ -413,6 +415,7 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
                     reinterpret_cast<uint32_t*>(d + o_seg), reinterpret_cast<uint32_t*>(d + o_row),
                     reinterpret_cast<double*>(d + o_delta), reinterpret_cast<double*>(d + o_mom), nseg, fd.dim,
                     M > 1 ? dirty.as<uint8_t>() + fd.vbase : nullptr, stream);
+  if (M > 1) snap_broken = true;  // not in the snapshot log (see shard_io)
   S2D_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -942,6 +945,7 @@ void Ctx::backward_update(const float* upstream, int mem) {
   if (!have_opt) throw Error(S2D_EINVAL, "set_optimizer first");
   if (mem != S2D_HOST && mem != S2D_DEVICE) throw Error(S2D_EINVAL, "mem must be S2D_HOST or S2D_DEVICE");
   S2D_CUDA(cudaSetDevice(device));
+  if (M > 1) dp_setup();  // DP-group collective: every replica calls backward_update every step
   const uint64_t BF = (uint64_t)B * F;
   const float* d_up = upstream;
   phase_begin(kPhInput);
@@ -1065,6 +1069,16 @@ void Ctx::backward_update(const float* upstream, int mem) {
       ua.grad_dbg = dbg_grad.as<double>();
       ua.head_ord = dbg_head.as<uint32_t>();
     }
+    if (snapshot_enabled()) {
+      snap_reserve(n);
+      if (!snap_broken) {
+        ua.snap = snap.as<float>();
+        ua.snap_pos = snap_pos.as<uint32_t>();
+        ua.snap_count = snap_meta.as<uint32_t>();
+        ua.snap_cap = snap_cap_rows;
+        ua.snap_rf = max_dim + 4;
+      }
+    }
     launch_update_stream(ua, bf16, stream);
     uniq = 1;
   }
@@ -1093,7 +1107,8 @@ void Ctx::refresh_stats() {
     const uint64_t rf = max_dim + 4;
     const uint64_t lo = (uint64_t)count * group / M, hi = (uint64_t)count * (group + 1) / M;
     stats.dirty_rows = count;
-    stats.sync_bytes = 2 * (hi - lo) * (M - 1) * rf * 4 + (uint64_t)sync_cmax * 4 * (M - 1);
+    stats.sync_bytes = sync_snapshot_used ? sync_sent_rows * (M - 1) * rf * 4 + (uint64_t)sync_cmax * 4 * (M - 1)
+                                          : 2 * (hi - lo) * (M - 1) * rf * 4 + (uint64_t)sync_cmax * 4 * (M - 1);
     sync_stats_pending = false;
   }
   if (!stats_counters_valid) return;
@@ -1115,6 +1130,48 @@ void Ctx::join_sync() {
   sync_pending = false;
 }
 
+bool Ctx::snapshot_enabled() const {
+  if (M <= 1 || dp_p2p != 1) return false;
+  static const bool off = [] {
+    const char* e = std::getenv("S2D_SYNC_SNAPSHOT");
+    return e && e[0] == '0';
+  }();
+  return !off;
+}
+
+// Room in the snapshot log for `items` more saved rows (an update of
+// `items` sorted items saves at most that many).  The log keeps 4 GB of HBM
+// free; when it cannot grow the interval is marked broken (the sync falls
+// back to exchanging every union row, which needs no snapshot).
+void Ctx::snap_reserve(uint64_t items) {
+  if (snap_broken) return;
+  const uint64_t rf = max_dim + 4;
+  if (!snap_pos.p) {
+    snap_pos.ensure((size_t)n_slots * 4);
+    snap_meta.ensure(64);
+    S2D_CUDA(cudaMemsetAsync(snap_meta.p, 0, 64, stream));
+  }
+  const uint64_t before = std::min<uint64_t>(snap_ub, snap_cap_rows);
+  snap_ub += items;
+  const uint64_t need = std::min<uint64_t>(n_slots, snap_ub);
+  if (need <= snap_cap_rows) return;
+  const uint64_t want = std::min<uint64_t>(n_slots, need + need / 4);
+  size_t fr = 0, tot = 0;
+  S2D_CUDA(cudaMemGetInfo(&fr, &tot));
+  void* p = nullptr;
+  if ((uint64_t)fr < want * rf * 4 + (4ull << 30) || cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
+    (void)cudaGetLastError();
+    snap_broken = true;
+    return;
+  }
+  if (before) S2D_CUDA(cudaMemcpyAsync(p, snap.p, before * rf * 4, cudaMemcpyDeviceToDevice, stream));
+  S2D_CUDA(cudaStreamSynchronize(stream));
+  snap.release();
+  snap.p = p;
+  snap.cap = want * rf * 4;
+  snap_cap_rows = want;
+}
+
 void Ctx::replica_sync() {
   if (M <= 1 || !F) return;
   S2D_CUDA(cudaSetDevice(device));
@@ -1125,19 +1182,46 @@ void Ctx::replica_sync() {
   // lists are all-gathered, every replica flags the others' slots and
   // compacts again -> the same ascending union list everywhere.
   sync_tmp.ensure(flag_tmp_bytes(n_slots));
-  sync_count.ensure(64 + (size_t)M * 4);
+  sync_count.ensure(64 + (size_t)M * 20);
   uint32_t* d_count = sync_count.as<uint32_t>();
-  uint32_t* d_counts = d_count + 16;  // [M] list lengths of the group
+  uint32_t* d_counts = d_count + 16;      // [M] list lengths of the group
+  uint32_t* d_gath = d_counts + M;        // [M][4] (list length, snapshot count, snapshot limit, 0)
+  // this replica's (count, snapshot rows saved, limit): the snapshot sync
+  // runs only if every replica's log saw every write of the interval
+  const bool snap_on = snapshot_enabled();
+  const uint32_t lim =
+      (snap_on && !snap_broken && snap_pos.p) ? (uint32_t)std::min<uint64_t>(snap_cap_rows + 1, 0xffffffffu) : 0u;
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
-  dp.allgather(d_count, d_counts, 4, stream);
-  S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_counts, (size_t)M * 4, cudaMemcpyDeviceToHost, stream));
+  if (snap_pos.p)
+    S2D_CUDA(cudaMemcpyAsync(d_count + 1, snap_meta.p, 4, cudaMemcpyDeviceToDevice, stream));
+  else
+    S2D_CUDA(cudaMemsetAsync(d_count + 1, 0, 4, stream));
+  const uint32_t lim_pair[2] = {lim, 0u};
+  S2D_CUDA(cudaMemcpyAsync(d_count + 2, lim_pair, 8, cudaMemcpyHostToDevice, stream));
+  dp.allgather(d_count, d_gath, 16, stream);
+  S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_gath, (size_t)M * 16, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
-  const uint32_t* hc = h_counts.as<uint32_t>();
+  const uint32_t* hg = h_counts.as<uint32_t>();
+  std::vector<uint32_t> hc(M);
+  bool use_snap = snap_on;
+  for (uint32_t g = 0; g < M; ++g) {
+    hc[g] = hg[4 * g];
+    use_snap = use_snap && hg[4 * g + 1] < hg[4 * g + 2];
+  }
   const uint32_t mine = hc[group];
   uint32_t cmax = 0;
   for (uint32_t g = 0; g < M; ++g) cmax = std::max(cmax, hc[g]);
+  // the next interval's log starts empty (the device count is reset on the
+  // sync's own stream, before any later update)
+  snap_ub = 0;
+  snap_broken = false;
+  auto reset_snap = [&](cudaStream_t st) {
+    if (snap_meta.p) S2D_CUDA(cudaMemsetAsync(snap_meta.p, 0, 4, st));
+  };
   if (cmax == 0) {
+    reset_snap(stream);
     stats.dirty_rows = 0;
+    stats.sync_mode = 0;
     phase_end();
     finish_call();
     return;
@@ -1148,10 +1232,58 @@ void Ctx::replica_sync() {
     S2D_CUDA(cudaMemsetAsync(sync_list.as<uint32_t>() + mine, 0xff, (size_t)(cmax - mine) * 4, stream));
   sync_lists.ensure((uint64_t)cmax * M * 4);
   dp.allgather(sync_list.p, sync_lists.p, (size_t)cmax * 4, stream);
-  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
+  if (use_snap) sync_map.ensure((size_t)M * n_slots * 4);
+  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(),
+                    use_snap ? sync_map.as<uint32_t>() : nullptr, cmax, stream);
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
   const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
   dp_setup();
+  sync_snapshot_used = false;
+  if (use_snap) {
+    // Snapshot sync (k_sync.cu): the rows each replica dirtied go once to
+    // every peer; every replica then averages every union row locally.
+    const uint32_t count_ub = (uint32_t)std::min<uint64_t>((uint64_t)M * cmax, n_slots);
+    sync_list.ensure((uint64_t)count_ub * 4);
+    launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+    S2D_CUDA(cudaMemcpyAsync(d_counts, hc.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
+    peer_alloc_in(dp_stage, (uint64_t)M * cmax * row_floats * 4, dp);  // same size everywhere
+    const int sgd = opt.variant == S2D_SGD;
+    const bool overlap = !dp.local() && !profile;
+    cudaStream_t ts = stream;
+    if (overlap) {
+      S2D_CUDA(cudaEventRecord(ev_union, stream));
+      S2D_CUDA(cudaStreamWaitEvent(sync_stream, ev_union, 0));
+      ts = sync_stream;
+    }
+    phase_begin(kPhSyncPush);
+    launch_sg_push(ptrs(dp_stage), group, M, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
+                   d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(),
+                   sync_lists.as<uint32_t>() + (uint64_t)group * cmax, d_counts + group, mine, weights.p, bf16,
+                   moments.as<float>(), row_floats, cmax, ts);
+    dp_barrier(ts);  // every replica's dirty rows are staged at every peer
+    phase_begin(kPhSyncMean);
+    launch_sg_mean(dp_stage.buf.as<float>(), M, group, sync_lists.as<uint32_t>(), d_counts, cmax,
+                   sync_map.as<uint32_t>(), sync_list.as<uint32_t>(), d_count, count_ub, d_feats.as<FeatDev>(),
+                   d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(),
+                   n_slots, snap.as<float>(), snap_pos.as<uint32_t>(), row_floats, weights.p, bf16,
+                   moments.as<float>(), sgd, ts);
+    phase_begin(kPhSyncScatter);
+    launch_zero(dirty.p, n_slots, ts);
+    reset_snap(ts);
+    if (overlap) {
+      S2D_CUDA(cudaEventRecord(ev_sync_done, ts));
+      sync_pending = true;
+    }
+    sync_stats_pending = true;
+    sync_snapshot_used = true;
+    stats.sync_mode = 1;
+    sync_sent_rows = mine;
+    sync_cmax = cmax;
+    phase_end();
+    finish_call();
+    return;
+  }
+  reset_snap(stream);
   if (dp_p2p == 1) {
     // The union's length stays on the device: every size below uses the
     // bound count_ub = min(M * cmax, n_slots), identical on every replica,
@@ -1199,6 +1331,7 @@ void Ctx::replica_sync() {
       sync_pending = true;
     }
     sync_stats_pending = true;  // dirty_rows / sync_bytes from the device count (refresh_stats)
+    stats.sync_mode = 2;
     sync_cmax = cmax;
     phase_end();
     finish_call();
@@ -1221,6 +1354,7 @@ void Ctx::replica_sync() {
                    row_floats, count, weights.p, bf16, moments.as<float>(), opt.variant == S2D_SGD,
                    dirty.as<uint8_t>(), stream);
   stats.sync_bytes = (uint64_t)count * row_floats * 4 * (M - 1) + (uint64_t)cmax * 4 * (M - 1);
+  stats.sync_mode = 3;
   phase_end();
   finish_call();
 }

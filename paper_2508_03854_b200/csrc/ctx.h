@@ -34,8 +34,8 @@ enum Phase : int {
   kPhCountSync,   // N > 1: host read of the count matrix (GPU waits for the next launch)
   kPhUpdate,      // K3b chunk sums + K4 fused update
   kPhSync,        // K5 replica sync: dirty-row union (flag compaction, list exchange, host reads)
-  kPhSyncPush,    // K5: rows pushed to the slice owners + barrier
-  kPhSyncMean,    // K5: slice means stored into every replica + barrier
+  kPhSyncPush,    // K5: rows pushed to the slice owners (snapshot sync: dirty rows to every peer) + barrier
+  kPhSyncMean,    // K5: slice means stored into every replica + barrier (snapshot sync: every union mean, local)
   kPhSyncScatter, // K5: means scattered into the shard, dirty flags cleared
   kNumPhases
 };
@@ -77,6 +77,18 @@ struct Ctx {
   cudaEvent_t ev_union = nullptr, ev_sync_done = nullptr;
   bool sync_pending = false, sync_stats_pending = false;
   uint32_t sync_cmax = 0;
+  uint64_t sync_sent_rows = 0;  // rows this replica pushed at the last sync (stats)
+  bool sync_snapshot_used = false;
+  // M > 1 snapshot log (StreamUpdateArgs::snap): rows saved since the last
+  // sync; snap_ub bounds the device count from the host's view (every item
+  // of every update since), snap_broken marks an interval with writes the
+  // log did not see (shard_io / apply_row_updates) or a log that could not
+  // grow -- the next sync then exchanges every union row instead
+  DevBuf snap, snap_pos, snap_meta, sync_map;
+  uint64_t snap_cap_rows = 0, snap_ub = 0;
+  bool snap_broken = false;
+  bool snapshot_enabled() const;
+  void snap_reserve(uint64_t items);
   void join_sync();
   void launch_sort(cudaStream_t st);
   const uint32_t* sorted_k = nullptr;  // sorted pairs of the last launch_sort

@@ -858,6 +858,27 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       if (!finite) {
         if (lane == 0) atomicOr(a.err, kErrNonfinite);
       } else {
+        if (a.snap) {  // first write since the last replica sync: save the pre-update row
+          uint32_t pos = 0xffffffffu;
+          if (lane == 0 && !a.dirty[cur]) pos = atomicAdd(a.snap_count, 1u);
+          pos = __shfl_sync(0xffffffffu, pos, 0);
+          if (pos < a.snap_cap) {
+            float* sp = a.snap + (uint64_t)pos * a.snap_rf;
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              const uint32_t c4 = lane + v * 32;
+              if (c4 < d4) {
+                double x[4];
+                Row<WT>::cvt(x, wraw[v]);
+                *reinterpret_cast<float4*>(sp + c4 * 4) = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
+              }
+            }
+            if (lane == 0) {
+              sp[a.snap_rf - 1] = vold;
+              a.snap_pos[cur] = pos;
+            }
+          }
+        }
         WT* w = W + wofs;
 #pragma unroll
         for (int v = 0; v < VPL; ++v) {

@@ -64,12 +64,19 @@ __global__ void __launch_bounds__(kThreads) k_flag_write(const uint8_t* __restri
     if (f[i]) list[off + ex[i]] = (uint32_t)(base + i);
 }
 
-// union: flag every slot another replica listed (0xffffffff = padding)
+// union: flag every slot another replica listed (0xffffffff = padding);
+// with `map`, also record each entry's position in its list
 __global__ void k_mark_slots(const uint32_t* __restrict__ lists, uint64_t n, uint32_t n_slots,
-                             uint8_t* __restrict__ flags) {
+                             uint8_t* __restrict__ flags, uint32_t* __restrict__ map, uint32_t cmax) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = __ldg(lists + i);
-    if (s < n_slots) flags[s] = 1;
+    if (s < n_slots) {
+      flags[s] = 1;
+      if (map) {
+        const uint64_t h = i / cmax;
+        map[h * n_slots + s] = (uint32_t)(i - h * cmax);
+      }
+    }
   }
 }
 
@@ -292,6 +299,150 @@ __global__ void k_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted
   }
 }
 
+// ---- snapshot replica sync -------------------------------------------------
+// Every union row x's replicas: x_g is replica g's current row if g dirtied
+// it this interval, else the row's value at the last sync (x_0 below).
+// Replica g pushes the rows it dirtied (its ascending list L_g, entry j) to
+// every peer h's staging [g][j]; replica h then has, for each union row,
+// its own current row, the pushed copies of the replicas that dirtied it
+// and x_0 (its current row if it left the row clean, else the snapshot the
+// update saved before its first write).  Each replica forms the same
+// f32((sum_{g asc} f64 x_g) * (1/M)) (deterministic_mean_inplace,
+// topology.cpp:150-163) for every union row, so one exchange of dirty rows
+// replaces the slice push / mean / scatter round trip: (M-1) x |L_g| rows
+// leave replica g instead of 2 (M-1)/M x |union|.
+template <typename WT, int kSyncV>
+__global__ void k_sg_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDev* feats,
+                          const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                          const uint32_t* __restrict__ list, const uint32_t* __restrict__ count_ptr,
+                          const WT* __restrict__ w, const float* __restrict__ moments, uint32_t row_floats,
+                          uint64_t cmax) {
+  pdl_wait();
+  const uint32_t count = *count_ptr;
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  for (uint32_t i0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kSyncRows; i0 < count;
+       i0 += warps * kSyncRows) {
+    float4 d[kSyncRows][kSyncV];
+    float mom[kSyncRows];
+    uint32_t dim[kSyncRows];
+#pragma unroll
+    for (int r = 0; r < kSyncRows; ++r) {
+      const uint32_t i = i0 + r;
+      dim[r] = 0;
+      if (i >= count) continue;
+      const uint32_t slot = list[i];
+      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+      dim[r] = feats[f].dim;
+      const WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim[r];
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) d[r][v] = load4_f32(row + (lane + v * 32) * 4);
+      mom[r] = lane == 0 ? moments[slot] : 0.f;
+    }
+    for (uint32_t h = 0; h < M; ++h) {
+      if (h == me) continue;
+      float* base = reinterpret_cast<float*>(stage.p[h]) + ((uint64_t)me * cmax + i0) * row_floats;
+#pragma unroll
+      for (int r = 0; r < kSyncRows; ++r) {
+        if (!dim[r]) continue;
+        float* out = base + (uint64_t)r * row_floats;
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v)
+          if (lane + v * 32 < dim[r] / 4) *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = d[r][v];
+        if (lane == 0) out[row_floats - 1] = mom[r];
+      }
+    }
+  }
+}
+
+template <typename WT, int kSyncV>
+__global__ void k_sg_mean(const float* __restrict__ stage, uint32_t M, uint32_t me, const uint32_t* __restrict__ lists,
+                          const uint32_t* __restrict__ counts, uint64_t cmax, const uint32_t* __restrict__ map,
+                          const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
+                          const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                          uint32_t n_feat, uint32_t n_slots, const float* __restrict__ snap,
+                          const uint32_t* __restrict__ snap_pos, uint32_t row_floats, WT* __restrict__ w,
+                          float* __restrict__ moments, int sgd) {
+  pdl_wait();
+  const uint32_t count = *ucount;
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  const double inv_m = 1.0 / (double)M;
+  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < count; i += warps) {
+    const uint32_t slot = ulist[i];
+    // lane h < M: position of the slot in L_h (validated against the list)
+    uint32_t pos = 0xffffffffu;
+    if (lane < M) {
+      const uint32_t p = map[(uint64_t)lane * n_slots + slot];
+      if (p < counts[lane] && lists[(uint64_t)lane * cmax + p] == slot) pos = p;
+    }
+    const uint32_t found = __ballot_sync(0xffffffffu, pos != 0xffffffffu);
+    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
+    const uint32_t dim = feats[f].dim;
+    WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
+    float4 own[kSyncV], x0[kSyncV];
+#pragma unroll
+    for (int v = 0; v < kSyncV; ++v)
+      if (lane + v * 32 < dim / 4) own[v] = load4_f32(row + (lane + v * 32) * 4);
+    float own_m = moments[slot], x0_m = own_m;
+    // x_0: own current row unless this replica dirtied the row and some
+    // replica did not (then the pre-interval snapshot)
+    const bool mine = (found >> me) & 1u;
+    const uint32_t all = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
+    if (mine && found != all) {
+      const float* sp = snap + (uint64_t)snap_pos[slot] * row_floats;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim / 4) x0[v] = *reinterpret_cast<const float4*>(sp + (lane + v * 32) * 4);
+      x0_m = sp[row_floats - 1];
+    } else {
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v) x0[v] = own[v];
+    }
+    double acc[kSyncV][4], acc_m = 0.0;
+#pragma unroll
+    for (int v = 0; v < kSyncV; ++v) acc[v][0] = acc[v][1] = acc[v][2] = acc[v][3] = 0.0;
+    for (uint32_t h = 0; h < M; ++h) {  // ascending group order
+      float4 x[kSyncV];
+      float xm;
+      if (h == me) {
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v) x[v] = own[v];
+        xm = own_m;
+      } else if ((found >> h) & 1u) {
+        const uint32_t p = __shfl_sync(0xffffffffu, pos, h);
+        const float* sp = stage + ((uint64_t)h * cmax + p) * row_floats;
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v)
+          if (lane + v * 32 < dim / 4) x[v] = *reinterpret_cast<const float4*>(sp + (lane + v * 32) * 4);
+        xm = sp[row_floats - 1];
+      } else {
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v) x[v] = x0[v];
+        xm = x0_m;
+      }
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v) {
+        acc[v][0] += (double)x[v].x;
+        acc[v][1] += (double)x[v].y;
+        acc[v][2] += (double)x[v].z;
+        acc[v][3] += (double)x[v].w;
+      }
+      acc_m += (double)xm;
+    }
+#pragma unroll
+    for (int v = 0; v < kSyncV; ++v)
+      if (lane + v * 32 < dim / 4) {
+        double d[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) d[j] = (double)(float)(acc[v][j] * inv_m);
+        Vec4<WT>::store(row + (lane + v * 32) * 4, d);
+      }
+    if (lane == 0 && !sgd) moments[slot] = (float)(acc_m * inv_m);
+  }
+}
+
 }  // namespace
 
 // tmp layout: tile counts [ntiles] | their exclusive scan [ntiles + 1] | scan workspace
@@ -327,10 +478,11 @@ void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, c
   S2D_LAUNCH_CHECK();
 }
 
-void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, cudaStream_t st) {
+void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, uint32_t* map,
+                       uint32_t cmax, cudaStream_t st) {
   if (!n) return;
   const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-  k_mark_slots<<<grid, 256, 0, st>>>(lists, n, n_slots, dirty);
+  k_mark_slots<<<grid, 256, 0, st>>>(lists, n, n_slots, dirty, map, cmax);
   S2D_LAUNCH_CHECK();
 }
 
@@ -435,6 +587,75 @@ void launch_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, cons
   else
     p2p_scatter_v<4>(feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, means, row_floats, weights, bf16,
                      moments, sgd, st);
+}
+
+template <int V>
+void sg_push_v(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats, const uint32_t* vbase_sorted,
+               const uint32_t* feat_of_vbase, uint32_t n_feat, const uint32_t* list, const uint32_t* count,
+               unsigned grid, const void* weights, int bf16, const float* moments, uint32_t row_floats, uint64_t cmax,
+               cudaStream_t st) {
+  if (bf16)
+    pdl_launch(k_sg_push<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted,
+               feat_of_vbase, n_feat, list, count, reinterpret_cast<const __nv_bfloat16*>(weights), moments,
+               row_floats, cmax);
+  else
+    pdl_launch(k_sg_push<float, V>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted, feat_of_vbase,
+               n_feat, list, count, reinterpret_cast<const float*>(weights), moments, row_floats, cmax);
+}
+
+void launch_sg_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
+                    const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                    const uint32_t* list, const uint32_t* count, uint32_t count_ub, const void* weights, int bf16,
+                    const float* moments, uint32_t row_floats, uint64_t cmax, cudaStream_t st) {
+  if (!count_ub) return;
+  const unsigned grid = (unsigned)std::min<uint64_t>((count_ub + 8 * kSyncRows - 1) / (8 * kSyncRows), 148ull * 16);
+  const uint32_t d4 = (row_floats - 4) / 4;
+  if (d4 <= 32)
+    sg_push_v<1>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
+                 row_floats, cmax, st);
+  else if (d4 <= 64)
+    sg_push_v<2>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
+                 row_floats, cmax, st);
+  else
+    sg_push_v<4>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
+                 row_floats, cmax, st);
+}
+
+template <int V>
+void sg_mean_v(unsigned grid, const float* stage, uint32_t M, uint32_t me, const uint32_t* lists,
+               const uint32_t* counts, uint64_t cmax, const uint32_t* map, const uint32_t* ulist, const uint32_t* ucount,
+               const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+               uint32_t n_slots, const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights,
+               int bf16, float* moments, int sgd, cudaStream_t st) {
+  if (bf16)
+    pdl_launch(k_sg_mean<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, stage, M, me, lists, counts, cmax, map,
+               ulist, ucount, feats, vbase_sorted, feat_of_vbase, n_feat, n_slots, snap, snap_pos, row_floats,
+               reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd);
+  else
+    pdl_launch(k_sg_mean<float, V>, dim3(grid), dim3(256), 0, st, stage, M, me, lists, counts, cmax, map, ulist,
+               ucount, feats, vbase_sorted, feat_of_vbase, n_feat, n_slots, snap, snap_pos, row_floats,
+               reinterpret_cast<float*>(weights), moments, sgd);
+}
+
+void launch_sg_mean(const float* stage, uint32_t M, uint32_t me, const uint32_t* lists, const uint32_t* counts,
+                    uint64_t cmax, const uint32_t* map, const uint32_t* ulist, const uint32_t* ucount,
+                    uint32_t ucount_ub, const FeatDev* feats, const uint32_t* vbase_sorted,
+                    const uint32_t* feat_of_vbase, uint32_t n_feat, uint32_t n_slots, const float* snap,
+                    const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16, float* moments, int sgd,
+                    cudaStream_t st) {
+  if (!ucount_ub) return;
+  if (M > 32) throw Error(S2D_EINVAL, "snapshot sync supports up to 32 replicas");
+  const unsigned grid = (unsigned)std::min<uint64_t>((ucount_ub + 7) / 8, 148ull * 16);
+  const uint32_t d4 = (row_floats - 4) / 4;
+  if (d4 <= 32)
+    sg_mean_v<1>(grid, stage, M, me, lists, counts, cmax, map, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
+                 n_feat, n_slots, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+  else if (d4 <= 64)
+    sg_mean_v<2>(grid, stage, M, me, lists, counts, cmax, map, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
+                 n_feat, n_slots, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+  else
+    sg_mean_v<4>(grid, stage, M, me, lists, counts, cmax, map, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
+                 n_feat, n_slots, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
 }
 
 }  // namespace s2d

@@ -134,6 +134,7 @@ def rank_main(args, rank, world, local, dist, hub):
 
     pooled_mine, layouts = [], None
     trace = None
+    sync_modes = []
     for step in range(args.steps):
         if step == args.steps - 1:  # measured trace covers the last step only
             eng.set_profiling(True)
@@ -157,6 +158,7 @@ def rank_main(args, rank, world, local, dist, hub):
         eng.backward_update(up)
         if M > 1 and (step + 1) % args.sync_interval == 0:
             eng.sync_replicas()
+            sync_modes.append(eng.stats()["sync_mode"])
         if step == args.steps - 1:
             layouts = {k: eng.debug(k) for k in (0, 1, 2, 3, 4, 5)}
             eng.synchronize()
@@ -182,7 +184,7 @@ def rank_main(args, rank, world, local, dist, hub):
             if hi > lo:
                 loaded[f] = (lo, hi) + eng.read_rows(f, lo, hi)
     gathered = [None] * world if rank == 0 else None
-    dist.gather_object((pooled_mine, layouts, shard, loaded, trace), gathered, dst=0)
+    dist.gather_object((pooled_mine, layouts, shard, loaded, trace, sync_modes), gathered, dst=0)
     eng.close()
     if rank != 0:
         dist.barrier()
@@ -259,6 +261,12 @@ def rank_main(args, rank, world, local, dist, hub):
                 if not (np.array_equal(w.view(np.uint32), ww.view(np.uint32))
                         and np.array_equal(v.view(np.uint32), vv.view(np.uint32))):
                     fails.append(f"checkpoint reload rank {r} table {f}")
+    # which replica-sync path ran: the snapshot dirty-row exchange (1) unless
+    # the environment forces the slice push / mean / scatter (2) or NCCL (3)
+    want_mode = 3 if os.environ.get("S2D_SYNC_NCCL") == "1" else 2 if os.environ.get("S2D_SYNC_SNAPSHOT") == "0" else 1
+    for r in range(world):
+        if any(md not in (0, want_mode) for md in gathered[r][5]) or (M > 1 and want_mode not in gathered[r][5]):
+            fails.append(f"rank {r} sync modes {gathered[r][5]} (want {want_mode})")
     # measured trace of the last step (reference trace.csv schema)
     last_sync = M > 1 and args.steps % args.sync_interval == 0
     for r in range(world):
