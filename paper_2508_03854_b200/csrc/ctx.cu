@@ -1159,7 +1159,8 @@ void Ctx::snap_reserve(uint64_t items) {
   size_t fr = 0, tot = 0;
   S2D_CUDA(cudaMemGetInfo(&fr, &tot));
   void* p = nullptr;
-  if ((uint64_t)fr < want * rf * 4 + (4ull << 30) || cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
+  // leave room for the sync's staging (about as large as the log) + 4 GB
+  if ((uint64_t)fr < 2 * want * rf * 4 + (4ull << 30) || cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
     (void)cudaGetLastError();
     snap_broken = true;
     return;
@@ -1232,9 +1233,7 @@ void Ctx::replica_sync() {
     S2D_CUDA(cudaMemsetAsync(sync_list.as<uint32_t>() + mine, 0xff, (size_t)(cmax - mine) * 4, stream));
   sync_lists.ensure((uint64_t)cmax * M * 4);
   dp.allgather(sync_list.p, sync_lists.p, (size_t)cmax * 4, stream);
-  if (use_snap) sync_map.ensure((size_t)M * n_slots * 4);
-  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(),
-                    use_snap ? sync_map.as<uint32_t>() : nullptr, cmax, stream);
+  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
   const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
   dp_setup();
@@ -1263,10 +1262,9 @@ void Ctx::replica_sync() {
     dp_barrier(ts);  // every replica's dirty rows are staged at every peer
     phase_begin(kPhSyncMean);
     launch_sg_mean(dp_stage.buf.as<float>(), M, group, sync_lists.as<uint32_t>(), d_counts, cmax,
-                   sync_map.as<uint32_t>(), sync_list.as<uint32_t>(), d_count, count_ub, d_feats.as<FeatDev>(),
-                   d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(),
-                   n_slots, snap.as<float>(), snap_pos.as<uint32_t>(), row_floats, weights.p, bf16,
-                   moments.as<float>(), sgd, ts);
+                   sync_list.as<uint32_t>(), d_count, count_ub, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
+                   d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), snap.as<float>(),
+                   snap_pos.as<uint32_t>(), row_floats, weights.p, bf16, moments.as<float>(), sgd, ts);
     phase_begin(kPhSyncScatter);
     launch_zero(dirty.p, n_slots, ts);
     reset_snap(ts);

@@ -84,7 +84,7 @@ struct Ctx {
   // of every update since), snap_broken marks an interval with writes the
   // log did not see (shard_io / apply_row_updates) or a log that could not
   // grow -- the next sync then exchanges every union row instead
-  DevBuf snap, snap_pos, snap_meta, sync_map;
+  DevBuf snap, snap_pos, snap_meta;
   uint64_t snap_cap_rows = 0, snap_ub = 0;
   bool snap_broken = false;
   bool snapshot_enabled() const;

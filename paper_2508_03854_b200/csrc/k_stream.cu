@@ -655,8 +655,8 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
 // FULL: every owned row is exactly VPL*128 floats, so each lane's chunk of
 // any item's gradient row -- sentinel items keep a real row offset, items past
 // the range name row 0 -- is in bounds and the ring copies need no predicate.
-template <typename WT, int VPL, bool FULL>
-__global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
+template <typename WT, int VPL, bool FULL, bool SNAP>
+__global__ void __launch_bounds__(128, SNAP ? 8 : 0) k_update_ring(const StreamUpdateArgs a) {
   pdl_wait();  // persistent single wave
   pdl_trigger();
   constexpr int kWinStages = 32 / kRowsPerStage;
@@ -666,11 +666,13 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   const uint32_t sbase = smem_u32(smem);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   // per warp: gradient ring | head moments of two windows (cp.async, 256 B) |
-  // the range's sorted keys and row offsets (cp.async, 2 x kC x 4 B)
-  constexpr uint32_t kWarpBytes = kSlots * kGRow + 256 + 8 * kC;
+  // the heads' dirty-flag words of two windows (snapshot log, 256 B) | the
+  // range's sorted keys and row offsets (cp.async, 2 x kC x 4 B)
+  constexpr uint32_t kWarpBytes = kSlots * kGRow + 512 + 8 * kC;
   const uint32_t g_lane = sbase + warp * kWarpBytes + lane * 16;  // gradient ring
   const uint32_t mom_s = sbase + warp * kWarpBytes + kSlots * kGRow;
-  const uint32_t uk_s = mom_s + 256, uv_s = uk_s + 4 * kC;
+  const uint32_t dty_s = mom_s + 256;
+  const uint32_t uk_s = dty_s + 256, uv_s = uk_s + 4 * kC;
   const uint32_t* const ukeys = reinterpret_cast<const uint32_t*>(smem + (uk_s - sbase));
   const uint32_t* const uvals = reinterpret_cast<const uint32_t*>(smem + (uv_s - sbase));
   const uint64_t n = a.n;
@@ -727,6 +729,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
     // heads.  Raw keys and rows are loaded one window before they are used.
     struct Win {
       uint32_t key, val, d4, vm, hm;
+      uint32_t snap0;  // lane 0: first snapshot-log position reserved for the window's heads
       uint64_t wofs;
     };
     uint32_t prev_key = 0xfffffffeu;  // key of the item before the window
@@ -751,6 +754,13 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       // each head's moment goes to shared memory by cp.async (it lands with
       // the next stage's group, long before the consumer reaches the head)
       cp_async_p<4>(mom_s + ((win & 1u) * 32u + lane) * 4u, a.moments + (head ? key : 0u), head);
+      if constexpr (SNAP) {
+        // the heads' dirty-flag words (read at the head: a clean row is
+        // saved before its first write) and one log reservation per
+        // window (read a window later, so the atomic's latency is hidden)
+        cp_async_p<4>(dty_s + ((win & 1u) * 32u + lane) * 4u, a.dirty + ((head ? key : 0u) & ~3u), head);
+        w.snap0 = (lane == 0 && w.hm) ? atomicAdd(a.snap_count, (uint32_t)__popc(w.hm)) : 0u;
+      }
       if constexpr (FULL) {  // slot-indexed rows of VPL*128 elements: no per-item row metadata
         if (head) {
           const char* row = reinterpret_cast<const char*>(W + (uint64_t)key * (VPL * 128));
@@ -807,6 +817,7 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[v][j] = 0.0;
     uint32_t cur = kNone, d4 = 0;
+    uint32_t cur_snap = kNone;  // snapshot-log position of `cur` (kNone: already dirty / log off)
     uint64_t wofs = 0, cur_pos = 0;
     typename Row<WT>::T wraw[VPL];  // weight row of `cur` (raw storage type)
     float vold = 0.f;
@@ -858,11 +869,9 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
       if (!finite) {
         if (lane == 0) atomicOr(a.err, kErrNonfinite);
       } else {
-        if (a.snap) {  // first write since the last replica sync: save the pre-update row
-          uint32_t pos = 0xffffffffu;
-          if (lane == 0 && !a.dirty[cur]) pos = atomicAdd(a.snap_count, 1u);
-          pos = __shfl_sync(0xffffffffu, pos, 0);
-          if (pos < a.snap_cap) {
+        if (SNAP && cur_snap < a.snap_cap) {  // first write since the last replica sync: save the pre-update row
+          const uint32_t pos = cur_snap;
+          {
             float* sp = a.snap + (uint64_t)pos * a.snap_rf;
 #pragma unroll
             for (int v = 0; v < VPL; ++v) {
@@ -948,6 +957,11 @@ __global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
             for (int v = 0; v < VPL; ++v)
               if (lane + v * 32 < d4) wraw[v] = Row<WT>::ldg(W + wofs + (lane + v * 32) * 4);
             vold = *reinterpret_cast<const float*>(smem + (mom_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
+            if constexpr (SNAP) {
+              const uint32_t dw = *reinterpret_cast<const uint32_t*>(smem + (dty_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
+              const uint32_t pos = __shfl_sync(0xffffffffu, wc_.snap0, 0) + __popc(wc_.hm & ((1u << i) - 1u));
+              cur_snap = ((dw >> ((cur & 3u) * 8u)) & 0xffu) ? kNone : pos;
+            }
           }
           add_grad(slot0 + r);
         }
@@ -1048,8 +1062,8 @@ void lookup_launch_t(const LookupArgs& a, cudaStream_t st) {
   const uint32_t nw = warps_for(per_warp, 8);
   const size_t smem = nw * per_warp;
   static int occ = 0;
+  set_smem(k_lookup_ring<WT, VPL, UNI>, smem);  // per device
   if (!occ) {
-    set_smem(k_lookup_ring<WT, VPL, UNI>, smem);
     S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lookup_ring<WT, VPL, UNI>, nw * 32, smem));
     if (occ < 1) occ = 1;
   }
@@ -1068,14 +1082,8 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
 
 template <typename WT, int VPL>
 void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
-  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16 + 256 + 8 * kC;  // ring + head moments + range keys/rows
+  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16 + 512 + 8 * kC;  // ring + head moments / dirty words + range keys/rows
   const uint32_t nw_u = warps_for(pw_u, 4);
-  static bool init = false;
-  if (!init) {
-    set_smem(k_update_ring<WT, VPL, false>, nw_u * pw_u);
-    set_smem(k_update_ring<WT, VPL, true>, nw_u * pw_u);
-    init = true;
-  }
   const bool full = a.uni_dim == 128u * VPL;
   if (a.n >= 2 * kC) {
     static const bool tma = [] {
@@ -1099,21 +1107,20 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   if (a.n >= 2ull * kC * kP * kP)
     pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP * kP), 8, 148 * 8)), dim3(256), 0, st, a,
                static_cast<const double*>(a.part2), a.part3, (uint64_t)kC * kP * kP);
-  static int occ[2] = {0, 0};  // per variant: their register counts differ
-  if (!occ[full]) {
-    if (full)
-      S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_update_ring<WT, VPL, true>, nw_u * 32,
-                                                             nw_u * pw_u));
-    else
-      S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_update_ring<WT, VPL, false>, nw_u * 32,
-                                                             nw_u * pw_u));
-    if (occ[full] < 1) occ[full] = 1;
+  // variants: FULL (slot-indexed uniform rows) x SNAP (M > 1 snapshot log);
+  // their register counts differ, so each has its own occupancy
+  const bool snap = a.snap != nullptr;
+  auto kern = full ? (snap ? k_update_ring<WT, VPL, true, true> : k_update_ring<WT, VPL, true, false>)
+                   : (snap ? k_update_ring<WT, VPL, false, true> : k_update_ring<WT, VPL, false, false>);
+  set_smem(kern, nw_u * pw_u);  // per device
+  static int occ[4] = {0, 0, 0, 0};
+  const int vi = (full ? 2 : 0) + (snap ? 1 : 0);
+  if (!occ[vi]) {
+    S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[vi], kern, nw_u * 32, nw_u * pw_u));
+    if (occ[vi] < 1) occ[vi] = 1;
   }
-  const unsigned grid = grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ[full]);
-  if (full)
-    pdl_launch(k_update_ring<WT, VPL, true>, dim3(grid), dim3(nw_u * 32), nw_u * pw_u, st, a);
-  else
-    pdl_launch(k_update_ring<WT, VPL, false>, dim3(grid), dim3(nw_u * 32), nw_u * pw_u, st, a);
+  const unsigned grid = grid_units((a.n + kC - 1) / kC, nw_u, 148 * occ[vi]);
+  pdl_launch(kern, dim3(grid), dim3(nw_u * 32), nw_u * pw_u, st, a);
 }
 
 }  // namespace

@@ -64,19 +64,12 @@ __global__ void __launch_bounds__(kThreads) k_flag_write(const uint8_t* __restri
     if (f[i]) list[off + ex[i]] = (uint32_t)(base + i);
 }
 
-// union: flag every slot another replica listed (0xffffffff = padding);
-// with `map`, also record each entry's position in its list
+// union: flag every slot another replica listed (0xffffffff = padding)
 __global__ void k_mark_slots(const uint32_t* __restrict__ lists, uint64_t n, uint32_t n_slots,
-                             uint8_t* __restrict__ flags, uint32_t* __restrict__ map, uint32_t cmax) {
+                             uint8_t* __restrict__ flags) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = __ldg(lists + i);
-    if (s < n_slots) {
-      flags[s] = 1;
-      if (map) {
-        const uint64_t h = i / cmax;
-        map[h * n_slots + s] = (uint32_t)(i - h * cmax);
-      }
-    }
+    if (s < n_slots) flags[s] = 1;
   }
 }
 
@@ -356,90 +349,142 @@ __global__ void k_sg_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDev
   }
 }
 
+// One warp per chunk of 32 union rows.  Membership of each row in every
+// replica's ascending list L_h comes from a merge: lane h finds the chunk's
+// first slot in L_h (binary search), the next 32 entries of every list are
+// staged in shared memory, and each lane locates its row in them.  Rows are
+// then averaged two at a time (their loads in flight together).
+constexpr int kMeanWarps = 8;
 template <typename WT, int kSyncV>
-__global__ void k_sg_mean(const float* __restrict__ stage, uint32_t M, uint32_t me, const uint32_t* __restrict__ lists,
-                          const uint32_t* __restrict__ counts, uint64_t cmax, const uint32_t* __restrict__ map,
-                          const uint32_t* __restrict__ ulist, const uint32_t* __restrict__ ucount,
-                          const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
-                          uint32_t n_feat, uint32_t n_slots, const float* __restrict__ snap,
-                          const uint32_t* __restrict__ snap_pos, uint32_t row_floats, WT* __restrict__ w,
-                          float* __restrict__ moments, int sgd) {
+__global__ void __launch_bounds__(kMeanWarps * 32) k_sg_mean(
+    const float* __restrict__ stage, uint32_t M, uint32_t me, const uint32_t* __restrict__ lists,
+    const uint32_t* __restrict__ counts, uint64_t cmax, const uint32_t* __restrict__ ulist,
+    const uint32_t* __restrict__ ucount, const FeatDev* feats, const uint32_t* vbase_sorted,
+    const uint32_t* feat_of_vbase, uint32_t n_feat, const float* __restrict__ snap,
+    const uint32_t* __restrict__ snap_pos, uint32_t row_floats, WT* __restrict__ w, float* __restrict__ moments,
+    int sgd) {
   pdl_wait();
+  extern __shared__ uint32_t s_mean[];  // per warp: next entries [M][32] | positions [M][32]
   const uint32_t count = *ucount;
-  const uint32_t lane = lane_id();
-  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
+  uint32_t* sl = s_mean + (size_t)wib * 64 * M;
+  uint32_t* spos = sl + 32 * M;
+  const uint64_t nwarps = (uint64_t)gridDim.x * kMeanWarps;
   const double inv_m = 1.0 / (double)M;
-  for (uint32_t i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < count; i += warps) {
-    const uint32_t slot = ulist[i];
-    // lane h < M: position of the slot in L_h (validated against the list)
-    uint32_t pos = 0xffffffffu;
-    if (lane < M) {
-      const uint32_t p = map[(uint64_t)lane * n_slots + slot];
-      if (p < counts[lane] && lists[(uint64_t)lane * cmax + p] == slot) pos = p;
+  const uint32_t all = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
+  for (uint64_t c0 = ((uint64_t)blockIdx.x * kMeanWarps + wib) * 32; c0 < count; c0 += nwarps * 32) {
+    const uint32_t rows = count - c0 < 32 ? (uint32_t)(count - c0) : 32u;
+    const uint32_t my_slot = lane < rows ? ulist[c0 + lane] : 0xffffffffu;
+    const uint32_t first = __shfl_sync(0xffffffffu, my_slot, 0);
+    uint32_t p = 0;
+    if (lane < M) {  // lower bound of the chunk's first slot in L_lane
+      const uint32_t* L = lists + (uint64_t)lane * cmax;
+      uint32_t lo = 0, hi = counts[lane];
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (L[mid] < first) lo = mid + 1;
+        else hi = mid;
+      }
+      p = lo;
     }
-    const uint32_t found = __ballot_sync(0xffffffffu, pos != 0xffffffffu);
-    const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
-    const uint32_t dim = feats[f].dim;
-    WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim;
-    float4 own[kSyncV], x0[kSyncV];
-#pragma unroll
-    for (int v = 0; v < kSyncV; ++v)
-      if (lane + v * 32 < dim / 4) own[v] = load4_f32(row + (lane + v * 32) * 4);
-    float own_m = moments[slot], x0_m = own_m;
-    // x_0: own current row unless this replica dirtied the row and some
-    // replica did not (then the pre-interval snapshot)
-    const bool mine = (found >> me) & 1u;
-    const uint32_t all = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
-    if (mine && found != all) {
-      const float* sp = snap + (uint64_t)snap_pos[slot] * row_floats;
-#pragma unroll
-      for (int v = 0; v < kSyncV; ++v)
-        if (lane + v * 32 < dim / 4) x0[v] = *reinterpret_cast<const float4*>(sp + (lane + v * 32) * 4);
-      x0_m = sp[row_floats - 1];
-    } else {
-#pragma unroll
-      for (int v = 0; v < kSyncV; ++v) x0[v] = own[v];
+    for (uint32_t h = 0; h < M; ++h) {
+      const uint32_t ph = __shfl_sync(0xffffffffu, p, h);
+      const uint32_t ch = counts[h];
+      sl[h * 32 + lane] = ph + lane < ch ? lists[(uint64_t)h * cmax + ph + lane] : 0xffffffffu;
     }
-    double acc[kSyncV][4], acc_m = 0.0;
+    __syncwarp();
+    uint32_t found = 0;
+    for (uint32_t h = 0; h < M; ++h) {
+      const uint32_t ph = __shfl_sync(0xffffffffu, p, h);
+      uint32_t lo = 0, hi = 32;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sl[h * 32 + mid] < my_slot) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lane < rows && lo < 32 && sl[h * 32 + lo] == my_slot) {
+        found |= 1u << h;
+        spos[h * 32 + lane] = ph + lo;
+      }
+    }
+    __syncwarp();
+    for (uint32_t j = 0; j < rows; j += 2) {
+      uint32_t slot[2], fnd[2], dim[2] = {0, 0};
+      WT* row[2] = {nullptr, nullptr};
+      const float* sp[2] = {nullptr, nullptr};
+      float4 own[2][kSyncV];
+      float own_m[2] = {0.f, 0.f}, snap_m[2] = {0.f, 0.f};
 #pragma unroll
-    for (int v = 0; v < kSyncV; ++v) acc[v][0] = acc[v][1] = acc[v][2] = acc[v][3] = 0.0;
-    for (uint32_t h = 0; h < M; ++h) {  // ascending group order
-      float4 x[kSyncV];
-      float xm;
-      if (h == me) {
-#pragma unroll
-        for (int v = 0; v < kSyncV; ++v) x[v] = own[v];
-        xm = own_m;
-      } else if ((found >> h) & 1u) {
-        const uint32_t p = __shfl_sync(0xffffffffu, pos, h);
-        const float* sp = stage + ((uint64_t)h * cmax + p) * row_floats;
+      for (int r = 0; r < 2; ++r) {
+        const uint32_t i = j + r;
+        slot[r] = __shfl_sync(0xffffffffu, my_slot, i & 31);
+        fnd[r] = __shfl_sync(0xffffffffu, found, i & 31);
+        if (i >= rows) continue;
+        const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot[r]);
+        dim[r] = feats[f].dim;
+        row[r] = w + feats[f].wbase + (uint64_t)(slot[r] - feats[f].vbase) * dim[r];
 #pragma unroll
         for (int v = 0; v < kSyncV; ++v)
-          if (lane + v * 32 < dim / 4) x[v] = *reinterpret_cast<const float4*>(sp + (lane + v * 32) * 4);
-        xm = sp[row_floats - 1];
-      } else {
+          if (lane + v * 32 < dim[r] / 4) own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
+        own_m[r] = moments[slot[r]];
+        // x_0 for the replicas that left the row clean: this replica's own
+        // copy, or its snapshot when it dirtied the row itself
+        if (((fnd[r] >> me) & 1u) && fnd[r] != all) sp[r] = snap + (uint64_t)snap_pos[slot[r]] * row_floats;
+      }
+      double acc[2][kSyncV][4], acc_m[2] = {0.0, 0.0};
 #pragma unroll
-        for (int v = 0; v < kSyncV; ++v) x[v] = x0[v];
-        xm = x0_m;
+      for (int r = 0; r < 2; ++r) {
+        if (sp[r]) snap_m[r] = sp[r][row_floats - 1];
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v) acc[r][v][0] = acc[r][v][1] = acc[r][v][2] = acc[r][v][3] = 0.0;
+      }
+      for (uint32_t h = 0; h < M; ++h) {  // ascending group order
+        float4 x[2][kSyncV];
+        float xm[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (!dim[r]) continue;
+          const float* src = nullptr;
+          if (h != me) src = ((fnd[r] >> h) & 1u) ? stage + ((uint64_t)h * cmax + spos[h * 32 + j + r]) * row_floats : sp[r];
+          if (src) {
+#pragma unroll
+            for (int v = 0; v < kSyncV; ++v)
+              if (lane + v * 32 < dim[r] / 4) x[r][v] = *reinterpret_cast<const float4*>(src + (lane + v * 32) * 4);
+            xm[r] = src == sp[r] ? snap_m[r] : src[row_floats - 1];
+          } else {
+#pragma unroll
+            for (int v = 0; v < kSyncV; ++v) x[r][v] = own[r][v];
+            xm[r] = own_m[r];
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          if (!dim[r]) continue;
+#pragma unroll
+          for (int v = 0; v < kSyncV; ++v) {
+            acc[r][v][0] += (double)x[r][v].x;
+            acc[r][v][1] += (double)x[r][v].y;
+            acc[r][v][2] += (double)x[r][v].z;
+            acc[r][v][3] += (double)x[r][v].w;
+          }
+          acc_m[r] += (double)xm[r];
+        }
       }
 #pragma unroll
-      for (int v = 0; v < kSyncV; ++v) {
-        acc[v][0] += (double)x[v].x;
-        acc[v][1] += (double)x[v].y;
-        acc[v][2] += (double)x[v].z;
-        acc[v][3] += (double)x[v].w;
+      for (int r = 0; r < 2; ++r) {
+        if (!dim[r]) continue;
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v)
+          if (lane + v * 32 < dim[r] / 4) {
+            double d[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) d[q] = (double)(float)(acc[r][v][q] * inv_m);
+            Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
+          }
+        if (lane == 0 && !sgd) moments[slot[r]] = (float)(acc_m[r] * inv_m);
       }
-      acc_m += (double)xm;
     }
-#pragma unroll
-    for (int v = 0; v < kSyncV; ++v)
-      if (lane + v * 32 < dim / 4) {
-        double d[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) d[j] = (double)(float)(acc[v][j] * inv_m);
-        Vec4<WT>::store(row + (lane + v * 32) * 4, d);
-      }
-    if (lane == 0 && !sgd) moments[slot] = (float)(acc_m * inv_m);
+    __syncwarp();
   }
 }
 
@@ -478,11 +523,10 @@ void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, c
   S2D_LAUNCH_CHECK();
 }
 
-void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, uint32_t* map,
-                       uint32_t cmax, cudaStream_t st) {
+void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, cudaStream_t st) {
   if (!n) return;
   const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
-  k_mark_slots<<<grid, 256, 0, st>>>(lists, n, n_slots, dirty, map, cmax);
+  k_mark_slots<<<grid, 256, 0, st>>>(lists, n, n_slots, dirty);
   S2D_LAUNCH_CHECK();
 }
 
@@ -622,40 +666,44 @@ void launch_sg_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDe
 }
 
 template <int V>
-void sg_mean_v(unsigned grid, const float* stage, uint32_t M, uint32_t me, const uint32_t* lists,
-               const uint32_t* counts, uint64_t cmax, const uint32_t* map, const uint32_t* ulist, const uint32_t* ucount,
+void sg_mean_v(unsigned grid, size_t smem, const float* stage, uint32_t M, uint32_t me, const uint32_t* lists,
+               const uint32_t* counts, uint64_t cmax, const uint32_t* ulist, const uint32_t* ucount,
                const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-               uint32_t n_slots, const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights,
-               int bf16, float* moments, int sgd, cudaStream_t st) {
-  if (bf16)
-    pdl_launch(k_sg_mean<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, stage, M, me, lists, counts, cmax, map,
-               ulist, ucount, feats, vbase_sorted, feat_of_vbase, n_feat, n_slots, snap, snap_pos, row_floats,
+               const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16,
+               float* moments, int sgd, cudaStream_t st) {
+  if (bf16) {
+    set_max_dynamic_smem(k_sg_mean<__nv_bfloat16, V>, smem);
+    pdl_launch(k_sg_mean<__nv_bfloat16, V>, dim3(grid), dim3(kMeanWarps * 32), smem, st, stage, M, me, lists, counts,
+               cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase, n_feat, snap, snap_pos, row_floats,
                reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd);
-  else
-    pdl_launch(k_sg_mean<float, V>, dim3(grid), dim3(256), 0, st, stage, M, me, lists, counts, cmax, map, ulist,
-               ucount, feats, vbase_sorted, feat_of_vbase, n_feat, n_slots, snap, snap_pos, row_floats,
+  } else {
+    set_max_dynamic_smem(k_sg_mean<float, V>, smem);
+    pdl_launch(k_sg_mean<float, V>, dim3(grid), dim3(kMeanWarps * 32), smem, st, stage, M, me, lists, counts, cmax,
+               ulist, ucount, feats, vbase_sorted, feat_of_vbase, n_feat, snap, snap_pos, row_floats,
                reinterpret_cast<float*>(weights), moments, sgd);
+  }
 }
 
 void launch_sg_mean(const float* stage, uint32_t M, uint32_t me, const uint32_t* lists, const uint32_t* counts,
-                    uint64_t cmax, const uint32_t* map, const uint32_t* ulist, const uint32_t* ucount,
-                    uint32_t ucount_ub, const FeatDev* feats, const uint32_t* vbase_sorted,
-                    const uint32_t* feat_of_vbase, uint32_t n_feat, uint32_t n_slots, const float* snap,
-                    const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16, float* moments, int sgd,
-                    cudaStream_t st) {
+                    uint64_t cmax, const uint32_t* ulist, const uint32_t* ucount, uint32_t ucount_ub,
+                    const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                    const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16,
+                    float* moments, int sgd, cudaStream_t st) {
   if (!ucount_ub) return;
   if (M > 32) throw Error(S2D_EINVAL, "snapshot sync supports up to 32 replicas");
-  const unsigned grid = (unsigned)std::min<uint64_t>((ucount_ub + 7) / 8, 148ull * 16);
+  const unsigned grid = (unsigned)std::max<uint64_t>(
+      1, std::min<uint64_t>((ucount_ub + 32 * kMeanWarps - 1) / (32 * kMeanWarps), 148ull * 8));
+  const size_t smem = (size_t)kMeanWarps * 64 * M * 4;
   const uint32_t d4 = (row_floats - 4) / 4;
   if (d4 <= 32)
-    sg_mean_v<1>(grid, stage, M, me, lists, counts, cmax, map, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
-                 n_feat, n_slots, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+    sg_mean_v<1>(grid, smem, stage, M, me, lists, counts, cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
+                 n_feat, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
   else if (d4 <= 64)
-    sg_mean_v<2>(grid, stage, M, me, lists, counts, cmax, map, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
-                 n_feat, n_slots, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+    sg_mean_v<2>(grid, smem, stage, M, me, lists, counts, cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
+                 n_feat, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
   else
-    sg_mean_v<4>(grid, stage, M, me, lists, counts, cmax, map, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
-                 n_feat, n_slots, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+    sg_mean_v<4>(grid, smem, stage, M, me, lists, counts, cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
+                 n_feat, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
 }
 
 }  // namespace s2d
