@@ -254,11 +254,11 @@ struct StreamUpdateArgs {
   const uint32_t* head_ord;      // debug: heads before each sorted position (scan_heads_u32)
   // M > 1 snapshot log (null: off): a row flushed while its dirty flag is
   // clear first saves its pre-update value (f32 row, moment at rf - 1) at
-  // snap[pos], pos = atomicAdd(snap_count), and snap_pos[slot] = pos; rows
-  // past snap_cap are not saved (the sync then takes the exchange-all path)
+  // snap[pos], pos = snap_base + the head's sorted position, and
+  // snap_pos[slot] = pos (the host reserves snap_base + n rows)
   float* snap;
   uint32_t* snap_pos;
-  uint32_t* snap_count;
+  uint64_t snap_base;
   uint64_t snap_cap;
   uint32_t snap_rf;
 };

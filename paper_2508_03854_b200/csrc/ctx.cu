@@ -1070,11 +1070,11 @@ void Ctx::backward_update(const float* upstream, int mem) {
       ua.head_ord = dbg_head.as<uint32_t>();
     }
     if (snapshot_enabled()) {
-      snap_reserve(n);
+      const uint64_t base = snap_reserve(n);
       if (!snap_broken) {
         ua.snap = snap.as<float>();
         ua.snap_pos = snap_pos.as<uint32_t>();
-        ua.snap_count = snap_meta.as<uint32_t>();
+        ua.snap_base = base;
         ua.snap_cap = snap_cap_rows;
         ua.snap_rf = max_dim + 4;
       }
@@ -1139,38 +1139,41 @@ bool Ctx::snapshot_enabled() const {
   return !off;
 }
 
-// Room in the snapshot log for `items` more saved rows (an update of
-// `items` sorted items saves at most that many).  The log keeps 4 GB of HBM
-// free; when it cannot grow the interval is marked broken (the sync falls
-// back to exchanging every union row, which needs no snapshot).
-void Ctx::snap_reserve(uint64_t items) {
-  if (snap_broken) return;
+// Room in the snapshot log for an update of `items` sorted items: its
+// heads save at log row base + their sorted position (no atomics), so the
+// interval's log spans every item of its updates (config 2: 4.7M rows, 2.5
+// GB per step).  The log leaves room for the sync's staging plus 4 GB of
+// HBM; when it cannot grow the interval is marked broken (the sync then
+// exchanges every union row, which needs no snapshot).  Returns base.
+uint64_t Ctx::snap_reserve(uint64_t items) {
+  if (snap_broken) return 0;
   const uint64_t rf = max_dim + 4;
-  if (!snap_pos.p) {
-    snap_pos.ensure((size_t)n_slots * 4);
-    snap_meta.ensure(64);
-    S2D_CUDA(cudaMemsetAsync(snap_meta.p, 0, 64, stream));
+  if (!snap_pos.p) snap_pos.ensure((size_t)n_slots * 4);
+  const uint64_t base = snap_ub;
+  const uint64_t need = snap_ub + items;
+  if (need >= 0xffffffffull) {  // log positions are 32-bit
+    snap_broken = true;
+    return 0;
   }
-  const uint64_t before = std::min<uint64_t>(snap_ub, snap_cap_rows);
-  snap_ub += items;
-  const uint64_t need = std::min<uint64_t>(n_slots, snap_ub);
-  if (need <= snap_cap_rows) return;
-  const uint64_t want = std::min<uint64_t>(n_slots, need + need / 4);
+  snap_ub = need;
+  if (need <= snap_cap_rows) return base;
+  const uint64_t want = std::min<uint64_t>(need + need / 4, 0xfffffffeull);
   size_t fr = 0, tot = 0;
   S2D_CUDA(cudaMemGetInfo(&fr, &tot));
   void* p = nullptr;
-  // leave room for the sync's staging (about as large as the log) + 4 GB
-  if ((uint64_t)fr < 2 * want * rf * 4 + (4ull << 30) || cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
+  if ((uint64_t)fr < (want + std::min<uint64_t>(items, n_slots)) * rf * 4 + (4ull << 30) ||
+      cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
     (void)cudaGetLastError();
     snap_broken = true;
-    return;
+    return 0;
   }
-  if (before) S2D_CUDA(cudaMemcpyAsync(p, snap.p, before * rf * 4, cudaMemcpyDeviceToDevice, stream));
+  if (base) S2D_CUDA(cudaMemcpyAsync(p, snap.p, base * rf * 4, cudaMemcpyDeviceToDevice, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
   snap.release();
   snap.p = p;
   snap.cap = want * rf * 4;
   snap_cap_rows = want;
+  return base;
 }
 
 void Ctx::replica_sync() {
@@ -1186,19 +1189,13 @@ void Ctx::replica_sync() {
   sync_count.ensure(64 + (size_t)M * 20);
   uint32_t* d_count = sync_count.as<uint32_t>();
   uint32_t* d_counts = d_count + 16;      // [M] list lengths of the group
-  uint32_t* d_gath = d_counts + M;        // [M][4] (list length, snapshot count, snapshot limit, 0)
-  // this replica's (count, snapshot rows saved, limit): the snapshot sync
-  // runs only if every replica's log saw every write of the interval
+  uint32_t* d_gath = d_counts + M;        // [M][4] (list length, snapshot log complete, 0, 0)
+  // this replica's (count, log complete): the snapshot sync runs only if
+  // every replica's log saw every write of the interval
   const bool snap_on = snapshot_enabled();
-  const uint32_t lim =
-      (snap_on && !snap_broken && snap_pos.p) ? (uint32_t)std::min<uint64_t>(snap_cap_rows + 1, 0xffffffffu) : 0u;
+  const uint32_t ok_word[3] = {(snap_on && !snap_broken && snap_pos.p) ? 1u : 0u, 0u, 0u};
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
-  if (snap_pos.p)
-    S2D_CUDA(cudaMemcpyAsync(d_count + 1, snap_meta.p, 4, cudaMemcpyDeviceToDevice, stream));
-  else
-    S2D_CUDA(cudaMemsetAsync(d_count + 1, 0, 4, stream));
-  const uint32_t lim_pair[2] = {lim, 0u};
-  S2D_CUDA(cudaMemcpyAsync(d_count + 2, lim_pair, 8, cudaMemcpyHostToDevice, stream));
+  S2D_CUDA(cudaMemcpyAsync(d_count + 1, ok_word, 12, cudaMemcpyHostToDevice, stream));
   dp.allgather(d_count, d_gath, 16, stream);
   S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_gath, (size_t)M * 16, cudaMemcpyDeviceToHost, stream));
   S2D_CUDA(cudaStreamSynchronize(stream));
@@ -1207,20 +1204,15 @@ void Ctx::replica_sync() {
   bool use_snap = snap_on;
   for (uint32_t g = 0; g < M; ++g) {
     hc[g] = hg[4 * g];
-    use_snap = use_snap && hg[4 * g + 1] < hg[4 * g + 2];
+    use_snap = use_snap && hg[4 * g + 1] == 1;
   }
   const uint32_t mine = hc[group];
   uint32_t cmax = 0;
   for (uint32_t g = 0; g < M; ++g) cmax = std::max(cmax, hc[g]);
-  // the next interval's log starts empty (the device count is reset on the
-  // sync's own stream, before any later update)
+  // the next interval's log starts empty
   snap_ub = 0;
   snap_broken = false;
-  auto reset_snap = [&](cudaStream_t st) {
-    if (snap_meta.p) S2D_CUDA(cudaMemsetAsync(snap_meta.p, 0, 4, st));
-  };
   if (cmax == 0) {
-    reset_snap(stream);
     stats.dirty_rows = 0;
     stats.sync_mode = 0;
     phase_end();
@@ -1267,7 +1259,6 @@ void Ctx::replica_sync() {
                    snap_pos.as<uint32_t>(), row_floats, weights.p, bf16, moments.as<float>(), sgd, ts);
     phase_begin(kPhSyncScatter);
     launch_zero(dirty.p, n_slots, ts);
-    reset_snap(ts);
     if (overlap) {
       S2D_CUDA(cudaEventRecord(ev_sync_done, ts));
       sync_pending = true;
@@ -1281,7 +1272,6 @@ void Ctx::replica_sync() {
     finish_call();
     return;
   }
-  reset_snap(stream);
   if (dp_p2p == 1) {
     // The union's length stays on the device: every size below uses the
     // bound count_ub = min(M * cmax, n_slots), identical on every replica,

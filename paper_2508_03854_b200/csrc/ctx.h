@@ -79,16 +79,16 @@ struct Ctx {
   uint32_t sync_cmax = 0;
   uint64_t sync_sent_rows = 0;  // rows this replica pushed at the last sync (stats)
   bool sync_snapshot_used = false;
-  // M > 1 snapshot log (StreamUpdateArgs::snap): rows saved since the last
-  // sync; snap_ub bounds the device count from the host's view (every item
-  // of every update since), snap_broken marks an interval with writes the
-  // log did not see (shard_io / apply_row_updates) or a log that could not
-  // grow -- the next sync then exchanges every union row instead
-  DevBuf snap, snap_pos, snap_meta;
+  // M > 1 snapshot log (StreamUpdateArgs::snap): snap_ub = log rows the
+  // interval's updates span (every item of every update since the last
+  // sync); snap_broken marks an interval with writes the log did not see
+  // (shard_io / apply_row_updates) or a log that could not grow -- the next
+  // sync then exchanges every union row instead
+  DevBuf snap, snap_pos;
   uint64_t snap_cap_rows = 0, snap_ub = 0;
   bool snap_broken = false;
   bool snapshot_enabled() const;
-  void snap_reserve(uint64_t items);
+  uint64_t snap_reserve(uint64_t items);
   void join_sync();
   void launch_sort(cudaStream_t st);
   const uint32_t* sorted_k = nullptr;  // sorted pairs of the last launch_sort

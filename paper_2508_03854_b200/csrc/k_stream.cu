@@ -60,11 +60,6 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-__device__ __forceinline__ uint64_t shfl64(uint64_t v, uint32_t src) {
-  const uint32_t lo = __shfl_sync(0xffffffffu, (uint32_t)v, src);
-  const uint32_t hi = __shfl_sync(0xffffffffu, (uint32_t)(v >> 32), src);
-  return ((uint64_t)hi << 32) | lo;
-}
 
 // Number of lanes j with end_j <= p (ends non-decreasing over lanes).
 __device__ __forceinline__ uint32_t count_le(uint32_t my_end, uint32_t p) {
@@ -655,8 +650,11 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
 // FULL: every owned row is exactly VPL*128 floats, so each lane's chunk of
 // any item's gradient row -- sentinel items keep a real row offset, items past
 // the range name row 0 -- is in bounds and the ring copies need no predicate.
+constexpr uint32_t update_warp_bytes(int vpl, bool snap) {
+  return (uint32_t)kSlots * vpl * 32 * 16 + 256 + 8 * kC + (snap ? 256 : 0);
+}
 template <typename WT, int VPL, bool FULL, bool SNAP>
-__global__ void __launch_bounds__(128, SNAP ? 8 : 0) k_update_ring(const StreamUpdateArgs a) {
+__global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
   pdl_wait();  // persistent single wave
   pdl_trigger();
   constexpr int kWinStages = 32 / kRowsPerStage;
@@ -666,13 +664,13 @@ __global__ void __launch_bounds__(128, SNAP ? 8 : 0) k_update_ring(const StreamU
   const uint32_t sbase = smem_u32(smem);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   // per warp: gradient ring | head moments of two windows (cp.async, 256 B) |
-  // the heads' dirty-flag words of two windows (snapshot log, 256 B) | the
-  // range's sorted keys and row offsets (cp.async, 2 x kC x 4 B)
-  constexpr uint32_t kWarpBytes = kSlots * kGRow + 512 + 8 * kC;
+  // the range's sorted keys and row offsets (cp.async, 2 x kC x 4 B) | with
+  // the snapshot log, the heads' dirty-flag words of two windows (256 B)
+  constexpr uint32_t kWarpBytes = update_warp_bytes(VPL, SNAP);
   const uint32_t g_lane = sbase + warp * kWarpBytes + lane * 16;  // gradient ring
   const uint32_t mom_s = sbase + warp * kWarpBytes + kSlots * kGRow;
-  const uint32_t dty_s = mom_s + 256;
-  const uint32_t uk_s = dty_s + 256, uv_s = uk_s + 4 * kC;
+  const uint32_t uk_s = mom_s + 256, uv_s = uk_s + 4 * kC;
+  const uint32_t dty_s = uv_s + 4 * kC;
   const uint32_t* const ukeys = reinterpret_cast<const uint32_t*>(smem + (uk_s - sbase));
   const uint32_t* const uvals = reinterpret_cast<const uint32_t*>(smem + (uv_s - sbase));
   const uint64_t n = a.n;
@@ -729,7 +727,6 @@ __global__ void __launch_bounds__(128, SNAP ? 8 : 0) k_update_ring(const StreamU
     // heads.  Raw keys and rows are loaded one window before they are used.
     struct Win {
       uint32_t key, val, d4, vm, hm;
-      uint32_t snap0;  // lane 0: first snapshot-log position reserved for the window's heads
       uint64_t wofs;
     };
     uint32_t prev_key = 0xfffffffeu;  // key of the item before the window
@@ -756,10 +753,8 @@ __global__ void __launch_bounds__(128, SNAP ? 8 : 0) k_update_ring(const StreamU
       cp_async_p<4>(mom_s + ((win & 1u) * 32u + lane) * 4u, a.moments + (head ? key : 0u), head);
       if constexpr (SNAP) {
         // the heads' dirty-flag words (read at the head: a clean row is
-        // saved before its first write) and one log reservation per
-        // window (read a window later, so the atomic's latency is hidden)
+        // saved before its first write)
         cp_async_p<4>(dty_s + ((win & 1u) * 32u + lane) * 4u, a.dirty + ((head ? key : 0u) & ~3u), head);
-        w.snap0 = (lane == 0 && w.hm) ? atomicAdd(a.snap_count, (uint32_t)__popc(w.hm)) : 0u;
       }
       if constexpr (FULL) {  // slot-indexed rows of VPL*128 elements: no per-item row metadata
         if (head) {
@@ -959,8 +954,8 @@ __global__ void __launch_bounds__(128, SNAP ? 8 : 0) k_update_ring(const StreamU
             vold = *reinterpret_cast<const float*>(smem + (mom_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
             if constexpr (SNAP) {
               const uint32_t dw = *reinterpret_cast<const uint32_t*>(smem + (dty_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
-              const uint32_t pos = __shfl_sync(0xffffffffu, wc_.snap0, 0) + __popc(wc_.hm & ((1u << i) - 1u));
-              cur_snap = ((dw >> ((cur & 3u) * 8u)) & 0xffu) ? kNone : pos;
+              // log position = the head's sorted position (unique, no atomics)
+              cur_snap = ((dw >> ((cur & 3u) * 8u)) & 0xffu) ? kNone : (uint32_t)(a.snap_base + cur_pos);
             }
           }
           add_grad(slot0 + r);
@@ -1082,7 +1077,8 @@ void lookup_launch(const LookupArgs& a, cudaStream_t st) {
 
 template <typename WT, int VPL>
 void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
-  const size_t pw_u = (size_t)kSlots * VPL * 32 * 16 + 512 + 8 * kC;  // ring + head moments / dirty words + range keys/rows
+  const bool snap = a.snap != nullptr;
+  const size_t pw_u = update_warp_bytes(VPL, snap);  // ring + head moments + range keys/rows (+ dirty words)
   const uint32_t nw_u = warps_for(pw_u, 4);
   const bool full = a.uni_dim == 128u * VPL;
   if (a.n >= 2 * kC) {
@@ -1109,7 +1105,6 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
                static_cast<const double*>(a.part2), a.part3, (uint64_t)kC * kP * kP);
   // variants: FULL (slot-indexed uniform rows) x SNAP (M > 1 snapshot log);
   // their register counts differ, so each has its own occupancy
-  const bool snap = a.snap != nullptr;
   auto kern = full ? (snap ? k_update_ring<WT, VPL, true, true> : k_update_ring<WT, VPL, true, false>)
                    : (snap ? k_update_ring<WT, VPL, false, true> : k_update_ring<WT, VPL, false, false>);
   set_smem(kern, nw_u * pw_u);  // per device

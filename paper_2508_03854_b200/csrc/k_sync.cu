@@ -356,7 +356,7 @@ __global__ void k_sg_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDev
 // then averaged two at a time (their loads in flight together).
 constexpr int kMeanWarps = 8;
 template <typename WT, int kSyncV>
-__global__ void __launch_bounds__(kMeanWarps * 32) k_sg_mean(
+__global__ void __launch_bounds__(kMeanWarps * 32, 2) k_sg_mean(
     const float* __restrict__ stage, uint32_t M, uint32_t me, const uint32_t* __restrict__ lists,
     const uint32_t* __restrict__ counts, uint64_t cmax, const uint32_t* __restrict__ ulist,
     const uint32_t* __restrict__ ucount, const FeatDev* feats, const uint32_t* vbase_sorted,
@@ -407,42 +407,53 @@ __global__ void __launch_bounds__(kMeanWarps * 32) k_sg_mean(
         spos[h * 32 + lane] = ph + lo;
       }
     }
+    // per lane (row): its weight row, dim and, when this replica dirtied the
+    // row and some replica did not, the snapshot of its pre-interval value
+    uint32_t my_dim = 0, my_snap = 0xffffffffu;
+    uint64_t my_wofs = 0;
+    if (lane < rows) {
+      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, my_slot);
+      my_dim = feats[f].dim;
+      my_wofs = feats[f].wbase + (uint64_t)(my_slot - feats[f].vbase) * my_dim;
+      if (((found >> me) & 1u) && found != all) my_snap = snap_pos[my_slot];
+    }
     __syncwarp();
-    for (uint32_t j = 0; j < rows; j += 2) {
-      uint32_t slot[2], fnd[2], dim[2] = {0, 0};
-      WT* row[2] = {nullptr, nullptr};
-      const float* sp[2] = {nullptr, nullptr};
-      float4 own[2][kSyncV];
-      float own_m[2] = {0.f, 0.f}, snap_m[2] = {0.f, 0.f};
+    constexpr int R = kSyncV == 1 ? 4 : kSyncV == 2 ? 2 : 1;  // rows in flight
+    for (uint32_t j = 0; j < rows; j += R) {
+      uint32_t slot[R], fnd[R], dim[R];
+      WT* row[R];
+      const float* sp[R];
+      float4 own[R][kSyncV];
+      float own_m[R];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const uint32_t i = j + r;
-        slot[r] = __shfl_sync(0xffffffffu, my_slot, i & 31);
-        fnd[r] = __shfl_sync(0xffffffffu, found, i & 31);
-        if (i >= rows) continue;
-        const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot[r]);
-        dim[r] = feats[f].dim;
-        row[r] = w + feats[f].wbase + (uint64_t)(slot[r] - feats[f].vbase) * dim[r];
+      for (int r = 0; r < R; ++r) {
+        const uint32_t i = (j + r) & 31;
+        slot[r] = __shfl_sync(0xffffffffu, my_slot, i);
+        fnd[r] = __shfl_sync(0xffffffffu, found, i);
+        dim[r] = j + r < rows ? __shfl_sync(0xffffffffu, my_dim, i) : 0u;
+        const uint64_t wofs = shfl64(my_wofs, i);
+        const uint32_t sn = __shfl_sync(0xffffffffu, my_snap, i);
+        row[r] = w + wofs;
+        sp[r] = sn != 0xffffffffu ? snap + (uint64_t)sn * row_floats : nullptr;
+        own_m[r] = 0.f;
+        if (!dim[r]) continue;
 #pragma unroll
         for (int v = 0; v < kSyncV; ++v)
           if (lane + v * 32 < dim[r] / 4) own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
         own_m[r] = moments[slot[r]];
-        // x_0 for the replicas that left the row clean: this replica's own
-        // copy, or its snapshot when it dirtied the row itself
-        if (((fnd[r] >> me) & 1u) && fnd[r] != all) sp[r] = snap + (uint64_t)snap_pos[slot[r]] * row_floats;
       }
-      double acc[2][kSyncV][4], acc_m[2] = {0.0, 0.0};
+      double acc[R][kSyncV][4], acc_m[R];
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        if (sp[r]) snap_m[r] = sp[r][row_floats - 1];
+      for (int r = 0; r < R; ++r) {
+        acc_m[r] = 0.0;
 #pragma unroll
         for (int v = 0; v < kSyncV; ++v) acc[r][v][0] = acc[r][v][1] = acc[r][v][2] = acc[r][v][3] = 0.0;
       }
       for (uint32_t h = 0; h < M; ++h) {  // ascending group order
-        float4 x[2][kSyncV];
-        float xm[2];
+        float4 x[R][kSyncV];
+        float xm[R];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < R; ++r) {
           if (!dim[r]) continue;
           const float* src = nullptr;
           if (h != me) src = ((fnd[r] >> h) & 1u) ? stage + ((uint64_t)h * cmax + spos[h * 32 + j + r]) * row_floats : sp[r];
@@ -450,7 +461,7 @@ __global__ void __launch_bounds__(kMeanWarps * 32) k_sg_mean(
 #pragma unroll
             for (int v = 0; v < kSyncV; ++v)
               if (lane + v * 32 < dim[r] / 4) x[r][v] = *reinterpret_cast<const float4*>(src + (lane + v * 32) * 4);
-            xm[r] = src == sp[r] ? snap_m[r] : src[row_floats - 1];
+            xm[r] = src[row_floats - 1];
           } else {
 #pragma unroll
             for (int v = 0; v < kSyncV; ++v) x[r][v] = own[r][v];
@@ -458,7 +469,7 @@ __global__ void __launch_bounds__(kMeanWarps * 32) k_sg_mean(
           }
         }
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
+        for (int r = 0; r < R; ++r) {
           if (!dim[r]) continue;
 #pragma unroll
           for (int v = 0; v < kSyncV; ++v) {
@@ -471,7 +482,7 @@ __global__ void __launch_bounds__(kMeanWarps * 32) k_sg_mean(
         }
       }
 #pragma unroll
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < R; ++r) {
         if (!dim[r]) continue;
 #pragma unroll
         for (int v = 0; v < kSyncV; ++v)

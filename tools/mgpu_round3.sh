@@ -23,5 +23,5 @@ run n4 4 --steps 20 --warmup 5 --no-cpu-baseline
 run n2 2 --steps 20 --warmup 5 --no-cpu-baseline
 run cfg4_2x2_raw 4 --config cfg4 --mesh 2x2 --steps 10 --warmup 3 --nbatches 1 --no-cpu-baseline --no-e2e
 run cfg4_2x2_scrambled 4 --config cfg4 --mesh 2x2 --steps 10 --warmup 3 --nbatches 1 --scramble --no-cpu-baseline --no-e2e
-run cfg5_2x2_cM 4 --config cfg5 --mesh 2x2 --steps 5 --warmup 3 --nbatches 1 --no-cpu-baseline --no-e2e
-run cfg5_2x2_c1 4 --config cfg5 --mesh 2x2 --steps 5 --warmup 3 --nbatches 1 --c 1 --no-cpu-baseline --no-e2e
+run cfg5_2x2_cM 4 --config cfg5 --mesh 2x2 --steps 5 --warmup 3 --nbatches 1 --batch 16384 --no-cpu-baseline --no-e2e
+run cfg5_2x2_c1 4 --config cfg5 --mesh 2x2 --steps 5 --warmup 3 --nbatches 1 --batch 16384 --c 1 --no-cpu-baseline --no-e2e
