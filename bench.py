@@ -413,9 +413,12 @@ def run_ours(args):
     host_s["forward"] = host_s["backward"] = 0.0
     wait0 = eng.stats()["host_wait_ns"]
     with ClockSampler(local) as clk:
+        # a step-boundary event per step (recording does not drain the stream)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
         ev0.record(stream)
         for k in range(args.steps):
             step(args.warmup + k)
+            evs[k].record(stream)
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -441,7 +444,9 @@ def run_ours(args):
     ms_step = ms_max / args.steps
     value = world * w.batch * args.steps / (ms_max / 1e3)
     st = eng.stats()
-    mine = {"nnz_owned": st["nnz_owned"], "unique_rows": st["unique_rows"], "ms": ms,
+    step_ms = [round(ev0.elapsed_time(evs[0]), 4)] + [round(evs[k - 1].elapsed_time(evs[k]), 4)
+                                                       for k in range(1, args.steps)]
+    mine = {"nnz_owned": st["nnz_owned"], "unique_rows": st["unique_rows"], "ms": ms, "step_ms": step_ms,
             "phase_ms": {p: round(v[0] / max(1, n_split), 4) for p, v in split.items()},
             "host_ms_per_step": {k: round(1e3 * v / max(1, args.steps), 4) for k, v in host_timed.items()}}
     per_rank = [mine]

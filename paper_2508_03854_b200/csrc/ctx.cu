@@ -1130,6 +1130,15 @@ void Ctx::join_sync() {
   sync_pending = false;
 }
 
+// S2D_SYNC_OVERLAP=0 keeps the sync tail on the main stream (A/B switch)
+static bool sync_overlap_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("S2D_SYNC_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 bool Ctx::snapshot_enabled() const {
   if (M <= 1 || dp_p2p != 1) return false;
   static const bool off = [] {
@@ -1239,7 +1248,7 @@ void Ctx::replica_sync() {
     S2D_CUDA(cudaMemcpyAsync(d_counts, hc.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
     peer_alloc_in(dp_stage, (uint64_t)M * cmax * row_floats * 4, dp);  // same size everywhere
     const int sgd = opt.variant == S2D_SGD;
-    const bool overlap = !dp.local() && !profile;
+    const bool overlap = sync_overlap_enabled() && !dp.local() && !profile;
     cudaStream_t ts = stream;
     if (overlap) {
       S2D_CUDA(cudaEventRecord(ev_union, stream));
@@ -1294,7 +1303,7 @@ void Ctx::replica_sync() {
     // overlap it, and its lookup waits for it (join_sync).  Virtual ranks
     // synchronise on the host, so their tail stays on the main stream, as
     // does a profiled one (its phases are timed on the main stream).
-    const bool overlap = !dp.local() && !profile;
+    const bool overlap = sync_overlap_enabled() && !dp.local() && !profile;
     cudaStream_t ts = stream;
     if (overlap) {
       S2D_CUDA(cudaEventRecord(ev_union, stream));
