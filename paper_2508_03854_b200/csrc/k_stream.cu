@@ -654,7 +654,7 @@ constexpr uint32_t update_warp_bytes(int vpl, bool snap) {
   return (uint32_t)kSlots * vpl * 32 * 16 + 256 + 8 * kC + (snap ? 256 : 0);
 }
 template <typename WT, int VPL, bool FULL, bool SNAP>
-__global__ void __launch_bounds__(128) k_update_ring(const StreamUpdateArgs a) {
+__global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(const StreamUpdateArgs a) {
   pdl_wait();  // persistent single wave
   pdl_trigger();
   constexpr int kWinStages = 32 / kRowsPerStage;

@@ -372,21 +372,27 @@ __global__ void __launch_bounds__(kMeanWarps * 32, 2) k_sg_mean(
   const uint64_t nwarps = (uint64_t)gridDim.x * kMeanWarps;
   const double inv_m = 1.0 / (double)M;
   const uint32_t all = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
-  for (uint64_t c0 = ((uint64_t)blockIdx.x * kMeanWarps + wib) * 32; c0 < count; c0 += nwarps * 32) {
-    const uint32_t rows = count - c0 < 32 ? (uint32_t)(count - c0) : 32u;
-    const uint32_t my_slot = lane < rows ? ulist[c0 + lane] : 0xffffffffu;
-    const uint32_t first = __shfl_sync(0xffffffffu, my_slot, 0);
-    uint32_t p = 0;
-    if (lane < M) {  // lower bound of the chunk's first slot in L_lane
-      const uint32_t* L = lists + (uint64_t)lane * cmax;
-      uint32_t lo = 0, hi = counts[lane];
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (L[mid] < first) lo = mid + 1;
-        else hi = mid;
-      }
-      p = lo;
+  // each warp owns a contiguous block of whole 32-row chunks: one binary
+  // search per list at its start, then the list positions advance by the
+  // rows each chunk found
+  const uint64_t chunks = (count + 31) / 32, per_warp = (chunks + nwarps - 1) / nwarps;
+  const uint64_t gw = (uint64_t)blockIdx.x * kMeanWarps + wib;
+  const uint64_t r0 = gw * per_warp * 32, r1 = min((uint64_t)count, r0 + per_warp * 32);
+  uint32_t p = 0;
+  if (r0 < r1 && lane < M) {  // lower bound of the block's first slot in L_lane
+    const uint32_t first = ulist[r0];
+    const uint32_t* L = lists + (uint64_t)lane * cmax;
+    uint32_t lo = 0, hi = counts[lane];
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (L[mid] < first) lo = mid + 1;
+      else hi = mid;
     }
+    p = lo;
+  }
+  for (uint64_t c0 = r0; c0 < r1; c0 += 32) {
+    const uint32_t rows = r1 - c0 < 32 ? (uint32_t)(r1 - c0) : 32u;
+    const uint32_t my_slot = lane < rows ? ulist[c0 + lane] : 0xffffffffu;
     for (uint32_t h = 0; h < M; ++h) {
       const uint32_t ph = __shfl_sync(0xffffffffu, p, h);
       const uint32_t ch = counts[h];
@@ -406,6 +412,10 @@ __global__ void __launch_bounds__(kMeanWarps * 32, 2) k_sg_mean(
         found |= 1u << h;
         spos[h * 32 + lane] = ph + lo;
       }
+    }
+    for (uint32_t h = 0; h < M; ++h) {  // advance past this chunk's entries
+      const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, (found >> h) & 1u));
+      if (lane == h) p += cnt;
     }
     // per lane (row): its weight row, dim and, when this replica dirtied the
     // row and some replica did not, the snapshot of its pre-interval value

@@ -4,6 +4,7 @@ set -u
 O=${1:-gpurun_out/sab}
 mkdir -p $O
 python -m paper_2508_03854_b200.build > /dev/null 2>&1
+timeout 600 python -m pytest tests/test_multigpu.py -q -x -k "local" 2>&1 | tail -2
 run() {  # name env mesh
   local name=$1 envs=$2 mesh=$3
   env $envs timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port $((29600 + RANDOM % 300)) bench.py --gpus 4 --mesh $mesh --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > $O/$name.json 2> $O/$name.err
@@ -11,8 +12,8 @@ run() {  # name env mesh
 import json; d=json.load(open('$O/$name.json')); print('$name', round(d['ms_per_step'],4), d['step_stats']['sync_mode'], [round(r['ms'],1) for r in d['per_rank']], [max(r['step_ms']) for r in d['per_rank']], {k: round(v,3) for k,v in d['phase_split_ms'].items() if k.startswith('sync') or k=='update'})" 2>/dev/null || tail -3 $O/$name.err
 }
 run 2x2_snap "S2D_SYNC_SNAPSHOT=1" 2x2
-run 2x2_snap_noov "S2D_SYNC_OVERLAP=0" 2x2
+
 run 2x2_slice "S2D_SYNC_SNAPSHOT=0" 2x2
-run 2x2_snap_b "S2D_SYNC_SNAPSHOT=1" 2x2
+
 run 1x4_snap "S2D_SYNC_SNAPSHOT=1" 1x4
 run 1x4_slice "S2D_SYNC_SNAPSHOT=0" 1x4
