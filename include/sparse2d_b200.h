@@ -103,7 +103,7 @@ typedef struct {
   uint64_t a2a_bytes_recv;
   uint64_t sync_bytes;     /* replica-sync payload bytes sent */
   uint32_t error_flags;    /* device-side fault bits of the last step */
-  uint32_t sync_mode;      /* last replica sync: 0 none, 1 snapshot dirty-row exchange, 2 slice push/mean/scatter, 3 NCCL all-gather */
+  uint32_t sync_mode;      /* last replica sync: 0 none, 1 pair snapshot exchange (M = 2), 2 slice push/mean/scatter, 3 NCCL all-gather */
   uint64_t ids_bytes_sent;    /* part of a2a_bytes_sent: lengths + ids (K1 permute) */
   uint64_t lookup_bytes_sent; /* part of a2a_bytes_sent: partials / pooled rows (K2) */
   uint64_t grad_bytes_sent;   /* part of a2a_bytes_sent: gradient rows (grad gather) */

@@ -312,21 +312,19 @@ void launch_flag_count(const uint8_t* dirty, uint32_t n_slots, uint32_t* count, 
 void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, const void* tmp, cudaStream_t st);
 size_t flag_tmp_bytes(uint32_t n_slots);
 void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, cudaStream_t st);
-// Snapshot replica sync (k_sync.cu): every replica pushes the rows it
-// dirtied (its list, f32 row + moment) into every peer's staging [M][cmax];
-// after a group barrier each replica forms every union row's mean itself
-// from its own copy, the peers' pushed copies and, for a peer that left
-// the row clean, the row's pre-interval value (its own snapshot when it
-// dirtied the row, else its current copy).
-void launch_sg_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
-                    const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                    const uint32_t* list, const uint32_t* count, uint32_t count_ub, const void* weights, int bf16,
-                    const float* moments, uint32_t row_floats, uint64_t cmax, cudaStream_t st);
-void launch_sg_mean(const float* stage, uint32_t M, uint32_t me, const uint32_t* lists, const uint32_t* counts,
-                    uint64_t cmax, const uint32_t* ulist, const uint32_t* ucount, uint32_t ucount_ub,
-                    const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                    const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16,
-                    float* moments, int sgd, cudaStream_t st);
+// Pair (M = 2) snapshot replica sync (k_sync.cu): each replica sends the
+// rows it dirtied once -- the final mean for a row only it dirtied (from its
+// row and the update's snapshot of the row's pre-interval value), its copy
+// for a row both dirtied -- and the receiver stores / averages them.
+void launch_pair_push(float* peer_stage, uint32_t me, const uint32_t* mine, const uint32_t* counts,
+                      const uint32_t* theirs, uint32_t mine_n, const FeatDev* feats, const uint32_t* vbase_sorted,
+                      const uint32_t* feat_of_vbase, uint32_t n_feat, const float* snap, const uint32_t* snap_pos,
+                      uint32_t row_floats, void* weights, int bf16, float* moments, int sgd, uint32_t* n_both,
+                      cudaStream_t st);
+void launch_pair_recv(const float* stage, uint32_t me, const uint32_t* theirs, const uint32_t* counts,
+                      uint32_t theirs_n, const FeatDev* feats, const uint32_t* vbase_sorted,
+                      const uint32_t* feat_of_vbase, uint32_t n_feat, uint32_t row_floats, void* weights, int bf16,
+                      float* moments, int sgd, cudaStream_t st);
 void launch_pack_rows(const FeatDev* feats, const uint32_t* vbase_sorted,
                       const uint32_t* feat_of_vbase, uint32_t n_feat_owned, const uint32_t* list,
                       const uint32_t* count, const void* weights, int bf16, const float* moments,

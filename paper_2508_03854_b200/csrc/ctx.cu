@@ -1102,8 +1102,10 @@ void Ctx::refresh_stats() {
   if (sync_stats_pending) {  // the last replica sync's union length (device-side count)
     join_sync();
     S2D_CUDA(cudaStreamSynchronize(stream));
-    uint32_t count = 0;
-    S2D_CUDA(cudaMemcpy(&count, sync_count.p, 4, cudaMemcpyDeviceToHost));
+    uint32_t cw[5] = {0, 0, 0, 0, 0};
+    S2D_CUDA(cudaMemcpy(cw, sync_count.p, 20, cudaMemcpyDeviceToHost));
+    // the union: counted on the device, or (pair sync) both lists less the rows both hold
+    const uint32_t count = sync_snapshot_used ? (uint32_t)(sync_pair_rows - cw[4]) : cw[0];
     const uint64_t rf = max_dim + 4;
     const uint64_t lo = (uint64_t)count * group / M, hi = (uint64_t)count * (group + 1) / M;
     stats.dirty_rows = count;
@@ -1140,7 +1142,7 @@ static bool sync_overlap_enabled() {
 }
 
 bool Ctx::snapshot_enabled() const {
-  if (M <= 1 || dp_p2p != 1) return false;
+  if (M != 2 || dp_p2p != 1) return false;  // the pair sync (M > 2: slice push / mean / scatter)
   static const bool off = [] {
     const char* e = std::getenv("S2D_SYNC_SNAPSHOT");
     return e && e[0] == '0';
@@ -1234,19 +1236,18 @@ void Ctx::replica_sync() {
     S2D_CUDA(cudaMemsetAsync(sync_list.as<uint32_t>() + mine, 0xff, (size_t)(cmax - mine) * 4, stream));
   sync_lists.ensure((uint64_t)cmax * M * 4);
   dp.allgather(sync_list.p, sync_lists.p, (size_t)cmax * 4, stream);
-  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
-  launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
   const uint32_t row_floats = max_dim + 4;  // row + moment, 16-byte pitch
   dp_setup();
   sync_snapshot_used = false;
   if (use_snap) {
-    // Snapshot sync (k_sync.cu): the rows each replica dirtied go once to
-    // every peer; every replica then averages every union row locally.
-    const uint32_t count_ub = (uint32_t)std::min<uint64_t>((uint64_t)M * cmax, n_slots);
-    sync_list.ensure((uint64_t)count_ub * 4);
-    launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+    // Pair sync (M = 2, k_sync.cu): each replica sends the rows it dirtied
+    // once -- the final mean of a row only it dirtied, its copy of a row
+    // both dirtied -- into the peer's staging (its list order); after a
+    // group barrier each replica stores / averages the peer's entries.
+    const uint32_t peer = group ^ 1u;
     S2D_CUDA(cudaMemcpyAsync(d_counts, hc.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
-    peer_alloc_in(dp_stage, (uint64_t)M * cmax * row_floats * 4, dp);  // same size everywhere
+    S2D_CUDA(cudaMemsetAsync(d_count + 4, 0, 4, stream));  // rows both replicas dirtied
+    peer_alloc_in(dp_stage, (uint64_t)cmax * row_floats * 4, dp);  // same size everywhere
     const int sgd = opt.variant == S2D_SGD;
     const bool overlap = sync_overlap_enabled() && !dp.local() && !profile;
     cudaStream_t ts = stream;
@@ -1255,17 +1256,17 @@ void Ctx::replica_sync() {
       S2D_CUDA(cudaStreamWaitEvent(sync_stream, ev_union, 0));
       ts = sync_stream;
     }
+    const uint32_t* lists = sync_lists.as<uint32_t>();
     phase_begin(kPhSyncPush);
-    launch_sg_push(ptrs(dp_stage), group, M, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
-                   d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(),
-                   sync_lists.as<uint32_t>() + (uint64_t)group * cmax, d_counts + group, mine, weights.p, bf16,
-                   moments.as<float>(), row_floats, cmax, ts);
-    dp_barrier(ts);  // every replica's dirty rows are staged at every peer
+    launch_pair_push(reinterpret_cast<float*>(ptrs(dp_stage).p[peer]), group, lists + (uint64_t)group * cmax, d_counts,
+                     lists + (uint64_t)peer * cmax, mine, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
+                     d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), snap.as<float>(),
+                     snap_pos.as<uint32_t>(), row_floats, weights.p, bf16, moments.as<float>(), sgd, d_count + 4, ts);
+    dp_barrier(ts);  // the peer's entries have landed here
     phase_begin(kPhSyncMean);
-    launch_sg_mean(dp_stage.buf.as<float>(), M, group, sync_lists.as<uint32_t>(), d_counts, cmax,
-                   sync_list.as<uint32_t>(), d_count, count_ub, d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(),
-                   d_feat_of_vbase.as<uint32_t>(), (uint32_t)feat_of_vbase.size(), snap.as<float>(),
-                   snap_pos.as<uint32_t>(), row_floats, weights.p, bf16, moments.as<float>(), sgd, ts);
+    launch_pair_recv(dp_stage.buf.as<float>(), group, lists + (uint64_t)peer * cmax, d_counts, hc[peer],
+                     d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
+                     (uint32_t)feat_of_vbase.size(), row_floats, weights.p, bf16, moments.as<float>(), sgd, ts);
     phase_begin(kPhSyncScatter);
     launch_zero(dirty.p, n_slots, ts);
     if (overlap) {
@@ -1276,11 +1277,14 @@ void Ctx::replica_sync() {
     sync_snapshot_used = true;
     stats.sync_mode = 1;
     sync_sent_rows = mine;
+    sync_pair_rows = (uint64_t)hc[0] + hc[1];
     sync_cmax = cmax;
     phase_end();
     finish_call();
     return;
   }
+  launch_mark_slots(sync_lists.as<uint32_t>(), (uint64_t)cmax * M, n_slots, dirty.as<uint8_t>(), stream);
+  launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
   if (dp_p2p == 1) {
     // The union's length stays on the device: every size below uses the
     // bound count_ub = min(M * cmax, n_slots), identical on every replica,

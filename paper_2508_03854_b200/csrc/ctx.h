@@ -78,6 +78,7 @@ struct Ctx {
   bool sync_pending = false, sync_stats_pending = false;
   uint32_t sync_cmax = 0;
   uint64_t sync_sent_rows = 0;  // rows this replica pushed at the last sync (stats)
+  uint64_t sync_pair_rows = 0;  // pair sync: both replicas' list lengths (stats)
   bool sync_snapshot_used = false;
   // M > 1 snapshot log (StreamUpdateArgs::snap): snap_ub = log rows the
   // interval's updates span (every item of every update since the last

@@ -292,220 +292,207 @@ __global__ void k_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted
   }
 }
 
-// ---- snapshot replica sync -------------------------------------------------
-// Every union row x's replicas: x_g is replica g's current row if g dirtied
-// it this interval, else the row's value at the last sync (x_0 below).
-// Replica g pushes the rows it dirtied (its ascending list L_g, entry j) to
-// every peer h's staging [g][j]; replica h then has, for each union row,
-// its own current row, the pushed copies of the replicas that dirtied it
-// and x_0 (its current row if it left the row clean, else the snapshot the
-// update saved before its first write).  Each replica forms the same
-// f32((sum_{g asc} f64 x_g) * (1/M)) (deterministic_mean_inplace,
-// topology.cpp:150-163) for every union row, so one exchange of dirty rows
-// replaces the slice push / mean / scatter round trip: (M-1) x |L_g| rows
-// leave replica g instead of 2 (M-1)/M x |union|.
+// ---- pair (M = 2) snapshot replica sync -----------------------------------
+// Row x's replicas x_0, x_1: replica g's current row if g dirtied it this
+// interval, else the row's value at the last sync (x_0 of the interval).
+// The update saved that value (snapshot log) before a replica's first write
+// to the row, so for a row only replica g dirtied, g alone forms the mean
+// f32((f64 x_0 + f64 x_1) * 0.5) (deterministic_mean_inplace,
+// topology.cpp:150-163, ascending group order) from its row and its
+// snapshot, stores it, and sends the mean; a row both dirtied is sent as
+// g's copy and both replicas average it on receipt.  Each replica sends its
+// dirty rows once (no union list, no slice round trip); the receiver streams
+// the peer's entries in the peer's list order.
+//
+// Staging entry j of the peer's list: f32 row | flag at rf - 2 (1 = final
+// mean, 0 = copy) | moment at rf - 1.
+constexpr int kPairWarps = 8;
 template <typename WT, int kSyncV>
-__global__ void k_sg_push(PeerPtrs stage, uint32_t me, uint32_t M, const FeatDev* feats,
-                          const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                          const uint32_t* __restrict__ list, const uint32_t* __restrict__ count_ptr,
-                          const WT* __restrict__ w, const float* __restrict__ moments, uint32_t row_floats,
-                          uint64_t cmax) {
+__global__ void __launch_bounds__(kPairWarps * 32) k_pair_push(
+    float* __restrict__ peer_stage, uint32_t me, const uint32_t* __restrict__ mine, const uint32_t* __restrict__ counts,
+    const uint32_t* __restrict__ theirs, const FeatDev* feats, const uint32_t* vbase_sorted,
+    const uint32_t* feat_of_vbase, uint32_t n_feat, const float* __restrict__ snap, const uint32_t* __restrict__ snap_pos,
+    uint32_t row_floats, WT* __restrict__ w, float* __restrict__ moments, int sgd, uint32_t* __restrict__ n_both) {
   pdl_wait();
-  const uint32_t count = *count_ptr;
-  const uint32_t lane = lane_id();
-  const uint32_t warps = gridDim.x * (blockDim.x / 32);
-  for (uint32_t i0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * kSyncRows; i0 < count;
-       i0 += warps * kSyncRows) {
-    float4 d[kSyncRows][kSyncV];
-    float mom[kSyncRows];
-    uint32_t dim[kSyncRows];
-#pragma unroll
-    for (int r = 0; r < kSyncRows; ++r) {
-      const uint32_t i = i0 + r;
-      dim[r] = 0;
-      if (i >= count) continue;
-      const uint32_t slot = list[i];
-      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot);
-      dim[r] = feats[f].dim;
-      const WT* row = w + feats[f].wbase + (uint64_t)(slot - feats[f].vbase) * dim[r];
-#pragma unroll
-      for (int v = 0; v < kSyncV; ++v)
-        if (lane + v * 32 < dim[r] / 4) d[r][v] = load4_f32(row + (lane + v * 32) * 4);
-      mom[r] = lane == 0 ? moments[slot] : 0.f;
-    }
-    for (uint32_t h = 0; h < M; ++h) {
-      if (h == me) continue;
-      float* base = reinterpret_cast<float*>(stage.p[h]) + ((uint64_t)me * cmax + i0) * row_floats;
-#pragma unroll
-      for (int r = 0; r < kSyncRows; ++r) {
-        if (!dim[r]) continue;
-        float* out = base + (uint64_t)r * row_floats;
-#pragma unroll
-        for (int v = 0; v < kSyncV; ++v)
-          if (lane + v * 32 < dim[r] / 4) *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = d[r][v];
-        if (lane == 0) out[row_floats - 1] = mom[r];
-      }
-    }
-  }
-}
-
-// One warp per chunk of 32 union rows.  Membership of each row in every
-// replica's ascending list L_h comes from a merge: lane h finds the chunk's
-// first slot in L_h (binary search), the next 32 entries of every list are
-// staged in shared memory, and each lane locates its row in them.  Rows are
-// then averaged two at a time (their loads in flight together).
-constexpr int kMeanWarps = 8;
-template <typename WT, int kSyncV>
-__global__ void __launch_bounds__(kMeanWarps * 32, 2) k_sg_mean(
-    const float* __restrict__ stage, uint32_t M, uint32_t me, const uint32_t* __restrict__ lists,
-    const uint32_t* __restrict__ counts, uint64_t cmax, const uint32_t* __restrict__ ulist,
-    const uint32_t* __restrict__ ucount, const FeatDev* feats, const uint32_t* vbase_sorted,
-    const uint32_t* feat_of_vbase, uint32_t n_feat, const float* __restrict__ snap,
-    const uint32_t* __restrict__ snap_pos, uint32_t row_floats, WT* __restrict__ w, float* __restrict__ moments,
-    int sgd) {
-  pdl_wait();
-  extern __shared__ uint32_t s_mean[];  // per warp: next entries [M][32] | positions [M][32]
-  const uint32_t count = *ucount;
+  __shared__ uint32_t s_their[kPairWarps][32];
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
-  uint32_t* sl = s_mean + (size_t)wib * 64 * M;
-  uint32_t* spos = sl + 32 * M;
-  const uint64_t nwarps = (uint64_t)gridDim.x * kMeanWarps;
-  const double inv_m = 1.0 / (double)M;
-  const uint32_t all = M >= 32 ? 0xffffffffu : ((1u << M) - 1u);
-  // each warp owns a contiguous block of whole 32-row chunks: one binary
-  // search per list at its start, then the list positions advance by the
-  // rows each chunk found
+  const uint32_t count = counts[me], their_n = counts[me ^ 1u];
+  const uint64_t nwarps = (uint64_t)gridDim.x * kPairWarps;
   const uint64_t chunks = (count + 31) / 32, per_warp = (chunks + nwarps - 1) / nwarps;
-  const uint64_t gw = (uint64_t)blockIdx.x * kMeanWarps + wib;
+  const uint64_t gw = (uint64_t)blockIdx.x * kPairWarps + wib;
   const uint64_t r0 = gw * per_warp * 32, r1 = min((uint64_t)count, r0 + per_warp * 32);
-  uint32_t p = 0;
-  if (r0 < r1 && lane < M) {  // lower bound of the block's first slot in L_lane
-    const uint32_t first = ulist[r0];
-    const uint32_t* L = lists + (uint64_t)lane * cmax;
-    uint32_t lo = 0, hi = counts[lane];
+  uint32_t q = 0;  // position in the peer's list (lane 0's search, then advanced per chunk)
+  if (r0 < r1) {
+    const uint32_t first = mine[r0];
+    uint32_t lo = 0, hi = their_n;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (L[mid] < first) lo = mid + 1;
+      if (theirs[mid] < first) lo = mid + 1;
       else hi = mid;
     }
-    p = lo;
+    q = lo;
   }
+  uint32_t both_n = 0;
   for (uint64_t c0 = r0; c0 < r1; c0 += 32) {
     const uint32_t rows = r1 - c0 < 32 ? (uint32_t)(r1 - c0) : 32u;
-    const uint32_t my_slot = lane < rows ? ulist[c0 + lane] : 0xffffffffu;
-    for (uint32_t h = 0; h < M; ++h) {
-      const uint32_t ph = __shfl_sync(0xffffffffu, p, h);
-      const uint32_t ch = counts[h];
-      sl[h * 32 + lane] = ph + lane < ch ? lists[(uint64_t)h * cmax + ph + lane] : 0xffffffffu;
-    }
+    const uint32_t my_slot = lane < rows ? mine[c0 + lane] : 0xffffffffu;
+    s_their[wib][lane] = q + lane < their_n ? theirs[q + lane] : 0xffffffffu;
     __syncwarp();
-    uint32_t found = 0;
-    for (uint32_t h = 0; h < M; ++h) {
-      const uint32_t ph = __shfl_sync(0xffffffffu, p, h);
-      uint32_t lo = 0, hi = 32;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (sl[h * 32 + mid] < my_slot) lo = mid + 1;
-        else hi = mid;
-      }
-      if (lane < rows && lo < 32 && sl[h * 32 + lo] == my_slot) {
-        found |= 1u << h;
-        spos[h * 32 + lane] = ph + lo;
-      }
+    uint32_t lo = 0, hi = 32;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (s_their[wib][mid] < my_slot) lo = mid + 1;
+      else hi = mid;
     }
-    for (uint32_t h = 0; h < M; ++h) {  // advance past this chunk's entries
-      const uint32_t cnt = __popc(__ballot_sync(0xffffffffu, (found >> h) & 1u));
-      if (lane == h) p += cnt;
-    }
-    // per lane (row): its weight row, dim and, when this replica dirtied the
-    // row and some replica did not, the snapshot of its pre-interval value
+    const bool both = lane < rows && lo < 32 && s_their[wib][lo] == my_slot;
+    const uint32_t bm = __ballot_sync(0xffffffffu, both);
+    q += __popc(bm);
+    both_n += __popc(bm);
+    __syncwarp();
+    // per lane (row): weight row, dim, snapshot (a row only this replica dirtied)
     uint32_t my_dim = 0, my_snap = 0xffffffffu;
     uint64_t my_wofs = 0;
     if (lane < rows) {
       const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, my_slot);
       my_dim = feats[f].dim;
       my_wofs = feats[f].wbase + (uint64_t)(my_slot - feats[f].vbase) * my_dim;
-      if (((found >> me) & 1u) && found != all) my_snap = snap_pos[my_slot];
+      if (!both) my_snap = snap_pos[my_slot];
     }
-    __syncwarp();
     constexpr int R = kSyncV == 1 ? 4 : kSyncV == 2 ? 2 : 1;  // rows in flight
     for (uint32_t j = 0; j < rows; j += R) {
-      uint32_t slot[R], fnd[R], dim[R];
+      float4 own[R][kSyncV], old[R][kSyncV];
+      float own_m[R], old_m[R];
+      uint32_t dim[R], slot[R];
       WT* row[R];
       const float* sp[R];
-      float4 own[R][kSyncV];
-      float own_m[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const uint32_t i = (j + r) & 31;
         slot[r] = __shfl_sync(0xffffffffu, my_slot, i);
-        fnd[r] = __shfl_sync(0xffffffffu, found, i);
         dim[r] = j + r < rows ? __shfl_sync(0xffffffffu, my_dim, i) : 0u;
-        const uint64_t wofs = shfl64(my_wofs, i);
+        row[r] = w + shfl64(my_wofs, i);
         const uint32_t sn = __shfl_sync(0xffffffffu, my_snap, i);
-        row[r] = w + wofs;
         sp[r] = sn != 0xffffffffu ? snap + (uint64_t)sn * row_floats : nullptr;
-        own_m[r] = 0.f;
-        if (!dim[r]) continue;
-#pragma unroll
-        for (int v = 0; v < kSyncV; ++v)
-          if (lane + v * 32 < dim[r] / 4) own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
-        own_m[r] = moments[slot[r]];
-      }
-      double acc[R][kSyncV][4], acc_m[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        acc_m[r] = 0.0;
-#pragma unroll
-        for (int v = 0; v < kSyncV; ++v) acc[r][v][0] = acc[r][v][1] = acc[r][v][2] = acc[r][v][3] = 0.0;
-      }
-      for (uint32_t h = 0; h < M; ++h) {  // ascending group order
-        float4 x[R][kSyncV];
-        float xm[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!dim[r]) continue;
-          const float* src = nullptr;
-          if (h != me) src = ((fnd[r] >> h) & 1u) ? stage + ((uint64_t)h * cmax + spos[h * 32 + j + r]) * row_floats : sp[r];
-          if (src) {
-#pragma unroll
-            for (int v = 0; v < kSyncV; ++v)
-              if (lane + v * 32 < dim[r] / 4) x[r][v] = *reinterpret_cast<const float4*>(src + (lane + v * 32) * 4);
-            xm[r] = src[row_floats - 1];
-          } else {
-#pragma unroll
-            for (int v = 0; v < kSyncV; ++v) x[r][v] = own[r][v];
-            xm[r] = own_m[r];
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          if (!dim[r]) continue;
-#pragma unroll
-          for (int v = 0; v < kSyncV; ++v) {
-            acc[r][v][0] += (double)x[r][v].x;
-            acc[r][v][1] += (double)x[r][v].y;
-            acc[r][v][2] += (double)x[r][v].z;
-            acc[r][v][3] += (double)x[r][v].w;
-          }
-          acc_m[r] += (double)xm[r];
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
+        own_m[r] = old_m[r] = 0.f;
         if (!dim[r]) continue;
 #pragma unroll
         for (int v = 0; v < kSyncV; ++v)
           if (lane + v * 32 < dim[r] / 4) {
-            double d[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) d[q] = (double)(float)(acc[r][v][q] * inv_m);
-            Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
+            own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
+            if (sp[r]) old[r][v] = *reinterpret_cast<const float4*>(sp[r] + (lane + v * 32) * 4);
           }
-        if (lane == 0 && !sgd) moments[slot[r]] = (float)(acc_m[r] * inv_m);
+        own_m[r] = moments[slot[r]];
+        if (sp[r]) old_m[r] = sp[r][row_floats - 1];
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!dim[r]) continue;
+        float* out = peer_stage + (c0 + j + r) * (uint64_t)row_floats;
+        if (sp[r]) {  // only this replica dirtied the row: the mean, here and at the peer
+#pragma unroll
+          for (int v = 0; v < kSyncV; ++v)
+            if (lane + v * 32 < dim[r] / 4) {
+              const float4 a = me == 0 ? own[r][v] : old[r][v], b = me == 0 ? old[r][v] : own[r][v];
+              const float4 m = make_float4((float)(((double)a.x + (double)b.x) * 0.5),
+                                           (float)(((double)a.y + (double)b.y) * 0.5),
+                                           (float)(((double)a.z + (double)b.z) * 0.5),
+                                           (float)(((double)a.w + (double)b.w) * 0.5));
+              const double d[4] = {(double)m.x, (double)m.y, (double)m.z, (double)m.w};
+              Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
+              *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = m;
+            }
+          if (lane == 0) {
+            const float am = me == 0 ? own_m[r] : old_m[r], bm2 = me == 0 ? old_m[r] : own_m[r];
+            const float mm = (float)(((double)am + (double)bm2) * 0.5);
+            if (!sgd) moments[slot[r]] = mm;
+            out[row_floats - 2] = 1.f;
+            out[row_floats - 1] = mm;
+          }
+        } else {  // both replicas dirtied it: send this replica's copy
+#pragma unroll
+          for (int v = 0; v < kSyncV; ++v)
+            if (lane + v * 32 < dim[r] / 4) *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = own[r][v];
+          if (lane == 0) {
+            out[row_floats - 2] = 0.f;
+            out[row_floats - 1] = own_m[r];
+          }
+        }
       }
     }
     __syncwarp();
+  }
+  if (lane == 0 && both_n) atomicAdd(n_both, both_n);
+}
+
+// The peer's entries (its list order): a final mean is stored as is; a copy
+// is averaged with this replica's row in ascending group order.
+template <typename WT, int kSyncV>
+__global__ void __launch_bounds__(256) k_pair_recv(const float* __restrict__ stage, uint32_t me,
+                                                   const uint32_t* __restrict__ theirs,
+                                                   const uint32_t* __restrict__ counts, const FeatDev* feats,
+                                                   const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase,
+                                                   uint32_t n_feat, uint32_t row_floats, WT* __restrict__ w,
+                                                   float* __restrict__ moments, int sgd) {
+  pdl_wait();
+  const uint32_t count = counts[me ^ 1u];
+  const uint32_t lane = lane_id();
+  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  constexpr int R = kSyncV == 1 ? 4 : kSyncV == 2 ? 2 : 1;
+  for (uint32_t i0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * R; i0 < count; i0 += warps * R) {
+    float4 x[R][kSyncV], own[R][kSyncV];
+    float xm[R], flag[R], own_m[R];
+    uint32_t dim[R], slot[R];
+    WT* row[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint32_t i = i0 + r;
+      dim[r] = 0;
+      if (i >= count) continue;
+      slot[r] = theirs[i];
+      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot[r]);
+      dim[r] = feats[f].dim;
+      row[r] = w + feats[f].wbase + (uint64_t)(slot[r] - feats[f].vbase) * dim[r];
+      const float* in = stage + (uint64_t)i * row_floats;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) x[r][v] = *reinterpret_cast<const float4*>(in + (lane + v * 32) * 4);
+      flag[r] = in[row_floats - 2];
+      xm[r] = in[row_floats - 1];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {  // a copy: this replica's row too
+      own_m[r] = 0.f;
+      if (!dim[r] || flag[r] != 0.f) continue;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
+      own_m[r] = moments[slot[r]];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!dim[r]) continue;
+      const bool fin = flag[r] != 0.f;
+#pragma unroll
+      for (int v = 0; v < kSyncV; ++v)
+        if (lane + v * 32 < dim[r] / 4) {
+          float4 m = x[r][v];
+          if (!fin) {
+            const float4 a = me == 0 ? own[r][v] : x[r][v], b = me == 0 ? x[r][v] : own[r][v];
+            m = make_float4((float)(((double)a.x + (double)b.x) * 0.5), (float)(((double)a.y + (double)b.y) * 0.5),
+                            (float)(((double)a.z + (double)b.z) * 0.5), (float)(((double)a.w + (double)b.w) * 0.5));
+          }
+          const double d[4] = {(double)m.x, (double)m.y, (double)m.z, (double)m.w};
+          Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
+        }
+      if (lane == 0 && !sgd) {
+        float mm = xm[r];
+        if (!fin) {
+          const float am = me == 0 ? own_m[r] : xm[r], bm = me == 0 ? xm[r] : own_m[r];
+          mm = (float)(((double)am + (double)bm) * 0.5);
+        }
+        moments[slot[r]] = mm;
+      }
+    }
   }
 }
 
@@ -655,76 +642,67 @@ void launch_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted, cons
 }
 
 template <int V>
-void sg_push_v(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats, const uint32_t* vbase_sorted,
-               const uint32_t* feat_of_vbase, uint32_t n_feat, const uint32_t* list, const uint32_t* count,
-               unsigned grid, const void* weights, int bf16, const float* moments, uint32_t row_floats, uint64_t cmax,
-               cudaStream_t st) {
-  if (bf16)
-    pdl_launch(k_sg_push<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted,
-               feat_of_vbase, n_feat, list, count, reinterpret_cast<const __nv_bfloat16*>(weights), moments,
-               row_floats, cmax);
-  else
-    pdl_launch(k_sg_push<float, V>, dim3(grid), dim3(256), 0, st, stage, me, M, feats, vbase_sorted, feat_of_vbase,
-               n_feat, list, count, reinterpret_cast<const float*>(weights), moments, row_floats, cmax);
-}
-
-void launch_sg_push(const PeerPtrs& stage, uint32_t me, uint32_t M, const FeatDev* feats,
-                    const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                    const uint32_t* list, const uint32_t* count, uint32_t count_ub, const void* weights, int bf16,
-                    const float* moments, uint32_t row_floats, uint64_t cmax, cudaStream_t st) {
-  if (!count_ub) return;
-  const unsigned grid = (unsigned)std::min<uint64_t>((count_ub + 8 * kSyncRows - 1) / (8 * kSyncRows), 148ull * 16);
-  const uint32_t d4 = (row_floats - 4) / 4;
-  if (d4 <= 32)
-    sg_push_v<1>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
-                 row_floats, cmax, st);
-  else if (d4 <= 64)
-    sg_push_v<2>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
-                 row_floats, cmax, st);
-  else
-    sg_push_v<4>(stage, me, M, feats, vbase_sorted, feat_of_vbase, n_feat, list, count, grid, weights, bf16, moments,
-                 row_floats, cmax, st);
-}
-
-template <int V>
-void sg_mean_v(unsigned grid, size_t smem, const float* stage, uint32_t M, uint32_t me, const uint32_t* lists,
-               const uint32_t* counts, uint64_t cmax, const uint32_t* ulist, const uint32_t* ucount,
-               const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-               const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16,
-               float* moments, int sgd, cudaStream_t st) {
-  if (bf16) {
-    set_max_dynamic_smem(k_sg_mean<__nv_bfloat16, V>, smem);
-    pdl_launch(k_sg_mean<__nv_bfloat16, V>, dim3(grid), dim3(kMeanWarps * 32), smem, st, stage, M, me, lists, counts,
-               cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase, n_feat, snap, snap_pos, row_floats,
-               reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd);
+void pair_v(bool push, unsigned grid, float* peer_stage, const float* stage, uint32_t me, const uint32_t* mine,
+            const uint32_t* counts, const uint32_t* theirs, const FeatDev* feats, const uint32_t* vbase_sorted,
+            const uint32_t* feat_of_vbase, uint32_t n_feat, const float* snap, const uint32_t* snap_pos,
+            uint32_t row_floats, void* weights, int bf16, float* moments, int sgd, uint32_t* n_both, cudaStream_t st) {
+  if (push) {
+    if (bf16)
+      pdl_launch(k_pair_push<__nv_bfloat16, V>, dim3(grid), dim3(kPairWarps * 32), 0, st, peer_stage, me, mine, counts,
+                 theirs, feats, vbase_sorted, feat_of_vbase, n_feat, snap, snap_pos, row_floats,
+                 reinterpret_cast<__nv_bfloat16*>(weights), moments, sgd, n_both);
+    else
+      pdl_launch(k_pair_push<float, V>, dim3(grid), dim3(kPairWarps * 32), 0, st, peer_stage, me, mine, counts, theirs,
+                 feats, vbase_sorted, feat_of_vbase, n_feat, snap, snap_pos, row_floats, reinterpret_cast<float*>(weights),
+                 moments, sgd, n_both);
   } else {
-    set_max_dynamic_smem(k_sg_mean<float, V>, smem);
-    pdl_launch(k_sg_mean<float, V>, dim3(grid), dim3(kMeanWarps * 32), smem, st, stage, M, me, lists, counts, cmax,
-               ulist, ucount, feats, vbase_sorted, feat_of_vbase, n_feat, snap, snap_pos, row_floats,
-               reinterpret_cast<float*>(weights), moments, sgd);
+    if (bf16)
+      pdl_launch(k_pair_recv<__nv_bfloat16, V>, dim3(grid), dim3(256), 0, st, stage, me, theirs, counts, feats,
+                 vbase_sorted, feat_of_vbase, n_feat, row_floats, reinterpret_cast<__nv_bfloat16*>(weights), moments,
+                 sgd);
+    else
+      pdl_launch(k_pair_recv<float, V>, dim3(grid), dim3(256), 0, st, stage, me, theirs, counts, feats, vbase_sorted,
+                 feat_of_vbase, n_feat, row_floats, reinterpret_cast<float*>(weights), moments, sgd);
   }
 }
 
-void launch_sg_mean(const float* stage, uint32_t M, uint32_t me, const uint32_t* lists, const uint32_t* counts,
-                    uint64_t cmax, const uint32_t* ulist, const uint32_t* ucount, uint32_t ucount_ub,
-                    const FeatDev* feats, const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
-                    const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16,
-                    float* moments, int sgd, cudaStream_t st) {
-  if (!ucount_ub) return;
-  if (M > 32) throw Error(S2D_EINVAL, "snapshot sync supports up to 32 replicas");
-  const unsigned grid = (unsigned)std::max<uint64_t>(
-      1, std::min<uint64_t>((ucount_ub + 32 * kMeanWarps - 1) / (32 * kMeanWarps), 148ull * 8));
-  const size_t smem = (size_t)kMeanWarps * 64 * M * 4;
+static void pair_dispatch(bool push, unsigned grid, float* peer_stage, const float* stage, uint32_t me,
+                          const uint32_t* mine, const uint32_t* counts, const uint32_t* theirs, const FeatDev* feats,
+                          const uint32_t* vbase_sorted, const uint32_t* feat_of_vbase, uint32_t n_feat,
+                          const float* snap, const uint32_t* snap_pos, uint32_t row_floats, void* weights, int bf16,
+                          float* moments, int sgd, uint32_t* n_both, cudaStream_t st) {
   const uint32_t d4 = (row_floats - 4) / 4;
   if (d4 <= 32)
-    sg_mean_v<1>(grid, smem, stage, M, me, lists, counts, cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
-                 n_feat, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+    pair_v<1>(push, grid, peer_stage, stage, me, mine, counts, theirs, feats, vbase_sorted, feat_of_vbase, n_feat, snap,
+              snap_pos, row_floats, weights, bf16, moments, sgd, n_both, st);
   else if (d4 <= 64)
-    sg_mean_v<2>(grid, smem, stage, M, me, lists, counts, cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
-                 n_feat, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+    pair_v<2>(push, grid, peer_stage, stage, me, mine, counts, theirs, feats, vbase_sorted, feat_of_vbase, n_feat, snap,
+              snap_pos, row_floats, weights, bf16, moments, sgd, n_both, st);
   else
-    sg_mean_v<4>(grid, smem, stage, M, me, lists, counts, cmax, ulist, ucount, feats, vbase_sorted, feat_of_vbase,
-                 n_feat, snap, snap_pos, row_floats, weights, bf16, moments, sgd, st);
+    pair_v<4>(push, grid, peer_stage, stage, me, mine, counts, theirs, feats, vbase_sorted, feat_of_vbase, n_feat, snap,
+              snap_pos, row_floats, weights, bf16, moments, sgd, n_both, st);
+}
+
+void launch_pair_push(float* peer_stage, uint32_t me, const uint32_t* mine, const uint32_t* counts,
+                      const uint32_t* theirs, uint32_t mine_n, const FeatDev* feats, const uint32_t* vbase_sorted,
+                      const uint32_t* feat_of_vbase, uint32_t n_feat, const float* snap, const uint32_t* snap_pos,
+                      uint32_t row_floats, void* weights, int bf16, float* moments, int sgd, uint32_t* n_both,
+                      cudaStream_t st) {
+  if (!mine_n) return;
+  const unsigned grid =
+      (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((mine_n + 32 * kPairWarps - 1) / (32 * kPairWarps), 148ull * 8));
+  pair_dispatch(true, grid, peer_stage, nullptr, me, mine, counts, theirs, feats, vbase_sorted, feat_of_vbase, n_feat,
+                snap, snap_pos, row_floats, weights, bf16, moments, sgd, n_both, st);
+}
+
+void launch_pair_recv(const float* stage, uint32_t me, const uint32_t* theirs, const uint32_t* counts,
+                      uint32_t theirs_n, const FeatDev* feats, const uint32_t* vbase_sorted,
+                      const uint32_t* feat_of_vbase, uint32_t n_feat, uint32_t row_floats, void* weights, int bf16,
+                      float* moments, int sgd, cudaStream_t st) {
+  if (!theirs_n) return;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((theirs_n + 31) / 32, 148ull * 8));
+  pair_dispatch(false, grid, nullptr, stage, me, nullptr, counts, theirs, feats, vbase_sorted, feat_of_vbase, n_feat,
+                nullptr, nullptr, row_floats, weights, bf16, moments, sgd, nullptr, st);
 }
 
 }  // namespace s2d

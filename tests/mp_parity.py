@@ -261,9 +261,11 @@ def rank_main(args, rank, world, local, dist, hub):
                 if not (np.array_equal(w.view(np.uint32), ww.view(np.uint32))
                         and np.array_equal(v.view(np.uint32), vv.view(np.uint32))):
                     fails.append(f"checkpoint reload rank {r} table {f}")
-    # which replica-sync path ran: the snapshot dirty-row exchange (1) unless
-    # the environment forces the slice push / mean / scatter (2) or NCCL (3)
-    want_mode = 3 if os.environ.get("S2D_SYNC_NCCL") == "1" else 2 if os.environ.get("S2D_SYNC_SNAPSHOT") == "0" else 1
+    # which replica-sync path ran: the pair snapshot exchange (1) at M = 2,
+    # the slice push / mean / scatter (2) otherwise or when the environment
+    # forces it, NCCL (3) when forced
+    want_mode = (3 if os.environ.get("S2D_SYNC_NCCL") == "1"
+                 else 2 if os.environ.get("S2D_SYNC_SNAPSHOT") == "0" or M != 2 else 1)
     for r in range(world):
         if any(md not in (0, want_mode) for md in gathered[r][5]) or (M > 1 and want_mode not in gathered[r][5]):
             fails.append(f"rank {r} sync modes {gathered[r][5]} (want {want_mode})")

@@ -44,6 +44,7 @@ CASES = [
     (2, 1, "table-wise", ["--bad-id"]),
     (4, 2, "table-wise", ["--sync-interval", "2", "--steps", "4", "ENV:S2D_SYNC_NCCL=1"]),
     (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4", "ENV:S2D_SYNC_SNAPSHOT=0"]),
+    (2, 2, "table-wise", ["--sgd", "--steps", "3"]),
     (3, 3, "row-wise", ["--steps", "3"]),
     (4, 1, "row-wise", ["--bad-id"]),
 ]

@@ -15,5 +15,5 @@ run 2x2_snap "S2D_SYNC_SNAPSHOT=1" 2x2
 
 run 2x2_slice "S2D_SYNC_SNAPSHOT=0" 2x2
 
-run 1x4_snap "S2D_SYNC_SNAPSHOT=1" 1x4
+
 run 1x4_slice "S2D_SYNC_SNAPSHOT=0" 1x4
