@@ -314,41 +314,26 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pair_push(
     const uint32_t* feat_of_vbase, uint32_t n_feat, const float* __restrict__ snap, const uint32_t* __restrict__ snap_pos,
     uint32_t row_floats, WT* __restrict__ w, float* __restrict__ moments, int sgd, uint32_t* __restrict__ n_both) {
   pdl_wait();
-  __shared__ uint32_t s_their[kPairWarps][32];
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
   const uint32_t count = counts[me], their_n = counts[me ^ 1u];
   const uint64_t nwarps = (uint64_t)gridDim.x * kPairWarps;
   const uint64_t chunks = (count + 31) / 32, per_warp = (chunks + nwarps - 1) / nwarps;
   const uint64_t gw = (uint64_t)blockIdx.x * kPairWarps + wib;
   const uint64_t r0 = gw * per_warp * 32, r1 = min((uint64_t)count, r0 + per_warp * 32);
-  uint32_t q = 0;  // position in the peer's list (lane 0's search, then advanced per chunk)
-  if (r0 < r1) {
-    const uint32_t first = mine[r0];
-    uint32_t lo = 0, hi = their_n;
-    while (lo < hi) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (theirs[mid] < first) lo = mid + 1;
-      else hi = mid;
-    }
-    q = lo;
-  }
   uint32_t both_n = 0;
   for (uint64_t c0 = r0; c0 < r1; c0 += 32) {
     const uint32_t rows = r1 - c0 < 32 ? (uint32_t)(r1 - c0) : 32u;
     const uint32_t my_slot = lane < rows ? mine[c0 + lane] : 0xffffffffu;
-    s_their[wib][lane] = q + lane < their_n ? theirs[q + lane] : 0xffffffffu;
-    __syncwarp();
-    uint32_t lo = 0, hi = 32;
+    // is the row in the peer's list too?  (per lane binary search; the
+    // lists are a few MB, L2-resident)
+    uint32_t lo = 0, hi = their_n;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
-      if (s_their[wib][mid] < my_slot) lo = mid + 1;
+      if (theirs[mid] < my_slot) lo = mid + 1;
       else hi = mid;
     }
-    const bool both = lane < rows && lo < 32 && s_their[wib][lo] == my_slot;
-    const uint32_t bm = __ballot_sync(0xffffffffu, both);
-    q += __popc(bm);
-    both_n += __popc(bm);
-    __syncwarp();
+    const bool both = lane < rows && lo < their_n && theirs[lo] == my_slot;
+    both_n += __popc(__ballot_sync(0xffffffffu, both));
     // per lane (row): weight row, dim, snapshot (a row only this replica dirtied)
     uint32_t my_dim = 0, my_snap = 0xffffffffu;
     uint64_t my_wofs = 0;
