@@ -130,13 +130,8 @@ void scan_count_pair(const uint32_t* in, uint32_t* out32, uint64_t* out64, uint6
 // `bits` bits of key.  keys/vals ping-pong between a and b; returns true if
 // the result ended in b.
 size_t radix_tmp_bytes(uint64_t n, int bits);
-// digit width and pass count of the sort for `bits`-bit keys; the digit
-// histograms live at the start of the sort workspace (hist_bytes bytes)
-void radix_hist_config(int bits, int* dbits, int* npass, size_t* hist_bytes);
-// hist_ready: the digit histograms were accumulated by the key producer
-// (LookupArgs::hist) and are not recomputed
 bool radix_sort_pairs(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b,
-                      uint64_t n, int bits, void* tmp, size_t tmp_bytes, cudaStream_t st, bool hist_ready = false);
+                      uint64_t n, int bits, void* tmp, size_t tmp_bytes, cudaStream_t st);
 
 // embedding kernels (k_embed.cu)
 void launch_init_rows(void* w, int bf16, const FeatDev* feats_host, uint32_t F, uint64_t seed,
@@ -173,11 +168,6 @@ struct LookupArgs {
   // rows straight into requester n's pooled buffer peer_pooled.p[n]
   PeerPtrs peer_pooled;
   uint32_t use_peer_pooled;    // bit n: requester n takes single-owner pooled rows from the owners
-  // K3a's digit histograms built while the keys are emitted (null: the sort
-  // runs its own histogram pass): hist[p][d] over hist_np passes of hist_db
-  // bits of hist_bits-bit keys (radix_hist_config), zeroed before the launch
-  uint32_t* hist;
-  int hist_db, hist_np, hist_bits;
 };
 
 struct CombineArgs {

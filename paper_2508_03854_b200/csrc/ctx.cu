@@ -596,7 +596,6 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
       S2D_CUDA(cudaEventRecord(ev_sorted, sort_stream));
       sort_pending = true;
     }
-    if (a.emit_keys) prep_lookup_hist(a, nnz);
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     stats.nnz_owned = nnz;
     stats.entries_owned = BF;
@@ -673,7 +672,6 @@ void Ctx::lookup_forward(uint32_t batch, const uint32_t* lengths, const uint32_t
     a.unit_rot = ((uint64_t)((local + 1) % N) * BF) / 32;  // start at the next requester
     join_sync();  // the bucketing and id exchange above overlapped the last replica sync's tail
     phase_begin(kPhLookup);
-    prep_lookup_hist(a, nnz_own);
     launch_lookup_stream(a, bf16, (int)max_dim, stream);
     // the gradient rows' (slot, offset) pairs are final: sort them now
     S2D_CUDA(cudaEventRecord(ev_keys, stream));
@@ -929,33 +927,15 @@ void Ctx::read_counts() {
 // pairs; the sorted pairs land in (keys_c, vals_c).  (A dense-rank variant
 // -- touched-slot bitmap, 2 passes of 10 bits -- measured no faster; see
 // DESIGN.md section 5.)
-// The lookup that emits the sort pairs also accumulates the sort's digit
-// histograms (one pass over the keys less); zeroed here on the main stream.
-void Ctx::prep_lookup_hist(LookupArgs& a, uint64_t n) {
-  const int bits = std::max(1, bit_width(n_slots));
-  int db = 0, np = 0;
-  size_t hb = 0;
-  radix_hist_config(bits, &db, &np, &hb);
-  sort_tmp.ensure(radix_tmp_bytes(std::max<uint64_t>(n, 1), bits));
-  launch_zero(sort_tmp.p, hb, stream);
-  a.hist = sort_tmp.as<uint32_t>();
-  a.hist_db = db;
-  a.hist_np = np;
-  a.hist_bits = bits;
-  hist_ready = true;
-}
-
 void Ctx::launch_sort(cudaStream_t st) {
   const uint64_t n = nnz_own;
-  const bool ready = hist_ready;
-  hist_ready = false;
   if (n == 0) return;
   keys_b.ensure(n * 4);
   vals_b.ensure(n * 4);
   const int bits = std::max(1, bit_width(n_slots));
   sort_tmp.ensure(radix_tmp_bytes(n, bits));
   const bool in_b = radix_sort_pairs(keys_a.as<uint32_t>(), vals_a.as<uint32_t>(), keys_b.as<uint32_t>(),
-                                     vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, st, ready);
+                                     vals_b.as<uint32_t>(), n, bits, sort_tmp.p, sort_tmp.cap, st);
   sorted_k = in_b ? keys_b.as<uint32_t>() : keys_a.as<uint32_t>();
   sorted_v = in_b ? vals_b.as<uint32_t>() : vals_a.as<uint32_t>();
 }

@@ -92,8 +92,6 @@ struct Ctx {
   uint64_t snap_reserve(uint64_t items);
   void join_sync();
   void launch_sort(cudaStream_t st);
-  void prep_lookup_hist(LookupArgs& a, uint64_t n);
-  bool hist_ready = false;  // the last lookup built the sort's digit histograms
   const uint32_t* sorted_k = nullptr;  // sorted pairs of the last launch_sort
   const uint32_t* sorted_v = nullptr;
   Comm world, mp, dp;

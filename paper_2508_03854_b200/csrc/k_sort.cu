@@ -241,14 +241,13 @@ __global__ void __launch_bounds__(kThreads) k_radix_pass(const uint32_t* __restr
 
 template <int RADIX>
 bool sort_impl(const Layout& L, uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b, uint64_t n,
-               int bits, char* base, cudaStream_t st, bool hist_ready) {
+               int bits, char* base, cudaStream_t st) {
   uint32_t* hist = reinterpret_cast<uint32_t*>(base + L.hist_off);
   uint64_t* lb = reinterpret_cast<uint64_t*>(base + L.lb_off);
   uint32_t* ctr = reinterpret_cast<uint32_t*>(base + L.ctr_off);
   const unsigned hblocks = (unsigned)std::min<uint64_t>(L.ntiles * 2, 148 * 8);
-  if (!hist_ready)
-    pdl_launch(k_radix_hist<RADIX>, dim3(hblocks ? hblocks : 1), dim3(kThreads), 0, st,
-               static_cast<const uint32_t*>(keys_a), n, bits, hist);
+  pdl_launch(k_radix_hist<RADIX>, dim3(hblocks ? hblocks : 1), dim3(kThreads), 0, st,
+             static_cast<const uint32_t*>(keys_a), n, bits, hist);
   uint32_t *ki = keys_a, *vi = vals_a, *ko = keys_b, *vo = vals_b;
   for (int p = 0; p < L.npass; ++p) {
     const int shift = p * L.dbits;
@@ -266,29 +265,17 @@ bool sort_impl(const Layout& L, uint32_t* keys_a, uint32_t* vals_a, uint32_t* ke
 
 size_t radix_tmp_bytes(uint64_t n, int bits) { return layout(n, bits).total; }
 
-void radix_hist_config(int bits, int* dbits, int* npass, size_t* hist_bytes) {
-  if (bits < 1) bits = 1;
-  if (bits > 32) bits = 32;
-  const Layout L = layout(1, bits);
-  *dbits = L.dbits;
-  *npass = L.npass;
-  *hist_bytes = L.lb_off;
-}
-
 bool radix_sort_pairs(uint32_t* keys_a, uint32_t* vals_a, uint32_t* keys_b, uint32_t* vals_b,
-                      uint64_t n, int bits, void* tmp, size_t tmp_bytes, cudaStream_t st, bool hist_ready) {
+                      uint64_t n, int bits, void* tmp, size_t tmp_bytes, cudaStream_t st) {
   if (n == 0) return false;
   if (bits < 1) bits = 1;
   if (bits > 32) bits = 32;
   const Layout L = layout(n, bits);
   if (L.total > tmp_bytes) throw Error(S2D_ECUDA, "radix sort workspace too small");
   char* base = reinterpret_cast<char*>(tmp);
-  if (hist_ready)
-    launch_zero(base + L.lb_off, L.total - L.lb_off, st);
-  else
-    launch_zero(base, L.total, st);
-  if (L.radix == 512) return sort_impl<512>(L, keys_a, vals_a, keys_b, vals_b, n, bits, base, st, hist_ready);
-  return sort_impl<256>(L, keys_a, vals_a, keys_b, vals_b, n, bits, base, st, hist_ready);
+  launch_zero(base, L.total, st);
+  if (L.radix == 512) return sort_impl<512>(L, keys_a, vals_a, keys_b, vals_b, n, bits, base, st);
+  return sort_impl<256>(L, keys_a, vals_a, keys_b, vals_b, n, bits, base, st);
 }
 
 }  // namespace s2d

@@ -149,12 +149,6 @@ template <typename WT, int VPL, bool UNI>
 __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
   pdl_wait();  // persistent single wave: let the next grid queue behind us
   pdl_trigger();
-  // K3a's digit histograms of the emitted keys (LookupArgs::hist)
-  __shared__ uint32_t s_hist[4 * 512];
-  if (a.hist) {
-    for (int i = threadIdx.x; i < 4 * 512; i += blockDim.x) s_hist[i] = 0;
-    __syncthreads();
-  }
   constexpr int VB = Row<WT>::kVecBytes;
   constexpr int kWinStages = 32 / kRowsPerStage;
   constexpr uint32_t kRowBytes = VPL * 32 * VB;  // ring slot stride
@@ -244,16 +238,6 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
       if (a.emit_keys && have) {
         a.keys[p] = ok ? vb_j + (id - lo_j) : 0xffffffffu;
         a.vals[p] = (uint32_t)(oo_j >> 2);
-      }
-      if (a.hist) {  // one shared atomic per distinct digit of the window
-        const uint32_t key = ok ? vb_j + (id - lo_j) : 0xffffffffu;
-        for (int q = 0; q < a.hist_np; ++q) {
-          const int sh = q * a.hist_db;
-          const int pb = min(a.hist_db, a.hist_bits - sh);
-          const uint32_t dg = have ? (key >> sh) & ((1u << pb) - 1u) : 0xffffffffu;
-          const uint32_t m = __match_any_sync(0xffffffffu, dg);
-          if (have && lane == (uint32_t)(__ffs(m) - 1)) atomicAdd(&s_hist[(q << a.hist_db) + dg], __popc(m));
-        }
       }
       if constexpr (UNI)
         ad = ok ? vb_j + (id - lo_j) : a.zero_row;
@@ -372,11 +356,6 @@ __global__ void __launch_bounds__(256) k_lookup_ring(const LookupArgs a) {
     }
     cp_wait<0>();
     flush();
-  }
-  if (a.hist) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < (a.hist_np << a.hist_db); i += blockDim.x)
-      if (s_hist[i]) atomicAdd(a.hist + i, s_hist[i]);
   }
 }
 
