@@ -351,9 +351,15 @@ int s2d_gen_upstream(s2d_ctx* ctx, uint64_t seed, uint64_t step, uint32_t rank, 
  * rank: the reference DataGenerator's ids (fixed pooling, trainer.hpp
  * ids_per_sample), the lookup, the upstream gradient, the backward + fused
  * update, and the replica sync every sync_interval steps
- * ((step+1) % sync_interval == 0, trainer.cpp:661).  The dense MLP is not
- * part of this build: the upstream gradient comes from the caller's callback
- * (the dense model's backward) or, without one, from s2d_gen_upstream. */
+ * ((step+1) % sync_interval == 0, trainer.cpp:661).  The upstream gradient
+ * comes from the caller's callback when one is set, else (dense_model = 1,
+ * the reference's Trainer) from the toy DLRM MLPs on the device: the
+ * DataGenerator's dense features and labels (data.cpp:37-68, 137-145),
+ * dense_arch + over_arch forward, sigmoid / log-loss, backward
+ * (trainer.cpp:366-438), and after every step the dense DP step -- the
+ * gradient left fold over (rank, sample) and one SGD step with eta / (T*B)
+ * adopted by every rank (trainer.cpp:507-545) -- else (dense_model = 0) from
+ * s2d_gen_upstream. */
 typedef struct {
   uint32_t total_ranks, groups;                 /* Topology */
   uint32_t num_tables, rows_per_table, dim;     /* DlrmConfig (embedding part) */
@@ -368,6 +374,10 @@ typedef struct {
   int32_t weight_dtype;                         /* S2D_F32 | S2D_BF16 */
   uint32_t n_devices;
   const int32_t* devices;
+  int32_t dense_model;                          /* 1: device MLPs (reference Trainer); 0: synthetic upstream */
+  uint32_t dense_dim;                           /* DataParams::dense_dim (data.hpp:51-56), default 8 */
+  uint32_t dense_hidden, over_hidden;           /* DlrmConfig (model.hpp:68-77), defaults 32, 64 */
+  double gt_id_scale, gt_dense_scale, gt_bias;  /* DataParams ground truth, defaults 0.25, 0.35, -0.8 */
 } s2d_trainer_options;
 
 /* Called on rank `rank`'s thread after the step's forward: fill upstream
@@ -396,6 +406,13 @@ int s2d_trainer_save_tables(s2d_trainer* t, const char* path);
 int s2d_trainer_load_tables(s2d_trainer* t, const char* path);
 /* MetricsRow moment columns of group 0's replica. */
 int s2d_trainer_metrics(s2d_trainer* t, s2d_metrics_row* out);
+/* Trainer::rank_model(rank) (trainer.hpp:125): arch 0 = dense_arch, 1 =
+ * over_arch; w1 [hidden][in], b1 [hidden], w2 [out][hidden], b2 [out] fp32
+ * (any may be NULL).  S2D_EINVAL without the dense model. */
+int s2d_trainer_rank_model(s2d_trainer* t, uint32_t rank, int32_t arch, float* w1, float* b1, float* w2, float* b2);
+/* MetricsRow::loss of the last step (trainer.cpp:538): the global-batch mean
+ * training loss; S2D_EINVAL without the dense model or before a step. */
+int s2d_trainer_last_loss(s2d_trainer* t, double* out);
 /* The context of one virtual rank (owned by the trainer). */
 int s2d_trainer_rank_ctx(s2d_trainer* t, uint32_t rank, s2d_ctx** out);
 

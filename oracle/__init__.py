@@ -480,6 +480,36 @@ def reference_trainer(o: RefTrainerOpts):
     return ws, vs, plan[: 4 * n.value].reshape(-1, 4)
 
 
+def reference_trainer_model(o: RefTrainerOpts):
+    """The REAL reference Trainer with its dense model's outputs:
+    (ws[g], vs[g], rank_model(0) as {"dense_arch": (w1, b1, w2, b2),
+    "over_arch": (...)}, per-step MetricsRow::loss [steps])."""
+    lib = C.CDLL(REF_SO)
+    fn = lib.ref_trainer_run_model
+    fn.argtypes = [C.POINTER(RefTrainerOpts), C.c_void_p, C.c_void_p, _f32p,
+                   np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")]
+    fn.restype = C.c_int
+    F, D = o.F, o.dim
+    shapes = [("dense_arch", o.dense_dim, o.dense_hidden, D), ("over_arch", F * D + D, o.over_hidden, 1)]
+    total = sum(h * i + h + n * h + n for _, i, h, n in shapes)
+    flat = np.zeros(total, np.float32)
+    loss = np.zeros(o.steps, np.float64)
+    ws = [np.zeros(o.F * o.rows * o.dim, np.float32) for _ in range(o.M)]
+    vs = [np.zeros(o.F * o.rows, np.float32) for _ in range(o.M)]
+    if fn(C.byref(o), _ptr_array(ws), _ptr_array(vs), flat, loss):
+        lib.ref_last_error.restype = C.c_char_p
+        raise RuntimeError(lib.ref_last_error().decode())
+    model, at = {}, 0
+    for name, i, h, n in shapes:
+        parts = []
+        for shape in [(h, i), (h,), (n, h), (n,)]:
+            k = int(np.prod(shape))
+            parts.append(flat[at:at + k].reshape(shape))
+            at += k
+        model[name] = tuple(parts)
+    return ws, vs, model, loss
+
+
 def restated_trainer(o: RefTrainerOpts):
     """The same loop composed from the reference's public API
     (ref_harness.cpp ref_restated_run), recording every step's per-rank

@@ -538,6 +538,41 @@ int ref_trainer_run(const RefTrainerOpts* o, float* const* w_out, float* const* 
   }
 }
 
+// Trainer(opts with eval_cadence 1).step_n(steps) with the dense model's
+// outputs as well: replicas as ref_trainer_run, rank_model(0)'s parameters
+// concatenated into mlp_out (dense_arch w1 b1 w2 b2, over_arch w1 b1 w2 b2)
+// and every step's MetricsRow::loss into loss_out[steps].
+int ref_trainer_run_model(const RefTrainerOpts* o, float* const* w_out, float* const* v_out, float* mlp_out,
+                          double* loss_out) {
+  try {
+    TrainerOptions t = make_options(*o);
+    t.eval_cadence = 1;
+    Trainer tr(t);
+    tr.step_n(o->steps);
+    for (uint32_t g = 0; g < o->M; ++g) {
+      const auto tabs = tr.replica_tables(g);
+      for (uint32_t f = 0; f < o->F; ++f) {
+        std::memcpy(w_out[g] + (size_t)f * o->rows * o->dim, tabs[f]->weights.data(),
+                    sizeof(float) * (size_t)o->rows * o->dim);
+        std::memcpy(v_out[g] + (size_t)f * o->rows, tabs[f]->moments.data(), sizeof(float) * o->rows);
+      }
+    }
+    const RankModel& m = tr.rank_model(0);
+    float* p = mlp_out;
+    for (const Mlp* a : {&m.dense_arch, &m.over_arch})
+      for (const std::vector<float>* v : {&a->w1, &a->b1, &a->w2, &a->b2}) {
+        std::memcpy(p, v->data(), v->size() * sizeof(float));
+        p += v->size();
+      }
+    const TrainResult res = tr.finalize();
+    for (size_t i = 0; i < res.metrics.size() && i < o->steps; ++i) loss_out[i] = res.metrics[i].loss;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // The same training loop composed from the public API (run_step,
 // trainer.cpp:615-663): DataGenerator batches, the embedding phases through
 // ref_group_step (forward, then backward with the MLP's f32 wire gradient),

@@ -57,7 +57,9 @@ class TrainerOptionsC(C.Structure):
                 ("zipf_exponent", C.c_double), ("ids_per_sample", C.c_uint32), ("per_rank_batch", C.c_uint32),
                 ("steps", C.c_uint64), ("sync_interval", C.c_uint32), ("data_seed", C.c_uint64),
                 ("init_seed", C.c_uint64), ("opt", OptimizerConfigC), ("weight_dtype", C.c_int32),
-                ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int32))]
+                ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int32)), ("dense_model", C.c_int32),
+                ("dense_dim", C.c_uint32), ("dense_hidden", C.c_uint32), ("over_hidden", C.c_uint32),
+                ("gt_id_scale", C.c_double), ("gt_dense_scale", C.c_double), ("gt_bias", C.c_double)]
 
 
 UPSTREAM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
@@ -130,6 +132,8 @@ SIGNATURES = {
     "s2d_trainer_load_tables": (C.c_int, [_P, C.c_char_p]),
     "s2d_trainer_metrics": (C.c_int, [_P, C.POINTER(MetricsRowC)]),
     "s2d_trainer_rank_ctx": (C.c_int, [_P, C.c_uint32, C.POINTER(_P)]),
+    "s2d_trainer_rank_model": (C.c_int, [_P, C.c_uint32, C.c_int32, _P, _P, _P, _P]),
+    "s2d_trainer_last_loss": (C.c_int, [_P, C.POINTER(C.c_double)]),
     "s2d_memory_overhead": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
     "s2d_sync_latency": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.c_double, C.POINTER(C.c_double)]),
     "s2d_qps_scaling_factor": (C.c_int, [C.c_double] * 4 + [C.POINTER(C.c_double)]),

@@ -665,9 +665,12 @@ class Sparse2DEmbedding:
 
 @dataclass
 class TrainerOptions:
-    """TrainerOptions (trainer.hpp:47-70), embedding part: topology, tables
-    (num_tables x rows_per_table x dim), the DataGenerator's Zipf exponent and
-    pooling fan-in, per-rank batch, steps, sync cadence, seeds, optimizer."""
+    """TrainerOptions (trainer.hpp:47-70): topology, tables (num_tables x
+    rows_per_table x dim), the DataGenerator's Zipf exponent and pooling
+    fan-in, per-rank batch, steps, sync cadence, seeds, optimizer, and the
+    dense model (DlrmConfig dense_hidden / over_hidden, DataParams dense_dim
+    and ground truth; model.hpp:68-77, data.hpp:51-56).  dense_model=False
+    trains on the synthetic upstream instead of the device MLPs."""
 
     total_ranks: int = 1
     groups: int = 1
@@ -685,6 +688,13 @@ class TrainerOptions:
     optimizer: OptimizerConfig | None = None
     weight_dtype: str = "fp32"
     devices: Sequence[int] | None = None
+    dense_model: bool = True
+    dense_dim: int = 8
+    dense_hidden: int = 32
+    over_hidden: int = 64
+    gt_id_scale: float = 0.25
+    gt_dense_scale: float = 0.35
+    gt_bias: float = -0.8
 
 
 class _DevArray:
@@ -701,7 +711,9 @@ class Trainer:
     process (s2d_trainer_*).  The upstream gradient of each step comes from
     ``set_upstream(fn)`` -- fn(rank, step, lengths, pooled, upstream) with
     torch CUDA tensor views, fn filling ``upstream`` (the dense model's
-    backward) -- or, by default, the synthetic f32(1e-3 N(0,1)) gradient."""
+    backward) -- or, by default, from the dense model on the device (the
+    reference's toy DLRM MLPs, dense.h), or with ``dense_model=False`` the
+    synthetic f32(1e-3 N(0,1)) gradient."""
 
     def __init__(self, opts: TrainerOptions):
         self.lib = _lib()
@@ -716,7 +728,9 @@ class Trainer:
                               opts.zipf_exponent, opts.ids_per_sample, opts.per_rank_batch, opts.steps,
                               opts.sync_interval, opts.data_seed, opts.init_seed, opt,
                               L.S2D_BF16 if opts.weight_dtype == "bf16" else L.S2D_F32, len(devs),
-                              C.cast(self._devs, C.POINTER(C.c_int32)) if devs else None)
+                              C.cast(self._devs, C.POINTER(C.c_int32)) if devs else None,
+                              1 if opts.dense_model else 0, opts.dense_dim, opts.dense_hidden, opts.over_hidden,
+                              opts.gt_id_scale, opts.gt_dense_scale, opts.gt_bias)
         self._t = C.c_void_p()
         L.check(self.lib.s2d_trainer_create(C.byref(c), C.byref(self._t)))
         self._cb = None
@@ -785,6 +799,30 @@ class Trainer:
         L.check(self.lib.s2d_trainer_plan(self._t, out, n.value, C.byref(n)))
         return [dict(table_id=out[i].table_id, row_lo=out[i].row_lo, row_hi=out[i].row_hi,
                      local_rank=out[i].local_rank) for i in range(n.value)]
+
+    def rank_model(self, rank: int) -> dict:
+        """Trainer::rank_model(rank) (trainer.hpp:125): {"dense_arch": (w1, b1,
+        w2, b2), "over_arch": (...)} fp32, w1 [hidden, in], w2 [out, hidden]."""
+        o = self.opts
+        F, D = o.num_tables, o.dim
+        out = {}
+        for arch, (name, i, h, n) in enumerate([("dense_arch", o.dense_dim, o.dense_hidden, D),
+                                                  ("over_arch", F * D + D, o.over_hidden, 1)]):
+            w1 = np.zeros((h, i), np.float32)
+            b1 = np.zeros(h, np.float32)
+            w2 = np.zeros((n, h), np.float32)
+            b2 = np.zeros(n, np.float32)
+            L.check(self.lib.s2d_trainer_rank_model(self._t, rank, arch, w1.ctypes.data, b1.ctypes.data,
+                                                    w2.ctypes.data, b2.ctypes.data))
+            out[name] = (w1, b1, w2, b2)
+        return out
+
+    @property
+    def last_loss(self) -> float:
+        """MetricsRow::loss of the last step: the global-batch mean log-loss."""
+        x = C.c_double(0)
+        L.check(self.lib.s2d_trainer_last_loss(self._t, C.byref(x)))
+        return x.value
 
     def replica_tables(self, group: int) -> list[tuple]:
         """[(weights [rows, dim] fp32, moments [rows] fp32)] per table of DP

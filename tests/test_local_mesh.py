@@ -260,7 +260,7 @@ def test_trainer_facade_default_upstream_checkpoint_metrics(tmp_path, port):
 
     opts = s2d.TrainerOptions(total_ranks=4, groups=2, num_tables=3, rows_per_table=200, dim=16, ids_per_sample=4,
                               per_rank_batch=32, steps=3, optimizer=s2d.OptimizerConfig(eta=0.1, c=2.0),
-                              devices=[0])
+                              devices=[0], dense_model=False)
     tr = s2d.Trainer(opts)
     try:
         tr.run()
@@ -286,3 +286,52 @@ def test_trainer_facade_default_upstream_checkpoint_metrics(tmp_path, port):
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     finally:
         eng.close()
+
+
+DENSE_MESHES = [dict(T=1, M=1, steps=5), dict(T=4, M=2), dict(T=4, M=1, strategy="table-wise", B=16),
+                dict(T=4, M=2, sgd=True, sync_interval=2), dict(T=6, M=3, rows=50, dim=12, L=5, dense_hidden=9,
+                                                                over_hidden=33, dense_dim=7)]
+
+
+@pytest.mark.parametrize("mesh", DENSE_MESHES, ids=[str(m) for m in DENSE_MESHES])
+def test_trainer_dense_model_matches_real_reference_trainer(mesh):
+    """The Trainer facade with its own dense model (the toy DLRM MLPs on the
+    device, dense.h: DataGenerator dense features + labels, forward, loss,
+    backward, the dense DP step) against the REAL reference Trainer with
+    ITS MLPs (trainer.cpp + model.cpp in oracle/_ref, nothing replayed):
+    every rank's MLP parameters and every replica after the last step are
+    bitwise equal; every step's global-batch loss agrees to 1e-15."""
+    import paper_2508_03854_b200 as s2d
+    from oracle import reference_available, reference_trainer_model, trainer_options
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    o = trainer_options(**mesh)
+    ws_real, vs_real, model_real, loss_real = reference_trainer_model(o)
+    tr = s2d.Trainer(s2d.TrainerOptions(
+        total_ranks=o.T, groups=o.M, num_tables=o.F, rows_per_table=o.rows, dim=o.dim,
+        strategy="row-wise" if o.strategy else "table-wise", zipf_exponent=o.zipf, ids_per_sample=o.ids_per_sample,
+        per_rank_batch=o.B, steps=o.steps, sync_interval=o.sync_interval, data_seed=o.data_seed,
+        init_seed=o.init_seed, optimizer=s2d.OptimizerConfig(o.eta, o.eps, o.c, "sgd" if o.sgd else "rowwise-adagrad"),
+        devices=[0], dense_model=True, dense_dim=o.dense_dim, dense_hidden=o.dense_hidden,
+        over_hidden=o.over_hidden))
+    try:
+        losses = []
+        for _ in range(o.steps):
+            tr.step_n(1)
+            losses.append(tr.last_loss)
+        # the loss is -log(p) (trainer.cpp:412): CUDA's log may round 1 ulp
+        # away from the host libm's; it feeds nothing downstream
+        np.testing.assert_allclose(np.array(losses), loss_real, rtol=1e-15, atol=0)
+        for r in range(o.T):
+            got = tr.rank_model(r)
+            for name in ("dense_arch", "over_arch"):
+                for a, b in zip(got[name], model_real[name]):
+                    assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (r, name)
+        for g in range(o.M):
+            for f, (w, v) in enumerate(tr.replica_tables(g)):
+                wr = ws_real[g][f * o.rows * o.dim:(f + 1) * o.rows * o.dim].reshape(o.rows, o.dim)
+                assert np.array_equal(w.view(np.uint32), wr.view(np.uint32)), (g, f)
+                assert np.array_equal(v.view(np.uint32), vs_real[g][f * o.rows:(f + 1) * o.rows].view(np.uint32))
+    finally:
+        tr.close()
