@@ -378,7 +378,20 @@ typedef struct {
   uint32_t dense_dim;                           /* DataParams::dense_dim (data.hpp:51-56), default 8 */
   uint32_t dense_hidden, over_hidden;           /* DlrmConfig (model.hpp:68-77), defaults 32, 64 */
   double gt_id_scale, gt_dense_scale, gt_bias;  /* DataParams ground truth, defaults 0.25, 0.35, -0.8 */
+  uint64_t eval_cadence;                        /* 0 = evaluate only after the final step (trainer.hpp:62-64) */
+  uint32_t eval_samples;                        /* default 100000 */
+  uint64_t eval_seed;                           /* default 3 */
 } s2d_trainer_options;
+
+/* MetricsRow (trainer.hpp:72-79) and NEReport (trainer.hpp:29-36). */
+typedef struct {
+  uint64_t step;
+  double loss, ne, eff_lr_p50, eff_lr_p99, v_mean;
+} s2d_train_metrics_row;
+typedef struct {
+  double ne, baseline_ctr;
+  uint64_t eval_samples;
+} s2d_ne_report;
 
 /* Called on rank `rank`'s thread after the step's forward: fill upstream
  * ([batch][num_tables*dim] fp32, device, per-sample, not batch-divided:
@@ -413,6 +426,16 @@ int s2d_trainer_rank_model(s2d_trainer* t, uint32_t rank, int32_t arch, float* w
 /* MetricsRow::loss of the last step (trainer.cpp:538): the global-batch mean
  * training loss; S2D_EINVAL without the dense model or before a step. */
 int s2d_trainer_last_loss(s2d_trainer* t, double* out);
+/* TrainResult::metrics (trainer.hpp:87-98): with the dense model, one row
+ * after every eval_cadence-th step and after step opts.steps -- loss, NE of
+ * the eval set (DataGenerator lane kEval, eval_seed, chunks of 1024;
+ * trainer.cpp:687-712) pooled from group 0's replica with rank 0's MLPs
+ * (eval_probs, trainer.cpp:714-743), and the moment columns
+ * (trainer.cpp:745-771).  n = rows so far; out may be NULL. */
+int s2d_trainer_metrics_rows(s2d_trainer* t, s2d_train_metrics_row* out, uint32_t cap, uint32_t* n);
+/* Trainer::finalize's final_ne (trainer.cpp:788-793): evaluates now unless
+ * the last step already did.  S2D_EINVAL without the dense model. */
+int s2d_trainer_final_ne(s2d_trainer* t, s2d_ne_report* out);
 /* The context of one virtual rank (owned by the trainer). */
 int s2d_trainer_rank_ctx(s2d_trainer* t, uint32_t rank, s2d_ctx** out);
 

@@ -483,7 +483,8 @@ def reference_trainer(o: RefTrainerOpts):
 def reference_trainer_model(o: RefTrainerOpts):
     """The REAL reference Trainer with its dense model's outputs:
     (ws[g], vs[g], rank_model(0) as {"dense_arch": (w1, b1, w2, b2),
-    "over_arch": (...)}, per-step MetricsRow::loss [steps])."""
+    "over_arch": (...)}, per-step MetricsRow [steps, 6]: step, loss, ne,
+    eff_lr_p50, eff_lr_p99, v_mean)."""
     lib = C.CDLL(REF_SO)
     fn = lib.ref_trainer_run_model
     fn.argtypes = [C.POINTER(RefTrainerOpts), C.c_void_p, C.c_void_p, _f32p,
@@ -493,7 +494,7 @@ def reference_trainer_model(o: RefTrainerOpts):
     shapes = [("dense_arch", o.dense_dim, o.dense_hidden, D), ("over_arch", F * D + D, o.over_hidden, 1)]
     total = sum(h * i + h + n * h + n for _, i, h, n in shapes)
     flat = np.zeros(total, np.float32)
-    loss = np.zeros(o.steps, np.float64)
+    loss = np.zeros((o.steps, 6), np.float64)
     ws = [np.zeros(o.F * o.rows * o.dim, np.float32) for _ in range(o.M)]
     vs = [np.zeros(o.F * o.rows, np.float32) for _ in range(o.M)]
     if fn(C.byref(o), _ptr_array(ws), _ptr_array(vs), flat, loss):

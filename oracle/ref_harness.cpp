@@ -541,7 +541,8 @@ int ref_trainer_run(const RefTrainerOpts* o, float* const* w_out, float* const* 
 // Trainer(opts with eval_cadence 1).step_n(steps) with the dense model's
 // outputs as well: replicas as ref_trainer_run, rank_model(0)'s parameters
 // concatenated into mlp_out (dense_arch w1 b1 w2 b2, over_arch w1 b1 w2 b2)
-// and every step's MetricsRow::loss into loss_out[steps].
+// and every step's MetricsRow into rows_out[steps][6] (step, loss, ne,
+// eff_lr_p50, eff_lr_p99, v_mean).
 int ref_trainer_run_model(const RefTrainerOpts* o, float* const* w_out, float* const* v_out, float* mlp_out,
                           double* loss_out) {
   try {
@@ -565,7 +566,11 @@ int ref_trainer_run_model(const RefTrainerOpts* o, float* const* w_out, float* c
         p += v->size();
       }
     const TrainResult res = tr.finalize();
-    for (size_t i = 0; i < res.metrics.size() && i < o->steps; ++i) loss_out[i] = res.metrics[i].loss;
+    for (size_t i = 0; i < res.metrics.size() && i < o->steps; ++i) {
+      const MetricsRow& m = res.metrics[i];
+      const double row[6] = {(double)m.step, m.loss, m.ne, m.eff_lr_p50, m.eff_lr_p99, m.v_mean};
+      std::memcpy(loss_out + 6 * i, row, sizeof(row));
+    }
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

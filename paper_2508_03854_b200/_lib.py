@@ -59,7 +59,17 @@ class TrainerOptionsC(C.Structure):
                 ("init_seed", C.c_uint64), ("opt", OptimizerConfigC), ("weight_dtype", C.c_int32),
                 ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int32)), ("dense_model", C.c_int32),
                 ("dense_dim", C.c_uint32), ("dense_hidden", C.c_uint32), ("over_hidden", C.c_uint32),
-                ("gt_id_scale", C.c_double), ("gt_dense_scale", C.c_double), ("gt_bias", C.c_double)]
+                ("gt_id_scale", C.c_double), ("gt_dense_scale", C.c_double), ("gt_bias", C.c_double),
+                ("eval_cadence", C.c_uint64), ("eval_samples", C.c_uint32), ("eval_seed", C.c_uint64)]
+
+
+class TrainMetricsRowC(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("loss", C.c_double), ("ne", C.c_double), ("eff_lr_p50", C.c_double),
+                ("eff_lr_p99", C.c_double), ("v_mean", C.c_double)]
+
+
+class NEReportC(C.Structure):
+    _fields_ = [("ne", C.c_double), ("baseline_ctr", C.c_double), ("eval_samples", C.c_uint64)]
 
 
 UPSTREAM_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint32, C.c_uint64, C.c_uint32, C.c_void_p, C.c_void_p,
@@ -134,6 +144,8 @@ SIGNATURES = {
     "s2d_trainer_rank_ctx": (C.c_int, [_P, C.c_uint32, C.POINTER(_P)]),
     "s2d_trainer_rank_model": (C.c_int, [_P, C.c_uint32, C.c_int32, _P, _P, _P, _P]),
     "s2d_trainer_last_loss": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "s2d_trainer_metrics_rows": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
+    "s2d_trainer_final_ne": (C.c_int, [_P, C.POINTER(NEReportC)]),
     "s2d_memory_overhead": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),
     "s2d_sync_latency": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.c_double, C.POINTER(C.c_double)]),
     "s2d_qps_scaling_factor": (C.c_int, [C.c_double] * 4 + [C.POINTER(C.c_double)]),

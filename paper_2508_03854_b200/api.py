@@ -695,6 +695,9 @@ class TrainerOptions:
     gt_id_scale: float = 0.25
     gt_dense_scale: float = 0.35
     gt_bias: float = -0.8
+    eval_cadence: int = 0
+    eval_samples: int = 100000
+    eval_seed: int = 3
 
 
 class _DevArray:
@@ -730,7 +733,8 @@ class Trainer:
                               L.S2D_BF16 if opts.weight_dtype == "bf16" else L.S2D_F32, len(devs),
                               C.cast(self._devs, C.POINTER(C.c_int32)) if devs else None,
                               1 if opts.dense_model else 0, opts.dense_dim, opts.dense_hidden, opts.over_hidden,
-                              opts.gt_id_scale, opts.gt_dense_scale, opts.gt_bias)
+                              opts.gt_id_scale, opts.gt_dense_scale, opts.gt_bias, opts.eval_cadence,
+                              opts.eval_samples, opts.eval_seed)
         self._t = C.c_void_p()
         L.check(self.lib.s2d_trainer_create(C.byref(c), C.byref(self._t)))
         self._cb = None
@@ -823,6 +827,24 @@ class Trainer:
         x = C.c_double(0)
         L.check(self.lib.s2d_trainer_last_loss(self._t, C.byref(x)))
         return x.value
+
+    def metrics(self) -> list[dict]:
+        """TrainResult::metrics so far: one MetricsRow dict (step, loss, ne,
+        eff_lr_p50, eff_lr_p99, v_mean) per eval_cadence-th step and after
+        the last step (dense model only)."""
+        n = C.c_uint32(0)
+        L.check(self.lib.s2d_trainer_metrics_rows(self._t, None, 0, C.byref(n)))
+        out = (L.TrainMetricsRowC * max(1, n.value))()
+        L.check(self.lib.s2d_trainer_metrics_rows(self._t, C.cast(out, C.c_void_p), n.value, C.byref(n)))
+        return [{k: getattr(out[i], k) for k, _ in L.TrainMetricsRowC._fields_} for i in range(n.value)]
+
+    def finalize(self) -> dict:
+        """Trainer::finalize (trainer.hpp:118): {"final_ne": {ne, baseline_ctr,
+        eval_samples}, "metrics": [...]}; evaluates unless the last step did."""
+        rep = L.NEReportC()
+        L.check(self.lib.s2d_trainer_final_ne(self._t, C.byref(rep)))
+        return {"final_ne": {"ne": rep.ne, "baseline_ctr": rep.baseline_ctr, "eval_samples": rep.eval_samples},
+                "metrics": self.metrics()}
 
     def replica_tables(self, group: int) -> list[tuple]:
         """[(weights [rows, dim] fp32, moments [rows] fp32)] per table of DP

@@ -281,6 +281,7 @@ struct GenArgs {
   const double* cdf;
   uint32_t* lengths;                // [B*F]
   uint32_t* ids;                    // [B*per_sample]
+  uint64_t lane;                    // DataGenerator::Lane: 0 train, 1 eval
 };
 void launch_gen_batch(const GenArgs& a, cudaStream_t st);
 void launch_gen_upstream(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, const FeatDev* feats,

@@ -192,7 +192,7 @@ struct Ctx {
   std::vector<double> gen_zipf;
   std::vector<uint64_t> gen_cdf_off;
   void gen_batch(uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, const double* zipf,
-                 const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int mem);
+                 const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int mem, uint64_t lane = 0);
   void gen_upstream(uint64_t seed, uint64_t step, uint32_t rank, uint32_t batch, float* out, int mem);
   void debug_read(int which, void* out, uint64_t cap, uint64_t* n);
   void gather_rows(uint32_t table, uint32_t n, const uint32_t* rows, float* w, float* v);

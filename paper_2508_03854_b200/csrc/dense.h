@@ -66,11 +66,23 @@ void launch_mirror(const float* w, double* wd, uint64_t n, cudaStream_t st);
 // DataGenerator side (data.cpp): ground-truth id contributions and dense
 // weights, the per-sample dense features and labels.
 void launch_gt_normals(uint64_t key, uint64_t n, double scale, float* out, cudaStream_t st);
-void launch_gen_dense(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t dd, float* out,
+void launch_gen_dense(uint64_t seed, uint64_t lane, uint64_t step, uint32_t rank, uint32_t B, uint32_t dd, float* out,
                       cudaStream_t st);
-void launch_gen_labels(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, uint32_t L,
+void launch_gen_labels(uint64_t seed, uint64_t lane, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, uint32_t L,
                        const uint32_t* ids, const float* id_contrib, uint32_t rows, const float* dense,
                        const float* dense_w, uint32_t dd, double bias, float* labels, cudaStream_t st);
+// One shard of the consensus replica as pool_ids sees it (ShardRef,
+// embedding.hpp): rows [lo, hi) of a table, row r at w + (r - lo) * dim
+// (fp32, or bf16 storage widened exactly).
+struct EvalShard {
+  uint32_t lo, hi;
+  const void* w;
+};
+// pool_ids (embedding.cpp:39-92) of S samples x F fixed-length bags of L ids
+// over shards[f * N + o] (o ascending, empty shards skipped): per-shard f64
+// partial -> f32, f64 sum over shards -> f32, into out [S][F * D].
+void launch_eval_pool(uint32_t S, uint32_t F, uint32_t L, uint32_t N, const uint32_t* ids, const EvalShard* shards,
+                      uint32_t D, int bf16, float* out, cudaStream_t st);
 // make_key({fields...}) of rng.hpp on the host
 uint64_t rng_make_key(const uint64_t* fields, int n);
 

@@ -14,7 +14,7 @@
 namespace s2d {
 
 void Ctx::gen_batch(uint64_t seed, uint64_t step, uint32_t rnk, uint32_t batch, const double* zipf,
-                    const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int mem) {
+                    const uint32_t* ids_per_sample, uint32_t* lengths, uint32_t* ids, int mem, uint64_t lane) {
   if (!F) throw Error(S2D_EINVAL, "register tables first");
   if (!zipf || !ids_per_sample) throw Error(S2D_EINVAL, "zipf and ids_per_sample are required");
   if (mem != S2D_HOST && mem != S2D_DEVICE) throw Error(S2D_EINVAL, "mem must be S2D_HOST or S2D_DEVICE");
@@ -62,6 +62,7 @@ void Ctx::gen_batch(uint64_t seed, uint64_t step, uint32_t rnk, uint32_t batch, 
   GenArgs a{};
   a.seed = seed;
   a.step = step;
+  a.lane = lane;
   a.rank = rnk;
   a.B = batch;
   a.F = F;

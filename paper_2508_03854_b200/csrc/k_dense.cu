@@ -227,12 +227,12 @@ __global__ void k_gt_normals(uint64_t key, uint64_t n, double scale, float* __re
 
 // Sample::dense (data.cpp:137-141): f32 normals of CounterRng({seed, lane 0,
 // step, rank, s, kTagDense = 2}).
-__global__ void k_gen_dense(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t dd,
+__global__ void k_gen_dense(uint64_t seed, uint64_t lane, uint64_t step, uint32_t rank, uint32_t B, uint32_t dd,
                             float* __restrict__ out) {
   const uint64_t n = (uint64_t)B * dd;
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = (uint32_t)(i / dd), j = (uint32_t)(i % dd);
-    const uint64_t f[6] = {seed, 0ull, step, rank, s, 2ull};
+    const uint64_t f[6] = {seed, lane, step, rank, s, 2ull};
     out[i] = (float)normal_at(key_of(f, 6), j);
   }
 }
@@ -241,7 +241,7 @@ __global__ void k_gen_dense(uint64_t seed, uint64_t step, uint32_t rank, uint32_
 // with logit = bias, + f64(dense_w[j]) * f64(dense[j]) for j ascending, +
 // f64(id_contrib[f][id]) for (f, id) in order (data.cpp:57-68); label =
 // (first uniform of CounterRng({seed, 0, step, rank, s, kTagLabel = 3})) < p.
-__global__ void k_gen_labels(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, uint32_t L,
+__global__ void k_gen_labels(uint64_t seed, uint64_t lane, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, uint32_t L,
                              const uint32_t* __restrict__ ids, const float* __restrict__ id_contrib, uint32_t rows,
                              const float* __restrict__ dense, const float* __restrict__ dense_w, uint32_t dd,
                              double bias, float* __restrict__ labels) {
@@ -252,8 +252,36 @@ __global__ void k_gen_labels(uint64_t seed, uint64_t step, uint32_t rank, uint32
     for (uint32_t f = 0; f < F; ++f)
       for (uint32_t j = 0; j < L; ++j) z += (double)id_contrib[(uint64_t)f * rows + id[f * L + j]];
     const double p = 1.0 / (1.0 + exp(-z));
-    const uint64_t k[6] = {seed, 0ull, step, rank, s, 3ull};
+    const uint64_t k[6] = {seed, lane, step, rank, s, 3ull};
     labels[s] = uniform_at(key_of(k, 6), 1) < p ? 1.0f : 0.0f;
+  }
+}
+
+template <typename WT>
+__global__ void k_eval_pool(uint32_t S, uint32_t F, uint32_t L, uint32_t N, const uint32_t* __restrict__ ids,
+                            const EvalShard* __restrict__ shards, uint32_t D, float* __restrict__ out) {
+  const uint64_t n = (uint64_t)S * F * D;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = (uint32_t)(i % D);
+    const uint64_t bag = i / D;
+    const uint32_t f = (uint32_t)(bag % F);
+    const uint32_t* id = ids + bag * L;
+    double pool = 0.0;
+    for (uint32_t o = 0; o < N; ++o) {
+      const EvalShard sh = shards[(uint64_t)f * N + o];
+      if (sh.hi <= sh.lo) continue;
+      const WT* w = reinterpret_cast<const WT*>(sh.w);
+      double partial = 0.0;
+      bool hit = false;
+      for (uint32_t q = 0; q < L; ++q) {
+        const uint32_t r = id[q];
+        if (r < sh.lo || r >= sh.hi) continue;
+        hit = true;
+        partial += (double)(float)w[(uint64_t)(r - sh.lo) * D + j];
+      }
+      if (hit) pool += (double)(float)partial;
+    }
+    out[i] = (float)pool;
   }
 }
 
@@ -323,25 +351,36 @@ void launch_mirror(const float* w, double* wd, uint64_t n, cudaStream_t st) {
   S2D_LAUNCH_CHECK();
 }
 
+void launch_eval_pool(uint32_t S, uint32_t F, uint32_t L, uint32_t N, const uint32_t* ids, const EvalShard* shards,
+                      uint32_t D, int bf16, float* out, cudaStream_t st) {
+  const uint64_t n = (uint64_t)S * F * D;
+  if (!n) return;
+  if (bf16)
+    k_eval_pool<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(S, F, L, N, ids, shards, D, out);
+  else
+    k_eval_pool<float><<<grid_for(n), 256, 0, st>>>(S, F, L, N, ids, shards, D, out);
+  S2D_LAUNCH_CHECK();
+}
+
 void launch_gt_normals(uint64_t key, uint64_t n, double scale, float* out, cudaStream_t st) {
   if (!n) return;
   k_gt_normals<<<grid_for(n), 256, 0, st>>>(key, n, scale, out);
   S2D_LAUNCH_CHECK();
 }
 
-void launch_gen_dense(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t dd, float* out,
+void launch_gen_dense(uint64_t seed, uint64_t lane, uint64_t step, uint32_t rank, uint32_t B, uint32_t dd, float* out,
                       cudaStream_t st) {
   const uint64_t n = (uint64_t)B * dd;
   if (!n) return;
-  k_gen_dense<<<grid_for(n), 256, 0, st>>>(seed, step, rank, B, dd, out);
+  k_gen_dense<<<grid_for(n), 256, 0, st>>>(seed, lane, step, rank, B, dd, out);
   S2D_LAUNCH_CHECK();
 }
 
-void launch_gen_labels(uint64_t seed, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, uint32_t L,
+void launch_gen_labels(uint64_t seed, uint64_t lane, uint64_t step, uint32_t rank, uint32_t B, uint32_t F, uint32_t L,
                        const uint32_t* ids, const float* id_contrib, uint32_t rows, const float* dense,
                        const float* dense_w, uint32_t dd, double bias, float* labels, cudaStream_t st) {
   if (!B) return;
-  k_gen_labels<<<grid_for(B), 256, 0, st>>>(seed, step, rank, B, F, L, ids, id_contrib, rows, dense, dense_w, dd,
+  k_gen_labels<<<grid_for(B), 256, 0, st>>>(seed, lane, step, rank, B, F, L, ids, id_contrib, rows, dense, dense_w, dd,
                                              bias, labels);
   S2D_LAUNCH_CHECK();
 }

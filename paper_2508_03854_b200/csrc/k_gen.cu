@@ -35,7 +35,7 @@ __global__ void k_gen_ids(const GenArgs a) {
         hi = mid;
     }
     const uint32_t f = lo, j = r - __ldg(a.cum + f);
-    const uint64_t fields[7] = {a.seed, 0ull, a.step, a.rank, s, 1ull, f};
+    const uint64_t fields[7] = {a.seed, a.lane, a.step, a.rank, s, 1ull, f};
     uint64_t key = 0x8A5CD789635D2DFFULL;
 #pragma unroll
     for (int q = 0; q < 7; ++q) key = mix64(key + 0x9E3779B97F4A7C15ULL + fields[q]);

@@ -56,6 +56,13 @@ struct Trainer {
   DevBuf fold_ptrs;  // rank 0: per-rank pointer tables of the fold
   double last_loss = 0.0;
   bool have_loss = false;
+  // evaluation (trainer.cpp:687-771), on rank 0's GPU
+  DevBuf ev_ids, ev_len, ev_dense, ev_labels, ev_pooled, ev_dout, ev_dhid, ev_ohid, ev_logit, ev_probs, ev_shards;
+  std::vector<float> ev_labels_host;
+  bool ev_ready = false;
+  std::vector<s2d_train_metrics_row> metrics_rows;
+  s2d_ne_report final_ne{};
+  bool final_done = false;
 
   MlpView view(uint32_t r, int a) {
     const MlpLayout& l = lay[a];
@@ -169,6 +176,7 @@ struct Trainer {
   void dense_create() {
     if (o.dense_dim < 1 || o.dense_hidden < 1 || o.over_hidden < 1)
       throw Error(S2D_EINVAL, "model dimensions must all be >= 1");  // DlrmConfig::validate (model.cpp:188-192)
+    if (o.eval_samples < 1) throw Error(S2D_EINVAL, "eval_samples must be >= 1");  // trainer.cpp:56-58
     const uint32_t FD = o.num_tables * o.dim;
     lay[0].in = o.dense_dim, lay[0].hidden = o.dense_hidden, lay[0].out = o.dim;
     lay[1].in = FD + o.dim, lay[1].hidden = o.over_hidden, lay[1].out = 1;  // DlrmConfig::over_in
@@ -241,8 +249,8 @@ struct Trainer {
     Ctx& c = *ranks[r];
     DenseRank& d = dn[r];
     const uint32_t B = o.per_rank_batch, FD = o.num_tables * o.dim;
-    launch_gen_dense(o.data_seed, k, r, B, o.dense_dim, d.dense.as<float>(), c.stream);
-    launch_gen_labels(o.data_seed, k, r, B, o.num_tables, o.ids_per_sample, d_ids[r].as<uint32_t>(),
+    launch_gen_dense(o.data_seed, 0, k, r, B, o.dense_dim, d.dense.as<float>(), c.stream);
+    launch_gen_labels(o.data_seed, 0, k, r, B, o.num_tables, o.ids_per_sample, d_ids[r].as<uint32_t>(),
                       d.gt_ids.as<float>(), o.rows_per_table, d.dense.as<float>(), d.gt_dense.as<float>(), o.dense_dim,
                       o.gt_bias, d.labels.as<float>(), c.stream);
     const MlpView da = view(r, 0), oa = view(r, 1);
@@ -351,6 +359,7 @@ struct Trainer {
         });
         dense_sync_and_apply(k);
         ++steps_done;
+        after_step();
       }
       return;
     }
@@ -360,6 +369,112 @@ struct Trainer {
       for (uint64_t k = first; k < first + count; ++k) one_step(r, k);
     });
     steps_done += count;
+  }
+
+  // ensure_eval_set (trainer.cpp:689-705): eval_samples samples in chunks of
+  // 1024, chunk c = DataGenerator::gen_batch_into(step c, rank 0, lane kEval)
+  // with eval_seed; ids, dense features and labels stay on rank 0's GPU
+  void ensure_eval_set() {
+    if (ev_ready) return;
+    Ctx& c = *ranks[0];
+    S2D_CUDA(cudaSetDevice(c.device));
+    const uint32_t S = o.eval_samples, F = o.num_tables, L = o.ids_per_sample, dd = o.dense_dim;
+    ev_ids.ensure((size_t)S * F * L * 4);
+    ev_len.ensure((size_t)std::min<uint32_t>(S, 1024) * F * 4);
+    ev_dense.ensure((size_t)S * dd * 4);
+    ev_labels.ensure((size_t)S * 4);
+    uint64_t idx = 0;
+    for (uint32_t c0 = 0; c0 < S; ++idx) {
+      const uint32_t take = std::min<uint32_t>(1024, S - c0);
+      c.gen_batch(o.eval_seed, idx, 0, take, zipf.data(), per_sample.data(), ev_len.as<uint32_t>(),
+                  ev_ids.as<uint32_t>() + (size_t)c0 * F * L, S2D_DEVICE, 1);
+      launch_gen_dense(o.eval_seed, 1, idx, 0, take, dd, ev_dense.as<float>() + (size_t)c0 * dd, c.stream);
+      launch_gen_labels(o.eval_seed, 1, idx, 0, take, F, L, ev_ids.as<uint32_t>() + (size_t)c0 * F * L,
+                        dn[0].gt_ids.as<float>(), o.rows_per_table, ev_dense.as<float>() + (size_t)c0 * dd,
+                        dn[0].gt_dense.as<float>(), dd, o.gt_bias, ev_labels.as<float>() + c0, c.stream);
+      c0 += take;
+    }
+    ev_labels_host.resize(S);
+    S2D_CUDA(cudaStreamSynchronize(c.stream));
+    S2D_CUDA(cudaMemcpy(ev_labels_host.data(), ev_labels.p, (size_t)S * 4, cudaMemcpyDeviceToHost));
+    const uint32_t FD = F * o.dim;
+    ev_pooled.ensure((size_t)S * FD * 4);
+    ev_dout.ensure((size_t)S * o.dim * 4);
+    ev_dhid.ensure((size_t)S * o.dense_hidden * 4);
+    ev_ohid.ensure((size_t)S * o.over_hidden * 4);
+    ev_logit.ensure((size_t)S * 4);
+    ev_probs.ensure((size_t)S * 8);
+    ev_shards.ensure((size_t)F * N * sizeof(EvalShard));
+    ev_ready = true;
+  }
+
+  // eval_probs (trainer.cpp:714-743): pool_ids over group 0's shards (peer
+  // reads when its ranks span GPUs), rank 0's dense_arch + over_arch, sigmoid
+  std::vector<double> eval_probs() {
+    ensure_eval_set();
+    const uint32_t S = o.eval_samples, F = o.num_tables, FD = F * o.dim;
+    std::vector<EvalShard> sh((size_t)F * N);
+    for (uint32_t f = 0; f < F; ++f)
+      for (uint32_t l = 0; l < N; ++l) {
+        Ctx& cl = *ranks[l];
+        const FeatDev& fd = cl.feats[f];
+        sh[(size_t)f * N + l] = {fd.lo, fd.hi, cl.weights.as<char>() + fd.wbase * (cl.bf16 ? 2 : 4)};
+      }
+    Ctx& c = *ranks[0];
+    S2D_CUDA(cudaSetDevice(c.device));
+    S2D_CUDA(cudaMemcpyAsync(ev_shards.p, sh.data(), sh.size() * sizeof(EvalShard), cudaMemcpyHostToDevice, c.stream));
+    launch_eval_pool(S, F, o.ids_per_sample, N, ev_ids.as<uint32_t>(), ev_shards.as<EvalShard>(), o.dim, c.bf16,
+                     ev_pooled.as<float>(), c.stream);
+    const MlpView da = view(0, 0), oa = view(0, 1);
+    launch_mlp_hidden(da, MlpInput{ev_dense.as<float>(), o.dense_dim, nullptr, 0}, S, ev_dhid.as<float>(), c.stream);
+    launch_mlp_out(da, ev_dhid.as<float>(), S, ev_dout.as<float>(), nullptr, c.stream);
+    launch_mlp_hidden(oa, MlpInput{ev_pooled.as<float>(), FD, ev_dout.as<float>(), o.dim}, S, ev_ohid.as<float>(),
+                      c.stream);
+    launch_mlp_out(oa, ev_ohid.as<float>(), S, ev_logit.as<float>(), ev_probs.as<double>(), c.stream);
+    std::vector<double> probs(S);
+    S2D_CUDA(cudaStreamSynchronize(c.stream));
+    S2D_CUDA(cudaMemcpy(probs.data(), ev_probs.p, (size_t)S * 8, cudaMemcpyDeviceToHost));
+    return probs;
+  }
+
+  s2d_ne_report evaluate(const std::vector<double>& probs) {
+    s2d_ne_report rep{};
+    const int rc = s2d_evaluate_ne(probs.data(), ev_labels_host.data(), probs.size(), &rep.ne, &rep.baseline_ctr);
+    if (rc) throw Error(rc, "evaluate_ne: all labels identical, baseline entropy is zero");
+    rep.eval_samples = probs.size();
+    return rep;
+  }
+
+  // make_metrics_row (trainer.cpp:745-771) + the step_n cadence (773-787)
+  void after_step() {
+    const bool last = steps_done == o.steps;
+    const bool cadence = o.eval_cadence > 0 && steps_done % o.eval_cadence == 0;
+    if (!cadence && !last) return;
+    const auto probs = eval_probs();
+    const s2d_ne_report rep = evaluate(probs);
+    std::vector<s2d_metrics_row> mr(T);
+    run_all([&](uint32_t r) { ranks[r]->metrics(&mr[r]); });
+    s2d_train_metrics_row row{};
+    row.step = steps_done;
+    row.loss = last_loss;
+    row.ne = rep.ne;
+    row.eff_lr_p50 = mr[0].eff_lr_p50;
+    row.eff_lr_p99 = mr[0].eff_lr_p99;
+    row.v_mean = mr[0].v_mean;
+    metrics_rows.push_back(row);
+    if (last) {
+      final_ne = rep;
+      final_done = true;
+    }
+  }
+
+  s2d_ne_report finalize_ne() {
+    if (!dense_on) throw Error(S2D_EINVAL, "the trainer has no dense model");
+    if (!final_done) {
+      final_ne = evaluate(eval_probs());
+      final_done = true;
+    }
+    return final_ne;
   }
 
   // Trainer::rank_model(rank) (trainer.hpp:125)
@@ -499,6 +614,22 @@ int s2d_trainer_last_loss(s2d_trainer* t, double* out) {
     if (!tr->dense_on) throw Error(S2D_EINVAL, "the trainer has no dense model");
     if (!tr->have_loss) throw Error(S2D_EINVAL, "no step has run");
     *out = tr->last_loss;
+  });
+}
+
+int s2d_trainer_metrics_rows(s2d_trainer* t, s2d_train_metrics_row* out, uint32_t cap, uint32_t* n) {
+  return tguard([&] {
+    auto* tr = as_trainer(t);
+    if (n) *n = (uint32_t)tr->metrics_rows.size();
+    if (out && cap < tr->metrics_rows.size()) throw Error(S2D_EINVAL, "metrics output capacity too small");
+    if (out) std::memcpy(out, tr->metrics_rows.data(), tr->metrics_rows.size() * sizeof(s2d_train_metrics_row));
+  });
+}
+
+int s2d_trainer_final_ne(s2d_trainer* t, s2d_ne_report* out) {
+  return tguard([&] {
+    if (!out) throw Error(S2D_EINVAL, "null argument");
+    *out = as_trainer(t)->finalize_ne();
   });
 }
 

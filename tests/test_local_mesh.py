@@ -300,21 +300,22 @@ def test_trainer_dense_model_matches_real_reference_trainer(mesh):
     backward, the dense DP step) against the REAL reference Trainer with
     ITS MLPs (trainer.cpp + model.cpp in oracle/_ref, nothing replayed):
     every rank's MLP parameters and every replica after the last step are
-    bitwise equal; every step's global-batch loss agrees to 1e-15."""
+    bitwise equal; every step's MetricsRow (global-batch loss, NE of the
+    eval set, effective-lr percentiles, mean moment) agrees."""
     import paper_2508_03854_b200 as s2d
     from oracle import reference_available, reference_trainer_model, trainer_options
 
     if not reference_available():
         pytest.skip("oracle/_ref not built")
     o = trainer_options(**mesh)
-    ws_real, vs_real, model_real, loss_real = reference_trainer_model(o)
+    ws_real, vs_real, model_real, rows_real = reference_trainer_model(o)
     tr = s2d.Trainer(s2d.TrainerOptions(
         total_ranks=o.T, groups=o.M, num_tables=o.F, rows_per_table=o.rows, dim=o.dim,
         strategy="row-wise" if o.strategy else "table-wise", zipf_exponent=o.zipf, ids_per_sample=o.ids_per_sample,
         per_rank_batch=o.B, steps=o.steps, sync_interval=o.sync_interval, data_seed=o.data_seed,
         init_seed=o.init_seed, optimizer=s2d.OptimizerConfig(o.eta, o.eps, o.c, "sgd" if o.sgd else "rowwise-adagrad"),
         devices=[0], dense_model=True, dense_dim=o.dense_dim, dense_hidden=o.dense_hidden,
-        over_hidden=o.over_hidden))
+        over_hidden=o.over_hidden, eval_cadence=1, eval_samples=512, eval_seed=o.eval_seed))
     try:
         losses = []
         for _ in range(o.steps):
@@ -322,7 +323,19 @@ def test_trainer_dense_model_matches_real_reference_trainer(mesh):
             losses.append(tr.last_loss)
         # the loss is -log(p) (trainer.cpp:412): CUDA's log may round 1 ulp
         # away from the host libm's; it feeds nothing downstream
-        np.testing.assert_allclose(np.array(losses), loss_real, rtol=1e-15, atol=0)
+        np.testing.assert_allclose(np.array(losses), rows_real[:, 1], rtol=1e-15, atol=0)
+        # MetricsRow per step: NE of the eval set (lane kEval, pooled from
+        # group 0's replica with rank 0's MLPs; CUDA exp in the sigmoid),
+        # the exact effective-lr percentiles, v_mean (blocked f64 sum)
+        rows = tr.metrics()
+        assert [r["step"] for r in rows] == list(range(1, o.steps + 1))
+        got = np.array([[r["loss"], r["ne"], r["eff_lr_p50"], r["eff_lr_p99"], r["v_mean"]] for r in rows])
+        np.testing.assert_allclose(got[:, 0], rows_real[:, 1], rtol=1e-15, atol=0)
+        np.testing.assert_allclose(got[:, 1], rows_real[:, 2], rtol=1e-13, atol=0)
+        np.testing.assert_array_equal(got[:, 2:4], rows_real[:, 3:5])
+        np.testing.assert_allclose(got[:, 4], rows_real[:, 5], rtol=1e-12, atol=0)
+        fin = tr.finalize()["final_ne"]
+        assert fin["ne"] == rows[-1]["ne"] and fin["eval_samples"] == 512
         for r in range(o.T):
             got = tr.rank_model(r)
             for name in ("dense_arch", "over_arch"):
