@@ -602,3 +602,21 @@ def read_checkpoint(path: str):
         raise RuntimeError("trailing bytes in checkpoint: " + path)
     cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.float32)
     return tables, cat(ws), cat(vs)
+
+
+def reference_train_toy(overrides: dict) -> dict:
+    """The REAL reference run_train (src/experiment.cpp:23-34, config.cpp and
+    trainer.cpp in oracle/_ref) for train_toy's {dotted_key: value} config."""
+    lib = C.CDLL(REF_SO)
+    fn = lib.ref_train_toy
+    fn.argtypes = [C.c_uint32, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), C.POINTER(C.c_double),
+                   C.POINTER(C.c_double), C.c_char_p]
+    fn.restype = C.c_int
+    ks = (C.c_char_p * max(1, len(overrides)))(*[k.encode() for k in overrides])
+    vs = (C.c_char_p * max(1, len(overrides)))(*[str(v).encode() for v in overrides.values()])
+    ne, ctr = C.c_double(0), C.c_double(0)
+    h = C.create_string_buffer(17)
+    if fn(len(overrides), ks, vs, C.byref(ne), C.byref(ctr), h):
+        lib.ref_last_error.restype = C.c_char_p
+        raise RuntimeError(lib.ref_last_error().decode())
+    return {"final_ne": ne.value, "baseline_ctr": ctr.value, "config_hash": h.value.decode()}

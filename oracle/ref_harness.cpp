@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <functional>
 #include <stdexcept>
@@ -21,7 +22,9 @@
 #include <thread>
 #include <vector>
 
+#include "sparse2d/config.hpp"
 #include "sparse2d/cost_model.hpp"
+#include "sparse2d/experiment.hpp"
 #include "sparse2d/data.hpp"
 #include "sparse2d/moment_analysis.hpp"
 #include "sparse2d/embedding.hpp"
@@ -571,6 +574,25 @@ int ref_trainer_run_model(const RefTrainerOpts* o, float* const* w_out, float* c
       const double row[6] = {(double)m.step, m.loss, m.ne, m.eff_lr_p50, m.eff_lr_p99, m.v_mean};
       std::memcpy(loss_out + 6 * i, row, sizeof(row));
     }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// The reference module's train_toy (bindings/module.cpp:148-163): run_train
+// of ExperimentConfig + {keys[i]: vals[i]} overrides; final NE, baseline
+// CTR and the 16-hex-digit config hash (hash_out, >= 17 bytes).
+int ref_train_toy(uint32_t n, const char* const* keys, const char* const* vals, double* final_ne, double* baseline_ctr,
+                  char* hash_out) {
+  try {
+    ExperimentConfig cfg;
+    for (uint32_t i = 0; i < n; ++i) cfg.set(keys[i], vals[i]);
+    const RunArtifact art = run_train(cfg);
+    *final_ne = art.result.final_ne.ne;
+    *baseline_ctr = art.result.final_ne.baseline_ctr;
+    std::snprintf(hash_out, 17, "%s", art.config_hash.c_str());
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -33,11 +33,13 @@ from .api import (  # noqa: F401
     plan_greedy,
     run_ranks,
     traces_to_csv,
+    train_toy,
     validate_plan,
 )
 
 __all__ = [
     "Trainer",
+    "train_toy",
     "TrainerOptions",
     "closed_form_ratio",
     "estimate_increment_ratio",

@@ -13,6 +13,7 @@ this module only marshals arguments.
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 from dataclasses import dataclass
 from typing import Iterable, Sequence
@@ -872,3 +873,158 @@ class Trainer:
         m = L.MetricsRowC()
         L.check(self.lib.s2d_trainer_metrics(self._t, C.byref(m)))
         return {"eff_lr_p50": m.eff_lr_p50, "eff_lr_p99": m.eff_lr_p99, "v_mean": m.v_mean, "rows": int(m.rows)}
+
+
+# ---- train_toy (bindings/module.cpp:148-163, src/experiment.cpp:23-34) ------
+
+# ExperimentConfig's keys and defaults (src/config.cpp:24-60)
+_CONFIG_DEFAULTS = {
+    "topology.total_ranks": "8", "topology.groups": "1",
+    "data.tables": "8", "data.rows_per_table": "10000", "data.ids_per_sample": "2", "data.zipf_exponent": "1.0",
+    "data.dense_dim": "8", "data.gt_id_scale": "0.25", "data.gt_dense_scale": "0.35", "data.gt_bias": "-0.8",
+    "model.dim": "16", "model.dense_hidden": "32", "model.over_hidden": "64",
+    "optimizer.variant": "rowwise-adagrad", "optimizer.eta": "0.1", "optimizer.eps": "1e-8", "optimizer.c": "1.0",
+    "run.steps": "1000", "run.per_rank_batch": "4", "run.sync_interval": "1", "run.eval_cadence": "0",
+    "run.eval_samples": "100000", "run.seed": "1", "run.threads": "1", "run.trace": "false",
+    "sharding.strategy": "row-wise",
+    "bandwidth.alpha_s": "2e-6", "bandwidth.inter_bytes_per_s": "2.5e10", "bandwidth.intra_bytes_per_s": "",
+    "bandwidth.ranks_per_host": "8", "compute.flops_per_s": "2e12",
+    "seeds.data": "", "seeds.init": "", "seeds.eval": "",
+}
+
+_M64 = (1 << 64) - 1
+
+
+def _mix64(x: int) -> int:
+    x ^= x >> 30
+    x = (x * 0xBF58476D1CE4E5B9) & _M64
+    x ^= x >> 27
+    x = (x * 0x94D049BB133111EB) & _M64
+    return x ^ (x >> 31)
+
+
+def _make_key(*fields: int) -> int:
+    """rng.hpp make_key: fold fields through mix64."""
+    h = 0x8A5CD789635D2DFF
+    for f in fields:
+        h = _mix64((h + 0x9E3779B97F4A7C15 + f) & _M64)
+    return h
+
+
+def _resolve_config(values: dict) -> tuple:
+    """ExperimentConfig::resolve (src/config.cpp:200-289): every issue is
+    collected and raised together as ValueError; seeds derive from run.seed
+    as make_key({master, lane}) unless given."""
+    issues = []
+
+    def u64(key, lo, hi):
+        raw = values[key]
+        try:
+            v = int(raw, 10)
+        except ValueError:
+            issues.append(f"{key} = '{raw}' is not a valid integer")
+            return lo
+        if v < lo or v > hi:
+            issues.append(f"{key} = {raw} out of range [{lo}, {hi}]")
+            return lo
+        return v
+
+    def dbl(key, lo, hi):
+        raw = values[key]
+        try:
+            v = float(raw)
+        except ValueError:
+            issues.append(f"{key} = '{raw}' is not a valid number")
+            return lo
+        if not math.isfinite(v) or v < lo or v > hi:
+            issues.append(f"{key} = {raw} out of range")
+            return lo
+        return v
+
+    total = u64("topology.total_ranks", 1, 1 << 20)
+    groups = u64("topology.groups", 1, 1 << 20)
+    if total % groups:
+        issues.append("topology.groups must divide topology.total_ranks")
+    o = dict(
+        total_ranks=total, groups=groups, num_tables=u64("data.tables", 1, 4096),
+        rows_per_table=u64("data.rows_per_table", 1, 100000000), ids_per_sample=u64("data.ids_per_sample", 0, 1024),
+        zipf_exponent=dbl("data.zipf_exponent", 0.0, 100.0), dense_dim=u64("data.dense_dim", 1, 4096),
+        gt_id_scale=dbl("data.gt_id_scale", 0.0, 1e6), gt_dense_scale=dbl("data.gt_dense_scale", 0.0, 1e6),
+        gt_bias=dbl("data.gt_bias", -1e6, 1e6), dim=u64("model.dim", 1, 512),
+        dense_hidden=u64("model.dense_hidden", 1, 65536), over_hidden=u64("model.over_hidden", 1, 65536),
+        steps=u64("run.steps", 1, 1 << 40), per_rank_batch=u64("run.per_rank_batch", 1, 1 << 20),
+        sync_interval=u64("run.sync_interval", 1, 1 << 20), eval_cadence=u64("run.eval_cadence", 0, 1 << 40),
+        eval_samples=u64("run.eval_samples", 1, 100000000))
+    variant = values["optimizer.variant"]
+    if variant not in ("rowwise-adagrad", "sgd"):
+        issues.append(f"unknown optimizer variant: {variant}")
+    opt = OptimizerConfig(eta=dbl("optimizer.eta", 1e-12, 1e6), eps=dbl("optimizer.eps", 1e-30, 1e6),
+                          c=dbl("optimizer.c", 1e-12, 1e9), variant=variant)
+    master = u64("run.seed", 0, _M64)
+    u64("run.threads", 1, 1024)
+    if values["run.trace"] not in ("true", "1", "false", "0"):
+        issues.append(f"run.trace = '{values['run.trace']}' is not a boolean (true/false)")
+    strategy = values["sharding.strategy"]
+    if strategy not in ("row-wise", "table-wise"):
+        issues.append(f"unknown sharding strategy: {strategy}")
+    dbl("bandwidth.alpha_s", 0.0, 1.0)
+    dbl("bandwidth.inter_bytes_per_s", 1.0, 1e18)
+    if values["bandwidth.intra_bytes_per_s"]:
+        dbl("bandwidth.intra_bytes_per_s", 1.0, 1e18)
+    u64("bandwidth.ranks_per_host", 1, 1 << 20)
+    dbl("compute.flops_per_s", 1.0, 1e24)
+
+    def seed(key, lane):
+        return _make_key(master, lane) if not values[key] else u64(key, 0, _M64)
+
+    o.update(data_seed=seed("seeds.data", 1), init_seed=seed("seeds.init", 2), eval_seed=seed("seeds.eval", 3))
+    if issues:
+        raise ValueError(f"configuration invalid ({len(issues)} issue(s)):" + "".join("\n  - " + i for i in issues))
+    return o, opt, strategy
+
+
+def _config_hash(values: dict) -> str:
+    """ExperimentConfig::hash_hex (src/config.cpp:291-316): FNV-1a 64 over the
+    sorted 'key=value\\n' entries."""
+    h = 0xCBF29CE484222325
+    for k in sorted(values):
+        for c in (k + "=" + values[k] + "\n").encode():
+            h = ((h ^ c) * 0x100000001B3) & _M64
+    return f"{h:016x}"
+
+
+def train_toy(overrides: dict | None = None) -> dict:
+    """run_train for a config given as {dotted_key: value} (the reference
+    module's train_toy): the Trainer facade with the device dense model on
+    this process's GPUs.  Returns final_ne, baseline_ctr, config_hash, the
+    metrics rows, and qps_sim -- here MEASURED samples/s of the whole run
+    (global batch x steps / wall seconds; the reference's alpha-beta
+    simulation is out of scope) -- and peak_mem_bytes, the reference's
+    footprint formula without its simulated all-to-all term (owned shard
+    state + MLP + one resident batch, trainer.cpp:796-829)."""
+    import time
+
+    values = dict(_CONFIG_DEFAULTS)
+    for k, v in (overrides or {}).items():
+        if k not in values:
+            raise ValueError(f"unknown config key '{k}'")
+        values[k] = str(v)
+    o, opt, strategy = _resolve_config(values)
+    tr = Trainer(TrainerOptions(optimizer=opt, strategy=strategy, dense_model=True, **o))
+    try:
+        t0 = time.perf_counter()
+        tr.run()
+        fin = tr.finalize()
+        wall = time.perf_counter() - t0
+        N = o["total_ranks"] // o["groups"]
+        shard = max(sum(e["row_hi"] - e["row_lo"] for e in tr.plan() if e["local_rank"] == n) for n in range(N))
+        D, F = o["dim"], o["num_tables"]
+        mlp = (o["dense_hidden"] * o["dense_dim"] + o["dense_hidden"] + D * o["dense_hidden"] + D
+               + o["over_hidden"] * (F * D + D) + 2 * o["over_hidden"] + 1)
+        batch = (F * o["ids_per_sample"] * 4 + o["dense_dim"] * 4 + 4) * o["per_rank_batch"]
+        return {"final_ne": fin["final_ne"]["ne"], "baseline_ctr": fin["final_ne"]["baseline_ctr"],
+                "qps_sim": o["total_ranks"] * o["per_rank_batch"] * o["steps"] / wall,
+                "peak_mem_bytes": shard * (D + 1) * 4 + mlp * 4 + batch, "config_hash": _config_hash(values),
+                "metrics": fin["metrics"]}
+    finally:
+        tr.close()

@@ -224,3 +224,28 @@ def test_reference_helper_functions_match_the_reference():
     p = rng.uniform(0.05, 0.95, 1000)
     y = (rng.random(1000) < 0.3).astype(np.float32)
     assert s2d.evaluate_ne(p, y)["ne"] == ref.ref_evaluate_ne(p.ctypes.data, y.ctypes.data, 1000)
+
+
+def test_train_toy_config_schema():
+    """train_toy's config layer (ExperimentConfig, src/config.cpp): unknown
+    keys and invalid values are errors (all issues reported together), seeds
+    derive from run.seed as make_key({master, lane}), and the config hash is
+    the reference's FNV-1a over the resolved key/value map."""
+    from paper_2508_03854_b200.api import _CONFIG_DEFAULTS, _config_hash, _make_key, _resolve_config
+    import paper_2508_03854_b200 as s2d
+
+    with pytest.raises(ValueError, match="unknown config key"):
+        s2d.train_toy({"model.nope": "1"})
+    v = dict(_CONFIG_DEFAULTS, **{"topology.total_ranks": "6", "topology.groups": "4", "model.dim": "x"})
+    with pytest.raises(ValueError, match=r"\(2 issue\(s\)\)"):
+        _resolve_config(v)
+    o, opt, strategy = _resolve_config(dict(_CONFIG_DEFAULTS, **{"run.seed": "3", "seeds.init": "77"}))
+    assert o["data_seed"] == _make_key(3, 1) and o["eval_seed"] == _make_key(3, 3) and o["init_seed"] == 77
+    assert strategy == "row-wise" and opt.variant == "rowwise-adagrad"
+    from oracle import reference_available, reference_train_toy
+
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    cfg = {"data.tables": "1", "run.steps": "1", "run.eval_samples": "64", "topology.total_ranks": "1"}
+    # cheap reference run: only its hash is compared here (the GPU test compares the training)
+    assert reference_train_toy(cfg)["config_hash"] == _config_hash(dict(_CONFIG_DEFAULTS, **cfg))

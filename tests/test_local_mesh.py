@@ -348,3 +348,26 @@ def test_trainer_dense_model_matches_real_reference_trainer(mesh):
                 assert np.array_equal(v.view(np.uint32), vs_real[g][f * o.rows:(f + 1) * o.rows].view(np.uint32))
     finally:
         tr.close()
+
+
+def test_train_toy_matches_reference_module():
+    """train_toy (the reference module's run_train entry point,
+    tests/python/test_smoke.py:62-90): the same config through the device
+    Trainer + dense model and through the REAL reference run_train gives the
+    same final NE, baseline CTR and config hash; reruns are deterministic."""
+    import paper_2508_03854_b200 as s2d
+    from oracle import reference_available, reference_train_toy
+
+    cfg = {"topology.total_ranks": "4", "topology.groups": "2", "data.tables": "2", "data.rows_per_table": "64",
+           "model.dim": "8", "model.dense_hidden": "4", "model.over_hidden": "8", "run.steps": "20",
+           "run.eval_samples": "256", "run.seed": "3"}
+    res = s2d.train_toy(cfg)
+    assert 0.0 < res["final_ne"] < 2.0 and res["qps_sim"] > 0.0
+    assert s2d.train_toy(cfg)["final_ne"] == res["final_ne"]
+    assert len(res["metrics"]) == 1 and res["metrics"][0]["step"] == 20
+    if not reference_available():
+        pytest.skip("oracle/_ref not built")
+    ref = reference_train_toy(cfg)
+    assert res["config_hash"] == ref["config_hash"]
+    assert res["baseline_ctr"] == ref["baseline_ctr"]
+    assert abs(res["final_ne"] - ref["final_ne"]) <= 1e-12 * abs(ref["final_ne"])
