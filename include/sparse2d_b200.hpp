@@ -156,9 +156,20 @@ struct TableCopy {
   const float* row(uint32_t r) const { return weights.data() + (size_t)r * dim; }
 };
 
+// Host copy of one Mlp's parameters (model.hpp:56): w1 [hidden][in], b1,
+// w2 [out][hidden], b2.
+struct MlpCopy {
+  uint32_t in = 0, hidden = 0, out = 0;
+  std::vector<float> w1, b1, w2, b2;
+};
+struct RankModelCopy {
+  MlpCopy dense_arch, over_arch;  // RankModel (model.hpp:80-83)
+};
+
 // Trainer (include/sparse2d/trainer.hpp:106-132) over s2d_trainer_*: the
-// whole 2D mesh as virtual ranks of this process.  The dense model's
-// gradient comes from set_upstream (else the synthetic one).
+// whole 2D mesh as virtual ranks of this process.  The upstream gradient
+// comes from the device dense model (opts.dense_model = 1), set_upstream,
+// or the synthetic generator.
 class Trainer {
  public:
   explicit Trainer(const s2d_trainer_options& opts) : opts_(opts) { check(s2d_trainer_create(&opts, &t_)); }
@@ -201,6 +212,41 @@ class Trainer {
   s2d_metrics_row metrics() const {
     s2d_metrics_row m{};
     check(s2d_trainer_metrics(t_, &m));
+    return m;
+  }
+  // TrainResult::metrics so far and finalize()'s final_ne (dense model only)
+  std::vector<s2d_train_metrics_row> metrics_rows() const {
+    uint32_t n = 0;
+    check(s2d_trainer_metrics_rows(t_, nullptr, 0, &n));
+    std::vector<s2d_train_metrics_row> out(n);
+    check(s2d_trainer_metrics_rows(t_, out.data(), n, &n));
+    return out;
+  }
+  s2d_ne_report final_ne() {
+    s2d_ne_report r{};
+    check(s2d_trainer_final_ne(t_, &r));
+    return r;
+  }
+  double last_loss() const {
+    double x = 0;
+    check(s2d_trainer_last_loss(t_, &x));
+    return x;
+  }
+  RankModelCopy rank_model(uint32_t rank) const {
+    RankModelCopy m;
+    const uint32_t FD = opts_.num_tables * opts_.dim;
+    MlpCopy* arch[2] = {&m.dense_arch, &m.over_arch};
+    const uint32_t dims[2][3] = {{opts_.dense_dim, opts_.dense_hidden, opts_.dim},
+                                 {FD + opts_.dim, opts_.over_hidden, 1}};
+    for (int a = 0; a < 2; ++a) {
+      MlpCopy& c = *arch[a];
+      c.in = dims[a][0], c.hidden = dims[a][1], c.out = dims[a][2];
+      c.w1.resize((size_t)c.hidden * c.in);
+      c.b1.resize(c.hidden);
+      c.w2.resize((size_t)c.out * c.hidden);
+      c.b2.resize(c.out);
+      check(s2d_trainer_rank_model(t_, rank, a, c.w1.data(), c.b1.data(), c.w2.data(), c.b2.data()));
+    }
     return m;
   }
 
