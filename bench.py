@@ -377,7 +377,6 @@ def run_ours(args):
         host.append((lengths, ids, up))
     dev = [(torch.from_numpy(l.view(np.int32)).cuda(), torch.from_numpy(i.view(np.int32)).cuda(),
             torch.from_numpy(u).cuda()) for l, i, u in host]
-    pooled = torch.empty((w.batch, w.sum_dims), dtype=torch.float32, device="cuda")
     nnz_mean = float(np.mean([len(h[1]) for h in host]))
 
     host_s = {"forward": 0.0, "backward": 0.0}
@@ -507,7 +506,7 @@ def run_ours(args):
     # overlaps step k+1's upload, lookup and update; one synchronize at the end
     # the device-resident inputs are no longer needed: their HBM goes to the
     # host-mode staging buffers
-    del dev, pooled
+    del dev
     torch.cuda.empty_cache()
     if args.no_e2e:
         e2e_serial = e2e_step = e2e = None

@@ -1153,9 +1153,11 @@ bool Ctx::snapshot_enabled() const {
 // Room in the snapshot log for an update of `items` sorted items: its
 // heads save at log row base + their sorted position (no atomics), so the
 // interval's log spans every item of its updates (config 2: 4.7M rows, 2.5
-// GB per step).  The log leaves room for the sync's staging plus 4 GB of
-// HBM; when it cannot grow the interval is marked broken (the sync then
-// exchanges every union row, which needs no snapshot).  Returns base.
+// GB per step).  The log is held to a quarter of the device's memory and
+// leaves the sync's staging plus a quarter of the device (at least 4 GB)
+// free for the other buffers' growth; when it cannot grow the interval is
+// marked broken (the sync then exchanges every union row, which needs no
+// snapshot).  Returns base.
 uint64_t Ctx::snap_reserve(uint64_t items) {
   if (snap_broken) return 0;
   const uint64_t rf = max_dim + 4;
@@ -1172,7 +1174,9 @@ uint64_t Ctx::snap_reserve(uint64_t items) {
   size_t fr = 0, tot = 0;
   S2D_CUDA(cudaMemGetInfo(&fr, &tot));
   void* p = nullptr;
-  if ((uint64_t)fr < (want + std::min<uint64_t>(items, n_slots)) * rf * 4 + (4ull << 30) ||
+  const uint64_t keep = std::max<uint64_t>(4ull << 30, (uint64_t)tot / 4);
+  if (want * rf * 4 > (uint64_t)tot / 4 ||
+      (uint64_t)fr < (want + std::min<uint64_t>(items, n_slots)) * rf * 4 + keep ||
       cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
     (void)cudaGetLastError();
     snap_broken = true;
