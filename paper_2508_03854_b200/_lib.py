@@ -168,16 +168,25 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    # SPARSE2D_EXT_DIR (python/sparse2d/__init__.py:8-10): a prebuilt library
+    # in that directory is used as is
+    ext = os.environ.get("SPARSE2D_EXT_DIR")
+    if ext and os.path.exists(os.path.join(ext, os.path.basename(LIB_PATH))):
+        _lib = _bind(C.CDLL(os.path.join(ext, os.path.basename(LIB_PATH))))
+        return _lib
     if not _build.up_to_date():
         if not build_if_missing:
             raise ImportError(f"{LIB_PATH} missing or stale; run python -m paper_2508_03854_b200.build")
         _build.build()
-    lib = C.CDLL(LIB_PATH)
+    _lib = _bind(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def _bind(lib: C.CDLL) -> C.CDLL:
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    _lib = lib
     return lib
 
 
