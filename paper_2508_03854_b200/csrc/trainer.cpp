@@ -236,6 +236,17 @@ struct Trainer {
     });
     fold_ptrs.release();
     S2D_CUDA(cudaSetDevice(ranks[0]->device));
+    // the dense DP fold and the evaluation read every rank's buffers from
+    // rank 0's GPU
+    for (uint32_t r = 1; r < T; ++r) {
+      const int d = ranks[r]->device;
+      if (d == ranks[0]->device) continue;
+      const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        (void)cudaGetLastError();
+      else
+        S2D_CUDA(e);
+    }
     fold_ptrs.ensure((size_t)9 * T * sizeof(void*));
     dense_on = true;
   }

@@ -288,7 +288,8 @@ def test_trainer_facade_default_upstream_checkpoint_metrics(tmp_path, port):
         eng.close()
 
 
-DENSE_MESHES = [dict(T=1, M=1, steps=5), dict(T=4, M=2), dict(T=4, M=1, strategy="table-wise", B=16),
+DENSE_MESHES = [dict(T=1, M=1, steps=5), dict(T=4, M=2), dict(T=4, M=2, all_gpus=True),
+                dict(T=4, M=1, strategy="table-wise", B=16),
                 dict(T=4, M=2, sgd=True, sync_interval=2), dict(T=6, M=3, rows=50, dim=12, L=5, dense_hidden=9,
                                                                 over_hidden=33, dense_dim=7)]
 
@@ -307,6 +308,8 @@ def test_trainer_dense_model_matches_real_reference_trainer(mesh):
 
     if not reference_available():
         pytest.skip("oracle/_ref not built")
+    mesh = dict(mesh)
+    devices = None if mesh.pop("all_gpus", False) else [0]  # None: ranks round-robin over every GPU
     o = trainer_options(**mesh)
     ws_real, vs_real, model_real, rows_real = reference_trainer_model(o)
     tr = s2d.Trainer(s2d.TrainerOptions(
@@ -314,7 +317,7 @@ def test_trainer_dense_model_matches_real_reference_trainer(mesh):
         strategy="row-wise" if o.strategy else "table-wise", zipf_exponent=o.zipf, ids_per_sample=o.ids_per_sample,
         per_rank_batch=o.B, steps=o.steps, sync_interval=o.sync_interval, data_seed=o.data_seed,
         init_seed=o.init_seed, optimizer=s2d.OptimizerConfig(o.eta, o.eps, o.c, "sgd" if o.sgd else "rowwise-adagrad"),
-        devices=[0], dense_model=True, dense_dim=o.dense_dim, dense_hidden=o.dense_hidden,
+        devices=devices, dense_model=True, dense_dim=o.dense_dim, dense_hidden=o.dense_hidden,
         over_hidden=o.over_hidden, eval_cadence=1, eval_samples=512, eval_seed=o.eval_seed))
     try:
         losses = []
