@@ -410,7 +410,10 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pair_push(
 }
 
 // The peer's entries (its list order): a final mean is stored as is; a copy
-// is averaged with this replica's row in ascending group order.
+// is averaged with this replica's row in ascending group order.  Each warp
+// takes 32-entry chunks of the peer's list: lane i resolves entry i's row,
+// flag and moments (one parallel feature lookup per chunk), then the warp
+// streams the rows R at a time.
 template <typename WT, int kSyncV>
 __global__ void __launch_bounds__(256) k_pair_recv(const float* __restrict__ stage, uint32_t me,
                                                    const uint32_t* __restrict__ theirs,
@@ -421,62 +424,68 @@ __global__ void __launch_bounds__(256) k_pair_recv(const float* __restrict__ sta
   pdl_wait();
   const uint32_t count = counts[me ^ 1u];
   const uint32_t lane = lane_id();
-  const uint32_t warps = gridDim.x * (blockDim.x / 32);
+  const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+  const uint64_t gw = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   constexpr int R = kSyncV == 1 ? 4 : kSyncV == 2 ? 2 : 1;
-  for (uint32_t i0 = (blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * R; i0 < count; i0 += warps * R) {
-    float4 x[R][kSyncV], own[R][kSyncV];
-    float xm[R], flag[R], own_m[R];
-    uint32_t dim[R], slot[R];
-    WT* row[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const uint32_t i = i0 + r;
-      dim[r] = 0;
-      if (i >= count) continue;
-      slot[r] = theirs[i];
-      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, slot[r]);
-      dim[r] = feats[f].dim;
-      row[r] = w + feats[f].wbase + (uint64_t)(slot[r] - feats[f].vbase) * dim[r];
-      const float* in = stage + (uint64_t)i * row_floats;
-#pragma unroll
-      for (int v = 0; v < kSyncV; ++v)
-        if (lane + v * 32 < dim[r] / 4) x[r][v] = *reinterpret_cast<const float4*>(in + (lane + v * 32) * 4);
-      flag[r] = in[row_floats - 2];
-      xm[r] = in[row_floats - 1];
+  for (uint64_t c0 = gw * 32; c0 < count; c0 += warps * 32) {
+    const uint32_t rows = count - c0 < 32 ? (uint32_t)(count - c0) : 32u;
+    uint32_t my_slot = 0, my_dim = 0;
+    uint64_t my_wofs = 0;
+    float my_flag = 1.f, my_xm = 0.f, my_own_m = 0.f;
+    if (lane < rows) {
+      my_slot = theirs[c0 + lane];
+      const uint32_t f = feature_of_slot(vbase_sorted, feat_of_vbase, n_feat, my_slot);
+      my_dim = feats[f].dim;
+      my_wofs = feats[f].wbase + (uint64_t)(my_slot - feats[f].vbase) * my_dim;
+      const float* in = stage + (c0 + lane) * (uint64_t)row_floats;
+      my_flag = in[row_floats - 2];
+      my_xm = in[row_floats - 1];
+      if (my_flag == 0.f) my_own_m = moments[my_slot];
     }
+    for (uint32_t j = 0; j < rows; j += R) {
+      float4 x[R][kSyncV], own[R][kSyncV];
+      uint32_t dim[R];
+      bool fin[R];
+      WT* row[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) {  // a copy: this replica's row too
-      own_m[r] = 0.f;
-      if (!dim[r] || flag[r] != 0.f) continue;
+      for (int r = 0; r < R; ++r) {
+        const uint32_t i = (j + r) & 31;
+        dim[r] = j + r < rows ? __shfl_sync(0xffffffffu, my_dim, i) : 0u;
+        row[r] = w + shfl64(my_wofs, i);
+        fin[r] = __shfl_sync(0xffffffffu, my_flag, i) != 0.f;
+        if (!dim[r]) continue;
+        const float* in = stage + (c0 + j + r) * (uint64_t)row_floats;
 #pragma unroll
-      for (int v = 0; v < kSyncV; ++v)
-        if (lane + v * 32 < dim[r] / 4) own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
-      own_m[r] = moments[slot[r]];
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (!dim[r]) continue;
-      const bool fin = flag[r] != 0.f;
-#pragma unroll
-      for (int v = 0; v < kSyncV; ++v)
-        if (lane + v * 32 < dim[r] / 4) {
-          float4 m = x[r][v];
-          if (!fin) {
-            const float4 a = me == 0 ? own[r][v] : x[r][v], b = me == 0 ? x[r][v] : own[r][v];
-            m = make_float4((float)(((double)a.x + (double)b.x) * 0.5), (float)(((double)a.y + (double)b.y) * 0.5),
-                            (float)(((double)a.z + (double)b.z) * 0.5), (float)(((double)a.w + (double)b.w) * 0.5));
+        for (int v = 0; v < kSyncV; ++v)
+          if (lane + v * 32 < dim[r] / 4) {
+            x[r][v] = *reinterpret_cast<const float4*>(in + (lane + v * 32) * 4);
+            if (!fin[r]) own[r][v] = load4_f32(row[r] + (lane + v * 32) * 4);
           }
-          const double d[4] = {(double)m.x, (double)m.y, (double)m.z, (double)m.w};
-          Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
-        }
-      if (lane == 0 && !sgd) {
-        float mm = xm[r];
-        if (!fin) {
-          const float am = me == 0 ? own_m[r] : xm[r], bm = me == 0 ? xm[r] : own_m[r];
-          mm = (float)(((double)am + (double)bm) * 0.5);
-        }
-        moments[slot[r]] = mm;
       }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!dim[r]) continue;
+#pragma unroll
+        for (int v = 0; v < kSyncV; ++v)
+          if (lane + v * 32 < dim[r] / 4) {
+            float4 m = x[r][v];
+            if (!fin[r]) {
+              const float4 a = me == 0 ? own[r][v] : x[r][v], b = me == 0 ? x[r][v] : own[r][v];
+              m = make_float4((float)(((double)a.x + (double)b.x) * 0.5), (float)(((double)a.y + (double)b.y) * 0.5),
+                              (float)(((double)a.z + (double)b.z) * 0.5), (float)(((double)a.w + (double)b.w) * 0.5));
+            }
+            const double d[4] = {(double)m.x, (double)m.y, (double)m.z, (double)m.w};
+            Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
+          }
+      }
+    }
+    if (!sgd && lane < rows) {  // moments: entry `lane` of the chunk
+      float mm = my_xm;
+      if (my_flag == 0.f) {
+        const float am = me == 0 ? my_own_m : my_xm, bm = me == 0 ? my_xm : my_own_m;
+        mm = (float)(((double)am + (double)bm) * 0.5);
+      }
+      moments[my_slot] = mm;
     }
   }
 }
@@ -685,7 +694,8 @@ void launch_pair_recv(const float* stage, uint32_t me, const uint32_t* theirs, c
                       const uint32_t* feat_of_vbase, uint32_t n_feat, uint32_t row_floats, void* weights, int bf16,
                       float* moments, int sgd, cudaStream_t st) {
   if (!theirs_n) return;
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((theirs_n + 31) / 32, 148ull * 8));
+  const uint64_t chunks = (theirs_n + 31) / 32;  // one warp per 32-entry chunk, 8 warps per block
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((chunks + 7) / 8, 148ull * 8));
   pair_dispatch(false, grid, nullptr, stage, me, nullptr, counts, theirs, feats, vbase_sorted, feat_of_vbase, n_feat,
                 nullptr, nullptr, row_floats, weights, bf16, moments, sgd, nullptr, st);
 }
