@@ -261,13 +261,6 @@ struct StreamUpdateArgs {
   uint64_t snap_base;
   uint64_t snap_cap;
   uint32_t snap_rf;
-  // M = 2 fused replica push (null: off): every flushed row goes, as written
-  // (f32 row | copy flag 0 at rf - 2 | moment at rf - 1), to the peer
-  // replica's staging at the row's head ordinal (head_ord), its slot to the
-  // peer's list and to this replica's own list at the same ordinal
-  float* push_stage;
-  uint32_t* push_list;
-  uint32_t* mine_list;
 };
 // mean pooling, N = 1 (k_embed.cu): out = upstream with the columns of
 // mean-pooled tables replaced by f32(f64(up) * (1/L_bag))

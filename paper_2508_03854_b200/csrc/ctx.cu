@@ -357,8 +357,6 @@ void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v,
   if (write && M > 1) {  // written rows join the next replica sync's dirty union
     S2D_CUDA(cudaMemset(dirty.as<uint8_t>() + fd.vbase + (lo - fd.lo), 1, hi - lo));
     snap_broken = true;  // not in the snapshot log: the next sync exchanges every union row
-    fs_ready = false;
-    dirty_clean = false;
   }
   if (v) {
     float* dst = moments.as<float>() + fd.vbase + (lo - fd.lo);
@@ -417,11 +415,7 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
                     reinterpret_cast<uint32_t*>(d + o_seg), reinterpret_cast<uint32_t*>(d + o_row),
                     reinterpret_cast<double*>(d + o_delta), reinterpret_cast<double*>(d + o_mom), nseg, fd.dim,
                     M > 1 ? dirty.as<uint8_t>() + fd.vbase : nullptr, stream);
-  if (M > 1) {
-    snap_broken = true;  // not in the snapshot log (see shard_io)
-    fs_ready = false;
-    dirty_clean = false;
-  }
+  if (M > 1) snap_broken = true;  // not in the snapshot log (see shard_io)
   S2D_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -1075,7 +1069,6 @@ void Ctx::backward_update(const float* upstream, int mem) {
       ua.grad_dbg = dbg_grad.as<double>();
       ua.head_ord = dbg_head.as<uint32_t>();
     }
-    bool fused = false;
     if (snapshot_enabled()) {
       const uint64_t base = snap_reserve(n);
       if (!snap_broken) {
@@ -1084,28 +1077,9 @@ void Ctx::backward_update(const float* upstream, int mem) {
         ua.snap_base = base;
         ua.snap_cap = snap_cap_rows;
         ua.snap_rf = max_dim + 4;
-        // fused replica push: this update's rows are the whole dirty set
-        // (none since the last sync) and fit the pair's staging
-        fused = fused_push_enabled() && dirty_clean && !bf16 && n <= fs_cap && !debug_grad;
       }
     }
-    if (fused) {
-      // parity of the sync this push feeds: the peer's previous sync may still
-      // read the other buffer
-      const uint32_t peer = group ^ 1u, par = (uint32_t)(sync_epoch & 1u);
-      fs_ord.ensure((n + 1) * 4);
-      scan_tmp.ensure(scan_tmp_bytes(n + 1));
-      scan_heads_u32(sk, fs_ord.as<uint32_t>(), n, n_slots, stream, scan_tmp.p, scan_tmp.cap);
-      ua.head_ord = fs_ord.as<uint32_t>();
-      ua.push_stage = reinterpret_cast<float*>(ptrs(fs_stage[par]).p[peer]);
-      ua.push_list = reinterpret_cast<uint32_t*>(ptrs(fs_list[par]).p[peer]);
-      ua.mine_list = fs_mine[par].as<uint32_t>();
-    }
     launch_update_stream(ua, bf16, stream);
-    if (M > 1) {
-      fs_ready = fused;  // a second update before the sync leaves rows the push did not carry
-      dirty_clean = false;
-    }
     uniq = 1;
   }
   (void)uniq;
@@ -1217,42 +1191,8 @@ uint64_t Ctx::snap_reserve(uint64_t items) {
   return base;
 }
 
-// S2D_SYNC_FUSED=0 keeps the pair sync's separate push (A/B switch)
-bool Ctx::fused_push_enabled() const {
-  if (M != 2 || dp_p2p != 1) return false;
-  static const bool off = [] {
-    const char* e = std::getenv("S2D_SYNC_FUSED");
-    return e && e[0] == '0';
-  }();
-  return !off;
-}
-
 void Ctx::replica_sync() {
   if (M <= 1 || !F) return;
-  replica_sync_body();
-  // every replica ran this sync: its rows are consistent and no row is dirty
-  ++sync_epoch;
-  dirty_clean = true;
-  fs_ready = false;
-  // fused push staging, sized (collectively, from the gathered demand) for
-  // the next interval's update; held to an eighth of the device
-  if (fused_push_enabled() && snapshot_enabled() && sync_nnz_max > fs_cap) {
-    const uint64_t want = sync_nnz_max + sync_nnz_max / 4;
-    const uint64_t rf = max_dim + 4;
-    size_t fr = 0, tot = 0;
-    S2D_CUDA(cudaMemGetInfo(&fr, &tot));
-    if (want * rf * 4 * 2 <= (uint64_t)tot / 8) {
-      for (int p = 0; p < 2; ++p) {
-        peer_alloc_in(fs_stage[p], want * rf * 4, dp);
-        peer_alloc_in(fs_list[p], want * 4, dp);
-        fs_mine[p].ensure(want * 4);
-      }
-      fs_cap = want;
-    }
-  }
-}
-
-void Ctx::replica_sync_body() {
   S2D_CUDA(cudaSetDevice(device));
   join_sync();
   phase_begin(kPhSync);
@@ -1268,10 +1208,7 @@ void Ctx::replica_sync_body() {
   // this replica's (count, log complete): the snapshot sync runs only if
   // every replica's log saw every write of the interval
   const bool snap_on = snapshot_enabled();
-  // (count, log complete, fused push ready | parity << 1, demand for the staging size)
-  const uint32_t fpar = (uint32_t)(sync_epoch & 1u);
-  const uint32_t ok_word[3] = {(snap_on && !snap_broken && snap_pos.p) ? 1u : 0u, fs_ready ? 1u + 2u * fpar : 0u,
-                               (uint32_t)std::min<uint64_t>(nnz_own, 0xffffffffull)};
+  const uint32_t ok_word[3] = {(snap_on && !snap_broken && snap_pos.p) ? 1u : 0u, 0u, 0u};
   launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
   S2D_CUDA(cudaMemcpyAsync(d_count + 1, ok_word, 12, cudaMemcpyHostToDevice, stream));
   dp.allgather(d_count, d_gath, 16, stream);
@@ -1280,15 +1217,10 @@ void Ctx::replica_sync_body() {
   const uint32_t* hg = h_counts.as<uint32_t>();
   std::vector<uint32_t> hc(M);
   bool use_snap = snap_on;
-  bool use_fused = snap_on && fused_push_enabled();
-  sync_nnz_max = 0;
   for (uint32_t g = 0; g < M; ++g) {
     hc[g] = hg[4 * g];
     use_snap = use_snap && hg[4 * g + 1] == 1;
-    use_fused = use_fused && hg[4 * g + 2] == 1u + 2u * fpar;
-    sync_nnz_max = std::max<uint64_t>(sync_nnz_max, hg[4 * g + 3]);
   }
-  use_fused = use_fused && use_snap;
   const uint32_t mine = hc[group];
   uint32_t cmax = 0;
   for (uint32_t g = 0; g < M; ++g) cmax = std::max(cmax, hc[g]);
@@ -1298,52 +1230,6 @@ void Ctx::replica_sync_body() {
   if (cmax == 0) {
     stats.dirty_rows = 0;
     stats.sync_mode = 0;
-    phase_end();
-    finish_call();
-    return;
-  }
-  const uint32_t row_floats_f = max_dim + 4;
-  if (use_fused) {
-    // Fused pair sync: each replica's update already stored every row it
-    // wrote (as a copy) into the peer's staging and its slot into the peer's
-    // list, both at the row's head ordinal (k_update_ring PUSH).  After one
-    // barrier each replica averages every entry of the peer's list with its
-    // own row, and the rows only it dirtied with their snapshots -- the same
-    // f32((f64 x_0 + f64 x_1) * 0.5) the pair sync forms, with no push pass.
-    dp_setup();
-    const uint32_t peer = group ^ 1u, par = fpar;
-    S2D_CUDA(cudaMemcpyAsync(d_counts, hc.data(), (size_t)M * 4, cudaMemcpyHostToDevice, stream));
-    S2D_CUDA(cudaMemsetAsync(d_count + 4, 0, 4, stream));
-    const int sgd = opt.variant == S2D_SGD;
-    const bool overlap = sync_overlap_enabled() && !dp.local() && !profile;
-    cudaStream_t ts = stream;
-    if (overlap) {
-      S2D_CUDA(cudaEventRecord(ev_union, stream));
-      S2D_CUDA(cudaStreamWaitEvent(sync_stream, ev_union, 0));
-      ts = sync_stream;
-    }
-    dp_barrier(ts);  // both updates (and their pushes into each other's staging) are complete
-    phase_begin(kPhSyncPush);
-    launch_pair_push(nullptr, group, fs_mine[par].as<uint32_t>(), d_counts, fs_list[par].buf.as<uint32_t>(), mine,
-                     d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
-                     (uint32_t)feat_of_vbase.size(), snap.as<float>(), snap_pos.as<uint32_t>(), row_floats_f,
-                     weights.p, bf16, moments.as<float>(), sgd, d_count + 4, ts);
-    phase_begin(kPhSyncMean);
-    launch_pair_recv(fs_stage[par].buf.as<float>(), group, fs_list[par].buf.as<uint32_t>(), d_counts, hc[peer],
-                     d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
-                     (uint32_t)feat_of_vbase.size(), row_floats_f, weights.p, bf16, moments.as<float>(), sgd, ts);
-    phase_begin(kPhSyncScatter);
-    launch_zero(dirty.p, n_slots, ts);
-    if (overlap) {
-      S2D_CUDA(cudaEventRecord(ev_sync_done, ts));
-      sync_pending = true;
-    }
-    sync_stats_pending = true;
-    sync_snapshot_used = true;
-    stats.sync_mode = 4;
-    sync_sent_rows = mine;
-    sync_pair_rows = (uint64_t)hc[0] + hc[1];
-    sync_cmax = cmax;
     phase_end();
     finish_call();
     return;

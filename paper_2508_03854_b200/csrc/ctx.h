@@ -214,18 +214,6 @@ struct Ctx {
   int dp_p2p = -1;  // -1 undecided, 0 NCCL path, 1 P2P path
   std::vector<void*> dp_w, dp_v, dp_opened;
   PeerBuf dp_flags, dp_stage;
-  // fused M = 2 replica push (k_update_ring PUSH): per step parity, the peer
-  // pushes its updated rows into fs_stage and its list into fs_list; fs_mine
-  // is this replica's own list; fs_ord the head ordinals of the update
-  PeerBuf fs_stage[2], fs_list[2];
-  DevBuf fs_mine[2], fs_ord;
-  uint64_t fs_cap = 0;      // entries per staging buffer (agreed across the pair)
-  bool fs_ready = false;    // the last update pushed every dirty row (no other writes since)
-  bool dirty_clean = true;  // no row dirtied since the last replica sync
-  bool fused_push_enabled() const;
-  uint64_t sync_epoch = 0;     // replica syncs so far (the fused staging parity)
-  uint64_t sync_nnz_max = 0;   // largest update demand in the DP group at the last sync
-  void replica_sync_body();
   uint64_t dp_epoch = 0;
   void dp_setup();
   void dp_barrier(cudaStream_t st);

@@ -20,7 +20,6 @@
 // capped at 12-16 warps/SM by f64 accumulators + in-flight rows
 // (128 regs), stalling on shuffles and load latency.
 #include <cstdlib>
-#include <type_traits>
 
 #include "device.cuh"
 
@@ -654,7 +653,7 @@ __global__ void __launch_bounds__(256) k_group_partials(const StreamUpdateArgs a
 constexpr uint32_t update_warp_bytes(int vpl, bool snap) {
   return (uint32_t)kSlots * vpl * 32 * 16 + 256 + 8 * kC + (snap ? 256 : 0);
 }
-template <typename WT, int VPL, bool FULL, bool SNAP, bool PUSH>
+template <typename WT, int VPL, bool FULL, bool SNAP>
 __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(const StreamUpdateArgs a) {
   pdl_wait();  // persistent single wave
   pdl_trigger();
@@ -836,7 +835,6 @@ __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(c
       }
       bool finite;
       double lr = a.eta;
-      float v_out = vold;  // the moment as stored (PUSH)
       if (!a.sgd) {
         double ns = 0.0;
 #pragma unroll
@@ -853,7 +851,6 @@ __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(c
           const double vc = a.c_pow2 ? (double)v_new * a.inv_c : (double)v_new / a.c;  // exact either way
           lr = a.eta / (sqrt(vc) + a.eps);  // effective_lr (optimizer.cpp:61-63)
           if (lane == 0) a.moments[cur] = v_new;
-          v_out = v_new;
         }
       } else {
         bool f = true;
@@ -864,22 +861,8 @@ __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(c
             if (lane + v * 32 < d4) f &= isfinite(acc[v][j]);
         finite = __all_sync(0xffffffffu, f);
       }
-      // PUSH: this row's staging entry at the peer (its head ordinal)
-      float* const ps = PUSH ? a.push_stage + (uint64_t)__ldg(a.head_ord + cur_pos) * a.snap_rf : nullptr;
       if (!finite) {
         if (lane == 0) atomicOr(a.err, kErrNonfinite);
-        if constexpr (PUSH) {  // the row stays as it was; it still fills its entry (the step faults anyway)
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) {
-            const uint32_t c4 = lane + v * 32;
-            if (c4 < d4) {
-              double x[4];
-              Row<WT>::cvt(x, wraw[v]);
-              *reinterpret_cast<float4*>(ps + c4 * 4) = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
-            }
-          }
-          if (lane == 0 && a.dirty) a.dirty[cur] = 1;
-        }
       } else {
         if (SNAP && cur_snap < a.snap_cap) {  // first write since the last replica sync: save the pre-update row
           const uint32_t pos = cur_snap;
@@ -910,21 +893,10 @@ __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(c
 #pragma unroll
             for (int j = 0; j < 4; ++j) x[j] = x[j] - lr * acc[v][j];
             Vec4<WT>::store(w + c4 * 4, x);
-            if constexpr (PUSH)  // fp32 storage: the stored value itself
-              *reinterpret_cast<float4*>(ps + c4 * 4) = make_float4((float)x[0], (float)x[1], (float)x[2], (float)x[3]);
           }
         }
         if (lane == 0 && a.dirty) a.dirty[cur] = 1;
         ++heads;
-      }
-      if constexpr (PUSH) {
-        if (lane == 0) {
-          const uint32_t ord = __ldg(a.head_ord + cur_pos);
-          ps[a.snap_rf - 2] = 0.f;
-          ps[a.snap_rf - 1] = v_out;
-          a.push_list[ord] = cur;
-          a.mine_list[ord] = cur;
-        }
       }
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
@@ -1131,18 +1103,13 @@ void update_launch(const StreamUpdateArgs& a, cudaStream_t st) {
   if (a.n >= 2ull * kC * kP * kP)
     pdl_launch(k_group_partials<VPL>, dim3(grid_units(a.n / (kC * kP * kP), 8, 148 * 8)), dim3(256), 0, st, a,
                static_cast<const double*>(a.part2), a.part3, (uint64_t)kC * kP * kP);
-  // variants: FULL (slot-indexed uniform rows) x SNAP (M > 1 snapshot log)
-  // x PUSH (fused M = 2 replica push, fp32 only); their register counts
-  // differ, so each has its own occupancy
-  const bool push = snap && a.push_stage != nullptr && std::is_same<WT, float>::value;
-  auto kern = full ? (push ? k_update_ring<WT, VPL, true, true, true>
-                           : snap ? k_update_ring<WT, VPL, true, true, false> : k_update_ring<WT, VPL, true, false, false>)
-                   : (push ? k_update_ring<WT, VPL, false, true, true>
-                           : snap ? k_update_ring<WT, VPL, false, true, false>
-                                  : k_update_ring<WT, VPL, false, false, false>);
+  // variants: FULL (slot-indexed uniform rows) x SNAP (M > 1 snapshot log);
+  // their register counts differ, so each has its own occupancy
+  auto kern = full ? (snap ? k_update_ring<WT, VPL, true, true> : k_update_ring<WT, VPL, true, false>)
+                   : (snap ? k_update_ring<WT, VPL, false, true> : k_update_ring<WT, VPL, false, false>);
   set_smem(kern, nw_u * pw_u);  // per device
-  static int occ[6] = {0, 0, 0, 0, 0, 0};
-  const int vi = (full ? 3 : 0) + (push ? 2 : snap ? 1 : 0);
+  static int occ[4] = {0, 0, 0, 0};
+  const int vi = (full ? 2 : 0) + (snap ? 1 : 0);
   if (!occ[vi]) {
     S2D_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[vi], kern, nw_u * 32, nw_u * pw_u));
     if (occ[vi] < 1) occ[vi] = 1;

@@ -305,9 +305,7 @@ __global__ void k_p2p_scatter(const FeatDev* feats, const uint32_t* vbase_sorted
 // the peer's entries in the peer's list order.
 //
 // Staging entry j of the peer's list: f32 row | flag at rf - 2 (1 = final
-// mean, 0 = copy) | moment at rf - 1.  With peer_stage == null the push is
-// local only (the fused form: the update already pushed every row as a copy):
-// it stores the mean of each row only this replica dirtied, nothing else.
+// mean, 0 = copy) | moment at rf - 1.
 constexpr int kPairWarps = 8;
 template <typename WT, int kSyncV>
 __global__ void __launch_bounds__(kPairWarps * 32) k_pair_push(
@@ -386,18 +384,16 @@ __global__ void __launch_bounds__(kPairWarps * 32) k_pair_push(
                                            (float)(((double)a.w + (double)b.w) * 0.5));
               const double d[4] = {(double)m.x, (double)m.y, (double)m.z, (double)m.w};
               Vec4<WT>::store(row[r] + (lane + v * 32) * 4, d);
-              if (peer_stage) *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = m;
+              *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = m;
             }
           if (lane == 0) {
             const float am = me == 0 ? own_m[r] : old_m[r], bm2 = me == 0 ? old_m[r] : own_m[r];
             const float mm = (float)(((double)am + (double)bm2) * 0.5);
             if (!sgd) moments[slot[r]] = mm;
-            if (peer_stage) {
-              out[row_floats - 2] = 1.f;
-              out[row_floats - 1] = mm;
-            }
+            out[row_floats - 2] = 1.f;
+            out[row_floats - 1] = mm;
           }
-        } else if (peer_stage) {  // both replicas dirtied it: send this replica's copy
+        } else {  // both replicas dirtied it: send this replica's copy
 #pragma unroll
           for (int v = 0; v < kSyncV; ++v)
             if (lane + v * 32 < dim[r] / 4) *reinterpret_cast<float4*>(out + (lane + v * 32) * 4) = own[r][v];

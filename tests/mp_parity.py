@@ -261,22 +261,14 @@ def rank_main(args, rank, world, local, dist, hub):
                 if not (np.array_equal(w.view(np.uint32), ww.view(np.uint32))
                         and np.array_equal(v.view(np.uint32), vv.view(np.uint32))):
                     fails.append(f"checkpoint reload rank {r} table {f}")
-    # which replica-sync path ran: at M = 2 the pair snapshot exchange (1) and,
-    # once the staging exists and the interval is one update, the fused pair
-    # sync whose push rode in the update (4); the slice push / mean / scatter
-    # (2) otherwise or when the environment forces it; NCCL (3) when forced
-    if os.environ.get("S2D_SYNC_NCCL") == "1":
-        want = {3}
-    elif os.environ.get("S2D_SYNC_SNAPSHOT") == "0" or M != 2:
-        want = {2}
-    else:
-        want = {1} if os.environ.get("S2D_SYNC_FUSED") == "0" else {1, 4}
-    n_syncs = args.steps // args.sync_interval
+    # which replica-sync path ran: the pair snapshot exchange (1) at M = 2,
+    # the slice push / mean / scatter (2) otherwise or when the environment
+    # forces it, NCCL (3) when forced
+    want_mode = (3 if os.environ.get("S2D_SYNC_NCCL") == "1"
+                 else 2 if os.environ.get("S2D_SYNC_SNAPSHOT") == "0" or M != 2 else 1)
     for r in range(world):
-        modes = gathered[r][5]
-        if (any(md not in want | {0} for md in modes) or (M > 1 and not any(md in want for md in modes))
-                or (4 in want and args.sync_interval == 1 and n_syncs >= 2 and 4 not in modes)):
-            fails.append(f"rank {r} sync modes {modes} (want {sorted(want)})")
+        if any(md not in (0, want_mode) for md in gathered[r][5]) or (M > 1 and want_mode not in gathered[r][5]):
+            fails.append(f"rank {r} sync modes {gathered[r][5]} (want {want_mode})")
     # measured trace of the last step (reference trace.csv schema)
     last_sync = M > 1 and args.steps % args.sync_interval == 0
     for r in range(world):
