@@ -23,8 +23,15 @@ done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_mesh2x2.csv \
     python tools/step_driver.py --config cfg3 --mesh 2x2 --batch 8192 --steps 2 > gpurun_out/ncu_mesh_launch.log 2>&1
 echo "mesh launch list rc=$?"
-for k in k_bucket_count k_bucket_permute k_combine k_grad_gather k_p2p_push k_p2p_mean k_p2p_scatter k_flag_count k_flag_write k_mark_slots k_publish_counts; do
+for k in k_bucket_count k_bucket_permute k_combine k_grad_gather k_pair_push k_pair_recv k_flag_count k_flag_write k_publish_counts; do
   ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 4 -c 1 \
+      -o gpurun_out/full_$k -f python tools/step_driver.py --config cfg3 --mesh 2x2 --batch 8192 --steps 3 \
+      > gpurun_out/ncu_$k.log 2>&1
+  echo "$k rc=$?"
+done
+# the M > 2 slice sync's kernels (forced on the 2x2 mesh)
+for k in k_p2p_push k_p2p_mean k_p2p_scatter k_mark_slots; do
+  S2D_SYNC_SNAPSHOT=0 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 4 -c 1 \
       -o gpurun_out/full_$k -f python tools/step_driver.py --config cfg3 --mesh 2x2 --batch 8192 --steps 3 \
       > gpurun_out/ncu_$k.log 2>&1
   echo "$k rc=$?"
@@ -37,6 +44,7 @@ python tools/ncu_summarize.py --round r02 --tag ${TAG} --full gpurun_out/full_k_
 cp profiles/r02/ncu_full_${TAG}_summary.csv $OUT/; cp profiles/r02/launches_${TAG}_summary.csv $OUT/
 python tools/ncu_summarize.py --round r02 --tag ${TAG}_mesh2x2 --full gpurun_out/full_k_bucket_count.ncu-rep \
     gpurun_out/full_k_bucket_permute.ncu-rep gpurun_out/full_k_combine.ncu-rep gpurun_out/full_k_grad_gather.ncu-rep \
+    gpurun_out/full_k_pair_push.ncu-rep gpurun_out/full_k_pair_recv.ncu-rep \
     gpurun_out/full_k_p2p_push.ncu-rep gpurun_out/full_k_p2p_mean.ncu-rep gpurun_out/full_k_p2p_scatter.ncu-rep \
     gpurun_out/full_k_flag_count.ncu-rep gpurun_out/full_k_flag_write.ncu-rep gpurun_out/full_k_mark_slots.ncu-rep \
     gpurun_out/full_k_publish_counts.ncu-rep --launches gpurun_out/launches_${TAG}_mesh2x2.csv
