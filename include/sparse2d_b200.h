@@ -449,6 +449,29 @@ uint64_t s2d_launch_count(void);
 int s2d_adagrad_rows(const s2d_optimizer_config* cfg, uint32_t n_rows, uint32_t dim, float* w,
                      float* v, const double* g, double* lr_out);
 
+/* pool_ids / lookup_and_pool (include/sparse2d/embedding.hpp:41-58,
+ * src/embedding.cpp:39-106) on the device: n_bags bags, bag b = ids
+ * [bag_off[b], bag_off[b+1]) of table `table_id` (w: rows x dim fp32, host,
+ * indexed by global row), over the shards [lo[s], hi[s]) in presentation
+ * order: per shard the f64 sum of its hits in id order rounded to f32, then
+ * the f64 sum of those partials rounded to f32, into out [n_bags][dim]
+ * (host).  An id covered by no shard: S2D_ERANGE "lookup id I outside shard
+ * ranges of table T: [lo,hi) ..." (the first in bag order, checked before
+ * any pooling); no shard or dim > 512: S2D_EINVAL. */
+int s2d_pool_ids(const float* w, uint32_t rows, uint32_t dim, uint32_t table_id, uint32_t n_shards,
+                 const uint32_t* lo, const uint32_t* hi, uint64_t n_bags, const uint64_t* bag_off,
+                 const uint32_t* ids, float* out);
+/* aggregate_group_gradient (include/sparse2d/optimizer.hpp:36-44,
+ * src/optimizer.cpp:25-59) on the device: contribution i is (rows[i],
+ * grads[i*dim .. +dim) f64) in canonical arrival order; for every row with a
+ * contribution, ascending: out_rows[k], out_g[k][dim] = (f64 sum in arrival
+ * order) * (1/group_batch), out_count[k] = contributions (sample_count).
+ * *n_out = rows (all outputs NULL: size query; else cap >= rows).
+ * group_batch == 0: S2D_EINVAL. */
+int s2d_aggregate_group_gradient(const uint32_t* rows, const double* grads, uint64_t n, uint32_t group_batch,
+                                 uint32_t dim, uint32_t* out_rows, double* out_g, uint32_t* out_count, uint64_t cap,
+                                 uint64_t* n_out);
+
 /* Debug view of the last step's wire buffers for bit-exact layout tests.
  * which: 0 demand lengths received [N requester][B*F] u32,
  *        1 demand ids received (canonical order) u32,

@@ -156,6 +156,62 @@ struct TableCopy {
   const float* row(uint32_t r) const { return weights.data() + (size_t)r * dim; }
 };
 
+// ShardRef (embedding.hpp:30-38) over a host table copy, and the
+// function-level pool_ids (embedding.hpp:52-53), run on the device.
+struct ShardView {
+  const TableCopy* table = nullptr;
+  uint32_t row_lo = 0, row_hi = 0;
+};
+inline void pool_ids(const std::vector<ShardView>& shards, const std::vector<uint32_t>& ids, float* out,
+                     uint32_t table_id = 0) {
+  if (shards.empty()) throw std::invalid_argument("empty shard set");
+  const TableCopy& t = *shards.front().table;
+  std::vector<uint32_t> lo, hi;
+  for (const auto& s : shards) {
+    lo.push_back(s.row_lo);
+    hi.push_back(s.row_hi);
+  }
+  const uint64_t off[2] = {0, ids.size()};
+  check(s2d_pool_ids(t.weights.data(), t.rows, t.dim, table_id, (uint32_t)shards.size(), lo.data(), hi.data(), 1,
+                     off, ids.data(), out));
+}
+
+// aggregate_group_gradient (optimizer.hpp:23-44), run on the device.
+struct RowGradient {
+  uint32_t row = 0;
+  std::vector<double> g;
+  uint32_t sample_count = 0;
+};
+struct RowGradContribution {
+  uint32_t row = 0;
+  std::vector<double> grad;
+};
+inline std::vector<RowGradient> aggregate_group_gradient(const std::vector<RowGradContribution>& cs,
+                                                         uint32_t group_batch_size, uint32_t dim) {
+  std::vector<uint32_t> rows(cs.size());
+  std::vector<double> g(cs.size() * (size_t)dim);
+  for (size_t i = 0; i < cs.size(); ++i) {
+    if (cs[i].grad.size() != dim) throw std::invalid_argument("gradient dim mismatch");
+    rows[i] = cs[i].row;
+    std::copy(cs[i].grad.begin(), cs[i].grad.end(), g.begin() + i * dim);
+  }
+  uint64_t n = 0;
+  check(s2d_aggregate_group_gradient(rows.data(), g.data(), cs.size(), group_batch_size, dim, nullptr, nullptr,
+                                     nullptr, 0, &n));
+  std::vector<uint32_t> r(n), c(n);
+  std::vector<double> og(n * (size_t)dim);
+  if (n)
+    check(s2d_aggregate_group_gradient(rows.data(), g.data(), cs.size(), group_batch_size, dim, r.data(), og.data(),
+                                       c.data(), n, &n));
+  std::vector<RowGradient> out(n);
+  for (uint64_t k = 0; k < n; ++k) {
+    out[k].row = r[k];
+    out[k].g.assign(og.begin() + k * dim, og.begin() + (k + 1) * dim);
+    out[k].sample_count = c[k];
+  }
+  return out;
+}
+
 // Host copy of one Mlp's parameters (model.hpp:56): w1 [hidden][in], b1,
 // w2 [out][hidden], b2.
 struct MlpCopy {

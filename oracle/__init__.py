@@ -620,3 +620,24 @@ def reference_train_toy(overrides: dict) -> dict:
         lib.ref_last_error.restype = C.c_char_p
         raise RuntimeError(lib.ref_last_error().decode())
     return {"final_ne": ne.value, "baseline_ctr": ctr.value, "config_hash": h.value.decode()}
+
+
+def reference_aggregate(rows, grads, group_batch: int):
+    """The REAL reference aggregate_group_gradient (optimizer.cpp:25-59):
+    (rows [U], g [U, dim] f64, sample_count [U])."""
+    lib = C.CDLL(REF_SO)
+    fn = lib.ref_aggregate
+    fn.restype = C.c_int
+    r = np.ascontiguousarray(rows, np.uint32)
+    g = np.ascontiguousarray(grads, np.float64)
+    n, dim = g.shape
+    out_r = np.zeros(max(n, 1), np.uint32)
+    out_g = np.zeros((max(n, 1), dim), np.float64)
+    out_c = np.zeros(max(n, 1), np.uint32)
+    m = C.c_uint32(0)
+    if fn(C.c_void_p(_ptr(r)), C.c_void_p(_ptr(g)), C.c_uint32(n), C.c_uint32(group_batch), C.c_uint32(dim),
+          C.c_void_p(_ptr(out_r)), C.c_void_p(_ptr(out_g)), C.c_void_p(_ptr(out_c)), C.byref(m)):
+        lib.ref_last_error.restype = C.c_char_p
+        raise ValueError(lib.ref_last_error().decode())
+    U = m.value
+    return out_r[:U], out_g[:U], out_c[:U]

@@ -92,6 +92,28 @@ int ref_init_rows(uint32_t table_id, uint32_t rows, uint32_t lo, uint32_t hi, ui
   }
 }
 
+// aggregate_group_gradient (optimizer.cpp:25-59) as is: contributions
+// (rows[i], grads[i*dim ..]); out_rows / out_g / out_count hold the result
+// (capacity n), *n_out its length.
+int ref_aggregate(const uint32_t* rows, const double* grads, uint32_t n, uint32_t group_batch, uint32_t dim,
+                  uint32_t* out_rows, double* out_g, uint32_t* out_count, uint32_t* n_out) {
+  try {
+    std::vector<RowGradContribution> cs(n);
+    for (uint32_t i = 0; i < n; ++i) cs[i] = {rows[i], std::span<const double>(grads + (size_t)i * dim, dim)};
+    const auto out = aggregate_group_gradient(cs, group_batch, dim);
+    *n_out = (uint32_t)out.size();
+    for (size_t k = 0; k < out.size(); ++k) {
+      out_rows[k] = out[k].row;
+      out_count[k] = out[k].sample_count;
+      std::memcpy(out_g + k * dim, out[k].g.data(), dim * sizeof(double));
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 int ref_pool_ids(const float* w, uint32_t rows, uint32_t dim, uint32_t n_shards,
                  const uint32_t* lo_hi, const uint32_t* ids, uint32_t n_ids, float* out) {
   EmbeddingTable t;

@@ -34,12 +34,18 @@ from .api import (  # noqa: F401
     run_ranks,
     traces_to_csv,
     train_toy,
+    pool_ids,
+    lookup_and_pool,
+    aggregate_group_gradient,
     validate_plan,
 )
 
 __all__ = [
     "Trainer",
     "train_toy",
+    "pool_ids",
+    "lookup_and_pool",
+    "aggregate_group_gradient",
     "TrainerOptions",
     "closed_form_ratio",
     "estimate_increment_ratio",

@@ -144,6 +144,9 @@ SIGNATURES = {
     "s2d_trainer_rank_ctx": (C.c_int, [_P, C.c_uint32, C.POINTER(_P)]),
     "s2d_trainer_rank_model": (C.c_int, [_P, C.c_uint32, C.c_int32, _P, _P, _P, _P]),
     "s2d_trainer_last_loss": (C.c_int, [_P, C.POINTER(C.c_double)]),
+    "s2d_pool_ids": (C.c_int, [_P, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, _P, _P, C.c_uint64, _P, _P, _P]),
+    "s2d_aggregate_group_gradient": (C.c_int, [_P, _P, C.c_uint64, C.c_uint32, C.c_uint32, _P, _P, _P, C.c_uint64,
+                                               C.POINTER(C.c_uint64)]),
     "s2d_trainer_metrics_rows": (C.c_int, [_P, _P, C.c_uint32, C.POINTER(C.c_uint32)]),
     "s2d_trainer_final_ne": (C.c_int, [_P, C.POINTER(NEReportC)]),
     "s2d_memory_overhead": (C.c_int, [C.c_double, C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]),

@@ -1028,3 +1028,55 @@ def train_toy(overrides: dict | None = None) -> dict:
                 "metrics": fin["metrics"]}
     finally:
         tr.close()
+
+
+# ---- function-level forms of the path's reductions (embedding.hpp, optimizer.hpp) ----
+
+def lookup_and_pool(weights, shards, per_sample_ids, table_id: int = 0) -> np.ndarray:
+    """lookup_and_pool / pool_ids (embedding.hpp:41-58) on the device:
+    weights [rows, dim] fp32 (the whole table, global row index), shards
+    [(row_lo, row_hi)] in presentation order, per_sample_ids a list of id
+    lists -> pooled [len(per_sample_ids), dim] fp32.  IndexError (the
+    reference's out_of_range) for an id no shard covers."""
+    w = np.ascontiguousarray(weights, np.float32)
+    if w.ndim != 2:
+        raise ValueError("weights must be [rows, dim]")
+    lo = np.ascontiguousarray([int(s[0]) for s in shards], np.uint32)
+    hi = np.ascontiguousarray([int(s[1]) for s in shards], np.uint32)
+    lens = np.array([len(x) for x in per_sample_ids], np.uint64)
+    off = np.zeros(len(lens) + 1, np.uint64)
+    np.cumsum(lens, out=off[1:])
+    ids = (np.concatenate([np.asarray(x, np.uint32) for x in per_sample_ids]) if len(lens) and off[-1]
+           else np.zeros(1, np.uint32))
+    out = np.zeros((len(lens), w.shape[1]), np.float32)
+    L.check(_lib().s2d_pool_ids(w.ctypes.data, w.shape[0], w.shape[1], int(table_id), len(lo), lo.ctypes.data,
+                                hi.ctypes.data, len(lens), off.ctypes.data, ids.ctypes.data, out.ctypes.data))
+    return out
+
+
+def pool_ids(weights, shards, ids, table_id: int = 0) -> np.ndarray:
+    """pool_ids (embedding.hpp:52-53): one bag -> [dim] fp32."""
+    return lookup_and_pool(weights, shards, [list(ids)], table_id)[0]
+
+
+def aggregate_group_gradient(rows, grads, group_batch: int) -> list[dict]:
+    """aggregate_group_gradient (optimizer.hpp:36-44) on the device:
+    contributions (rows[i], grads[i] f64 [dim]) in arrival order ->
+    [{"row", "g" (f64 [dim]), "sample_count"}] by ascending row."""
+    r = np.ascontiguousarray(rows, np.uint32)
+    g = np.ascontiguousarray(grads, np.float64)
+    if g.ndim != 2 or g.shape[0] != len(r):
+        raise ValueError("grads must be [n, dim] with one row per contribution")
+    lib = _lib()
+    n = C.c_uint64(0)
+    L.check(lib.s2d_aggregate_group_gradient(r.ctypes.data, g.ctypes.data, len(r), int(group_batch), g.shape[1],
+                                             None, None, None, 0, C.byref(n)))
+    U = n.value
+    out_r = np.zeros(max(U, 1), np.uint32)
+    out_g = np.zeros((max(U, 1), g.shape[1]), np.float64)
+    out_c = np.zeros(max(U, 1), np.uint32)
+    if U:
+        L.check(lib.s2d_aggregate_group_gradient(r.ctypes.data, g.ctypes.data, len(r), int(group_batch), g.shape[1],
+                                                 out_r.ctypes.data, out_g.ctypes.data, out_c.ctypes.data, U,
+                                                 C.byref(n)))
+    return [{"row": int(out_r[k]), "g": out_g[k], "sample_count": int(out_c[k])} for k in range(U)]
