@@ -485,6 +485,34 @@ def run_ours(args):
         if sync_each:
             eng.synchronize()  # the step's pooled rows are in host memory
 
+    def pcie_probe(nbytes):
+        """Pinned host <-> device copy bandwidth of this GPU with both
+        directions in flight (two streams), best of 3."""
+        nb = max(1 << 20, int(nbytes)) // 4 * 4
+        hs = torch.empty(nb // 4, dtype=torch.float32).pin_memory()
+        hd = torch.empty(nb // 4, dtype=torch.float32).pin_memory()
+        ds = torch.empty(nb // 4, dtype=torch.float32, device="cuda")
+        dd = torch.empty(nb // 4, dtype=torch.float32, device="cuda")
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+        best = (0.0, 0.0)
+        for _ in range(3):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s1):
+                e[0].record()
+                ds.copy_(hs, non_blocking=True)
+                e[1].record()
+            with torch.cuda.stream(s2):
+                e[2].record()
+                hd.copy_(dd, non_blocking=True)
+                e[3].record()
+            torch.cuda.synchronize()
+            up, down = nb / (e[0].elapsed_time(e[1]) / 1e3) / 1e9, nb / (e[2].elapsed_time(e[3]) / 1e3) / 1e9
+            best = (max(best[0], up), max(best[1], down))
+        del hs, hd, ds, dd
+        return {"h2d_gbs": best[0], "d2h_gbs": best[1], "bytes": nb,
+                "how": "pinned tensors, H2D and D2H copies in flight together on two streams, best of 3"}
+
     def time_e2e(async_host, sync_each):
         eng.set_async_host(async_host)
         step_host(0, True)
@@ -517,6 +545,13 @@ def run_ours(args):
     eng.set_async_host(False)
     h2d = int(sum(x.numel() * 4 for x in pin[0]) / 1)
     d2h = int(pooled_h.numel() * 4)
+    # the e2e ceiling: this GPU's pinned-host copy bandwidth, both directions
+    # at once (as the e2e loop drives them), measured now
+    pcie = None if args.no_e2e else pcie_probe(min(h2d, d2h))
+    if pcie and e2e:
+        floor_ms = 1e3 * max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9))
+        pcie["e2e_floor_samples_per_s"] = world * w.batch / (floor_ms / 1e3)
+        pcie["e2e_frac"] = e2e / pcie["e2e_floor_samples_per_s"]
 
     # ---- roofline of the dominant phase (SURVEY.md 8(d) bytes) ----
     peak, peak_src = load_peaks()
@@ -590,7 +625,7 @@ def run_ours(args):
                        "every step, synchronize after the last; wall clock around the loop (max over ranks)",
                 "copy_overlap": "inputs on the H2D copy stream, pooled read-back on the D2H stream; at N = 1 two "
                                 "staging buffers per direction let step k's read-back overlap step k+1",
-                "per_step_sync_value": e2e_step, "serial_value": e2e_serial},
+                "per_step_sync_value": e2e_step, "serial_value": e2e_serial, "pcie_ceiling": pcie},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "step_stats": {k: st[k] for k in ("nnz_owned", "unique_rows", "long_segments", "a2a_bytes_sent",
