@@ -254,13 +254,15 @@ struct StreamUpdateArgs {
   const uint32_t* head_ord;      // debug: heads before each sorted position (scan_heads_u32)
   // M > 1 snapshot log (null: off): a row flushed while its dirty flag is
   // clear first saves its pre-update value (f32 row, moment at rf - 1) at
-  // snap[pos], pos = snap_base + the head's sorted position, and
-  // snap_pos[slot] = pos (the host reserves snap_base + n rows)
+  // snap[pos], pos = snap_base + the head's sorted position (or, snap_dense,
+  // its ordinal head_ord[position]), and snap_pos[slot] = pos (the host
+  // reserves snap_base + n items, or + the update's rows when dense)
   float* snap;
   uint32_t* snap_pos;
   uint64_t snap_base;
   uint64_t snap_cap;
   uint32_t snap_rf;
+  int snap_dense;
 };
 // mean pooling, N = 1 (k_embed.cu): out = upstream with the columns of
 // mean-pooled tables replaced by f32(f64(up) * (1/L_bag))

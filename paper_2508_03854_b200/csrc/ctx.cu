@@ -1069,9 +1069,35 @@ void Ctx::backward_update(const float* upstream, int mem) {
       ua.grad_dbg = dbg_grad.as<double>();
       ua.head_ord = dbg_head.as<uint32_t>();
     }
-    if (snapshot_enabled()) {
-      const uint64_t base = snap_reserve(n);
+    if (snapshot_enabled() && !snap_broken) {
+      // A head saves at base + its sorted position (the log spans the
+      // update's n items) while that fits a quarter of the device; beyond,
+      // the log is dense: base + the head's ordinal among the update's heads
+      // (a scan of the sorted keys, one host read of the row count)
+      if (!dev_total) {
+        size_t fr = 0;
+        S2D_CUDA(cudaMemGetInfo(&fr, &dev_total));
+      }
+      uint64_t rows = n;
+      bool dense = false;
+      static const bool force_dense = [] {  // S2D_SNAP_DENSE=1: always the dense log (tests)
+        const char* e = std::getenv("S2D_SNAP_DENSE");
+        return e && e[0] == '1';
+      }();
+      if (force_dense || (snap_ub + rows) * (uint64_t)(max_dim + 4) * 4 > (uint64_t)dev_total / 4) {
+        head_ord_buf.ensure((n + 1) * 4);
+        scan_tmp.ensure(scan_tmp_bytes(n + 1));
+        scan_heads_u32(sk, head_ord_buf.as<uint32_t>(), n, n_slots, stream, scan_tmp.p, scan_tmp.cap);
+        uint32_t U = 0;
+        S2D_CUDA(cudaMemcpyAsync(&U, head_ord_buf.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, stream));
+        S2D_CUDA(cudaStreamSynchronize(stream));
+        rows = U;
+        dense = true;
+      }
+      const uint64_t base = snap_reserve(rows);
       if (!snap_broken) {
+        if (dense) ua.head_ord = head_ord_buf.as<uint32_t>();
+        ua.snap_dense = dense ? 1 : 0;
         ua.snap = snap.as<float>();
         ua.snap_pos = snap_pos.as<uint32_t>();
         ua.snap_base = base;
@@ -1150,10 +1176,10 @@ bool Ctx::snapshot_enabled() const {
   return !off;
 }
 
-// Room in the snapshot log for an update of `items` sorted items: its
-// heads save at log row base + their sorted position (no atomics), so the
-// interval's log spans every item of its updates (config 2: 4.7M rows, 2.5
-// GB per step).  The log is held to a quarter of the device's memory and
+// Room in the snapshot log for an update of at most `items` rows: its heads
+// save at log row base + their ordinal (no atomics), so the interval's log
+// spans every row its updates write (config 2: 0.45M rows, 0.23 GB per
+// step; config 5 at B = 16384 on 2x2: 17.6M rows, 18 GB).  The log is held to a quarter of the device's memory and
 // leaves the sync's staging plus a quarter of the device (at least 4 GB)
 // free for the other buffers' growth; when it cannot grow the interval is
 // marked broken (the sync then exchanges every union row, which needs no
@@ -1170,12 +1196,13 @@ uint64_t Ctx::snap_reserve(uint64_t items) {
   }
   snap_ub = need;
   if (need <= snap_cap_rows) return base;
-  const uint64_t want = std::min<uint64_t>(need + need / 4, 0xfffffffeull);
   size_t fr = 0, tot = 0;
   S2D_CUDA(cudaMemGetInfo(&fr, &tot));
+  const uint64_t cap_rows = (uint64_t)tot / 4 / (rf * 4);  // a quarter of the device
+  const uint64_t want = std::min<uint64_t>(std::min<uint64_t>(need + need / 4, 0xfffffffeull), cap_rows);
   void* p = nullptr;
   const uint64_t keep = std::max<uint64_t>(4ull << 30, (uint64_t)tot / 4);
-  if (want * rf * 4 > (uint64_t)tot / 4 ||
+  if (need > want ||
       (uint64_t)fr < (want + std::min<uint64_t>(items, n_slots)) * rf * 4 + keep ||
       cudaMalloc(&p, want * rf * 4) != cudaSuccess) {
     (void)cudaGetLastError();

@@ -87,6 +87,8 @@ struct Ctx {
   // sync then exchanges every union row instead
   DevBuf snap, snap_pos;
   uint64_t snap_cap_rows = 0, snap_ub = 0;
+  DevBuf head_ord_buf;  // heads before each sorted position (the dense snapshot log's row index)
+  size_t dev_total = 0;  // device memory size (bounds the snapshot log)
   bool snap_broken = false;
   bool snapshot_enabled() const;
   uint64_t snap_reserve(uint64_t items);

@@ -954,8 +954,11 @@ __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(c
             vold = *reinterpret_cast<const float*>(smem + (mom_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
             if constexpr (SNAP) {
               const uint32_t dw = *reinterpret_cast<const uint32_t*>(smem + (dty_s - sbase) + ((wc & 1u) * 32u + i) * 4u);
-              // log position = the head's sorted position (unique, no atomics)
-              cur_snap = ((dw >> ((cur & 3u) * 8u)) & 0xffu) ? kNone : (uint32_t)(a.snap_base + cur_pos);
+              // log position (unique, no atomics): the head's sorted position, or
+              // with head_ord its ordinal among this update's heads (dense log)
+              cur_snap = ((dw >> ((cur & 3u) * 8u)) & 0xffu)
+                             ? kNone
+                             : (uint32_t)(a.snap_base + (a.snap_dense ? __ldg(a.head_ord + cur_pos) : cur_pos));
             }
           }
           add_grad(slot0 + r);
