@@ -263,6 +263,10 @@ struct StreamUpdateArgs {
   uint64_t snap_cap;
   uint32_t snap_rf;
   int snap_dense;
+  // M > 1, the first update of a sync interval (null: off): each written
+  // row's slot at its head ordinal (head_ord) -- the replica's ascending
+  // dirty list, so the sync needs no scan of the dirty flags
+  uint32_t* dirty_list;
 };
 // mean pooling, N = 1 (k_embed.cu): out = upstream with the columns of
 // mean-pooled tables replaced by f32(f64(up) * (1/L_bag))
@@ -313,6 +317,8 @@ void launch_rows_adagrad(float* w, float* v, const double* g, double* lr, uint32
 void launch_flag_count(const uint8_t* dirty, uint32_t n_slots, uint32_t* count, void* tmp, size_t tmp_bytes,
                        cudaStream_t st);
 void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, const void* tmp, cudaStream_t st);
+// dirty[list[i]] = 0 for i < *count (count on the device, at most n)
+void launch_clear_listed(uint8_t* dirty, const uint32_t* list, const uint32_t* count, uint32_t n, cudaStream_t st);
 size_t flag_tmp_bytes(uint32_t n_slots);
 void launch_mark_slots(const uint32_t* lists, uint64_t n, uint32_t n_slots, uint8_t* dirty, cudaStream_t st);
 // Pair (M = 2) snapshot replica sync (k_sync.cu): each replica sends the

@@ -357,6 +357,8 @@ void Ctx::shard_io(uint32_t table, uint32_t lo, uint32_t hi, float* w, float* v,
   if (write && M > 1) {  // written rows join the next replica sync's dirty union
     S2D_CUDA(cudaMemset(dirty.as<uint8_t>() + fd.vbase + (lo - fd.lo), 1, hi - lo));
     snap_broken = true;  // not in the snapshot log: the next sync exchanges every union row
+    dirty_clean = false;
+    list_ready = false;
   }
   if (v) {
     float* dst = moments.as<float>() + fd.vbase + (lo - fd.lo);
@@ -415,7 +417,11 @@ void Ctx::apply_row_updates(uint32_t table, uint32_t n, const uint32_t* rows, co
                     reinterpret_cast<uint32_t*>(d + o_seg), reinterpret_cast<uint32_t*>(d + o_row),
                     reinterpret_cast<double*>(d + o_delta), reinterpret_cast<double*>(d + o_mom), nseg, fd.dim,
                     M > 1 ? dirty.as<uint8_t>() + fd.vbase : nullptr, stream);
-  if (M > 1) snap_broken = true;  // not in the snapshot log (see shard_io)
+  if (M > 1) {
+    snap_broken = true;  // not in the snapshot log (see shard_io)
+    dirty_clean = false;
+    list_ready = false;
+  }
   S2D_CUDA(cudaStreamSynchronize(stream));
 }
 
@@ -1069,30 +1075,53 @@ void Ctx::backward_update(const float* upstream, int mem) {
       ua.grad_dbg = dbg_grad.as<double>();
       ua.head_ord = dbg_head.as<uint32_t>();
     }
-    if (snapshot_enabled() && !snap_broken) {
-      // A head saves at base + its sorted position (the log spans the
-      // update's n items) while that fits a quarter of the device; beyond,
-      // the log is dense: base + the head's ordinal among the update's heads
-      // (a scan of the sorted keys, one host read of the row count)
-      if (!dev_total) {
-        size_t fr = 0;
-        S2D_CUDA(cudaMemGetInfo(&fr, &dev_total));
-      }
+    // head ordinals (heads before each sorted position), scanned at most once
+    bool have_ord = false;
+    auto ensure_ord = [&] {
+      if (have_ord) return;
+      head_ord_buf.ensure((n + 1) * 4);
+      scan_tmp.ensure(scan_tmp_bytes(n + 1));
+      scan_heads_u32(sk, head_ord_buf.as<uint32_t>(), n, n_slots, stream, scan_tmp.p, scan_tmp.cap);
+      have_ord = true;
+    };
+    if (!dev_total) {
+      size_t fr = 0;
+      S2D_CUDA(cudaMemGetInfo(&fr, &dev_total));
+    }
+    static const bool force_dense = [] {  // S2D_SNAP_DENSE=1: always the dense log (tests)
+      const char* e = std::getenv("S2D_SNAP_DENSE");
+      return e && e[0] == '1';
+    }();
+    // the snapshot log: indexed by a head's sorted position (it spans the
+    // update's n items) while that fits a quarter of the device, else dense
+    // (by the head's ordinal)
+    const bool snap_path = snapshot_enabled() && !snap_broken;
+    const bool dense = snap_path && (force_dense || (snap_ub + n) * (uint64_t)(max_dim + 4) * 4 > (uint64_t)dev_total / 4);
+    // M = 2: the first update after a sync also writes this replica's
+    // ascending dirty list, so the sync scans no dirty flags -- worth it when
+    // the flags (one byte per owned row) outweigh the scan of the sorted keys
+    // (measured: config 4 2x2 1.875 -> 1.713 ms; config 3 2x2 1.777 -> 1.849)
+    // or when the dense log scans the keys anyway
+    static const bool force_list = [] {  // S2D_SYNC_LIST=1: always (tests)
+      const char* e = std::getenv("S2D_SYNC_LIST");
+      return e && e[0] == '1';
+    }();
+    const bool want_list = M == 2 && dirty_clean && sync_list_mode_enabled() &&
+                           (force_list || dense || (uint64_t)n_slots > 8 * n);
+    if (want_list) {
+      ensure_ord();
+      dlist.ensure(std::max<uint64_t>(std::min<uint64_t>(n, n_slots), 1) * 4);
+      ua.head_ord = head_ord_buf.as<uint32_t>();
+      ua.dirty_list = dlist.as<uint32_t>();
+    }
+    if (snap_path) {
       uint64_t rows = n;
-      bool dense = false;
-      static const bool force_dense = [] {  // S2D_SNAP_DENSE=1: always the dense log (tests)
-        const char* e = std::getenv("S2D_SNAP_DENSE");
-        return e && e[0] == '1';
-      }();
-      if (force_dense || (snap_ub + rows) * (uint64_t)(max_dim + 4) * 4 > (uint64_t)dev_total / 4) {
-        head_ord_buf.ensure((n + 1) * 4);
-        scan_tmp.ensure(scan_tmp_bytes(n + 1));
-        scan_heads_u32(sk, head_ord_buf.as<uint32_t>(), n, n_slots, stream, scan_tmp.p, scan_tmp.cap);
+      if (dense) {  // one host read of the update's row count
+        ensure_ord();
         uint32_t U = 0;
         S2D_CUDA(cudaMemcpyAsync(&U, head_ord_buf.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, stream));
         S2D_CUDA(cudaStreamSynchronize(stream));
         rows = U;
-        dense = true;
       }
       const uint64_t base = snap_reserve(rows);
       if (!snap_broken) {
@@ -1106,6 +1135,11 @@ void Ctx::backward_update(const float* upstream, int mem) {
       }
     }
     launch_update_stream(ua, bf16, stream);
+    if (M > 1) {
+      list_ready = want_list;  // a second update before the sync dirties rows this list lacks
+      list_n = n;
+      dirty_clean = false;
+    }
     uniq = 1;
   }
   (void)uniq;
@@ -1156,6 +1190,15 @@ void Ctx::join_sync() {
   if (!sync_pending) return;
   S2D_CUDA(cudaStreamWaitEvent(stream, ev_sync_done, 0));
   sync_pending = false;
+}
+
+// S2D_SYNC_LIST=0 keeps the dirty-flag scans at M = 2 (A/B switch; =1 forces the list)
+bool Ctx::sync_list_mode_enabled() const {
+  static const bool off = [] {
+    const char* e = std::getenv("S2D_SYNC_LIST");
+    return e && e[0] == '0';
+  }();
+  return !off;
 }
 
 // S2D_SYNC_OVERLAP=0 keeps the sync tail on the main stream (A/B switch)
@@ -1236,7 +1279,15 @@ void Ctx::replica_sync() {
   // every replica's log saw every write of the interval
   const bool snap_on = snapshot_enabled();
   const uint32_t ok_word[3] = {(snap_on && !snap_broken && snap_pos.p) ? 1u : 0u, 0u, 0u};
-  launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
+  // this replica's dirty count: its update's row count when that update's
+  // list is the whole dirty set, else a scan of the flags
+  const bool use_list = list_ready;
+  if (use_list)
+    S2D_CUDA(cudaMemcpyAsync(d_count, head_ord_buf.as<uint32_t>() + list_n, 4, cudaMemcpyDeviceToDevice, stream));
+  else
+    launch_flag_count(dirty.as<uint8_t>(), n_slots, d_count, sync_tmp.p, sync_tmp.cap, stream);
+  list_ready = false;
+  dirty_clean = true;  // (after this sync; the early returns below included)
   S2D_CUDA(cudaMemcpyAsync(d_count + 1, ok_word, 12, cudaMemcpyHostToDevice, stream));
   dp.allgather(d_count, d_gath, 16, stream);
   S2D_CUDA(cudaMemcpyAsync(h_counts.p, d_gath, (size_t)M * 16, cudaMemcpyDeviceToHost, stream));
@@ -1262,7 +1313,11 @@ void Ctx::replica_sync() {
     return;
   }
   sync_list.ensure((uint64_t)cmax * 4);
-  launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+  if (use_list) {
+    if (mine) S2D_CUDA(cudaMemcpyAsync(sync_list.p, dlist.p, (size_t)mine * 4, cudaMemcpyDeviceToDevice, stream));
+  } else {
+    launch_flag_write(dirty.as<uint8_t>(), n_slots, sync_list.as<uint32_t>(), sync_tmp.p, stream);
+  }
   if (cmax > mine)  // pad to the longest list (0xffffffff is not a slot)
     S2D_CUDA(cudaMemsetAsync(sync_list.as<uint32_t>() + mine, 0xff, (size_t)(cmax - mine) * 4, stream));
   sync_lists.ensure((uint64_t)cmax * M * 4);
@@ -1299,7 +1354,10 @@ void Ctx::replica_sync() {
                      d_feats.as<FeatDev>(), d_vbase_sorted.as<uint32_t>(), d_feat_of_vbase.as<uint32_t>(),
                      (uint32_t)feat_of_vbase.size(), row_floats, weights.p, bf16, moments.as<float>(), sgd, ts);
     phase_begin(kPhSyncScatter);
-    launch_zero(dirty.p, n_slots, ts);
+    if (use_list)  // only this replica's rows carry a flag
+      launch_clear_listed(dirty.as<uint8_t>(), dlist.as<uint32_t>(), d_counts + group, mine, ts);
+    else
+      launch_zero(dirty.p, n_slots, ts);
     if (overlap) {
       S2D_CUDA(cudaEventRecord(ev_sync_done, ts));
       sync_pending = true;

@@ -88,9 +88,16 @@ struct Ctx {
   DevBuf snap, snap_pos;
   uint64_t snap_cap_rows = 0, snap_ub = 0;
   DevBuf head_ord_buf;  // heads before each sorted position (the dense snapshot log's row index)
+  // the update's own dirty list (M = 2): valid while no other write followed
+  // the first update after a sync
+  DevBuf dlist;
+  bool dirty_clean = true;  // no row dirtied since the last replica sync
+  bool list_ready = false;  // dlist is this replica's whole dirty set
+  uint64_t list_n = 0;      // items of the update that wrote dlist (head_ord_buf[list_n] = its rows)
   size_t dev_total = 0;  // device memory size (bounds the snapshot log)
   bool snap_broken = false;
   bool snapshot_enabled() const;
+  bool sync_list_mode_enabled() const;
   uint64_t snap_reserve(uint64_t items);
   void join_sync();
   void launch_sort(cudaStream_t st);

@@ -898,6 +898,12 @@ __global__ void __launch_bounds__(128, SNAP && VPL == 1 ? 8 : 0) k_update_ring(c
         if (lane == 0 && a.dirty) a.dirty[cur] = 1;
         ++heads;
       }
+      // the update's dirty list (every head at its ordinal; a faulted row
+      // too -- the step reports the fault)
+      if (lane == 0 && a.dirty_list) {
+        a.dirty_list[__ldg(a.head_ord + cur_pos)] = cur;
+        if (!finite) a.dirty[cur] = 1;
+      }
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
 #pragma unroll

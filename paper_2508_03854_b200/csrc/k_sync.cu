@@ -518,6 +518,18 @@ void launch_flag_count(const uint8_t* dirty, uint32_t n_slots, uint32_t* count, 
   S2D_CUDA(cudaMemcpyAsync(count, tx + ntiles, 4, cudaMemcpyDeviceToDevice, st));
 }
 
+__global__ void k_clear_listed(uint8_t* __restrict__ dirty, const uint32_t* __restrict__ list,
+                               const uint32_t* __restrict__ count) {
+  const uint32_t n = *count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) dirty[list[i]] = 0;
+}
+
+void launch_clear_listed(uint8_t* dirty, const uint32_t* list, const uint32_t* count, uint32_t n, cudaStream_t st) {
+  if (!n) return;
+  k_clear_listed<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(dirty, list, count);
+  S2D_LAUNCH_CHECK();
+}
+
 void launch_flag_write(const uint8_t* dirty, uint32_t n_slots, uint32_t* list, const void* tmp, cudaStream_t st) {
   const uint32_t ntiles = flag_tiles(n_slots);
   if (ntiles == 0) return;

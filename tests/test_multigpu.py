@@ -46,6 +46,8 @@ CASES = [
     (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4", "ENV:S2D_SYNC_SNAPSHOT=0"]),
     (4, 2, "row-wise", ["--sync-interval", "2", "--steps", "4", "ENV:S2D_SNAP_DENSE=1"]),
     (2, 2, "table-wise", ["--mean", "ENV:S2D_SNAP_DENSE=1"]),
+    (2, 2, "row-wise", ["--steps", "4", "ENV:S2D_SYNC_LIST=1"]),
+    (4, 2, "table-wise", ["--sync-interval", "2", "--steps", "4", "ENV:S2D_SYNC_LIST=1"]),
     (2, 2, "table-wise", ["--sgd", "--steps", "3"]),
     (3, 3, "row-wise", ["--steps", "3"]),
     (4, 1, "row-wise", ["--bad-id"]),
@@ -57,7 +59,8 @@ def _case_id(c):
     return (f"T{T}-M{M}-{strategy}" + "".join(x.replace("--", "-") for x in extra if x.startswith("--")) +
             "".join("-nccl-sync" for x in extra if x.startswith("ENV:S2D_SYNC_NCCL")) +
             "".join("-slice-sync" for x in extra if x.startswith("ENV:S2D_SYNC_SNAPSHOT")) +
-            "".join("-dense-log" for x in extra if x.startswith("ENV:S2D_SNAP_DENSE")))
+            "".join("-dense-log" for x in extra if x.startswith("ENV:S2D_SNAP_DENSE")) +
+            "".join("-dirty-list" for x in extra if x.startswith("ENV:S2D_SYNC_LIST")))
 
 
 def _env_args(extra):
