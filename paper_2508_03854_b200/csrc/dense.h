@@ -62,7 +62,6 @@ void launch_mlp_dhidden(const MlpView& m, const float* hid, const double* dout, 
                         cudaStream_t st);
 void launch_loss_sum(const double* loss, uint32_t B, double* out, cudaStream_t st);
 void launch_fold_sgd(const FoldArgs& a, cudaStream_t st);
-void launch_mirror(const float* w, double* wd, uint64_t n, cudaStream_t st);
 // DataGenerator side (data.cpp): ground-truth id contributions and dense
 // weights, the per-sample dense features and labels.
 void launch_gt_normals(uint64_t key, uint64_t n, double scale, float* out, cudaStream_t st);

@@ -212,11 +212,6 @@ __global__ void k_fold_sgd(const FoldArgs a) {
   }
 }
 
-__global__ void k_mirror(const float* __restrict__ w, double* __restrict__ wd, uint64_t n) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    wd[i] = (double)w[i];
-}
-
 // out[i] = f32(scale * normal #i) of the stream `key` (GroundTruthModel:
 // id contributions with key make_key({seed, 10, f}), dense weights with
 // make_key({seed, 11}); data.cpp:43-55)
@@ -342,12 +337,6 @@ void launch_fold_sgd(const FoldArgs& a, cudaStream_t st) {
   const uint64_t n = (uint64_t)a.P * a.Q + a.P;
   if (!n) return;
   k_fold_sgd<<<grid_for(n), 256, 0, st>>>(a);
-  S2D_LAUNCH_CHECK();
-}
-
-void launch_mirror(const float* w, double* wd, uint64_t n, cudaStream_t st) {
-  if (!n) return;
-  k_mirror<<<grid_for(n), 256, 0, st>>>(w, wd, n);
   S2D_LAUNCH_CHECK();
 }
 
