@@ -1,6 +1,6 @@
 # usage: bash tools/try_variants.sh "<sed expr per variant>"... ; runs parity + bench for each
 set -u
-f=paper_2508_03854_b200/csrc/k_stream.cu
+f=${VARIANT_FILE:-paper_2508_03854_b200/csrc/k_stream.cu}
 cp $f /tmp/orig.cu
 i=0
 for expr in "$@"; do
