@@ -249,3 +249,30 @@ def test_train_toy_config_schema():
     cfg = {"data.tables": "1", "run.steps": "1", "run.eval_samples": "64", "topology.total_ranks": "1"}
     # cheap reference run: only its hash is compared here (the GPU test compares the training)
     assert reference_train_toy(cfg)["config_hash"] == _config_hash(dict(_CONFIG_DEFAULTS, **cfg))
+
+
+REF_SMOKE = "/root/reference/proj/tests/python/test_smoke.py"
+HOST_ONLY = ("test_topology_mapping", "test_cost_formulas", "test_moment_analysis", "test_planner",
+             "test_evaluate_ne")
+
+
+@pytest.mark.parametrize("name", HOST_ONLY)
+def test_reference_python_smoke_suite_against_this_package(name, monkeypatch):
+    """The reference binding's own smoke tests (tests/python/test_smoke.py),
+    read from the reference tree and run unchanged with `sparse2d` bound to
+    this package: the host-only ones here (adagrad_row_step and train_toy
+    run on the device; their assertions are the GPU tests
+    test_adagrad_row_step_known_answers and test_train_toy_matches_reference_module)."""
+    import sys
+    import types
+
+    import paper_2508_03854_b200 as s2d
+
+    if not os.path.exists(REF_SMOKE):
+        pytest.skip("reference tree absent")
+    monkeypatch.setitem(sys.modules, "sparse2d", s2d)
+    mod = types.ModuleType("ref_test_smoke")
+    mod.__file__ = REF_SMOKE
+    with open(REF_SMOKE) as f:
+        exec(compile(f.read(), REF_SMOKE, "exec"), mod.__dict__)
+    getattr(mod, name)()
