@@ -276,3 +276,18 @@ def test_reference_python_smoke_suite_against_this_package(name, monkeypatch):
     with open(REF_SMOKE) as f:
         exec(compile(f.read(), REF_SMOKE, "exec"), mod.__dict__)
     getattr(mod, name)()
+
+
+def test_function_level_forms_validate_before_touching_the_device():
+    """pool_ids / aggregate_group_gradient raise the reference's argument
+    errors (embedding.cpp:41, 71; optimizer.cpp:28-30) before any device
+    work, so they hold without a GPU too."""
+    import paper_2508_03854_b200 as s2d
+
+    w = np.zeros((4, 2), np.float32)
+    with pytest.raises(ValueError, match="empty shard set"):
+        s2d.pool_ids(w, [], [0])
+    with pytest.raises(ValueError, match="dim too large"):
+        s2d.pool_ids(np.zeros((1, 513), np.float32), [(0, 1)], [0])
+    with pytest.raises(ValueError, match="group batch size must be > 0"):
+        s2d.aggregate_group_gradient([0], [[1.0]], 0)
